@@ -1,0 +1,453 @@
+"""Benchmark: scan Gelem/s (B*L*H*N) fwd+bwd on B200, with the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl lrx|reference]
+
+One JSON line on rank 0 (driver contract).  A step is one forward + backward
+pass of the scan operator over one batch of synthetic inputs that are already
+resident in HBM (the `value`); `e2e` is the same metric through the public
+Python API with pinned HOST buffers and the H2D/D2H copies inside the timed
+region.  Workloads are BASELINE.json's configs:
+
+  lru     configs[0]  LRU   B=8  L=1024   H=128  N=64  (complex)    f32
+  s5      configs[1]  S5    B=32 L=4096   H=256  P=128 (complex)    f32, ZOH
+  s6      configs[2]  S6    B=16 L=8192   D=1536 N=16               bf16 I/O, fp32 accum
+  rglru   configs[3]  RG-LRU B=64 L=16384 W=2560                    f32   (default)
+  s6_long configs[4]  S6    B=1  L=2^20   D=2048 N=16               bf16 I/O (1 GPU)
+
+The default is the RG-LRU config: BASELINE.json's metric is the scan's HBM
+throughput at 1/2/4/8 GPUs, and configs[3] is the config it names for the
+8-GPU batch sharding ("Benchmark").  Multi-GPU: one process
+per GPU (torchrun); the batch is split across ranks with no data-path
+collective (total work fixed: strong scaling); time = max over ranks.
+
+The operator boundary is the one a framework binds (paper_2602_08810_b200.ops):
+for S6 / RG-LRU the dense projections producing (pre, B_k, C_k) / (qr, qi) are
+outside the scan; for S5 / LRU the B and C
+projections are part of the recurrence x = abar x + B u, y = Re(C x) + D u and
+are inside the step.
+
+`--impl reference` times the reference's own CPU algorithm (the oracle
+restatement in oracle/port.py: numpy + the C restatement of the numba loops,
+chunk-parallel over all host threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "lru": dict(kind="lru", B=8, L=1024, H=128, N=64, dtype="f32", cfg=0),
+    "s5": dict(kind="s5", B=32, L=4096, H=256, N=128, dtype="f32", cfg=1),
+    "s6": dict(kind="s6", B=16, L=8192, H=1536, N=16, dtype="bf16", cfg=2),
+    "rglru": dict(kind="rglru", B=64, L=16384, H=2560, N=1, dtype="f32", cfg=3),
+    "s6_long": dict(kind="s6", B=1, L=2 ** 20, H=2048, N=16, dtype="bf16", cfg=4),
+}
+DEFAULT_WORKLOAD = "rglru"
+METRIC = "scan Gelem/s (B·L·H·N) fwd+bwd, HBM GB/s vs peak, at 1/2/4/8 B200"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _traffic(workload, kernel):
+    """Per-launch DRAM bytes from the committed ncu capture (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def _state_dims(w):
+    """(lanes description, elements per step) for a workload dict."""
+    return w["B"] * w["L"] * w["H"] * w["N"]
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (driver timing rules)
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.idx = device_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        rows = [r for r in self.rows if len(r) == 6 and r[0].replace(".", "").isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(float(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+def build_problem(w, B, device):
+    """Synthetic inputs (reference init + N(0,1) activations, on device) and a
+    step function fwd+bwd at the operator boundary."""
+    import torch
+
+    import paper_2602_08810_b200 as lrx
+    from paper_2602_08810_b200 import ops
+
+    kind, L, H, N = w["kind"], w["L"], w["H"], w["N"]
+    layer = lrx.make_layer(kind, H, None if kind == "rglru" else (N if kind != "s5" else 2 * N), dtype=w["dtype"],
+                           seed=0, device=device)
+    g = torch.Generator(device=device).manual_seed(1234 + (torch.distributed.get_rank()
+                                                           if torch.distributed.is_initialized() else 0))
+    io = layer.io_dtype
+    u = torch.randn((B, L, H), generator=g, device=device, dtype=torch.float32).to(io)
+    gy = torch.randn((B, L, H), generator=g, device=device, dtype=torch.float32).to(io)
+    prob = {"layer": layer, "u": u, "gy": gy, "B": B}
+    if kind == "rglru":
+        with torch.no_grad():
+            u2 = u.reshape(B * L, H)
+            prob["qr"] = (u2 @ layer.W_r.T.to(io)).reshape(B, L, H)
+            prob["qi"] = (u2 @ layer.W_i.T.to(io)).reshape(B, L, H)
+        args = (layer.lambda_param, layer.b_r, layer.b_i)
+
+        def fwd():
+            return ops.rglru_scan_fwd(prob["u"], prob["qr"], prob["qi"], *args)
+
+        def bwd(ctx):
+            return ops.rglru_scan_bwd(prob["u"], prob["qr"], prob["qi"], *args, ctx[1], prob["gy"], y=ctx[0])
+
+        bpe = torch.tensor([], dtype=io).element_size()
+        # algorithmic bytes: fwd reads u, qr, qi, writes y; bwd reads
+        # u, qr, qi, gy and writes gu, gqr, gqi (the states are not counted)
+        prob["bytes"] = {"fwd": 4 * B * L * H * bpe, "bwd": 7 * B * L * H * bpe}
+    elif kind == "s6":
+        with torch.no_grad():
+            from paper_2602_08810_b200.layers import _mm
+            u2 = u.reshape(B * L, H)
+            prob["pre"] = (_mm(u2, layer.W_delta) @ layer.W_delta_proj).reshape(B, L, H)
+            prob["Bk"] = _mm(u2, layer.W_B.T).reshape(B, L, N)
+            prob["Ck"] = _mm(u2, layer.W_C.T).reshape(B, L, N)
+        pa = (layer.b_delta, layer.a_log)
+
+        def fwd():
+            return ops.s6_scan_fwd(prob["u"], prob["pre"], *pa, prob["Bk"], prob["Ck"], layer.D)
+
+        def bwd(ctx):
+            return ops.s6_scan_bwd(prob["u"], prob["pre"], *pa, prob["Bk"], prob["Ck"], layer.D, ctx[1], prob["gy"])
+
+        bu, bp = u.element_size(), prob["pre"].element_size()
+        per = B * L * H
+        prob["bytes"] = {"fwd": per * (2 * bu + bp) + 2 * B * L * N * bp,
+                         "bwd": per * (3 * bu + 2 * bp) + 4 * B * L * N * bp}
+    else:  # s5 / lru: projections are part of the recurrence
+        def fwd():
+            return layer._forward(prob["u"], None, True)
+
+        def bwd(ctx):
+            saved = dict(ctx[1])
+            saved["host"] = False
+            return layer._backward(saved, prob["gy"])
+
+        c = 8  # complex64 bytes
+        per = B * L * H * 4
+        st = B * L * N * c
+        prob["bytes"] = {"fwd": 2 * per, "bwd": 3 * per}  # fused minimum: u,y / u,gy,gu
+        prob["bytes_scan"] = {"fwd": 2 * st, "bwd": 4 * st}
+    prob["fwd"], prob["bwd"] = fwd, bwd
+    return prob
+
+
+def run_gpu(args, w, rank, world, device):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_08810_b200 import _lib
+
+    B_total = w["B"]
+    if B_total % world:
+        raise SystemExit(f"batch {B_total} does not split over {world} GPUs")
+    B = B_total // world
+    prob = build_problem(w, B, device)
+    fwd, bwd = prob["fwd"], prob["bwd"]
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        bwd(fwd())
+    torch.cuda.synchronize()
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    n0 = _lib.launch_count()
+    with Clocks(device.index) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            ctx = fwd()
+            ev[k][1].record(stream)
+            bwd(ctx)
+            ev[k][2].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = _lib.launch_count() - n0
+    ms = t_start.elapsed_time(t_end) / args.steps
+    ms_fwd = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    ms_bwd = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    t = torch.tensor([ms, ms_fwd, ms_bwd], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, ms_fwd, ms_bwd = (float(v) for v in t.tolist())
+
+    # e2e through the public API with pinned host buffers (a batch slice)
+    e2e = run_e2e(args, w, prob, device)
+    if world > 1:
+        te = torch.tensor([e2e["ms"]], device=device, dtype=torch.float64)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e["ms"] = float(te.item())
+    return {"ms": ms, "ms_fwd": ms_fwd, "ms_bwd": ms_bwd, "launches": launches, "clocks": clocks.summary(),
+            "bytes": prob["bytes"], "B_rank": B, "e2e": e2e}
+
+
+def run_e2e(args, w, prob, device):
+    """Same step through the public API with HOST (pinned) buffers: H2D of the
+    step's inputs, the operator fwd+bwd, D2H of every output, all timed."""
+    import torch
+
+    from paper_2602_08810_b200 import ops
+
+    kind, L, H, N = w["kind"], w["L"], w["H"], w["N"]
+    Bs = min(prob["B"], args.e2e_batch)
+    names = {"rglru": ("u", "qr", "qi", "gy"), "s6": ("u", "pre", "Bk", "Ck", "gy")}.get(kind, ("u", "gy"))
+    host = {n: prob[n][:Bs].cpu().pin_memory() for n in names}
+    layer = prob["layer"]
+    h2d = sum(t.numel() * t.element_size() for t in host.values())
+
+    def step():
+        d = {n: t.to(device, non_blocking=True) for n, t in host.items()}
+        if kind == "rglru":
+            y, ck = ops.rglru_scan_fwd(d["u"], d["qr"], d["qi"], layer.lambda_param, layer.b_r, layer.b_i)
+            r = ops.rglru_scan_bwd(d["u"], d["qr"], d["qi"], layer.lambda_param, layer.b_r, layer.b_i, ck, d["gy"],
+                                   y=y)
+            outs = [y, r["gu_local"], r["gqr"], r["gqi"], r["gla"], r["gb_r"], r["gb_i"]]
+        elif kind == "s6":
+            y, ck = ops.s6_scan_fwd(d["u"], d["pre"], layer.b_delta, layer.a_log, d["Bk"], d["Ck"], layer.D)
+            r = ops.s6_scan_bwd(d["u"], d["pre"], layer.b_delta, layer.a_log, d["Bk"], d["Ck"], layer.D, ck, d["gy"])
+            outs = [y] + list(r.values())
+        else:
+            y, tape = layer.forward(d["u"], tape=True)
+            from paper_2602_08810_b200 import layer_backward
+            g = layer_backward(layer, tape, d["gy"])
+            outs = [y, g.u] + list(g.params.values())
+        res = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+        for r_, o in zip(res, outs):
+            r_.copy_(o, non_blocking=True)
+        return res, sum(o.numel() * o.element_size() for o in outs)
+
+    step()
+    torch.cuda.synchronize()
+    reps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    st = torch.cuda.Event(enable_timing=True)
+    en = torch.cuda.Event(enable_timing=True)
+    st.record()
+    for _ in range(reps):
+        res, d2h = step()
+    en.record()
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en) / reps
+    wall = (time.perf_counter() - t0) * 1e3 / reps
+    return {"ms": ms, "wall_ms": wall, "batch": Bs, "h2d": h2d, "d2h": d2h,
+            "elems": Bs * L * H * N}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle restatement of the reference algorithm)
+
+def cpu_sample(w, budget_s=12.0, seed=0):
+    """Bounded sample of the workload on the host's cores: (Gelem/s, desc, cores)."""
+    from oracle import port
+
+    kind, H, N = w["kind"], w["H"], w["N"]
+    cores = os.cpu_count() or 1
+    dt = np.float32
+    p = port.init_params(kind, H, None if kind == "rglru" else (N if kind != "s5" else 2 * N), dtype="f32",
+                         seed=seed)
+    # sample: one batch row, L chosen so one fwd+bwd is a few seconds
+    B, L = {"rglru": (2, 1024), "s6": (2, 256), "s5": (8, 512), "lru": (8, 1024)}[kind]
+    if kind == "s6" and H > 1536:
+        B = 1
+    rng = port.Rng(seed + 1)
+    u = rng.normal((B, L, H)).astype(dt)
+    gy = rng.normal((B, L, H)).astype(dt)
+    if kind == "rglru":
+        qr, qi = u @ p["W_r"].T, u @ p["W_i"].T
+
+        def one():
+            port.rglru_scan(u, qr, qi, p["lambda_param"], p["b_r"], p["b_i"], gy, "parallel", cores)
+    elif kind == "s6":
+        pre = (u @ p["W_delta"]) @ p["W_delta_proj"]
+        Bk, Ck = u @ p["W_B"].T, u @ p["W_C"].T
+
+        def one():
+            port.s6_scan(u, pre, p["b_delta"], p["a_log"], Bk, Ck, p["D"], gy, "parallel", cores)
+    else:
+        lay = port.Layer(kind, p)
+
+        def one():
+            y, s = lay.forward(u, "parallel", cores)
+            lay.backward(s, gy)
+    one()  # warm (pools, page-in)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        one()
+        n += 1
+        if time.perf_counter() - t0 > budget_s or n >= 20:
+            break
+    dt_s = (time.perf_counter() - t0) / n
+    elems = B * L * H * N
+    desc = (f"{kind} B={B} L={L} H={H} N={N} f32, fwd+bwd at the same operator boundary, "
+            f"parallel mode workers={cores}, mean of {n} runs")
+    return elems / dt_s / 1e9, desc, cores
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="lrx", choices=["lrx", "reference"])
+    ap.add_argument("--e2e-batch", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    w = WORKLOADS[args.workload]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    elems = _state_dims(w)
+    config = {"workload": f"{args.workload}: configs[{w['cfg']}] {w['kind']} B={w['B']} L={w['L']} H={w['H']} "
+                          f"N={w['N']}", "global_batch": w["B"], "seq_len": w["L"], "width": w["H"],
+              "d_state": w["N"], "parallelism": f"batch-sharded x{world}" if world > 1 else "single GPU",
+              "l2": "inputs > L2 (126 MB): no flush needed"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+        for _ in range(args.warmup):
+            cpu_sample(w, budget_s=min(budget, 3.0))
+        vals = []
+        for _ in range(args.steps):
+            v, desc, cores = cpu_sample(w, budget_s=budget)
+            vals.append(v)
+        v = float(np.mean(vals))
+        print(json.dumps({"metric": METRIC, "value": v, "unit": "Gelem/s", "n_gpus": args.gpus, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": elems / (v * 1e9) * 1e3, "higher_is_better": True,
+                          "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                          "impl": "reference", "config": config,
+                          "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "port",
+                                           "sample": desc},
+                          "e2e": {"value": v, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
+    torch.cuda.set_device(device)
+    if w["kind"] == "s6" and w["B"] == 1 and world > 1:
+        raise SystemExit("s6_long runs on one GPU in this build (sequence-parallel mode: see DESIGN.md)")
+    r = run_gpu(args, w, rank, world, device)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    value = elems / (r["ms"] * 1e-3) / 1e9
+    peak, peak_kind = _peaks()
+    dom = "bwd" if r["ms_bwd"] >= r["ms_fwd"] else "fwd"
+    dom_ms = r["ms_bwd"] if dom == "bwd" else r["ms_fwd"]
+    achieved = r["bytes"][dom] / (dom_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": _traffic(args.workload, dom), "kernel": f"lrx_{w['kind']}_{dom}",
+            "peak_source": peak_kind, "per_launch_ms": dom_ms,
+            "algorithmic_bytes_per_launch": r["bytes"][dom]}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, desc, cores = cpu_sample(w)
+        cpu = {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "port", "sample": desc}
+    e = r["e2e"]
+    e2e = {"value": e["elems"] * world / (e["ms"] * 1e-3) / 1e9, "unit": "Gelem/s",
+           "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"],
+           "sample": f"batch slice B={e['batch']} per rank through paper_2602_08810_b200.ops / layer API, "
+                     f"pinned host buffers", "ms_per_step": e["ms"]}
+    line = {"metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": {"f32": "f32", "bf16": "bf16 io / f32 accum"}[w["dtype"]],
+            "data": "synthetic (reference init, N(0,1) activations, projections from the layer's weights)",
+            "config": config, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": r["launches"],
+            "clocks": r["clocks"],
+            "kernels": {"fwd_ms": r["ms_fwd"], "bwd_ms": r["ms_bwd"],
+                        "fwd_GBps": r["bytes"]["fwd"] / (r["ms_fwd"] * 1e-3) / 1e9,
+                        "bwd_GBps": r["bytes"]["bwd"] / (r["ms_bwd"] * 1e-3) / 1e9}}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

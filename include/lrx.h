@@ -1,0 +1,180 @@
+/*
+ * lrx — B200-native (sm_100a) diagonal linear-recurrence scan: the C-ABI.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `linrec` (arxiv 2602.08810, /root/reference/pkg/src/linrec).  Every entry
+ * point below replaces one reference interface; the citation is given per
+ * function.  Conventions (mirroring the reference's native loops,
+ * _scan_kernels.py:1-8):
+ *
+ *   - plain device pointers and sizes, no framework types;
+ *   - the CALLER allocates every output and the workspace (the reference's
+ *     kernels also write into a caller-allocated `out`), sized with the
+ *     matching *_workspace_bytes() query;
+ *   - every call is stream-ordered and asynchronous on `stream`
+ *     (a cudaStream_t passed as void*); nothing synchronises the host;
+ *   - calls are reentrant across streams and devices (the reference's
+ *     kernels are nogil and write disjoint slices);
+ *   - return value: LRX_OK or an error code; lrx_last_error() returns a
+ *     thread-local message for the last failure.  Shape/value errors are
+ *     detected before any launch.
+ *
+ * Layouts: generic operator arrays are time-major [L, N] C-contiguous, as in
+ * _scan_kernels.py.  Fused layer kernels take the layer-level layout
+ * [B, L, H] (batch, time, channel) of Layer.forward(u[B, L, d_model])
+ * (layers.py:218-249); parameters keep the shapes of Layer.parameters().
+ * Complex arrays are interleaved (re, im) pairs.
+ */
+#ifndef LRX_H
+#define LRX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (map to ShapeError / ValueError / SingularBilinear in Python) */
+#define LRX_OK 0
+#define LRX_ERR_SHAPE 1       /* numerics.py:42 ShapeError                  */
+#define LRX_ERR_VALUE 2       /* ValueError (bad mode / scheme / dtype)      */
+#define LRX_ERR_SINGULAR 3    /* discretize.py:47 SingularBilinear           */
+#define LRX_ERR_CUDA 4        /* CUDA launch / runtime failure               */
+#define LRX_ERR_UNSUPPORTED 5 /* size outside the compiled kernel range      */
+
+/* element types */
+#define LRX_F32 0
+#define LRX_F64 1
+#define LRX_C64 2
+#define LRX_C128 3
+#define LRX_BF16 4
+
+/* discretization schemes (discretize.py:118-128 SCHEMES) */
+#define LRX_ZOH 0
+#define LRX_BILINEAR 1
+#define LRX_DIRAC 2
+
+const char* lrx_last_error(void);
+int lrx_version(void);
+/* number of kernels launched by this library in this process (monotonic) */
+int64_t lrx_launch_count(void);
+
+/* ------------------------------------------------------------------------ *
+ * Generic operator.  Replaces scan.scan_sequential / scan.scan_parallel
+ * (scan.py:127-201) and the numba loops scan_const/scan_var,
+ * compose_*, local_scan_*, fixup_* (_scan_kernels.py:17-128): one pass,
+ * chunks chained by a decoupled look-back instead of the 3-phase thread pool.
+ *   out[k] = a_k * out[k-1] + b[k],  out[-1] = x0 (zeros when x0 == NULL)
+ * a is [N] (a_per_step = 0) or [L, N]; dtype in {F32, F64, C64, C128}.
+ * ------------------------------------------------------------------------ */
+size_t lrx_scan_workspace_bytes(int dtype, int64_t L, int64_t N);
+int lrx_scan_fwd(int dtype, int a_per_step, const void* a, const void* b, const void* x0,
+                 void* out, int64_t L, int64_t N, void* workspace, size_t workspace_bytes,
+                 void* stream);
+
+/* Reverse-mode pullback.  Replaces autograd._scan_pullback / scan_backward
+ * (autograd.py:113-179) and backward_const/backward_var
+ * (_scan_kernels.py:131-153).  `a` is NOT conjugated by the caller (the
+ * conjugation of the reference's callers happens inside):
+ *   g[k]   = gx[k] + conj(a_{k+1}) g[k+1]          -> gb   [L, N]
+ *   ga     = g[k] conj(x[k-1])  ([L,N] per-step; summed over k to [N] for
+ *            constant a)                            -> ga   (NULL to skip; needs x)
+ *   gx0    = conj(a_0) g[0]                         -> gx0  (NULL to skip)
+ * x is the forward state [L, N]; x0 the forward seed (NULL = zeros). */
+size_t lrx_scan_bwd_workspace_bytes(int dtype, int64_t L, int64_t N);
+int lrx_scan_bwd(int dtype, int a_per_step, const void* a, const void* x, const void* x0,
+                 const void* gx, void* gb, void* ga, void* gx0, int64_t L, int64_t N,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * RG-LRU gated scan, fused (layers.py:1171-1291: _log_a 1208-1210, _gates
+ * 1212-1218, _forward_tape 1239-1250, _backward 1252-1291).
+ *   r = sigmoid(qr + b_r), i = sigmoid(qi + b_i), log a = 8 r log sigmoid(lambda)
+ *   x_k = a_k x_{k-1} + sqrt(-expm1(2 log a_k)) i_k u_k ,  y = x
+ * qr = u W_r^T and qi = u W_i^T are the layer's gate GEMM outputs (bias not
+ * added).  io_dtype in {F32, F64, BF16}; params (lambda, b_r, b_i) are F32 for
+ * F32/BF16 I/O and F64 for F64 I/O.  ckpt receives the state entering every
+ * time chunk ([n_chunks, B*W], compute precision) for the recomputing backward.
+ * ------------------------------------------------------------------------ */
+int lrx_rglru_chunking(int io_dtype, int64_t L, int64_t* chunk_len, int64_t* n_chunks);
+size_t lrx_rglru_workspace_bytes(int io_dtype, int64_t B, int64_t L, int64_t W);
+int lrx_rglru_fwd(int io_dtype, const void* u, const void* qr, const void* qi, const void* lambda_param,
+                  const void* b_r, const void* b_i, void* y, void* ckpt, int64_t B, int64_t L, int64_t W,
+                  void* workspace, size_t workspace_bytes, void* stream);
+/* Backward.  Outputs gu_local = sqrt(1-a^2) i g (the GEMM terms gqr W_r +
+ * gqi W_i are the caller's), gqr, gqi ([B, L, W], io dtype), and the
+ * parameter-gradient sums over batch and time gla = sum 8 r dlog(a),
+ * gb_r = sum gqr, gb_i = sum gqi ([W], compute precision; fixed-order,
+ * compensated).  y is the forward output (= the state); when given (f32/f64
+ * I/O) the backward streams it instead of recomputing, otherwise it
+ * recomputes from ckpt.  Workspace: lrx_rglru_workspace_bytes(). */
+int lrx_rglru_bwd(int io_dtype, const void* u, const void* qr, const void* qi, const void* lambda_param,
+                  const void* b_r, const void* b_i, const void* ckpt, const void* y, const void* gy,
+                  void* gu_local, void* gqr, void* gqi, void* gla, void* gb_r, void* gb_i, int64_t B,
+                  int64_t L, int64_t W, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * S6 selective scan, fused (layers.py:983-1118: _projections 1020-1027,
+ * _forward_tape 1051-1066, _backward 1068-1118).
+ *   delta = softplus(pre + b_delta), abar = exp(delta * a), a = -exp(a_log)
+ *   x_k[d,n] = abar x_{k-1} + delta u B_k[n],  y = sum_n C_k[n] x_k + D u
+ * pre [B,L,D] = (u W_delta) W_delta_proj (bias not added); Bk, Ck [B,L,N].
+ * u / y / gy / gu_local use io_dtype; pre, Bk, Ck and gpre use the compute
+ * precision (F32 for F32/BF16 io, F64 for F64 io).
+ * io_dtype in {F32, F64, BF16}; params (b_delta [D], a_log [D,N], Dskip [D])
+ * F32 (F64 for F64 I/O).  ckpt receives the state at
+ * every ckpt_len-step boundary and, in its last slot, the final state:
+ * [B, n_ckpt, D, N] compute precision (n_ckpt = ceil(L/ckpt_len) + 1).
+ * ------------------------------------------------------------------------ */
+/* geometry: checkpoint interval and count, and the number of channel blocks
+ * (= rows of the gBk/gCk partials) the kernels use for these extents. */
+int lrx_s6_ckpt_len(int io_dtype, int64_t L, int64_t D, int64_t N, int64_t* ckpt_len, int64_t* n_ckpt,
+                    int64_t* n_dblk);
+int lrx_s6_fwd(int io_dtype, const void* u, const void* pre, const void* b_delta, const void* a_log,
+               const void* Bk, const void* Ck, const void* Dskip, void* y, void* ckpt, int64_t B,
+               int64_t L, int64_t D, int64_t N, void* stream);
+/* Outputs: gu_local = D gy + delta * sum_n g B   (GEMM terms are the
+ * caller's) [B,L,D] io dtype; gpre = sigmoid(pre+b) * gdelta [B,L,D]
+ * compute precision;
+ * gBk_part, gCk_part [n_dblk, B, L, N] per channel-block partials;
+ * ga_part (d/d a_log, already times a) [B, D, N]; gD_part, gb_part [B, D]
+ * (compute precision).  Reduce the partial axes with lrx_reduce_rows. */
+int lrx_s6_bwd(int io_dtype, const void* u, const void* pre, const void* b_delta, const void* a_log,
+               const void* Bk, const void* Ck, const void* Dskip, const void* ckpt, const void* gy,
+               void* gu_local, void* gpre, void* gBk_part, void* gCk_part, void* ga_part, void* gD_part,
+               void* gb_part, int64_t B, int64_t L, int64_t D, int64_t N, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * MIMO complex diagonal scan for S5 / LRU (layers.py:616-980): the recurrence
+ * between the dense projections bu = B u and y = Re(C x) (cuBLAS GEMMs):
+ *   x_k[b,p] = abar[p] x_{k-1} + scale[p] bu_k[b,p]        (lanes b*P + p)
+ * bu, x: [B, L, P] complex (C64/C128); abar, scale: [P] complex.
+ * ------------------------------------------------------------------------ */
+size_t lrx_mimo_workspace_bytes(int dtype, int64_t B, int64_t L, int64_t P);
+int lrx_mimo_fwd(int dtype, const void* abar, const void* scale, const void* bu, void* x, int64_t B,
+                 int64_t L, int64_t P, void* workspace, size_t workspace_bytes, void* stream);
+/* Reverse pass, fused with the LTI coefficient reductions
+ * (_MIMOBase._mimo_input_pullback 701-704, S5._backward 836-895,
+ * LRU._backward 945-980):
+ *   g_k = gx_k + conj(abar) g_{k+1};  gbu = conj(scale) g  -> gbu [B,L,P]
+ *   gabar_part[c, b*P+p] = sum_{k in chunk c} g_k conj(x_{k-1})
+ *   gscale_part[c, b*P+p] = sum_{k in chunk c} conj(bu_k) g_k
+ * (reduce the [n_chunks*B, P] partials with lrx_reduce_rows). */
+int lrx_mimo_chunking(int dtype, int64_t L, int64_t* chunk_len, int64_t* n_chunks);
+size_t lrx_mimo_bwd_workspace_bytes(int dtype, int64_t B, int64_t L, int64_t P);
+int lrx_mimo_bwd(int dtype, const void* abar, const void* scale, const void* bu, const void* x,
+                 const void* gx, void* gbu, void* gabar_part, void* gscale_part, int64_t B, int64_t L,
+                 int64_t P, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ *
+ * Deterministic fixed-order reduction: out[j] = sum_r in[r, j]  (dtype any
+ * of F32/F64/C64/C128).  Used for every parameter-gradient partial above so
+ * training is bitwise reproducible (test_acceptance.py:249-250).
+ * ------------------------------------------------------------------------ */
+int lrx_reduce_rows(int dtype, const void* in, void* out, int64_t R, int64_t N, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LRX_H */

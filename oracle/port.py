@@ -836,3 +836,57 @@ def rel_err(got, ref):
     got = np.asarray(got, np.complex128 if np.iscomplexobj(got) else np.float64)
     ref = np.asarray(ref, np.complex128 if np.iscomplexobj(ref) else np.float64)
     return float(np.max(np.abs(got - ref))) / max(float(np.max(np.abs(ref))), 1e-30)
+
+
+# ---------------------------------------------------------------------------
+# scan-level operators (the benchmark unit): the layer math between the dense
+# projections, restated from the same reference lines, for the CPU baseline.
+
+def rglru_scan(u, qr, qi, lam, b_r, b_i, gy, mode="parallel", workers=1):
+    """RG-LRU gates + scan + pullback from gate pre-activations
+    (layers.py:1208-1218, 1239-1291 without the W_r / W_i GEMMs)."""
+    B, L, W = u.shape
+    r = sigmoid(qr + b_r)
+    ig = sigmoid(qi + b_i)
+    la = -softplus(-lam)
+    loga = GATE_POWER * r * la
+    ak = np.exp(loga)
+    sq = np.sqrt(-np.expm1(2.0 * loga))
+    a2 = _tm(ak)
+    xt = _run(mode, workers, a2, True, _tm(sq * ig * u)).reshape(L, B, W)
+    y = np.moveaxis(xt, 0, 1)
+    g2, ga, _ = pullback(a2, True, xt.reshape(L, -1), None, np.ascontiguousarray(_tm(gy)))
+    g = np.moveaxis(g2.reshape(L, B, W), 0, 1)
+    gak = np.moveaxis(ga.reshape(L, B, W), 0, 1)
+    gloga = ak * gak - (ak * ak / sq) * (ig * u * g)
+    gqr = r * (1.0 - r) * (GATE_POWER * la * gloga)
+    gqi = ig * (1.0 - ig) * (sq * u * g)
+    return y, {"gu_local": sq * ig * g, "gqr": gqr, "gqi": gqi,
+               "gla": (GATE_POWER * r * gloga).sum(axis=(0, 1)), "gb_r": gqr.sum(axis=(0, 1)),
+               "gb_i": gqi.sum(axis=(0, 1))}
+
+
+def s6_scan(u, pre, b_delta, a_log, Bk, Ck, D, gy, mode="parallel", workers=1):
+    """S6 selective scan fwd + pullback from the projection outputs
+    (layers.py:1041-1042, 1051-1066, 1068-1098 without the projection GEMMs)."""
+    B, L, m = u.shape
+    n = Bk.shape[-1]
+    a = -np.exp(a_log)
+    pre_b = pre + b_delta
+    delta = softplus(pre_b)
+    abar = np.exp(delta[..., None] * a)
+    a2 = _tm(abar)
+    xt = _run(mode, workers, a2, True, _tm((delta * u)[..., None] * Bk[:, :, None, :])).reshape(L, B, m, n)
+    y = np.einsum("lbhn,bln->blh", xt, Ck, optimize=True) + D * u
+    gxt = np.moveaxis(gy, 1, 0)[..., None] * np.moveaxis(Ck, 1, 0)[:, :, None, :]
+    g2, ga, _ = pullback(a2, True, xt.reshape(L, -1), None, np.ascontiguousarray(gxt.reshape(L, -1)))
+    gw = np.moveaxis(g2.reshape(L, B, m, n), 0, 1)
+    t = abar * np.moveaxis(ga.reshape(L, B, m, n), 0, 1)
+    s1 = np.einsum("blhn,bln->blh", gw, Bk, optimize=True)
+    gdelta = np.einsum("blhn,hn->blh", t, a, optimize=True) + s1 * u
+    gpre = sigmoid(pre_b) * gdelta
+    return y, {"gu_local": gy * D + delta * s1, "gpre": gpre,
+               "gBk": np.einsum("blhn,blh->bln", gw, delta * u, optimize=True),
+               "gCk": np.einsum("blh,lbhn->bln", gy, xt, optimize=True),
+               "ga_log": a * np.einsum("blhn,blh->hn", t, delta, optimize=True),
+               "gD": np.einsum("blh,blh->h", gy, u, optimize=True), "gb_delta": gpre.sum(axis=(0, 1))}

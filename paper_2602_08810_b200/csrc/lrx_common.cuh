@@ -1,0 +1,255 @@
+// Shared device-side building blocks for the lrx sm_100a kernels.
+//
+//  * value types: real float/double, complex cplx<float>/cplx<double> with the
+//    plain (non-Annex-G) product the reference's numba kernels use;
+//  * I/O element conversion (bf16 / f32 / f64 storage -> compute precision);
+//  * the overflow-safe softplus / sigmoid of the reference
+//    (pkg/src/linrec/numerics.py:36-39, 86-105);
+//  * the decoupled look-back that chains time chunks of a first-order
+//    recurrence across CTAs: each (lane block, chunk) tile publishes its
+//    aggregate (A = prod a, X = local state from zero) and, once its carry is
+//    known, the inclusive state; successors fold a FIXED set of predecessor
+//    aggregates and one anchor's inclusive value (bitwise deterministic).
+//    Tiles are handed out in launch order by an atomic ticket, so every awaited
+//    predecessor is already resident or done (forward progress without
+//    cooperative launch).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lrx {
+
+// ---------------------------------------------------------------- complex
+template <typename T>
+struct cplx {
+    T re, im;
+};
+
+template <typename T> __host__ __device__ __forceinline__ cplx<T> mk(T r, T i) { return cplx<T>{r, i}; }
+template <typename T> __device__ __forceinline__ cplx<T> operator+(cplx<T> a, cplx<T> b) { return {a.re + b.re, a.im + b.im}; }
+template <typename T> __device__ __forceinline__ cplx<T> operator-(cplx<T> a, cplx<T> b) { return {a.re - b.re, a.im - b.im}; }
+template <typename T> __device__ __forceinline__ cplx<T> operator*(cplx<T> a, cplx<T> b) {
+    return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+template <typename T> __device__ __forceinline__ cplx<T> operator*(T s, cplx<T> b) { return {s * b.re, s * b.im}; }
+template <typename T> __device__ __forceinline__ cplx<T> conj(cplx<T> a) { return {a.re, -a.im}; }
+
+template <typename V> struct Traits;
+template <> struct Traits<float> {
+    using R = float;
+    static constexpr bool complex = false;
+    __device__ static float one() { return 1.f; }
+    __device__ static float zero() { return 0.f; }
+    __device__ static float cj(float a) { return a; }
+};
+template <> struct Traits<double> {
+    using R = double;
+    static constexpr bool complex = false;
+    __device__ static double one() { return 1.0; }
+    __device__ static double zero() { return 0.0; }
+    __device__ static double cj(double a) { return a; }
+};
+template <typename T> struct Traits<cplx<T>> {
+    using R = T;
+    static constexpr bool complex = true;
+    __device__ static cplx<T> one() { return {T(1), T(0)}; }
+    __device__ static cplx<T> zero() { return {T(0), T(0)}; }
+    __device__ static cplx<T> cj(cplx<T> a) { return conj(a); }
+};
+
+// ---------------------------------------------------------------- I/O
+__device__ __forceinline__ float ld_io(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float ld_io(const float* p) { return *p; }
+__device__ __forceinline__ double ld_io(const double* p) { return *p; }
+template <typename C> __device__ __forceinline__ void st_io(__nv_bfloat16* p, C v) { *p = __float2bfloat16_rn(float(v)); }
+template <typename C> __device__ __forceinline__ void st_io(float* p, C v) { *p = float(v); }
+template <typename C> __device__ __forceinline__ void st_io(double* p, C v) { *p = double(v); }
+
+// register value -> compute precision
+__device__ __forceinline__ float cvt(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float cvt(float v) { return v; }
+__device__ __forceinline__ double cvt(double v) { return v; }
+
+// streaming (read-once) loads: keep them out of L1
+template <typename X> __device__ __forceinline__ X ld_stream(const X* p) { return __ldcs(p); }
+__device__ __forceinline__ __nv_bfloat16 ld_stream(const __nv_bfloat16* p) {
+    unsigned short r = __ldcs(reinterpret_cast<const unsigned short*>(p));
+    return *reinterpret_cast<__nv_bfloat16*>(&r);
+}
+
+// ---------------------------------------------------------------- math
+template <typename C> struct Math;
+template <> struct Math<float> {
+    static constexpr float SOFTPLUS_T = 30.f;  // numerics.py:36-39 (float32)
+    __device__ static float exp(float x) { return expf(x); }
+    __device__ static float log1p(float x) { return log1pf(x); }
+    __device__ static float expm1(float x) { return expm1f(x); }
+    __device__ static float sqrt(float x) { return sqrtf(x); }
+    __device__ static float softplus(float x) { return x > SOFTPLUS_T ? x : log1pf(expf(fminf(x, SOFTPLUS_T))); }
+    __device__ static float sigmoid(float x) {  // numerics.py:97-105
+        float e = expf(x >= 0.f ? -x : x);
+        return x >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+    }
+};
+template <> struct Math<double> {
+    static constexpr double SOFTPLUS_T = 50.0;  // numerics.py:36-39 (float64)
+    __device__ static double exp(double x) { return ::exp(x); }
+    __device__ static double log1p(double x) { return ::log1p(x); }
+    __device__ static double expm1(double x) { return ::expm1(x); }
+    __device__ static double sqrt(double x) { return ::sqrt(x); }
+    __device__ static double softplus(double x) { return x > SOFTPLUS_T ? x : ::log1p(::exp(fmin(x, SOFTPLUS_T))); }
+    __device__ static double sigmoid(double x) {
+        double e = ::exp(x >= 0.0 ? -x : x);
+        return x >= 0.0 ? 1.0 / (1.0 + e) : e / (1.0 + e);
+    }
+};
+
+// Fast fp32 math for the hot loops (MUFU ex2 / rcp based).  Accuracy is
+// ~2 ulp, well inside the 1e-4 fp32 parity bar; expm1 keeps full relative
+// accuracy near 0 with a short Taylor polynomial (sqrt(1 - a^2) for a -> 1 is
+// exactly where a naive exp(x) - 1 cancels, layers.py:1217).
+template <typename C> struct Fast;
+template <> struct Fast<float> {
+    __device__ static float exp(float x) { return __expf(x); }
+    __device__ static float rcp(float x) { return __frcp_rn(x); }
+    __device__ static float div(float a, float b) { return __fdividef(a, b); }
+    __device__ static float sqrt(float x) { return __fsqrt_rn(x); }
+    __device__ static float sigmoid(float x) {
+        const float e = __expf(-fabsf(x));           // never overflows
+        const float r = __frcp_rn(1.f + e);
+        return x >= 0.f ? r : e * r;
+    }
+    __device__ static float expm1(float x) {
+        if (fabsf(x) < 0.35f) {
+            float p = 1.f / 5040.f;
+            p = fmaf(p, x, 1.f / 720.f);
+            p = fmaf(p, x, 1.f / 120.f);
+            p = fmaf(p, x, 1.f / 24.f);
+            p = fmaf(p, x, 1.f / 6.f);
+            p = fmaf(p, x, 0.5f);
+            p = fmaf(p, x, 1.f);
+            return p * x;
+        }
+        return __expf(x) - 1.f;
+    }
+};
+template <> struct Fast<double> {
+    __device__ static double exp(double x) { return ::exp(x); }
+    __device__ static double rcp(double x) { return 1.0 / x; }
+    __device__ static double div(double a, double b) { return a / b; }
+    __device__ static double sqrt(double x) { return ::sqrt(x); }
+    __device__ static double sigmoid(double x) { return Math<double>::sigmoid(x); }
+    __device__ static double expm1(double x) { return ::expm1(x); }
+};
+
+// ---------------------------------------------------------------- look-back
+// Status words per tile: 0 = nothing yet, 1 = aggregate published,
+// 2 = inclusive published.  Tiles are (chunk, lane block); values are per lane.
+enum : int { LB_EMPTY = 0, LB_AGG = 1, LB_INC = 2 };
+
+struct LookbackWS {
+    int* ticket;   // [1]
+    int* status;   // [n_chunks * n_blk]
+    void* agg_a;   // [n_chunks * n_lanes] of V
+    void* agg_x;   // [n_chunks * n_lanes] of V
+    void* inc_x;   // [n_chunks * n_lanes] of V  (state leaving the chunk)
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// CTA-wide: obtain this CTA's tile index in launch order.
+__device__ __forceinline__ int next_tile(int* ticket) {
+    __shared__ int s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+    __syncthreads();
+    return s_tile;
+}
+
+// Publish per-lane values, then the tile status (CTA-wide call).
+template <typename V> __device__ __forceinline__ V ldcg(const V* p) { return __ldcg(p); }
+template <> __device__ __forceinline__ cplx<float> ldcg(const cplx<float>* p) {
+    float2 v = __ldcg(reinterpret_cast<const float2*>(p));
+    return {v.x, v.y};
+}
+template <> __device__ __forceinline__ cplx<double> ldcg(const cplx<double>* p) {
+    double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+    return {v.x, v.y};
+}
+__device__ __forceinline__ void stcg_v(cplx<float>* p, cplx<float> v) { __stcg(reinterpret_cast<float2*>(p), make_float2(v.re, v.im)); }
+__device__ __forceinline__ void stcg_v(cplx<double>* p, cplx<double> v) { __stcg(reinterpret_cast<double2*>(p), make_double2(v.re, v.im)); }
+__device__ __forceinline__ void stcg_v(float* p, float v) { __stcg(p, v); }
+__device__ __forceinline__ void stcg_v(double* p, double v) { __stcg(p, v); }
+
+// Publish per-lane values (a may be skipped), then the tile status.  CTA-wide.
+template <typename V>
+__device__ __forceinline__ void lb_publish(int* status_word, int flag, V* dst_a, V a, V* dst_x, V x,
+                                           bool valid) {
+    if (valid) {
+        if (dst_a) stcg_v(dst_a, a);
+        stcg_v(dst_x, x);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(status_word, flag);
+}
+
+// Anchored look-back: return the carry entering scan-order chunk c (c >= 1)
+// for this thread's lane.  Chunk c folds the aggregates of chunks
+// anchor+1 .. c-1 and then the INCLUSIVE value of its anchor, where
+// anchor = the nearest multiple of kAnchor below c.  The fold set is a fixed
+// function of c, so the result is bitwise reproducible run to run (unlike a
+// classic decoupled look-back whose fold depth depends on timing); the
+// serial dependency only runs through the anchors (1 in kAnchor chunks).
+// CTA-wide call.
+constexpr int kAnchor = 8;
+
+__device__ __forceinline__ int lb_wait(const int* w, int want) {
+    __shared__ int s_flag;
+    if (threadIdx.x == 0) {
+        int f;
+        while ((f = ld_acquire(w)) < want) __nanosleep(20);
+        s_flag = f;
+    }
+    __syncthreads();
+    const int f = s_flag;
+    __syncthreads();
+    return f;
+}
+
+template <typename V>
+__device__ V lb_lookback(const LookbackWS& ws, int c, int blk, int n_blk, int64_t lane, int64_t n_lanes,
+                         bool valid) {
+    using Tr = Traits<V>;
+    const V* agg_a = static_cast<const V*>(ws.agg_a);
+    const V* agg_x = static_cast<const V*>(ws.agg_x);
+    const V* inc_x = static_cast<const V*>(ws.inc_x);
+    const int anchor = ((c - 1) / kAnchor) * kAnchor;
+    V A = Tr::one(), X = Tr::zero();
+    for (int p = c - 1; p > anchor; --p) {
+        lb_wait(ws.status + (int64_t)p * n_blk + blk, LB_AGG);
+        if (valid) {
+            const int64_t off = (int64_t)p * n_lanes + lane;
+            const V pa = ldcg(agg_a + off), px = ldcg(agg_x + off);
+            X = A * px + X;
+            A = A * pa;
+        }
+    }
+    lb_wait(ws.status + (int64_t)anchor * n_blk + blk, LB_INC);
+    if (valid) X = A * ldcg(inc_x + (int64_t)anchor * n_lanes + lane) + X;
+    return X;
+}
+
+template <typename V>
+__device__ __forceinline__ void lb_store(V* base, int64_t off, V v, bool valid) {
+    if (valid) stcg_v(base + off, v);
+}
+
+}  // namespace lrx

@@ -1,0 +1,831 @@
+// RG-LRU (Griffin) gated recurrence, fused forward / backward.
+//
+// Reference: pkg/src/linrec/layers.py RGLRU (1171-1336): _log_a 1208-1210,
+// _gates 1212-1218, _forward_tape 1239-1250, _backward 1252-1291.
+//
+//   r = sigmoid(qr + b_r), i = sigmoid(qi + b_i)      qr = u W_r^T, qi = u W_i^T
+//   log a_k = 8 r_k log sigmoid(lambda),  a_k = exp(log a_k)
+//   s_k = sqrt(-expm1(2 log a_k)),  x_k = a_k x_{k-1} + s_k i_k u_k,  y = x
+//
+// Layout [B, L, W] (channel-contiguous, as the layer's u); lane = (b, w).
+// Gates and discretisation are computed in the load path: the forward reads
+// u, qr, qi once and writes y once; the backward reads u, qr, qi, gy and the
+// saved output y (= the state, so x_{k-1} needs no recompute) once and writes
+// gu, gqr, gqi once.
+//
+// Three kernel families, chosen per call (LRX_RGLRU_MODE overrides):
+//  * tma      one CTA per LW-lane column block walks the whole sequence; time
+//             tiles of PF steps x LW channels arrive by TMA into an S-stage
+//             shared-memory ring (full/empty mbarriers), threads read their
+//             channel column.  Registers hold no in-flight data, so every
+//             lane of the problem is resident in one wave.  LW in {128,64,32}
+//             keeps >= 4 CTAs per SM when lanes are scarce (8-GPU sharding).
+//  * stream   same walk with a register prefetch (fallback when the rows are
+//             not 16-byte aligned for TMA).
+//  * lookback time chunks of T steps across CTAs chained by the anchored
+//             look-back (lrx_common.cuh); the backward recomputes states from
+//             per-chunk checkpoints (used for bf16 I/O, where y is rounded).
+#include <stdlib.h>
+#include <string.h>
+
+#include "lrx_common.cuh"
+#include "lrx_host.h"
+#include "lrx_tma.cuh"
+
+namespace lrx {
+namespace rglru {
+
+constexpr int kThreads = 128;
+constexpr float kGate = 8.0f;  // GATE_POWER, layers.py:1177
+
+template <typename IO> struct Tile { static constexpr int T = 16; };
+template <> struct Tile<double> { static constexpr int T = 8; };
+
+template <typename C>
+struct Coef {
+    C r, i, a, s, u;
+};
+
+template <typename C, typename IO>
+__device__ __forceinline__ Coef<C> gates(IO uu, IO q_r, IO q_i, C la, C br, C bi) {
+    using F = Fast<C>;
+    Coef<C> k;
+    k.u = cvt(uu);
+    k.r = F::sigmoid(C(cvt(q_r)) + br);
+    k.i = F::sigmoid(C(cvt(q_i)) + bi);
+    const C loga = (C(kGate) * k.r) * la;
+    k.a = F::exp(loga);
+    k.s = F::sqrt(-F::expm1(C(2) * loga));
+    return k;
+}
+
+// Compensated (Kahan) accumulator: the per-lane parameter-gradient sums run
+// over up to 2^20 steps in fp32.
+template <typename C>
+struct Kahan {
+    C s = 0, c = 0;
+    __device__ __forceinline__ void add(C v) {
+        const C y = v - c;
+        const C t = s + y;
+        c = (t - s) - y;
+        s = t;
+    }
+};
+
+template <typename C>
+struct BwdOut {
+    C gu, gqr, gqi, la_term;
+};
+template <typename C>
+__device__ __forceinline__ BwdOut<C> bwd_step(const Coef<C>& q, C g, C xprev, C la) {
+    const C gak = g * xprev;
+    const C gs = (q.i * q.u) * g;
+    const C gloga = q.a * gak - Fast<C>::div(q.a * q.a, q.s) * gs;
+    BwdOut<C> o;
+    o.gqr = (q.r * (C(1) - q.r)) * ((C(kGate) * la) * gloga);
+    o.gqi = (q.i * (C(1) - q.i)) * ((q.s * q.u) * g);
+    o.gu = (q.s * q.i) * g;
+    o.la_term = (C(kGate) * q.r) * gloga;
+    return o;
+}
+
+// ====================================================================== TMA
+template <typename IO>
+struct Ring {
+    uint64_t* full;
+    uint64_t* empty;
+    IO* data;  // [S][NARR][PF][LW]
+};
+
+template <typename IO>
+__device__ __forceinline__ Ring<IO> ring(unsigned char* smem, int S) {
+    Ring<IO> r;
+    r.full = reinterpret_cast<uint64_t*>(smem);
+    r.empty = r.full + S;
+    r.data = reinterpret_cast<IO*>(smem + 128 * ((2 * S * 8 + 127) / 128));
+    return r;
+}
+
+template <typename IO, typename C, int LW, int PF>
+__global__ void __launch_bounds__(LW) fwd_tma_kernel(const __grid_constant__ CUtensorMap mu,
+                                                     const __grid_constant__ CUtensorMap mr,
+                                                     const __grid_constant__ CUtensorMap mi, const C* __restrict__ lam,
+                                                     const C* __restrict__ b_r, const C* __restrict__ b_i,
+                                                     IO* __restrict__ y, C* __restrict__ ckpt, int64_t L, int64_t W,
+                                                     int n_wblk, int Bn, int S) {
+    constexpr int CK = Tile<IO>::T;
+    constexpr int NW = LW / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    auto R = ring<IO>(smem, S);
+    const int tid = threadIdx.x;
+    const int b = blockIdx.x / n_wblk;
+    const int w0 = (blockIdx.x % n_wblk) * LW;
+    const int64_t w = w0 + tid;
+    const bool valid = w < W;
+    const int row0 = b * (int)L;
+    const int n_tiles = (int)((L + PF - 1) / PF);
+    constexpr uint32_t kStageBytes = 3u * PF * LW * sizeof(IO);
+    if (tid == 0) {
+        tma::prefetch_map(&mu);
+        tma::prefetch_map(&mr);
+        tma::prefetch_map(&mi);
+        for (int s = 0; s < S; ++s) {
+            tma::mbar_init(&R.full[s], 1);
+            tma::mbar_init(&R.empty[s], NW);
+        }
+        tma::fence_barrier_init();
+    }
+    __syncthreads();
+    auto issue = [&](int j) {
+        const int s = j % S;
+        IO* dst = R.data + (size_t)s * 3 * PF * LW;
+        tma::mbar_arrive_expect_tx(&R.full[s], kStageBytes);
+        tma::load_2d(dst, &mu, w0, row0 + j * PF, &R.full[s]);
+        tma::load_2d(dst + PF * LW, &mr, w0, row0 + j * PF, &R.full[s]);
+        tma::load_2d(dst + 2 * PF * LW, &mi, w0, row0 + j * PF, &R.full[s]);
+    };
+    if (tid == 0)
+        for (int j = 0; j < S && j < n_tiles; ++j) issue(j);
+
+    C la = 0, br = 0, bi = 0;
+    if (valid) {
+        la = -Math<C>::softplus(-lam[w]);
+        br = b_r[w];
+        bi = b_i[w];
+    }
+    C x = 0;
+    IO* py = y + (int64_t)row0 * W + w;
+    C* pc = ckpt ? ckpt + (int64_t)b * W + w : nullptr;
+    const int64_t ck_stride = (int64_t)Bn * W;
+    for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % S;
+        const uint32_t ph = (j / S) & 1;
+        tma::mbar_wait(&R.full[s], ph);
+        const IO* src = R.data + (size_t)s * 3 * PF * LW + tid;
+        IO cu[PF], cr[PF], ci[PF];
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            cu[k] = src[k * LW];
+            cr[k] = src[(PF + k) * LW];
+            ci[k] = src[(2 * PF + k) * LW];
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) tma::mbar_arrive(&R.empty[s]);
+        if (tid == 0 && j + S < n_tiles) {
+            tma::mbar_wait(&R.empty[s], ph);
+            issue(j + S);
+        }
+        const int64_t t0 = (int64_t)j * PF;
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            const int64_t t = t0 + k;
+            if (t < L) {
+                if (pc && (t % CK) == 0) {
+                    if (valid) __stcs(pc, x);
+                    pc += ck_stride;
+                }
+                const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
+                x = q.a * x + (q.s * q.i) * q.u;
+                if (valid) st_io(py + t * W, x);
+            }
+        }
+    }
+}
+
+// Reverse streaming pass; the y tile of a time tile is loaded one row early
+// so its row k holds x_{t-1}.
+template <typename IO, typename C, int LW, int PF>
+__global__ void __launch_bounds__(LW) bwd_tma_kernel(
+    const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mr,
+    const __grid_constant__ CUtensorMap mi, const __grid_constant__ CUtensorMap mg,
+    const __grid_constant__ CUtensorMap my, const C* __restrict__ lam, const C* __restrict__ b_r,
+    const C* __restrict__ b_i, IO* __restrict__ gu, IO* __restrict__ gqr, IO* __restrict__ gqi,
+    C* __restrict__ gla_part, C* __restrict__ gbr_part, C* __restrict__ gbi_part, int64_t L, int64_t W, int n_wblk,
+    int S) {
+    constexpr int NW = LW / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    auto R = ring<IO>(smem, S);
+    const int tid = threadIdx.x;
+    const int b = blockIdx.x / n_wblk;
+    const int w0 = (blockIdx.x % n_wblk) * LW;
+    const int64_t w = w0 + tid;
+    const bool valid = w < W;
+    const int row0 = b * (int)L;
+    const int n_tiles = (int)((L + PF - 1) / PF);
+    constexpr uint32_t kStageBytes = 5u * PF * LW * sizeof(IO);
+    if (tid == 0) {
+        tma::prefetch_map(&mu);
+        tma::prefetch_map(&mr);
+        tma::prefetch_map(&mi);
+        tma::prefetch_map(&mg);
+        tma::prefetch_map(&my);
+        for (int s = 0; s < S; ++s) {
+            tma::mbar_init(&R.full[s], 1);
+            tma::mbar_init(&R.empty[s], NW);
+        }
+        tma::fence_barrier_init();
+    }
+    __syncthreads();
+    auto issue = [&](int j) {  // j-th tile in reverse order
+        const int tt = n_tiles - 1 - j;
+        const int s = j % S;
+        IO* dst = R.data + (size_t)s * 5 * PF * LW;
+        const int r = row0 + tt * PF;
+        tma::mbar_arrive_expect_tx(&R.full[s], kStageBytes);
+        tma::load_2d(dst, &mu, w0, r, &R.full[s]);
+        tma::load_2d(dst + PF * LW, &mr, w0, r, &R.full[s]);
+        tma::load_2d(dst + 2 * PF * LW, &mi, w0, r, &R.full[s]);
+        tma::load_2d(dst + 3 * PF * LW, &mg, w0, r, &R.full[s]);
+        tma::load_2d(dst + 4 * PF * LW, &my, w0, r - 1, &R.full[s]);  // rows t-1
+    };
+    if (tid == 0)
+        for (int j = 0; j < S && j < n_tiles; ++j) issue(j);
+
+    C la = 0, br = 0, bi = 0;
+    if (valid) {
+        la = -Math<C>::softplus(-lam[w]);
+        br = b_r[w];
+        bi = b_i[w];
+    }
+    C h = 0;
+    Kahan<C> sla, sbr, sbi;
+    const int64_t base = (int64_t)row0 * W + w;
+    for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % S;
+        const uint32_t ph = (j / S) & 1;
+        const int tt = n_tiles - 1 - j;
+        tma::mbar_wait(&R.full[s], ph);
+        const IO* src = R.data + (size_t)s * 5 * PF * LW + tid;
+        IO cu[PF], cr[PF], ci[PF], cg[PF], cy[PF];
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            cu[k] = src[k * LW];
+            cr[k] = src[(PF + k) * LW];
+            ci[k] = src[(2 * PF + k) * LW];
+            cg[k] = src[(3 * PF + k) * LW];
+            cy[k] = src[(4 * PF + k) * LW];
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) tma::mbar_arrive(&R.empty[s]);
+        if (tid == 0 && j + S < n_tiles) {
+            tma::mbar_wait(&R.empty[s], ph);
+            issue(j + S);
+        }
+        const int64_t t0 = (int64_t)tt * PF;
+#pragma unroll
+        for (int k = PF - 1; k >= 0; --k) {
+            const int64_t t = t0 + k;
+            if (t < L) {
+                const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
+                const C g = C(cvt(cg[k])) + h;
+                h = q.a * g;
+                const C xp = t == 0 ? C(0) : C(cvt(cy[k]));
+                const BwdOut<C> o = bwd_step<C>(q, g, xp, la);
+                if (valid) {
+                    const int64_t off = base + t * W;
+                    st_io(gu + off, o.gu);
+                    st_io(gqr + off, o.gqr);
+                    st_io(gqi + off, o.gqi);
+                }
+                sla.add(o.la_term);
+                sbr.add(o.gqr);
+                sbi.add(o.gqi);
+            }
+        }
+    }
+    if (valid) {
+        const int64_t p = (int64_t)b * W + w;
+        gla_part[p] = sla.s;
+        gbr_part[p] = sbr.s;
+        gbi_part[p] = sbi.s;
+    }
+}
+
+// ==================================================================== stream
+template <typename IO, typename C, int PF>
+__global__ void __launch_bounds__(kThreads) fwd_stream_kernel(
+    const IO* __restrict__ u, const IO* __restrict__ qr, const IO* __restrict__ qi, const C* __restrict__ lam,
+    const C* __restrict__ b_r, const C* __restrict__ b_i, IO* __restrict__ y, C* __restrict__ ckpt, int64_t L,
+    int64_t W, int n_wblk, int Bn) {
+    constexpr int CK = Tile<IO>::T;
+    static_assert(CK % PF == 0, "checkpoint interval must be a multiple of the prefetch tile");
+    using M = Math<C>;
+    const int blk = blockIdx.x;
+    const int b = blk / n_wblk;
+    const int64_t w = (int64_t)(blk % n_wblk) * kThreads + threadIdx.x;
+    if (w >= W) return;
+    const C la = -M::softplus(-lam[w]), br = b_r[w], bi = b_i[w];
+    const int64_t base = (int64_t)b * L * W + w;
+    const IO *pu = u + base, *pr = qr + base, *pi = qi + base;
+    IO* py = y + base;
+    C* pc = ckpt ? ckpt + (int64_t)b * W + w : nullptr;
+    const int64_t ck_stride = (int64_t)Bn * W;
+    IO nu[PF], nr[PF], ni[PF];
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+        const bool ok = k < L;
+        nu[k] = ok ? ld_stream(pu + k * W) : IO(0);
+        nr[k] = ok ? ld_stream(pr + k * W) : IO(0);
+        ni[k] = ok ? ld_stream(pi + k * W) : IO(0);
+    }
+    C x = 0;
+    for (int64_t t0 = 0; t0 < L; t0 += PF) {
+        IO cu[PF], cr[PF], ci[PF];
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            cu[k] = nu[k];
+            cr[k] = nr[k];
+            ci[k] = ni[k];
+        }
+        const int64_t tn = t0 + PF;
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            const bool ok = tn + k < L;
+            const int64_t off = (tn + k) * W;
+            nu[k] = ok ? ld_stream(pu + off) : IO(0);
+            nr[k] = ok ? ld_stream(pr + off) : IO(0);
+            ni[k] = ok ? ld_stream(pi + off) : IO(0);
+        }
+        if (pc && (t0 % CK) == 0) {
+            __stcs(pc, x);
+            pc += ck_stride;
+        }
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            if (t0 + k < L) {
+                const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
+                x = q.a * x + (q.s * q.i) * q.u;
+                st_io(py + (t0 + k) * W, x);
+            }
+        }
+    }
+}
+
+// ================================================================== lookback
+template <typename IO, typename C>
+__global__ void __launch_bounds__(kThreads, 4) fwd_kernel(const IO* __restrict__ u, const IO* __restrict__ qr,
+                                                          const IO* __restrict__ qi, const C* __restrict__ lam,
+                                                          const C* __restrict__ b_r, const C* __restrict__ b_i,
+                                                          IO* __restrict__ y, C* __restrict__ ckpt, int64_t L,
+                                                          int64_t W, int n_wblk, int n_blk, LookbackWS ws) {
+    constexpr int T = Tile<IO>::T;
+    using M = Math<C>;
+    const int tile = next_tile(ws.ticket);
+    const int c = tile / n_blk, blk = tile % n_blk;
+    const int b = blk / n_wblk;
+    const int64_t w = (int64_t)(blk % n_wblk) * kThreads + threadIdx.x;
+    const bool valid = w < W;
+    const int64_t n_lanes = (int64_t)n_blk * kThreads;
+    const int64_t lane = (int64_t)blk * kThreads + threadIdx.x;  // padded lane id
+    const int64_t t0 = (int64_t)c * T;
+    const int nt = (int)min((int64_t)T, L - t0);
+
+    C la = 0, br = 0, bi = 0;
+    if (valid) {
+        la = -M::softplus(-lam[w]);  // log sigmoid(lambda), layers.py:1208-1210
+        br = b_r[w];
+        bi = b_i[w];
+    }
+    IO uu[T], rr[T], ii[T];
+    const int64_t base = ((int64_t)b * L + t0) * W + (valid ? w : 0);
+    {
+        const IO *pu = u + base, *pr = qr + base, *pi = qi + base;
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+            const bool ok = valid && k < nt;
+            uu[k] = ok ? ld_stream(pu) : IO(0);
+            rr[k] = ok ? ld_stream(pr) : IO(0);
+            ii[k] = ok ? ld_stream(pi) : IO(0);
+            pu += W;
+            pr += W;
+            pi += W;
+        }
+    }
+    C av[T], bv[T];
+    C A = 1, X = 0;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        const Coef<C> q = gates<C>(uu[k], rr[k], ii[k], la, br, bi);
+        const bool ok = k < nt;
+        av[k] = ok ? q.a : C(1);
+        bv[k] = ok ? (q.s * q.i) * q.u : C(0);
+        X = av[k] * X + bv[k];
+        A = av[k] * A;
+    }
+    C* agg_a = static_cast<C*>(ws.agg_a);
+    C* agg_x = static_cast<C*>(ws.agg_x);
+    C* inc_x = static_cast<C*>(ws.inc_x);
+    const int64_t woff = (int64_t)c * n_lanes + lane;
+    int* sw = ws.status + (int64_t)c * n_blk + blk;
+    C xin = 0;
+    if (c > 0) {
+        lb_publish<C>(sw, LB_AGG, agg_a + woff, A, agg_x + woff, X, valid);
+        xin = lb_lookback<C>(ws, c, blk, n_blk, lane, n_lanes, valid);
+    }
+    if ((c % kAnchor) == 0) lb_publish<C>(sw, LB_INC, (C*)nullptr, A, inc_x + woff, A * xin + X, valid);
+    const int Bn = n_blk / n_wblk;
+    if (valid && ckpt) ckpt[((int64_t)c * Bn + b) * W + w] = xin;
+    C x = xin;
+    IO* py = y + base;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        x = av[k] * x + bv[k];
+        if (valid && k < nt) st_io(py, x);
+        py += W;
+    }
+}
+
+// Backward.  Reverse recurrence g_k = gy_k + a_{k+1} g_{k+1}; the carry passed
+// leftwards between chunks is h = a_{t0} g_{t0} (layers.py:1252-1291 with
+// autograd._scan_pullback 113-140).  States are recomputed from the chunk's
+// entering state saved by the forward.
+template <typename IO, typename C>
+__global__ void __launch_bounds__(kThreads, 3) bwd_kernel(
+    const IO* __restrict__ u, const IO* __restrict__ qr, const IO* __restrict__ qi, const C* __restrict__ lam,
+    const C* __restrict__ b_r, const C* __restrict__ b_i, const C* __restrict__ ckpt, const IO* __restrict__ gy,
+    IO* __restrict__ gu, IO* __restrict__ gqr, IO* __restrict__ gqi, C* __restrict__ gla_part,
+    C* __restrict__ gbr_part, C* __restrict__ gbi_part, int64_t L, int64_t W, int n_wblk, int n_blk,
+    int n_chunks, LookbackWS ws) {
+    constexpr int T = Tile<IO>::T;
+    using M = Math<C>;
+    const int tile = next_tile(ws.ticket);
+    const int s = tile / n_blk, blk = tile % n_blk;
+    const int c = n_chunks - 1 - s;
+    const int b = blk / n_wblk;
+    const int64_t w = (int64_t)(blk % n_wblk) * kThreads + threadIdx.x;
+    const bool valid = w < W;
+    const int64_t n_lanes = (int64_t)n_blk * kThreads;
+    const int64_t lane = (int64_t)blk * kThreads + threadIdx.x;
+    const int64_t t0 = (int64_t)c * T;
+    const int nt = (int)min((int64_t)T, L - t0);
+
+    C la = 0, br = 0, bi = 0;
+    if (valid) {
+        la = -M::softplus(-lam[w]);
+        br = b_r[w];
+        bi = b_i[w];
+    }
+    IO uu[T], rr[T], ii[T], gg[T];
+    const int64_t base = ((int64_t)b * L + t0) * W + (valid ? w : 0);
+    {
+        const IO *pu = u + base, *pr = qr + base, *pi = qi + base, *pg = gy + base;
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+            const bool ok = valid && k < nt;
+            uu[k] = ok ? ld_stream(pu) : IO(0);
+            rr[k] = ok ? ld_stream(pr) : IO(0);
+            ii[k] = ok ? ld_stream(pi) : IO(0);
+            gg[k] = ok ? ld_stream(pg) : IO(0);
+            pu += W;
+            pr += W;
+            pi += W;
+            pg += W;
+        }
+    }
+    C xprev[T], av[T];
+    const int Bn = n_blk / n_wblk;
+    C x = valid ? ckpt[((int64_t)c * Bn + b) * W + w] : C(0);
+    C A = 1;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        const Coef<C> q = gates<C>(uu[k], rr[k], ii[k], la, br, bi);
+        const bool ok = k < nt;
+        xprev[k] = x;
+        av[k] = ok ? q.a : C(1);
+        x = av[k] * x + (ok ? (q.s * q.i) * q.u : C(0));
+        A = av[k] * A;
+    }
+    C H = 0;
+#pragma unroll
+    for (int k = T - 1; k >= 0; --k) {
+        const C g = C(cvt(gg[k])) + H;
+        H = av[k] * g;
+    }
+    C* agg_a = static_cast<C*>(ws.agg_a);
+    C* agg_x = static_cast<C*>(ws.agg_x);
+    C* inc_x = static_cast<C*>(ws.inc_x);
+    const int64_t woff = (int64_t)s * n_lanes + lane;
+    int* sw = ws.status + (int64_t)s * n_blk + blk;
+    C hin = 0;
+    if (s > 0) {
+        lb_publish<C>(sw, LB_AGG, agg_a + woff, A, agg_x + woff, H, valid);
+        hin = lb_lookback<C>(ws, s, blk, n_blk, lane, n_lanes, valid);
+    }
+    if ((s % kAnchor) == 0) lb_publish<C>(sw, LB_INC, (C*)nullptr, A, inc_x + woff, A * hin + H, valid);
+
+    C h = hin, sla = 0, sbr = 0, sbi = 0;
+#pragma unroll
+    for (int k = T - 1; k >= 0; --k) {
+        if (valid && k < nt) {
+            const Coef<C> q = gates<C>(uu[k], rr[k], ii[k], la, br, bi);
+            const C g = C(cvt(gg[k])) + h;
+            h = q.a * g;
+            const BwdOut<C> o = bwd_step<C>(q, g, xprev[k], la);
+            const int64_t off = base + (int64_t)k * W;
+            st_io(gu + off, o.gu);
+            st_io(gqr + off, o.gqr);
+            st_io(gqi + off, o.gqi);
+            sla += o.la_term;
+            sbr += o.gqr;
+            sbi += o.gqi;
+        }
+    }
+    if (valid) {
+        const int64_t p = ((int64_t)c * Bn + b) * W + w;
+        gla_part[p] = sla;
+        gbr_part[p] = sbr;
+        gbi_part[p] = sbi;
+    }
+}
+
+// Kahan-compensated fixed-order column sums: out[j] = sum_r in[r, j].
+template <typename C>
+__global__ void colsum_kernel(const C* __restrict__ in, C* __restrict__ out, int64_t R, int64_t N) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    Kahan<C> k;
+    for (int64_t r = 0; r < R; ++r) k.add(in[r * N + j]);
+    out[j] = k.s;
+}
+
+// ====================================================================== host
+static int mode_env() {
+    static int m = -1;
+    if (m < 0) {
+        const char* e = getenv("LRX_RGLRU_MODE");
+        m = !e ? 0 : !strcmp(e, "tma") ? 1 : !strcmp(e, "stream") ? 2 : !strcmp(e, "lookback") ? 3 : 0;
+    }
+    return m;
+}
+
+static int sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+template <typename IO>
+static void geometry(int64_t B, int64_t L, int64_t W, int* n_chunks, int* n_wblk, int* n_blk) {
+    *n_chunks = (int)cdiv(L, Tile<IO>::T);
+    *n_wblk = (int)cdiv(W, kThreads);
+    *n_blk = (int)(B * *n_wblk);
+}
+
+template <typename IO, typename C>
+static size_t ws_lookback(int64_t B, int64_t L, int64_t W) {
+    int nc, nw, nb;
+    geometry<IO>(B, L, W, &nc, &nw, &nb);
+    const size_t lanes = (size_t)nb * kThreads;
+    Carver cv(nullptr);
+    cv.take<int>(1);
+    cv.take<int>((size_t)nc * nb);
+    for (int i = 0; i < 3; ++i) cv.take<C>((size_t)nc * lanes);
+    return cv.off;
+}
+
+template <typename IO, typename C>
+static int carve(void* w, size_t wb, int64_t B, int64_t L, int64_t W, LookbackWS* ws, Carver* cv,
+                 cudaStream_t st) {
+    int nc, nw, nb;
+    geometry<IO>(B, L, W, &nc, &nw, &nb);
+    const size_t lanes = (size_t)nb * kThreads;
+    ws->ticket = cv->take<int>(1);
+    ws->status = cv->take<int>((size_t)nc * nb);
+    const size_t head = cv->off;
+    ws->agg_a = cv->take<C>((size_t)nc * lanes);
+    ws->agg_x = cv->take<C>((size_t)nc * lanes);
+    ws->inc_x = cv->take<C>((size_t)nc * lanes);
+    LRX_REQUIRE(w && cv->off <= wb, LRX_ERR_VALUE, "rglru workspace too small: %zu < %zu", wb, cv->off);
+    LRX_REQUIRE(cudaMemsetAsync(w, 0, head, st) == cudaSuccess, LRX_ERR_CUDA, "workspace memset failed");
+    return LRX_OK;
+}
+
+// TMA plan: lanes per CTA, ring stages, shared-memory bytes.  False when TMA
+// does not apply (row alignment, residency), so the caller falls back.
+struct TmaPlan {
+    int LW, S, n_wblk, n_blk;
+    size_t smem;
+};
+
+template <typename IO>
+static bool tma_plan(int64_t B, int64_t W, int narr, int PF, TmaPlan* p) {
+    if ((W * (int64_t)sizeof(IO)) % 16) return false;
+    const int sms = sm_count();
+    int LW = 128;
+    while (LW > 32 && B * cdiv(W, LW) < 4 * sms) LW /= 2;
+    p->LW = LW;
+    p->n_wblk = (int)cdiv(W, LW);
+    p->n_blk = (int)(B * p->n_wblk);
+    const int per_sm = (int)cdiv(p->n_blk, sms);
+    if (per_sm > 32) return false;
+    const size_t stage = (size_t)narr * PF * LW * sizeof(IO);
+    // 228 KB per SM minus the 1 KB the runtime reserves per resident CTA
+    const size_t budget = ((size_t)(228 - per_sm - 4) * 1024u) / per_sm;
+    if (budget < 256 + 2 * stage) return false;
+    int S = (int)((budget - 256) / stage);
+    if (S > 6) S = 6;
+    p->S = S;
+    p->smem = 128 * ((2 * S * 8 + 127) / 128) + (size_t)S * stage;
+    return true;
+}
+
+template <typename IO, typename C, int LW, int PF>
+static int launch_fwd_tma(const TmaPlan& pl, const CUtensorMap* m, const void* lam, const void* br, const void* bi,
+                          void* y, void* ckpt, int64_t B, int64_t L, int64_t W, cudaStream_t st) {
+    auto k = fwd_tma_kernel<IO, C, LW, PF>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem) != cudaSuccess) {
+        set_error("rglru fwd: cannot reserve %zu B of shared memory", pl.smem);
+        return LRX_ERR_CUDA;
+    }
+    k<<<pl.n_blk, LW, pl.smem, st>>>(m[0], m[1], m[2], (const C*)lam, (const C*)br, (const C*)bi, (IO*)y, (C*)ckpt,
+                                     L, W, pl.n_wblk, (int)B, pl.S);
+    return launched("lrx_rglru_fwd/tma");
+}
+
+template <typename IO, typename C, int LW, int PF>
+static int launch_bwd_tma(const TmaPlan& pl, const CUtensorMap* m, const void* lam, const void* br, const void* bi,
+                          void* gu, void* gqr, void* gqi, C* parts, int64_t B, int64_t L, int64_t W,
+                          cudaStream_t st) {
+    auto k = bwd_tma_kernel<IO, C, LW, PF>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem) != cudaSuccess) {
+        set_error("rglru bwd: cannot reserve %zu B of shared memory", pl.smem);
+        return LRX_ERR_CUDA;
+    }
+    const int64_t n = B * W;
+    k<<<pl.n_blk, LW, pl.smem, st>>>(m[0], m[1], m[2], m[3], m[4], (const C*)lam, (const C*)br, (const C*)bi,
+                                     (IO*)gu, (IO*)gqr, (IO*)gqi, parts, parts + n, parts + 2 * n, L, W, pl.n_wblk,
+                                     pl.S);
+    return launched("lrx_rglru_bwd/tma");
+}
+
+constexpr int kPfF = 4;  // forward TMA tile rows
+constexpr int kPfB = 4;  // backward TMA tile rows
+
+template <typename IO, typename C>
+static int colsums(C* parts, int64_t rows, int64_t B, int64_t W, void* gla, void* gbr, void* gbi,
+                   cudaStream_t st) {
+    const int64_t pn = rows * B * W;
+    const unsigned g = (unsigned)cdiv(W, 256);
+    colsum_kernel<C><<<g, 256, 0, st>>>(parts, (C*)gla, rows * B, W);
+    colsum_kernel<C><<<g, 256, 0, st>>>(parts + pn, (C*)gbr, rows * B, W);
+    colsum_kernel<C><<<g, 256, 0, st>>>(parts + 2 * pn, (C*)gbi, rows * B, W);
+    return launched("lrx_rglru_bwd/colsum", 3);
+}
+
+template <typename IO, typename C>
+static int fwd_t(const void* u, const void* qr, const void* qi, const void* lam, const void* br, const void* bi,
+                 void* y, void* ckpt, int64_t B, int64_t L, int64_t W, void* w, size_t wb, cudaStream_t st) {
+    const int mode = mode_env();
+    TmaPlan pl;
+    if ((mode == 0 || mode == 1) && B * L < (1ll << 31) && tma_plan<IO>(B, W, 3, kPfF, &pl)) {
+        CUtensorMap m[3];
+        const void* src[3] = {u, qr, qi};
+        bool ok = true;
+        for (int i = 0; i < 3; ++i) ok &= tma::encode_2d(&m[i], src[i], sizeof(IO), B * L, W, kPfF, pl.LW);
+        if (ok) {
+            switch (pl.LW) {
+                case 128: return launch_fwd_tma<IO, C, 128, kPfF>(pl, m, lam, br, bi, y, ckpt, B, L, W, st);
+                case 64: return launch_fwd_tma<IO, C, 64, kPfF>(pl, m, lam, br, bi, y, ckpt, B, L, W, st);
+                default: return launch_fwd_tma<IO, C, 32, kPfF>(pl, m, lam, br, bi, y, ckpt, B, L, W, st);
+            }
+        }
+        LRX_REQUIRE(mode != 1, LRX_ERR_UNSUPPORTED, "rglru: TMA descriptors unavailable");
+    }
+    int nc, nw, nb;
+    geometry<IO>(B, L, W, &nc, &nw, &nb);
+    if (mode == 2 || (mode == 0 && nb >= 4 * sm_count())) {
+        fwd_stream_kernel<IO, C, 4><<<(unsigned)nb, kThreads, 0, st>>>(
+            (const IO*)u, (const IO*)qr, (const IO*)qi, (const C*)lam, (const C*)br, (const C*)bi, (IO*)y, (C*)ckpt,
+            L, W, nw, (int)B);
+        return launched("lrx_rglru_fwd/stream");
+    }
+    LookbackWS ws;
+    Carver cv(w);
+    if (int rc = carve<IO, C>(w, wb, B, L, W, &ws, &cv, st)) return rc;
+    fwd_kernel<IO, C><<<(unsigned)((int64_t)nc * nb), kThreads, 0, st>>>(
+        (const IO*)u, (const IO*)qr, (const IO*)qi, (const C*)lam, (const C*)br, (const C*)bi, (IO*)y, (C*)ckpt,
+        L, W, nw, nb, ws);
+    return launched("lrx_rglru_fwd/lookback");
+}
+
+template <typename IO, typename C>
+static int bwd_t(const void* u, const void* qr, const void* qi, const void* lam, const void* br, const void* bi,
+                 const void* ckpt, const void* y, const void* gy, void* gu, void* gqr, void* gqi, void* gla,
+                 void* gbr, void* gbi, int64_t B, int64_t L, int64_t W, void* w, size_t wb, cudaStream_t st) {
+    const int mode = mode_env();
+    const int64_t n = B * W;
+    TmaPlan pl;
+    // y (= the state) is exact only at fp32/f64 I/O; bf16 recomputes instead
+    if (y && sizeof(IO) != 2 && (mode == 0 || mode == 1) && B * L < (1ll << 31) &&
+        tma_plan<IO>(B, W, 5, kPfB, &pl)) {
+        CUtensorMap m[5];
+        const void* src[5] = {u, qr, qi, gy, y};
+        bool ok = true;
+        for (int i = 0; i < 5; ++i) ok &= tma::encode_2d(&m[i], src[i], sizeof(IO), B * L, W, kPfB, pl.LW);
+        if (ok) {
+            Carver cv(w);
+            C* parts = cv.take<C>((size_t)3 * n);
+            LRX_REQUIRE(w && cv.off <= wb, LRX_ERR_VALUE, "rglru workspace too small");
+            int rc;
+            switch (pl.LW) {
+                case 128: rc = launch_bwd_tma<IO, C, 128, kPfB>(pl, m, lam, br, bi, gu, gqr, gqi, parts, B, L, W, st); break;
+                case 64: rc = launch_bwd_tma<IO, C, 64, kPfB>(pl, m, lam, br, bi, gu, gqr, gqi, parts, B, L, W, st); break;
+                default: rc = launch_bwd_tma<IO, C, 32, kPfB>(pl, m, lam, br, bi, gu, gqr, gqi, parts, B, L, W, st); break;
+            }
+            if (rc) return rc;
+            return colsums<IO, C>(parts, 1, B, W, gla, gbr, gbi, st);
+        }
+        LRX_REQUIRE(mode != 1, LRX_ERR_UNSUPPORTED, "rglru: TMA descriptors unavailable");
+    }
+    LRX_REQUIRE(ckpt, LRX_ERR_VALUE, "rglru bwd: this path recomputes states and needs the forward checkpoints");
+    int nc, nw, nb;
+    geometry<IO>(B, L, W, &nc, &nw, &nb);
+    LookbackWS ws;
+    Carver cv(w);
+    if (int rc = carve<IO, C>(w, wb, B, L, W, &ws, &cv, st)) return rc;
+    C* parts = cv.take<C>((size_t)3 * nc * n);
+    LRX_REQUIRE(cv.off <= wb, LRX_ERR_VALUE, "rglru workspace too small");
+    const size_t pn = (size_t)nc * n;
+    bwd_kernel<IO, C><<<(unsigned)((int64_t)nc * nb), kThreads, 0, st>>>(
+        (const IO*)u, (const IO*)qr, (const IO*)qi, (const C*)lam, (const C*)br, (const C*)bi, (const C*)ckpt,
+        (const IO*)gy, (IO*)gu, (IO*)gqr, (IO*)gqi, parts, parts + pn, parts + 2 * pn, L, W, nw, nb, nc, ws);
+    if (int rc = launched("lrx_rglru_bwd/lookback")) return rc;
+    return colsums<IO, C>(parts, nc, B, W, gla, gbr, gbi, st);
+}
+
+template <typename IO, typename C>
+static size_t bwd_ws_bytes(int64_t B, int64_t L, int64_t W) {
+    int nc, nw, nb;
+    geometry<IO>(B, L, W, &nc, &nw, &nb);
+    return ws_lookback<IO, C>(B, L, W) + align_up((size_t)3 * nc * B * W * sizeof(C));
+}
+
+}  // namespace rglru
+}  // namespace lrx
+
+using namespace lrx;
+
+extern "C" {
+
+int lrx_rglru_chunking(int io_dtype, int64_t L, int64_t* chunk_len, int64_t* n_chunks) {
+    LRX_REQUIRE(L >= 1, LRX_ERR_SHAPE, "length must be >= 1");
+    const int T = io_dtype == LRX_F64 ? rglru::Tile<double>::T : rglru::Tile<float>::T;
+    *chunk_len = T;
+    *n_chunks = cdiv(L, T);
+    return LRX_OK;
+}
+
+size_t lrx_rglru_workspace_bytes(int io_dtype, int64_t B, int64_t L, int64_t W) {
+    if (B < 1 || L < 1 || W < 1) return 256;
+    switch (io_dtype) {
+        case LRX_F32: return rglru::bwd_ws_bytes<float, float>(B, L, W);
+        case LRX_BF16: return rglru::bwd_ws_bytes<__nv_bfloat16, float>(B, L, W);
+        case LRX_F64: return rglru::bwd_ws_bytes<double, double>(B, L, W);
+    }
+    return 0;
+}
+
+int lrx_rglru_fwd(int io_dtype, const void* u, const void* qr, const void* qi, const void* lambda_param,
+                  const void* b_r, const void* b_i, void* y, void* ckpt, int64_t B, int64_t L, int64_t W,
+                  void* workspace, size_t workspace_bytes, void* stream) {
+    LRX_REQUIRE(B >= 1 && L >= 1 && W >= 1, LRX_ERR_SHAPE, "bad extents B=%lld L=%lld W=%lld", (long long)B,
+                (long long)L, (long long)W);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (io_dtype) {
+        case LRX_F32:
+            return rglru::fwd_t<float, float>(u, qr, qi, lambda_param, b_r, b_i, y, ckpt, B, L, W, workspace,
+                                              workspace_bytes, st);
+        case LRX_BF16:
+            return rglru::fwd_t<__nv_bfloat16, float>(u, qr, qi, lambda_param, b_r, b_i, y, ckpt, B, L, W,
+                                                      workspace, workspace_bytes, st);
+        case LRX_F64:
+            return rglru::fwd_t<double, double>(u, qr, qi, lambda_param, b_r, b_i, y, ckpt, B, L, W, workspace,
+                                                workspace_bytes, st);
+    }
+    set_error("rglru: unsupported io dtype %d", io_dtype);
+    return LRX_ERR_VALUE;
+}
+
+int lrx_rglru_bwd(int io_dtype, const void* u, const void* qr, const void* qi, const void* lambda_param,
+                  const void* b_r, const void* b_i, const void* ckpt, const void* y, const void* gy, void* gu_local,
+                  void* gqr, void* gqi, void* gla, void* gb_r, void* gb_i, int64_t B, int64_t L, int64_t W,
+                  void* workspace, size_t workspace_bytes, void* stream) {
+    LRX_REQUIRE(B >= 1 && L >= 1 && W >= 1, LRX_ERR_SHAPE, "bad extents");
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (io_dtype) {
+        case LRX_F32:
+            return rglru::bwd_t<float, float>(u, qr, qi, lambda_param, b_r, b_i, ckpt, y, gy, gu_local, gqr, gqi,
+                                              gla, gb_r, gb_i, B, L, W, workspace, workspace_bytes, st);
+        case LRX_BF16:
+            return rglru::bwd_t<__nv_bfloat16, float>(u, qr, qi, lambda_param, b_r, b_i, ckpt, y, gy, gu_local, gqr,
+                                                      gqi, gla, gb_r, gb_i, B, L, W, workspace, workspace_bytes, st);
+        case LRX_F64:
+            return rglru::bwd_t<double, double>(u, qr, qi, lambda_param, b_r, b_i, ckpt, y, gy, gu_local, gqr, gqi,
+                                                gla, gb_r, gb_i, B, L, W, workspace, workspace_bytes, st);
+    }
+    set_error("rglru: unsupported io dtype %d", io_dtype);
+    return LRX_ERR_VALUE;
+}
+
+}  // extern "C"

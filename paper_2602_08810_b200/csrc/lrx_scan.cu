@@ -1,0 +1,357 @@
+// Generic diagonal scan operator on time-major [L, N] arrays.
+//
+// Replaces the reference's scan operator: scan_sequential / scan_parallel
+// (pkg/src/linrec/scan.py:127-201) over the numba loops scan_const,
+// scan_var, compose_*, local_scan_*, fixup_* (_scan_kernels.py:17-128), and
+// the pullback backward_const / backward_var + _scan_pullback
+// (_scan_kernels.py:131-153, autograd.py:113-140).
+//
+// B200 design: one thread per lane (consecutive threads = consecutive lanes,
+// so every step is one coalesced 128 B+ row segment per warp), a register
+// tile of T time steps per thread, and time chunks chained across CTAs by a
+// decoupled look-back (lrx_common.cuh).  One read of a/b and one write of
+// out per element: the HBM minimum.  The reference's three passes
+// (local scan, serial stitch, fixup) collapse into this single pass.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "lrx_common.cuh"
+#include "lrx_host.h"
+
+namespace lrx {
+
+static thread_local char g_err[512];
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+constexpr int kLanes = 128;  // threads (= lanes) per CTA
+
+template <typename V> struct Tile;            // register tile length per type
+template <> struct Tile<float> { static constexpr int T = 32; };
+template <> struct Tile<double> { static constexpr int T = 16; };
+template <> struct Tile<cplx<float>> { static constexpr int T = 16; };
+template <> struct Tile<cplx<double>> { static constexpr int T = 8; };
+
+template <typename V> __device__ __forceinline__ V ld(const V* p) { return *p; }
+template <> __device__ __forceinline__ cplx<float> ld(const cplx<float>* p) {
+    float2 v = __ldcs(reinterpret_cast<const float2*>(p));
+    return {v.x, v.y};
+}
+template <> __device__ __forceinline__ cplx<double> ld(const cplx<double>* p) {
+    double2 v = __ldcs(reinterpret_cast<const double2*>(p));
+    return {v.x, v.y};
+}
+template <> __device__ __forceinline__ float ld(const float* p) { return __ldcs(p); }
+template <> __device__ __forceinline__ double ld(const double* p) { return __ldcs(p); }
+template <typename V> __device__ __forceinline__ void st(V* p, V v) { *p = v; }
+template <> __device__ __forceinline__ void st(cplx<float>* p, cplx<float> v) {
+    __stcs(reinterpret_cast<float2*>(p), make_float2(v.re, v.im));
+}
+template <> __device__ __forceinline__ void st(cplx<double>* p, cplx<double> v) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(v.re, v.im));
+}
+template <> __device__ __forceinline__ void st(float* p, float v) { __stcs(p, v); }
+template <> __device__ __forceinline__ void st(double* p, double v) { __stcs(p, v); }
+
+// ---------------------------------------------------------------- forward
+template <typename V, bool PER_STEP>
+__global__ void __launch_bounds__(kLanes) scan_fwd_kernel(const V* __restrict__ a, const V* __restrict__ b,
+                                                          const V* __restrict__ x0, V* __restrict__ out,
+                                                          int64_t L, int64_t N, int n_blk, LookbackWS ws) {
+    using Tr = Traits<V>;
+    constexpr int T = Tile<V>::T;
+    const int tile = next_tile(ws.ticket);
+    const int c = tile / n_blk, blk = tile % n_blk;
+    const int64_t lane = (int64_t)blk * kLanes + threadIdx.x;
+    const bool valid = lane < N;
+    const int64_t t0 = (int64_t)c * T;
+    const int nt = (int)min((int64_t)T, L - t0);
+
+    V av[T], bv[T];
+    const V ac = (!PER_STEP && valid) ? ld(a + lane) : Tr::one();
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        const bool ok = valid && k < nt;
+        const int64_t off = (t0 + k) * N + lane;
+        bv[k] = ok ? ld(b + off) : Tr::zero();
+        av[k] = ok ? (PER_STEP ? ld(a + off) : ac) : Tr::one();
+    }
+    V A = Tr::one(), X = Tr::zero();
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        X = av[k] * X + bv[k];
+        A = av[k] * A;
+    }
+    V* agg_a = static_cast<V*>(ws.agg_a);
+    V* agg_x = static_cast<V*>(ws.agg_x);
+    V* inc_x = static_cast<V*>(ws.inc_x);
+    const int64_t woff = (int64_t)c * N + lane;
+    int* sw = ws.status + (int64_t)c * n_blk + blk;
+    V xin;
+    if (c == 0) {
+        xin = (x0 && valid) ? ld(x0 + lane) : Tr::zero();
+    } else {
+        lb_publish<V>(sw, LB_AGG, agg_a + woff, A, agg_x + woff, X, valid);
+        xin = lb_lookback<V>(ws, c, blk, n_blk, lane, N, valid);
+    }
+    if ((c % kAnchor) == 0)
+        lb_publish<V>(sw, LB_INC, (V*)nullptr, A, inc_x + woff, A * xin + X, valid);
+    V x = xin;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        x = av[k] * x + bv[k];
+        if (valid && k < nt) st(out + (t0 + k) * N + lane, x);
+    }
+}
+
+// ---------------------------------------------------------------- backward
+// Reverse chunks in scan order s = n_chunks-1-c.  Within chunk c the carry
+// entering from the right is h = conj(a[t1]) g[t1] (t1 = first step of chunk
+// c+1); the chunk publishes h_out = conj(a[t0]) g[t0].  For chunk 0 that is
+// exactly grad_x0 = conj(a_0) g_0.
+template <typename V, bool PER_STEP>
+__global__ void __launch_bounds__(kLanes) scan_bwd_kernel(const V* __restrict__ a, const V* __restrict__ x,
+                                                          const V* __restrict__ x0, const V* __restrict__ gx,
+                                                          V* __restrict__ gb, V* __restrict__ ga,
+                                                          V* __restrict__ ga_part, V* __restrict__ gx0,
+                                                          int64_t L, int64_t N, int n_blk, int n_chunks,
+                                                          LookbackWS ws) {
+    using Tr = Traits<V>;
+    constexpr int T = Tile<V>::T;
+    const int tile = next_tile(ws.ticket);
+    const int s = tile / n_blk, blk = tile % n_blk;
+    const int c = n_chunks - 1 - s;
+    const int64_t lane = (int64_t)blk * kLanes + threadIdx.x;
+    const bool valid = lane < N;
+    const int64_t t0 = (int64_t)c * T;
+    const int nt = (int)min((int64_t)T, L - t0);
+
+    V acv[T], gxv[T];
+    const V acst = (!PER_STEP && valid) ? Tr::cj(ld(a + lane)) : Tr::one();
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        const bool ok = valid && k < nt;
+        const int64_t off = (t0 + k) * N + lane;
+        gxv[k] = ok ? ld(gx + off) : Tr::zero();
+        acv[k] = ok ? (PER_STEP ? Tr::cj(ld(a + off)) : acst) : Tr::one();
+    }
+    // local aggregate from h_in = 0
+    V A = Tr::one(), H = Tr::zero();
+#pragma unroll
+    for (int k = T - 1; k >= 0; --k) {
+        const V g = gxv[k] + H;
+        H = acv[k] * g;
+        A = acv[k] * A;
+    }
+    V* agg_a = static_cast<V*>(ws.agg_a);
+    V* agg_x = static_cast<V*>(ws.agg_x);
+    V* inc_x = static_cast<V*>(ws.inc_x);
+    const int64_t woff = (int64_t)s * N + lane;
+    int* sw = ws.status + (int64_t)s * n_blk + blk;
+    V hin;
+    if (s == 0) {
+        hin = Tr::zero();
+    } else {
+        lb_publish<V>(sw, LB_AGG, agg_a + woff, A, agg_x + woff, H, valid);
+        hin = lb_lookback<V>(ws, s, blk, n_blk, lane, N, valid);
+    }
+    if ((s % kAnchor) == 0)
+        lb_publish<V>(sw, LB_INC, (V*)nullptr, A, inc_x + woff, A * hin + H, valid);
+
+    V h = hin, gsum = Tr::zero();
+#pragma unroll
+    for (int k = T - 1; k >= 0; --k) {
+        if (valid && k < nt) {
+            const V g = gxv[k] + h;
+            h = acv[k] * g;
+            const int64_t off = (t0 + k) * N + lane;
+            st(gb + off, g);
+            if (ga || ga_part) {
+                const int64_t tk = t0 + k;
+                V xp = (tk == 0) ? (x0 ? ld(x0 + lane) : Tr::zero()) : ld(x + off - N);
+                const V contrib = g * Tr::cj(xp);
+                if constexpr (PER_STEP) st(ga + off, contrib);
+                else gsum = gsum + contrib;
+            }
+        }
+    }
+    if (!PER_STEP && ga_part && valid) st(ga_part + (int64_t)c * N + lane, gsum);
+    if (c == 0 && gx0 && valid) st(gx0 + lane, h);
+}
+
+// ---------------------------------------------------------------- reduce
+template <typename V>
+__global__ void reduce_rows_kernel(const V* __restrict__ in, V* __restrict__ out, int64_t R, int64_t N) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    V acc = Traits<V>::zero();
+    for (int64_t r = 0; r < R; ++r) acc = acc + in[r * N + j];
+    out[j] = acc;
+}
+
+// ---------------------------------------------------------------- host side
+template <typename V>
+static void chunking(int64_t L, int64_t N, int* n_chunks, int* n_blk) {
+    *n_chunks = (int)cdiv(L, Tile<V>::T);
+    *n_blk = (int)cdiv(N, kLanes);
+}
+
+template <typename V>
+static size_t ws_bytes(int64_t L, int64_t N, bool bwd) {
+    int nc, nb;
+    chunking<V>(L, N, &nc, &nb);
+    Carver cv(nullptr);
+    cv.take<int>(1);
+    cv.take<int>((size_t)nc * nb);
+    cv.take<V>((size_t)nc * N);
+    cv.take<V>((size_t)nc * N);
+    cv.take<V>((size_t)nc * N);
+    if (bwd) cv.take<V>((size_t)nc * N);
+    return cv.off;
+}
+
+template <typename V>
+static int carve(void* w, size_t wb, int64_t L, int64_t N, bool bwd, LookbackWS* ws, V** part,
+                 cudaStream_t st) {
+    int nc, nb;
+    chunking<V>(L, N, &nc, &nb);
+    const size_t need = ws_bytes<V>(L, N, bwd);
+    LRX_REQUIRE(w != nullptr && wb >= need, LRX_ERR_VALUE, "workspace too small: %zu < %zu", wb, need);
+    Carver cv(w);
+    ws->ticket = cv.take<int>(1);
+    ws->status = cv.take<int>((size_t)nc * nb);
+    const size_t head = cv.off;
+    ws->agg_a = cv.take<V>((size_t)nc * N);
+    ws->agg_x = cv.take<V>((size_t)nc * N);
+    ws->inc_x = cv.take<V>((size_t)nc * N);
+    if (part) *part = bwd ? cv.take<V>((size_t)nc * N) : nullptr;
+    if (cudaMemsetAsync(w, 0, head, st) != cudaSuccess) {
+        set_error("workspace memset failed");
+        return LRX_ERR_CUDA;
+    }
+    return LRX_OK;
+}
+
+template <typename V>
+static int fwd_t(int per_step, const void* a, const void* b, const void* x0, void* out, int64_t L, int64_t N,
+                 void* w, size_t wb, cudaStream_t st) {
+    int nc, nb;
+    chunking<V>(L, N, &nc, &nb);
+    LookbackWS ws;
+    int rc = carve<V>(w, wb, L, N, false, &ws, nullptr, st);
+    if (rc) return rc;
+    const dim3 grid((unsigned)((int64_t)nc * nb));
+    if (per_step)
+        scan_fwd_kernel<V, true><<<grid, kLanes, 0, st>>>((const V*)a, (const V*)b, (const V*)x0, (V*)out, L, N,
+                                                          nb, ws);
+    else
+        scan_fwd_kernel<V, false><<<grid, kLanes, 0, st>>>((const V*)a, (const V*)b, (const V*)x0, (V*)out, L, N,
+                                                           nb, ws);
+    return launched("lrx_scan_fwd");
+}
+
+template <typename V>
+static int bwd_t(int per_step, const void* a, const void* x, const void* x0, const void* gx, void* gb, void* ga,
+                 void* gx0, int64_t L, int64_t N, void* w, size_t wb, cudaStream_t st) {
+    int nc, nb;
+    chunking<V>(L, N, &nc, &nb);
+    LookbackWS ws;
+    V* part = nullptr;
+    int rc = carve<V>(w, wb, L, N, true, &ws, &part, st);
+    if (rc) return rc;
+    const dim3 grid((unsigned)((int64_t)nc * nb));
+    if (per_step) {
+        scan_bwd_kernel<V, true><<<grid, kLanes, 0, st>>>((const V*)a, (const V*)x, (const V*)x0, (const V*)gx,
+                                                          (V*)gb, (V*)ga, nullptr, (V*)gx0, L, N, nb, nc, ws);
+        return launched("lrx_scan_bwd");
+    }
+    scan_bwd_kernel<V, false><<<grid, kLanes, 0, st>>>((const V*)a, (const V*)x, (const V*)x0, (const V*)gx,
+                                                       (V*)gb, nullptr, ga ? part : nullptr, (V*)gx0, L, N, nb,
+                                                       nc, ws);
+    rc = launched("lrx_scan_bwd");
+    if (rc || !ga) return rc;
+    reduce_rows_kernel<V><<<(unsigned)cdiv(N, 256), 256, 0, st>>>(part, (V*)ga, nc, N);
+    return launched("lrx_scan_bwd/reduce");
+}
+
+}  // namespace lrx
+
+using namespace lrx;
+
+#define LRX_DISPATCH(dt, FN, ...)                                         \
+    switch (dt) {                                                         \
+        case LRX_F32: return FN<float>(__VA_ARGS__);                      \
+        case LRX_F64: return FN<double>(__VA_ARGS__);                     \
+        case LRX_C64: return FN<cplx<float>>(__VA_ARGS__);                \
+        case LRX_C128: return FN<cplx<double>>(__VA_ARGS__);              \
+        default: set_error("unsupported dtype %d", dt); return LRX_ERR_VALUE; \
+    }
+
+#define LRX_DISPATCH_SZ(dt, FN, ...)                                      \
+    switch (dt) {                                                         \
+        case LRX_F32: return FN<float>(__VA_ARGS__);                      \
+        case LRX_F64: return FN<double>(__VA_ARGS__);                     \
+        case LRX_C64: return FN<cplx<float>>(__VA_ARGS__);                \
+        case LRX_C128: return FN<cplx<double>>(__VA_ARGS__);              \
+        default: return 0;                                                \
+    }
+
+extern "C" {
+
+const char* lrx_last_error(void) { return g_err; }
+int lrx_version(void) { return 1; }
+int64_t lrx_launch_count(void) { return g_launches.load(); }
+
+size_t lrx_scan_workspace_bytes(int dtype, int64_t L, int64_t N) {
+    if (L < 1 || N < 1) return 256;
+    LRX_DISPATCH_SZ(dtype, ws_bytes, L, N, false)
+}
+
+size_t lrx_scan_bwd_workspace_bytes(int dtype, int64_t L, int64_t N) {
+    if (L < 1 || N < 1) return 256;
+    LRX_DISPATCH_SZ(dtype, ws_bytes, L, N, true)
+}
+
+int lrx_scan_fwd(int dtype, int a_per_step, const void* a, const void* b, const void* x0, void* out, int64_t L,
+                 int64_t N, void* workspace, size_t workspace_bytes, void* stream) {
+    LRX_REQUIRE(L >= 1, LRX_ERR_SHAPE, "length must be >= 1, got %lld", (long long)L);
+    LRX_REQUIRE(N >= 1, LRX_ERR_SHAPE, "lane count must be >= 1, got %lld", (long long)N);
+    LRX_REQUIRE(a && b && out, LRX_ERR_VALUE, "null array argument");
+    LRX_DISPATCH(dtype, fwd_t, a_per_step, a, b, x0, out, L, N, workspace, workspace_bytes, (cudaStream_t)stream)
+}
+
+int lrx_scan_bwd(int dtype, int a_per_step, const void* a, const void* x, const void* x0, const void* gx, void* gb,
+                 void* ga, void* gx0, int64_t L, int64_t N, void* workspace, size_t workspace_bytes, void* stream) {
+    LRX_REQUIRE(L >= 1 && N >= 1, LRX_ERR_SHAPE, "bad extents L=%lld N=%lld", (long long)L, (long long)N);
+    LRX_REQUIRE(a && gx && gb, LRX_ERR_VALUE, "null array argument");
+    LRX_REQUIRE(!ga || x, LRX_ERR_VALUE, "grad_a needs the forward states x");
+    LRX_DISPATCH(dtype, bwd_t, a_per_step, a, x, x0, gx, gb, ga, gx0, L, N, workspace, workspace_bytes,
+                 (cudaStream_t)stream)
+}
+
+int lrx_reduce_rows(int dtype, const void* in, void* out, int64_t R, int64_t N, void* stream) {
+    LRX_REQUIRE(R >= 1 && N >= 1, LRX_ERR_SHAPE, "bad extents R=%lld N=%lld", (long long)R, (long long)N);
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned g = (unsigned)cdiv(N, 256);
+    switch (dtype) {
+        case LRX_F32: reduce_rows_kernel<float><<<g, 256, 0, st>>>((const float*)in, (float*)out, R, N); break;
+        case LRX_F64: reduce_rows_kernel<double><<<g, 256, 0, st>>>((const double*)in, (double*)out, R, N); break;
+        case LRX_C64:
+            reduce_rows_kernel<cplx<float>><<<g, 256, 0, st>>>((const cplx<float>*)in, (cplx<float>*)out, R, N);
+            break;
+        case LRX_C128:
+            reduce_rows_kernel<cplx<double>><<<g, 256, 0, st>>>((const cplx<double>*)in, (cplx<double>*)out, R, N);
+            break;
+        default: set_error("unsupported dtype %d", dtype); return LRX_ERR_VALUE;
+    }
+    return launched("lrx_reduce_rows");
+}
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// Host-side tensor-map encoding through the driver entry point (no -lcuda).
+#include <cudaTypedefs.h>
+#include <mutex>
+
+#include "lrx_tma.cuh"
+
+namespace lrx {
+namespace tma {
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+bool encode_2d(CUtensorMap* map, const void* base, int esize, uint64_t rows, uint64_t cols, uint32_t box_rows,
+               uint32_t box_cols) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((cols * esize) & 15) || ((box_cols * esize) & 15)) return false;
+    CUtensorMapDataType dt;
+    switch (esize) {
+        case 2: dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16; break;
+        case 4: dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32; break;
+        case 8: dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT64; break;
+        default: return false;
+    }
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * (cuuint64_t)esize};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace tma
+}  // namespace lrx

@@ -1,0 +1,683 @@
+"""The layer zoo, device-backed (mirrors pkg/src/linrec/layers.py).
+
+Same constructors, parameter names/shapes/initialisation (bit-identical for
+the same seed), forward signature and GradBundle layout as the reference, so
+`make_layer` / `Layer.forward` / `layer_backward` are a drop-in.  Execution:
+
+  * s6     lrx_s6_fwd / lrx_s6_bwd       fused selective scan (discretisation,
+                                          softplus, readout, D skip) around the
+                                          layer's projection GEMMs (cuBLAS)
+  * rglru  lrx_rglru_fwd / lrx_rglru_bwd fused gated scan around the gate GEMMs
+  * s5/lru lrx_mimo_fwd / lrx_mimo_bwd   complex scan fused with the input
+                                          scaling and coefficient reductions,
+                                          between the dense B/C projections
+                                          (real GEMMs on interleaved complex)
+  * s4d and the event-stream (per-step delta) paths of s4d/s5 run on the
+    generic operator lrx_scan_fwd / lrx_scan_bwd.
+
+`mode` ("sequential" / "parallel") and `workers` are accepted and validated;
+both modes run the same chunk-parallel kernels and agree bitwise.  Inputs may
+be numpy arrays (results come back as numpy) or CUDA tensors.  dtype "f32" /
+"f64" as in the reference; "bf16" (s6, rglru) = bf16 activations, fp32
+parameters and fp32 accumulation.
+"""
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import ops
+from .autograd import Tape, layer_backward, pullback, scheme_partials
+from .discretize import scheme_factors
+from .numerics import Rng, ShapeError, real_dtype, sigmoid
+from .scan import run_fwd
+
+__all__ = ["LAYER_KINDS", "SCHEMES_BY_KIND", "UnknownLayer", "LayerConfig", "LayerStepState", "LinearRecurrence",
+           "S4D", "S5", "LRU", "S6", "RGLRU", "make_layer", "init_layer", "lti_forward", "ltv_forward",
+           "layer_step"]
+
+LAYER_KINDS = ("s4d", "s5", "lru", "s6", "rglru")
+SCHEMES_BY_KIND = {"s4d": ("zoh", "bilinear", "dirac"), "s5": ("zoh", "bilinear", "dirac"),
+                   "lru": (), "s6": (), "rglru": ()}
+STREAM_BLOCK = 512  # layers.py:77 (kept for API parity; the device path is not block-streamed)
+
+
+class UnknownLayer(ValueError):
+    """Requested layer kind is not in the registry."""
+
+
+@dataclass
+class LayerConfig:
+    d_model: int
+    d_state: int | None = None
+    discretization: str | None = None
+    asynchronous: bool = False
+    dtype: str = "f64"
+    extras: dict = field(default_factory=dict)
+
+
+class LayerStepState:
+    """Carry returned by forward(return_state=True): the state after the last
+    step (x, on the device) and the step count k."""
+
+    def __init__(self, kind: str, batch: int):
+        self.kind = kind
+        self.batch = batch
+        self.k = 0
+        self.x = None
+
+
+def _device(device=None):
+    if device is not None:
+        return torch.device(device)
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _pair(rng, shape, std, dt):
+    g = rng.split(2)
+    return np.asarray(g[0].normal(shape) * std, dt), np.asarray(g[1].normal(shape) * std, dt)
+
+
+def _log_delta_init(rng, shape, dt):
+    return np.asarray(rng.uniform(np.log(1e-3), np.log(1e-1), shape), dt)
+
+
+def _mm(a, b):
+    """Projection GEMM (cuBLAS).  bf16 activations multiply bf16-cast weights
+    with fp32 accumulation AND fp32 output, so the scan sees unrounded
+    projections (layers.py:1020-1027 computes them at full precision)."""
+    if a.dtype == torch.bfloat16:
+        return torch.mm(a, b.to(torch.bfloat16), out_dtype=torch.float32)
+    return a @ b
+
+
+class LinearRecurrence:
+    """Validation, mode dispatch and host/device plumbing shared by all kinds."""
+
+    kind = ""
+    lti = True
+    continuous = True
+    bf16_ok = False
+
+    def __init__(self, d_model, d_state, discretization, asynchronous, dtype, device=None):
+        if d_model < 1 or d_state < 1:
+            raise ValueError(f"extents must be positive, got d_model={d_model}, d_state={d_state}")
+        self.d_model = int(d_model)
+        self.d_state = int(d_state)
+        self.asynchronous = bool(asynchronous)
+        if dtype == "bf16" and not self.bf16_ok:
+            raise ValueError(f"{self.kind} supports dtype 'f32' or 'f64'; 'bf16' I/O is s6/rglru only")
+        if dtype not in ("f32", "f64", "bf16"):
+            real_dtype(dtype)  # raises the reference's ValueError for unknown specs
+            dtype = "f32" if real_dtype(dtype) == np.dtype(np.float32) else "f64"
+        self.dtype = dtype
+        self.rdt = real_dtype(dtype)                         # numpy parameter dtype
+        self.tdt = torch.float64 if dtype == "f64" else torch.float32
+        self.tcdt = torch.complex128 if dtype == "f64" else torch.complex64
+        self.io_dtype = torch.bfloat16 if dtype == "bf16" else self.tdt
+        self.cdt = np.dtype(np.complex128) if dtype == "f64" else np.dtype(np.complex64)
+        self.device = _device(device)
+        # fail loudly now if the kernels cannot run; device="cpu" builds the
+        # parameters only (inspection / checkpoint tooling) and cannot forward
+        _lib.load(require_gpu=self.device.type == "cuda")
+        if self.continuous:
+            if discretization is None:
+                discretization = "dirac" if self.asynchronous else "zoh"
+            if discretization not in SCHEMES_BY_KIND[self.kind]:
+                raise ValueError(f"{self.kind} supports discretizations {SCHEMES_BY_KIND[self.kind]}, "
+                                 f"got {discretization!r}")
+        elif discretization is not None:
+            warnings.warn(f"{self.kind} is parameterized directly in discrete time; "
+                          f"discretization={discretization!r} is ignored")
+            discretization = None
+        self.discretization = discretization
+
+    # -- parameters --------------------------------------------------------
+    def _p(self, arr):
+        return torch.as_tensor(np.ascontiguousarray(arr)).to(self.device, self.tdt)
+
+    def parameters(self):
+        raise NotImplementedError
+
+    # -- public API ----------------------------------------------------------
+    def forward(self, u, mode="sequential", *, workers=1, deltas=None, tape=False, return_state=False):
+        """Batched forward over u [batch, length, d_model] (layers.py:218-249)."""
+        if self.device.type != "cuda":
+            raise RuntimeError(f"{self.kind} layer lives on {self.device}; the scan runs on CUDA only "
+                               "(no CPU fallback)")
+        u, host = self._check_u(u)
+        if mode not in ("sequential", "parallel"):
+            raise ValueError(f"mode must be 'sequential' or 'parallel', got {mode!r}")
+        if workers < 1:
+            raise ValueError(f"workers must be >= 1, got {workers}")
+        B, L, _ = u.shape
+        deltas = self._check_deltas(deltas, B, L)
+        y, saved, xf = self._forward(u, deltas, tape or return_state)
+        out_y = y.cpu().numpy() if host else y
+        if not (tape or return_state):
+            return out_y
+        out = [out_y]
+        if tape:
+            saved["host"] = host
+            out.append(Tape(self.kind, **saved))
+        if return_state:
+            st = self.init_state(B)
+            st.x = xf
+            st.k = L
+            out.append(st)
+        return tuple(out)
+
+    def backward(self, tape, grad_y):
+        return layer_backward(self, tape, grad_y)
+
+    def init_state(self, batch: int = 1) -> LayerStepState:
+        return LayerStepState(self.kind, batch)
+
+    def step(self, state, u_k, delta_k=None):
+        raise NotImplementedError(
+            "single-step decode is outside the device scan hot path (SURVEY section 8(f), rank 3); "
+            "use forward() over the sequence")
+
+    # -- plumbing --------------------------------------------------------------
+    def _check_u(self, u):
+        host = not isinstance(u, torch.Tensor)
+        shape = tuple(np.shape(u)) if host else tuple(u.shape)
+        if len(shape) != 3 or shape[2] != self.d_model:
+            raise ShapeError(f"u must be [batch, length, d_model={self.d_model}], got shape {shape}")
+        if shape[1] < 1:
+            raise ShapeError("length must be >= 1")
+        if host:
+            ut = torch.as_tensor(np.ascontiguousarray(np.asarray(u, dtype=self.rdt)))
+            ut = ut.to(self.device, non_blocking=False)
+        else:
+            ut = u.to(self.device)
+        return ut.to(self.io_dtype).contiguous(), host
+
+    def _check_deltas(self, deltas, B, L):
+        if deltas is None:
+            return None
+        if not (self.lti and self.continuous):
+            raise ValueError(f"per-step deltas apply to continuous-time LTI layers only, not {self.kind}")
+        d = deltas if isinstance(deltas, torch.Tensor) else torch.as_tensor(np.asarray(deltas, dtype=self.rdt))
+        d = d.to(self.device, self.tdt)
+        if d.ndim == 1:
+            d = d[None, :].expand(B, L) if d.shape[0] == L else d
+        if tuple(d.shape) != (B, L):
+            raise ShapeError(f"deltas must be [length] or [batch, length], got {tuple(np.shape(deltas))}")
+        if bool(torch.any(d < 0)):
+            raise ValueError("deltas must be non-negative")
+        return d.contiguous()
+
+    def _gy(self, gy, shape):
+        g = gy if isinstance(gy, torch.Tensor) else torch.as_tensor(np.asarray(gy))
+        g = g.to(self.device, self.io_dtype).contiguous()
+        if tuple(g.shape) != tuple(shape):
+            raise ShapeError(f"grad_y shape {tuple(g.shape)} does not match output {tuple(shape)}")
+        return g
+
+    @staticmethod
+    def _out(grads, gu, host):
+        if not host:
+            return grads, gu
+        return ({k: v.detach().cpu().numpy() for k, v in grads.items()}, gu.detach().cpu().numpy())
+
+    def _w(self, t):
+        """Weight in the activation dtype for the projection GEMMs."""
+        return t.to(self.io_dtype) if self.io_dtype != t.dtype else t
+
+
+# ---------------------------------------------------------------------------
+# generic-operator helpers (s4d, async s4d/s5)
+
+def _tm(x):
+    """[B, L, ...] -> contiguous time-major [L, B*...]."""
+    L = x.shape[1]
+    return x.transpose(0, 1).contiguous().reshape(L, -1)
+
+
+class S4D(LinearRecurrence):
+    """Per-channel SISO complex diagonal SSM (layers.py:352-613)."""
+
+    kind = "s4d"
+    lti = True
+    continuous = True
+
+    def __init__(self, d_model, d_state=None, discretization=None, *, asynchronous=False, dtype="f64", rng=None,
+                 seed=0, device=None):
+        super().__init__(d_model, 64 if d_state is None else d_state, discretization, asynchronous, dtype, device)
+        rng = rng if rng is not None else Rng(seed)
+        r_b, r_c, r_d = rng.split(3)
+        m, n, dt = self.d_model, self.d_state, self.rdt
+        self.lambda_re_log = self._p(np.full((m, n), np.log(0.5), dt))
+        self.lambda_im = self._p(np.broadcast_to(np.pi * np.arange(n, dtype=dt), (m, n)))
+        br, bi = _pair(r_b, (m, n), 1.0, dt)
+        cr, ci = _pair(r_c, (m, n), 1.0 / np.sqrt(n), dt)
+        self.b_re, self.b_im, self.c_re, self.c_im = map(self._p, (br, bi, cr, ci))
+        self.d = self._p(np.ones(m, dt))
+        self.log_delta = self._p(_log_delta_init(r_d, m, dt))
+
+    def parameters(self):
+        return {"lambda_re_log": self.lambda_re_log, "lambda_im": self.lambda_im, "b.re": self.b_re,
+                "b.im": self.b_im, "c.re": self.c_re, "c.im": self.c_im, "d": self.d, "log_delta": self.log_delta}
+
+    def _lam(self):
+        return torch.complex(-torch.exp(self.lambda_re_log), self.lambda_im)
+
+    def _coeffs(self, deltas):
+        """Coefficients in f64 (parameter-sized; see S5._abar_scale)."""
+        lam = torch.complex(-torch.exp(self.lambda_re_log.double()), self.lambda_im.double())
+        delta = torch.exp(self.log_delta.double())
+        b = torch.complex(self.b_re.double(), self.b_im.double())
+        if deltas is None:
+            abar, scale = scheme_factors(self.discretization, lam, delta[:, None])
+        else:
+            deff = deltas.double()[:, :, None] * delta                       # [B,L,m]
+            abar, scale = scheme_factors(self.discretization, lam, deff[..., None])
+        return lam, delta, b, abar, scale
+
+    def _forward(self, u, deltas, keep):
+        B, L, m = u.shape
+        n = self.d_state
+        lam, delta, b, abar, scale = self._coeffs(deltas)
+        w = (scale * b).to(self.tcdt) * u[..., None]                          # [B,L,m,n]
+        abar = abar.to(self.tcdt)
+        if deltas is None:
+            a2, per = abar.reshape(-1).repeat(B), False
+        else:
+            a2, per = _tm(abar), True
+        x2 = run_fwd(a2.contiguous(), per, _tm(w), None)                     # [L, B*m*n]
+        xt = x2.reshape(L, B, m, n)
+        c = torch.complex(self.c_re, self.c_im)
+        y = torch.einsum("lbhn,hn->blh", xt, c).real + self.d * u
+        saved = {"u": u, "x2": x2, "deltas": deltas} if keep else {}
+        return y.contiguous(), saved, xt[-1]
+
+    def _backward(self, s, gy):
+        u, x2, deltas, host = s["u"], s["x2"], s["deltas"], s["host"]
+        B, L, m = u.shape
+        n = self.d_state
+        gy = self._gy(gy, u.shape)
+        lam, delta, b, abar, scale = self._coeffs(deltas)
+        cd = self.tcdt
+        c = torch.complex(self.c_re, self.c_im)
+        xt = x2.reshape(L, B, m, n)
+        gd = (gy * u).sum((0, 1))
+        gu = gy * self.d
+        gyt = gy.transpose(0, 1)
+        gc = torch.einsum("lbh,lbhn->hn", gyt.to(cd), xt.conj())
+        gxt = gyt[..., None] * c.conj()
+        per = deltas is not None
+        a2 = _tm(abar.to(cd)) if per else abar.to(cd).reshape(-1).repeat(B)
+        g2, ga, _ = pullback(a2.contiguous(), per, x2, None, gxt.reshape(L, -1).contiguous())
+        gw = g2.reshape(L, B, m, n)
+        c128 = torch.complex128
+        if not per:
+            gabar = ga.reshape(B, m, n).sum(0).to(c128)
+            gpsi = torch.einsum("lbhn,blh->hn", gw, u.to(cd)).to(c128)
+            gu = gu + torch.einsum("lbhn,hn->blh", gw, (scale * b).conj().to(cd)).real
+            gscale = b.conj() * gpsi
+            gb = scale.conj() * gpsi
+            dal, dad, dsl, dsd = scheme_partials(self.discretization, lam, delta[:, None], abar, scale)
+            glam = dal.conj() * gabar + dsl.conj() * gscale
+            gdel = ((dad.conj() * gabar).real + (dsd.conj() * gscale).real).sum(-1)
+            glog_delta = gdel * delta
+        else:
+            ga_k = ga.reshape(L, B, m, n).transpose(0, 1).to(c128)
+            gw_b = gw.transpose(0, 1)
+            gpsi_k = (gw_b * u[..., None]).to(c128)
+            gu = gu + torch.einsum("blhn,blhn->blh", gw_b, (scale * b).conj().to(cd)).real
+            gscale_k = b.conj() * gpsi_k
+            gb = (scale.conj() * gpsi_k).sum((0, 1))
+            deff = deltas.double()[:, :, None] * delta
+            dal, dad, dsl, dsd = scheme_partials(self.discretization, lam, deff[..., None], abar, scale)
+            glam = (dal.conj() * ga_k + dsl.conj() * gscale_k).sum((0, 1))
+            gdeff = ((dad.conj() * ga_k).real + (dsd.conj() * gscale_k).real).sum(-1)
+            glog_delta = torch.einsum("blh,bl->h", gdeff, deltas.double()) * delta
+        t = self.tdt
+        grads = {"lambda_re_log": (-torch.exp(self.lambda_re_log.double()) * glam.real).to(t),
+                 "lambda_im": glam.imag.to(t).contiguous(),
+                 "b.re": gb.real.to(t).contiguous(), "b.im": gb.imag.to(t).contiguous(),
+                 "c.re": gc.real.contiguous(), "c.im": gc.imag.contiguous(), "d": gd,
+                 "log_delta": glog_delta.to(t)}
+        return self._out(grads, gu, host)
+
+
+# ---------------------------------------------------------------------------
+# MIMO: S5 / LRU
+
+
+class _MIMOBase(LinearRecurrence):
+    """x [B, L, P] complex between bu = B u and y = OUT Re(C x) + D u
+    (layers.py:616-704).  Complex projections run as real GEMMs on the
+    interleaved (re, im) layout."""
+
+    OUT_SCALE = 1.0
+
+    @property
+    def _P(self):
+        raise NotImplementedError
+
+    def _wb(self):
+        """[m, 2P] real: u @ Wb = interleaved B u."""
+        return torch.stack((self.B_re.T, self.B_im.T), dim=-1).reshape(self.d_model, 2 * self._P).contiguous()
+
+    def _wc(self):
+        """[2P, m] real: x2 @ Wc = Re(C x)."""
+        return torch.stack((self.C_re.T, -self.C_im.T), dim=1).reshape(2 * self._P, self.d_model).contiguous()
+
+    def _abar_scale(self, deltas):
+        """(abar, scale) in the compute dtype plus f64 context for the grads."""
+        raise NotImplementedError
+
+    def _forward(self, u, deltas, keep):
+        B, L, m = u.shape
+        P = self._P
+        u2 = u.reshape(B * L, m)
+        bu = torch.view_as_complex((u2 @ self._wb()).reshape(B, L, P, 2))   # [B,L,P]
+        abar, scale, extra = self._abar_scale(deltas)
+        if deltas is None:
+            x = ops.mimo_scan_fwd(abar, scale, bu)
+        else:
+            x2 = run_fwd(_tm(abar), True, _tm(scale * bu), None)
+            x = x2.reshape(L, B, P).transpose(0, 1).contiguous()
+        y = torch.addmm((self.D * u).reshape(B * L, m), torch.view_as_real(x).reshape(B * L, 2 * P), self._wc(),
+                        alpha=self.OUT_SCALE).reshape(B, L, m)
+        saved = {"u": u, "x": x, "bu": bu, "deltas": deltas} if keep else {}
+        return y, saved, x[:, -1]
+
+    def _scan_backward(self, x, bu, gx, abar, scale, deltas):
+        """(gbu [B,L,P], gabar or ga_k, gscale or gscale_k)."""
+        B, L, P = x.shape
+        if deltas is None:
+            return ops.mimo_scan_bwd(abar, scale, bu, x, gx)
+        g2, ga, _ = pullback(_tm(abar), True, _tm(x), None, _tm(gx))
+        gv = g2.reshape(L, B, P).transpose(0, 1)
+        ga_k = ga.reshape(L, B, P).transpose(0, 1)
+        return scale.conj() * gv, ga_k, bu.conj() * gv
+
+    def _backward(self, s, gy):
+        u, x, bu, deltas, host = s["u"], s["x"], s["bu"], s["deltas"], s["host"]
+        B, L, m = u.shape
+        P = self._P
+        gy = self._gy(gy, u.shape)
+        gy2, u2 = gy.reshape(B * L, m), u.reshape(B * L, m)
+        x2 = torch.view_as_real(x).reshape(B * L, 2 * P)
+        osc = self.OUT_SCALE
+        gD = (gy * u).sum((0, 1))
+        R = gy2.T @ x2                                                      # [m, 2P]
+        gC_re, gC_im = osc * R[:, 0::2], -osc * R[:, 1::2]
+        wg = torch.stack((self.C_re, -self.C_im), dim=-1).reshape(m, 2 * P)
+        gx = torch.view_as_complex((osc * (gy2 @ wg)).reshape(B, L, P, 2)).contiguous()
+        abar, scale, extra = self._abar_scale(deltas)
+        gbu, ga, gsc = self._scan_backward(x, bu, gx, abar, scale, deltas)
+        gbu2 = torch.view_as_real(gbu.contiguous()).reshape(B * L, 2 * P)
+        R2 = gbu2.T @ u2                                                    # [2P, m]
+        gu = gy * self.D + (gbu2 @ self._wb().T).reshape(B, L, m)
+        grads = {k: v.to(self.tdt) for k, v in self._coef_grads(ga, gsc, extra, deltas).items()}
+        grads.update({"B.re": R2[0::2].contiguous(), "B.im": R2[1::2].contiguous(),
+                      "C.re": gC_re.contiguous(), "C.im": gC_im.contiguous(), "D": gD})
+        return self._out({k: grads[k] for k in self.parameters()}, gu, host)
+
+
+class S5(_MIMOBase):
+    """MIMO SSM, conjugate-pair storage, y = 2 Re(C x) + D u (layers.py:786-895)."""
+
+    kind = "s5"
+    lti = True
+    continuous = True
+    OUT_SCALE = 2.0
+
+    def __init__(self, d_model, d_state=None, discretization=None, *, asynchronous=False, dtype="f64", rng=None,
+                 seed=0, device=None):
+        d_state = 64 if d_state is None else d_state
+        if d_state % 2:
+            raise ValueError(f"s5 stores conjugate pairs and needs even d_state, got {d_state}")
+        super().__init__(d_model, d_state, discretization, asynchronous, dtype, device)
+        rng = rng if rng is not None else Rng(seed)
+        r_b, r_c, r_d = rng.split(3)
+        m, P, dt = self.d_model, d_state // 2, self.rdt
+        self.lambda_re_log = self._p(np.full((P,), np.log(0.5), dt))
+        self.lambda_im = self._p(np.pi * np.arange(P, dtype=dt))
+        Br, Bi = _pair(r_b, (P, m), 1.0 / np.sqrt(m), dt)
+        Cr, Ci = _pair(r_c, (m, P), 1.0 / np.sqrt(P), dt)
+        self.B_re, self.B_im, self.C_re, self.C_im = map(self._p, (Br, Bi, Cr, Ci))
+        self.D = self._p(np.ones(m, dt))
+        self.log_delta = self._p(_log_delta_init(r_d, P, dt))
+
+    @property
+    def _P(self):
+        return self.d_state // 2
+
+    def parameters(self):
+        return {"lambda_re_log": self.lambda_re_log, "lambda_im": self.lambda_im, "B.re": self.B_re,
+                "B.im": self.B_im, "C.re": self.C_re, "C.im": self.C_im, "D": self.D, "log_delta": self.log_delta}
+
+    def _abar_scale(self, deltas):
+        # parameter-sized discretisation in f64 (the f32 ZOH partial
+        # (delta abar lam - (abar - 1)) / lam^2 cancels catastrophically)
+        lam = torch.complex(-torch.exp(self.lambda_re_log.double()), self.lambda_im.double())
+        delta = torch.exp(self.log_delta.double())
+        d_arg = delta if deltas is None else deltas.double()[:, :, None] * delta
+        abar, scale = scheme_factors(self.discretization, lam, d_arg)
+        return abar.to(self.tcdt), scale.to(self.tcdt), {"lam": lam, "delta": delta, "d_arg": d_arg,
+                                                         "abar": abar, "scale": scale}
+
+    def _coef_grads(self, ga, gsc, extra, deltas):
+        lam, delta, d_arg = extra["lam"], extra["delta"], extra["d_arg"]
+        ga, gsc = ga.to(torch.complex128), gsc.to(torch.complex128)
+        dal, dad, dsl, dsd = scheme_partials(self.discretization, lam, d_arg, extra["abar"], extra["scale"])
+        if deltas is None:
+            glam = dal.conj() * ga + dsl.conj() * gsc
+            gdel = (dad.conj() * ga).real + (dsd.conj() * gsc).real
+            glog_delta = gdel * delta
+        else:
+            glam = (dal.conj() * ga + dsl.conj() * gsc).sum((0, 1))
+            gdeff = (dad.conj() * ga).real + (dsd.conj() * gsc).real
+            glog_delta = torch.einsum("blp,bl->p", gdeff, deltas.double()) * delta
+        return {"lambda_re_log": -torch.exp(self.lambda_re_log.double()) * glam.real,
+                "lambda_im": glam.imag.contiguous(), "log_delta": glog_delta}
+
+
+class LRU(_MIMOBase):
+    """Linear recurrent unit, ring parameterisation (layers.py:898-980)."""
+
+    kind = "lru"
+    lti = True
+    continuous = False
+    OUT_SCALE = 1.0
+
+    def __init__(self, d_model, d_state=None, discretization=None, *, asynchronous=False, dtype="f64", rng=None,
+                 seed=0, r_min=0.9, r_max=0.999, max_phase=np.pi / 10, device=None):
+        super().__init__(d_model, 64 if d_state is None else d_state, discretization, asynchronous, dtype, device)
+        rng = rng if rng is not None else Rng(seed)
+        r_mag, r_ph, r_b, r_c = rng.split(4)
+        m, n, dt = self.d_model, self.d_state, self.rdt
+        mag = np.asarray(r_mag.uniform(r_min, r_max, n), dt)
+        phase = np.maximum(np.asarray(r_ph.uniform(0.0, max_phase, n), dt), 1e-9)
+        self.nu_log = self._p(np.asarray(np.log(-np.log(mag)), dt))
+        self.theta_log = self._p(np.asarray(np.log(phase), dt))
+        self.gamma_log = self._p(np.asarray(0.5 * np.log(1.0 - mag.astype(np.float64) ** 2), dt))
+        Br, Bi = _pair(r_b, (n, m), 1.0 / np.sqrt(m), dt)
+        Cr, Ci = _pair(r_c, (m, n), 1.0 / np.sqrt(n), dt)
+        self.B_re, self.B_im, self.C_re, self.C_im = map(self._p, (Br, Bi, Cr, Ci))
+        self.D = self._p(np.ones(m, dt))
+
+    @property
+    def _P(self):
+        return self.d_state
+
+    def parameters(self):
+        return {"nu_log": self.nu_log, "theta_log": self.theta_log, "gamma_log": self.gamma_log,
+                "B.re": self.B_re, "B.im": self.B_im, "C.re": self.C_re, "C.im": self.C_im, "D": self.D}
+
+    def _abar_scale(self, deltas):
+        # lambda in f64, then rounded to the layer dtype (layers.py:936-940)
+        z = torch.complex(-torch.exp(self.nu_log.double()), torch.exp(self.theta_log.double()))
+        lam64 = torch.exp(z)
+        gamma = torch.exp(self.gamma_log)
+        return lam64.to(self.tcdt), torch.complex(gamma, torch.zeros_like(gamma)), {"lam": lam64}
+
+    def _coef_grads(self, ga, gsc, extra, deltas):
+        cl = extra["lam"].conj() * ga.to(torch.complex128)
+        return {"nu_log": -torch.exp(self.nu_log.double()) * cl.real,
+                "theta_log": torch.exp(self.theta_log.double()) * cl.imag,
+                "gamma_log": torch.exp(self.gamma_log.double()) * gsc.real.double()}
+
+
+# ---------------------------------------------------------------------------
+# S6
+
+
+class S6(LinearRecurrence):
+    """Selective SISO recurrence (layers.py:983-1168)."""
+
+    kind = "s6"
+    lti = False
+    continuous = False
+    bf16_ok = True
+
+    def __init__(self, d_model, d_state=None, discretization=None, *, asynchronous=False, dtype="f64", rng=None,
+                 seed=0, d_rank=None, device=None):
+        super().__init__(d_model, 64 if d_state is None else d_state, discretization, asynchronous, dtype, device)
+        rng = rng if rng is not None else Rng(seed)
+        r_b, r_c, r_dn, r_up, r_dt = rng.split(5)
+        m, n, dt = self.d_model, self.d_state, self.rdt
+        self.d_rank = int(d_rank) if d_rank else max(1, -(-m // 16))
+        r = self.d_rank
+        self.a_log = self._p(np.broadcast_to(np.log(np.arange(1, n + 1, dtype=dt)), (m, n)))
+        self.W_B = self._p(np.asarray(r_b.normal((n, m)) / np.sqrt(m), dt))
+        self.W_C = self._p(np.asarray(r_c.normal((n, m)) / np.sqrt(m), dt))
+        self.W_delta = self._p(np.asarray(r_dn.normal((m, r)) / np.sqrt(m), dt))
+        self.W_delta_proj = self._p(np.asarray(r_up.normal((r, m)) / np.sqrt(r), dt))
+        d0 = np.exp(r_dt.uniform(np.log(1e-3), np.log(1e-1), m))
+        self.b_delta = self._p(np.asarray(np.log(np.expm1(d0)), dt))
+        self.D = self._p(np.ones(m, dt))
+
+    def parameters(self):
+        return {"a_log": self.a_log, "W_B": self.W_B, "W_C": self.W_C, "W_delta": self.W_delta,
+                "W_delta_proj": self.W_delta_proj, "b_delta": self.b_delta, "D": self.D}
+
+    def _forward(self, u, deltas, keep):
+        B, L, m = u.shape
+        n = self.d_state
+        u2 = u.reshape(B * L, m)
+        p1 = _mm(u2, self.W_delta)
+        pre = (p1 @ self.W_delta_proj).reshape(B, L, m)
+        Bk = _mm(u2, self.W_B.T).reshape(B, L, n)
+        Ck = _mm(u2, self.W_C.T).reshape(B, L, n)
+        y, ckpt = ops.s6_scan_fwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D)
+        saved = {"u": u, "p1": p1, "pre": pre, "Bk": Bk, "Ck": Ck, "ckpt": ckpt} if keep else {}
+        return y, saved, ckpt[:, -1]
+
+    def _backward(self, s, gy):
+        u, p1, pre, Bk, Ck, ckpt, host = (s[k] for k in ("u", "p1", "pre", "Bk", "Ck", "ckpt", "host"))
+        B, L, m = u.shape
+        n = self.d_state
+        gy = self._gy(gy, u.shape)
+        r = ops.s6_scan_bwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, ckpt, gy)
+        # projection GEMMs (layers.py:1100-1112), compute precision
+        c = self.tdt
+        u2 = u.reshape(B * L, m).to(c)
+        gpre2 = r["gpre"].reshape(B * L, m)
+        gBk, gCk = r["gBk"].reshape(B * L, n), r["gCk"].reshape(B * L, n)
+        gp1 = gpre2 @ self.W_delta_proj.T
+        gu = (r["gu_local"].reshape(B * L, m).to(c) + gp1 @ self.W_delta.T + gBk @ self.W_B + gCk @ self.W_C)
+        grads = {"a_log": r["ga_log"], "W_B": gBk.T @ u2, "W_C": gCk.T @ u2, "W_delta": u2.T @ gp1,
+                 "W_delta_proj": p1.to(c).T @ gpre2, "b_delta": r["gb_delta"], "D": r["gD"]}
+        return self._out(grads, gu.reshape(B, L, m).to(self.io_dtype), host)
+
+
+# ---------------------------------------------------------------------------
+# RG-LRU
+
+
+class RGLRU(LinearRecurrence):
+    """Gated real recurrence of width d_model, y = x (layers.py:1171-1336)."""
+
+    kind = "rglru"
+    lti = False
+    continuous = False
+    bf16_ok = True
+    GATE_POWER = 8.0
+
+    def __init__(self, d_model, d_state=None, discretization=None, *, asynchronous=False, dtype="f64", rng=None,
+                 seed=0, a_min=0.9, a_max=0.999, device=None):
+        if d_state is not None and d_state != d_model:
+            warnings.warn(f"rglru's recurrence width is structurally d_model={d_model}; d_state={d_state} is ignored")
+        super().__init__(d_model, d_model, discretization, asynchronous, dtype, device)
+        rng = rng if rng is not None else Rng(seed)
+        r_a, r_r, r_i = rng.split(3)
+        m, dt = self.d_model, self.rdt
+        a0 = np.asarray(r_a.uniform(a_min, a_max, m), np.float64)
+        self.lambda_param = self._p(np.asarray(np.log(a0) - np.log1p(-a0), dt))
+        self.W_r = self._p(np.asarray(r_r.normal((m, m)) / np.sqrt(m), dt))
+        self.b_r = self._p(np.zeros(m, dt))
+        self.W_i = self._p(np.asarray(r_i.normal((m, m)) / np.sqrt(m), dt))
+        self.b_i = self._p(np.zeros(m, dt))
+
+    def parameters(self):
+        return {"lambda_param": self.lambda_param, "W_r": self.W_r, "b_r": self.b_r, "W_i": self.W_i,
+                "b_i": self.b_i}
+
+    def _forward(self, u, deltas, keep):
+        B, L, W = u.shape
+        u2 = u.reshape(B * L, W)
+        qr = (u2 @ self._w(self.W_r).T).reshape(B, L, W)
+        qi = (u2 @ self._w(self.W_i).T).reshape(B, L, W)
+        y, ckpt = ops.rglru_scan_fwd(u, qr, qi, self.lambda_param, self.b_r, self.b_i)
+        saved = {"u": u, "qr": qr, "qi": qi, "ckpt": ckpt, "y": y} if keep else {}
+        return y, saved, y[:, -1].to(self.tdt)
+
+    def _backward(self, s, gy):
+        u, qr, qi, ckpt, host = s["u"], s["qr"], s["qi"], s["ckpt"], s["host"]
+        B, L, W = u.shape
+        gy = self._gy(gy, u.shape)
+        r = ops.rglru_scan_bwd(u, qr, qi, self.lambda_param, self.b_r, self.b_i, ckpt, gy, y=s["y"])
+        c = self.tdt
+        u2 = u.reshape(B * L, W).to(c)
+        gqr2, gqi2 = r["gqr"].reshape(B * L, W).to(c), r["gqi"].reshape(B * L, W).to(c)
+        gu = r["gu_local"].reshape(B * L, W).to(c) + gqr2 @ self.W_r + gqi2 @ self.W_i
+        grads = {"lambda_param": sigmoid(-self.lambda_param) * r["gla"], "W_r": gqr2.T @ u2, "b_r": r["gb_r"],
+                 "W_i": gqi2.T @ u2, "b_i": r["gb_i"]}
+        return self._out(grads, gu.reshape(B, L, W).to(self.io_dtype), host)
+
+
+# ---------------------------------------------------------------------------
+# registry (layers.py:1343-1383)
+
+_REGISTRY = {"s4d": S4D, "s5": S5, "lru": LRU, "s6": S6, "rglru": RGLRU}
+
+
+def make_layer(kind, d_model, d_state=None, discretization=None, *, asynchronous=False, dtype="f64", rng=None,
+               seed=0, **extras):
+    try:
+        cls = _REGISTRY[kind]
+    except KeyError:
+        raise UnknownLayer(f"unknown layer kind {kind!r}; registered kinds: {sorted(_REGISTRY)}") from None
+    return cls(d_model, d_state=d_state, discretization=discretization, asynchronous=asynchronous, dtype=dtype,
+               rng=rng, seed=seed, **extras)
+
+
+def init_layer(kind, cfg: LayerConfig, rng: Rng):
+    return make_layer(kind, cfg.d_model, d_state=cfg.d_state, discretization=cfg.discretization,
+                      asynchronous=cfg.asynchronous, dtype=cfg.dtype, rng=rng, **cfg.extras)
+
+
+def lti_forward(layer, u, mode="sequential", *, workers=1, deltas=None, **kw):
+    if not layer.lti:
+        raise ValueError(f"{layer.kind} is time-varying; use ltv_forward")
+    return layer.forward(u, mode, workers=workers, deltas=deltas, **kw)
+
+
+def ltv_forward(layer, u, mode="sequential", *, workers=1, **kw):
+    if layer.lti:
+        raise ValueError(f"{layer.kind} is time-invariant; use lti_forward")
+    return layer.forward(u, mode, workers=workers, **kw)
+
+
+def layer_step(layer, state, u_k, delta_k=None):
+    return layer.step(state, u_k, delta_k)

@@ -1,0 +1,146 @@
+"""Scan-level operators: thin torch wrappers over the fused C-ABI kernels.
+
+These are the operator boundary between a layer's dense projections (GEMMs)
+and its recurrence — the unit the benchmark measures ("scan Gelem/s") and the
+unit a framework integration binds.  All tensors live on the
+current CUDA device; outputs are allocated here, workspaces are transient.
+
+  rglru_scan_fwd / rglru_scan_bwd   layers.py:1208-1291 (gates + scan + pullback)
+  s6_scan_fwd / s6_scan_bwd         layers.py:1038-1118 (delta softplus, ZOH/Euler
+                                    discretisation, scan, C readout, D skip)
+  mimo_scan_fwd / mimo_scan_bwd     layers.py:666-704 (v = scale * Bu, scan,
+                                    d abar / d scale reductions)
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+__all__ = ["rglru_scan_fwd", "rglru_scan_bwd", "s6_geometry", "s6_scan_fwd", "s6_scan_bwd", "mimo_scan_fwd",
+           "mimo_scan_bwd", "reduce_rows"]
+
+
+def reduce_rows(part, rows, cols):
+    """Fixed-order device reduction out[j] = sum_r part[r, j]."""
+    out = torch.empty(cols, dtype=part.dtype, device=part.device)
+    _lib.check(_lib.lib().lrx_reduce_rows(_lib.code_of(part.dtype), _lib.ptr(part), _lib.ptr(out), rows, cols,
+                                          _lib.stream()))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# RG-LRU
+
+def rglru_scan_fwd(u, qr, qi, lambda_param, b_r, b_i):
+    """y = x of the gated recurrence; u/qr/qi [B, L, W] (f32/f64/bf16).
+    Returns (y, ckpt) where ckpt holds the state entering every time chunk."""
+    B, L, W = u.shape
+    lib = _lib.lib()
+    code = _lib.code_of(u.dtype)
+    ck, nc = _lib.i64(), _lib.i64()
+    _lib.check(lib.lrx_rglru_chunking(code, L, _lib.ref(ck), _lib.ref(nc)))
+    y = torch.empty_like(u)
+    ckpt = torch.empty((nc.value, B * W), dtype=lambda_param.dtype, device=u.device)
+    ws = _lib.workspace(lib.lrx_rglru_workspace_bytes(code, B, L, W), u.device)
+    _lib.check(lib.lrx_rglru_fwd(code, _lib.ptr(u), _lib.ptr(qr), _lib.ptr(qi), _lib.ptr(lambda_param),
+                                 _lib.ptr(b_r), _lib.ptr(b_i), _lib.ptr(y), _lib.ptr(ckpt), B, L, W, _lib.ptr(ws),
+                                 ws.numel(), _lib.stream()))
+    return y, ckpt
+
+
+def rglru_scan_bwd(u, qr, qi, lambda_param, b_r, b_i, ckpt, gy, y=None):
+    """Pullback of rglru_scan_fwd.  Pass the forward output y (= the state) to
+    let the kernel stream it instead of recomputing from ckpt.  Returns dict
+    with gu_local (the s*i*g term; the gate-GEMM terms are the caller's), gqr,
+    gqi ([B, L, W]) and the batch/time sums gla (sum 8 r gloga), gb_r, gb_i."""
+    B, L, W = u.shape
+    lib = _lib.lib()
+    code = _lib.code_of(u.dtype)
+    gu, gqr, gqi = torch.empty_like(u), torch.empty_like(u), torch.empty_like(u)
+    f = dict(dtype=lambda_param.dtype, device=u.device)
+    gla, gbr, gbi = (torch.empty(W, **f) for _ in range(3))
+    ws = _lib.workspace(lib.lrx_rglru_workspace_bytes(code, B, L, W), u.device)
+    _lib.check(lib.lrx_rglru_bwd(code, _lib.ptr(u), _lib.ptr(qr), _lib.ptr(qi), _lib.ptr(lambda_param),
+                                 _lib.ptr(b_r), _lib.ptr(b_i), _lib.ptr(ckpt), _lib.ptr(y), _lib.ptr(gy),
+                                 _lib.ptr(gu), _lib.ptr(gqr), _lib.ptr(gqi), _lib.ptr(gla), _lib.ptr(gbr),
+                                 _lib.ptr(gbi), B, L, W, _lib.ptr(ws), ws.numel(), _lib.stream()))
+    return {"gu_local": gu, "gqr": gqr, "gqi": gqi, "gla": gla, "gb_r": gbr, "gb_i": gbi}
+
+
+# ---------------------------------------------------------------------------
+# S6
+
+def s6_geometry(io_dtype, L, D, N):
+    ck, nck, ndb = _lib.i64(), _lib.i64(), _lib.i64()
+    _lib.check(_lib.lib().lrx_s6_ckpt_len(_lib.code_of(io_dtype), L, D, N, _lib.ref(ck), _lib.ref(nck),
+                                          _lib.ref(ndb)))
+    return ck.value, nck.value, ndb.value
+
+
+def s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip):
+    """Selective scan; u/pre [B, L, D], Bk/Ck [B, L, N] (same dtype as u).
+    Returns (y, ckpt); ckpt[:, -1] is the final state [B, D, N]."""
+    B, L, D = u.shape
+    N = Bk.shape[-1]
+    _, nck, _ = s6_geometry(u.dtype, L, D, N)
+    y = torch.empty_like(u)
+    ckpt = torch.empty((B, nck, D, N), dtype=a_log.dtype, device=u.device)
+    _lib.check(_lib.lib().lrx_s6_fwd(_lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(pre), _lib.ptr(b_delta),
+                                     _lib.ptr(a_log), _lib.ptr(Bk), _lib.ptr(Ck), _lib.ptr(Dskip), _lib.ptr(y),
+                                     _lib.ptr(ckpt), B, L, D, N, _lib.stream()))
+    return y, ckpt
+
+
+def s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy):
+    """Pullback of s6_scan_fwd.  Returns dict: gu_local (D gy + delta sum_n g B),
+    gpre (d/d pre) [B, L, D]; gBk, gCk [B, L, N]; ga_log [D, N]; gD, gb_delta [D]."""
+    B, L, D = u.shape
+    N = Bk.shape[-1]
+    _, nck, ndb = s6_geometry(u.dtype, L, D, N)
+    f = dict(dtype=a_log.dtype, device=u.device)
+    gu, gpre = torch.empty_like(u), torch.empty(u.shape, **f)
+    gBp, gCp = torch.empty((ndb, B * L * N), **f), torch.empty((ndb, B * L * N), **f)
+    gap, gDp, gbp = torch.empty((B, D * N), **f), torch.empty((B, D), **f), torch.empty((B, D), **f)
+    _lib.check(_lib.lib().lrx_s6_bwd(
+        _lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(pre), _lib.ptr(b_delta), _lib.ptr(a_log), _lib.ptr(Bk),
+        _lib.ptr(Ck), _lib.ptr(Dskip), _lib.ptr(ckpt), _lib.ptr(gy), _lib.ptr(gu), _lib.ptr(gpre), _lib.ptr(gBp),
+        _lib.ptr(gCp), _lib.ptr(gap), _lib.ptr(gDp), _lib.ptr(gbp), B, L, D, N, _lib.stream()))
+    return {"gu_local": gu, "gpre": gpre,
+            "gBk": reduce_rows(gBp, ndb, B * L * N).reshape(B, L, N),
+            "gCk": reduce_rows(gCp, ndb, B * L * N).reshape(B, L, N),
+            "ga_log": reduce_rows(gap, B, D * N).reshape(D, N),
+            "gD": reduce_rows(gDp, B, D), "gb_delta": reduce_rows(gbp, B, D)}
+
+
+# ---------------------------------------------------------------------------
+# MIMO (S5 / LRU)
+
+def mimo_scan_fwd(abar, scale, bu):
+    """x_k = abar x_{k-1} + scale bu_k over complex bu [B, L, P]."""
+    B, L, P = bu.shape
+    lib = _lib.lib()
+    code = _lib.code_of(bu.dtype)
+    x = torch.empty_like(bu)
+    ws = _lib.workspace(lib.lrx_mimo_workspace_bytes(code, B, L, P), bu.device)
+    _lib.check(lib.lrx_mimo_fwd(code, _lib.ptr(abar.contiguous()), _lib.ptr(scale.contiguous()), _lib.ptr(bu),
+                                _lib.ptr(x), B, L, P, _lib.ptr(ws), ws.numel(), _lib.stream()))
+    return x
+
+
+def mimo_scan_bwd(abar, scale, bu, x, gx):
+    """Returns (gbu [B,L,P], gabar [P], gscale [P]) (complex)."""
+    B, L, P = x.shape
+    lib = _lib.lib()
+    code = _lib.code_of(x.dtype)
+    ck, nc = _lib.i64(), _lib.i64()
+    _lib.check(lib.lrx_mimo_chunking(code, L, _lib.ref(ck), _lib.ref(nc)))
+    nc = nc.value
+    gbu = torch.empty_like(x)
+    gap = torch.empty(nc * B * P, dtype=x.dtype, device=x.device)
+    gsp = torch.empty_like(gap)
+    ws = _lib.workspace(lib.lrx_mimo_bwd_workspace_bytes(code, B, L, P), x.device)
+    _lib.check(lib.lrx_mimo_bwd(code, _lib.ptr(abar.contiguous()), _lib.ptr(scale.contiguous()), _lib.ptr(bu),
+                                _lib.ptr(x), _lib.ptr(gx), _lib.ptr(gbu), _lib.ptr(gap), _lib.ptr(gsp), B, L, P,
+                                _lib.ptr(ws), ws.numel(), _lib.stream()))
+    return gbu, reduce_rows(gap, nc * B, P), reduce_rows(gsp, nc * B, P)

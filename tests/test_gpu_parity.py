@@ -1,0 +1,235 @@
+"""GPU parity: the sm_100a kernels (through the drop-in API / C-ABI) against the
+reference's golden outputs and the f64 oracle restatement.
+
+Error metric everywhere: max|got - ref| / max|ref| (reference bench.py:239-241).
+Tolerances (north_star): fp32 1e-4, bf16 I/O with fp32 accumulation 1e-2;
+f64 kernels are held to 1e-10 (the reference's own mode-equivalence bar).
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import port
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-10, "f32": 1e-4, "bf16": 1e-2}
+LAYER_FILES = sorted(glob.glob(os.path.join(GOLDEN, "layer_*.npz")))
+
+
+@pytest.fixture(scope="module")
+def lrx():
+    import paper_2602_08810_b200 as m
+    return m
+
+
+def rel(got, ref):
+    if isinstance(got, torch.Tensor):
+        got = got.detach().float().cpu().numpy() if got.dtype == torch.bfloat16 else got.detach().cpu().numpy()
+    return port.rel_err(got, ref)
+
+
+def _golden(path):
+    z = np.load(path)
+    rec = {k: z[k] for k in z.files}
+    n = int(rec["d_state"])
+    return rec, str(rec["kind"]), (str(rec["scheme"]) or None), (None if n < 0 else n)
+
+
+def _oracle_f64(kind, scheme, params, u, gy, deltas=None, asyn=False):
+    p64 = {k: np.asarray(v, np.float64) for k, v in params.items()}
+    lay = port.Layer(kind, p64, scheme, asynchronous=asyn)
+    y, saved = lay.forward(np.asarray(u, np.float64), deltas=None if deltas is None else np.asarray(deltas, np.float64))
+    g, gu = lay.backward(saved, np.asarray(gy, np.float64))
+    return y, g, gu
+
+
+@pytest.mark.parametrize("path", LAYER_FILES, ids=lambda p: os.path.basename(p)[6:-4])
+def test_layer_matches_reference_golden(lrx, path):
+    rec, kind, scheme, n = _golden(path)
+    dtype = str(rec["dtype"])
+    asyn = "deltas" in rec
+    layer = lrx.make_layer(kind, int(rec["d_model"]), n, scheme, asynchronous=asyn, dtype=dtype, seed=11)
+    deltas = rec.get("deltas")
+    for mode in ("sequential", "parallel"):
+        y, tape = layer.forward(rec["u"], mode, workers=3, deltas=deltas, tape=True)
+        g = lrx.layer_backward(layer, tape, rec["gy"])
+        assert isinstance(y, np.ndarray) and y.dtype == layer.rdt
+        if dtype == "f64":
+            ref_y, ref_g, ref_gu = rec["y"], {k[5:]: rec[k] for k in rec if k.startswith("grad:")}, rec["gu"]
+        else:  # f32 path is judged against the f64 ground truth on the same inputs
+            params = {k[6:]: rec[k] for k in rec if k.startswith("param:")}
+            ref_y, ref_g, ref_gu = _oracle_f64(kind, scheme, params, rec["u"], rec["gy"], deltas, asyn)
+        tol = TOL[dtype]
+        assert rel(y, ref_y) < tol, (mode, rel(y, ref_y))
+        assert rel(g.u, ref_gu) < tol, (mode, rel(g.u, ref_gu))
+        assert list(g.params) == list(layer.parameters())
+        for k, v in ref_g.items():
+            assert g.params[k].shape == v.shape, k
+            assert rel(g.params[k], v) < tol, (mode, k, rel(g.params[k], v))
+
+
+def test_modes_agree_bitwise_and_runs_are_deterministic(lrx):
+    for kind, n in (("s6", 16), ("rglru", None), ("s5", 32), ("lru", 16), ("s4d", 8)):
+        layer = lrx.make_layer(kind, 24, n, dtype="f32", seed=3)
+        u = port.Rng(5).normal((2, 700, 24)).astype(np.float32)
+        gy = port.Rng(6).normal((2, 700, 24)).astype(np.float32)
+        outs = []
+        for mode in ("sequential", "parallel", "parallel"):
+            y, tape = layer.forward(u, mode, workers=7, tape=True)
+            g = lrx.layer_backward(layer, tape, gy)
+            outs.append((y, g.u, g.params))
+        for y, gu, gp in outs[1:]:
+            np.testing.assert_array_equal(y, outs[0][0])
+            np.testing.assert_array_equal(gu, outs[0][1])
+            for k in gp:
+                np.testing.assert_array_equal(gp[k], outs[0][2][k], err_msg=f"{kind}:{k}")
+
+
+@pytest.mark.parametrize("kind,m,n,B,L", [
+    ("s6", 40, 16, 2, 1500), ("s6", 33, 4, 3, 70), ("s6", 16, 8, 1, 129), ("s6", 8, 32, 2, 100),
+    ("s6", 12, 64, 1, 80), ("s6", 20, 13, 2, 65),
+    ("rglru", 200, None, 3, 1111), ("rglru", 7, None, 1, 1), ("rglru", 130, None, 2, 33),
+    ("s5", 64, 128, 2, 1024), ("s5", 10, 6, 3, 2), ("lru", 128, 64, 2, 1024), ("lru", 5, 3, 1, 17),
+    ("s4d", 6, 10, 2, 300),
+])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_layer_matches_oracle_multichunk(lrx, kind, m, n, B, L, dtype):
+    layer = lrx.make_layer(kind, m, n, dtype=dtype, seed=17)
+    u = port.Rng(1).normal((B, L, m)).astype(layer.rdt)
+    gy = port.Rng(2).normal((B, L, m)).astype(layer.rdt)
+    y, tape = layer.forward(u, tape=True)
+    g = lrx.layer_backward(layer, tape, gy)
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64(kind, layer.discretization, params, u, gy)
+    tol = TOL[dtype]
+    assert rel(y, ry) < tol
+    assert rel(g.u, rgu) < tol
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < tol, (k, rel(g.params[k], rg[k]))
+
+
+@pytest.mark.parametrize("kind", ["s6", "rglru"])
+def test_bf16_io_matches_f64_oracle(lrx, kind):
+    m, n, B, L = (64, 16, 2, 1200) if kind == "s6" else (256, None, 2, 1500)
+    layer = lrx.make_layer(kind, m, n, dtype="bf16", seed=23)
+    u = torch.from_numpy(port.Rng(3).normal((B, L, m))).to("cuda", torch.bfloat16)
+    gy = torch.from_numpy(port.Rng(4).normal((B, L, m))).to("cuda", torch.bfloat16)
+    y, tape = layer.forward(u, tape=True)
+    assert y.dtype == torch.bfloat16 and y.is_cuda
+    g = lrx.layer_backward(layer, tape, gy)
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64(kind, None, params, u.float().cpu().numpy(), gy.float().cpu().numpy())
+    assert rel(y, ry) < TOL["bf16"]
+    assert rel(g.u, rgu) < TOL["bf16"]
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < TOL["bf16"], (k, rel(g.params[k], rg[k]))
+
+
+@pytest.mark.parametrize("key", ["real_const", "real_var", "cplx_const", "cplx_var"])
+def test_scan_operator_matches_reference(lrx, key):
+    z = np.load(os.path.join(GOLDEN, "scan_ops.npz"))
+    a, b, x0 = z[key + ":a"], z[key + ":b"], z[key + ":x0"]
+    assert rel(lrx.scan_sequential(a, b, x0), z[key + ":seq"]) < 1e-13
+    assert rel(lrx.scan_parallel(a, b, x0, workers=3), z[key + ":par3"]) < 1e-13
+    states, tape = lrx.scan_forward(a, b, x0)
+    ga, gb, gx0 = lrx.scan_backward(tape, z[key + ":gx"])
+    assert rel(ga, z[key + ":ga"]) < 1e-12
+    assert rel(gb, z[key + ":gb"]) < 1e-12
+    assert rel(gx0, z[key + ":gx0"]) < 1e-12
+    with pytest.raises(lrx.TapeConsumed):
+        lrx.scan_backward(tape, z[key + ":gx"])
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64, np.complex64, np.complex128])
+@pytest.mark.parametrize("L,N", [(1, 1), (2, 3), (255, 129), (4097, 300), (33, 5000)])
+def test_scan_operator_sizes_vs_oracle(lrx, dt, L, N):
+    rng = port.Rng(L * 7 + N)
+    cplx = np.dtype(dt).kind == "c"
+
+    def draw(shape):
+        x = rng.normal(shape)
+        return (x + 1j * rng.normal(shape)) if cplx else x
+
+    for per in (False, True):
+        a = (0.97 * np.exp(1j * rng.normal((L, N) if per else N)) if cplx else
+             rng.uniform(-0.99, 0.99, (L, N) if per else N)).astype(dt)
+        b, x0, gx = draw((L, N)).astype(dt), draw(N).astype(dt), draw((L, N)).astype(dt)
+        tol = 1e-5 if np.dtype(dt) in (np.float32, np.complex64) else 1e-12
+        ref = port.scan_sequential(a.astype(np.complex128 if cplx else np.float64),
+                                   b.astype(np.complex128 if cplx else np.float64), x0)
+        assert rel(lrx.scan_sequential(a, b, x0), ref) < tol
+        st, tape = lrx.scan_forward(a, b, x0)
+        ga, gb, gx0 = lrx.scan_backward(tape, gx)
+        ra, rb, rx0 = port.scan_backward(a.astype(ref.dtype), ref, x0.astype(ref.dtype), gx.astype(ref.dtype))
+        assert rel(gb, rb) < tol and rel(gx0, rx0) < tol and rel(ga, ra) < tol * 10
+
+
+def test_known_answers(lrx):  # reference test_scan.py:19-30, 112-117, 155-160
+    np.testing.assert_array_equal(lrx.scan_sequential(np.array(0.5), np.ones(3)), [1.0, 1.5, 1.75])
+    np.testing.assert_array_equal(lrx.scan_sequential(np.array(0.5), np.ones(3), x0=np.array(1.0)),
+                                  [1.5, 1.75, 1.875])
+    out = lrx.scan_sequential(np.array([0.5]), np.zeros((4, 1)), x0=np.array([16.0]))
+    np.testing.assert_array_equal(out[:, 0], [8.0, 4.0, 2.0, 1.0])
+    out = lrx.scan_sequential(np.array([0.5], np.float32), np.array([[2.0]], np.float32))
+    assert out.dtype == np.float32 and out[0, 0] == 2.0
+    with pytest.raises(lrx.ShapeError):
+        lrx.scan_sequential(np.ones(3), np.ones((10, 4)))
+    with pytest.raises(lrx.ShapeError):
+        lrx.scan_sequential(np.ones((9, 3)), np.ones((10, 3)))
+
+
+def test_api_contract(lrx):
+    layer = lrx.make_layer("lru", 2, 4, seed=3)
+    u = port.Rng(4).normal((1, 8, 2))
+    y, tape = layer.forward(u, tape=True)
+    lrx.layer_backward(layer, tape, np.ones_like(y))
+    with pytest.raises(lrx.TapeConsumed):
+        lrx.layer_backward(layer, tape, np.ones_like(y))
+    with pytest.raises(lrx.ShapeError):
+        layer.forward(np.zeros((1, 8, 3)))
+    with pytest.raises(ValueError):
+        layer.forward(u, "turbo")
+    with pytest.raises(ValueError):
+        layer.forward(u, deltas=np.ones(8))  # LRU is discrete-time
+    y, st = layer.forward(u, return_state=True)
+    assert st.k == 8 and tuple(st.x.shape) == (1, 4)
+    with pytest.raises(lrx.SingularBilinear):  # reference test_discretize.py:97-99
+        lrx.scheme_factors("bilinear", torch.tensor([2.0 + 0j], device="cuda"), torch.tensor([1.0], device="cuda"))
+
+
+def test_fault_hook_is_detected(lrx):
+    from paper_2602_08810_b200 import autograd as ag
+    layer = lrx.make_layer("lru", 2, 4, seed=3)
+    u = port.Rng(4).normal((1, 6, 2))
+    _, t1 = layer.forward(u, tape=True)
+    clean = lrx.layer_backward(layer, t1, np.ones((1, 6, 2)))
+    ag._grad_fault = "nu_log"
+    try:
+        _, t2 = layer.forward(u, tape=True)
+        dirty = lrx.layer_backward(layer, t2, np.ones((1, 6, 2)))
+    finally:
+        ag._grad_fault = None
+    np.testing.assert_allclose(dirty.params["nu_log"], 1.01 * clean.params["nu_log"], rtol=1e-12)
+    np.testing.assert_array_equal(dirty.params["D"], clean.params["D"])
+
+
+@pytest.mark.parametrize("kind", ["s4d", "s5", "lru", "s6", "rglru"])
+def test_finite_differences_on_device(lrx, kind):  # reference test_autograd.py:238-254
+    layer = lrx.make_layer(kind, 3, None if kind == "rglru" else 4, seed=31)
+    u = port.Rng(32).normal((2, 10, 3))
+    rep = lrx.check_layer_gradients(layer, u, rng=lrx.Rng(33))
+    assert rep.passed, str(rep)
+
+
+def test_native_kernels_ran(lrx):
+    from paper_2602_08810_b200 import _lib
+    before = _lib.launch_count()
+    layer = lrx.make_layer("s6", 16, 16, dtype="f32")
+    y, tape = layer.forward(np.ones((1, 5, 16), np.float32), tape=True)
+    lrx.layer_backward(layer, tape, np.ones_like(y))
+    assert _lib.launch_count() > before

@@ -1,0 +1,61 @@
+"""Host-side logic of the drop-in API that runs without a GPU: parameter
+initialisation (bit-identical to the reference), validation and errors."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import paper_2602_08810_b200 as lrx
+from tests.conftest import GOLDEN
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "layer_*.npz"))),
+                         ids=lambda p: os.path.basename(p)[6:-4])
+def test_parameter_init_matches_reference(path):
+    z = np.load(path)
+    n = int(z["d_state"])
+    layer = lrx.make_layer(str(z["kind"]), int(z["d_model"]), None if n < 0 else n,
+                           str(z["scheme"]) or None, asynchronous="deltas" in z.files,
+                           dtype=str(z["dtype"]), seed=int(z["seed"]), device="cpu")
+    params = layer.parameters()
+    want = {k[6:]: z[k] for k in z.files if k.startswith("param:")}
+    assert list(params) == list(want)  # same keys, same order
+    for k, v in want.items():
+        np.testing.assert_array_equal(params[k].numpy(), v, err_msg=k)
+
+
+def test_registry_and_errors():
+    with pytest.raises(lrx.UnknownLayer):
+        lrx.make_layer("s7", 4, device="cpu")
+    with pytest.raises(ValueError):
+        lrx.make_layer("s5", 4, 5, device="cpu")  # odd d_state
+    with pytest.raises(ValueError):
+        lrx.make_layer("s4d", 4, discretization="euler", device="cpu")
+    with pytest.raises(ValueError):
+        lrx.make_layer("lru", 4, dtype="bf16", device="cpu")
+    with pytest.warns(UserWarning):
+        lrx.make_layer("lru", 4, discretization="zoh", device="cpu")
+    layer = lrx.make_layer("s6", 4, dtype="bf16", device="cpu")
+    assert layer.parameters()["a_log"].dtype.is_floating_point
+
+
+def test_cpu_layer_refuses_to_compute():
+    layer = lrx.make_layer("rglru", 4, device="cpu")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        layer.forward(np.zeros((1, 3, 4)))
+
+
+def test_plan_chunks_and_combine_host():
+    assert lrx.plan_chunks(513, 2) == [(0, 257), (257, 513)]
+    a, b = lrx.combine((np.array(0.5), np.array(1.0)), (np.array(0.5), np.array(1.0)))
+    assert a == 0.25 and b == 1.5
+    with pytest.raises(lrx.ShapeError):
+        lrx.combine((np.zeros(3), np.zeros(3)), (np.zeros(4), np.zeros(4)))
+
+
+def test_host_numerics():
+    x = np.array([-100.0, 0.0, 40.0, 60.0])
+    np.testing.assert_allclose(lrx.softplus(x), [0.0, np.log(2), 40.0, 60.0], atol=1e-15)
+    np.testing.assert_allclose(lrx.sigmoid(np.array([-800.0, 0.0, 800.0])), [0.0, 0.5, 1.0])
+    assert lrx.real_dtype("f32") == np.float32
