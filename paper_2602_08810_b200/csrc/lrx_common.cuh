@@ -111,27 +111,40 @@ template <> struct Math<double> {
 // exactly where a naive exp(x) - 1 cancels, layers.py:1217).
 template <typename C> struct Fast;
 template <> struct Fast<float> {
-    __device__ static float exp(float x) { return __expf(x); }
-    __device__ static float rcp(float x) { return __frcp_rn(x); }
-    __device__ static float div(float a, float b) { return __fdividef(a, b); }
-    __device__ static float sqrt(float x) { return __fsqrt_rn(x); }
-    __device__ static float sigmoid(float x) {
-        const float e = __expf(-fabsf(x));           // never overflows
-        const float r = __frcp_rn(1.f + e);
-        return x >= 0.f ? r : e * r;
+    __device__ static float ex2(float x) {
+        float y;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+        return y;
     }
+    __device__ static float exp(float x) { return ex2(x * 1.4426950408889634f); }
+    __device__ static float rcp(float x) {
+        float y;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+        return y;
+    }
+    __device__ static float div(float a, float b) { return a * rcp(b); }
+    __device__ static float sqrt(float x) {
+        float y;
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+        return y;
+    }
+    // 1/(1+e^-x): saturates cleanly (e^-x -> inf gives rcp -> 0)
+    __device__ static float sigmoid(float x) { return rcp(1.f + exp(-x)); }
+    // Relative-accurate e^x - 1 without branches: for |x| < 0.7 a degree-6
+    // Taylor polynomial at h = x/2 and the doubling expm1(x) = p (p + 2);
+    // otherwise e^x - 1 carries no cancellation.
     __device__ static float expm1(float x) {
-        if (fabsf(x) < 0.35f) {
-            float p = 1.f / 5040.f;
-            p = fmaf(p, x, 1.f / 720.f);
-            p = fmaf(p, x, 1.f / 120.f);
-            p = fmaf(p, x, 1.f / 24.f);
-            p = fmaf(p, x, 1.f / 6.f);
-            p = fmaf(p, x, 0.5f);
-            p = fmaf(p, x, 1.f);
-            return p * x;
-        }
-        return __expf(x) - 1.f;
+        const float h = 0.5f * x;
+        float p = 1.f / 720.f;
+        p = fmaf(p, h, 1.f / 120.f);
+        p = fmaf(p, h, 1.f / 24.f);
+        p = fmaf(p, h, 1.f / 6.f);
+        p = fmaf(p, h, 0.5f);
+        p = fmaf(p, h, 1.f);
+        p *= h;
+        const float small = p * (p + 2.f);
+        const float big = exp(x) - 1.f;
+        return fabsf(x) < 0.7f ? small : big;
     }
 };
 template <> struct Fast<double> {

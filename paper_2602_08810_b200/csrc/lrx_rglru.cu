@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(LW) fwd_tma_kernel(const __grid_constant__ CUt
     IO* py = y + (int64_t)row0 * W + w;
     C* pc = ckpt ? ckpt + (int64_t)b * W + w : nullptr;
     const int64_t ck_stride = (int64_t)Bn * W;
+    static_assert(CK % PF == 0, "checkpoint interval must be a multiple of the tile");
     for (int j = 0; j < n_tiles; ++j) {
         const int s = j % S;
         const uint32_t ph = (j / S) & 1;
@@ -175,18 +176,28 @@ __global__ void __launch_bounds__(LW) fwd_tma_kernel(const __grid_constant__ CUt
             tma::mbar_wait(&R.empty[s], ph);
             issue(j + S);
         }
-        const int64_t t0 = (int64_t)j * PF;
+        if (pc && (j % (CK / PF)) == 0) {  // state entering this checkpoint chunk
+            if (valid) __stcs(pc, x);
+            pc += ck_stride;
+        }
+        const int nk = (int)min((int64_t)PF, L - (int64_t)j * PF);
+        if (nk == PF) {
 #pragma unroll
-        for (int k = 0; k < PF; ++k) {
-            const int64_t t = t0 + k;
-            if (t < L) {
-                if (pc && (t % CK) == 0) {
-                    if (valid) __stcs(pc, x);
-                    pc += ck_stride;
-                }
+            for (int k = 0; k < PF; ++k) {
                 const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
                 x = q.a * x + (q.s * q.i) * q.u;
-                if (valid) st_io(py + t * W, x);
+                if (valid) st_io(py, x);
+                py += W;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < PF; ++k) {
+                if (k < nk) {
+                    const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
+                    x = q.a * x + (q.s * q.i) * q.u;
+                    if (valid) st_io(py, x);
+                    py += W;
+                }
             }
         }
     }
@@ -249,7 +260,7 @@ __global__ void __launch_bounds__(LW) bwd_tma_kernel(
     }
     C h = 0;
     Kahan<C> sla, sbr, sbi;
-    const int64_t base = (int64_t)row0 * W + w;
+    IO *pgu = gu + (int64_t)row0 * W + w, *pgr = gqr + (int64_t)row0 * W + w, *pgi = gqi + (int64_t)row0 * W + w;
     for (int j = 0; j < n_tiles; ++j) {
         const int s = j % S;
         const uint32_t ph = (j / S) & 1;
@@ -272,26 +283,31 @@ __global__ void __launch_bounds__(LW) bwd_tma_kernel(
             issue(j + S);
         }
         const int64_t t0 = (int64_t)tt * PF;
+        const int nk = (int)min((int64_t)PF, L - t0);
+        if (tt == 0) cy[0] = IO(0);  // x_{-1} = 0
+        C tla = 0, tbr = 0, tbi = 0;
+        const int64_t o0 = t0 * W;
 #pragma unroll
         for (int k = PF - 1; k >= 0; --k) {
-            const int64_t t = t0 + k;
-            if (t < L) {
+            if (k < nk) {
                 const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
                 const C g = C(cvt(cg[k])) + h;
                 h = q.a * g;
-                const C xp = t == 0 ? C(0) : C(cvt(cy[k]));
-                const BwdOut<C> o = bwd_step<C>(q, g, xp, la);
+                const BwdOut<C> o = bwd_step<C>(q, g, C(cvt(cy[k])), la);
                 if (valid) {
-                    const int64_t off = base + t * W;
-                    st_io(gu + off, o.gu);
-                    st_io(gqr + off, o.gqr);
-                    st_io(gqi + off, o.gqi);
+                    const int64_t off = o0 + (int64_t)k * W;
+                    st_io(pgu + off, o.gu);
+                    st_io(pgr + off, o.gqr);
+                    st_io(pgi + off, o.gqi);
                 }
-                sla.add(o.la_term);
-                sbr.add(o.gqr);
-                sbi.add(o.gqi);
+                tla += o.la_term;
+                tbr += o.gqr;
+                tbi += o.gqi;
             }
         }
+        sla.add(tla);
+        sbr.add(tbr);
+        sbi.add(tbi);
     }
     if (valid) {
         const int64_t p = (int64_t)b * W + w;
