@@ -12,7 +12,7 @@ region.  Workloads are BASELINE.json's configs:
   s5      configs[1]  S5    B=32 L=4096   H=256  P=128 (complex)    f32, ZOH
   s6      configs[2]  S6    B=16 L=8192   D=1536 N=16               bf16 I/O, fp32 accum
   rglru   configs[3]  RG-LRU B=64 L=16384 W=2560                    f32   (default)
-  s6_long configs[4]  S6    B=1  L=2^20   D=2048 N=16               bf16 I/O (1 GPU)
+  s6_long configs[4]  S6    B=1  L=2^20   D=2048 N=16               bf16 I/O, sequence-parallel
 
 The default is the RG-LRU config: BASELINE.json's metric is the scan's HBM
 throughput at 1/2/4/8 GPUs, and configs[3] is the config it names for the
@@ -50,7 +50,7 @@ WORKLOADS = {
     "s5": dict(kind="s5", B=32, L=4096, H=256, N=128, dtype="f32", cfg=1),
     "s6": dict(kind="s6", B=16, L=8192, H=1536, N=16, dtype="bf16", cfg=2),
     "rglru": dict(kind="rglru", B=64, L=16384, H=2560, N=1, dtype="f32", cfg=3),
-    "s6_long": dict(kind="s6", B=1, L=2 ** 20, H=2048, N=16, dtype="bf16", cfg=4),
+    "s6_long": dict(kind="s6", B=1, L=2 ** 20, H=2048, N=16, dtype="bf16", cfg=4, seqpar=True, sub=64),
 }
 DEFAULT_WORKLOAD = "rglru"
 METRIC = "scan Gelem/s (B·L·H·N) fwd+bwd, HBM GB/s vs peak, at 1/2/4/8 B200"
@@ -131,15 +131,17 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # GPU arm
 
-def build_problem(w, B, device):
+def build_problem(w, B, device, L=None, group=None):
     """Synthetic inputs (reference init + N(0,1) activations, on device) and a
-    step function fwd+bwd at the operator boundary."""
+    step function fwd+bwd at the operator boundary.  `L` overrides the
+    sequence length (this rank's slice in sequence-parallel mode)."""
     import torch
 
     import paper_2602_08810_b200 as lrx
     from paper_2602_08810_b200 import ops
 
-    kind, L, H, N = w["kind"], w["L"], w["H"], w["N"]
+    kind, H, N = w["kind"], w["H"], w["N"]
+    L = L or w["L"]
     layer = lrx.make_layer(kind, H, None if kind == "rglru" else (N if kind != "s5" else 2 * N), dtype=w["dtype"],
                            seed=0, device=device)
     g = torch.Generator(device=device).manual_seed(1234 + (torch.distributed.get_rank()
@@ -173,12 +175,23 @@ def build_problem(w, B, device):
             prob["Bk"] = _mm(u2, layer.W_B.T).reshape(B, L, N)
             prob["Ck"] = _mm(u2, layer.W_C.T).reshape(B, L, N)
         pa = (layer.b_delta, layer.a_log)
+        if w.get("seqpar"):
+            from paper_2602_08810_b200.distributed import LongS6
+            ls = LongS6(sub=w["sub"], group=group)
+            args = (prob["u"], prob["pre"], *pa, prob["Bk"], prob["Ck"], layer.D)
 
-        def fwd():
-            return ops.s6_scan_fwd(prob["u"], prob["pre"], *pa, prob["Bk"], prob["Ck"], layer.D)
+            def fwd():
+                return ls.forward(*args)
 
-        def bwd(ctx):
-            return ops.s6_scan_bwd(prob["u"], prob["pre"], *pa, prob["Bk"], prob["Ck"], layer.D, ctx[1], prob["gy"])
+            def bwd(ctx):
+                return ls.backward(ctx[1], *args, prob["gy"])
+        else:
+            def fwd():
+                return ops.s6_scan_fwd(prob["u"], prob["pre"], *pa, prob["Bk"], prob["Ck"], layer.D)
+
+            def bwd(ctx):
+                return ops.s6_scan_bwd(prob["u"], prob["pre"], *pa, prob["Bk"], prob["Ck"], layer.D, ctx[1],
+                                       prob["gy"])
 
         bu, bp = u.element_size(), prob["pre"].element_size()
         per = B * L * H
@@ -209,10 +222,16 @@ def run_gpu(args, w, rank, world, device):
     from paper_2602_08810_b200 import _lib
 
     B_total = w["B"]
-    if B_total % world:
-        raise SystemExit(f"batch {B_total} does not split over {world} GPUs")
-    B = B_total // world
-    prob = build_problem(w, B, device)
+    L_rank = None
+    if w.get("seqpar"):  # the time axis is split across ranks (C5)
+        if w["L"] % (world * w["sub"]):
+            raise SystemExit(f"L={w['L']} does not split into {world} x {w['sub']} slices")
+        B, L_rank = B_total, w["L"] // world
+    else:
+        if B_total % world:
+            raise SystemExit(f"batch {B_total} does not split over {world} GPUs")
+        B = B_total // world
+    prob = build_problem(w, B, device, L=L_rank, group=dist.group.WORLD if world > 1 else None)
     fwd, bwd = prob["fwd"], prob["bwd"]
     stream = torch.cuda.current_stream()
 
@@ -270,8 +289,14 @@ def run_e2e(args, w, prob, device):
 
     from paper_2602_08810_b200 import layer_backward, ops
 
-    kind, L, H, N = w["kind"], w["L"], w["H"], w["N"]
+    kind, H, N = w["kind"], w["H"], w["N"]
+    L = prob["u"].shape[1]
     Bs = min(prob["B"], args.e2e_batch)
+    if w.get("seqpar"):  # e2e on a 1/16 time slice of this rank's sequence (host memory)
+        L = L // 16
+        for n in ("u", "pre", "Bk", "Ck", "gy"):
+            prob = dict(prob)
+            prob[n] = prob[n][:, :L].contiguous()
     names = {"rglru": ("u", "qr", "qi", "gy"), "s6": ("u", "pre", "Bk", "Ck", "gy")}.get(kind, ("u", "gy"))
     host = {n: prob[n][:Bs].cpu().pin_memory() for n in names}
     layer = prob["layer"]
@@ -286,6 +311,12 @@ def run_e2e(args, w, prob, device):
             r = ops.rglru_scan_bwd(d["u"], d["qr"], d["qi"], layer.lambda_param, layer.b_r, layer.b_i, ck, d["gy"],
                                    y=y)
             return [y, r["gu_local"], r["gqr"], r["gqi"], r["gla"], r["gb_r"], r["gb_i"]]
+        if kind == "s6" and w.get("seqpar"):
+            from paper_2602_08810_b200.distributed import LongS6
+            ls = LongS6(sub=w["sub"])
+            a = (d["u"], d["pre"], layer.b_delta, layer.a_log, d["Bk"], d["Ck"], layer.D)
+            y, ctx = ls.forward(*a)
+            return [y] + list(ls.backward(ctx, *a, d["gy"]).values())
         if kind == "s6":
             y, ck = ops.s6_scan_fwd(d["u"], d["pre"], layer.b_delta, layer.a_log, d["Bk"], d["Ck"], layer.D)
             r = ops.s6_scan_bwd(d["u"], d["pre"], layer.b_delta, layer.a_log, d["Bk"], d["Ck"], layer.D, ck,
@@ -388,7 +419,9 @@ def main():
     elems = _state_dims(w)
     config = {"workload": f"{args.workload}: configs[{w['cfg']}] {w['kind']} B={w['B']} L={w['L']} H={w['H']} "
                           f"N={w['N']}", "global_batch": w["B"], "seq_len": w["L"], "width": w["H"],
-              "d_state": w["N"], "parallelism": f"batch-sharded x{world}" if world > 1 else "single GPU",
+              "d_state": w["N"],
+              "parallelism": (f"sequence-parallel x{world} (x{w.get('sub')} sub-slices per GPU)" if w.get("seqpar")
+                              else f"batch-sharded x{world}" if world > 1 else "single GPU"),
               "l2": "inputs > L2 (126 MB): no flush needed"}
 
     if args.impl == "reference":
@@ -419,8 +452,6 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
     torch.cuda.set_device(device)
-    if w["kind"] == "s6" and w["B"] == 1 and world > 1:
-        raise SystemExit("s6_long runs on one GPU in this build (sequence-parallel mode: see DESIGN.md)")
     r = run_gpu(args, w, rank, world, device)
     if rank != 0:
         if world > 1:

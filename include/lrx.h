@@ -131,19 +131,25 @@ int lrx_rglru_bwd(int io_dtype, const void* u, const void* qr, const void* qi, c
  * (= rows of the gBk/gCk partials) the kernels use for these extents. */
 int lrx_s6_ckpt_len(int io_dtype, int64_t L, int64_t D, int64_t N, int64_t* ckpt_len, int64_t* n_ckpt,
                     int64_t* n_dblk);
+/* x0 [B, D, N] (compute precision, NULL = zeros) seeds the state: the
+ * sequence-parallel mode continues a scan another rank started. */
 int lrx_s6_fwd(int io_dtype, const void* u, const void* pre, const void* b_delta, const void* a_log,
-               const void* Bk, const void* Ck, const void* Dskip, void* y, void* ckpt, int64_t B,
-               int64_t L, int64_t D, int64_t N, void* stream);
+               const void* Bk, const void* Ck, const void* Dskip, const void* x0, void* y, void* ckpt,
+               int64_t B, int64_t L, int64_t D, int64_t N, void* stream);
 /* Outputs: gu_local = D gy + delta * sum_n g B   (GEMM terms are the
  * caller's) [B,L,D] io dtype; gpre = sigmoid(pre+b) * gdelta [B,L,D]
  * compute precision;
  * gBk_part, gCk_part [n_dblk, B, L, N] per channel-block partials;
  * ga_part (d/d a_log, already times a) [B, D, N]; gD_part, gb_part [B, D]
  * (compute precision).  Reduce the partial axes with lrx_reduce_rows. */
+/* h_in [B, D, N] (NULL = zeros) is the cotangent carry entering from the
+ * right (abar_{L} g_{L} of the next slice); h_out [B, D, N] (NULL to skip)
+ * receives abar_0 g_0 = d loss / d x0 (the carry for the slice to the left). */
 int lrx_s6_bwd(int io_dtype, const void* u, const void* pre, const void* b_delta, const void* a_log,
                const void* Bk, const void* Ck, const void* Dskip, const void* ckpt, const void* gy,
-               void* gu_local, void* gpre, void* gBk_part, void* gCk_part, void* ga_part, void* gD_part,
-               void* gb_part, int64_t B, int64_t L, int64_t D, int64_t N, void* stream);
+               const void* h_in, void* gu_local, void* gpre, void* gBk_part, void* gCk_part, void* ga_part,
+               void* gD_part, void* gb_part, void* h_out, int64_t B, int64_t L, int64_t D, int64_t N,
+               void* stream);
 
 /* ------------------------------------------------------------------------ *
  * MIMO complex diagonal scan for S5 / LRU (layers.py:616-980): the recurrence

@@ -20,37 +20,35 @@ int lrx_s6_ckpt_len(int io_dtype, int64_t L, int64_t D, int64_t N, int64_t* ckpt
 }
 
 int lrx_s6_fwd(int io_dtype, const void* u, const void* pre, const void* b_delta, const void* a_log, const void* Bk,
-               const void* Ck, const void* Dskip, void* y, void* ckpt, int64_t B, int64_t L, int64_t D, int64_t N,
-               void* stream) {
+               const void* Ck, const void* Dskip, const void* x0, void* y, void* ckpt, int64_t B, int64_t L,
+               int64_t D, int64_t N, void* stream) {
     LRX_REQUIRE(B >= 1 && L >= 1 && D >= 1 && N >= 1, LRX_ERR_SHAPE, "bad extents");
     cudaStream_t st = (cudaStream_t)stream;
     switch (io_dtype) {
-        case LRX_F32: return s6::fwd_f32(u, pre, b_delta, a_log, Bk, Ck, Dskip, y, ckpt, B, L, D, N, st);
-        case LRX_BF16:
-            return s6::fwd_bf16(u, pre, b_delta, a_log, Bk, Ck, Dskip, y, ckpt, B, L, D, N, st);
-        case LRX_F64:
-            return s6::fwd_f64(u, pre, b_delta, a_log, Bk, Ck, Dskip, y, ckpt, B, L, D, N, st);
+        case LRX_F32: return s6::fwd_f32(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0, y, ckpt, B, L, D, N, st);
+        case LRX_BF16: return s6::fwd_bf16(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0, y, ckpt, B, L, D, N, st);
+        case LRX_F64: return s6::fwd_f64(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0, y, ckpt, B, L, D, N, st);
     }
     set_error("s6: unsupported io dtype %d", io_dtype);
     return LRX_ERR_VALUE;
 }
 
 int lrx_s6_bwd(int io_dtype, const void* u, const void* pre, const void* b_delta, const void* a_log, const void* Bk,
-               const void* Ck, const void* Dskip, const void* ckpt, const void* gy, void* gu_local, void* gpre,
-               void* gBk_part, void* gCk_part, void* ga_part, void* gD_part, void* gb_part, int64_t B, int64_t L,
-               int64_t D, int64_t N, void* stream) {
+               const void* Ck, const void* Dskip, const void* ckpt, const void* gy, const void* h_in, void* gu_local,
+               void* gpre, void* gBk_part, void* gCk_part, void* ga_part, void* gD_part, void* gb_part, void* h_out,
+               int64_t B, int64_t L, int64_t D, int64_t N, void* stream) {
     LRX_REQUIRE(B >= 1 && L >= 1 && D >= 1 && N >= 1, LRX_ERR_SHAPE, "bad extents");
     cudaStream_t st = (cudaStream_t)stream;
     switch (io_dtype) {
         case LRX_F32:
-            return s6::bwd_f32(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, gu_local, gpre, gBk_part,
-                                           gCk_part, ga_part, gD_part, gb_part, B, L, D, N, st);
+            return s6::bwd_f32(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in, gu_local, gpre, gBk_part,
+                               gCk_part, ga_part, gD_part, gb_part, h_out, B, L, D, N, st);
         case LRX_BF16:
-            return s6::bwd_bf16(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, gu_local, gpre,
-                                                   gBk_part, gCk_part, ga_part, gD_part, gb_part, B, L, D, N, st);
+            return s6::bwd_bf16(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in, gu_local, gpre, gBk_part,
+                                gCk_part, ga_part, gD_part, gb_part, h_out, B, L, D, N, st);
         case LRX_F64:
-            return s6::bwd_f64(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, gu_local, gpre,
-                                             gBk_part, gCk_part, ga_part, gD_part, gb_part, B, L, D, N, st);
+            return s6::bwd_f64(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in, gu_local, gpre, gBk_part,
+                               gCk_part, ga_part, gD_part, gb_part, h_out, B, L, D, N, st);
     }
     set_error("s6: unsupported io dtype %d", io_dtype);
     return LRX_ERR_VALUE;

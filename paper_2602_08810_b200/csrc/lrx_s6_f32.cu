@@ -4,15 +4,13 @@
 namespace lrx {
 namespace s6 {
 
-int fwd_f32(const void* u, const void* pre, const void* bd, const void* al, const void* Bk, const void* Ck,
-            const void* Dk, void* y, void* ckpt, int64_t B, int64_t L, int64_t D, int64_t N, cudaStream_t st) {
-    return fwd_t<float, float>(u, pre, bd, al, Bk, Ck, Dk, y, ckpt, B, L, D, N, st);
+int fwd_f32(LRX_S6_FWD_PARAMS) {
+    return fwd_t<float, float>(u, pre, bd, al, Bk, Ck, Dk, x0, y, ckpt, B, L, D, N, st);
 }
 
-int bwd_f32(const void* u, const void* pre, const void* bd, const void* al, const void* Bk, const void* Ck,
-            const void* Dk, const void* ckpt, const void* gy, void* gu, void* gpre, void* gBp, void* gCp, void* gap,
-            void* gDp, void* gbp, int64_t B, int64_t L, int64_t D, int64_t N, cudaStream_t st) {
-    return bwd_t<float, float>(u, pre, bd, al, Bk, Ck, Dk, ckpt, gy, gu, gpre, gBp, gCp, gap, gDp, gbp, B, L, D, N, st);
+int bwd_f32(LRX_S6_BWD_PARAMS) {
+    return bwd_t<float, float>(u, pre, bd, al, Bk, Ck, Dk, ckpt, gy, h_in, gu, gpre, gBp, gCp, gap, gDp, gbp, h_out, B, L,
+                            D, N, st);
 }
 
 }  // namespace s6

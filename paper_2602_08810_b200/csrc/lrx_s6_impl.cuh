@@ -27,6 +27,7 @@
 // per value), across the CTA's warps in shared memory, and across CTAs as
 // per-channel-block partials reduced in a fixed order (deterministic).
 #pragma once
+#include <stdlib.h>
 #include "lrx_common.cuh"
 #include "lrx_host.h"
 
@@ -61,8 +62,8 @@ template <> struct Exp<false> {
 template <typename IO, typename C, int NS>
 __global__ void __launch_bounds__(Cfg<C, NS>::THREADS) fwd_kernel(
     const IO* __restrict__ u, const C* __restrict__ pre, const C* __restrict__ bdelta, const C* __restrict__ a_log,
-    const C* __restrict__ Bk, const C* __restrict__ Ck, const C* __restrict__ Dskip, IO* __restrict__ y,
-    C* __restrict__ ckpt, int64_t L, int64_t D, int N, int n_ck) {
+    const C* __restrict__ Bk, const C* __restrict__ Ck, const C* __restrict__ Dskip, const C* __restrict__ x0,
+    IO* __restrict__ y, C* __restrict__ ckpt, int64_t L, int64_t D, int N, int n_ck) {
     using CF = Cfg<C, NS>;
     using E = Exp<sizeof(IO) == 2>;
     using M = Math<C>;
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(Cfg<C, NS>::THREADS) fwd_kernel(
 #pragma unroll
     for (int n = 0; n < NS; ++n) {
         a[n] = (valid && n < N) ? -M::exp(a_log[d * N + n]) : C(0);
-        x[n] = C(0);
+        x[n] = (x0 && valid && n < N) ? x0[((int64_t)b * D + d) * N + n] : C(0);
     }
     const C bd = valid ? bdelta[d] : C(0), Dd = valid ? Dskip[d] : C(0);
     for (int64_t t0 = 0; t0 < L; t0 += kTT) {
@@ -168,9 +169,9 @@ template <typename IO, typename C, int NS>
 __global__ void __launch_bounds__(Cfg<C, NS>::THREADS) bwd_kernel(
     const IO* __restrict__ u, const C* __restrict__ pre, const C* __restrict__ bdelta, const C* __restrict__ a_log,
     const C* __restrict__ Bk, const C* __restrict__ Ck, const C* __restrict__ Dskip, const C* __restrict__ ckpt,
-    const IO* __restrict__ gy, IO* __restrict__ gu, C* __restrict__ gpre, C* __restrict__ gB_part,
-    C* __restrict__ gC_part, C* __restrict__ ga_part, C* __restrict__ gD_part, C* __restrict__ gb_part, int64_t B,
-    int64_t L, int64_t D, int N, int n_ck) {
+    const IO* __restrict__ gy, const C* __restrict__ h_in, IO* __restrict__ gu, C* __restrict__ gpre,
+    C* __restrict__ gB_part, C* __restrict__ gC_part, C* __restrict__ ga_part, C* __restrict__ gD_part,
+    C* __restrict__ gb_part, C* __restrict__ h_out, int64_t B, int64_t L, int64_t D, int N, int n_ck) {
     using CF = Cfg<C, NS>;
     using E = Exp<sizeof(IO) == 2>;
     using M = Math<C>;
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(Cfg<C, NS>::THREADS) bwd_kernel(
 #pragma unroll
     for (int n = 0; n < NS; ++n) {
         a[n] = (valid && n < N) ? -M::exp(a_log[d * N + n]) : C(0);
-        h[n] = C(0);
+        h[n] = (h_in && valid && n < N) ? h_in[((int64_t)b * D + d) * N + n] : C(0);
         gacc[n] = C(0);
     }
     const C bd = valid ? bdelta[d] : C(0), Dd = valid ? Dskip[d] : C(0);
@@ -323,6 +324,349 @@ __global__ void __launch_bounds__(Cfg<C, NS>::THREADS) bwd_kernel(
             if (n < N) ga_part[((int64_t)b * D + d) * N + n] = a[n] * gacc[n];
         gD_part[(int64_t)b * D + d] = gD_acc;
         gb_part[(int64_t)b * D + d] = gb_acc;
+        if (h_out) {
+#pragma unroll
+            for (int n = 0; n < NS; ++n)
+                if (n < N) h_out[((int64_t)b * D + d) * N + n] = h[n];
+        }
+    }
+}
+
+// ============================================================================
+// v2 (fp32 compute, d_state 16 / 32): TPC = 4 threads per channel, NPT states
+// each.  4x the warps of the thread-per-channel mapping (C3 has only
+// B*D = 24576 channels), softplus once per channel-step shared by shuffle,
+// MUFU ex2 discretisation with a*log2(e) folded in, pairwise readout.
+template <int NST>
+struct V2 {
+    static constexpr int TPC = 4;
+    static constexpr int NPT = NST / TPC;
+    static constexpr int FWD_T = 128;                 // threads per forward CTA
+    static constexpr int BWD_T = 256;                 // = Cfg<float,NST>::THREADS channels * TPC
+    static constexpr int CK = Cfg<float, NST>::CK;
+    static constexpr int SUB = Cfg<float, NST>::SUB;
+    static constexpr int NSUB = CK / SUB;
+    static constexpr int NV = 2 * NPT;                // dB/dC values per thread per step
+    static constexpr size_t smem_bwd() {
+        return sizeof(float) * ((size_t)NSUB * NPT * BWD_T + (size_t)SUB * NPT * BWD_T + 2 * (size_t)SUB * NST +
+                                (size_t)SUB * (BWD_T / 32) * TPC * NV);
+    }
+};
+static_assert(V2<16>::BWD_T / V2<16>::TPC == Cfg<float, 16>::THREADS, "v2/v1 channel blocks must match");
+static_assert(V2<32>::BWD_T / V2<32>::TPC == Cfg<float, 32>::THREADS, "v2/v1 channel blocks must match");
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// softplus for the compute path: x > 30 -> x; small e = e^x uses the series
+// of log1p so delta keeps full relative precision (numerics.py:86-94).
+__device__ __forceinline__ float softplus_fast(float x) {
+    const float e = Fast<float>::ex2(fminf(x, 30.f) * kLog2e);
+    const float lg = __log2f(1.f + e) * 0.6931471805599453f;
+    const float ser = e * (1.f - e * (0.5f - e * (1.f / 3.f)));
+    return x > 30.f ? x : (e < 1e-2f ? ser : lg);
+}
+
+// Transpose-reduction of NV values over the 8 lanes that share lane bits
+// outside [2, 5) (the 8 channels of one state group in a warp).  On return
+// v[chunk] holds, for value index chunk*8 + ((lane >> 2) & 7), the 8-lane sum.
+template <int NV>
+__device__ __forceinline__ void tr_reduce8(float* v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int c = 0; c < NV; c += 8) {
+#pragma unroll
+        for (int m = 4; m >= 1; m >>= 1) {
+            const bool up = (lane >> 2) & m;
+#pragma unroll
+            for (int i = 0; i < m; ++i) {
+                const float send = up ? v[c + i] : v[c + i + m];
+                const float keep = up ? v[c + i + m] : v[c + i];
+                v[c + i] = keep + __shfl_xor_sync(0xffffffffu, send, m << 2);
+            }
+        }
+        v[c / 8] = v[c];
+    }
+}
+
+template <typename IO, int NST>
+__global__ void __launch_bounds__(V2<NST>::FWD_T) fwd_v2_kernel(
+    const IO* __restrict__ u, const float* __restrict__ pre, const float* __restrict__ bdelta,
+    const float* __restrict__ a_log, const float* __restrict__ Bk, const float* __restrict__ Ck,
+    const float* __restrict__ Dskip, const float* __restrict__ x0, IO* __restrict__ y, float* __restrict__ ckpt,
+    int64_t L, int64_t D, int N, int n_ck) {
+    using G = V2<NST>;
+    constexpr int TPC = G::TPC, NPT = G::NPT, CPB = G::FWD_T / TPC;
+    __shared__ float sB[kTT][NST], sC[kTT][NST];
+    const int tid = threadIdx.x, lane = tid & 31, q = tid % TPC;
+    const int b = blockIdx.y;
+    const int64_t d = (int64_t)blockIdx.x * CPB + tid / TPC;
+    const bool valid = d < D;
+    const int n0 = q * NPT;
+    float a2[NPT], x[NPT];
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        const int n = n0 + j;
+        a2[j] = (valid && n < N) ? -__expf(a_log[d * N + n]) * kLog2e : 0.f;
+        x[j] = (x0 && valid && n < N) ? x0[((int64_t)b * D + d) * N + n] : 0.f;
+    }
+    const float bd = valid ? bdelta[d] : 0.f, Dd = valid ? Dskip[d] : 0.f;
+    const int gbase = lane & ~(TPC - 1);
+    for (int64_t t0 = 0; t0 < L; t0 += kTT) {
+        const int nt = (int)min((int64_t)kTT, L - t0);
+        __syncthreads();
+        for (int i = tid; i < kTT * NST; i += G::FWD_T) {
+            const int k = i / NST, n = i % NST;
+            const bool ok = k < nt && n < N;
+            const int64_t off = ((int64_t)b * L + t0 + k) * N + n;
+            sB[k][n] = ok ? Bk[off] : 0.f;
+            sC[k][n] = ok ? Ck[off] : 0.f;
+        }
+        __syncthreads();
+        IO uu[kTT];
+        float dl_own[kTT / TPC];
+#pragma unroll
+        for (int k = 0; k < kTT; ++k) {
+            const bool ok = valid && k < nt;
+            uu[k] = ok ? u[((int64_t)b * L + t0 + k) * D + d] : IO(0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < kTT / TPC; ++kk) {
+            const int k = kk * TPC + q;
+            const bool ok = valid && k < nt;
+            const float p = ok ? pre[((int64_t)b * L + t0 + k) * D + d] : 0.f;
+            dl_own[kk] = softplus_fast(p + bd);
+        }
+#pragma unroll
+        for (int k = 0; k < kTT; ++k) {
+            const float delta = __shfl_sync(0xffffffffu, dl_own[k / TPC], gbase | (k % TPC));
+            if (k < nt) {
+                const int64_t t = t0 + k;
+                if (valid && (t % G::CK) == 0) {
+                    float* cp = ckpt + (((int64_t)b * (n_ck + 1) + t / G::CK) * D + d) * N + n0;
+#pragma unroll
+                    for (int j = 0; j < NPT; ++j)
+                        if (n0 + j < N) cp[j] = x[j];
+                }
+                const float uk = cvt(uu[k]);
+                const float du = delta * uk;
+                float yp[NPT];
+#pragma unroll
+                for (int j = 0; j < NPT; ++j) {
+                    const float ab = Fast<float>::ex2(delta * a2[j]);
+                    x[j] = fmaf(ab, x[j], du * sB[k][n0 + j]);
+                    yp[j] = x[j] * sC[k][n0 + j];
+                }
+#pragma unroll
+                for (int w2 = NPT / 2; w2 >= 1; w2 >>= 1)
+#pragma unroll
+                    for (int j = 0; j < w2; ++j) yp[j] += yp[j + w2];
+                float yv = yp[0];
+                yv += __shfl_xor_sync(0xffffffffu, yv, 1);
+                yv += __shfl_xor_sync(0xffffffffu, yv, 2);
+                if (valid && q == 0) st_io(y + ((int64_t)b * L + t) * D + d, yv + Dd * uk);
+            }
+        }
+    }
+    if (valid) {
+        float* cp = ckpt + (((int64_t)b * (n_ck + 1) + n_ck) * D + d) * N + n0;
+#pragma unroll
+        for (int j = 0; j < NPT; ++j)
+            if (n0 + j < N) cp[j] = x[j];
+    }
+}
+
+template <typename IO, int NST>
+__global__ void __launch_bounds__(V2<NST>::BWD_T) bwd_v2_kernel(
+    const IO* __restrict__ u, const float* __restrict__ pre, const float* __restrict__ bdelta,
+    const float* __restrict__ a_log, const float* __restrict__ Bk, const float* __restrict__ Ck,
+    const float* __restrict__ Dskip, const float* __restrict__ ckpt, const IO* __restrict__ gy,
+    const float* __restrict__ h_in, IO* __restrict__ gu, float* __restrict__ gpre, float* __restrict__ gB_part,
+    float* __restrict__ gC_part, float* __restrict__ ga_part, float* __restrict__ gD_part,
+    float* __restrict__ gb_part, float* __restrict__ h_out, int64_t B, int64_t L, int64_t D, int N, int n_ck) {
+    using G = V2<NST>;
+    constexpr int TH = G::BWD_T, TPC = G::TPC, NPT = G::NPT, SUB = G::SUB, NV = G::NV, WARPS = TH / 32;
+    constexpr int CPB = TH / TPC;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* subx = reinterpret_cast<float*>(smem_raw);             // [NSUB][NPT][TH]
+    float* xs = subx + (size_t)G::NSUB * NPT * TH;                // [SUB][NPT][TH]
+    float* sB = xs + (size_t)SUB * NPT * TH;                      // [SUB][NST]
+    float* sC = sB + (size_t)SUB * NST;                           // [SUB][NST]
+    float* red = sC + (size_t)SUB * NST;                          // [SUB][WARPS][TPC*NV]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q = tid % TPC;
+    const int b = blockIdx.y;
+    const int64_t d = (int64_t)blockIdx.x * CPB + tid / TPC;
+    const bool valid = d < D;
+    const int n0 = q * NPT;
+    const int gbase = lane & ~(TPC - 1);
+    float a[NPT], a2[NPT], h[NPT], gacc[NPT];
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        const int n = n0 + j;
+        a[j] = (valid && n < N) ? -__expf(a_log[d * N + n]) : 0.f;
+        a2[j] = a[j] * kLog2e;
+        h[j] = (h_in && valid && n < N) ? h_in[((int64_t)b * D + d) * N + n] : 0.f;
+        gacc[j] = 0.f;
+    }
+    const float bd = valid ? bdelta[d] : 0.f, Dd = valid ? Dskip[d] : 0.f;
+    float gD_acc = 0.f, gb_acc = 0.f;
+
+    // delta for step t (shared by the TPC lanes of a channel): lane q computes
+    // the steps k with k % TPC == q of a SUB block
+    auto deltas = [&](int64_t ts0, int nts, float* dl_own) {
+#pragma unroll
+        for (int kk = 0; kk < SUB / TPC; ++kk) {
+            const int k = kk * TPC + q;
+            const bool ok = valid && k < nts;
+            const float p = ok ? pre[((int64_t)b * L + ts0 + k) * D + d] : 0.f;
+            dl_own[kk] = softplus_fast(p + bd);
+        }
+    };
+
+    for (int ci = n_ck - 1; ci >= 0; --ci) {
+        const int64_t tc0 = (int64_t)ci * G::CK;
+        const int ncs = (int)min((int64_t)G::CK, L - tc0);
+        const int nsub = (ncs + SUB - 1) / SUB;
+        float x[NPT];
+        {
+            const float* cp = ckpt + (((int64_t)b * (n_ck + 1) + ci) * D + (valid ? d : 0)) * N + n0;
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) x[j] = (valid && n0 + j < N) ? cp[j] : 0.f;
+        }
+        // pass 1: chunk forward, keep the state entering every SUB block
+        for (int jb = 0; jb < nsub; ++jb) {
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) subx[((size_t)jb * NPT + j) * TH + tid] = x[j];
+            const int64_t ts0 = tc0 + (int64_t)jb * SUB;
+            const int nts = (int)min((int64_t)SUB, L - ts0);
+            float dl_own[SUB / TPC];
+            deltas(ts0, nts, dl_own);
+#pragma unroll
+            for (int k = 0; k < SUB; ++k) {
+                const float delta = __shfl_sync(0xffffffffu, dl_own[k / TPC], gbase | (k % TPC));
+                if (k < nts) {
+                    const int64_t t = ts0 + k;
+                    const float uk = valid ? float(cvt(u[((int64_t)b * L + t) * D + d])) : 0.f;
+                    const float du = delta * uk;
+                    const float* brow = Bk + ((int64_t)b * L + t) * N + n0;
+#pragma unroll
+                    for (int j = 0; j < NPT; ++j) {
+                        const float bn = n0 + j < N ? brow[j] : 0.f;
+                        x[j] = fmaf(Fast<float>::ex2(delta * a2[j]), x[j], du * bn);
+                    }
+                }
+            }
+        }
+        // pass 2: SUB blocks right-to-left
+        for (int jb = nsub - 1; jb >= 0; --jb) {
+            const int64_t ts0 = tc0 + (int64_t)jb * SUB;
+            const int nts = (int)min((int64_t)SUB, L - ts0);
+            __syncthreads();
+            for (int i = tid; i < SUB * NST; i += TH) {
+                const int k = i / NST, n = i % NST;
+                const bool ok = k < nts && n < N;
+                const int64_t off = ((int64_t)b * L + ts0 + k) * N + n;
+                sB[i] = ok ? Bk[off] : 0.f;
+                sC[i] = ok ? Ck[off] : 0.f;
+            }
+            __syncthreads();
+            float dl_own[SUB / TPC], uk[SUB], gk[SUB];
+            deltas(ts0, nts, dl_own);
+#pragma unroll
+            for (int j = 0; j < NPT; ++j) x[j] = subx[((size_t)jb * NPT + j) * TH + tid];
+#pragma unroll
+            for (int k = 0; k < SUB; ++k) {
+                const bool ok = valid && k < nts;
+                const int64_t off = ((int64_t)b * L + ts0 + k) * D + d;
+                uk[k] = ok ? float(cvt(u[off])) : 0.f;
+                gk[k] = ok ? float(cvt(gy[off])) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < SUB; ++k) {
+                const float delta = __shfl_sync(0xffffffffu, dl_own[k / TPC], gbase | (k % TPC));
+                if (k < nts) {
+                    const float du = delta * uk[k];
+#pragma unroll
+                    for (int j = 0; j < NPT; ++j) {
+                        xs[((size_t)k * NPT + j) * TH + tid] = x[j];
+                        x[j] = fmaf(Fast<float>::ex2(delta * a2[j]), x[j], du * sB[k * NST + n0 + j]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = SUB - 1; k >= 0; --k) {
+                const float delta = __shfl_sync(0xffffffffu, dl_own[k / TPC], gbase | (k % TPC));
+                if (k < nts) {
+                    const float du = delta * uk[k];
+                    float sa = 0.f, sb = 0.f;
+                    float cv[NV];
+#pragma unroll
+                    for (int j = 0; j < NPT; ++j) {
+                        const float ab = Fast<float>::ex2(delta * a2[j]);
+                        const float xp = xs[((size_t)k * NPT + j) * TH + tid];
+                        const float bn = sB[k * NST + n0 + j], cn = sC[k * NST + n0 + j];
+                        const float g = fmaf(gk[k], cn, h[j]);
+                        const float term = ab * (g * xp);
+                        sa = fmaf(term, a[j], sa);
+                        gacc[j] = fmaf(term, delta, gacc[j]);
+                        sb = fmaf(g, bn, sb);
+                        cv[j] = g * du;
+                        cv[NPT + j] = gk[k] * fmaf(ab, xp, du * bn);
+                        h[j] = ab * g;
+                    }
+                    sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+                    sb += __shfl_xor_sync(0xffffffffu, sb, 1);
+                    sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+                    sb += __shfl_xor_sync(0xffffffffu, sb, 2);
+                    if (valid && q == 0) {
+                        const float p = pre[((int64_t)b * L + ts0 + k) * D + d] + bd;
+                        const float gp = Fast<float>::sigmoid(p) * fmaf(sb, uk[k], sa);
+                        const int64_t off = ((int64_t)b * L + ts0 + k) * D + d;
+                        st_io(gu + off, fmaf(Dd, gk[k], delta * sb));
+                        gpre[off] = gp;
+                        gD_acc = fmaf(gk[k], uk[k], gD_acc);
+                        gb_acc += gp;
+                    }
+                    if (!valid) {
+#pragma unroll
+                        for (int i = 0; i < NV; ++i) cv[i] = 0.f;
+                    }
+                    tr_reduce8<NV>(cv);
+                    const int c = (lane >> 2) & 7;
+#pragma unroll
+                    for (int ch = 0; ch < NV / 8; ++ch)
+                        red[((size_t)k * WARPS + warp) * (TPC * NV) + q * NV + ch * 8 + c] = cv[ch];
+                }
+            }
+            __syncthreads();
+            const int64_t dblk = blockIdx.x;
+            for (int i = tid; i < nts * TPC * NV; i += TH) {
+                const int k = i / (TPC * NV), r = i % (TPC * NV);
+                float sum = 0.f;
+#pragma unroll
+                for (int w = 0; w < WARPS; ++w) sum += red[((size_t)k * WARPS + w) * (TPC * NV) + r];
+                const int qq = r / NV, v = r % NV;
+                const int n = qq * NPT + (v < NPT ? v : v - NPT);
+                if (n < N) {
+                    float* dst = v < NPT ? gB_part : gC_part;
+                    dst[((dblk * B + b) * L + ts0 + k) * N + n] = sum;
+                }
+            }
+        }
+    }
+    if (valid) {
+#pragma unroll
+        for (int j = 0; j < NPT; ++j)
+            if (n0 + j < N) ga_part[((int64_t)b * D + d) * N + n0 + j] = a[j] * gacc[j];
+        if (q == 0) {
+            gD_part[(int64_t)b * D + d] = gD_acc;
+            gb_part[(int64_t)b * D + d] = gb_acc;
+        }
+        if (h_out) {  // carry to the left of step 0: abar_0 g_0 (= d loss / d x0)
+#pragma unroll
+            for (int j = 0; j < NPT; ++j)
+                if (n0 + j < N) h_out[((int64_t)b * D + d) * N + n0 + j] = h[j];
+        }
     }
 }
 
@@ -357,22 +701,51 @@ static int geom_rt(int64_t L, int64_t D, int64_t N, int* ck, int* n_ck, int* n_d
 
 template <typename IO, typename C, int NS>
 static int fwd_launch(const void* u, const void* pre, const void* bd, const void* al, const void* Bk, const void* Ck,
-                      const void* Dk, void* y, void* ckpt, int64_t B, int64_t L, int64_t D, int64_t N,
-                      cudaStream_t st) {
+                      const void* Dk, const void* x0, void* y, void* ckpt, int64_t B, int64_t L, int64_t D,
+                      int64_t N, cudaStream_t st) {
     using CF = Cfg<C, NS>;
+    if constexpr (sizeof(C) == 4 && (NS == 16 || NS == 32)) {
+        if (!getenv("LRX_S6_V1")) {
+            using G = V2<NS>;
+            const dim3 grid((unsigned)cdiv(D, G::FWD_T / G::TPC), (unsigned)B);
+            fwd_v2_kernel<IO, NS><<<grid, G::FWD_T, 0, st>>>((const IO*)u, (const float*)pre, (const float*)bd,
+                                                              (const float*)al, (const float*)Bk, (const float*)Ck,
+                                                              (const float*)Dk, (const float*)x0, (IO*)y,
+                                                              (float*)ckpt, L, D, (int)N, (int)cdiv(L, G::CK));
+            return launched("lrx_s6_fwd/v2");
+        }
+    }
     const dim3 grid((unsigned)cdiv(D, CF::THREADS), (unsigned)B);
     fwd_kernel<IO, C, NS><<<grid, CF::THREADS, 0, st>>>((const IO*)u, (const C*)pre, (const C*)bd, (const C*)al,
-                                                        (const C*)Bk, (const C*)Ck, (const C*)Dk, (IO*)y,
-                                                        (C*)ckpt, L, D, (int)N, (int)cdiv(L, CF::CK));
+                                                        (const C*)Bk, (const C*)Ck, (const C*)Dk, (const C*)x0,
+                                                        (IO*)y, (C*)ckpt, L, D, (int)N, (int)cdiv(L, CF::CK));
     return launched("lrx_s6_fwd");
 }
 
 template <typename IO, typename C, int NS>
 static int bwd_launch(const void* u, const void* pre, const void* bd, const void* al, const void* Bk, const void* Ck,
-                      const void* Dk, const void* ckpt, const void* gy, void* gu, void* gpre, void* gBp, void* gCp,
-                      void* gap, void* gDp, void* gbp, int64_t B, int64_t L, int64_t D, int64_t N,
-                      cudaStream_t st) {
+                      const void* Dk, const void* ckpt, const void* gy, const void* h_in, void* gu, void* gpre,
+                      void* gBp, void* gCp, void* gap, void* gDp, void* gbp, void* h_out, int64_t B, int64_t L,
+                      int64_t D, int64_t N, cudaStream_t st) {
     using CF = Cfg<C, NS>;
+    if constexpr (sizeof(C) == 4 && (NS == 16 || NS == 32)) {
+        if (!getenv("LRX_S6_V1")) {
+            using G = V2<NS>;
+            const size_t smem2 = G::smem_bwd();
+            auto k2 = bwd_v2_kernel<IO, NS>;
+            if (cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2) != cudaSuccess) {
+                set_error("s6 bwd: cannot reserve %zu bytes of shared memory", smem2);
+                return LRX_ERR_CUDA;
+            }
+            const dim3 grid((unsigned)cdiv(D, G::BWD_T / G::TPC), (unsigned)B);
+            k2<<<grid, G::BWD_T, smem2, st>>>((const IO*)u, (const float*)pre, (const float*)bd, (const float*)al,
+                                              (const float*)Bk, (const float*)Ck, (const float*)Dk,
+                                              (const float*)ckpt, (const IO*)gy, (const float*)h_in, (IO*)gu,
+                                              (float*)gpre, (float*)gBp, (float*)gCp, (float*)gap, (float*)gDp,
+                                              (float*)gbp, (float*)h_out, B, L, D, (int)N, (int)cdiv(L, G::CK));
+            return launched("lrx_s6_bwd/v2");
+        }
+    }
     const size_t smem = CF::smem_bwd();
     auto kfn = bwd_kernel<IO, C, NS>;
     if (smem > 48 * 1024) {
@@ -383,9 +756,9 @@ static int bwd_launch(const void* u, const void* pre, const void* bd, const void
     }
     const dim3 grid((unsigned)cdiv(D, CF::THREADS), (unsigned)B);
     kfn<<<grid, CF::THREADS, smem, st>>>((const IO*)u, (const C*)pre, (const C*)bd, (const C*)al, (const C*)Bk,
-                                         (const C*)Ck, (const C*)Dk, (const C*)ckpt, (const IO*)gy, (IO*)gu,
-                                         (C*)gpre, (C*)gBp, (C*)gCp, (C*)gap, (C*)gDp, (C*)gbp, B, L, D, (int)N,
-                                         (int)cdiv(L, CF::CK));
+                                         (const C*)Ck, (const C*)Dk, (const C*)ckpt, (const IO*)gy,
+                                         (const C*)h_in, (IO*)gu, (C*)gpre, (C*)gBp, (C*)gCp, (C*)gap, (C*)gDp,
+                                         (C*)gbp, (C*)h_out, B, L, D, (int)N, (int)cdiv(L, CF::CK));
     return launched("lrx_s6_bwd");
 }
 
@@ -400,34 +773,32 @@ static int bwd_launch(const void* u, const void* pre, const void* bd, const void
             return LRX_ERR_UNSUPPORTED;                                          \
     }
 
+#define LRX_S6_FWD_PARAMS const void* u, const void* pre, const void* bd, const void* al, const void* Bk, \
+    const void* Ck, const void* Dk, const void* x0, void* y, void* ckpt, int64_t B, int64_t L, int64_t D,  \
+    int64_t N, cudaStream_t st
+#define LRX_S6_BWD_PARAMS const void* u, const void* pre, const void* bd, const void* al, const void* Bk, \
+    const void* Ck, const void* Dk, const void* ckpt, const void* gy, const void* h_in, void* gu, void* gpre, \
+    void* gBp, void* gCp, void* gap, void* gDp, void* gbp, void* h_out, int64_t B, int64_t L, int64_t D,   \
+    int64_t N, cudaStream_t st
+
 template <typename IO, typename C>
-static int fwd_t(const void* u, const void* pre, const void* bd, const void* al, const void* Bk, const void* Ck,
-                 const void* Dk, void* y, void* ckpt, int64_t B, int64_t L, int64_t D, int64_t N, cudaStream_t st) {
-    S6_NS_SWITCH(C, N, (fwd_launch<IO, C, NS>(u, pre, bd, al, Bk, Ck, Dk, y, ckpt, B, L, D, N, st)))
+static int fwd_t(LRX_S6_FWD_PARAMS) {
+    S6_NS_SWITCH(C, N, (fwd_launch<IO, C, NS>(u, pre, bd, al, Bk, Ck, Dk, x0, y, ckpt, B, L, D, N, st)))
 }
 
 template <typename IO, typename C>
-static int bwd_t(const void* u, const void* pre, const void* bd, const void* al, const void* Bk, const void* Ck,
-                 const void* Dk, const void* ckpt, const void* gy, void* gu, void* gpre, void* gBp, void* gCp,
-                 void* gap, void* gDp, void* gbp, int64_t B, int64_t L, int64_t D, int64_t N, cudaStream_t st) {
-    S6_NS_SWITCH(C, N,
-                 (bwd_launch<IO, C, NS>(u, pre, bd, al, Bk, Ck, Dk, ckpt, gy, gu, gpre, gBp, gCp, gap, gDp, gbp, B,
-                                        L, D, N, st)))
+static int bwd_t(LRX_S6_BWD_PARAMS) {
+    S6_NS_SWITCH(C, N, (bwd_launch<IO, C, NS>(u, pre, bd, al, Bk, Ck, Dk, ckpt, gy, h_in, gu, gpre, gBp, gCp, gap,
+                                              gDp, gbp, h_out, B, L, D, N, st)))
 }
 
 // per-I/O-dtype entry points, each compiled in its own translation unit
-int fwd_f32(const void*, const void*, const void*, const void*, const void*, const void*, const void*, void*, void*,
-            int64_t, int64_t, int64_t, int64_t, cudaStream_t);
-int fwd_bf16(const void*, const void*, const void*, const void*, const void*, const void*, const void*, void*, void*,
-             int64_t, int64_t, int64_t, int64_t, cudaStream_t);
-int fwd_f64(const void*, const void*, const void*, const void*, const void*, const void*, const void*, void*, void*,
-            int64_t, int64_t, int64_t, int64_t, cudaStream_t);
-#define LRX_S6_BWD_ARGS const void*, const void*, const void*, const void*, const void*, const void*, const void*, \
-    const void*, const void*, void*, void*, void*, void*, void*, void*, void*, int64_t, int64_t, int64_t, int64_t, \
-    cudaStream_t
-int bwd_f32(LRX_S6_BWD_ARGS);
-int bwd_bf16(LRX_S6_BWD_ARGS);
-int bwd_f64(LRX_S6_BWD_ARGS);
+int fwd_f32(LRX_S6_FWD_PARAMS);
+int fwd_bf16(LRX_S6_FWD_PARAMS);
+int fwd_f64(LRX_S6_FWD_PARAMS);
+int bwd_f32(LRX_S6_BWD_PARAMS);
+int bwd_bf16(LRX_S6_BWD_PARAMS);
+int bwd_f64(LRX_S6_BWD_PARAMS);
 
 }  // namespace s6
 }  // namespace lrx

@@ -78,8 +78,9 @@ def s6_geometry(io_dtype, L, D, N):
     return ck.value, nck.value, ndb.value
 
 
-def s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip):
-    """Selective scan; u/pre [B, L, D], Bk/Ck [B, L, N] (same dtype as u).
+def s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=None):
+    """Selective scan; u [B, L, D] (f32/f64/bf16), pre [B, L, D] and Bk/Ck
+    [B, L, N] in compute precision.  x0 [B, D, N] optionally seeds the state.
     Returns (y, ckpt); ckpt[:, -1] is the final state [B, D, N]."""
     B, L, D = u.shape
     N = Bk.shape[-1]
@@ -87,14 +88,16 @@ def s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip):
     y = torch.empty_like(u)
     ckpt = torch.empty((B, nck, D, N), dtype=a_log.dtype, device=u.device)
     _lib.check(_lib.lib().lrx_s6_fwd(_lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(pre), _lib.ptr(b_delta),
-                                     _lib.ptr(a_log), _lib.ptr(Bk), _lib.ptr(Ck), _lib.ptr(Dskip), _lib.ptr(y),
-                                     _lib.ptr(ckpt), B, L, D, N, _lib.stream()))
+                                     _lib.ptr(a_log), _lib.ptr(Bk), _lib.ptr(Ck), _lib.ptr(Dskip), _lib.ptr(x0),
+                                     _lib.ptr(y), _lib.ptr(ckpt), B, L, D, N, _lib.stream()))
     return y, ckpt
 
 
-def s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy):
+def s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in=None, want_h_out=False):
     """Pullback of s6_scan_fwd.  Returns dict: gu_local (D gy + delta sum_n g B),
-    gpre (d/d pre) [B, L, D]; gBk, gCk [B, L, N]; ga_log [D, N]; gD, gb_delta [D]."""
+    gpre (d/d pre) [B, L, D]; gBk, gCk [B, L, N]; ga_log [D, N]; gD, gb_delta [D];
+    with want_h_out also h_out [B, D, N] = d loss / d x0.  h_in [B, D, N] is
+    the cotangent carry entering from the right (sequence-parallel mode)."""
     B, L, D = u.shape
     N = Bk.shape[-1]
     _, nck, ndb = s6_geometry(u.dtype, L, D, N)
@@ -102,15 +105,20 @@ def s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy):
     gu, gpre = torch.empty_like(u), torch.empty(u.shape, **f)
     gBp, gCp = torch.empty((ndb, B * L * N), **f), torch.empty((ndb, B * L * N), **f)
     gap, gDp, gbp = torch.empty((B, D * N), **f), torch.empty((B, D), **f), torch.empty((B, D), **f)
+    h_out = torch.empty((B, D, N), **f) if want_h_out else None
     _lib.check(_lib.lib().lrx_s6_bwd(
         _lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(pre), _lib.ptr(b_delta), _lib.ptr(a_log), _lib.ptr(Bk),
-        _lib.ptr(Ck), _lib.ptr(Dskip), _lib.ptr(ckpt), _lib.ptr(gy), _lib.ptr(gu), _lib.ptr(gpre), _lib.ptr(gBp),
-        _lib.ptr(gCp), _lib.ptr(gap), _lib.ptr(gDp), _lib.ptr(gbp), B, L, D, N, _lib.stream()))
-    return {"gu_local": gu, "gpre": gpre,
-            "gBk": reduce_rows(gBp, ndb, B * L * N).reshape(B, L, N),
-            "gCk": reduce_rows(gCp, ndb, B * L * N).reshape(B, L, N),
-            "ga_log": reduce_rows(gap, B, D * N).reshape(D, N),
-            "gD": reduce_rows(gDp, B, D), "gb_delta": reduce_rows(gbp, B, D)}
+        _lib.ptr(Ck), _lib.ptr(Dskip), _lib.ptr(ckpt), _lib.ptr(gy), _lib.ptr(h_in), _lib.ptr(gu), _lib.ptr(gpre),
+        _lib.ptr(gBp), _lib.ptr(gCp), _lib.ptr(gap), _lib.ptr(gDp), _lib.ptr(gbp), _lib.ptr(h_out), B, L, D, N,
+        _lib.stream()))
+    out = {"gu_local": gu, "gpre": gpre,
+           "gBk": reduce_rows(gBp, ndb, B * L * N).reshape(B, L, N),
+           "gCk": reduce_rows(gCp, ndb, B * L * N).reshape(B, L, N),
+           "ga_log": reduce_rows(gap, B, D * N).reshape(D, N),
+           "gD": reduce_rows(gDp, B, D), "gb_delta": reduce_rows(gbp, B, D)}
+    if want_h_out:
+        out["h_out"] = h_out
+    return out
 
 
 # ---------------------------------------------------------------------------

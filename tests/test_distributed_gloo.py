@@ -1,0 +1,177 @@
+"""Multi-process host logic on CPU (gloo, world size 2): batch sharding and the
+sequence-parallel carry exchange of paper_2602_08810_b200.distributed, with a
+test-only torch restatement of the S6 slice scan (x0 / h_in aware) standing in
+for the device kernels."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import port
+from paper_2602_08810_b200.distributed import SeqParallelS6, compose_prefix, compose_suffix, shard_range
+
+
+def test_shard_range_partitions():
+    for n in (1, 7, 64, 1000):
+        for world in (1, 2, 3, 8):
+            parts = [shard_range(n, world, r) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+            sizes = [e - s for s, e in parts]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_range(4, 2, 2)
+
+
+def test_carry_composition_matches_sequential():
+    rng = np.random.default_rng(0)
+    A = torch.tensor(rng.uniform(0.2, 1.0, (4, 3)))
+    X = torch.tensor(rng.normal(size=(4, 3)))
+    # sequential: x_{r+1} = A_r x_r + X_r from x_0 = 0
+    x = torch.zeros(3, dtype=torch.float64)
+    for r in range(4):
+        assert torch.allclose(compose_prefix(A, X, r), x)
+        x = A[r] * x + X[r]
+    h = torch.zeros(3, dtype=torch.float64)
+    for r in range(3, -1, -1):
+        assert torch.allclose(compose_suffix(A, X, r), h)
+        h = A[r] * h + X[r]
+
+
+# ---- test-only torch restatement of the S6 slice scan (layers.py:1038-1098) --
+
+def _fwd(u, pre, b_delta, a_log, Bk, Ck, D, x0=None):
+    a = -torch.exp(a_log)
+    delta = torch.nn.functional.softplus(pre + b_delta)
+    B, L, m = u.shape
+    x = torch.zeros((B, m, a.shape[1]), dtype=u.dtype) if x0 is None else x0.clone()
+    xs, ys = [], []
+    for t in range(L):
+        xs.append(x)
+        x = torch.exp(delta[:, t, :, None] * a) * x + (delta[:, t] * u[:, t])[..., None] * Bk[:, t, None, :]
+        ys.append((x * Ck[:, t, None, :]).sum(-1) + D * u[:, t])
+    ckpt = torch.stack(xs + [x], dim=1)          # every state + final (test layout)
+    return torch.stack(ys, 1), ckpt
+
+
+def _bwd(u, pre, b_delta, a_log, Bk, Ck, D, ckpt, gy, h_in=None, want_h_out=False):
+    a = -torch.exp(a_log)
+    pre_b = pre + b_delta
+    delta = torch.nn.functional.softplus(pre_b)
+    B, L, m = u.shape
+    h = torch.zeros_like(ckpt[:, 0]) if h_in is None else h_in.clone()
+    gu = torch.zeros_like(u)
+    gpre = torch.zeros_like(u)
+    ga = torch.zeros_like(a)
+    for t in range(L - 1, -1, -1):
+        ab = torch.exp(delta[:, t, :, None] * a)
+        g = gy[:, t, :, None] * Ck[:, t, None, :] + h
+        term = ab * g * ckpt[:, t]
+        s1 = (g * Bk[:, t, None, :]).sum(-1)
+        gdelta = (term * a).sum(-1) + s1 * u[:, t]
+        gpre[:, t] = torch.sigmoid(pre_b[:, t]) * gdelta
+        gu[:, t] = gy[:, t] * D + delta[:, t] * s1
+        ga += (term * delta[:, t, :, None]).sum(0)
+        h = ab * g
+    out = {"gu_local": gu, "gpre": gpre, "ga_log": a * ga}
+    if want_h_out:
+        out["h_out"] = h
+    return out
+
+
+def _problem(L=24, m=3, n=4):
+    p = port.init_params("s6", m, n, seed=3)
+    rng = port.Rng(7)
+    u = rng.normal((1, L, m))
+    pre = (u @ p["W_delta"]) @ p["W_delta_proj"]
+    T = lambda x: torch.tensor(np.asarray(x))
+    return dict(u=T(u), pre=T(pre), b_delta=T(p["b_delta"]), a_log=T(p["a_log"]), Bk=T(u @ p["W_B"].T),
+                Ck=T(u @ p["W_C"].T), D=T(p["D"]), gy=T(rng.normal((1, L, m)))), p, u, pre
+
+
+def _worker(rank, world, port_no, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pb, p, u, pre = _problem()
+        s, e = shard_range(pb["u"].shape[1], world, rank)
+        sl = {k: (v[:, s:e].contiguous() if k in ("u", "pre", "Bk", "Ck", "gy") else v) for k, v in pb.items()}
+        sp = SeqParallelS6(scan_fwd=_fwd, scan_bwd=_bwd)
+        args = (sl["u"], sl["pre"], sl["b_delta"], sl["a_log"], sl["Bk"], sl["Ck"], sl["D"])
+        y, ctx = sp.forward(*args)
+        r = sp.backward(ctx, *args, sl["gy"])
+        ga = r["ga_log"].clone()
+        dist.all_reduce(ga)  # parameter grads sum over ranks
+        q.put((rank, y.numpy(), r["gu_local"].numpy(), r["gpre"].numpy(), ga.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sequence_parallel_exchange_gloo():
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port_no = sck.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port_no, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    pb, p, u, pre = _problem()
+    y_ref, o = port.s6_scan(u, pre, p["b_delta"], p["a_log"], u @ p["W_B"].T, u @ p["W_C"].T, p["D"],
+                            pb["gy"].numpy())
+    y = np.concatenate([r[1] for r in res], axis=1)
+    gu = np.concatenate([r[2] for r in res], axis=1)
+    gpre = np.concatenate([r[3] for r in res], axis=1)
+    assert port.rel_err(y, y_ref) < 1e-12
+    assert port.rel_err(gu, o["gu_local"]) < 1e-12
+    assert port.rel_err(gpre, o["gpre"]) < 1e-12
+    assert port.rel_err(res[0][4], o["ga_log"]) < 1e-12
+
+
+def _worker_long(rank, world, port_no, q):
+    from paper_2602_08810_b200.distributed import LongS6
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pb, p, u, pre = _problem(L=36)
+        s, e = shard_range(36, world, rank)
+        sl = {k: (v[:, s:e].contiguous() if k in ("u", "pre", "Bk", "Ck", "gy") else v) for k, v in pb.items()}
+        ls = LongS6(sub=3, scan_fwd=_fwd, scan_bwd=_bwd)
+        args = (sl["u"], sl["pre"], sl["b_delta"], sl["a_log"], sl["Bk"], sl["Ck"], sl["D"])
+        y, ctx = ls.forward(*args)
+        r = ls.backward(ctx, *args, sl["gy"])
+        ga = r["ga_log"].clone()
+        dist.all_reduce(ga)
+        q.put((rank, y.numpy(), r["gu_local"].numpy(), r["gpre"].numpy(), ga.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_hierarchical_long_sequence_gloo():
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port_no = sck.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_long, args=(r, 2, port_no, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    pb, p, u, pre = _problem(L=36)
+    y_ref, o = port.s6_scan(u, pre, p["b_delta"], p["a_log"], u @ p["W_B"].T, u @ p["W_C"].T, p["D"],
+                            pb["gy"].numpy())
+    assert port.rel_err(np.concatenate([r[1] for r in res], 1), y_ref) < 1e-12
+    assert port.rel_err(np.concatenate([r[2] for r in res], 1), o["gu_local"]) < 1e-12
+    assert port.rel_err(np.concatenate([r[3] for r in res], 1), o["gpre"]) < 1e-12
+    assert port.rel_err(res[0][4], o["ga_log"]) < 1e-12

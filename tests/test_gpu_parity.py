@@ -233,3 +233,35 @@ def test_native_kernels_ran(lrx):
     y, tape = layer.forward(np.ones((1, 5, 16), np.float32), tape=True)
     lrx.layer_backward(layer, tape, np.ones_like(y))
     assert _lib.launch_count() > before
+
+
+def _s6_inputs(lrx, m, n, L, seed=5, dtype="f32"):
+    from paper_2602_08810_b200.layers import _mm
+    layer = lrx.make_layer("s6", m, n, dtype=dtype, seed=seed)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    u = torch.randn((1, L, m), generator=g, device="cuda").to(layer.io_dtype)
+    gy = torch.randn((1, L, m), generator=g, device="cuda").to(layer.io_dtype)
+    u2 = u.reshape(L, m)
+    pre = (_mm(u2, layer.W_delta) @ layer.W_delta_proj).reshape(1, L, m)
+    Bk = _mm(u2, layer.W_B.T).reshape(1, L, n)
+    Ck = _mm(u2, layer.W_C.T).reshape(1, L, n)
+    return layer, (u, pre, layer.b_delta, layer.a_log, Bk, Ck, layer.D), gy
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_long_sequence_parallel_matches_single_pass(lrx, dtype):
+    from paper_2602_08810_b200 import ops
+    from paper_2602_08810_b200.distributed import LongS6, SeqParallelS6
+    layer, args, gy = _s6_inputs(lrx, 64, 16, 4096, dtype=dtype)
+    y_ref, ck = ops.s6_scan_fwd(*args)
+    r_ref = ops.s6_scan_bwd(*args, ck, gy)
+    tol = 1e-5 if dtype == "f32" else 1e-2
+    ls = LongS6(sub=16)
+    y, ctx = ls.forward(*args)
+    r = ls.backward(ctx, *args, gy)
+    assert rel(y, y_ref.float().cpu().numpy()) < tol
+    for k in ("gu_local", "gpre", "gBk", "gCk", "ga_log", "gD", "gb_delta"):
+        assert rel(r[k], r_ref[k].float().cpu().numpy()) < tol, k
+    y2, g2 = SeqParallelS6.simulate(3, *args, gy)
+    assert rel(y2, y_ref.float().cpu().numpy()) < tol
+    assert rel(g2["ga_log"], r_ref["ga_log"].cpu().numpy()) < tol
