@@ -50,7 +50,7 @@ WORKLOADS = {
     "s5": dict(kind="s5", B=32, L=4096, H=256, N=128, dtype="f32", cfg=1),
     "s6": dict(kind="s6", B=16, L=8192, H=1536, N=16, dtype="bf16", cfg=2),
     "rglru": dict(kind="rglru", B=64, L=16384, H=2560, N=1, dtype="f32", cfg=3),
-    "s6_long": dict(kind="s6", B=1, L=2 ** 20, H=2048, N=16, dtype="bf16", cfg=4, seqpar=True, sub=64),
+    "s6_long": dict(kind="s6", B=1, L=2 ** 20, H=2048, N=16, dtype="bf16", cfg=4, seqpar=True),
 }
 DEFAULT_WORKLOAD = "rglru"
 METRIC = "scan Gelem/s (B·L·H·N) fwd+bwd, HBM GB/s vs peak, at 1/2/4/8 B200"
@@ -177,7 +177,7 @@ def build_problem(w, B, device, L=None, group=None):
         pa = (layer.b_delta, layer.a_log)
         if w.get("seqpar"):
             from paper_2602_08810_b200.distributed import LongS6
-            ls = LongS6(sub=w["sub"], group=group)
+            ls = LongS6(group=group)
             args = (prob["u"], prob["pre"], *pa, prob["Bk"], prob["Ck"], layer.D)
 
             def fwd():
@@ -224,8 +224,8 @@ def run_gpu(args, w, rank, world, device):
     B_total = w["B"]
     L_rank = None
     if w.get("seqpar"):  # the time axis is split across ranks (C5)
-        if w["L"] % (world * w["sub"]):
-            raise SystemExit(f"L={w['L']} does not split into {world} x {w['sub']} slices")
+        if w["L"] % world:
+            raise SystemExit(f"L={w['L']} does not split into {world} slices")
         B, L_rank = B_total, w["L"] // world
     else:
         if B_total % world:
@@ -313,7 +313,7 @@ def run_e2e(args, w, prob, device):
             return [y, r["gu_local"], r["gqr"], r["gqi"], r["gla"], r["gb_r"], r["gb_i"]]
         if kind == "s6" and w.get("seqpar"):
             from paper_2602_08810_b200.distributed import LongS6
-            ls = LongS6(sub=w["sub"])
+            ls = LongS6()
             a = (d["u"], d["pre"], layer.b_delta, layer.a_log, d["Bk"], d["Ck"], layer.D)
             y, ctx = ls.forward(*a)
             return [y] + list(ls.backward(ctx, *a, d["gy"]).values())
@@ -420,7 +420,7 @@ def main():
     config = {"workload": f"{args.workload}: configs[{w['cfg']}] {w['kind']} B={w['B']} L={w['L']} H={w['H']} "
                           f"N={w['N']}", "global_batch": w["B"], "seq_len": w["L"], "width": w["H"],
               "d_state": w["N"],
-              "parallelism": (f"sequence-parallel x{world} (x{w.get('sub')} sub-slices per GPU)" if w.get("seqpar")
+              "parallelism": (f"sequence-parallel x{world} (+ in-kernel time segments)" if w.get("seqpar")
                               else f"batch-sharded x{world}" if world > 1 else "single GPU"),
               "l2": "inputs > L2 (126 MB): no flush needed"}
 

@@ -127,21 +127,27 @@ int lrx_rglru_bwd(int io_dtype, const void* u, const void* qr, const void* qi, c
  * every ckpt_len-step boundary and, in its last slot, the final state:
  * [B, n_ckpt, D, N] compute precision (n_ckpt = ceil(L/ckpt_len) + 1).
  * ------------------------------------------------------------------------ */
-/* geometry: checkpoint interval and count, and the number of channel blocks
- * (= rows of the gBk/gCk partials) the kernels use for these extents. */
-int lrx_s6_ckpt_len(int io_dtype, int64_t L, int64_t D, int64_t N, int64_t* ckpt_len, int64_t* n_ckpt,
-                    int64_t* n_dblk);
+/* Geometry for these extents: out[0] ckpt_len, out[1] n_ckpt, out[2] n_dblk
+ * (rows of the gBk/gCk partials), out[3] n_seg (time segments run
+ * concurrently when B*D alone cannot fill the GPU), out[4] part_rows (rows of
+ * the ga/gD/gb partials = n_seg*B), out[5] workspace bytes. */
+int lrx_s6_geometry(int io_dtype, int64_t B, int64_t L, int64_t D, int64_t N, int64_t* out6);
+/* flags for lrx_s6_fwd / lrx_s6_bwd */
+#define LRX_S6_REUSE_AGG 1 /* ws already holds the per-segment maps from a
+                              preceding lrx_s6_{fwd,bwd}_carry on the same inputs */
 /* x0 [B, D, N] (compute precision, NULL = zeros) seeds the state: the
- * sequence-parallel mode continues a scan another rank started. */
+ * sequence-parallel mode continues a scan another rank started.
+ * ws: caller-allocated device workspace of out[5] bytes (transient). */
 int lrx_s6_fwd(int io_dtype, const void* u, const void* pre, const void* b_delta, const void* a_log,
                const void* Bk, const void* Ck, const void* Dskip, const void* x0, void* y, void* ckpt,
-               int64_t B, int64_t L, int64_t D, int64_t N, void* stream);
+               int64_t B, int64_t L, int64_t D, int64_t N, void* ws, int64_t ws_bytes, int flags, void* stream);
 /* Outputs: gu_local = D gy + delta * sum_n g B   (GEMM terms are the
  * caller's) [B,L,D] io dtype; gpre = sigmoid(pre+b) * gdelta [B,L,D]
  * compute precision;
  * gBk_part, gCk_part [n_dblk, B, L, N] per channel-block partials;
- * ga_part (d/d a_log, already times a) [B, D, N]; gD_part, gb_part [B, D]
- * (compute precision).  Reduce the partial axes with lrx_reduce_rows. */
+ * ga_part (d/d a_log, already times a) [part_rows, D, N]; gD_part, gb_part
+ * [part_rows, D] (compute precision).  Reduce the partial axes with
+ * lrx_reduce_rows. */
 /* h_in [B, D, N] (NULL = zeros) is the cotangent carry entering from the
  * right (abar_{L} g_{L} of the next slice); h_out [B, D, N] (NULL to skip)
  * receives abar_0 g_0 = d loss / d x0 (the carry for the slice to the left). */
@@ -149,7 +155,20 @@ int lrx_s6_bwd(int io_dtype, const void* u, const void* pre, const void* b_delta
                const void* Bk, const void* Ck, const void* Dskip, const void* ckpt, const void* gy,
                const void* h_in, void* gu_local, void* gpre, void* gBk_part, void* gCk_part, void* ga_part,
                void* gD_part, void* gb_part, void* h_out, int64_t B, int64_t L, int64_t D, int64_t N,
-               void* stream);
+               void* ws, int64_t ws_bytes, int flags, void* stream);
+/* Sequence-parallel carry exchange (config C5; F32/BF16 io, N = 16).
+ * fwd_carry: the slice's affine map x_end = prod(abar) x_in + x_agg, returned
+ * as x_agg [B, D, N] (state reached from a zero start) and sd_agg [B, D]
+ * (sum of delta; prod abar = exp(a * sd_agg)).  bwd_carry: the same for the
+ * cotangent carry travelling right to left (h_agg = d loss / d x_in with a
+ * zero carry entering on the right).  Both leave the per-segment maps in ws
+ * for a following lrx_s6_fwd / lrx_s6_bwd with LRX_S6_REUSE_AGG. */
+int lrx_s6_fwd_carry(int io_dtype, const void* u, const void* pre, const void* b_delta, const void* a_log,
+                     const void* Bk, void* x_agg, void* sd_agg, int64_t B, int64_t L, int64_t D, int64_t N,
+                     void* ws, int64_t ws_bytes, void* stream);
+int lrx_s6_bwd_carry(int io_dtype, const void* gy, const void* pre, const void* b_delta, const void* a_log,
+                     const void* Ck, void* h_agg, void* sd_agg, int64_t B, int64_t L, int64_t D, int64_t N,
+                     void* ws, int64_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ *
  * MIMO complex diagonal scan for S5 / LRU (layers.py:616-980): the recurrence

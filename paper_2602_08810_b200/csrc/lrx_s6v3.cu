@@ -1,0 +1,952 @@
+// S6 / Mamba selective scan, v3: TMA-staged time tiles, channel-pair threads,
+// in-kernel time segmentation.  fp32 compute, bf16 or f32 I/O, d_state 16.
+//
+// Reference: pkg/src/linrec/layers.py S6 (983-1168): _projections 1020-1027,
+// _forward_tape 1051-1066, _backward 1068-1118; the pullback of
+// autograd._scan_pullback 113-140; numerics.softplus/sigmoid 86-105.
+//
+//   delta_k[d] = softplus(pre_k[d] + b_delta[d]),  a[d,n] = -exp(a_log[d,n])
+//   x_k[d,n]   = exp(delta_k[d] a[d,n]) x_{k-1}[d,n] + delta_k[d] u_k[d] B_k[n]
+//   y_k[d]     = sum_n C_k[n] x_k[d,n] + D[d] u_k[d]
+//
+// Layout.  A CTA owns 64 channels of one batch row and one time segment.
+// Thread (warp w, lane = 4 g + q) owns the channel pair p = 8 w + g (channels
+// 2p, 2p+1) x the four states 4q..4q+3: 8 (channel, state) lanes, so
+//   * the readout sum over n is a 4-lane reduction (lane bits 0-1),
+//   * the backward's dB_k / dC_k sums over channels are first summed over the
+//     thread's channel pair in registers, then over lane bits 2-4 and the
+//     CTA's 4 warps, then across channel blocks as fixed-order partials.
+// Time tiles of 16 steps x 64 channels of u / pre (/ gy) and 16 x 16 of
+// B_k / C_k arrive by TMA (cp.async.bulk.tensor.3d, zero-filled past L and
+// D) into a ring of stages; a cooperative prologue per tile turns pre into
+// delta (softplus, once per (t, d)), delta*u and, backward, sigmoid(pre);
+// outputs (y, or gu and gpre) leave through smem tiles by TMA store.
+//
+// Checkpoints.  The forward writes the state entering every 8-step chunk
+// (ckpt [B, ceil(L/8)+1, D, 16], last slot = final state).  The backward
+// walks tiles right to left; per chunk it recomputes the 8 states from the
+// checkpoint into registers, then runs the reverse recurrence: 2 ex2 per
+// (t, d, n) instead of storing every state.
+//
+// Segments.  When B * D / 64 CTAs cannot fill the GPU (batch-sharded C3 on
+// 8 GPUs: 48 CTAs; long-sequence C5: 32), the sequence is cut into S
+// segments of whole tiles that run concurrently.  An aggregate pass computes
+// each segment's map (x_end from a zero start, sum of delta -> prod abar =
+// exp(a sum delta)); each main CTA folds its predecessors' maps to get its
+// entering state (the multi-segment analog of the reference's chunk stitch,
+// scan.py:184-189, layers.py:157-175).  The backward does the same with the
+// cotangent carry from the right.  The fold order is fixed: deterministic.
+#include "lrx_common.cuh"
+#include "lrx_host.h"
+#include "lrx_tma.cuh"
+
+#include <stdlib.h>
+
+#include <algorithm>
+
+namespace lrx {
+namespace s6v3 {
+
+constexpr int NST = 16;     // d_state
+constexpr int CH = 64;      // channels per CTA
+constexpr int THREADS = 128;
+constexpr int T = 16;       // time tile
+constexpr int CK = 8;       // checkpoint interval = backward recompute chunk
+constexpr int NSF = 4;      // forward pipeline stages
+constexpr int NSB = 3;      // backward pipeline stages
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// delta = softplus(x) (x > 30 -> x; small e^x through the log1p series so
+// delta keeps its relative precision, numerics.py:86-94) and sigmoid(x).
+__device__ __forceinline__ float softplus_sig(float x, float* sig) {
+    const float e = ex2(fminf(x, 30.f) * kLog2e);
+    const float lg = lg2(1.f + e) * kLn2;
+    const float ser = e * (1.f - e * (0.5f - e * (1.f / 3.f)));
+    *sig = e * rcp(1.f + e);
+    return x > 30.f ? x : (e < 1e-2f ? ser : lg);
+}
+
+__device__ __forceinline__ float2 ld_pair(const __nv_bfloat16* p) {
+    const uint32_t v = *reinterpret_cast<const uint32_t*>(p);
+    return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
+}
+__device__ __forceinline__ float2 ld_pair(const float* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ void st_pair(__nv_bfloat16* p, float a, float b) {
+    *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(a, b);
+}
+__device__ __forceinline__ void st_pair(float* p, float a, float b) { *reinterpret_cast<float2*>(p) = make_float2(a, b); }
+__device__ __forceinline__ float ld1(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float ld1(const float* p) { return *p; }
+__device__ __forceinline__ void st1(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+__device__ __forceinline__ void st1(float* p, float v) { *p = v; }
+
+// Transposed butterfly: reduce V values over the lane bits HI, HI/2, ..., LO.
+// Afterwards v[0 .. V/R) of a lane hold the R-lane sums of the value block
+// selected by the lane's bits (bit HI picks the upper half first).
+template <int V, int HI, int LO>
+__device__ __forceinline__ void tr_reduce(float* v) {
+    const int lane = threadIdx.x & 31;
+    int cnt = V;
+#pragma unroll
+    for (int m = HI; m >= LO; m >>= 1) {
+        const int half = cnt / 2;
+        const bool up = lane & m;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const float send = up ? v[i] : v[i + half];
+            const float keep = up ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+        cnt = half;
+    }
+}
+
+template <typename IO>
+struct Lay {
+    static constexpr int U = T * CH * (int)sizeof(IO);  // u / gy / y / gu tile
+    static constexpr int P = T * CH * 4;                 // pre / delta / du / sigmoid / gpre tile
+    static constexpr int BC = T * NST * 4;               // B_k or C_k tile
+    // stage compositions
+    static constexpr int FWD = U + P + 2 * BC;           // u, pre, B, C
+    static constexpr int BWD = 2 * U + P + 2 * BC;       // u, pre, gy, B, C
+    static constexpr int FAGG = U + P + BC;              // u, pre, B
+    static constexpr int BAGG = U + P + BC;              // gy, pre, C
+    static constexpr int RED = T * 4 * 32 * 4;          // [T][warp][32] dB/dC warp sums
+    static constexpr size_t smem_fwd() { return 128 + (size_t)NSF * FWD + P + 2 * U; }
+    static constexpr size_t smem_bwd() { return 128 + (size_t)NSB * BWD + 2 * P + 2 * (U + P) + RED; }
+    static constexpr size_t smem_fagg() { return 128 + (size_t)NSF * FAGG + P + 2 * CH * 4; }
+    static constexpr size_t smem_bagg() { return 128 + (size_t)NSF * BAGG + 2 * CH * 4; }
+};
+
+struct Seg {
+    int64_t t_beg, t_end;
+    int tile0, ntiles;
+};
+__device__ __forceinline__ Seg segment(int s, int64_t seg_len, int64_t L) {
+    Seg r;
+    r.t_beg = (int64_t)s * seg_len;
+    r.t_end = min(L, r.t_beg + seg_len);
+    r.tile0 = (int)(r.t_beg / T);
+    r.ntiles = (int)((r.t_end - r.t_beg + T - 1) / T);
+    return r;
+}
+
+__device__ __forceinline__ void init_bars(uint64_t* full, int n) {
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < n; ++i) tma::mbar_init(&full[i], 1);
+        tma::fence_barrier_init();
+    }
+    __syncthreads();
+}
+
+// ============================================================================
+// Forward aggregate pass: per segment s, x_end from a zero start and sum delta.
+// grid (n_dblk, B, n_segments_covered); segment = blockIdx.z + s_lo.
+template <typename IO>
+__global__ void __launch_bounds__(THREADS) fwd_agg_kernel(
+    const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mp,
+    const __grid_constant__ CUtensorMap mB, const float* __restrict__ bdelta, const float* __restrict__ a_log,
+    float* __restrict__ aggX, float* __restrict__ aggSD, int64_t Bn, int64_t L, int64_t D, int64_t seg_len,
+    int s_lo) {
+    using LY = Lay<IO>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    unsigned char* stages = smem + 128;
+    float* dub = reinterpret_cast<float*>(stages + NSF * LY::FAGG);
+    float* sdx = dub + T * CH;  // [2][CH]
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, q = lane & 3, g = lane >> 2;
+    const int pp = w * 8 + g;
+    const int b = blockIdx.y, s = blockIdx.z + s_lo;
+    const int d0 = blockIdx.x * CH;
+    const Seg sg = segment(s, seg_len, L);
+    init_bars(full, NSF);
+    auto issue = [&](int j) {
+        const int st = j % NSF;
+        unsigned char* sp = stages + st * LY::FAGG;
+        const int t = (sg.tile0 + j) * T;
+        tma::mbar_arrive_expect_tx(&full[st], LY::FAGG);
+        tma::load_3d(sp, &mu, d0, t, b, &full[st]);
+        tma::load_3d(sp + LY::U, &mp, d0, t, b, &full[st]);
+        tma::load_3d(sp + LY::U + LY::P, &mB, 0, t, b, &full[st]);
+    };
+    if (tid == 0)
+        for (int j = 0; j < NSF && j < sg.ntiles; ++j) issue(j);
+
+    float a2[2][4], x[2][4];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int64_t dg = d0 + 2 * pp + c;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            a2[c][j] = dg < D ? -expf(a_log[dg * NST + 4 * q + j]) * kLog2e : 0.f;
+            x[c][j] = 0.f;
+        }
+    }
+    const int pd = tid & (CH - 1), pr = tid >> 6;
+    const float pbd = d0 + pd < D ? bdelta[d0 + pd] : 0.f;
+    float sd = 0.f;
+    for (int j = 0; j < sg.ntiles; ++j) {
+        const int st = j % NSF;
+        const int64_t t0 = (int64_t)(sg.tile0 + j) * T;
+        const int nt = (int)min((int64_t)T, sg.t_end - t0);
+        unsigned char* sp = stages + st * LY::FAGG;
+        const IO* us = reinterpret_cast<const IO*>(sp);
+        float* ps = reinterpret_cast<float*>(sp + LY::U);
+        const float* Bs = reinterpret_cast<const float*>(sp + LY::U + LY::P);
+        tma::mbar_wait(&full[st], (j / NSF) & 1);
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) {
+            const int r = pr + 2 * i, idx = r * CH + pd;
+            float sig;
+            float dl = softplus_sig(ps[idx] + pbd, &sig);
+            dl = r < nt ? dl : 0.f;
+            sd += dl;
+            ps[idx] = dl;
+            dub[idx] = dl * ld1(us + idx);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+            const float2 dl = ld_pair(ps + k * CH + 2 * pp), du = ld_pair(dub + k * CH + 2 * pp);
+            const float4 bb = *reinterpret_cast<const float4*>(Bs + k * NST + 4 * q);
+            const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
+            const float dlc[2] = {dl.x, dl.y}, duc[2] = {du.x, du.y};
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) x[c][jj] = fmaf(ex2(dlc[c] * a2[c][jj]), x[c][jj], duc[c] * bv[jj]);
+        }
+        tma::fence_proxy_async();
+        __syncthreads();
+        if (tid == 0 && j + NSF < sg.ntiles) issue(j + NSF);
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int64_t dg = d0 + 2 * pp + c;
+        if (dg < D)
+            *reinterpret_cast<float4*>(aggX + (((int64_t)s * Bn + b) * D + dg) * NST + 4 * q) =
+                make_float4(x[c][0], x[c][1], x[c][2], x[c][3]);
+    }
+    sdx[pr * CH + pd] = sd;
+    __syncthreads();
+    if (tid < CH && d0 + tid < D) aggSD[((int64_t)s * Bn + b) * D + d0 + tid] = sdx[tid] + sdx[CH + tid];
+}
+
+// ============================================================================
+// Forward main pass.
+template <typename IO>
+__global__ void __launch_bounds__(THREADS) fwd_kernel(
+    const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mp,
+    const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mC,
+    const __grid_constant__ CUtensorMap my, const float* __restrict__ bdelta, const float* __restrict__ a_log,
+    const float* __restrict__ Dskip, const float* __restrict__ x0, const float* __restrict__ aggX,
+    const float* __restrict__ aggSD, float* __restrict__ ckpt, int64_t Bn, int64_t L, int64_t D, int64_t seg_len,
+    int n_ck) {
+    using LY = Lay<IO>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    unsigned char* stages = smem + 128;
+    float* dub = reinterpret_cast<float*>(stages + NSF * LY::FWD);
+    IO* ybuf = reinterpret_cast<IO*>(reinterpret_cast<unsigned char*>(dub) + LY::P);  // [2][T][CH]
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, q = lane & 3, g = lane >> 2;
+    const int pp = w * 8 + g;
+    const int b = blockIdx.y, s = blockIdx.z;
+    const int d0 = blockIdx.x * CH;
+    const Seg sg = segment(s, seg_len, L);
+    init_bars(full, NSF);
+    auto issue = [&](int j) {
+        const int st = j % NSF;
+        unsigned char* sp = stages + st * LY::FWD;
+        const int t = (sg.tile0 + j) * T;
+        tma::mbar_arrive_expect_tx(&full[st], LY::FWD);
+        tma::load_3d(sp, &mu, d0, t, b, &full[st]);
+        tma::load_3d(sp + LY::U, &mp, d0, t, b, &full[st]);
+        tma::load_3d(sp + LY::U + LY::P, &mB, 0, t, b, &full[st]);
+        tma::load_3d(sp + LY::U + LY::P + LY::BC, &mC, 0, t, b, &full[st]);
+    };
+    if (tid == 0)
+        for (int j = 0; j < NSF && j < sg.ntiles; ++j) issue(j);
+
+    float a2[2][4], x[2][4], Dd[2];
+    bool okc[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int64_t dg = d0 + 2 * pp + c;
+        okc[c] = dg < D;
+        Dd[c] = okc[c] ? Dskip[dg] : 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            a2[c][j] = okc[c] ? -expf(a_log[dg * NST + 4 * q + j]) * kLog2e : 0.f;
+            x[c][j] = (x0 && okc[c]) ? x0[((int64_t)b * D + dg) * NST + 4 * q + j] : 0.f;
+        }
+        // fold the maps of the segments to the left (fixed order)
+        for (int r = 0; r < s; ++r) {
+            if (!okc[c]) break;
+            const int64_t o = ((int64_t)r * Bn + b) * D + dg;
+            const float sdr = aggSD[o];
+            const float4 X = *reinterpret_cast<const float4*>(aggX + o * NST + 4 * q);
+            const float Xv[4] = {X.x, X.y, X.z, X.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[c][j] = fmaf(ex2(a2[c][j] * sdr), x[c][j], Xv[j]);
+        }
+    }
+    const int pd = tid & (CH - 1), pr = tid >> 6;
+    const float pbd = d0 + pd < D ? bdelta[d0 + pd] : 0.f;
+
+    for (int j = 0; j < sg.ntiles; ++j) {
+        const int st = j % NSF;
+        const int64_t t0 = (int64_t)(sg.tile0 + j) * T;
+        const int nt = (int)min((int64_t)T, sg.t_end - t0);
+        unsigned char* sp = stages + st * LY::FWD;
+        const IO* us = reinterpret_cast<const IO*>(sp);
+        float* ps = reinterpret_cast<float*>(sp + LY::U);
+        const float* Bs = reinterpret_cast<const float*>(sp + LY::U + LY::P);
+        const float* Cs = Bs + T * NST;
+        IO* yo = ybuf + (j & 1) * T * CH;
+        if (tid == 0 && j >= 2) tma::bulk_wait_read<1>();  // the store that used yo is done reading
+        tma::mbar_wait(&full[st], (j / NSF) & 1);
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) {
+            const int r = pr + 2 * i, idx = r * CH + pd;
+            float sig;
+            float dl = softplus_sig(ps[idx] + pbd, &sig);
+            dl = r < nt ? dl : 0.f;  // past L: abar = 1, no input -> the state is carried unchanged
+            ps[idx] = dl;
+            dub[idx] = dl * ld1(us + idx);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kb = 0; kb < T / 4; ++kb) {
+            float yp[8];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int k = kb * 4 + kk;
+                if (k % CK == 0 && ckpt != nullptr && t0 + k < sg.t_end) {
+                    float* cp = ckpt + (((int64_t)b * (n_ck + 1) + (t0 + k) / CK) * D + d0 + 2 * pp) * NST + 4 * q;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+                        if (okc[c])
+                            __stcs(reinterpret_cast<float4*>(cp + c * NST),
+                                   make_float4(x[c][0], x[c][1], x[c][2], x[c][3]));
+                }
+                const float2 dl = ld_pair(ps + k * CH + 2 * pp), du = ld_pair(dub + k * CH + 2 * pp);
+                const float4 bb = *reinterpret_cast<const float4*>(Bs + k * NST + 4 * q);
+                const float4 cc = *reinterpret_cast<const float4*>(Cs + k * NST + 4 * q);
+                const float bv[4] = {bb.x, bb.y, bb.z, bb.w}, cv[4] = {cc.x, cc.y, cc.z, cc.w};
+                const float dlc[2] = {dl.x, dl.y}, duc[2] = {du.x, du.y};
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        x[c][jj] = fmaf(ex2(dlc[c] * a2[c][jj]), x[c][jj], duc[c] * bv[jj]);
+                        acc = fmaf(x[c][jj], cv[jj], acc);
+                    }
+                    yp[kk * 2 + c] = acc;
+                }
+            }
+            tr_reduce<8, 2, 1>(yp);  // lane q: step kb*4 + q, both channels
+            const int k = kb * 4 + q;
+            const float2 uu = ld_pair(us + k * CH + 2 * pp);
+            st_pair(yo + k * CH + 2 * pp, fmaf(Dd[0], uu.x, yp[0]), fmaf(Dd[1], uu.y, yp[1]));
+        }
+        tma::fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tma::store_3d(&my, yo, d0, (int)t0, b);
+            tma::bulk_commit();
+            if (j + NSF < sg.ntiles) issue(j + NSF);
+        }
+    }
+    if (ckpt != nullptr && s == (int)gridDim.z - 1) {  // final state in the last slot
+        float* cp = ckpt + (((int64_t)b * (n_ck + 1) + n_ck) * D + d0 + 2 * pp) * NST + 4 * q;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+            if (okc[c]) *reinterpret_cast<float4*>(cp + c * NST) = make_float4(x[c][0], x[c][1], x[c][2], x[c][3]);
+    }
+    if (tid == 0) tma::bulk_wait<0>();
+}
+
+// ============================================================================
+// Backward aggregate pass: per segment s, the cotangent carry leaving the
+// segment to the left from a zero carry entering on the right, and sum delta.
+template <typename IO>
+__global__ void __launch_bounds__(THREADS) bwd_agg_kernel(
+    const __grid_constant__ CUtensorMap mg, const __grid_constant__ CUtensorMap mp,
+    const __grid_constant__ CUtensorMap mC, const float* __restrict__ bdelta, const float* __restrict__ a_log,
+    float* __restrict__ aggH, float* __restrict__ aggSD, int64_t Bn, int64_t L, int64_t D, int64_t seg_len,
+    int s_lo) {
+    using LY = Lay<IO>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    unsigned char* stages = smem + 128;
+    float* sdx = reinterpret_cast<float*>(stages + NSF * LY::BAGG);  // [2][CH]
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, q = lane & 3, g = lane >> 2;
+    const int pp = w * 8 + g;
+    const int b = blockIdx.y, s = blockIdx.z + s_lo;
+    const int d0 = blockIdx.x * CH;
+    const Seg sg = segment(s, seg_len, L);
+    init_bars(full, NSF);
+    auto issue = [&](int j) {  // j-th tile from the right
+        const int st = j % NSF;
+        unsigned char* sp = stages + st * LY::BAGG;
+        const int t = (sg.tile0 + sg.ntiles - 1 - j) * T;
+        tma::mbar_arrive_expect_tx(&full[st], LY::BAGG);
+        tma::load_3d(sp, &mg, d0, t, b, &full[st]);
+        tma::load_3d(sp + LY::U, &mp, d0, t, b, &full[st]);
+        tma::load_3d(sp + LY::U + LY::P, &mC, 0, t, b, &full[st]);
+    };
+    if (tid == 0)
+        for (int j = 0; j < NSF && j < sg.ntiles; ++j) issue(j);
+    float a2[2][4], h[2][4];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int64_t dg = d0 + 2 * pp + c;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            a2[c][j] = dg < D ? -expf(a_log[dg * NST + 4 * q + j]) * kLog2e : 0.f;
+            h[c][j] = 0.f;
+        }
+    }
+    const int pd = tid & (CH - 1), pr = tid >> 6;
+    const float pbd = d0 + pd < D ? bdelta[d0 + pd] : 0.f;
+    float sd = 0.f;
+    for (int j = 0; j < sg.ntiles; ++j) {
+        const int st = j % NSF;
+        const int64_t t0 = (int64_t)(sg.tile0 + sg.ntiles - 1 - j) * T;
+        const int nt = (int)min((int64_t)T, sg.t_end - t0);
+        unsigned char* sp = stages + st * LY::BAGG;
+        const IO* gs = reinterpret_cast<const IO*>(sp);
+        float* ps = reinterpret_cast<float*>(sp + LY::U);
+        const float* Cs = reinterpret_cast<const float*>(sp + LY::U + LY::P);
+        tma::mbar_wait(&full[st], (j / NSF) & 1);
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) {
+            const int r = pr + 2 * i, idx = r * CH + pd;
+            float sig;
+            float dl = softplus_sig(ps[idx] + pbd, &sig);
+            dl = r < nt ? dl : 0.f;
+            sd += dl;
+            ps[idx] = dl;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = T - 1; k >= 0; --k) {
+            const float2 dl = ld_pair(ps + k * CH + 2 * pp), gy = ld_pair(gs + k * CH + 2 * pp);
+            const float4 cc = *reinterpret_cast<const float4*>(Cs + k * NST + 4 * q);
+            const float cv[4] = {cc.x, cc.y, cc.z, cc.w};
+            const float dlc[2] = {dl.x, dl.y}, gyc[2] = {gy.x, gy.y};
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) h[c][jj] = ex2(dlc[c] * a2[c][jj]) * fmaf(gyc[c], cv[jj], h[c][jj]);
+        }
+        tma::fence_proxy_async();
+        __syncthreads();
+        if (tid == 0 && j + NSF < sg.ntiles) issue(j + NSF);
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int64_t dg = d0 + 2 * pp + c;
+        if (dg < D)
+            *reinterpret_cast<float4*>(aggH + (((int64_t)s * Bn + b) * D + dg) * NST + 4 * q) =
+                make_float4(h[c][0], h[c][1], h[c][2], h[c][3]);
+    }
+    sdx[pr * CH + pd] = sd;
+    __syncthreads();
+    if (tid < CH && d0 + tid < D) aggSD[((int64_t)s * Bn + b) * D + d0 + tid] = sdx[tid] + sdx[CH + tid];
+}
+
+// ============================================================================
+// Backward main pass.
+template <typename IO>
+__global__ void __launch_bounds__(THREADS) bwd_kernel(
+    const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mp,
+    const __grid_constant__ CUtensorMap mg, const __grid_constant__ CUtensorMap mB,
+    const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mgu,
+    const __grid_constant__ CUtensorMap mgp, const float* __restrict__ bdelta, const float* __restrict__ a_log,
+    const float* __restrict__ Dskip, const float* __restrict__ ckpt, const float* __restrict__ h_in,
+    const float* __restrict__ aggH, const float* __restrict__ aggSD, float* __restrict__ gB_part,
+    float* __restrict__ gC_part, float* __restrict__ ga_part, float* __restrict__ gD_part,
+    float* __restrict__ gb_part, float* __restrict__ h_out, int64_t Bn, int64_t L, int64_t D, int64_t seg_len,
+    int n_ck) {
+    using LY = Lay<IO>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    unsigned char* stages = smem + 128;
+    float* dub = reinterpret_cast<float*>(stages + NSB * LY::BWD);  // delta * u
+    float* sgb = dub + T * CH;                                       // sigmoid(pre + b)
+    unsigned char* ob = reinterpret_cast<unsigned char*>(sgb + T * CH);  // [2] x (gu tile IO, gpre tile f32)
+    float* red = reinterpret_cast<float*>(ob + 2 * (LY::U + LY::P));    // [T][4][32]
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, q = lane & 3, g = lane >> 2;
+    const int pp = w * 8 + g;
+    const int b = blockIdx.y, s = blockIdx.z, S = gridDim.z;
+    const int d0 = blockIdx.x * CH;
+    const Seg sg = segment(s, seg_len, L);
+    init_bars(full, NSB);
+    auto issue = [&](int j) {
+        const int st = j % NSB;
+        unsigned char* sp = stages + st * LY::BWD;
+        const int t = (sg.tile0 + sg.ntiles - 1 - j) * T;
+        tma::mbar_arrive_expect_tx(&full[st], LY::BWD);
+        tma::load_3d(sp, &mu, d0, t, b, &full[st]);
+        tma::load_3d(sp + LY::U, &mg, d0, t, b, &full[st]);
+        tma::load_3d(sp + 2 * LY::U, &mp, d0, t, b, &full[st]);
+        tma::load_3d(sp + 2 * LY::U + LY::P, &mB, 0, t, b, &full[st]);
+        tma::load_3d(sp + 2 * LY::U + LY::P + LY::BC, &mC, 0, t, b, &full[st]);
+    };
+    if (tid == 0)
+        for (int j = 0; j < NSB && j < sg.ntiles; ++j) issue(j);
+
+    float a2[2][4], h[2][4], gacc[2][4], Dd[2];
+    bool okc[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int64_t dg = d0 + 2 * pp + c;
+        okc[c] = dg < D;
+        Dd[c] = okc[c] ? Dskip[dg] : 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            a2[c][j] = okc[c] ? -expf(a_log[dg * NST + 4 * q + j]) * kLog2e : 0.f;
+            h[c][j] = (h_in && okc[c]) ? h_in[((int64_t)b * D + dg) * NST + 4 * q + j] : 0.f;
+            gacc[c][j] = 0.f;
+        }
+        // fold the cotangent maps of the segments to the right (fixed order)
+        for (int r = S - 1; r > s; --r) {
+            if (!okc[c]) break;
+            const int64_t o = ((int64_t)r * Bn + b) * D + dg;
+            const float sdr = aggSD[o];
+            const float4 H = *reinterpret_cast<const float4*>(aggH + o * NST + 4 * q);
+            const float Hv[4] = {H.x, H.y, H.z, H.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) h[c][j] = fmaf(ex2(a2[c][j] * sdr), h[c][j], Hv[j]);
+        }
+    }
+    const int pd = tid & (CH - 1), pr = tid >> 6;
+    const float pbd = d0 + pd < D ? bdelta[d0 + pd] : 0.f;
+    float gD_acc = 0.f, gb_acc = 0.f;
+    const int cq = q & 1;                         // channel of this lane's per-step output
+    const float Dq = cq ? Dd[1] : Dd[0];
+    float xn[2][4];                               // checkpoint of the next chunk (prefetched)
+    auto load_ck = [&](int64_t t) {
+        const int64_t slot = min((int64_t)n_ck, t / CK);
+        const float* cp = ckpt + (((int64_t)b * (n_ck + 1) + slot) * D + d0 + 2 * pp) * NST + 4 * q;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const float4 v = okc[c] ? __ldcs(reinterpret_cast<const float4*>(cp + c * NST)) : make_float4(0, 0, 0, 0);
+            xn[c][0] = v.x; xn[c][1] = v.y; xn[c][2] = v.z; xn[c][3] = v.w;
+        }
+    };
+    load_ck((int64_t)(sg.tile0 + sg.ntiles - 1) * T + CK);
+
+    for (int j = 0; j < sg.ntiles; ++j) {
+        const int st = j % NSB;
+        const int64_t t0 = (int64_t)(sg.tile0 + sg.ntiles - 1 - j) * T;
+        const int nt = (int)min((int64_t)T, sg.t_end - t0);
+        unsigned char* sp = stages + st * LY::BWD;
+        const IO* us = reinterpret_cast<const IO*>(sp);
+        const IO* gs = reinterpret_cast<const IO*>(sp + LY::U);
+        float* ps = reinterpret_cast<float*>(sp + 2 * LY::U);
+        const float* Bs = reinterpret_cast<const float*>(sp + 2 * LY::U + LY::P);
+        const float* Cs = Bs + T * NST;
+        IO* gu_o = reinterpret_cast<IO*>(ob + (j & 1) * (LY::U + LY::P));
+        float* gp_o = reinterpret_cast<float*>(ob + (j & 1) * (LY::U + LY::P) + LY::U);
+        if (tid == 0 && j >= 2) tma::bulk_wait_read<1>();
+        tma::mbar_wait(&full[st], (j / NSB) & 1);
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) {
+            const int r = pr + 2 * i, idx = r * CH + pd;
+            float sig;
+            float dl = softplus_sig(ps[idx] + pbd, &sig);
+            const bool in = r < nt;
+            dl = in ? dl : 0.f;
+            const float uu = ld1(us + idx);
+            gD_acc = fmaf(ld1(gs + idx), uu, gD_acc);  // zero-filled past L
+            ps[idx] = dl;
+            dub[idx] = dl * uu;
+            sgb[idx] = in ? sig : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int ch = 1; ch >= 0; --ch) {
+            // recompute the chunk's states: hist[k] = x_{k-1} for step k of the chunk
+            float hist[CK][2][4], xe[2][4];
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) xe[c][jj] = xn[c][jj];
+            // prefetch the checkpoint of the next chunk to the left
+            if (ch == 1) load_ck(t0);
+            else if (j + 1 < sg.ntiles) load_ck(t0 - T + CK);
+#pragma unroll
+            for (int kk = 0; kk < CK; ++kk) {
+                const int k = ch * CK + kk;
+                const float2 dl = ld_pair(ps + k * CH + 2 * pp), du = ld_pair(dub + k * CH + 2 * pp);
+                const float4 bb = *reinterpret_cast<const float4*>(Bs + k * NST + 4 * q);
+                const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
+                const float dlc[2] = {dl.x, dl.y}, duc[2] = {du.x, du.y};
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        hist[kk][c][jj] = xe[c][jj];
+                        xe[c][jj] = fmaf(ex2(dlc[c] * a2[c][jj]), xe[c][jj], duc[c] * bv[jj]);
+                    }
+            }
+            // reverse recurrence over the chunk
+#pragma unroll
+            for (int kk = CK - 1; kk >= 0; --kk) {
+                const int k = ch * CK + kk;
+                const float2 dl = ld_pair(ps + k * CH + 2 * pp), du = ld_pair(dub + k * CH + 2 * pp);
+                const float2 gy = ld_pair(gs + k * CH + 2 * pp), uu = ld_pair(us + k * CH + 2 * pp);
+                const float4 bb = *reinterpret_cast<const float4*>(Bs + k * NST + 4 * q);
+                const float4 cc = *reinterpret_cast<const float4*>(Cs + k * NST + 4 * q);
+                const float bv[4] = {bb.x, bb.y, bb.z, bb.w}, cv[4] = {cc.x, cc.y, cc.z, cc.w};
+                const float dlc[2] = {dl.x, dl.y}, duc[2] = {du.x, du.y}, gyc[2] = {gy.x, gy.y};
+                const float uc[2] = {uu.x, uu.y};
+                float nv[4];      // r1[c0], r1[c1], r2[c0], r2[c1]
+                float dv[8];      // dB[4q..4q+3], dC[4q..4q+3] summed over the pair
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) dv[jj] = 0.f;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    float sa = 0.f, sb = 0.f;
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const float ab = ex2(dlc[c] * a2[c][jj]);
+                        const float xp = hist[kk][c][jj];
+                        const float xk = kk == CK - 1 ? xe[c][jj] : hist[kk + 1 < CK ? kk + 1 : 0][c][jj];
+                        const float gg = fmaf(gyc[c], cv[jj], h[c][jj]);
+                        const float tt = ab * (gg * xp);         // abar * g * x_{k-1}
+                        sa = fmaf(tt, a2[c][jj], sa);
+                        gacc[c][jj] = fmaf(tt, dlc[c], gacc[c][jj]);
+                        sb = fmaf(gg, bv[jj], sb);
+                        dv[jj] = fmaf(gg, duc[c], dv[jj]);
+                        dv[4 + jj] = fmaf(gyc[c], xk, dv[4 + jj]);
+                        h[c][jj] = ab * gg;
+                    }
+                    nv[c] = fmaf(uc[c], sb, sa * kLn2);   // d delta (a = a2 ln 2)
+                    nv[2 + c] = sb;
+                }
+                tr_reduce<4, 2, 1>(nv);    // lane q: nv[0] = value q
+                tr_reduce<8, 16, 4>(dv);   // lane g: dv[0] = value g of its q block
+                red[(k * 4 + w) * 32 + q * 8 + g] = dv[0];
+                const float dlq = cq ? dlc[1] : dlc[0], gyq = cq ? gyc[1] : gyc[0];
+                if (q < 2) {
+                    const float gp = sgb[k * CH + 2 * pp + cq] * nv[0];
+                    gp_o[k * CH + 2 * pp + cq] = gp;
+                    gb_acc += gp;
+                } else {
+                    st1(gu_o + k * CH + 2 * pp + cq, fmaf(Dq, gyq, dlq * nv[0]));
+                }
+            }
+        }
+        tma::fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tma::store_3d(&mgu, gu_o, d0, (int)t0, b);
+            tma::store_3d(&mgp, gp_o, d0, (int)t0, b);
+            tma::bulk_commit();
+            if (j + NSB < sg.ntiles) issue(j + NSB);
+        }
+        // cross-warp sums of dB_k / dC_k -> this channel block's partial rows
+#pragma unroll
+        for (int i = 0; i < T * 32 / THREADS; ++i) {
+            const int idx = tid + THREADS * i;
+            const int k = idx >> 5, v = idx & 31;
+            const float sum = red[(k * 4 + 0) * 32 + v] + red[(k * 4 + 1) * 32 + v] + red[(k * 4 + 2) * 32 + v] +
+                              red[(k * 4 + 3) * 32 + v];
+            const int qq = v >> 3, gg = v & 7;
+            const int n = 4 * qq + (gg & 3);
+            if (t0 + k < sg.t_end) {
+                float* dst = gg < 4 ? gB_part : gC_part;
+                dst[(((int64_t)blockIdx.x * Bn + b) * L + t0 + k) * NST + n] = sum;
+            }
+        }
+    }
+    // parameter-gradient partials of this (segment, batch row)
+    const int64_t prow = (int64_t)s * Bn + b;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int64_t dg = d0 + 2 * pp + c;
+        if (okc[c]) {
+            float ga[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) ga[jj] = -expf(a_log[dg * NST + 4 * q + jj]) * gacc[c][jj];
+            *reinterpret_cast<float4*>(ga_part + (prow * D + dg) * NST + 4 * q) = make_float4(ga[0], ga[1], ga[2], ga[3]);
+            if (h_out && s == 0)
+                *reinterpret_cast<float4*>(h_out + ((int64_t)b * D + dg) * NST + 4 * q) =
+                    make_float4(h[c][0], h[c][1], h[c][2], h[c][3]);
+        }
+    }
+    if (q < 2 && okc[cq]) gb_part[prow * D + d0 + 2 * pp + cq] = gb_acc;
+    __syncthreads();
+    red[tid] = gD_acc;
+    __syncthreads();
+    if (tid < CH && d0 + tid < D) gD_part[prow * D + d0 + tid] = red[tid] + red[CH + tid];
+    if (tid == 0) tma::bulk_wait<0>();
+}
+
+// ============================================================================
+// Fold per-segment maps into one whole-slice map (sequence-parallel carry).
+// dir = +1: x = prod-fold left to right; dir = -1: right to left.
+__global__ void fold_kernel(const float* __restrict__ a_log, const float* __restrict__ agg,
+                            const float* __restrict__ aggSD, float* __restrict__ out, float* __restrict__ out_sd,
+                            int64_t Bn, int64_t D, int S, int dir) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over B*D*N
+    if (i >= Bn * D * NST) return;
+    const int64_t bd = i / NST, n = i % NST, d = bd % D;
+    const float a2 = -expf(a_log[d * NST + n]) * kLog2e;
+    float x = 0.f, sd = 0.f;
+    for (int k = 0; k < S; ++k) {
+        const int r = dir > 0 ? k : S - 1 - k;
+        const float sdr = aggSD[(int64_t)r * Bn * D + bd];
+        x = fmaf(ex2(a2 * sdr), x, agg[(int64_t)r * Bn * D * NST + i]);
+        sd += sdr;
+    }
+    out[i] = x;
+    if (n == 0 && out_sd) out_sd[bd] = sd;
+}
+
+// ============================================================================
+// Host side
+
+static int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) ==
+                                                      cudaSuccess && v > 0)
+            n = v;
+        else {
+            cudaGetLastError();
+            n = 148;
+        }
+    }
+    return n;
+}
+
+bool eligible(int io, int64_t D, int64_t N) {
+    if (getenv("LRX_S6_V2")) return false;
+    if (N != NST) return false;
+    if (io == LRX_BF16) return D % 8 == 0;
+    if (io == LRX_F32) return D % 4 == 0;
+    return false;
+}
+
+struct Geo {
+    int64_t n_ck, n_dblk, n_seg, seg_len, ws_bytes;
+};
+
+Geo geometry(int64_t B, int64_t L, int64_t D) {
+    Geo g;
+    g.n_ck = cdiv(L, CK);
+    g.n_dblk = cdiv(D, CH);
+    const int64_t ctas = g.n_dblk * B;
+    int64_t S = 1;
+    if (const char* e = getenv("LRX_S6_SEGS")) S = atoll(e);
+    else {
+        const int64_t want = 3LL * num_sms();  // ~12 warps per SM
+        if (ctas < want) S = cdiv(want, ctas);
+    }
+    const int64_t tiles = cdiv(L, T);
+    S = std::max<int64_t>(1, std::min<int64_t>(S, std::max<int64_t>(1, tiles / 4)));  // >= 4 tiles per segment
+    g.seg_len = cdiv(tiles, S) * T;
+    g.n_seg = cdiv(L, g.seg_len);
+    // workspace: per-segment maps [S, B, D, 16] and delta sums [S, B, D]
+    g.ws_bytes = (int64_t)(align_up((size_t)g.n_seg * B * D * NST * 4) + align_up((size_t)g.n_seg * B * D * 4));
+    return g;
+}
+
+struct Maps {
+    CUtensorMap m[7];
+};
+
+template <typename IO>
+static bool enc_act(CUtensorMap* m, const void* p, int64_t B, int64_t L, int64_t D) {
+    return tma::encode_3d(m, p, sizeof(IO), B, L, D, T, CH);
+}
+static bool enc_bc(CUtensorMap* m, const void* p, int64_t B, int64_t L) {
+    return tma::encode_3d(m, p, 4, B, L, NST, T, NST);
+}
+
+template <typename K>
+static int set_smem(K kfn, size_t bytes, const char* what) {
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+        set_error("%s: cannot reserve %zu bytes of shared memory", what, bytes);
+        return LRX_ERR_CUDA;
+    }
+    return LRX_OK;
+}
+
+#define S6V3_MAP(expr)                                                                        \
+    do {                                                                                      \
+        if (!(expr)) {                                                                        \
+            set_error("s6: TMA descriptor rejected (operands must be 16-byte aligned): %s", #expr); \
+            return LRX_ERR_VALUE;                                                             \
+        }                                                                                     \
+    } while (0)
+
+struct WS {
+    float* X;
+    float* SD;
+};
+static WS carve(void* ws, const Geo& g, int64_t B, int64_t D) {
+    Carver cv(ws);
+    WS w;
+    w.X = cv.take<float>((size_t)g.n_seg * B * D * NST);
+    w.SD = cv.take<float>((size_t)g.n_seg * B * D);
+    return w;
+}
+
+template <typename IO>
+static int fwd_agg_launch(const void* u, const void* pre, const void* bd, const void* al, const void* Bk, WS w,
+                          const Geo& g, int64_t B, int64_t L, int64_t D, int s_lo, int s_hi, cudaStream_t st) {
+    if (s_hi <= s_lo) return LRX_OK;
+    CUtensorMap mu, mp, mB;
+    S6V3_MAP(enc_act<IO>(&mu, u, B, L, D));
+    S6V3_MAP(enc_act<float>(&mp, pre, B, L, D));
+    S6V3_MAP(enc_bc(&mB, Bk, B, L));
+    const size_t smem = Lay<IO>::smem_fagg();
+    if (int e = set_smem(fwd_agg_kernel<IO>, smem, "s6 fwd agg")) return e;
+    fwd_agg_kernel<IO><<<dim3((unsigned)g.n_dblk, (unsigned)B, (unsigned)(s_hi - s_lo)), THREADS, smem, st>>>(
+        mu, mp, mB, (const float*)bd, (const float*)al, w.X, w.SD, B, L, D, g.seg_len, s_lo);
+    return launched("lrx_s6_fwd_agg/v3");
+}
+
+template <typename IO>
+static int bwd_agg_launch(const void* gy, const void* pre, const void* bd, const void* al, const void* Ck, WS w,
+                          const Geo& g, int64_t B, int64_t L, int64_t D, int s_lo, int s_hi, cudaStream_t st) {
+    if (s_hi <= s_lo) return LRX_OK;
+    CUtensorMap mg, mp, mC;
+    S6V3_MAP(enc_act<IO>(&mg, gy, B, L, D));
+    S6V3_MAP(enc_act<float>(&mp, pre, B, L, D));
+    S6V3_MAP(enc_bc(&mC, Ck, B, L));
+    const size_t smem = Lay<IO>::smem_bagg();
+    if (int e = set_smem(bwd_agg_kernel<IO>, smem, "s6 bwd agg")) return e;
+    bwd_agg_kernel<IO><<<dim3((unsigned)g.n_dblk, (unsigned)B, (unsigned)(s_hi - s_lo)), THREADS, smem, st>>>(
+        mg, mp, mC, (const float*)bd, (const float*)al, w.X, w.SD, B, L, D, g.seg_len, s_lo);
+    return launched("lrx_s6_bwd_agg/v3");
+}
+
+template <typename IO>
+int fwd(const void* u, const void* pre, const void* bd, const void* al, const void* Bk, const void* Ck,
+        const void* Dk, const void* x0, void* y, void* ckpt, int64_t B, int64_t L, int64_t D, void* ws,
+        int64_t ws_bytes, int flags, cudaStream_t st) {
+    const Geo g = geometry(B, L, D);
+    LRX_REQUIRE(ws != nullptr && ws_bytes >= g.ws_bytes, LRX_ERR_VALUE, "s6: workspace of %lld bytes needed",
+                (long long)g.ws_bytes);
+    const WS w = carve(ws, g, B, D);
+    if (g.n_seg > 1 && !(flags & LRX_S6_REUSE_AGG))
+        if (int e = fwd_agg_launch<IO>(u, pre, bd, al, Bk, w, g, B, L, D, 0, (int)g.n_seg - 1, st)) return e;
+    CUtensorMap mu, mp, mB, mC, my;
+    S6V3_MAP(enc_act<IO>(&mu, u, B, L, D));
+    S6V3_MAP(enc_act<float>(&mp, pre, B, L, D));
+    S6V3_MAP(enc_bc(&mB, Bk, B, L));
+    S6V3_MAP(enc_bc(&mC, Ck, B, L));
+    S6V3_MAP(enc_act<IO>(&my, y, B, L, D));
+    const size_t smem = Lay<IO>::smem_fwd();
+    if (int e = set_smem(fwd_kernel<IO>, smem, "s6 fwd")) return e;
+    fwd_kernel<IO><<<dim3((unsigned)g.n_dblk, (unsigned)B, (unsigned)g.n_seg), THREADS, smem, st>>>(
+        mu, mp, mB, mC, my, (const float*)bd, (const float*)al, (const float*)Dk, (const float*)x0, w.X, w.SD,
+        (float*)ckpt, B, L, D, g.seg_len, (int)g.n_ck);
+    return launched("lrx_s6_fwd/v3");
+}
+
+template <typename IO>
+int bwd(const void* u, const void* pre, const void* bd, const void* al, const void* Bk, const void* Ck,
+        const void* Dk, const void* ckpt, const void* gy, const void* h_in, void* gu, void* gpre, void* gBp,
+        void* gCp, void* gap, void* gDp, void* gbp, void* h_out, int64_t B, int64_t L, int64_t D, void* ws,
+        int64_t ws_bytes, int flags, cudaStream_t st) {
+    const Geo g = geometry(B, L, D);
+    LRX_REQUIRE(ws != nullptr && ws_bytes >= g.ws_bytes, LRX_ERR_VALUE, "s6: workspace of %lld bytes needed",
+                (long long)g.ws_bytes);
+    const WS w = carve(ws, g, B, D);
+    if (g.n_seg > 1 && !(flags & LRX_S6_REUSE_AGG))
+        if (int e = bwd_agg_launch<IO>(gy, pre, bd, al, Ck, w, g, B, L, D, 1, (int)g.n_seg, st)) return e;
+    CUtensorMap mu, mp, mg, mB, mC, mgu, mgp;
+    S6V3_MAP(enc_act<IO>(&mu, u, B, L, D));
+    S6V3_MAP(enc_act<float>(&mp, pre, B, L, D));
+    S6V3_MAP(enc_act<IO>(&mg, gy, B, L, D));
+    S6V3_MAP(enc_bc(&mB, Bk, B, L));
+    S6V3_MAP(enc_bc(&mC, Ck, B, L));
+    S6V3_MAP(enc_act<IO>(&mgu, gu, B, L, D));
+    S6V3_MAP(enc_act<float>(&mgp, gpre, B, L, D));
+    const size_t smem = Lay<IO>::smem_bwd();
+    if (int e = set_smem(bwd_kernel<IO>, smem, "s6 bwd")) return e;
+    bwd_kernel<IO><<<dim3((unsigned)g.n_dblk, (unsigned)B, (unsigned)g.n_seg), THREADS, smem, st>>>(
+        mu, mp, mg, mB, mC, mgu, mgp, (const float*)bd, (const float*)al, (const float*)Dk, (const float*)ckpt,
+        (const float*)h_in, w.X, w.SD, (float*)gBp, (float*)gCp, (float*)gap, (float*)gDp, (float*)gbp,
+        (float*)h_out, B, L, D, g.seg_len, (int)g.n_ck);
+    return launched("lrx_s6_bwd/v3");
+}
+
+// Whole-slice maps for the sequence-parallel exchange; leaves every
+// segment's map in ws for a following call with LRX_S6_REUSE_AGG.
+template <typename IO>
+int fwd_carry(const void* u, const void* pre, const void* bd, const void* al, const void* Bk, void* x_agg,
+              void* sd_agg, int64_t B, int64_t L, int64_t D, void* ws, int64_t ws_bytes, cudaStream_t st) {
+    const Geo g = geometry(B, L, D);
+    LRX_REQUIRE(ws != nullptr && ws_bytes >= g.ws_bytes, LRX_ERR_VALUE, "s6: workspace of %lld bytes needed",
+                (long long)g.ws_bytes);
+    const WS w = carve(ws, g, B, D);
+    if (int e = fwd_agg_launch<IO>(u, pre, bd, al, Bk, w, g, B, L, D, 0, (int)g.n_seg, st)) return e;
+    const int64_t n = B * D * NST;
+    fold_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const float*)al, w.X, w.SD, (float*)x_agg, (float*)sd_agg,
+                                                        B, D, (int)g.n_seg, +1);
+    return launched("lrx_s6_fold/v3");
+}
+
+template <typename IO>
+int bwd_carry(const void* gy, const void* pre, const void* bd, const void* al, const void* Ck, void* h_agg,
+              void* sd_agg, int64_t B, int64_t L, int64_t D, void* ws, int64_t ws_bytes, cudaStream_t st) {
+    const Geo g = geometry(B, L, D);
+    LRX_REQUIRE(ws != nullptr && ws_bytes >= g.ws_bytes, LRX_ERR_VALUE, "s6: workspace of %lld bytes needed",
+                (long long)g.ws_bytes);
+    const WS w = carve(ws, g, B, D);
+    if (int e = bwd_agg_launch<IO>(gy, pre, bd, al, Ck, w, g, B, L, D, 0, (int)g.n_seg, st)) return e;
+    const int64_t n = B * D * NST;
+    fold_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const float*)al, w.X, w.SD, (float*)h_agg, (float*)sd_agg,
+                                                        B, D, (int)g.n_seg, -1);
+    return launched("lrx_s6_fold/v3");
+}
+
+template int fwd<__nv_bfloat16>(const void*, const void*, const void*, const void*, const void*, const void*,
+                                const void*, const void*, void*, void*, int64_t, int64_t, int64_t, void*, int64_t,
+                                int, cudaStream_t);
+template int fwd<float>(const void*, const void*, const void*, const void*, const void*, const void*, const void*,
+                        const void*, void*, void*, int64_t, int64_t, int64_t, void*, int64_t, int, cudaStream_t);
+template int bwd<__nv_bfloat16>(const void*, const void*, const void*, const void*, const void*, const void*,
+                                const void*, const void*, const void*, const void*, void*, void*, void*, void*, void*,
+                                void*, void*, void*, int64_t, int64_t, int64_t, void*, int64_t, int, cudaStream_t);
+template int bwd<float>(const void*, const void*, const void*, const void*, const void*, const void*, const void*,
+                        const void*, const void*, const void*, void*, void*, void*, void*, void*, void*, void*, void*,
+                        int64_t, int64_t, int64_t, void*, int64_t, int, cudaStream_t);
+template int fwd_carry<__nv_bfloat16>(const void*, const void*, const void*, const void*, const void*, void*, void*,
+                                      int64_t, int64_t, int64_t, void*, int64_t, cudaStream_t);
+template int fwd_carry<float>(const void*, const void*, const void*, const void*, const void*, void*, void*,
+                              int64_t, int64_t, int64_t, void*, int64_t, cudaStream_t);
+template int bwd_carry<__nv_bfloat16>(const void*, const void*, const void*, const void*, const void*, void*, void*,
+                                      int64_t, int64_t, int64_t, void*, int64_t, cudaStream_t);
+template int bwd_carry<float>(const void*, const void*, const void*, const void*, const void*, void*, void*,
+                              int64_t, int64_t, int64_t, void*, int64_t, cudaStream_t);
+
+}  // namespace s6v3
+}  // namespace lrx

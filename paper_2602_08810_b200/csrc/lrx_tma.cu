@@ -42,5 +42,27 @@ bool encode_2d(CUtensorMap* map, const void* base, int esize, uint64_t rows, uin
     return r == CUDA_SUCCESS;
 }
 
+bool encode_3d(CUtensorMap* map, const void* base, int esize, uint64_t d2, uint64_t d1, uint64_t d0,
+               uint32_t box1, uint32_t box0) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((d0 * esize) & 15) || ((box0 * esize) & 15)) return false;
+    CUtensorMapDataType dt;
+    switch (esize) {
+        case 2: dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16; break;
+        case 4: dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32; break;
+        case 8: dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT64; break;
+        default: return false;
+    }
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {d0 * (cuuint64_t)esize, d1 * d0 * (cuuint64_t)esize};
+    cuuint32_t box[3] = {box0, box1, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 }  // namespace tma
 }  // namespace lrx

@@ -68,12 +68,45 @@ __device__ __forceinline__ void load_2d(void* dst, const CUtensorMap* m, int c0,
         : "memory");
 }
 
+// 3D tile load: box origin (c0, c1, c2) -> dst, completion on bar.  Elements
+// outside the tensor are zero-filled (and still count toward complete_tx).
+__device__ __forceinline__ void load_3d(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// 3D tile store smem -> global (bulk group); out-of-bounds parts of the box
+// are clipped.  Writers must fence.proxy.async before the issuing barrier.
+__device__ __forceinline__ void store_3d(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ---------------------------------------------------------------- host
 // Encode a row-major 2D tensor [rows, cols] of `esize`-byte elements with a
 // box of [box_rows, box_cols].  Returns false when the driver entry point is
 // unavailable or the encode fails.
 bool encode_2d(CUtensorMap* map, const void* base, int esize, uint64_t rows, uint64_t cols, uint32_t box_rows,
                uint32_t box_cols);
+
+// Encode a row-major 3D tensor [d2, d1, d0] (d0 contiguous) with a box of
+// [1, box1, box0]; out-of-bounds box elements read as zero.
+bool encode_3d(CUtensorMap* map, const void* base, int esize, uint64_t d2, uint64_t d1, uint64_t d0,
+               uint32_t box1, uint32_t box0);
 
 }  // namespace tma
 }  // namespace lrx

@@ -33,7 +33,7 @@ import torch
 from . import ops
 from .numerics import softplus
 
-__all__ = ["shard_range", "compose_prefix", "compose_suffix", "SeqParallelS6"]
+__all__ = ["shard_range", "compose_prefix", "compose_suffix", "SeqParallelS6", "LongS6"]
 
 
 def shard_range(n: int, world: int, rank: int):
@@ -151,44 +151,35 @@ class SeqParallelS6:
 
 
 # ---------------------------------------------------------------------------
-# Hierarchical sequence parallelism: sub-slices as a batch inside each GPU,
-# carry exchange across ranks.  C5 has B*D = 2048 channels -- a single GPU
-# needs ~100x more independent lanes -- so each rank cuts its slice into `sub`
-# pieces, runs them as one batch, and composes the carries itself.
-
-def _fold(A, X):
-    """(A_total, X_total) of consecutive pieces [G, ...] (left to right)."""
-    a, x = A[0], X[0]
-    for k in range(1, A.shape[0]):
-        x = A[k] * x + X[k]
-        a = A[k] * a
-    return a, x
-
-
-def _as_batch(t, sub):
-    """[1, L, ...] -> [sub, L/sub, ...] (L divisible by sub)."""
-    return t.reshape(sub, t.shape[1] // sub, *t.shape[2:])
-
+# Sequence parallelism for B = 1, long L (config C5), two levels:
+#   * inside a GPU the kernels cut the rank's slice into time segments that run
+#     concurrently (C5 has B*D = 2048 channels; a GPU needs ~30x more
+#     independent lanes), composing the segment maps themselves (lrx_s6v3.cu);
+#   * across GPUs each rank computes its slice's map once (lrx_s6_fwd_carry:
+#     x_agg, sum delta -- 2 x 131 KB at C5), the maps are all-gathered over
+#     NVLink, each rank composes the carry entering its slice, and the main
+#     pass reuses the per-segment maps already in the workspace
+#     (LRX_S6_REUSE_AGG), so a rank does one aggregate pass + one main pass,
+#     the same work as on a single GPU.  The backward mirrors it right to left.
 
 class LongS6:
     """Sequence-parallel selective scan for B = 1, long L (config C5).
 
-    forward/backward operate on this rank's contiguous slice [1, Ls, D] with
-    Ls divisible by `sub`; with `group=None` the slice is the whole sequence
-    (single GPU)."""
+    forward/backward operate on this rank's contiguous slice [1, Ls, D]; with
+    `group=None` and no initialised process group the slice is the whole
+    sequence (single GPU)."""
 
-    def __init__(self, sub=64, group=None, scan_fwd=None, scan_bwd=None):
-        self.sub = sub
+    def __init__(self, group=None, impl=None):
+        """`impl` provides s6_fwd_carry / s6_scan_fwd / s6_bwd_carry / s6_scan_bwd /
+        S6_REUSE_AGG (default: the device operators in ops.py); injectable so
+        the exchange protocol can be exercised by CPU tests."""
         self.group = group
-        self.scan_fwd = scan_fwd or ops.s6_scan_fwd
-        self.scan_bwd = scan_bwd or ops.s6_scan_bwd
+        self.ops = impl or ops
 
     def _rank_world(self):
-        if self.group is None:
-            import torch.distributed as dist
-            if not (dist.is_available() and dist.is_initialized()):
-                return 0, 1
         import torch.distributed as dist
+        if not (dist.is_available() and dist.is_initialized()):
+            return 0, 1
         return dist.get_rank(self.group), dist.get_world_size(self.group)
 
     def _gather(self, t):
@@ -199,51 +190,58 @@ class LongS6:
         dist.all_gather_into_tensor(out, t, group=self.group)
         return out.view(world, *t.shape)
 
+    @staticmethod
+    def _prod(a_log, sd):
+        """prod abar over a slice = exp(a * sum delta), [B, D, N]."""
+        return torch.exp(-torch.exp(a_log)[None] * sd[..., None])
+
     def forward(self, u, pre, b_delta, a_log, Bk, Ck, Dskip):
-        S = self.sub
-        ub, pb, bb, cb = (_as_batch(t, S) for t in (u, pre, Bk, Ck))
-        _, ck0 = self.scan_fwd(ub, pb, b_delta, a_log, bb, cb, Dskip)          # pass 1: zero carries
-        A = _slice_product(pb, b_delta, a_log)                                  # [S, D, N]
-        X = ck0[:, -1]                                                           # [S, D, N]
+        o = self.ops
         rank, world = self._rank_world()
-        x_in = torch.zeros_like(X[0])
-        if world > 1:
-            Ar, Xr = _fold(A, X)
-            AX = self._gather(torch.stack((Ar, Xr)))                            # [G, 2, D, N]
-            x_in = compose_prefix(AX[:, 0], AX[:, 1], rank)
-            A_rank = AX[:, 0]
-        else:
-            A_rank = None
-        x0 = torch.empty_like(X)
-        x = x_in
-        for k in range(S):                                                       # sub-slice entering states
-            x0[k] = x
-            x = A[k] * x + X[k]
-        y, ckpt = self.scan_fwd(ub, pb, b_delta, a_log, bb, cb, Dskip, x0=x0)   # pass 2
-        return y.reshape(u.shape), {"ckpt": ckpt, "A": A, "A_rank": A_rank}
+        if world == 1:
+            y, ckpt = o.s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip)
+            return y, {"ckpt": ckpt}
+        x_agg, sd, ws = o.s6_fwd_carry(u, pre, b_delta, a_log, Bk)
+        AX = self._gather(torch.stack((self._prod(a_log, sd), x_agg)))       # [G, 2, B, D, N]
+        x_in = compose_prefix(AX[:, 0], AX[:, 1], rank).contiguous()
+        y, ckpt = o.s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=x_in, ws=ws, flags=o.S6_REUSE_AGG)
+        return y, {"ckpt": ckpt, "A": AX[:, 0]}
 
     def backward(self, ctx, u, pre, b_delta, a_log, Bk, Ck, Dskip, gy):
-        S = self.sub
-        ub, pb, bb, cb, gb = (_as_batch(t, S) for t in (u, pre, Bk, Ck, gy))
-        r0 = self.scan_bwd(ub, pb, b_delta, a_log, bb, cb, Dskip, ctx["ckpt"], gb, want_h_out=True)
-        A, H = ctx["A"], r0["h_out"]
+        o = self.ops
         rank, world = self._rank_world()
-        h_in = torch.zeros_like(H[0])
-        if world > 1:
-            Ar = A[0]
-            Hr = H[S - 1]
-            for k in range(S - 2, -1, -1):                                       # fold right to left
-                Hr = A[k] * Hr + H[k]
-                Ar = A[k] * Ar
-            Hs = self._gather(Hr)
-            h_in = compose_suffix(ctx["A_rank"], Hs, rank)
-        hin = torch.empty_like(H)
-        h = h_in
-        for k in range(S - 1, -1, -1):
-            hin[k] = h
-            h = A[k] * h + H[k]
-        r = self.scan_bwd(ub, pb, b_delta, a_log, bb, cb, Dskip, ctx["ckpt"], gb, h_in=hin)
-        # per-time outputs back to [1, Ls, ...]; parameter grads are already
-        # summed over the sub-slices (the batch) by the kernel reductions
-        return {k: (v.reshape(1, -1, *v.shape[2:]) if k in ("gu_local", "gpre", "gBk", "gCk") else v)
-                for k, v in r.items() if k != "h_out"}
+        if world == 1:
+            return o.s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ctx["ckpt"], gy)
+        h_agg, _, ws = o.s6_bwd_carry(gy, pre, b_delta, a_log, Ck)
+        H = self._gather(h_agg)
+        h_in = compose_suffix(ctx["A"], H, rank).contiguous()
+        # per-rank parameter-gradient contributions: the caller sums them across ranks
+        return o.s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ctx["ckpt"], gy, h_in=h_in, ws=ws,
+                             flags=o.S6_REUSE_AGG)
+
+    @staticmethod
+    def simulate(G, u, pre, b_delta, a_log, Bk, Ck, Dskip, gy):
+        """Run the two-level protocol with the sequence split into G rank slices
+        on one device (the all-gathers become stacks).  Returns (y, grads)
+        assembled over slices, parameter grads summed."""
+        L = u.shape[1]
+        cuts = [shard_range(L, G, r) for r in range(G)]
+        sl = [(lambda t, s=s, e=e: t[:, s:e].contiguous()) for s, e in cuts]
+        fc = [ops.s6_fwd_carry(sl[r](u), sl[r](pre), b_delta, a_log, sl[r](Bk)) for r in range(G)]
+        A = torch.stack([LongS6._prod(a_log, sd) for _, sd, _ in fc])
+        X = torch.stack([x for x, _, _ in fc])
+        ys, ckpts = [], []
+        for r in range(G):
+            y, c = ops.s6_scan_fwd(sl[r](u), sl[r](pre), b_delta, a_log, sl[r](Bk), sl[r](Ck), Dskip,
+                                   x0=compose_prefix(A, X, r).contiguous(), ws=fc[r][2], flags=ops.S6_REUSE_AGG)
+            ys.append(y)
+            ckpts.append(c)
+        bc = [ops.s6_bwd_carry(sl[r](gy), sl[r](pre), b_delta, a_log, sl[r](Ck)) for r in range(G)]
+        H = torch.stack([h for h, _, _ in bc])
+        outs = [ops.s6_scan_bwd(sl[r](u), sl[r](pre), b_delta, a_log, sl[r](Bk), sl[r](Ck), Dskip, ckpts[r], sl[r](gy),
+                                h_in=compose_suffix(A, H, r).contiguous(), ws=bc[r][2], flags=ops.S6_REUSE_AGG)
+                for r in range(G)]
+        grads = {k: torch.cat([o[k] for o in outs], dim=1) for k in ("gu_local", "gpre", "gBk", "gCk")}
+        for k in ("ga_log", "gD", "gb_delta"):
+            grads[k] = sum(o[k] for o in outs)
+        return torch.cat(ys, dim=1), grads

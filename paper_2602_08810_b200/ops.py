@@ -13,12 +13,14 @@ current CUDA device; outputs are allocated here, workspaces are transient.
 """
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
 from . import _lib
 
-__all__ = ["rglru_scan_fwd", "rglru_scan_bwd", "s6_geometry", "s6_scan_fwd", "s6_scan_bwd", "mimo_scan_fwd",
-           "mimo_scan_bwd", "reduce_rows"]
+__all__ = ["rglru_scan_fwd", "rglru_scan_bwd", "s6_geometry", "s6_scan_fwd", "s6_scan_bwd", "s6_fwd_carry",
+           "s6_bwd_carry", "mimo_scan_fwd", "mimo_scan_bwd", "reduce_rows"]
 
 
 def reduce_rows(part, rows, cols):
@@ -71,54 +73,100 @@ def rglru_scan_bwd(u, qr, qi, lambda_param, b_r, b_i, ckpt, gy, y=None):
 # ---------------------------------------------------------------------------
 # S6
 
-def s6_geometry(io_dtype, L, D, N):
-    ck, nck, ndb = _lib.i64(), _lib.i64(), _lib.i64()
-    _lib.check(_lib.lib().lrx_s6_ckpt_len(_lib.code_of(io_dtype), L, D, N, _lib.ref(ck), _lib.ref(nck),
-                                          _lib.ref(ndb)))
-    return ck.value, nck.value, ndb.value
+S6_REUSE_AGG = 1
 
 
-def s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=None):
+def s6_geometry(io_dtype, B, L, D, N):
+    """dict(ckpt_len, n_ckpt, n_dblk, n_seg, part_rows, ws_bytes) for these extents."""
+    g = (ctypes.c_int64 * 6)()
+    _lib.check(_lib.lib().lrx_s6_geometry(_lib.code_of(io_dtype), B, L, D, N, g))
+    return dict(zip(("ckpt_len", "n_ckpt", "n_dblk", "n_seg", "part_rows", "ws_bytes"), (int(v) for v in g)))
+
+
+def _s6_ws(geo, device, ws):
+    if ws is not None:
+        return ws
+    return _lib.workspace(geo["ws_bytes"], device)
+
+
+def s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=None, ws=None, flags=0, ckpt=True):
     """Selective scan; u [B, L, D] (f32/f64/bf16), pre [B, L, D] and Bk/Ck
     [B, L, N] in compute precision.  x0 [B, D, N] optionally seeds the state.
-    Returns (y, ckpt); ckpt[:, -1] is the final state [B, D, N]."""
+    Returns (y, ckpt); ckpt[:, -1] is the final state [B, D, N] (None with
+    ckpt=False: inference, no checkpoint writes).  `ws`/`flags`: workspace
+    holding per-segment maps from s6_fwd_carry (flags=S6_REUSE_AGG)."""
     B, L, D = u.shape
     N = Bk.shape[-1]
-    _, nck, _ = s6_geometry(u.dtype, L, D, N)
+    geo = s6_geometry(u.dtype, B, L, D, N)
     y = torch.empty_like(u)
-    ckpt = torch.empty((B, nck, D, N), dtype=a_log.dtype, device=u.device)
+    ck = torch.empty((B, geo["n_ckpt"], D, N), dtype=a_log.dtype, device=u.device) if ckpt else None
+    ws = _s6_ws(geo, u.device, ws)
     _lib.check(_lib.lib().lrx_s6_fwd(_lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(pre), _lib.ptr(b_delta),
                                      _lib.ptr(a_log), _lib.ptr(Bk), _lib.ptr(Ck), _lib.ptr(Dskip), _lib.ptr(x0),
-                                     _lib.ptr(y), _lib.ptr(ckpt), B, L, D, N, _lib.stream()))
-    return y, ckpt
+                                     _lib.ptr(y), _lib.ptr(ck), B, L, D, N, _lib.ptr(ws), ws.numel(), flags,
+                                     _lib.stream()))
+    return y, ck
 
 
-def s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in=None, want_h_out=False):
+def s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in=None, want_h_out=False, ws=None, flags=0):
     """Pullback of s6_scan_fwd.  Returns dict: gu_local (D gy + delta sum_n g B),
     gpre (d/d pre) [B, L, D]; gBk, gCk [B, L, N]; ga_log [D, N]; gD, gb_delta [D];
     with want_h_out also h_out [B, D, N] = d loss / d x0.  h_in [B, D, N] is
     the cotangent carry entering from the right (sequence-parallel mode)."""
     B, L, D = u.shape
     N = Bk.shape[-1]
-    _, nck, ndb = s6_geometry(u.dtype, L, D, N)
+    geo = s6_geometry(u.dtype, B, L, D, N)
+    ndb, prow = geo["n_dblk"], geo["part_rows"]
     f = dict(dtype=a_log.dtype, device=u.device)
     gu, gpre = torch.empty_like(u), torch.empty(u.shape, **f)
     gBp, gCp = torch.empty((ndb, B * L * N), **f), torch.empty((ndb, B * L * N), **f)
-    gap, gDp, gbp = torch.empty((B, D * N), **f), torch.empty((B, D), **f), torch.empty((B, D), **f)
+    gap, gDp, gbp = torch.empty((prow, D * N), **f), torch.empty((prow, D), **f), torch.empty((prow, D), **f)
     h_out = torch.empty((B, D, N), **f) if want_h_out else None
+    ws = _s6_ws(geo, u.device, ws)
     _lib.check(_lib.lib().lrx_s6_bwd(
         _lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(pre), _lib.ptr(b_delta), _lib.ptr(a_log), _lib.ptr(Bk),
         _lib.ptr(Ck), _lib.ptr(Dskip), _lib.ptr(ckpt), _lib.ptr(gy), _lib.ptr(h_in), _lib.ptr(gu), _lib.ptr(gpre),
         _lib.ptr(gBp), _lib.ptr(gCp), _lib.ptr(gap), _lib.ptr(gDp), _lib.ptr(gbp), _lib.ptr(h_out), B, L, D, N,
-        _lib.stream()))
+        _lib.ptr(ws), ws.numel(), flags, _lib.stream()))
     out = {"gu_local": gu, "gpre": gpre,
            "gBk": reduce_rows(gBp, ndb, B * L * N).reshape(B, L, N),
            "gCk": reduce_rows(gCp, ndb, B * L * N).reshape(B, L, N),
-           "ga_log": reduce_rows(gap, B, D * N).reshape(D, N),
-           "gD": reduce_rows(gDp, B, D), "gb_delta": reduce_rows(gbp, B, D)}
+           "ga_log": reduce_rows(gap, prow, D * N).reshape(D, N),
+           "gD": reduce_rows(gDp, prow, D), "gb_delta": reduce_rows(gbp, prow, D)}
     if want_h_out:
         out["h_out"] = h_out
     return out
+
+
+def s6_fwd_carry(u, pre, b_delta, a_log, Bk, ws=None):
+    """The slice's forward map for the sequence-parallel exchange:
+    x_end = exp(a * sd) * x_in + x_agg.  Returns (x_agg [B, D, N], sd [B, D], ws);
+    pass ws with flags=S6_REUSE_AGG to the following s6_scan_fwd."""
+    B, L, D = u.shape
+    N = Bk.shape[-1]
+    geo = s6_geometry(u.dtype, B, L, D, N)
+    f = dict(dtype=a_log.dtype, device=u.device)
+    x_agg, sd = torch.empty((B, D, N), **f), torch.empty((B, D), **f)
+    ws = _s6_ws(geo, u.device, ws)
+    _lib.check(_lib.lib().lrx_s6_fwd_carry(_lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(pre), _lib.ptr(b_delta),
+                                           _lib.ptr(a_log), _lib.ptr(Bk), _lib.ptr(x_agg), _lib.ptr(sd), B, L, D,
+                                           N, _lib.ptr(ws), ws.numel(), _lib.stream()))
+    return x_agg, sd, ws
+
+
+def s6_bwd_carry(gy, pre, b_delta, a_log, Ck, ws=None):
+    """The slice's cotangent map (right to left): h_left = exp(a * sd) * h_right + h_agg.
+    Returns (h_agg [B, D, N], sd [B, D], ws) for s6_scan_bwd(flags=S6_REUSE_AGG)."""
+    B, L, D = gy.shape
+    N = Ck.shape[-1]
+    geo = s6_geometry(gy.dtype, B, L, D, N)
+    f = dict(dtype=a_log.dtype, device=gy.device)
+    h_agg, sd = torch.empty((B, D, N), **f), torch.empty((B, D), **f)
+    ws = _s6_ws(geo, gy.device, ws)
+    _lib.check(_lib.lib().lrx_s6_bwd_carry(_lib.code_of(gy.dtype), _lib.ptr(gy), _lib.ptr(pre), _lib.ptr(b_delta),
+                                           _lib.ptr(a_log), _lib.ptr(Ck), _lib.ptr(h_agg), _lib.ptr(sd), B, L, D,
+                                           N, _lib.ptr(ws), ws.numel(), _lib.stream()))
+    return h_agg, sd, ws
 
 
 # ---------------------------------------------------------------------------

@@ -41,12 +41,18 @@ def test_host_queries_without_gpu():
     ck, nc = ctypes.c_int64(), ctypes.c_int64()
     assert lib.lrx_rglru_chunking(_lib.F32, 1000, ctypes.byref(ck), ctypes.byref(nc)) == 0
     assert ck.value * nc.value >= 1000
-    ndb = ctypes.c_int64()
-    assert lib.lrx_s6_ckpt_len(_lib.BF16, 8192, 1536, 16, ctypes.byref(ck), ctypes.byref(nc), ctypes.byref(ndb)) == 0
-    assert nc.value == -(-8192 // ck.value) + 1 and ndb.value >= 1
+    geo = (ctypes.c_int64 * 6)()
+    assert lib.lrx_s6_geometry(_lib.BF16, 16, 8192, 1536, 16, geo) == 0
+    ck, nck, ndb, nseg, prow, ws = geo
+    assert nck == -(-8192 // ck) + 1 and ndb == 1536 // 64 and prow == nseg * 16 and ws > 0
+    # B=1 long sequence: time segments fill the GPU
+    assert lib.lrx_s6_geometry(_lib.BF16, 1, 2 ** 20, 2048, 16, geo) == 0
+    assert geo[3] > 1 and geo[4] == geo[3]
+    # f64 runs the generic kernels (one segment, no workspace)
+    assert lib.lrx_s6_geometry(_lib.F64, 2, 100, 24, 16, geo) == 0
+    assert geo[3] == 1 and geo[4] == 2 and geo[5] == 0
     # d_state beyond the compiled range is a loud, typed error
-    assert lib.lrx_s6_ckpt_len(_lib.F32, 10, 10, 65, ctypes.byref(ck), ctypes.byref(nc),
-                               ctypes.byref(ndb)) == _lib.ERR_UNSUPPORTED
+    assert lib.lrx_s6_geometry(_lib.F32, 1, 10, 10, 65, geo) == _lib.ERR_UNSUPPORTED
     assert b"65" in lib.lrx_last_error()
 
 

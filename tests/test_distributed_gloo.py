@@ -83,6 +83,34 @@ def _bwd(u, pre, b_delta, a_log, Bk, Ck, D, ckpt, gy, h_in=None, want_h_out=Fals
     return out
 
 
+class _CpuOps:
+    """Test-only stand-in for ops.py's carry API (ws / flags are ignored)."""
+    S6_REUSE_AGG = 1
+
+    @staticmethod
+    def s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, D, x0=None, ws=None, flags=0):
+        return _fwd(u, pre, b_delta, a_log, Bk, Ck, D, x0=x0)
+
+    @staticmethod
+    def s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, D, ckpt, gy, h_in=None, ws=None, flags=0):
+        return _bwd(u, pre, b_delta, a_log, Bk, Ck, D, ckpt, gy, h_in=h_in)
+
+    @staticmethod
+    def s6_fwd_carry(u, pre, b_delta, a_log, Bk, ws=None):
+        zero = torch.zeros_like(Bk)
+        _, ck = _fwd(u, pre, b_delta, a_log, Bk, zero, torch.zeros(u.shape[-1], dtype=u.dtype))
+        return ck[:, -1], torch.nn.functional.softplus(pre + b_delta).sum(1), None
+
+    @staticmethod
+    def s6_bwd_carry(gy, pre, b_delta, a_log, Ck, ws=None):
+        a = -torch.exp(a_log)
+        delta = torch.nn.functional.softplus(pre + b_delta)
+        h = torch.zeros((gy.shape[0], gy.shape[2], a.shape[1]), dtype=gy.dtype)
+        for t in range(gy.shape[1] - 1, -1, -1):
+            h = torch.exp(delta[:, t, :, None] * a) * (gy[:, t, :, None] * Ck[:, t, None, :] + h)
+        return h, delta.sum(1), None
+
+
 def _problem(L=24, m=3, n=4):
     p = port.init_params("s6", m, n, seed=3)
     rng = port.Rng(7)
@@ -144,7 +172,7 @@ def _worker_long(rank, world, port_no, q):
         pb, p, u, pre = _problem(L=36)
         s, e = shard_range(36, world, rank)
         sl = {k: (v[:, s:e].contiguous() if k in ("u", "pre", "Bk", "Ck", "gy") else v) for k, v in pb.items()}
-        ls = LongS6(sub=3, scan_fwd=_fwd, scan_bwd=_bwd)
+        ls = LongS6(impl=_CpuOps)
         args = (sl["u"], sl["pre"], sl["b_delta"], sl["a_log"], sl["Bk"], sl["Ck"], sl["D"])
         y, ctx = ls.forward(*args)
         r = ls.backward(ctx, *args, sl["gy"])
