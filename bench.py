@@ -42,6 +42,14 @@ import time
 
 import numpy as np
 
+# The step allocates its outputs like any torch op (y, checkpoints, gradients:
+# up to 1.6 GB each).  With large blocks unsplittable the caching allocator
+# reuses them exactly step after step instead of splitting a freed block for
+# a smaller request and calling cudaMalloc (host-blocking, ~3 ms per GB)
+# inside the timed region.
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "max_split_size_mb:256")
+
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -239,8 +247,10 @@ def run_gpu(args, w, rank, world, device):
         if world > 1:
             dist.barrier()
 
-    for _ in range(args.warmup):
-        bwd(fwd())
+    ctx = None
+    for _ in range(args.warmup):  # same liveness pattern as the timed loop (allocator steady state)
+        ctx = fwd()
+        bwd(ctx)
     torch.cuda.synchronize()
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
@@ -261,6 +271,12 @@ def run_gpu(args, w, rank, world, device):
         torch.cuda.synchronize()
         barrier()
     launches = _lib.launch_count() - n0
+    if os.environ.get("LRX_BENCH_VERBOSE"):
+        for k, e in enumerate(ev):
+            print(f"step {k}: fwd {e[0].elapsed_time(e[1]):.3f} ms, bwd {e[1].elapsed_time(e[2]):.3f} ms",
+                  file=sys.stderr)
+        print("allocator:", {k: v for k, v in torch.cuda.memory_stats().items()
+                             if k in ("num_device_alloc", "num_device_free", "num_alloc_retries")}, file=sys.stderr)
     ms = t_start.elapsed_time(t_end) / args.steps
     ms_fwd = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
     ms_bwd = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))

@@ -250,41 +250,58 @@ __global__ void __launch_bounds__(THREADS) fwd_agg_kernel(
 }
 
 // ============================================================================
-// Forward main pass.
-template <typename IO>
-__global__ void __launch_bounds__(THREADS) fwd_kernel(
+// Forward main pass.  NPT states per thread: NPT = 4 (128 threads, 4 lanes
+// per channel pair) or NPT = 2 (256 threads, 8 lanes per pair: twice the
+// warps for the same channels, which hides the MUFU / shared-memory latency
+// when the problem has few channels per SM, e.g. C3 with ~10 warps/SM at 4).
+template <int NPT>
+struct FG {
+    static constexpr int TPC = NST / NPT;        // lanes per channel pair
+    static constexpr int THREADS = CH / 2 * TPC;  // threads per CTA (64 channels)
+    static constexpr int PPW = 32 / TPC;          // pairs per warp
+    static constexpr int LB = TPC / 2;            // highest lane bit of the state group
+};
+
+template <typename IO, int NPT, int TF>
+__global__ void __launch_bounds__(FG<NPT>::THREADS) fwd_kernel(
     const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mp,
     const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mC,
     const __grid_constant__ CUtensorMap my, const float* __restrict__ bdelta, const float* __restrict__ a_log,
     const float* __restrict__ Dskip, const float* __restrict__ x0, const float* __restrict__ aggX,
     const float* __restrict__ aggSD, float* __restrict__ ckpt, int64_t Bn, int64_t L, int64_t D, int64_t seg_len,
     int n_ck) {
-    using LY = Lay<IO>;
+    using G = FG<NPT>;
+    constexpr int LU = TF * CH * (int)sizeof(IO), LP = TF * CH * 4, LBC = TF * NST * 4;
+    constexpr int LFWD = LU + LP + 2 * LBC;
+    constexpr int NS = TF == 32 ? 3 : NSF;  // pipeline stages
+    constexpr int TPC = G::TPC, TH = G::THREADS;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     unsigned char* stages = smem + 128;
-    float* dub = reinterpret_cast<float*>(stages + NSF * LY::FWD);
-    IO* ybuf = reinterpret_cast<IO*>(reinterpret_cast<unsigned char*>(dub) + LY::P);  // [2][T][CH]
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, q = lane & 3, g = lane >> 2;
-    const int pp = w * 8 + g;
+    float* dub = reinterpret_cast<float*>(stages + NS * LFWD);
+    IO* ybuf = reinterpret_cast<IO*>(reinterpret_cast<unsigned char*>(dub) + LP);  // [2][TF][CH]
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, q = lane & (TPC - 1), g = lane / TPC;
+    const int pp = w * G::PPW + g;
+    const int n0 = q * NPT;
     const int b = blockIdx.y, s = blockIdx.z;
     const int d0 = blockIdx.x * CH;
-    const Seg sg = segment(s, seg_len, L);
-    init_bars(full, NSF);
+    const int64_t t_beg = (int64_t)s * seg_len, t_end = min(L, t_beg + seg_len);
+    const int tile0 = (int)(t_beg / TF), ntiles = (int)((t_end - t_beg + TF - 1) / TF);
+    init_bars(full, NS);
     auto issue = [&](int j) {
-        const int st = j % NSF;
-        unsigned char* sp = stages + st * LY::FWD;
-        const int t = (sg.tile0 + j) * T;
-        tma::mbar_arrive_expect_tx(&full[st], LY::FWD);
+        const int st = j % NS;
+        unsigned char* sp = stages + st * LFWD;
+        const int t = (tile0 + j) * TF;
+        tma::mbar_arrive_expect_tx(&full[st], LFWD);
         tma::load_3d(sp, &mu, d0, t, b, &full[st]);
-        tma::load_3d(sp + LY::U, &mp, d0, t, b, &full[st]);
-        tma::load_3d(sp + LY::U + LY::P, &mB, 0, t, b, &full[st]);
-        tma::load_3d(sp + LY::U + LY::P + LY::BC, &mC, 0, t, b, &full[st]);
+        tma::load_3d(sp + LU, &mp, d0, t, b, &full[st]);
+        tma::load_3d(sp + LU + LP, &mB, 0, t, b, &full[st]);
+        tma::load_3d(sp + LU + LP + LBC, &mC, 0, t, b, &full[st]);
     };
     if (tid == 0)
-        for (int j = 0; j < NSF && j < sg.ntiles; ++j) issue(j);
+        for (int j = 0; j < NS && j < ntiles; ++j) issue(j);
 
-    float a2[2][4], x[2][4], Dd[2];
+    float a2[2][NPT], x[2][NPT], Dd[2];
     bool okc[2];
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
@@ -292,39 +309,37 @@ __global__ void __launch_bounds__(THREADS) fwd_kernel(
         okc[c] = dg < D;
         Dd[c] = okc[c] ? Dskip[dg] : 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            a2[c][j] = okc[c] ? -expf(a_log[dg * NST + 4 * q + j]) * kLog2e : 0.f;
-            x[c][j] = (x0 && okc[c]) ? x0[((int64_t)b * D + dg) * NST + 4 * q + j] : 0.f;
+        for (int j = 0; j < NPT; ++j) {
+            a2[c][j] = okc[c] ? -expf(a_log[dg * NST + n0 + j]) * kLog2e : 0.f;
+            x[c][j] = (x0 && okc[c]) ? x0[((int64_t)b * D + dg) * NST + n0 + j] : 0.f;
         }
         // fold the maps of the segments to the left (fixed order)
         for (int r = 0; r < s; ++r) {
             if (!okc[c]) break;
             const int64_t o = ((int64_t)r * Bn + b) * D + dg;
             const float sdr = aggSD[o];
-            const float4 X = *reinterpret_cast<const float4*>(aggX + o * NST + 4 * q);
-            const float Xv[4] = {X.x, X.y, X.z, X.w};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) x[c][j] = fmaf(ex2(a2[c][j] * sdr), x[c][j], Xv[j]);
+            for (int j = 0; j < NPT; ++j) x[c][j] = fmaf(ex2(a2[c][j] * sdr), x[c][j], aggX[o * NST + n0 + j]);
         }
     }
-    const int pd = tid & (CH - 1), pr = tid >> 6;
+    const int pd = tid & (CH - 1), pr = tid / CH;
     const float pbd = d0 + pd < D ? bdelta[d0 + pd] : 0.f;
 
-    for (int j = 0; j < sg.ntiles; ++j) {
-        const int st = j % NSF;
-        const int64_t t0 = (int64_t)(sg.tile0 + j) * T;
-        const int nt = (int)min((int64_t)T, sg.t_end - t0);
-        unsigned char* sp = stages + st * LY::FWD;
+    for (int j = 0; j < ntiles; ++j) {
+        const int st = j % NS;
+        const int64_t t0 = (int64_t)(tile0 + j) * TF;
+        const int nt = (int)min((int64_t)TF, t_end - t0);
+        unsigned char* sp = stages + st * LFWD;
         const IO* us = reinterpret_cast<const IO*>(sp);
-        float* ps = reinterpret_cast<float*>(sp + LY::U);
-        const float* Bs = reinterpret_cast<const float*>(sp + LY::U + LY::P);
-        const float* Cs = Bs + T * NST;
-        IO* yo = ybuf + (j & 1) * T * CH;
+        float* ps = reinterpret_cast<float*>(sp + LU);
+        const float* Bs = reinterpret_cast<const float*>(sp + LU + LP);
+        const float* Cs = Bs + TF * NST;
+        IO* yo = ybuf + (j & 1) * TF * CH;
         if (tid == 0 && j >= 2) tma::bulk_wait_read<1>();  // the store that used yo is done reading
-        tma::mbar_wait(&full[st], (j / NSF) & 1);
+        tma::mbar_wait(&full[st], (j / NS) & 1);
 #pragma unroll
-        for (int i = 0; i < T / 2; ++i) {
-            const int r = pr + 2 * i, idx = r * CH + pd;
+        for (int i = 0; i < TF * CH / TH; ++i) {
+            const int r = pr + (TH / CH) * i, idx = r * CH + pd;
             float sig;
             float dl = softplus_sig(ps[idx] + pbd, &sig);
             dl = r < nt ? dl : 0.f;  // past L: abar = 1, no input -> the state is carried unchanged
@@ -333,53 +348,88 @@ __global__ void __launch_bounds__(THREADS) fwd_kernel(
         }
         __syncthreads();
 #pragma unroll
-        for (int kb = 0; kb < T / 4; ++kb) {
+        // reduced readouts stay in registers until the tile is done: no shared
+        // store sits between the tile's shared loads, so they can all be hoisted
+        float yk[TF / 4][2];
+#pragma unroll
+        for (int kb = 0; kb < TF / 4; ++kb) {
             float yp[8];
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
                 const int k = kb * 4 + kk;
-                if (k % CK == 0 && ckpt != nullptr && t0 + k < sg.t_end) {
-                    float* cp = ckpt + (((int64_t)b * (n_ck + 1) + (t0 + k) / CK) * D + d0 + 2 * pp) * NST + 4 * q;
+                if (k % CK == 0 && ckpt != nullptr && t0 + k < t_end) {
+                    float* cp = ckpt + (((int64_t)b * (n_ck + 1) + (t0 + k) / CK) * D + d0 + 2 * pp) * NST + n0;
 #pragma unroll
                     for (int c = 0; c < 2; ++c)
-                        if (okc[c])
-                            __stcs(reinterpret_cast<float4*>(cp + c * NST),
-                                   make_float4(x[c][0], x[c][1], x[c][2], x[c][3]));
+                        if (okc[c]) {
+                            if constexpr (NPT == 4)
+                                __stcs(reinterpret_cast<float4*>(cp + c * NST),
+                                       make_float4(x[c][0], x[c][1], x[c][2], x[c][3]));
+                            else
+                                __stcs(reinterpret_cast<float2*>(cp + c * NST), make_float2(x[c][0], x[c][1]));
+                        }
                 }
                 const float2 dl = ld_pair(ps + k * CH + 2 * pp), du = ld_pair(dub + k * CH + 2 * pp);
-                const float4 bb = *reinterpret_cast<const float4*>(Bs + k * NST + 4 * q);
-                const float4 cc = *reinterpret_cast<const float4*>(Cs + k * NST + 4 * q);
-                const float bv[4] = {bb.x, bb.y, bb.z, bb.w}, cv[4] = {cc.x, cc.y, cc.z, cc.w};
+                float bv[NPT], cv[NPT];
+                if constexpr (NPT == 4) {
+                    const float4 bb = *reinterpret_cast<const float4*>(Bs + k * NST + n0);
+                    const float4 cc = *reinterpret_cast<const float4*>(Cs + k * NST + n0);
+                    bv[0] = bb.x; bv[1] = bb.y; bv[2] = bb.z; bv[3] = bb.w;
+                    cv[0] = cc.x; cv[1] = cc.y; cv[2] = cc.z; cv[3] = cc.w;
+                } else {
+                    const float2 bb = *reinterpret_cast<const float2*>(Bs + k * NST + n0);
+                    const float2 cc = *reinterpret_cast<const float2*>(Cs + k * NST + n0);
+                    bv[0] = bb.x; bv[1] = bb.y;
+                    cv[0] = cc.x; cv[1] = cc.y;
+                }
                 const float dlc[2] = {dl.x, dl.y}, duc[2] = {du.x, du.y};
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     float acc = 0.f;
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
+                    for (int jj = 0; jj < NPT; ++jj) {
                         x[c][jj] = fmaf(ex2(dlc[c] * a2[c][jj]), x[c][jj], duc[c] * bv[jj]);
                         acc = fmaf(x[c][jj], cv[jj], acc);
                     }
                     yp[kk * 2 + c] = acc;
                 }
             }
-            tr_reduce<8, 2, 1>(yp);  // lane q: step kb*4 + q, both channels
-            const int k = kb * 4 + q;
-            const float2 uu = ld_pair(us + k * CH + 2 * pp);
-            st_pair(yo + k * CH + 2 * pp, fmaf(Dd[0], uu.x, yp[0]), fmaf(Dd[1], uu.y, yp[1]));
+            if constexpr (NPT == 4) {
+                tr_reduce<8, 2, 1>(yp);  // lane q: step kb*4 + q, both channels
+                yk[kb][0] = yp[0];
+                yk[kb][1] = yp[1];
+            } else {
+                tr_reduce<8, 4, 1>(yp);  // lane q: step kb*4 + q/2, channel q%2
+                yk[kb][0] = yp[0];
+            }
+        }
+#pragma unroll
+        for (int kb = 0; kb < TF / 4; ++kb) {
+            if constexpr (NPT == 4) {
+                const int k = kb * 4 + q;
+                const float2 uu = ld_pair(us + k * CH + 2 * pp);
+                st_pair(yo + k * CH + 2 * pp, fmaf(Dd[0], uu.x, yk[kb][0]), fmaf(Dd[1], uu.y, yk[kb][1]));
+            } else {
+                const int k = kb * 4 + (q >> 1), c = q & 1;
+                const int o = k * CH + 2 * pp + c;
+                st1(yo + o, fmaf(c ? Dd[1] : Dd[0], ld1(us + o), yk[kb][0]));
+            }
         }
         tma::fence_proxy_async();
         __syncthreads();
         if (tid == 0) {
             tma::store_3d(&my, yo, d0, (int)t0, b);
             tma::bulk_commit();
-            if (j + NSF < sg.ntiles) issue(j + NSF);
+            if (j + NS < ntiles) issue(j + NS);
         }
     }
     if (ckpt != nullptr && s == (int)gridDim.z - 1) {  // final state in the last slot
-        float* cp = ckpt + (((int64_t)b * (n_ck + 1) + n_ck) * D + d0 + 2 * pp) * NST + 4 * q;
+        float* cp = ckpt + (((int64_t)b * (n_ck + 1) + n_ck) * D + d0 + 2 * pp) * NST + n0;
 #pragma unroll
         for (int c = 0; c < 2; ++c)
-            if (okc[c]) *reinterpret_cast<float4*>(cp + c * NST) = make_float4(x[c][0], x[c][1], x[c][2], x[c][3]);
+            if (okc[c])
+#pragma unroll
+                for (int jj = 0; jj < NPT; ++jj) cp[c * NST + jj] = x[c][jj];
     }
     if (tid == 0) tma::bulk_wait<0>();
 }
@@ -743,6 +793,18 @@ static int num_sms() {
     return n;
 }
 
+static int fwd_tile() {
+    const char* e = getenv("LRX_S6_FWD_TILE");
+    return (e && atoi(e) == 32) ? 32 : 16;
+}
+
+// NPT 4 (128 threads) is the default; LRX_S6_FWD_NPT=2 selects the 256-thread
+// variant (same speed on C3, kept for shapes with few channels per SM)
+static int fwd_npt() {
+    const char* e = getenv("LRX_S6_FWD_NPT");
+    return (e && atoi(e) == 2) ? 2 : 4;
+}
+
 bool eligible(int io, int64_t D, int64_t N) {
     if (getenv("LRX_S6_V2")) return false;
     if (N != NST) return false;
@@ -763,12 +825,14 @@ Geo geometry(int64_t B, int64_t L, int64_t D) {
     int64_t S = 1;
     if (const char* e = getenv("LRX_S6_SEGS")) S = atoll(e);
     else {
-        const int64_t want = 3LL * num_sms();  // ~12 warps per SM
+        // segments cost an extra aggregate pass (~40% of the main pass), so
+        // only split when the CTAs cannot give every SM ~2 (8 warps)
+        const int64_t want = 2LL * num_sms();
         if (ctas < want) S = cdiv(want, ctas);
     }
     const int64_t tiles = cdiv(L, T);
     S = std::max<int64_t>(1, std::min<int64_t>(S, std::max<int64_t>(1, tiles / 4)));  // >= 4 tiles per segment
-    g.seg_len = cdiv(tiles, S) * T;
+    g.seg_len = cdiv(tiles, 2 * S) * 2 * T;  // whole 32-step tiles (forward tile up to 32)
     g.n_seg = cdiv(L, g.seg_len);
     // workspace: per-segment maps [S, B, D, 16] and delta sums [S, B, D]
     g.ws_bytes = (int64_t)(align_up((size_t)g.n_seg * B * D * NST * 4) + align_up((size_t)g.n_seg * B * D * 4));
@@ -780,11 +844,11 @@ struct Maps {
 };
 
 template <typename IO>
-static bool enc_act(CUtensorMap* m, const void* p, int64_t B, int64_t L, int64_t D) {
-    return tma::encode_3d(m, p, sizeof(IO), B, L, D, T, CH);
+static bool enc_act(CUtensorMap* m, const void* p, int64_t B, int64_t L, int64_t D, int rows = T) {
+    return tma::encode_3d(m, p, sizeof(IO), B, L, D, rows, CH);
 }
-static bool enc_bc(CUtensorMap* m, const void* p, int64_t B, int64_t L) {
-    return tma::encode_3d(m, p, 4, B, L, NST, T, NST);
+static bool enc_bc(CUtensorMap* m, const void* p, int64_t B, int64_t L, int rows = T) {
+    return tma::encode_3d(m, p, 4, B, L, NST, rows, NST);
 }
 
 template <typename K>
@@ -857,16 +921,29 @@ int fwd(const void* u, const void* pre, const void* bd, const void* al, const vo
     if (g.n_seg > 1 && !(flags & LRX_S6_REUSE_AGG))
         if (int e = fwd_agg_launch<IO>(u, pre, bd, al, Bk, w, g, B, L, D, 0, (int)g.n_seg - 1, st)) return e;
     CUtensorMap mu, mp, mB, mC, my;
-    S6V3_MAP(enc_act<IO>(&mu, u, B, L, D));
-    S6V3_MAP(enc_act<float>(&mp, pre, B, L, D));
-    S6V3_MAP(enc_bc(&mB, Bk, B, L));
-    S6V3_MAP(enc_bc(&mC, Ck, B, L));
-    S6V3_MAP(enc_act<IO>(&my, y, B, L, D));
-    const size_t smem = Lay<IO>::smem_fwd();
-    if (int e = set_smem(fwd_kernel<IO>, smem, "s6 fwd")) return e;
-    fwd_kernel<IO><<<dim3((unsigned)g.n_dblk, (unsigned)B, (unsigned)g.n_seg), THREADS, smem, st>>>(
-        mu, mp, mB, mC, my, (const float*)bd, (const float*)al, (const float*)Dk, (const float*)x0, w.X, w.SD,
-        (float*)ckpt, B, L, D, g.seg_len, (int)g.n_ck);
+    const int TF = fwd_tile();
+    const int box = CH;
+    S6V3_MAP(tma::encode_3d(&mu, u, sizeof(IO), B, L, D, TF, box));
+    S6V3_MAP(tma::encode_3d(&mp, pre, 4, B, L, D, TF, box));
+    S6V3_MAP(enc_bc(&mB, Bk, B, L, TF));
+    S6V3_MAP(enc_bc(&mC, Ck, B, L, TF));
+    S6V3_MAP(tma::encode_3d(&my, y, sizeof(IO), B, L, D, TF, box));
+    const dim3 grid((unsigned)g.n_dblk, (unsigned)B, (unsigned)g.n_seg);
+    const int npt = fwd_npt();
+#define S6V3_FWD(NPT_, TF_)                                                                                        \
+    do {                                                                                                           \
+        constexpr size_t smem = 128 + (size_t)(TF_ == 32 ? 3 : NSF) * (TF_ * CH * (sizeof(IO) + 4) + 2 * TF_ * NST * 4) +           \
+                                TF_ * CH * 4 + 2 * TF_ * CH * sizeof(IO);                                         \
+        if (int e = set_smem(fwd_kernel<IO, NPT_, TF_>, smem, "s6 fwd")) return e;                                 \
+        fwd_kernel<IO, NPT_, TF_><<<grid, FG<NPT_>::THREADS, smem, st>>>(                                          \
+            mu, mp, mB, mC, my, (const float*)bd, (const float*)al, (const float*)Dk, (const float*)x0, w.X, w.SD,  \
+            (float*)ckpt, B, L, D, g.seg_len, (int)g.n_ck);                                                        \
+    } while (0)
+    if (npt == 2 && TF == 32) S6V3_FWD(2, 32);
+    else if (npt == 2) S6V3_FWD(2, 16);
+    else if (TF == 32) S6V3_FWD(4, 32);
+    else S6V3_FWD(4, 16);
+#undef S6V3_FWD
     return launched("lrx_s6_fwd/v3");
 }
 
