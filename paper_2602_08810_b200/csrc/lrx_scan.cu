@@ -189,11 +189,34 @@ __global__ void __launch_bounds__(kLanes) scan_bwd_kernel(const V* __restrict__ 
 // ---------------------------------------------------------------- reduce
 template <typename V>
 __global__ void reduce_rows_kernel(const V* __restrict__ in, V* __restrict__ out, int64_t R, int64_t N) {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= N) return;
+    // block = 32 columns x RL row lanes; lane r folds rows r, r+RL, ... then
+    // the RL partial sums are combined by a fixed tree: deterministic, and
+    // coalesced over the 32 columns of every row
+    extern __shared__ __align__(16) unsigned char red_raw[];
+    V* red = reinterpret_cast<V*>(red_raw);
+    const int RL = blockDim.x / 32;
+    const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * 32 + c;
     V acc = Traits<V>::zero();
-    for (int64_t r = 0; r < R; ++r) acc = acc + in[r * N + j];
-    out[j] = acc;
+    if (j < N)
+        for (int64_t r = r0; r < R; r += RL) acc = acc + in[r * N + j];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int h = RL / 2; h >= 1; h >>= 1) {
+        if (r0 < h) red[threadIdx.x] = red[threadIdx.x] + red[threadIdx.x + 32 * h];
+        __syncthreads();
+    }
+    if (r0 == 0 && j < N) out[j] = red[c];
+}
+
+// launch: many row lanes when there are few columns (the S5/LRU parameter
+// partials: R ~ 1e4 rows of P columns), 8 when columns are plentiful
+template <typename V>
+static void reduce_rows_launch(const V* in, V* out, int64_t R, int64_t N, cudaStream_t st) {
+    const int64_t blocks = cdiv(N, 32);
+    int RL = 8;
+    while (RL < 32 && blocks * RL < 148 * 64 && RL * 8 < R) RL *= 2;
+    reduce_rows_kernel<V><<<(unsigned)blocks, 32 * RL, 32 * RL * sizeof(V), st>>>(in, out, R, N);
 }
 
 // ---------------------------------------------------------------- host side
@@ -277,7 +300,7 @@ static int bwd_t(int per_step, const void* a, const void* x, const void* x0, con
                                                        nc, ws);
     rc = launched("lrx_scan_bwd");
     if (rc || !ga) return rc;
-    reduce_rows_kernel<V><<<(unsigned)cdiv(N, 256), 256, 0, st>>>(part, (V*)ga, nc, N);
+    reduce_rows_launch<V>(part, (V*)ga, nc, N, st);
     return launched("lrx_scan_bwd/reduce");
 }
 
@@ -339,16 +362,11 @@ int lrx_scan_bwd(int dtype, int a_per_step, const void* a, const void* x, const 
 int lrx_reduce_rows(int dtype, const void* in, void* out, int64_t R, int64_t N, void* stream) {
     LRX_REQUIRE(R >= 1 && N >= 1, LRX_ERR_SHAPE, "bad extents R=%lld N=%lld", (long long)R, (long long)N);
     cudaStream_t st = (cudaStream_t)stream;
-    const unsigned g = (unsigned)cdiv(N, 256);
     switch (dtype) {
-        case LRX_F32: reduce_rows_kernel<float><<<g, 256, 0, st>>>((const float*)in, (float*)out, R, N); break;
-        case LRX_F64: reduce_rows_kernel<double><<<g, 256, 0, st>>>((const double*)in, (double*)out, R, N); break;
-        case LRX_C64:
-            reduce_rows_kernel<cplx<float>><<<g, 256, 0, st>>>((const cplx<float>*)in, (cplx<float>*)out, R, N);
-            break;
-        case LRX_C128:
-            reduce_rows_kernel<cplx<double>><<<g, 256, 0, st>>>((const cplx<double>*)in, (cplx<double>*)out, R, N);
-            break;
+        case LRX_F32: reduce_rows_launch<float>((const float*)in, (float*)out, R, N, st); break;
+        case LRX_F64: reduce_rows_launch<double>((const double*)in, (double*)out, R, N, st); break;
+        case LRX_C64: reduce_rows_launch<cplx<float>>((const cplx<float>*)in, (cplx<float>*)out, R, N, st); break;
+        case LRX_C128: reduce_rows_launch<cplx<double>>((const cplx<double>*)in, (cplx<double>*)out, R, N, st); break;
         default: set_error("unsupported dtype %d", dtype); return LRX_ERR_VALUE;
     }
     return launched("lrx_reduce_rows");
