@@ -171,6 +171,17 @@ int lrx_s6_bwd_carry(int io_dtype, const void* gy, const void* pre, const void* 
                      void* ws, int64_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ *
+ * fp32 GEMM on the tcgen05 tensor cores with the 3xTF32 split (the dense
+ * projections of S5 / LRU, layers.py:650-704):
+ *   C[M,N] = alpha A[M,K] Bt[N,K]^T + (colscale ? colscale[n] : beta) Cin[M,N]
+ * fp32 row-major, K contiguous in both A and Bt; Bt_lo = Bt - tf32(Bt) is the
+ * caller's pre-split low part of the (small) right operand.  Cin may be NULL
+ * or alias C.  Rows must be 16-byte aligned (K % 4 == 0).
+ * ------------------------------------------------------------------------ */
+int lrx_gemm_f32(const void* A, const void* Bt, const void* Bt_lo, void* C, const void* Cin, const void* colscale,
+                 int64_t M, int64_t N, int64_t K, float alpha, float beta, void* stream);
+
+/* ------------------------------------------------------------------------ *
  * MIMO complex diagonal scan for S5 / LRU (layers.py:616-980): the recurrence
  * between the dense projections bu = B u and y = Re(C x) (cuBLAS GEMMs):
  *   x_k[b,p] = abar[p] x_{k-1} + scale[p] bu_k[b,p]        (lanes b*P + p)

@@ -1,0 +1,311 @@
+// fp32 GEMM on the 5th-generation tensor cores (tcgen05, kind::tf32) with the
+// 3xTF32 split, for the dense projections of the MIMO layers (S5 / LRU:
+// layers.py:650-704, bu = B u, y = Re(C x) + D u and their pullbacks).
+//
+//   C[M, N] = alpha * A[M, K] . Bt[N, K]^T + (colscale ? colscale[n] : beta) * Cin[M, N]
+//
+// All operands fp32 row-major, both A and Bt K-contiguous ("K-major").  TF32
+// keeps 10 mantissa bits, far from the 1e-4 fp32 parity bar, so each product
+// is split: a = a_hi + a_lo with a_hi the TF32 truncation (what the tensor core
+// reads from an fp32 word) and a_lo = a - a_hi (exact in fp32), and
+//   a b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi        (error ~2^-20 |a b|)
+// i.e. three MMAs per k-step into one fp32 TMEM accumulator.  Bt (a small
+// weight) arrives pre-split from the host (Bt, Bt_lo); A's low part is made
+// in shared memory from the TMA-landed tile by the split warps.
+//
+// CTA = 6 warps, one 128 x BN output tile:
+//   warp 0      TMA producer (A, Bt, Bt_lo k-blocks of 32 into a 3-stage ring,
+//               128-byte swizzle = the UMMA K-major SW128 canonical layout)
+//   warp 1      MMA issuer (one thread; 4 k-steps x 3 products per k-block,
+//               tcgen05.commit frees the stage / signals the epilogue)
+//   warps 2..5  split (A_lo = A - trunc_tf32(A), same swizzled offsets), then
+//               the epilogue: tcgen05.ld of its 32 TMEM lanes (= rows),
+//               alpha / colscale / Cin, direct 128-byte row stores.
+#include "lrx_host.h"
+#include "lrx_tma.cuh"
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lrx {
+namespace gemm {
+
+constexpr int BM = 128, BK = 32, THREADS = 192;
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    // UMMA shared-memory descriptor, K-major SWIZZLE_128B: LBO = 1 (unused),
+    // SBO = 1024 B between 8-row groups, version 1 (sm_100), layout type 2
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+template <int BN>
+__host__ __device__ constexpr uint32_t idesc_tf32() {
+    // c_format F32 (1) [4,6), a/b format TF32 (2) [7,10) [10,13), K-major both,
+    // N >> 3 at [17,23), M >> 4 at [24,29)
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     tma::smem_u32(bar))
+                 : "memory");
+}
+
+template <int BN>
+struct Lay {
+    static constexpr int A = BM * BK * 4;   // 16 KB
+    static constexpr int B = BN * BK * 4;
+    static constexpr int STAGE = 2 * A + 2 * B;  // A, A_lo, Bt, Bt_lo
+    static constexpr int STAGES = BN >= 256 ? 2 : 3;
+    // 1 KB alignment slack + 1 KB barrier block + the stage ring
+    static constexpr size_t smem() { return 2048 + (size_t)STAGES * STAGE; }
+};
+
+template <int BN>
+__global__ void __launch_bounds__(THREADS, 1) gemm_tf32x3_kernel(
+    const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
+    const __grid_constant__ CUtensorMap mBl, float* C, const float* Cin,
+    const float* __restrict__ colscale, int M, int N, int K, float alpha, float beta) {
+    using LY = Lay<BN>;
+    constexpr int STAGES = LY::STAGES;
+    extern __shared__ unsigned char smem_raw[];
+    // 1024-byte alignment for the 128B-swizzle atoms
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(base);     // [STAGES] TMA landed
+    uint64_t* split = full + STAGES;                         // [STAGES] A_lo written
+    uint64_t* empty = split + STAGES;                        // [STAGES] MMAs done with the stage
+    uint64_t* tfull = empty + STAGES;                        // accumulator ready
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+    unsigned char* stages = base + 1024;                     // 1024-aligned ring
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int nk = (K + BK - 1) / BK;
+    constexpr uint32_t kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+
+    if (threadIdx.x == 0) {
+        tma::prefetch_map(&mA);
+        tma::prefetch_map(&mB);
+        tma::prefetch_map(&mBl);
+        for (int i = 0; i < STAGES; ++i) {
+            tma::mbar_init(&full[i], 1);
+            tma::mbar_init(&split[i], 128);
+            tma::mbar_init(&empty[i], 1);
+        }
+        tma::mbar_init(tfull, 1);
+        tma::fence_barrier_init();
+    }
+    if (warp == 1) {  // TMEM accumulator: 128 lanes x BN fp32 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         tma::smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ------------------------------------------ producer
+            for (int kb = 0; kb < nk; ++kb) {
+                const int st = kb % STAGES;
+                if (kb >= STAGES) tma::mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+                unsigned char* sp = stages + st * LY::STAGE;
+                tma::mbar_arrive_expect_tx(&full[st], LY::A + 2 * LY::B);
+                tma::load_2d(sp, &mA, kb * BK, m0, &full[st]);
+                tma::load_2d(sp + 2 * LY::A, &mB, kb * BK, n0, &full[st]);
+                tma::load_2d(sp + 2 * LY::A + LY::B, &mBl, kb * BK, n0, &full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ------------------------------------------ MMA issuer
+            constexpr uint32_t idesc = idesc_tf32<BN>();
+            for (int kb = 0; kb < nk; ++kb) {
+                const int st = kb % STAGES;
+                tma::mbar_wait(&split[st], (kb / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t sa = tma::smem_u32(stages + st * LY::STAGE);
+                const uint32_t sal = sa + LY::A, sb = sa + 2 * LY::A, sbl = sb + LY::B;
+#pragma unroll
+                for (int k = 0; k < BK / 8; ++k) {  // 8 tf32 = 32 bytes per UMMA k-step
+                    const uint32_t off = k * 32;
+                    const uint64_t dA = sw128_desc(sa + off), dAl = sw128_desc(sal + off);
+                    const uint64_t dB = sw128_desc(sb + off), dBl = sw128_desc(sbl + off);
+                    mma_tf32(tmem, dA, dB, idesc, (kb | k) != 0);
+                    mma_tf32(tmem, dA, dBl, idesc, 1);
+                    mma_tf32(tmem, dAl, dB, idesc, 1);
+                }
+                mma_commit(&empty[st]);  // stage reusable once these MMAs have read it
+            }
+            mma_commit(tfull);
+        }
+    } else {
+        // ---------------------------------------------------------- split
+        const int t = threadIdx.x - 64;  // 0..127
+        for (int kb = 0; kb < nk; ++kb) {
+            const int st = kb % STAGES;
+            tma::mbar_wait(&full[st], (kb / STAGES) & 1);
+            const float4* a4 = reinterpret_cast<const float4*>(stages + st * LY::STAGE);
+            float4* l4 = reinterpret_cast<float4*>(stages + st * LY::STAGE + LY::A);
+#pragma unroll
+            for (int i = 0; i < LY::A / 16 / 128; ++i) {
+                const float4 v = a4[t + 128 * i];
+                float4 lo;
+                lo.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                l4[t + 128 * i] = lo;
+            }
+            tma::fence_proxy_async();  // generic writes -> async-proxy (MMA) reads
+            tma::mbar_arrive(&split[st]);
+        }
+        // ---------------------------------------------------------- epilogue
+        tma::mbar_wait(tfull, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int row = m0 + 32 * q + lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t r[32];
+            const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (row < M) {
+                const int64_t ro = (int64_t)row * N;
+                if (n0 + c0 + 32 <= N && (N & 3) == 0) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const int col = n0 + c0 + j;
+                        float4 o = make_float4(alpha * __uint_as_float(r[j]), alpha * __uint_as_float(r[j + 1]),
+                                               alpha * __uint_as_float(r[j + 2]), alpha * __uint_as_float(r[j + 3]));
+                        if (Cin) {
+                            const float4 ci = *reinterpret_cast<const float4*>(Cin + ro + col);
+                            float4 s = make_float4(beta, beta, beta, beta);
+                            if (colscale) s = *reinterpret_cast<const float4*>(colscale + col);
+                            o.x = fmaf(s.x, ci.x, o.x);
+                            o.y = fmaf(s.y, ci.y, o.y);
+                            o.z = fmaf(s.z, ci.z, o.z);
+                            o.w = fmaf(s.w, ci.w, o.w);
+                        }
+                        *reinterpret_cast<float4*>(C + ro + col) = o;
+                    }
+                } else {
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = n0 + c0 + j;
+                        if (col < N) {
+                            float o = alpha * __uint_as_float(r[j]);
+                            if (Cin) o = fmaf(colscale ? colscale[col] : beta, Cin[ro + col], o);
+                            C[ro + col] = o;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+}
+
+static bool enc_sw128(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows);
+
+template <int BN>
+static int launch(const float* A, const float* Bt, const float* Btl, float* C, const float* Cin, const float* cs,
+                  int64_t M, int64_t N, int64_t K, float alpha, float beta, cudaStream_t st) {
+    CUtensorMap mA, mB, mBl;
+    if (!enc_sw128(&mA, A, M, K, BM) || !enc_sw128(&mB, Bt, N, K, BN) || !enc_sw128(&mBl, Btl, N, K, BN)) {
+        set_error("gemm: TMA descriptor rejected (K %% 4 == 0 and 16-byte aligned rows required)");
+        return LRX_ERR_VALUE;
+    }
+    const size_t smem = Lay<BN>::smem();
+    auto k = gemm_tf32x3_kernel<BN>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        set_error("gemm: cannot reserve %zu B of shared memory", smem);
+        return LRX_ERR_CUDA;
+    }
+    const dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN));
+    k<<<grid, THREADS, smem, st>>>(mA, mB, mBl, C, Cin, cs, (int)M, (int)N, (int)K, alpha, beta);
+    return launched("lrx_gemm_f32/tcgen05");
+}
+
+}  // namespace gemm
+}  // namespace lrx
+
+#include <cudaTypedefs.h>
+
+namespace lrx {
+namespace gemm {
+
+static PFN_cuTensorMapEncodeTiled_v12000 enc_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// [rows, cols] fp32 row-major, box [box_rows, 32 cols = 128 B], 128-byte swizzle
+static bool enc_sw128(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    auto fn = enc_fn();
+    if (!fn || (reinterpret_cast<uintptr_t>(p) & 15) || ((cols * 4) & 15)) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 4};
+    cuuint32_t box[2] = {BK, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(p), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace gemm
+}  // namespace lrx
+
+using namespace lrx;
+
+extern "C" {
+
+int lrx_gemm_f32(const void* A, const void* Bt, const void* Bt_lo, void* C, const void* Cin, const void* colscale,
+                 int64_t M, int64_t N, int64_t K, float alpha, float beta, void* stream) {
+    LRX_REQUIRE(M >= 1 && N >= 1 && K >= 1, LRX_ERR_SHAPE, "gemm: bad extents M=%lld N=%lld K=%lld", (long long)M,
+                (long long)N, (long long)K);
+    LRX_REQUIRE(M < (1ll << 31) && N <= (1 << 16) && K < (1 << 24), LRX_ERR_UNSUPPORTED, "gemm: extents too large");
+    cudaStream_t st = (cudaStream_t)stream;
+    const float *a = (const float*)A, *b = (const float*)Bt, *bl = (const float*)Bt_lo;
+    if (N <= 64) return gemm::launch<64>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K, alpha,
+                                         beta, st);
+    if (N <= 128) return gemm::launch<128>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K,
+                                           alpha, beta, st);
+    return gemm::launch<256>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K, alpha, beta, st);
+}
+
+}  // extern "C"

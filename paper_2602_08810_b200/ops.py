@@ -20,7 +20,7 @@ import torch
 from . import _lib
 
 __all__ = ["rglru_scan_fwd", "rglru_scan_bwd", "s6_geometry", "s6_scan_fwd", "s6_scan_bwd", "s6_fwd_carry",
-           "s6_bwd_carry", "mimo_scan_fwd", "mimo_scan_bwd", "reduce_rows"]
+           "s6_bwd_carry", "mimo_scan_fwd", "mimo_scan_bwd", "reduce_rows", "gemm_f32", "tf32_lo"]
 
 
 def reduce_rows(part, rows, cols):
@@ -167,6 +167,27 @@ def s6_bwd_carry(gy, pre, b_delta, a_log, Ck, ws=None):
                                            _lib.ptr(a_log), _lib.ptr(Ck), _lib.ptr(h_agg), _lib.ptr(sd), B, L, D,
                                            N, _lib.ptr(ws), ws.numel(), _lib.stream()))
     return h_agg, sd, ws
+
+
+# ---------------------------------------------------------------------------
+# fp32 GEMM on tcgen05 (3xTF32)
+
+def tf32_lo(t):
+    """t - tf32(t): the low part of the 3xTF32 split (TF32 = the top 19 bits)."""
+    return t - (t.view(torch.int32) & -8192).view(torch.float32)
+
+
+def gemm_f32(A, Bt, Bt_lo=None, Cin=None, colscale=None, alpha=1.0, beta=0.0, out=None):
+    """C = alpha A Bt^T + (colscale or beta) * Cin on the tensor cores (3xTF32,
+    fp32-accurate).  A [M, K], Bt [N, K] fp32 contiguous (K % 4 == 0)."""
+    M, K = A.shape
+    N = Bt.shape[0]
+    if Bt_lo is None:
+        Bt_lo = tf32_lo(Bt)
+    C = out if out is not None else torch.empty((M, N), dtype=torch.float32, device=A.device)
+    _lib.check(_lib.lib().lrx_gemm_f32(_lib.ptr(A), _lib.ptr(Bt), _lib.ptr(Bt_lo), _lib.ptr(C), _lib.ptr(Cin),
+                                       _lib.ptr(colscale), M, N, K, alpha, beta, _lib.stream()))
+    return C
 
 
 # ---------------------------------------------------------------------------

@@ -352,3 +352,24 @@ def test_s6_is_deterministic_with_segments(lrx, monkeypatch):
     assert torch.equal(outs[0][0], outs[1][0])
     for k in outs[0][1]:
         assert torch.equal(outs[0][1][k], outs[1][1][k]), k
+
+
+# ---- tcgen05 3xTF32 GEMM ---------------------------------------------------
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 256), (1000, 256, 256), (4096, 128, 256), (300, 64, 36),
+                                   (131072, 256, 256), (257, 200, 64)])
+def test_gemm_f32_tcgen05_matches_f64(lrx, M, N, K):
+    from paper_2602_08810_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn((M, K), generator=g, device="cuda")
+    Bt = torch.randn((N, K), generator=g, device="cuda")
+    Cin = torch.randn((M, N), generator=g, device="cuda")
+    cs = torch.randn(N, generator=g, device="cuda")
+    ref = A.double() @ Bt.double().T
+    C = ops.gemm_f32(A, Bt)
+    assert rel(C, ref.cpu().numpy()) < 1e-5
+    C2 = ops.gemm_f32(A, Bt, Cin=Cin, colscale=cs, alpha=2.0)
+    ref2 = 2.0 * ref + cs.double() * Cin.double()
+    assert rel(C2, ref2.cpu().numpy()) < 1e-5
+    C3 = ops.gemm_f32(A, Bt, Cin=Cin, beta=-0.5)
+    assert rel(C3, (ref - 0.5 * Cin.double()).cpu().numpy()) < 1e-5
