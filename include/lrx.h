@@ -180,6 +180,13 @@ int lrx_s6_bwd_carry(int io_dtype, const void* gy, const void* pre, const void* 
  * ------------------------------------------------------------------------ */
 int lrx_gemm_f32(const void* A, const void* Bt, const void* Bt_lo, void* C, const void* Cin, const void* colscale,
                  int64_t M, int64_t N, int64_t K, float alpha, float beta, void* stream);
+/* Reduction ("TN") GEMM for the weight gradients: with A [K, M] and B [K, N]
+ * row-major (K = tokens, long), part[s, M, N] = alpha sum_{k in split s}
+ * A[k, m] B[k, n] for s < n_splits; sum the split axis with lrx_reduce_rows.
+ * M, N % 4 == 0. */
+int lrx_gemm_f32_tn_splits(int64_t M, int64_t N, int64_t K, int64_t* n_splits);
+int lrx_gemm_f32_tn(const void* A, const void* B, void* part, int64_t M, int64_t N, int64_t K, float alpha,
+                    void* stream);
 
 /* ------------------------------------------------------------------------ *
  * MIMO complex diagonal scan for S5 / LRU (layers.py:616-980): the recurrence

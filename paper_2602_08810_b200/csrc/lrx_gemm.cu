@@ -27,6 +27,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
+#include <algorithm>
+
 namespace lrx {
 namespace gemm {
 
@@ -233,6 +237,191 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tf32x3_kernel(
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
 }
 
+// ============================================================================
+// "TN" reduction GEMM for the weight gradients (R = gy^T x, R2 = g^T u):
+//   part[kz][m][n] = alpha * sum_{k in split kz} A[k, m] B[k, n]
+// A [K, M] and B [K, N] row-major: both operands are MN-major for the MMA.
+// K (= B*L tokens, 1e5+) is split across CTAs; the partial tiles are summed
+// in a fixed order by lrx_reduce_rows (deterministic).  Both operands are
+// activations, so the split warps make both low parts.
+//
+// MN-major tf32 operands use the 128B swizzle with 32-byte atoms: a TMA box
+// of 32 K-rows x 32 fp32 (128 B) is 8 atoms of 4 K-rows x 128 B stacked at
+// 512 B (SBO); the next 32-wide MN chunk is the next box, 4 KB on (LBO).  One
+// UMMA k-step of 8 tf32 rows = two atoms: advance the start address by 1 KB.
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr) {
+    // MN-major tf32 needs the 128B swizzle with 32-byte atoms (layout type 1,
+    // SWIZZLE_128B_BASE32B; TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 4-row
+    // swizzle period, SBO = 512 B between 4-row K groups, LBO = 4 KB between
+    // 32-element MN chunks (one TMA box each)
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)(4096 >> 4) << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)1 << 61;
+    return d;
+}
+
+template <int BN>
+__host__ __device__ constexpr uint32_t idesc_tf32_mn() {
+    return idesc_tf32<BN>() | (1u << 15) | (1u << 16);  // A and B MN-major
+}
+
+template <int BN>
+struct LayTN {
+    static constexpr int A = BM * BK * 4;   // 4 boxes of 32 x 32
+    static constexpr int B = BN * BK * 4;   // BN/32 boxes
+    static constexpr int STAGE = 2 * A + 2 * B;
+    static constexpr int STAGES = BN >= 256 ? 2 : 3;
+    static constexpr size_t smem() { return 2048 + (size_t)STAGES * STAGE; }
+};
+
+__device__ __forceinline__ float4 tf32_low4(float4 v) {
+    float4 lo;
+    lo.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    return lo;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(THREADS, 1) gemm_tn_kernel(
+    const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, float* __restrict__ part,
+    int M, int N, int K, int kb_per_split, float alpha) {
+    using LY = LayTN<BN>;
+    constexpr int STAGES = LY::STAGES;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(base);
+    uint64_t* split = full + STAGES;
+    uint64_t* empty = split + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+    unsigned char* stages = base + 1024;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, kz = blockIdx.z;
+    const int nk_all = (K + BK - 1) / BK;
+    const int kb0 = kz * kb_per_split, kb1 = min(nk_all, kb0 + kb_per_split);
+    const int nk = max(0, kb1 - kb0);
+    constexpr uint32_t kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+
+    if (threadIdx.x == 0) {
+        tma::prefetch_map(&mA);
+        tma::prefetch_map(&mB);
+        for (int i = 0; i < STAGES; ++i) {
+            tma::mbar_init(&full[i], 1);
+            tma::mbar_init(&split[i], 128);
+            tma::mbar_init(&empty[i], 1);
+        }
+        tma::mbar_init(tfull, 1);
+        tma::fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         tma::smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < nk; ++i) {
+                const int st = i % STAGES;
+                if (i >= STAGES) tma::mbar_wait(&empty[st], ((i / STAGES) & 1) ^ 1);
+                unsigned char* sp = stages + st * LY::STAGE;
+                const int k0 = (kb0 + i) * BK;
+                tma::mbar_arrive_expect_tx(&full[st], LY::A + LY::B);
+#pragma unroll
+                for (int c = 0; c < BM / 32; ++c) tma::load_2d(sp + c * 4096, &mA, m0 + 32 * c, k0, &full[st]);
+#pragma unroll
+                for (int c = 0; c < BN / 32; ++c)
+                    tma::load_2d(sp + 2 * LY::A + c * 4096, &mB, n0 + 32 * c, k0, &full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32_mn<BN>();
+            for (int i = 0; i < nk; ++i) {
+                const int st = i % STAGES;
+                tma::mbar_wait(&split[st], (i / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t sa = tma::smem_u32(stages + st * LY::STAGE);
+                const uint32_t sal = sa + LY::A, sb = sa + 2 * LY::A, sbl = sb + LY::B;
+#pragma unroll
+                for (int k = 0; k < BK / 8; ++k) {
+                    const uint32_t off = k * 1024;  // 8 K-rows x 128 B
+                    const uint64_t dA = sw128_mn_desc(sa + off), dAl = sw128_mn_desc(sal + off);
+                    const uint64_t dB = sw128_mn_desc(sb + off), dBl = sw128_mn_desc(sbl + off);
+                    mma_tf32(tmem, dA, dB, idesc, (i | k) != 0);
+                    mma_tf32(tmem, dA, dBl, idesc, 1);
+                    mma_tf32(tmem, dAl, dB, idesc, 1);
+                }
+                mma_commit(&empty[st]);
+            }
+            mma_commit(tfull);
+        }
+    } else {
+        const int t = threadIdx.x - 64;
+        for (int i = 0; i < nk; ++i) {
+            const int st = i % STAGES;
+            tma::mbar_wait(&full[st], (i / STAGES) & 1);
+            unsigned char* sp = stages + st * LY::STAGE;
+            const float4* a4 = reinterpret_cast<const float4*>(sp);
+            float4* al4 = reinterpret_cast<float4*>(sp + LY::A);
+            const float4* b4 = reinterpret_cast<const float4*>(sp + 2 * LY::A);
+            float4* bl4 = reinterpret_cast<float4*>(sp + 2 * LY::A + LY::B);
+#pragma unroll
+            for (int j = 0; j < LY::A / 16 / 128; ++j) al4[t + 128 * j] = tf32_low4(a4[t + 128 * j]);
+#pragma unroll
+            for (int j = 0; j < LY::B / 16 / 128; ++j) bl4[t + 128 * j] = tf32_low4(b4[t + 128 * j]);
+            tma::fence_proxy_async();
+            tma::mbar_arrive(&split[st]);
+        }
+        const int q = warp & 3;
+        const int row = m0 + 32 * q + lane;
+        float* dst = part + ((int64_t)kz * M + row) * N;
+        if (nk == 0) {
+            if (row < M)
+                for (int c = n0; c < min(N, n0 + BN); ++c) dst[c] = 0.f;
+        } else {
+            tma::mbar_wait(tfull, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                    "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                      "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                      "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+                      "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+                      "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (row < M)
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = n0 + c0 + j;
+                        if (col < N) dst[col] = alpha * __uint_as_float(r[j]);
+                    }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+}
+
 static bool enc_sw128(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows);
 
 template <int BN>
@@ -287,6 +476,53 @@ static bool enc_sw128(CUtensorMap* m, const void* p, uint64_t rows, uint64_t col
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// [rows, cols] fp32 row-major, box [32 rows, 32 cols = 128 B], 128-byte
+// swizzle with 32-byte atoms (the MN-major tf32 UMMA layout)
+static bool enc_sw128_box32(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols) {
+    auto fn = enc_fn();
+    if (!fn || (reinterpret_cast<uintptr_t>(p) & 15) || ((cols * 4) & 15)) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(p), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct TNPlan {
+    int BN, ks, kb_per_split;
+};
+static TNPlan tn_plan(int64_t M, int64_t N, int64_t K) {
+    TNPlan p;
+    p.BN = N <= 64 ? 64 : N <= 128 ? 128 : 256;
+    const int64_t tiles = cdiv(M, BM) * cdiv(N, p.BN);
+    const int64_t nk = cdiv(K, BK);
+    int64_t ks = std::max<int64_t>(1, std::min<int64_t>(cdiv(2 * 148, tiles), nk / 4 > 0 ? nk / 4 : 1));
+    p.kb_per_split = (int)cdiv(nk, ks);
+    p.ks = (int)cdiv(nk, p.kb_per_split);
+    return p;
+}
+
+template <int BN>
+static int launch_tn(const float* A, const float* B, float* part, const TNPlan& pl, int64_t M, int64_t N, int64_t K,
+                     float alpha, cudaStream_t st) {
+    CUtensorMap mA, mB;
+    if (!enc_sw128_box32(&mA, A, K, M) || !enc_sw128_box32(&mB, B, K, N)) {
+        set_error("gemm_tn: TMA descriptor rejected (M, N %% 4 == 0 and 16-byte aligned rows required)");
+        return LRX_ERR_VALUE;
+    }
+    const size_t smem = LayTN<BN>::smem();
+    auto k = gemm_tn_kernel<BN>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        set_error("gemm_tn: cannot reserve %zu B of shared memory", smem);
+        return LRX_ERR_CUDA;
+    }
+    const dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN), (unsigned)pl.ks);
+    k<<<grid, THREADS, smem, st>>>(mA, mB, part, (int)M, (int)N, (int)K, pl.kb_per_split, alpha);
+    return launched("lrx_gemm_f32_tn/tcgen05");
+}
+
 }  // namespace gemm
 }  // namespace lrx
 
@@ -306,6 +542,25 @@ int lrx_gemm_f32(const void* A, const void* Bt, const void* Bt_lo, void* C, cons
     if (N <= 128) return gemm::launch<128>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K,
                                            alpha, beta, st);
     return gemm::launch<256>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K, alpha, beta, st);
+}
+
+int lrx_gemm_f32_tn_splits(int64_t M, int64_t N, int64_t K, int64_t* n_splits) {
+    LRX_REQUIRE(M >= 1 && N >= 1 && K >= 1, LRX_ERR_SHAPE, "gemm_tn: bad extents");
+    *n_splits = gemm::tn_plan(M, N, K).ks;
+    return LRX_OK;
+}
+
+int lrx_gemm_f32_tn(const void* A, const void* B, void* part, int64_t M, int64_t N, int64_t K, float alpha,
+                    void* stream) {
+    LRX_REQUIRE(M >= 1 && N >= 1 && K >= 1, LRX_ERR_SHAPE, "gemm_tn: bad extents M=%lld N=%lld K=%lld",
+                (long long)M, (long long)N, (long long)K);
+    LRX_REQUIRE(M <= (1 << 16) && N <= (1 << 16) && K < (1ll << 31), LRX_ERR_UNSUPPORTED, "gemm_tn: extents too large");
+    const gemm::TNPlan pl = gemm::tn_plan(M, N, K);
+    cudaStream_t st = (cudaStream_t)stream;
+    const float *a = (const float*)A, *b = (const float*)B;
+    if (pl.BN == 64) return gemm::launch_tn<64>(a, b, (float*)part, pl, M, N, K, alpha, st);
+    if (pl.BN == 128) return gemm::launch_tn<128>(a, b, (float*)part, pl, M, N, K, alpha, st);
+    return gemm::launch_tn<256>(a, b, (float*)part, pl, M, N, K, alpha, st);
 }
 
 }  // extern "C"

@@ -373,19 +373,35 @@ class _MIMOBase(LinearRecurrence):
         """(abar, scale) in the compute dtype plus f64 context for the grads."""
         raise NotImplementedError
 
+    def _tc(self, K, T):
+        """fp32 projections run on the tcgen05 3xTF32 GEMMs (ops.gemm_f32 /
+        gemm_f32_tn) when the row width keeps TMA rows 16-byte aligned and
+        there are enough tokens T to fill the GPU with 128-row tiles; f64
+        layers, odd widths and small batches (C1: 8k tokens, launch-bound)
+        use the library (cuBLAS) GEMM."""
+        return self.tdt == torch.float32 and K % 4 == 0 and T >= 32768
+
     def _forward(self, u, deltas, keep):
         B, L, m = u.shape
         P = self._P
         u2 = u.reshape(B * L, m)
-        bu = torch.view_as_complex((u2 @ self._wb()).reshape(B, L, P, 2))   # [B,L,P]
+        if self._tc(m, B * L):
+            bu = torch.view_as_complex(ops.gemm_f32(u2.contiguous(), self._wb().T.contiguous()).reshape(B, L, P, 2))
+        else:
+            bu = torch.view_as_complex((u2 @ self._wb()).reshape(B, L, P, 2))   # [B,L,P]
         abar, scale, extra = self._abar_scale(deltas)
         if deltas is None:
             x = ops.mimo_scan_fwd(abar, scale, bu)
         else:
             x2 = run_fwd(_tm(abar), True, _tm(scale * bu), None)
             x = x2.reshape(L, B, P).transpose(0, 1).contiguous()
-        y = torch.addmm((self.D * u).reshape(B * L, m), torch.view_as_real(x).reshape(B * L, 2 * P), self._wc(),
-                        alpha=self.OUT_SCALE).reshape(B, L, m)
+        if self._tc(2 * P, B * L):  # y = OUT Re(C x) + D u, the D u skip fused into the GEMM epilogue
+            y = ops.gemm_f32(torch.view_as_real(x).reshape(B * L, 2 * P), self._wc().T.contiguous(),
+                             Cin=u2.contiguous(), colscale=self.D.contiguous(),
+                             alpha=self.OUT_SCALE).reshape(B, L, m)
+        else:
+            y = torch.addmm((self.D * u).reshape(B * L, m), torch.view_as_real(x).reshape(B * L, 2 * P), self._wc(),
+                            alpha=self.OUT_SCALE).reshape(B, L, m)
         saved = {"u": u, "x": x, "bu": bu, "deltas": deltas} if keep else {}
         return y, saved, x[:, -1]
 
@@ -408,15 +424,22 @@ class _MIMOBase(LinearRecurrence):
         x2 = torch.view_as_real(x).reshape(B * L, 2 * P)
         osc = self.OUT_SCALE
         gD = (gy * u).sum((0, 1))
-        R = gy2.T @ x2                                                      # [m, 2P]
+        tn = self._tc(m, B * L) and self._tc(2 * P, B * L)
+        R = ops.gemm_f32_tn(gy2.contiguous(), x2) if tn else gy2.T @ x2     # [m, 2P]
         gC_re, gC_im = osc * R[:, 0::2], -osc * R[:, 1::2]
         wg = torch.stack((self.C_re, -self.C_im), dim=-1).reshape(m, 2 * P)
-        gx = torch.view_as_complex((osc * (gy2 @ wg)).reshape(B, L, P, 2)).contiguous()
+        if self._tc(m, B * L):
+            gx = torch.view_as_complex(ops.gemm_f32(gy2.contiguous(), wg.T.contiguous(), alpha=osc).reshape(B, L, P, 2))
+        else:
+            gx = torch.view_as_complex((osc * (gy2 @ wg)).reshape(B, L, P, 2)).contiguous()
         abar, scale, extra = self._abar_scale(deltas)
         gbu, ga, gsc = self._scan_backward(x, bu, gx, abar, scale, deltas)
         gbu2 = torch.view_as_real(gbu.contiguous()).reshape(B * L, 2 * P)
-        R2 = gbu2.T @ u2                                                    # [2P, m]
-        gu = gy * self.D + (gbu2 @ self._wb().T).reshape(B, L, m)
+        R2 = ops.gemm_f32_tn(gbu2, u2.contiguous()) if tn else gbu2.T @ u2  # [2P, m]
+        if self._tc(2 * P, B * L):  # gu = D gy + Re(g conj(B)), the skip fused into the epilogue
+            gu = ops.gemm_f32(gbu2, self._wb(), Cin=gy2.contiguous(), colscale=self.D.contiguous()).reshape(B, L, m)
+        else:
+            gu = gy * self.D + (gbu2 @ self._wb().T).reshape(B, L, m)
         grads = {k: v.to(self.tdt) for k, v in self._coef_grads(ga, gsc, extra, deltas).items()}
         grads.update({"B.re": R2[0::2].contiguous(), "B.im": R2[1::2].contiguous(),
                       "C.re": gC_re.contiguous(), "C.im": gC_im.contiguous(), "D": gD})

@@ -20,7 +20,7 @@ import torch
 from . import _lib
 
 __all__ = ["rglru_scan_fwd", "rglru_scan_bwd", "s6_geometry", "s6_scan_fwd", "s6_scan_bwd", "s6_fwd_carry",
-           "s6_bwd_carry", "mimo_scan_fwd", "mimo_scan_bwd", "reduce_rows", "gemm_f32", "tf32_lo"]
+           "s6_bwd_carry", "mimo_scan_fwd", "mimo_scan_bwd", "reduce_rows", "gemm_f32", "gemm_f32_tn", "tf32_lo"]
 
 
 def reduce_rows(part, rows, cols):
@@ -188,6 +188,18 @@ def gemm_f32(A, Bt, Bt_lo=None, Cin=None, colscale=None, alpha=1.0, beta=0.0, ou
     _lib.check(_lib.lib().lrx_gemm_f32(_lib.ptr(A), _lib.ptr(Bt), _lib.ptr(Bt_lo), _lib.ptr(C), _lib.ptr(Cin),
                                        _lib.ptr(colscale), M, N, K, alpha, beta, _lib.stream()))
     return C
+
+
+def gemm_f32_tn(A, B, alpha=1.0):
+    """C = alpha A^T B for A [K, M], B [K, N] fp32 row-major (K long): split-K
+    tcgen05 3xTF32 partials, summed in a fixed order."""
+    K, M = A.shape
+    N = B.shape[1]
+    ks = _lib.i64()
+    _lib.check(_lib.lib().lrx_gemm_f32_tn_splits(M, N, K, _lib.ref(ks)))
+    part = torch.empty((ks.value, M * N), dtype=torch.float32, device=A.device)
+    _lib.check(_lib.lib().lrx_gemm_f32_tn(_lib.ptr(A), _lib.ptr(B), _lib.ptr(part), M, N, K, alpha, _lib.stream()))
+    return reduce_rows(part, ks.value, M * N).reshape(M, N)
 
 
 # ---------------------------------------------------------------------------

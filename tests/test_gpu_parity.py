@@ -373,3 +373,37 @@ def test_gemm_f32_tcgen05_matches_f64(lrx, M, N, K):
     assert rel(C2, ref2.cpu().numpy()) < 1e-5
     C3 = ops.gemm_f32(A, Bt, Cin=Cin, beta=-0.5)
     assert rel(C3, (ref - 0.5 * Cin.double()).cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("K,M,N", [(4096, 256, 256), (131072, 256, 256), (1000, 128, 64), (77, 64, 192),
+                                   (8192, 128, 128)])
+def test_gemm_f32_tn_tcgen05_matches_f64(lrx, K, M, N):
+    from paper_2602_08810_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(K + M + N)
+    A = torch.randn((K, M), generator=g, device="cuda")
+    B = torch.randn((K, N), generator=g, device="cuda")
+    ref = (A.double().T @ B.double()) * 1.5
+    C = ops.gemm_f32_tn(A, B, alpha=1.5)
+    assert rel(C, ref.cpu().numpy()) < 1e-5
+    C2 = ops.gemm_f32_tn(A, B, alpha=1.5)
+    assert torch.equal(C, C2)  # deterministic split-K
+
+
+@pytest.mark.parametrize("kind", ["s5", "lru"])
+def test_mimo_layer_on_tensor_cores_matches_oracle(lrx, kind):
+    """B*L = 32768 tokens: the projections run on the tcgen05 3xTF32 GEMMs."""
+    from paper_2602_08810_b200 import _lib
+    m, n, B, L = 64, 64, 8, 4096
+    layer = lrx.make_layer(kind, m, n, dtype="f32", seed=19)
+    u = port.Rng(11).normal((B, L, m)).astype(np.float32)
+    gy = port.Rng(12).normal((B, L, m)).astype(np.float32)
+    before = _lib.launch_count()
+    y, tape = layer.forward(u, tape=True)
+    g = lrx.layer_backward(layer, tape, gy)
+    assert _lib.launch_count() - before >= 8  # 4 projection GEMMs + 2 reductions + scans
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64(kind, layer.discretization, params, u, gy)
+    assert rel(y, ry) < TOL["f32"]
+    assert rel(g.u, rgu) < TOL["f32"]
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < TOL["f32"], (k, rel(g.params[k], rg[k]))
