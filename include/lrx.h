@@ -216,6 +216,12 @@ int lrx_mimo_bwd(int dtype, const void* abar, const void* scale, const void* bu,
  * training is bitwise reproducible (test_acceptance.py:249-250).
  * ------------------------------------------------------------------------ */
 int lrx_reduce_rows(int dtype, const void* in, void* out, int64_t R, int64_t N, void* stream);
+/* Same with row groups spread over the GPU (long columns): out[j] =
+ * sum_r in[r,j] (* in2[r,j] when in2 is not NULL: a column-wise dot
+ * product).  Workspace: lrx_reduce_rows_ws_bytes() (0 = none needed). */
+size_t lrx_reduce_rows_ws_bytes(int dtype, int64_t R, int64_t N);
+int lrx_reduce_rows_ws(int dtype, const void* in, const void* in2, void* out, int64_t R, int64_t N, void* ws,
+                       size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -49,6 +49,8 @@ SIGNATURES = {
     "lrx_mimo_bwd_workspace_bytes": (_sz, [_i, _i64, _i64, _i64]),
     "lrx_mimo_bwd": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp]),
     "lrx_reduce_rows": (_i, [_i, _vp, _vp, _i64, _i64, _vp]),
+    "lrx_reduce_rows_ws_bytes": (_sz, [_i, _i64, _i64]),
+    "lrx_reduce_rows_ws": (_i, [_i, _vp, _vp, _vp, _i64, _i64, _vp, _sz, _vp]),
     "lrx_gemm_f32": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_float, ctypes.c_float, _vp]),
     "lrx_gemm_f32_tn_splits": (_i, [_i64, _i64, _i64, _P64]),
     "lrx_gemm_f32_tn": (_i, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_float, _vp]),

@@ -35,6 +35,18 @@ namespace lrx {
 namespace gemm {
 
 constexpr int BM = 128, BK = 32, THREADS = 192;
+constexpr int BKT = 16;  // K-block of the tall kernel: 64-byte rows, 64B swizzle, 4 stages in flight
+
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+    // K-major SWIZZLE_64B: 8-row groups of 64-byte rows = 512 B (SBO), layout type 4
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;
+    return d;
+}
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     // UMMA shared-memory descriptor, K-major SWIZZLE_128B: LBO = 1 (unused),
@@ -71,35 +83,44 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 
 template <int BN>
 struct Lay {
-    static constexpr int A = BM * BK * 4;   // 16 KB
-    static constexpr int B = BN * BK * 4;
+    static constexpr int A = BM * BKT * 4;  // 8 KB
+    static constexpr int B = BN * BKT * 4;
     static constexpr int STAGE = 2 * A + 2 * B;  // A, A_lo, Bt, Bt_lo
-    static constexpr int STAGES = BN >= 256 ? 2 : 3;
-    // 1 KB alignment slack + 1 KB barrier block + the stage ring
-    static constexpr size_t smem() { return 2048 + (size_t)STAGES * STAGE; }
+    static constexpr int STAGES = BN >= 256 ? 4 : 6;
+    static constexpr int EPI = 8 * 32 * 33 * 4;  // per epilogue warp: 32 x 32 fp32 transpose tile (padded)
+    // 1 KB alignment slack + 1 KB barrier block + the stage ring + epilogue tiles
+    static constexpr size_t smem() { return 2048 + (size_t)STAGES * STAGE + EPI; }
 };
 
+// Persistent: CTA c walks output tiles c, c + grid, ... (M-fastest).  Warps:
+// 0 TMA producer, 1 MMA issuer, 2..5 split (A_lo), 6..9 epilogue.  The
+// accumulator is double-buffered in TMEM (2 x BN columns), so the epilogue of
+// tile i (tcgen05.ld -> smem transpose -> coalesced alpha/colscale/Cin
+// row stores) overlaps the mainloop of tile i+1.
+constexpr int THREADS_P = 448;  // + 8 epilogue warps (2 per TMEM lane quarter)
+
 template <int BN>
-__global__ void __launch_bounds__(THREADS, 1) gemm_tf32x3_kernel(
+__global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
     const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
     const __grid_constant__ CUtensorMap mBl, float* C, const float* Cin,
     const float* __restrict__ colscale, int M, int N, int K, float alpha, float beta) {
     using LY = Lay<BN>;
     constexpr int STAGES = LY::STAGES;
     extern __shared__ unsigned char smem_raw[];
-    // 1024-byte alignment for the 128B-swizzle atoms
     unsigned char* base = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(base);     // [STAGES] TMA landed
     uint64_t* split = full + STAGES;                         // [STAGES] A_lo written
     uint64_t* empty = split + STAGES;                        // [STAGES] MMAs done with the stage
-    uint64_t* tfull = empty + STAGES;                        // accumulator ready
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-    unsigned char* stages = base + 1024;                     // 1024-aligned ring
+    uint64_t* tfull = empty + STAGES;                        // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;                            // [2] accumulator drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    unsigned char* stages = base + 1024;
+    float* epi = reinterpret_cast<float*>(stages + STAGES * LY::STAGE);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-    const int nk = (K + BK - 1) / BK;
-    constexpr uint32_t kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    const int nk = (K + BKT - 1) / BKT;
+    const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN, ntiles = tm * tn;
+    constexpr uint32_t kCols = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
 
     if (threadIdx.x == 0) {
         tma::prefetch_map(&mA);
@@ -110,13 +131,16 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tf32x3_kernel(
             tma::mbar_init(&split[i], 128);
             tma::mbar_init(&empty[i], 1);
         }
-        tma::mbar_init(tfull, 1);
+        for (int i = 0; i < 2; ++i) {
+            tma::mbar_init(&tfull[i], 1);
+            tma::mbar_init(&tempty[i], 256);
+        }
         tma::fence_barrier_init();
     }
-    if (warp == 1) {  // TMEM accumulator: 128 lanes x BN fp32 columns
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          tma::smem_u32(tmem_slot)),
-                     "r"(kTmemCols)
+                     "r"(kCols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -127,114 +151,143 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tf32x3_kernel(
 
     if (warp == 0) {
         if (lane == 0) {  // ------------------------------------------ producer
-            for (int kb = 0; kb < nk; ++kb) {
-                const int st = kb % STAGES;
-                if (kb >= STAGES) tma::mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
-                unsigned char* sp = stages + st * LY::STAGE;
-                tma::mbar_arrive_expect_tx(&full[st], LY::A + 2 * LY::B);
-                tma::load_2d(sp, &mA, kb * BK, m0, &full[st]);
-                tma::load_2d(sp + 2 * LY::A, &mB, kb * BK, n0, &full[st]);
-                tma::load_2d(sp + 2 * LY::A + LY::B, &mBl, kb * BK, n0, &full[st]);
+            int it = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int m0 = (tile % tm) * BM, n0 = (tile / tm) * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % STAGES;
+                    if (it >= STAGES) tma::mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
+                    unsigned char* sp = stages + st * LY::STAGE;
+                    tma::mbar_arrive_expect_tx(&full[st], LY::A + 2 * LY::B);
+                    tma::load_2d(sp, &mA, kb * BKT, m0, &full[st]);
+                    tma::load_2d(sp + 2 * LY::A, &mB, kb * BKT, n0, &full[st]);
+                    tma::load_2d(sp + 2 * LY::A + LY::B, &mBl, kb * BKT, n0, &full[st]);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ------------------------------------------ MMA issuer
             constexpr uint32_t idesc = idesc_tf32<BN>();
-            for (int kb = 0; kb < nk; ++kb) {
-                const int st = kb % STAGES;
-                tma::mbar_wait(&split[st], (kb / STAGES) & 1);
+            int it = 0, ti = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+                const int acc = ti & 1;
+                if (ti >= 2) tma::mbar_wait(&tempty[acc], ((ti >> 1) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t sa = tma::smem_u32(stages + st * LY::STAGE);
-                const uint32_t sal = sa + LY::A, sb = sa + 2 * LY::A, sbl = sb + LY::B;
+                const uint32_t td = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % STAGES;
+                    tma::mbar_wait(&split[st], (it / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t sa = tma::smem_u32(stages + st * LY::STAGE);
+                    const uint32_t sal = sa + LY::A, sb = sa + 2 * LY::A, sbl = sb + LY::B;
 #pragma unroll
-                for (int k = 0; k < BK / 8; ++k) {  // 8 tf32 = 32 bytes per UMMA k-step
-                    const uint32_t off = k * 32;
-                    const uint64_t dA = sw128_desc(sa + off), dAl = sw128_desc(sal + off);
-                    const uint64_t dB = sw128_desc(sb + off), dBl = sw128_desc(sbl + off);
-                    mma_tf32(tmem, dA, dB, idesc, (kb | k) != 0);
-                    mma_tf32(tmem, dA, dBl, idesc, 1);
-                    mma_tf32(tmem, dAl, dB, idesc, 1);
+                    for (int k = 0; k < BKT / 8; ++k) {  // 8 tf32 = 32 bytes per UMMA k-step
+                        const uint32_t off = k * 32;
+                        const uint64_t dA = sw64_desc(sa + off), dAl = sw64_desc(sal + off);
+                        const uint64_t dB = sw64_desc(sb + off), dBl = sw64_desc(sbl + off);
+                        mma_tf32(td, dA, dB, idesc, (kb | k) != 0);
+                        mma_tf32(td, dA, dBl, idesc, 1);
+                        mma_tf32(td, dAl, dB, idesc, 1);
+                    }
+                    mma_commit(&empty[st]);  // stage reusable once these MMAs have read it
                 }
-                mma_commit(&empty[st]);  // stage reusable once these MMAs have read it
+                mma_commit(&tfull[acc]);
             }
-            mma_commit(tfull);
         }
-    } else {
+    } else if (warp < 6) {
         // ---------------------------------------------------------- split
         const int t = threadIdx.x - 64;  // 0..127
-        for (int kb = 0; kb < nk; ++kb) {
-            const int st = kb % STAGES;
-            tma::mbar_wait(&full[st], (kb / STAGES) & 1);
-            const float4* a4 = reinterpret_cast<const float4*>(stages + st * LY::STAGE);
-            float4* l4 = reinterpret_cast<float4*>(stages + st * LY::STAGE + LY::A);
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+            for (int kb = 0; kb < nk; ++kb, ++it) {
+                const int st = it % STAGES;
+                tma::mbar_wait(&full[st], (it / STAGES) & 1);
+                const float4* a4 = reinterpret_cast<const float4*>(stages + st * LY::STAGE);
+                float4* l4 = reinterpret_cast<float4*>(stages + st * LY::STAGE + LY::A);
 #pragma unroll
-            for (int i = 0; i < LY::A / 16 / 128; ++i) {
-                const float4 v = a4[t + 128 * i];
-                float4 lo;
-                lo.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                l4[t + 128 * i] = lo;
+                for (int i = 0; i < LY::A / 16 / 128; ++i) {
+                    const float4 v = a4[t + 128 * i];
+                    float4 lo;
+                    lo.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                    l4[t + 128 * i] = lo;
+                }
+                tma::fence_proxy_async();  // generic writes -> async-proxy (MMA) reads
+                tma::mbar_arrive(&split[st]);
             }
-            tma::fence_proxy_async();  // generic writes -> async-proxy (MMA) reads
-            tma::mbar_arrive(&split[st]);
-        }
+    } else {
         // ---------------------------------------------------------- epilogue
-        tma::mbar_wait(tfull, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const int row = m0 + 32 * q + lane;
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-            uint32_t r[32];
-            const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (row < M) {
-                const int64_t ro = (int64_t)row * N;
-                if (n0 + c0 + 32 <= N && (N & 3) == 0) {
+        const int q = warp & 3;            // TMEM lane quarter this warp may access
+        const int half = (warp - 6) >> 2;  // which of the interleaved 32-column chunks
+        float* tp = epi + (warp - 6) * 32 * 33;
+        int ti = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+            const int m0 = (tile % tm) * BM, n0 = (tile / tm) * BN;
+            const int acc = ti & 1;
+            const int rbase = m0 + 32 * q;
+            // skip-input rows for column chunk c0 (lane = column: coalesced);
+            // the next chunk's loads are issued before this chunk is stored
+            float cin[32], cnext[32];
+            auto load_cin = [&](int c0, float* dst) {
+                const int col = n0 + c0 + lane;
+                const bool colok = col < N;
+                const float cs = colok ? (colscale ? colscale[col] : beta) : 0.f;
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        const int col = n0 + c0 + j;
-                        float4 o = make_float4(alpha * __uint_as_float(r[j]), alpha * __uint_as_float(r[j + 1]),
-                                               alpha * __uint_as_float(r[j + 2]), alpha * __uint_as_float(r[j + 3]));
-                        if (Cin) {
-                            const float4 ci = *reinterpret_cast<const float4*>(Cin + ro + col);
-                            float4 s = make_float4(beta, beta, beta, beta);
-                            if (colscale) s = *reinterpret_cast<const float4*>(colscale + col);
-                            o.x = fmaf(s.x, ci.x, o.x);
-                            o.y = fmaf(s.y, ci.y, o.y);
-                            o.z = fmaf(s.z, ci.z, o.z);
-                            o.w = fmaf(s.w, ci.w, o.w);
-                        }
-                        *reinterpret_cast<float4*>(C + ro + col) = o;
-                    }
-                } else {
-                    for (int j = 0; j < 32; ++j) {
-                        const int col = n0 + c0 + j;
-                        if (col < N) {
-                            float o = alpha * __uint_as_float(r[j]);
-                            if (Cin) o = fmaf(colscale ? colscale[col] : beta, Cin[ro + col], o);
-                            C[ro + col] = o;
-                        }
+                for (int i = 0; i < 32; ++i)
+                    dst[i] = (colok && rbase + i < M) ? cs * __ldcs(Cin + (int64_t)(rbase + i) * N + col) : 0.f;
+            };
+            if (Cin) load_cin(32 * half, cnext);
+            tma::mbar_wait(&tfull[acc], (ti >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int c0 = 32 * half; c0 < BN; c0 += 64) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + acc * BN + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                    "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                      "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                      "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+                      "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+                      "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c0 + 64 >= BN) {  // this warp's last chunk: accumulator reads done
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    tma::mbar_arrive(&tempty[acc]);
+                }
+                // transpose through shared memory: lane holds row (32q + lane), 32 columns;
+                // write back rows with the lane index on the column (coalesced)
+#pragma unroll
+                for (int j = 0; j < 32; ++j) tp[lane * 33 + j] = __uint_as_float(r[j]);
+                __syncwarp();
+                const int col = n0 + c0 + lane;
+                const bool colok = col < N;
+                if (Cin) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) cin[i] = cnext[i];
+                    if (c0 + 64 < BN) load_cin(c0 + 64, cnext);
+                }
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int row = rbase + i;
+                    if (row < M && colok) {
+                        float v = alpha * tp[i * 33 + lane];
+                        if (Cin) v += cin[i];
+                        __stcs(C + (int64_t)row * N + col, v);
                     }
                 }
+                __syncwarp();
             }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
 }
 
 // ============================================================================
@@ -249,14 +302,17 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tf32x3_kernel(
 // of 32 K-rows x 32 fp32 (128 B) is 8 atoms of 4 K-rows x 128 B stacked at
 // 512 B (SBO); the next 32-wide MN chunk is the next box, 4 KB on (LBO).  One
 // UMMA k-step of 8 tf32 rows = two atoms: advance the start address by 1 KB.
+constexpr int BKN = 16;  // K-block (rows) of the TN kernel: boxes of 16 rows x 128 B
+constexpr int THREADS_TN = 320;  // TMA, MMA, 8 split warps (the first 4 also run the epilogue)
+
 __device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr) {
     // MN-major tf32 needs the 128B swizzle with 32-byte atoms (layout type 1,
     // SWIZZLE_128B_BASE32B; TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 4-row
-    // swizzle period, SBO = 512 B between 4-row K groups, LBO = 4 KB between
-    // 32-element MN chunks (one TMA box each)
+    // swizzle period, SBO = 512 B between 4-row K groups, LBO = one box
+    // (BKN rows x 128 B) between 32-element MN chunks
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)(4096 >> 4) << 16;
+    d |= (uint64_t)((BKN * 128) >> 4) << 16;
     d |= (uint64_t)(512 >> 4) << 32;
     d |= (uint64_t)1 << 46;
     d |= (uint64_t)1 << 61;
@@ -270,10 +326,10 @@ __host__ __device__ constexpr uint32_t idesc_tf32_mn() {
 
 template <int BN>
 struct LayTN {
-    static constexpr int A = BM * BK * 4;   // 4 boxes of 32 x 32
-    static constexpr int B = BN * BK * 4;   // BN/32 boxes
+    static constexpr int A = BM * BKN * 4;  // 4 boxes of BKN x 32
+    static constexpr int B = BN * BKN * 4;  // BN/32 boxes
     static constexpr int STAGE = 2 * A + 2 * B;
-    static constexpr int STAGES = BN >= 256 ? 2 : 3;
+    static constexpr int STAGES = BN >= 256 ? 4 : 6;
     static constexpr size_t smem() { return 2048 + (size_t)STAGES * STAGE; }
 };
 
@@ -287,7 +343,7 @@ __device__ __forceinline__ float4 tf32_low4(float4 v) {
 }
 
 template <int BN>
-__global__ void __launch_bounds__(THREADS, 1) gemm_tn_kernel(
+__global__ void __launch_bounds__(THREADS_TN, 1) gemm_tn_kernel(
     const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, float* __restrict__ part,
     int M, int N, int K, int kb_per_split, float alpha) {
     using LY = LayTN<BN>;
@@ -303,7 +359,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tn_kernel(
     unsigned char* stages = base + 1024;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, kz = blockIdx.z;
-    const int nk_all = (K + BK - 1) / BK;
+    const int nk_all = (K + BKN - 1) / BKN;
     const int kb0 = kz * kb_per_split, kb1 = min(nk_all, kb0 + kb_per_split);
     const int nk = max(0, kb1 - kb0);
     constexpr uint32_t kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
@@ -313,7 +369,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tn_kernel(
         tma::prefetch_map(&mB);
         for (int i = 0; i < STAGES; ++i) {
             tma::mbar_init(&full[i], 1);
-            tma::mbar_init(&split[i], 128);
+            tma::mbar_init(&split[i], 256);
             tma::mbar_init(&empty[i], 1);
         }
         tma::mbar_init(tfull, 1);
@@ -337,13 +393,13 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tn_kernel(
                 const int st = i % STAGES;
                 if (i >= STAGES) tma::mbar_wait(&empty[st], ((i / STAGES) & 1) ^ 1);
                 unsigned char* sp = stages + st * LY::STAGE;
-                const int k0 = (kb0 + i) * BK;
+                const int k0 = (kb0 + i) * BKN;
                 tma::mbar_arrive_expect_tx(&full[st], LY::A + LY::B);
 #pragma unroll
-                for (int c = 0; c < BM / 32; ++c) tma::load_2d(sp + c * 4096, &mA, m0 + 32 * c, k0, &full[st]);
+                for (int c = 0; c < BM / 32; ++c) tma::load_2d(sp + c * BKN * 128, &mA, m0 + 32 * c, k0, &full[st]);
 #pragma unroll
                 for (int c = 0; c < BN / 32; ++c)
-                    tma::load_2d(sp + 2 * LY::A + c * 4096, &mB, n0 + 32 * c, k0, &full[st]);
+                    tma::load_2d(sp + 2 * LY::A + c * BKN * 128, &mB, n0 + 32 * c, k0, &full[st]);
             }
         }
     } else if (warp == 1) {
@@ -356,7 +412,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tn_kernel(
                 const uint32_t sa = tma::smem_u32(stages + st * LY::STAGE);
                 const uint32_t sal = sa + LY::A, sb = sa + 2 * LY::A, sbl = sb + LY::B;
 #pragma unroll
-                for (int k = 0; k < BK / 8; ++k) {
+                for (int k = 0; k < BKN / 8; ++k) {
                     const uint32_t off = k * 1024;  // 8 K-rows x 128 B
                     const uint64_t dA = sw128_mn_desc(sa + off), dAl = sw128_mn_desc(sal + off);
                     const uint64_t dB = sw128_mn_desc(sb + off), dBl = sw128_mn_desc(sbl + off);
@@ -369,7 +425,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tn_kernel(
             mma_commit(tfull);
         }
     } else {
-        const int t = threadIdx.x - 64;
+        const int t = threadIdx.x - 64;  // 8 split warps: 0..255
         for (int i = 0; i < nk; ++i) {
             const int st = i % STAGES;
             tma::mbar_wait(&full[st], (i / STAGES) & 1);
@@ -379,12 +435,14 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tn_kernel(
             const float4* b4 = reinterpret_cast<const float4*>(sp + 2 * LY::A);
             float4* bl4 = reinterpret_cast<float4*>(sp + 2 * LY::A + LY::B);
 #pragma unroll
-            for (int j = 0; j < LY::A / 16 / 128; ++j) al4[t + 128 * j] = tf32_low4(a4[t + 128 * j]);
+            for (int j = 0; j < LY::A / 16 / 256; ++j) al4[t + 256 * j] = tf32_low4(a4[t + 256 * j]);
 #pragma unroll
-            for (int j = 0; j < LY::B / 16 / 128; ++j) bl4[t + 128 * j] = tf32_low4(b4[t + 128 * j]);
+            for (int j = 0; j < LY::B / 16 / 256; ++j) bl4[t + 256 * j] = tf32_low4(b4[t + 256 * j]);
             tma::fence_proxy_async();
             tma::mbar_arrive(&split[st]);
         }
+        if (warp >= 6) goto done;  // warps 2..5 cover the four TMEM lane quarters
+        {
         const int q = warp & 3;
         const int row = m0 + 32 * q + lane;
         float* dst = part + ((int64_t)kz * M + row) * N;
@@ -415,7 +473,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tn_kernel(
                     }
             }
         }
+        }
     }
+done:
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1)
@@ -423,12 +483,13 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tn_kernel(
 }
 
 static bool enc_sw128(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows);
+static bool enc_k(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows);
 
 template <int BN>
 static int launch(const float* A, const float* Bt, const float* Btl, float* C, const float* Cin, const float* cs,
                   int64_t M, int64_t N, int64_t K, float alpha, float beta, cudaStream_t st) {
     CUtensorMap mA, mB, mBl;
-    if (!enc_sw128(&mA, A, M, K, BM) || !enc_sw128(&mB, Bt, N, K, BN) || !enc_sw128(&mBl, Btl, N, K, BN)) {
+    if (!enc_k(&mA, A, M, K, BM) || !enc_k(&mB, Bt, N, K, BN) || !enc_k(&mBl, Btl, N, K, BN)) {
         set_error("gemm: TMA descriptor rejected (K %% 4 == 0 and 16-byte aligned rows required)");
         return LRX_ERR_VALUE;
     }
@@ -438,8 +499,16 @@ static int launch(const float* A, const float* Bt, const float* Btl, float* C, c
         set_error("gemm: cannot reserve %zu B of shared memory", smem);
         return LRX_ERR_CUDA;
     }
-    const dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN));
-    k<<<grid, THREADS, smem, st>>>(mA, mB, mBl, C, Cin, cs, (int)M, (int)N, (int)K, alpha, beta);
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const int64_t tiles = cdiv(M, BM) * cdiv(N, BN);
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+    k<<<grid, THREADS_P, smem, st>>>(mA, mB, mBl, C, Cin, cs, (int)M, (int)N, (int)K, alpha, beta);
     return launched("lrx_gemm_f32/tcgen05");
 }
 
@@ -476,6 +545,19 @@ static bool enc_sw128(CUtensorMap* m, const void* p, uint64_t rows, uint64_t col
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// [rows, cols] fp32 row-major, box [box_rows, BKT = 16 cols = 64 B], 64-byte swizzle
+static bool enc_k(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    auto fn = enc_fn();
+    if (!fn || (reinterpret_cast<uintptr_t>(p) & 15) || ((cols * 4) & 15)) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 4};
+    cuuint32_t box[2] = {BKT, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(p), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // [rows, cols] fp32 row-major, box [32 rows, 32 cols = 128 B], 128-byte
 // swizzle with 32-byte atoms (the MN-major tf32 UMMA layout)
 static bool enc_sw128_box32(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols) {
@@ -483,7 +565,7 @@ static bool enc_sw128_box32(CUtensorMap* m, const void* p, uint64_t rows, uint64
     if (!fn || (reinterpret_cast<uintptr_t>(p) & 15) || ((cols * 4) & 15)) return false;
     cuuint64_t dims[2] = {cols, rows};
     cuuint64_t strides[1] = {cols * 4};
-    cuuint32_t box[2] = {32, 32};
+    cuuint32_t box[2] = {32, BKN};
     cuuint32_t es[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(p), dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -497,7 +579,7 @@ static TNPlan tn_plan(int64_t M, int64_t N, int64_t K) {
     TNPlan p;
     p.BN = N <= 64 ? 64 : N <= 128 ? 128 : 256;
     const int64_t tiles = cdiv(M, BM) * cdiv(N, p.BN);
-    const int64_t nk = cdiv(K, BK);
+    const int64_t nk = cdiv(K, BKN);
     int64_t ks = std::max<int64_t>(1, std::min<int64_t>(cdiv(2 * 148, tiles), nk / 4 > 0 ? nk / 4 : 1));
     p.kb_per_split = (int)cdiv(nk, ks);
     p.ks = (int)cdiv(nk, p.kb_per_split);
@@ -519,7 +601,7 @@ static int launch_tn(const float* A, const float* B, float* part, const TNPlan& 
         return LRX_ERR_CUDA;
     }
     const dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN), (unsigned)pl.ks);
-    k<<<grid, THREADS, smem, st>>>(mA, mB, part, (int)M, (int)N, (int)K, pl.kb_per_split, alpha);
+    k<<<grid, THREADS_TN, smem, st>>>(mA, mB, part, (int)M, (int)N, (int)K, pl.kb_per_split, alpha);
     return launched("lrx_gemm_f32_tn/tcgen05");
 }
 
@@ -539,7 +621,9 @@ int lrx_gemm_f32(const void* A, const void* Bt, const void* Bt_lo, void* C, cons
     const float *a = (const float*)A, *b = (const float*)Bt, *bl = (const float*)Bt_lo;
     if (N <= 64) return gemm::launch<64>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K, alpha,
                                          beta, st);
-    if (N <= 128) return gemm::launch<128>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K,
+    const char* e = getenv("LRX_GEMM_BN");
+    const int bn_cap = e ? atoi(e) : 256;
+    if (N <= 128 || bn_cap <= 128) return gemm::launch<128>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K,
                                            alpha, beta, st);
     return gemm::launch<256>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K, alpha, beta, st);
 }

@@ -17,6 +17,8 @@
 #include <string.h>
 
 #include "lrx_common.cuh"
+
+#include <algorithm>
 #include "lrx_host.h"
 
 namespace lrx {
@@ -219,6 +221,80 @@ static void reduce_rows_launch(const V* in, V* out, int64_t R, int64_t N, cudaSt
     reduce_rows_kernel<V><<<(unsigned)blocks, 32 * RL, 32 * RL * sizeof(V), st>>>(in, out, R, N);
 }
 
+// Two-stage variant for long columns: stage 1 folds row groups of `rpg`
+// rows (optionally of the elementwise product in[r,j] * in2[r,j]) into
+// partials [G, N]; stage 2 is reduce_rows_kernel over the G partials.  Fixed
+// order throughout (deterministic for given R, N).
+template <typename V>
+__global__ void reduce_rows_part_kernel(const V* __restrict__ in, const V* __restrict__ in2, V* __restrict__ part,
+                                        int64_t R, int64_t N, int64_t rpg) {
+    __shared__ V red[256];
+    const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;  // 8 row lanes
+    const int64_t j = (int64_t)blockIdx.x * 32 + c;
+    const int64_t rb = (int64_t)blockIdx.y * rpg, re = min(R, rb + rpg);
+    V acc = Traits<V>::zero();
+    if (j < N) {
+        // four independent partial sums keep four rows' loads in flight
+        V a1 = Traits<V>::zero(), a2 = a1, a3 = a1;
+        int64_t r = rb + r0;
+        if (in2) {
+            for (; r + 24 < re; r += 32) {
+                acc = acc + in[r * N + j] * in2[r * N + j];
+                a1 = a1 + in[(r + 8) * N + j] * in2[(r + 8) * N + j];
+                a2 = a2 + in[(r + 16) * N + j] * in2[(r + 16) * N + j];
+                a3 = a3 + in[(r + 24) * N + j] * in2[(r + 24) * N + j];
+            }
+            for (; r < re; r += 8) acc = acc + in[r * N + j] * in2[r * N + j];
+        } else {
+            for (; r + 24 < re; r += 32) {
+                acc = acc + in[r * N + j];
+                a1 = a1 + in[(r + 8) * N + j];
+                a2 = a2 + in[(r + 16) * N + j];
+                a3 = a3 + in[(r + 24) * N + j];
+            }
+            for (; r < re; r += 8) acc = acc + in[r * N + j];
+        }
+        acc = (acc + a1) + (a2 + a3);
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int h = 4; h >= 1; h >>= 1) {
+        if (r0 < h) red[threadIdx.x] = red[threadIdx.x] + red[threadIdx.x + 32 * h];
+        __syncthreads();
+    }
+    if (r0 == 0 && j < N) part[(int64_t)blockIdx.y * N + j] = red[c];
+}
+
+static int64_t reduce_groups(int64_t R, int64_t N) {
+    const int64_t cb = cdiv(N, 32);
+    int64_t G = cdiv(4 * 148, cb);                 // ~4 blocks of 256 threads per SM
+    G = std::min<int64_t>(G, std::max<int64_t>(1, R / 256));
+    return std::max<int64_t>(1, G);
+}
+
+template <typename V>
+static size_t reduce_ws(int64_t R, int64_t N) {
+    const int64_t G = reduce_groups(R, N);
+    return G > 1 ? (size_t)G * N * sizeof(V) : 0;
+}
+
+template <typename V>
+static int reduce_rows2(const V* in, const V* in2, V* out, int64_t R, int64_t N, void* ws, size_t wb,
+                        cudaStream_t st) {
+    const int64_t G = reduce_groups(R, N);
+    const int64_t rpg = cdiv(R, G);
+    if (G == 1) {
+        reduce_rows_part_kernel<V><<<dim3((unsigned)cdiv(N, 32), 1), 256, 0, st>>>(in, in2, out, R, N, rpg);
+        return launched("lrx_reduce_rows_ws");
+    }
+    LRX_REQUIRE(ws && wb >= (size_t)G * N * sizeof(V), LRX_ERR_VALUE, "reduce_rows: workspace of %zu bytes needed",
+                (size_t)G * N * sizeof(V));
+    V* part = static_cast<V*>(ws);
+    reduce_rows_part_kernel<V><<<dim3((unsigned)cdiv(N, 32), (unsigned)G), 256, 0, st>>>(in, in2, part, R, N, rpg);
+    reduce_rows_launch<V>(part, out, G, N, st);
+    return launched("lrx_reduce_rows_ws", 2);
+}
+
 // ---------------------------------------------------------------- host side
 template <typename V>
 static void chunking(int64_t L, int64_t N, int* n_chunks, int* n_blk) {
@@ -357,6 +433,30 @@ int lrx_scan_bwd(int dtype, int a_per_step, const void* a, const void* x, const 
     LRX_REQUIRE(!ga || x, LRX_ERR_VALUE, "grad_a needs the forward states x");
     LRX_DISPATCH(dtype, bwd_t, a_per_step, a, x, x0, gx, gb, ga, gx0, L, N, workspace, workspace_bytes,
                  (cudaStream_t)stream)
+}
+
+size_t lrx_reduce_rows_ws_bytes(int dtype, int64_t R, int64_t N) {
+    if (R < 1 || N < 1) return 0;
+    LRX_DISPATCH_SZ(dtype, reduce_ws, R, N)
+}
+
+int lrx_reduce_rows_ws(int dtype, const void* in, const void* in2, void* out, int64_t R, int64_t N, void* ws,
+                       size_t ws_bytes, void* stream) {
+    LRX_REQUIRE(R >= 1 && N >= 1, LRX_ERR_SHAPE, "bad extents R=%lld N=%lld", (long long)R, (long long)N);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (dtype) {
+        case LRX_F32: return reduce_rows2<float>((const float*)in, (const float*)in2, (float*)out, R, N, ws, ws_bytes, st);
+        case LRX_F64:
+            return reduce_rows2<double>((const double*)in, (const double*)in2, (double*)out, R, N, ws, ws_bytes, st);
+        case LRX_C64:
+            return reduce_rows2<cplx<float>>((const cplx<float>*)in, (const cplx<float>*)in2, (cplx<float>*)out, R, N,
+                                             ws, ws_bytes, st);
+        case LRX_C128:
+            return reduce_rows2<cplx<double>>((const cplx<double>*)in, (const cplx<double>*)in2, (cplx<double>*)out,
+                                              R, N, ws, ws_bytes, st);
+    }
+    set_error("unsupported dtype %d", dtype);
+    return LRX_ERR_VALUE;
 }
 
 int lrx_reduce_rows(int dtype, const void* in, void* out, int64_t R, int64_t N, void* stream) {

@@ -423,7 +423,7 @@ class _MIMOBase(LinearRecurrence):
         gy2, u2 = gy.reshape(B * L, m), u.reshape(B * L, m)
         x2 = torch.view_as_real(x).reshape(B * L, 2 * P)
         osc = self.OUT_SCALE
-        gD = (gy * u).sum((0, 1))
+        gD = ops.reduce_rows(gy2.contiguous(), B * L, m, other=u2.contiguous())  # sum_t gy u per channel
         tn = self._tc(m, B * L) and self._tc(2 * P, B * L)
         R = ops.gemm_f32_tn(gy2.contiguous(), x2) if tn else gy2.T @ x2     # [m, 2P]
         gC_re, gC_im = osc * R[:, 0::2], -osc * R[:, 1::2]

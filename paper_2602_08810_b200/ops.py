@@ -23,11 +23,17 @@ __all__ = ["rglru_scan_fwd", "rglru_scan_bwd", "s6_geometry", "s6_scan_fwd", "s6
            "s6_bwd_carry", "mimo_scan_fwd", "mimo_scan_bwd", "reduce_rows", "gemm_f32", "gemm_f32_tn", "tf32_lo"]
 
 
-def reduce_rows(part, rows, cols):
-    """Fixed-order device reduction out[j] = sum_r part[r, j]."""
+def reduce_rows(part, rows, cols, other=None):
+    """Fixed-order device reduction out[j] = sum_r part[r, j] (* other[r, j]:
+    a column-wise dot product when `other` is given)."""
     out = torch.empty(cols, dtype=part.dtype, device=part.device)
-    _lib.check(_lib.lib().lrx_reduce_rows(_lib.code_of(part.dtype), _lib.ptr(part), _lib.ptr(out), rows, cols,
-                                          _lib.stream()))
+    lib, code = _lib.lib(), _lib.code_of(part.dtype)
+    if other is None and rows <= 4096:  # short columns: one launch, no workspace
+        _lib.check(lib.lrx_reduce_rows(code, _lib.ptr(part), _lib.ptr(out), rows, cols, _lib.stream()))
+        return out
+    ws = _lib.workspace(lib.lrx_reduce_rows_ws_bytes(code, rows, cols), part.device)
+    _lib.check(lib.lrx_reduce_rows_ws(code, _lib.ptr(part), _lib.ptr(other), _lib.ptr(out), rows, cols,
+                                      _lib.ptr(ws), ws.numel(), _lib.stream()))
     return out
 
 
