@@ -73,6 +73,16 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _tensor_peak():
+    """TF32 dense tensor peak = half the measured bf16 GEMM rate (Blackwell runs
+    kind::tf32 at 1/2 the kind::f16 rate)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]) / 2, "measured bf16 / 2 (tf32)"
+    except Exception:
+        return 1590.0 / 2, "fallback bf16 / 2 (tf32)"
+
+
 def _traffic(workload, kernel):
     """Per-launch DRAM bytes from the committed ncu capture (profiles/), or None."""
     try:
@@ -139,6 +149,11 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # GPU arm
 
+def _lib_ws(nbytes, device):
+    import torch
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
 def build_problem(w, B, device, L=None, group=None):
     """Synthetic inputs (reference init + N(0,1) activations, on device) and a
     step function fwd+bwd at the operator boundary.  `L` overrides the
@@ -175,6 +190,8 @@ def build_problem(w, B, device, L=None, group=None):
         # algorithmic bytes: fwd reads u, qr, qi, writes y; bwd reads
         # u, qr, qi, gy and writes gu, gqr, gqi (the states are not counted)
         prob["bytes"] = {"fwd": 4 * B * L * H * bpe, "bwd": 7 * B * L * H * bpe}
+        prob["probe"] = dict(name="lrx_rglru_bwd (+3 column sums)", bound="hbm", amount=prob["bytes"]["bwd"],
+                             fn=bwd)
     elif kind == "s6":
         with torch.no_grad():
             from paper_2602_08810_b200.layers import _mm
@@ -205,6 +222,30 @@ def build_problem(w, B, device, L=None, group=None):
         per = B * L * H
         prob["bytes"] = {"fwd": per * (2 * bu + bp) + 2 * B * L * N * bp,
                          "bwd": per * (3 * bu + 2 * bp) + 4 * B * L * N * bp}
+        # dominant kernel: the backward scan alone (C-ABI call, outputs preallocated)
+        geo = ops.s6_geometry(u.dtype, B, L, H, N)
+        f = dict(dtype=torch.float32, device=device)
+        pb = {"gu": torch.empty_like(u), "gpre": torch.empty((B, L, H), **f),
+              "gB": torch.empty((geo["n_dblk"], B * L * N), **f), "gC": torch.empty((geo["n_dblk"], B * L * N), **f),
+              "ga": torch.empty((geo["part_rows"], H * N), **f), "gD": torch.empty((geo["part_rows"], H), **f),
+              "gb": torch.empty((geo["part_rows"], H), **f), "ws": _lib_ws(geo["ws_bytes"], device)}
+
+        def probe(ctx):
+            from paper_2602_08810_b200 import _lib as L_
+            ck = ctx[1]["ckpt"] if isinstance(ctx[1], dict) else ctx[1]
+            L_.check(L_.lib().lrx_s6_bwd(
+                L_.code_of(u.dtype), L_.ptr(prob["u"]), L_.ptr(prob["pre"]), L_.ptr(pa[0]), L_.ptr(pa[1]),
+                L_.ptr(prob["Bk"]), L_.ptr(prob["Ck"]), L_.ptr(layer.D), L_.ptr(ck), L_.ptr(prob["gy"]), None,
+                L_.ptr(pb["gu"]), L_.ptr(pb["gpre"]), L_.ptr(pb["gB"]), L_.ptr(pb["gC"]), L_.ptr(pb["ga"]),
+                L_.ptr(pb["gD"]), L_.ptr(pb["gb"]), None, B, L, H, N, L_.ptr(pb["ws"]), pb["ws"].numel(), 0,
+                L_.stream()))
+
+        # MUFU-bound in fact (2 ex2 per (t, d, n) + softplus per (t, d)): reported beside the HBM roofline
+        prob["probe"] = dict(name="lrx_s6_bwd" + (" (segment aggregates + main)" if geo["n_seg"] > 1 else ""),
+                             bound="hbm", amount=prob["bytes"]["bwd"], fn=probe,
+                             # main pass: 2 ex2 per (t,d,n) + softplus/sigmoid per (t,d); aggregate
+                             # pass (segments > 1): 1 ex2 per (t,d,n) + softplus on (S-1)/S of the steps
+                             mufu_ops=B * L * H * ((2 * N + 3) + (N + 2) * (geo["n_seg"] - 1) / geo["n_seg"]))
     else:  # s5 / lru: projections are part of the recurrence
         def fwd():
             return layer._forward(prob["u"], None, True)
@@ -219,6 +260,22 @@ def build_problem(w, B, device, L=None, group=None):
         st = B * L * N * c
         prob["bytes"] = {"fwd": 2 * per, "bwd": 3 * per}  # fused minimum: u,y / u,gy,gu
         prob["bytes_scan"] = {"fwd": 2 * st, "bwd": 4 * st}
+        T_, P2 = B * L, 2 * (N if kind == "lru" else N // 2)
+        if layer._tc(H, T_) and layer._tc(P2, T_):
+            # dominant kernel: the skip-fused output projection y = OUT Re(C x) + D u on tcgen05 (3xTF32);
+            # achieved = issued TF32 tensor FLOP/s (3 MMAs per fp32 product)
+            xs = torch.randn((T_, P2), device=device)
+            wct = layer._wc().T.contiguous()
+            wcl = ops.tf32_lo(wct)
+            u2 = prob["u"].reshape(T_, H)
+            yo = torch.empty((T_, H), device=device)
+            prob["probe"] = dict(name="lrx_gemm_f32 (tcgen05 3xTF32, y = OUT Re(Cx) + D u)", bound="tensor",
+                                 amount=3 * 2 * T_ * P2 * H,
+                                 fn=lambda ctx: ops.gemm_f32(xs, wct, wcl, Cin=u2, colscale=layer.D,
+                                                             alpha=layer.OUT_SCALE, out=yo))
+        else:
+            prob["probe"] = dict(name=f"lrx_{kind}_bwd (projections + scan)", bound="hbm", amount=3 * per,
+                                 fn=lambda ctx: bwd(ctx))
     prob["fwd"], prob["bwd"] = fwd, bwd
     return prob
 
@@ -285,6 +342,26 @@ def run_gpu(args, w, rank, world, device):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, ms_fwd, ms_bwd = (float(v) for v in t.tolist())
 
+    # dominant kernel alone, CUDA events on the launching stream, after the timed region
+    pr = prob["probe"]
+    ctx = fwd()
+    for _ in range(2):
+        pr["fn"](ctx)
+    torch.cuda.synchronize()
+    ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ka.record(stream)
+    nrep = max(3, args.steps)
+    for _ in range(nrep):
+        pr["fn"](ctx)
+    kb.record(stream)
+    torch.cuda.synchronize()
+    probe_ms = ka.elapsed_time(kb) / nrep
+    del ctx
+    pt = torch.tensor([probe_ms], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+    probe_ms = float(pt.item())
+
     # e2e through the public API with pinned host buffers (a batch slice)
     e2e = run_e2e(args, w, prob, device)
     if world > 1:
@@ -292,7 +369,8 @@ def run_gpu(args, w, rank, world, device):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e["ms"] = float(te.item())
     return {"ms": ms, "ms_fwd": ms_fwd, "ms_bwd": ms_bwd, "launches": launches, "clocks": clocks.summary(),
-            "bytes": prob["bytes"], "B_rank": B, "e2e": e2e}
+            "bytes": prob["bytes"], "B_rank": B, "e2e": e2e, "probe": {k: v for k, v in pr.items() if k != "fn"},
+            "probe_ms": probe_ms}
 
 
 def run_e2e(args, w, prob, device):
@@ -474,14 +552,24 @@ def main():
             dist.destroy_process_group()
         return
     value = elems / (r["ms"] * 1e-3) / 1e9
-    peak, peak_kind = _peaks()
-    dom = "bwd" if r["ms_bwd"] >= r["ms_fwd"] else "fwd"
-    dom_ms = r["ms_bwd"] if dom == "bwd" else r["ms_fwd"]
-    achieved = r["bytes"][dom] / (dom_ms * 1e-3) / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": _traffic(args.workload, dom), "kernel": f"lrx_{w['kind']}_{dom}",
-            "peak_source": peak_kind, "per_launch_ms": dom_ms,
-            "algorithmic_bytes_per_launch": r["bytes"][dom]}
+    pr, pms = r["probe"], r["probe_ms"]
+    if pr["bound"] == "tensor":
+        tpk, tsrc = _tensor_peak()
+        achieved = pr["amount"] / (pms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tpk, "unit": "TFLOP/s", "frac": achieved / tpk,
+                "traffic": _traffic(args.workload, "probe"), "kernel": pr["name"], "peak_source": tsrc,
+                "per_launch_ms": pms, "algorithmic_flops_per_launch": pr["amount"]}
+    else:
+        peak, peak_kind = _peaks()
+        achieved = pr["amount"] / (pms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": _traffic(args.workload, "probe"), "kernel": pr["name"], "peak_source": peak_kind,
+                "per_launch_ms": pms, "algorithmic_bytes_per_launch": pr["amount"],
+                "step_share": pms / r["ms"]}
+        if "mufu_ops" in pr:  # the binding unit of the S6 scan: MUFU ex2 (16/clk/SM, ubench-measured 4.62 T/s)
+            mu = pr["mufu_ops"] / (pms * 1e-3) / 1e12
+            roof["compute"] = {"bound": "mufu", "achieved": mu, "peak": 4.62, "unit": "Tops/s", "frac": mu / 4.62,
+                               "peak_source": "tools/ubench/mufu.cu on this pool's B200 (ex2.approx.f32)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         v, desc, cores = cpu_sample(w)
