@@ -317,6 +317,127 @@ __global__ void __launch_bounds__(LW) bwd_tma_kernel(
     }
 }
 
+// Backward without the y stream: time tiles of one checkpoint chunk (RC = 16
+// rows of u, qr, qi, gy by TMA); per chunk the states are recomputed from the
+// forward's checkpoint into registers, then the reverse recurrence runs over
+// the staged rows again.  7 array passes instead of 8 (y is not read) for a
+// second evaluation of the gates (MUFU has the headroom: the kernel is
+// HBM-bound).  CTAs are not all co-resident (waves of LW-lane blocks).
+template <typename IO, typename C, int LW, int RC>
+__global__ void __launch_bounds__(LW) bwd_rc_kernel(
+    const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mr,
+    const __grid_constant__ CUtensorMap mi, const __grid_constant__ CUtensorMap mg, const C* __restrict__ lam,
+    const C* __restrict__ b_r, const C* __restrict__ b_i, const C* __restrict__ ckpt, IO* __restrict__ gu,
+    IO* __restrict__ gqr, IO* __restrict__ gqi, C* __restrict__ gla_part, C* __restrict__ gbr_part,
+    C* __restrict__ gbi_part, int64_t L, int64_t W, int n_wblk, int Bn, int S) {
+    constexpr int NW = LW / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    auto R = ring<IO>(smem, S);
+    const int tid = threadIdx.x;
+    const int b = blockIdx.x / n_wblk;
+    const int w0 = (blockIdx.x % n_wblk) * LW;
+    const int64_t w = w0 + tid;
+    const bool valid = w < W;
+    const int row0 = b * (int)L;
+    const int n_tiles = (int)((L + RC - 1) / RC);
+    constexpr uint32_t kStageBytes = 4u * RC * LW * sizeof(IO);
+    if (tid == 0) {
+        tma::prefetch_map(&mu);
+        tma::prefetch_map(&mr);
+        tma::prefetch_map(&mi);
+        tma::prefetch_map(&mg);
+        for (int s = 0; s < S; ++s) {
+            tma::mbar_init(&R.full[s], 1);
+            tma::mbar_init(&R.empty[s], NW);
+        }
+        tma::fence_barrier_init();
+    }
+    __syncthreads();
+    auto issue = [&](int j) {  // j-th tile in reverse order
+        const int tt = n_tiles - 1 - j;
+        const int s = j % S;
+        IO* dst = R.data + (size_t)s * 4 * RC * LW;
+        const int r = row0 + tt * RC;
+        tma::mbar_arrive_expect_tx(&R.full[s], kStageBytes);
+        tma::load_2d(dst, &mu, w0, r, &R.full[s]);
+        tma::load_2d(dst + RC * LW, &mr, w0, r, &R.full[s]);
+        tma::load_2d(dst + 2 * RC * LW, &mi, w0, r, &R.full[s]);
+        tma::load_2d(dst + 3 * RC * LW, &mg, w0, r, &R.full[s]);
+    };
+    if (tid == 0)
+        for (int j = 0; j < S && j < n_tiles; ++j) issue(j);
+
+    C la = 0, br = 0, bi = 0;
+    if (valid) {
+        la = -Math<C>::softplus(-lam[w]);
+        br = b_r[w];
+        bi = b_i[w];
+    }
+    C h = 0;
+    Kahan<C> sla, sbr, sbi;
+    IO *pgu = gu + (int64_t)row0 * W + w, *pgr = gqr + (int64_t)row0 * W + w, *pgi = gqi + (int64_t)row0 * W + w;
+    const int64_t ck_stride = (int64_t)Bn * W;
+    const C* pc = ckpt + (int64_t)b * W + (valid ? w : 0);
+    C xnext = valid ? __ldcg(pc + (int64_t)(n_tiles - 1) * ck_stride) : C(0);
+    for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % S;
+        const uint32_t ph = (j / S) & 1;
+        const int tt = n_tiles - 1 - j;
+        const C xin = xnext;  // state entering this chunk
+        if (valid && tt > 0) xnext = __ldcg(pc + (int64_t)(tt - 1) * ck_stride);  // prefetch the next chunk's
+        tma::mbar_wait(&R.full[s], ph);
+        const IO* src = R.data + (size_t)s * 4 * RC * LW + tid;
+        const int64_t t0 = (int64_t)tt * RC;
+        const int nk = (int)min((int64_t)RC, L - t0);
+        // forward recompute: xs[k] = x_{k-1}
+        C xs[RC];
+        C x = xin;
+#pragma unroll
+        for (int k = 0; k < RC; ++k) {
+            xs[k] = x;
+            if (k < nk) {
+                const Coef<C> q = gates<C>(src[k * LW], src[(RC + k) * LW], src[(2 * RC + k) * LW], la, br, bi);
+                x = q.a * x + (q.s * q.i) * q.u;
+            }
+        }
+        C tla = 0, tbr = 0, tbi = 0;
+        const int64_t o0 = t0 * W;
+#pragma unroll
+        for (int k = RC - 1; k >= 0; --k) {
+            if (k < nk) {
+                const Coef<C> q = gates<C>(src[k * LW], src[(RC + k) * LW], src[(2 * RC + k) * LW], la, br, bi);
+                const C g = C(cvt(src[(3 * RC + k) * LW])) + h;
+                h = q.a * g;
+                const BwdOut<C> o = bwd_step<C>(q, g, xs[k], la);
+                if (valid) {
+                    const int64_t off = o0 + (int64_t)k * W;
+                    st_io(pgu + off, o.gu);
+                    st_io(pgr + off, o.gqr);
+                    st_io(pgi + off, o.gqi);
+                }
+                tla += o.la_term;
+                tbr += o.gqr;
+                tbi += o.gqi;
+            }
+        }
+        sla.add(tla);
+        sbr.add(tbr);
+        sbi.add(tbi);
+        __syncwarp();
+        if ((tid & 31) == 0) tma::mbar_arrive(&R.empty[s]);
+        if (tid == 0 && j + S < n_tiles) {
+            tma::mbar_wait(&R.empty[s], ph);
+            issue(j + S);
+        }
+    }
+    if (valid) {
+        const int64_t p = (int64_t)b * W + w;
+        gla_part[p] = sla.s;
+        gbr_part[p] = sbr.s;
+        gbi_part[p] = sbi.s;
+    }
+}
+
 // ==================================================================== stream
 template <typename IO, typename C, int PF>
 __global__ void __launch_bounds__(kThreads) fwd_stream_kernel(
@@ -569,7 +690,7 @@ static int mode_env() {
     static int m = -1;
     if (m < 0) {
         const char* e = getenv("LRX_RGLRU_MODE");
-        m = !e ? 0 : !strcmp(e, "tma") ? 1 : !strcmp(e, "stream") ? 2 : !strcmp(e, "lookback") ? 3 : 0;
+        m = !e ? 0 : !strcmp(e, "tma") ? 1 : !strcmp(e, "stream") ? 2 : !strcmp(e, "lookback") ? 3 : !strcmp(e, "rc") ? 4 : 0;
     }
     return m;
 }
@@ -675,6 +796,25 @@ static int launch_bwd_tma(const TmaPlan& pl, const CUtensorMap* m, const void* l
     return launched("lrx_rglru_bwd/tma");
 }
 
+template <typename IO, typename C, int LW>
+static int launch_bwd_rc(const CUtensorMap* m, const void* lam, const void* br, const void* bi, const void* ckpt,
+                         void* gu, void* gqr, void* gqi, C* parts, int64_t B, int64_t L, int64_t W, int S,
+                         cudaStream_t st) {
+    constexpr int RC = Tile<IO>::T;
+    auto k = bwd_rc_kernel<IO, C, LW, RC>;
+    const size_t smem = 128 * ((2 * S * 8 + 127) / 128) + (size_t)S * 4 * RC * LW * sizeof(IO);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        set_error("rglru bwd: cannot reserve %zu B of shared memory", smem);
+        return LRX_ERR_CUDA;
+    }
+    const int n_wblk = (int)cdiv(W, LW);
+    const int64_t n = B * W;
+    k<<<(unsigned)(B * n_wblk), LW, smem, st>>>(m[0], m[1], m[2], m[3], (const C*)lam, (const C*)br, (const C*)bi,
+                                                (const C*)ckpt, (IO*)gu, (IO*)gqr, (IO*)gqi, parts, parts + n,
+                                                parts + 2 * n, L, W, n_wblk, (int)B, S);
+    return launched("lrx_rglru_bwd/rc");
+}
+
 constexpr int kPfF = 4;  // forward TMA tile rows
 constexpr int kPfB = 4;  // backward TMA tile rows
 
@@ -732,6 +872,29 @@ static int bwd_t(const void* u, const void* qr, const void* qi, const void* lam,
     const int mode = mode_env();
     const int64_t n = B * W;
     TmaPlan pl;
+    // recompute variant (LRX_RGLRU_MODE=rc): 7 array passes, no y stream.
+    // Measured slower on C4 (18.3 vs 16.4 ms: the 2 x gates per element at
+    // ~14 warps/SM, limited by the 512 B of staged rows per thread), so the
+    // y-streaming kernel stays the default.
+    if (ckpt && sizeof(IO) == 4 && mode == 4 && B * L < (1ll << 31) && (W * 4) % 16 == 0) {
+        constexpr int RC = Tile<IO>::T;
+        const int LW = B * cdiv(W, 64) >= 4 * sm_count() ? 64 : 32;
+        CUtensorMap m[4];
+        const void* src[4] = {u, qr, qi, gy};
+        bool ok = true;
+        for (int i = 0; i < 4; ++i) ok &= tma::encode_2d(&m[i], src[i], sizeof(IO), B * L, W, RC, LW);
+        if (ok) {
+            Carver cv(w);
+            C* parts = cv.take<C>((size_t)3 * n);
+            LRX_REQUIRE(w && cv.off <= wb, LRX_ERR_VALUE, "rglru workspace too small");
+            const int S = 2;
+            const int rc = LW == 64 ? launch_bwd_rc<IO, C, 64>(m, lam, br, bi, ckpt, gu, gqr, gqi, parts, B, L, W, S, st)
+                                    : launch_bwd_rc<IO, C, 32>(m, lam, br, bi, ckpt, gu, gqr, gqi, parts, B, L, W, S, st);
+            if (rc) return rc;
+            return colsums<IO, C>(parts, 1, B, W, gla, gbr, gbi, st);
+        }
+        LRX_REQUIRE(mode != 4, LRX_ERR_UNSUPPORTED, "rglru: TMA descriptors unavailable");
+    }
     // y (= the state) is exact only at fp32/f64 I/O; bf16 recomputes instead
     if (y && sizeof(IO) != 2 && (mode == 0 || mode == 1) && B * L < (1ll << 31) &&
         tma_plan<IO>(B, W, 5, kPfB, &pl)) {
