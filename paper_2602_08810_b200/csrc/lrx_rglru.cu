@@ -686,13 +686,9 @@ __global__ void colsum_kernel(const C* __restrict__ in, C* __restrict__ out, int
 }
 
 // ====================================================================== host
-static int mode_env() {
-    static int m = -1;
-    if (m < 0) {
-        const char* e = getenv("LRX_RGLRU_MODE");
-        m = !e ? 0 : !strcmp(e, "tma") ? 1 : !strcmp(e, "stream") ? 2 : !strcmp(e, "lookback") ? 3 : !strcmp(e, "rc") ? 4 : 0;
-    }
-    return m;
+static int mode_env() {  // read per call so tests can switch kernels in-process
+    const char* e = getenv("LRX_RGLRU_MODE");
+    return !e ? 0 : !strcmp(e, "tma") ? 1 : !strcmp(e, "stream") ? 2 : !strcmp(e, "lookback") ? 3 : !strcmp(e, "rc") ? 4 : 0;
 }
 
 static int sm_count() {

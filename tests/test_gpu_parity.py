@@ -407,3 +407,21 @@ def test_mimo_layer_on_tensor_cores_matches_oracle(lrx, kind):
     assert rel(g.u, rgu) < TOL["f32"]
     for k in rg:
         assert rel(g.params[k], rg[k]) < TOL["f32"], (k, rel(g.params[k], rg[k]))
+
+
+@pytest.mark.parametrize("mode", ["tma", "stream", "lookback", "rc"])
+def test_rglru_kernel_variants_match_oracle(lrx, monkeypatch, mode):
+    """Every RG-LRU kernel family (LRX_RGLRU_MODE) gives the oracle's answer."""
+    monkeypatch.setenv("LRX_RGLRU_MODE", mode)
+    m, B, L = 96, 3, 777
+    layer = lrx.make_layer("rglru", m, dtype="f32", seed=29)
+    u = port.Rng(13).normal((B, L, m)).astype(np.float32)
+    gy = port.Rng(14).normal((B, L, m)).astype(np.float32)
+    y, tape = layer.forward(u, tape=True)
+    g = lrx.layer_backward(layer, tape, gy)
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64("rglru", None, params, u, gy)
+    assert rel(y, ry) < TOL["f32"]
+    assert rel(g.u, rgu) < TOL["f32"]
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < TOL["f32"], (mode, k)
