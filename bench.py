@@ -376,7 +376,7 @@ def run_gpu(args, w, rank, world, device):
 def run_e2e(args, w, prob, device):
     """Same step through the public API with HOST (pinned) buffers: H2D of the
     step's inputs, the operator fwd+bwd, D2H of every output, all timed.  The
-    batch slice is processed in sub-batches on two CUDA streams so the PCIe
+    batch slice is processed in sub-batches on their own CUDA streams so the PCIe
     copies of one sub-batch overlap the kernels of the next (the host buffers
     are allocated and pinned once, outside the timed region)."""
     import torch
@@ -395,7 +395,10 @@ def run_e2e(args, w, prob, device):
     host = {n: prob[n][:Bs].cpu().pin_memory() for n in names}
     layer = prob["layer"]
     h2d = sum(t.numel() * t.element_size() for t in host.values())
-    n_sub = 2 if Bs % 2 == 0 and kind in ("rglru", "s6") else 1
+    # sub-batches pipeline the PCIe copies: H2D of sub-batch i+1 and D2H of i
+    # run on the two copy engines while i computes; the step approaches
+    # max(H2D, D2H) + one sub-batch's share
+    n_sub = next((k for k in (8, 4, 2) if Bs % k == 0), 1) if kind in ("rglru", "s6") else 1
     sb = Bs // n_sub
     streams = [torch.cuda.Stream(device) for _ in range(n_sub)]
 
