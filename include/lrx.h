@@ -171,6 +171,34 @@ int lrx_s6_bwd_carry(int io_dtype, const void* gy, const void* pre, const void* 
                      void* ws, int64_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ *
+ * Single-step (decode) updates on a device-resident state, one token per
+ * sequence (Layer.step, layers.py:251-269; per kind S4D 578-613, S5/LRU
+ * 748-783, S6 1145-1168, RG-LRU 1310-1336).  x is updated in place, y is
+ * written; nothing is allocated.
+ * ------------------------------------------------------------------------ */
+/* Operator-level step (scan.py:232-250): x[n] <- a x + b, with a / b of
+ * period a_period / b_period (n = full, 1 = scalar, p = trailing lanes). */
+int lrx_scan_step(int dtype, void* x, const void* a, const void* b, int64_t n, int64_t a_period, int64_t b_period,
+                  void* stream);
+/* S4D: x[B,H,N] = abar[H,N] x + w[H,N] u[B,H]; y[B,H] = Re(sum_n c x) + d u.
+ * dtype C64 / C128 (x, abar, w, c complex; d, u, y the matching real type). */
+int lrx_s4d_step(int dtype, void* x, const void* abar, const void* w, const void* c, const void* d, const void* u,
+                 void* y, int64_t B, int64_t H, int64_t N, void* stream);
+/* S5 / LRU: x[B,P] = abar[P] x + scale[P] (B u); y[B,H] = out_scale Re(C x) + D u
+ * with B = Bre + i Bim [P,H], C = Cre + i Cim [H,P] real planes. */
+int lrx_mimo_step(int dtype, void* x, const void* abar, const void* scale, const void* Bre, const void* Bim,
+                  const void* Cre, const void* Cim, const void* D, const void* u, void* y, double out_scale,
+                  int64_t B, int64_t P, int64_t H, void* stream);
+/* S6: x[B,D,N] compute precision; u, y io dtype; pre [B,D] = the delta
+ * projection (bias not added), Bk, Ck [B,N] compute precision. */
+int lrx_s6_step(int io_dtype, void* x, const void* u, const void* pre, const void* Bk, const void* Ck,
+                const void* b_delta, const void* a_log, const void* Dskip, void* y, int64_t B, int64_t D, int64_t N,
+                void* stream);
+/* RG-LRU: x[B,W] compute precision; u, qr, qi, y io dtype. */
+int lrx_rglru_step(int io_dtype, void* x, const void* u, const void* qr, const void* qi, const void* lambda_param,
+                   const void* b_r, const void* b_i, void* y, int64_t B, int64_t W, void* stream);
+
+/* ------------------------------------------------------------------------ *
  * fp32 GEMM on the tcgen05 tensor cores with the 3xTF32 split (the dense
  * projections of S5 / LRU, layers.py:650-704):
  *   C[M,N] = alpha A[M,K] Bt[N,K]^T + (colscale ? colscale[n] : beta) Cin[M,N]

@@ -7,7 +7,8 @@ mirror of the reference interface.  There is no CPU fallback.
 from .numerics import REAL_DTYPES, Rng, ShapeError, complex_dtype, real_dtype, sigmoid, softplus
 from .discretize import (NonMonotoneTimestamps, SingularBilinear, deltas_from_timestamps, discretize,
                          discretize_bilinear, discretize_dirac, discretize_zoh, scheme_factors)
-from .scan import MIN_CHUNK_LEN, combine, identity_element, plan_chunks, scan_parallel, scan_sequential
+from .scan import (MIN_CHUNK_LEN, StepState, combine, identity_element, init_step_state, plan_chunks, scan_parallel,
+                   scan_sequential, step)
 from .autograd import (FiniteDiffReport, GradBundle, RecomputeTape, Tape, TapeConsumed, check_layer_gradients,
                        finite_diff_check, layer_backward, scan_backward, scan_forward, scheme_partials)
 from .layers import (LAYER_KINDS, LRU, RGLRU, S4D, S5, S6, SCHEMES_BY_KIND, LayerConfig, LayerStepState,

@@ -51,6 +51,12 @@ SIGNATURES = {
     "lrx_reduce_rows": (_i, [_i, _vp, _vp, _i64, _i64, _vp]),
     "lrx_reduce_rows_ws_bytes": (_sz, [_i, _i64, _i64]),
     "lrx_reduce_rows_ws": (_i, [_i, _vp, _vp, _vp, _i64, _i64, _vp, _sz, _vp]),
+    "lrx_scan_step": (_i, [_i, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "lrx_s4d_step": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "lrx_mimo_step": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_double, _i64, _i64,
+                           _i64, _vp]),
+    "lrx_s6_step": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "lrx_rglru_step": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp]),
     "lrx_gemm_f32": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_float, ctypes.c_float, _vp]),
     "lrx_gemm_f32_tn_splits": (_i, [_i64, _i64, _i64, _P64]),
     "lrx_gemm_f32_tn": (_i, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_float, _vp]),

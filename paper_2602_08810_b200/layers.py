@@ -61,14 +61,18 @@ class LayerConfig:
 
 
 class LayerStepState:
-    """Carry returned by forward(return_state=True): the state after the last
-    step (x, on the device) and the step count k."""
+    """Step-mode carry (layers.py:96-107): the device-resident state x, the
+    step count k and the coefficient cache snapshotted from the layer's
+    parameters when the state was created (init_state / forward with
+    return_state=True).  step() updates x in place and allocates nothing but
+    its output."""
 
     def __init__(self, kind: str, batch: int):
         self.kind = kind
         self.batch = batch
         self.k = 0
         self.x = None
+        self.coef = {}
 
 
 def _device(device=None):
@@ -166,7 +170,7 @@ class LinearRecurrence:
             out.append(Tape(self.kind, **saved))
         if return_state:
             st = self.init_state(B)
-            st.x = xf
+            st.x = xf.contiguous().clone()  # step() updates it in place; the tape keeps its own copy
             st.k = L
             out.append(st)
         return tuple(out)
@@ -175,12 +179,45 @@ class LinearRecurrence:
         return layer_backward(self, tape, grad_y)
 
     def init_state(self, batch: int = 1) -> LayerStepState:
-        return LayerStepState(self.kind, batch)
+        """A zeroed step-mode state for `batch` sequences (layers.py:271-273)."""
+        if batch < 1:
+            raise ValueError(f"batch must be >= 1, got {batch}")
+        st = LayerStepState(self.kind, batch)
+        st.x = self._zero_state(batch)
+        st.coef = self._step_coef()
+        return st
 
     def step(self, state, u_k, delta_k=None):
-        raise NotImplementedError(
-            "single-step decode is outside the device scan hot path (SURVEY section 8(f), rank 3); "
-            "use forward() over the sequence")
+        """One recurrence update on the device state (layers.py:251-269):
+        u_k [batch, d_model] (or [d_model] for a batch-1 state); returns
+        (y_k, state).  numpy in -> numpy out, CUDA tensor in -> CUDA tensor out."""
+        if self.device.type != "cuda":
+            raise RuntimeError(f"{self.kind} layer lives on {self.device}; step runs on CUDA only")
+        host = not isinstance(u_k, torch.Tensor)
+        shape = tuple(np.shape(u_k)) if host else tuple(u_k.shape)
+        squeeze = len(shape) == 1
+        if squeeze:
+            shape = (1,) + shape
+        if shape != (state.batch, self.d_model):
+            raise ShapeError(f"u_k shape {tuple(np.shape(u_k))} does not match state batch {state.batch} x "
+                             f"d_model {self.d_model}")
+        if delta_k is not None and not (self.continuous and self.lti):
+            raise ValueError(f"{self.kind} does not accept per-step deltas")
+        if host:
+            uk = torch.as_tensor(np.ascontiguousarray(np.asarray(u_k, dtype=self.rdt)).reshape(shape))
+        else:
+            uk = u_k.reshape(shape)
+        uk = uk.to(self.device, self.io_dtype).contiguous()
+        y = self._step(state, uk, delta_k)
+        state.k += 1
+        out = y.cpu().numpy() if host else y
+        return (out[0] if squeeze else out), state
+
+    def _zero_state(self, batch):
+        raise NotImplementedError
+
+    def _step_coef(self):
+        return {}
 
     # -- plumbing --------------------------------------------------------------
     def _check_u(self, u):
@@ -296,6 +333,30 @@ class S4D(LinearRecurrence):
         saved = {"u": u, "x2": x2, "deltas": deltas} if keep else {}
         return y.contiguous(), saved, xt[-1]
 
+    # -- step mode (layers.py:550-613) ----------------------------------------
+    def _zero_state(self, batch):
+        return torch.zeros((batch, self.d_model, self.d_state), dtype=self.tcdt, device=self.device)
+
+    def _step_coef(self):
+        lam, delta, b, abar, scale = self._coeffs(None)
+        return {"lam": lam, "delta": delta, "b": b, "abar": abar.to(self.tcdt).contiguous(),
+                "w": (scale * b).to(self.tcdt).contiguous(),
+                "c": torch.complex(self.c_re, self.c_im).contiguous(), "d": self.d.contiguous()}
+
+    def _step(self, st, uk, delta_k):
+        cf = st.coef
+        abar, w = cf["abar"], cf["w"]
+        if delta_k is not None:
+            if self.discretization != "dirac":
+                raise NotImplementedError("per-step deltas in step mode require the dirac scheme")
+            a_k, s_k = scheme_factors("dirac", cf["lam"], cf["delta"][:, None] * float(delta_k))
+            abar, w = a_k.to(self.tcdt).contiguous(), (s_k * cf["b"]).to(self.tcdt).contiguous()
+        y = torch.empty((st.batch, self.d_model), dtype=self.tdt, device=self.device)
+        _lib.check(_lib.lib().lrx_s4d_step(_lib.code_of(self.tcdt), _lib.ptr(st.x), _lib.ptr(abar), _lib.ptr(w),
+                                           _lib.ptr(cf["c"]), _lib.ptr(cf["d"]), _lib.ptr(uk), _lib.ptr(y),
+                                           st.batch, self.d_model, self.d_state, _lib.stream()))
+        return y
+
     def _backward(self, s, gy):
         u, x2, deltas, host = s["u"], s["x2"], s["deltas"], s["host"]
         B, L, m = u.shape
@@ -404,6 +465,32 @@ class _MIMOBase(LinearRecurrence):
                             alpha=self.OUT_SCALE).reshape(B, L, m)
         saved = {"u": u, "x": x, "bu": bu, "deltas": deltas} if keep else {}
         return y, saved, x[:, -1]
+
+    # -- step mode (layers.py:708-783) ----------------------------------------
+    def _zero_state(self, batch):
+        return torch.zeros((batch, self._P), dtype=self.tcdt, device=self.device)
+
+    def _step_coef(self):
+        abar, scale, extra = self._abar_scale(None)
+        return {"abar": abar.contiguous(), "scale": scale.contiguous(), "extra": extra,
+                "B": (self.B_re.contiguous(), self.B_im.contiguous()),
+                "C": (self.C_re.contiguous(), self.C_im.contiguous()), "D": self.D.contiguous()}
+
+    def _step(self, st, uk, delta_k):
+        cf = st.coef
+        abar, scale = cf["abar"], cf["scale"]
+        if delta_k is not None:
+            if self.discretization != "dirac":
+                raise NotImplementedError("per-step deltas in step mode require the dirac scheme")
+            ex = cf["extra"]
+            a_k, s_k = scheme_factors("dirac", ex["lam"], ex["delta"] * float(delta_k))
+            abar, scale = a_k.to(self.tcdt).contiguous(), s_k.to(self.tcdt).contiguous()
+        y = torch.empty((st.batch, self.d_model), dtype=self.tdt, device=self.device)
+        _lib.check(_lib.lib().lrx_mimo_step(
+            _lib.code_of(self.tcdt), _lib.ptr(st.x), _lib.ptr(abar), _lib.ptr(scale), _lib.ptr(cf["B"][0]),
+            _lib.ptr(cf["B"][1]), _lib.ptr(cf["C"][0]), _lib.ptr(cf["C"][1]), _lib.ptr(cf["D"]), _lib.ptr(uk),
+            _lib.ptr(y), float(self.OUT_SCALE), st.batch, self._P, self.d_model, _lib.stream()))
+        return y
 
     def _scan_backward(self, x, bu, gx, abar, scale, deltas):
         """(gbu [B,L,P], gabar or ga_k, gscale or gscale_k)."""
@@ -596,6 +683,22 @@ class S6(LinearRecurrence):
         saved = {"u": u, "p1": p1, "pre": pre, "Bk": Bk, "Ck": Ck, "ckpt": ckpt} if keep else {}
         return y, saved, ckpt[:, -1]
 
+    # -- step mode (layers.py:1120-1168) --------------------------------------
+    def _zero_state(self, batch):
+        return torch.zeros((batch, self.d_model, self.d_state), dtype=self.tdt, device=self.device)
+
+    def _step(self, st, uk, delta_k):
+        p1 = _mm(uk, self.W_delta)
+        pre = (p1 @ self.W_delta_proj).contiguous()
+        Bk = _mm(uk, self.W_B.T).contiguous()
+        Ck = _mm(uk, self.W_C.T).contiguous()
+        y = torch.empty((st.batch, self.d_model), dtype=self.io_dtype, device=self.device)
+        _lib.check(_lib.lib().lrx_s6_step(
+            _lib.code_of(self.io_dtype), _lib.ptr(st.x), _lib.ptr(uk), _lib.ptr(pre), _lib.ptr(Bk), _lib.ptr(Ck),
+            _lib.ptr(self.b_delta), _lib.ptr(self.a_log), _lib.ptr(self.D), _lib.ptr(y), st.batch, self.d_model,
+            self.d_state, _lib.stream()))
+        return y
+
     def _backward(self, s, gy):
         u, p1, pre, Bk, Ck, ckpt, host = (s[k] for k in ("u", "p1", "pre", "Bk", "Ck", "ckpt", "host"))
         B, L, m = u.shape
@@ -654,6 +757,20 @@ class RGLRU(LinearRecurrence):
         y, ckpt = ops.rglru_scan_fwd(u, qr, qi, self.lambda_param, self.b_r, self.b_i)
         saved = {"u": u, "qr": qr, "qi": qi, "ckpt": ckpt, "y": y} if keep else {}
         return y, saved, y[:, -1].to(self.tdt)
+
+    # -- step mode (layers.py:1293-1336) --------------------------------------
+    def _zero_state(self, batch):
+        return torch.zeros((batch, self.d_model), dtype=self.tdt, device=self.device)
+
+    def _step(self, st, uk, delta_k):
+        qr = (uk @ self._w(self.W_r).T).contiguous()
+        qi = (uk @ self._w(self.W_i).T).contiguous()
+        y = torch.empty((st.batch, self.d_model), dtype=self.io_dtype, device=self.device)
+        _lib.check(_lib.lib().lrx_rglru_step(
+            _lib.code_of(self.io_dtype), _lib.ptr(st.x), _lib.ptr(uk), _lib.ptr(qr), _lib.ptr(qi),
+            _lib.ptr(self.lambda_param), _lib.ptr(self.b_r), _lib.ptr(self.b_i), _lib.ptr(y), st.batch,
+            self.d_model, _lib.stream()))
+        return y
 
     def _backward(self, s, gy):
         u, qr, qi, ckpt, host = s["u"], s["qr"], s["qi"], s["ckpt"], s["host"]

@@ -20,7 +20,7 @@ from . import _lib
 from .numerics import ShapeError
 
 __all__ = ["MIN_CHUNK_LEN", "combine", "identity_element", "plan_chunks", "scan_sequential", "scan_parallel",
-           "prepare"]
+           "prepare", "StepState", "init_step_state", "step"]
 
 MIN_CHUNK_LEN = 256  # scan.py:44 (host planning helper kept for API parity)
 
@@ -131,3 +131,72 @@ def scan_parallel(a, b, x0=None, workers: int = 1):
     if workers < 1:
         raise ValueError(f"workers must be >= 1, got {workers}")
     return scan_sequential(a, b, x0)
+
+
+# ---------------------------------------------------------------------------
+# single-step mode (scan.py:209-250)
+
+class StepState:
+    """Mutable carry for step(): the current state x (device tensor, updated in
+    place) and the step count k (scan.py:209-216)."""
+
+    def __init__(self, x, k=0):
+        self.x = x
+        self.k = k
+
+
+def init_step_state(lanes, dtype=np.complex128, x0=None) -> StepState:
+    """Fresh state of lane shape `lanes` (from x0 if given, else zeros) on the
+    current CUDA device (scan.py:219-229)."""
+    lanes = (lanes,) if np.isscalar(lanes) else tuple(lanes)
+    td = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+          np.dtype(np.complex64): torch.complex64, np.dtype(np.complex128): torch.complex128}.get(np.dtype(dtype))
+    if td is None:
+        raise ValueError(f"unsupported state dtype {dtype}")
+    x = torch.zeros(lanes, dtype=td, device=_dev())
+    if x0 is not None:
+        x0t = _as_dev(x0)[0]
+        if tuple(x0t.shape) != lanes:
+            raise ShapeError(f"x0 shape {tuple(x0t.shape)} != state shape {lanes}")
+        x.copy_(x0t.to(td))
+    return StepState(x=x, k=0)
+
+
+def _period(t, shape):
+    """Period of `t` when broadcast to `shape` in flat order, or None when it is
+    not a plain trailing-dims broadcast (then it is materialised)."""
+    if t.numel() == 1:
+        return 1
+    ts = tuple(t.shape)
+    while ts and ts[0] == 1:  # leading singleton dims do not change the flat pattern
+        ts = ts[1:]
+    if ts == tuple(shape[len(shape) - len(ts):]):
+        return t.numel()
+    return None
+
+
+def step(state: StepState, a_k, b_k):
+    """Advance one step in place, x <- a_k x + b_k, on the device; returns
+    (x, state).  a_k / b_k must broadcast to the state's shape without
+    enlarging it (scan.py:232-250)."""
+    x = state.x
+    a = _as_dev(a_k)[0].to(x.dtype)
+    b = _as_dev(b_k)[0].to(x.dtype)
+    try:
+        if torch.broadcast_shapes(x.shape, a.shape, b.shape) != x.shape:
+            raise ShapeError(f"step operands {tuple(a.shape)}/{tuple(b.shape)} would enlarge state "
+                             f"{tuple(x.shape)}")
+    except RuntimeError as exc:
+        raise ShapeError(str(exc)) from None
+    shape = tuple(x.shape)
+    ops = []
+    for t in (a, b):
+        p = _period(t, shape)
+        if p is None:  # non-trailing broadcast (rare): materialise once
+            t, p = torch.broadcast_to(t, shape).contiguous(), x.numel()
+        ops.append((t.contiguous(), p))
+    (a2, pa), (b2, pb) = ops
+    _lib.check(_lib.lib().lrx_scan_step(_lib.code_of(x.dtype), _lib.ptr(x), _lib.ptr(a2), _lib.ptr(b2), x.numel(),
+                                        pa, pb, _lib.stream()))
+    state.k += 1
+    return x, state

@@ -425,3 +425,103 @@ def test_rglru_kernel_variants_match_oracle(lrx, monkeypatch, mode):
     assert rel(g.u, rgu) < TOL["f32"]
     for k in rg:
         assert rel(g.params[k], rg[k]) < TOL["f32"], (mode, k)
+
+
+# ---- step mode (decode), reference test_layers.py:277-315 -------------------
+
+STEP_KINDS = [("s4d", 4), ("s5", 8), ("lru", 4), ("s6", 4), ("rglru", None)]
+
+
+@pytest.mark.parametrize("kind,n", STEP_KINDS)
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_step_matches_forward(lrx, kind, n, dtype):
+    m, B, L = 6, 2, 40
+    layer = lrx.make_layer(kind, m, n, dtype=dtype, seed=41)
+    u = port.Rng(42).normal((B, L, m)).astype(layer.rdt)
+    ref = layer.forward(u)
+    st = layer.init_state(B)
+    tol = 1e-10 if dtype == "f64" else 1e-4
+    for k in range(L):
+        yk, st = layer.step(st, u[:, k])
+        assert isinstance(yk, np.ndarray) and yk.shape == (B, m)
+        assert rel(yk, ref[:, k]) < tol, (k, rel(yk, ref[:, k]))
+    assert st.k == L
+    # prefill half with forward(return_state=True), decode the rest
+    _, st2 = layer.forward(u[:, :L // 2], return_state=True)
+    assert st2.k == L // 2
+    for k in range(L // 2, L):
+        yk, st2 = layer.step(st2, u[:, k])
+        assert rel(yk, ref[:, k]) < tol
+
+
+@pytest.mark.parametrize("kind", ["s6", "rglru"])
+def test_step_bf16_and_device_tensors(lrx, kind):
+    m, B, L = 64, 2, 50
+    layer = lrx.make_layer(kind, m, 16 if kind == "s6" else None, dtype="bf16", seed=43)
+    u = torch.from_numpy(port.Rng(44).normal((B, L, m))).to("cuda", torch.bfloat16)
+    ref = layer.forward(u).float()
+    st = layer.init_state(B)
+    for k in range(L):
+        yk, st = layer.step(st, u[:, k])
+        assert yk.is_cuda and yk.dtype == torch.bfloat16
+        assert rel(yk, ref[:, k].cpu().numpy()) < 1e-2
+
+
+def test_step_api_contract(lrx):  # reference test_layers.py:277-303
+    layer = lrx.make_layer("lru", 2, d_state=4, seed=1)
+    u = port.Rng(2).normal((1, 10, 2))
+    ref = layer.forward(u)
+    s1, s2 = layer.init_state(1), layer.init_state(1)
+    for k in range(10):
+        y1, s1 = layer.step(s1, u[:, k])
+        layer.step(s2, port.Rng(k).normal((1, 2)))  # unrelated traffic
+        np.testing.assert_allclose(y1, ref[:, k], atol=1e-12)
+    assert s1.k == 10
+    rg = lrx.make_layer("rglru", 3, seed=4)
+    st = rg.init_state(1)
+    y, st = rg.step(st, np.zeros(3))
+    assert y.shape == (3,)
+    with pytest.raises(lrx.ShapeError):
+        rg.step(st, np.zeros((2, 3)))
+    with pytest.raises(ValueError):
+        rg.step(st, np.zeros(3), delta_k=0.5)
+    s4 = lrx.make_layer("s4d", 2, d_state=2, discretization="zoh")
+    with pytest.raises(NotImplementedError):
+        s4.step(s4.init_state(1), np.zeros((1, 2)), delta_k=0.5)
+    y, st = lrx.layer_step(rg, rg.init_state(1), np.zeros((1, 3)))
+    assert y.shape == (1, 3)
+
+
+@pytest.mark.parametrize("kind", ["s4d", "s5"])
+def test_async_step_matches_batched_forward(lrx, kind):  # reference test_layers.py:305-315
+    layer = lrx.make_layer(kind, 2, d_state=4, asynchronous=True, seed=6)
+    u = port.Rng(7).normal((1, 12, 2))
+    deltas = port.Rng(8).uniform(0.2, 2.0, 12)
+    ref = layer.forward(u, deltas=deltas)
+    st = layer.init_state(1)
+    for k in range(12):
+        yk, st = layer.step(st, u[:, k], delta_k=deltas[k])
+        np.testing.assert_allclose(yk, ref[:, k], atol=1e-12)
+
+
+def test_scan_step_operator(lrx):  # reference test_scan.py:133-146
+    rng = port.Rng(5)
+    a = 0.9 * np.exp(1j * rng.normal(5))
+    bs = rng.normal((7, 5)) + 1j * rng.normal((7, 5))
+    ref = port.scan_sequential(a, bs, None)
+    st = lrx.init_step_state((5,), np.complex128)
+    for k in range(7):
+        xk, st = lrx.step(st, a, bs[k])
+        np.testing.assert_allclose(xk.cpu().numpy(), ref[k], atol=1e-12)
+    assert st.k == 7
+    st = lrx.init_step_state((4,), np.float64)
+    with pytest.raises(lrx.ShapeError):
+        lrx.step(st, np.ones(3), np.ones(3))
+    # lane-periodic, scalar and leading-singleton operands against numpy broadcasting
+    st = lrx.init_step_state((3, 4), np.float32, x0=np.arange(12, dtype=np.float32).reshape(3, 4))
+    x = np.arange(12, dtype=np.float64).reshape(3, 4)
+    for a_k, b_k in ((np.full(4, 0.5), np.float64(2.0)), (np.float64(0.25), np.ones((1, 4))),
+                     (np.full((3, 1), 0.5), np.ones((3, 4)))):
+        xk, st = lrx.step(st, a_k, b_k)
+        x = a_k * x + b_k
+        np.testing.assert_allclose(xk.cpu().numpy(), x, rtol=1e-6)
