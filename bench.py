@@ -310,6 +310,32 @@ def run_gpu(args, w, rank, world, device):
         bwd(ctx)
     torch.cuda.synchronize()
 
+    # CUDA graphs: the step's kernels are captured once (after the warm-up) and
+    # replayed, so the timed steps are not bounded by host launch overhead
+    # (LRU C1 is ~70 launches of a few us each).  Every kernel of fwd + bwd
+    # still runs every step on the same inputs; collectives (sequence-parallel
+    # carries over NCCL) stay eager.
+    graphed = False
+    launches_per_step = None
+    if args.graphs and not (world > 1 and w.get("seqpar")):
+        try:
+            n_c = _lib.launch_count()
+            g_f, g_b = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_f):
+                gctx = fwd()
+            with torch.cuda.graph(g_b):
+                gout = bwd(gctx)
+            launches_per_step = _lib.launch_count() - n_c
+            for _ in range(2):
+                g_f.replay()
+                g_b.replay()
+            torch.cuda.synchronize()
+            fwd, bwd = (lambda: g_f.replay()), (lambda c: g_b.replay())
+            graphed = True
+        except Exception as exc:  # capture unsupported for this path: stay eager
+            print(f"[bench] CUDA graph capture failed ({type(exc).__name__}: {exc}); eager steps", file=sys.stderr)
+            torch.cuda.synchronize()
+
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     n0 = _lib.launch_count()
     with Clocks(device.index) as clocks:
@@ -328,6 +354,8 @@ def run_gpu(args, w, rank, world, device):
         torch.cuda.synchronize()
         barrier()
     launches = _lib.launch_count() - n0
+    if graphed:  # replays do not pass through the host launch counter
+        launches = launches_per_step * args.steps
     if os.environ.get("LRX_BENCH_VERBOSE"):
         for k, e in enumerate(ev):
             print(f"step {k}: fwd {e[0].elapsed_time(e[1]):.3f} ms, bwd {e[1].elapsed_time(e[2]):.3f} ms",
@@ -344,7 +372,7 @@ def run_gpu(args, w, rank, world, device):
 
     # dominant kernel alone, CUDA events on the launching stream, after the timed region
     pr = prob["probe"]
-    ctx = fwd()
+    ctx = prob["fwd"]()  # eager (the probe launches the kernel itself)
     for _ in range(2):
         pr["fn"](ctx)
     torch.cuda.synchronize()
@@ -368,7 +396,8 @@ def run_gpu(args, w, rank, world, device):
         te = torch.tensor([e2e["ms"]], device=device, dtype=torch.float64)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e["ms"] = float(te.item())
-    return {"ms": ms, "ms_fwd": ms_fwd, "ms_bwd": ms_bwd, "launches": launches, "clocks": clocks.summary(),
+    return {"ms": ms, "ms_fwd": ms_fwd, "ms_bwd": ms_bwd, "launches": launches, "graphed": graphed,
+            "clocks": clocks.summary(),
             "bytes": prob["bytes"], "B_rank": B, "e2e": e2e, "probe": {k: v for k, v in pr.items() if k != "fn"},
             "probe_ms": probe_ms}
 
@@ -508,6 +537,8 @@ def main():
     ap.add_argument("--impl", default="lrx", choices=["lrx", "reference"])
     ap.add_argument("--e2e-batch", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graphs", dest="graphs", action="store_false",
+                    help="launch every kernel from the host instead of replaying the captured step")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -587,7 +618,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": {"f32": "f32", "bf16": "bf16 io / f32 accum"}[w["dtype"]],
             "data": "synthetic (reference init, N(0,1) activations, projections from the layer's weights)",
-            "config": config, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": r["launches"],
+            "config": dict(config, cuda_graphs=r["graphed"]), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": r["launches"],
             "clocks": r["clocks"],
             "kernels": {"fwd_ms": r["ms_fwd"], "bwd_ms": r["ms_bwd"],
                         "fwd_GBps": r["bytes"]["fwd"] / (r["ms_fwd"] * 1e-3) / 1e9,
