@@ -34,7 +34,7 @@
 namespace lrx {
 namespace gemm {
 
-constexpr int BM = 128, BK = 32, THREADS = 192;
+constexpr int BM = 128;
 constexpr int BKT = 16;  // K-block of the tall kernel: 64-byte rows, 64B swizzle, 4 stages in flight
 
 __device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
@@ -48,17 +48,6 @@ __device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
     return d;
 }
 
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-    // UMMA shared-memory descriptor, K-major SWIZZLE_128B: LBO = 1 (unused),
-    // SBO = 1024 B between 8-row groups, version 1 (sm_100), layout type 2
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;
-    d |= (uint64_t)(1024 >> 4) << 32;
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)2 << 61;
-    return d;
-}
 
 template <int BN>
 __host__ __device__ constexpr uint32_t idesc_tf32() {
@@ -482,7 +471,6 @@ done:
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
 }
 
-static bool enc_sw128(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows);
 static bool enc_k(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows);
 
 template <int BN>
@@ -532,18 +520,6 @@ static PFN_cuTensorMapEncodeTiled_v12000 enc_fn() {
     return fn;
 }
 
-// [rows, cols] fp32 row-major, box [box_rows, 32 cols = 128 B], 128-byte swizzle
-static bool enc_sw128(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows) {
-    auto fn = enc_fn();
-    if (!fn || (reinterpret_cast<uintptr_t>(p) & 15) || ((cols * 4) & 15)) return false;
-    cuuint64_t dims[2] = {cols, rows};
-    cuuint64_t strides[1] = {cols * 4};
-    cuuint32_t box[2] = {BK, box_rows};
-    cuuint32_t es[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(p), dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 
 // [rows, cols] fp32 row-major, box [box_rows, BKT = 16 cols = 64 B], 64-byte swizzle
 static bool enc_k(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows) {

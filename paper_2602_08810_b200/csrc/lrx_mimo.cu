@@ -20,8 +20,6 @@ namespace lrx {
 namespace mimo {
 
 constexpr int kThreads = 128;
-template <typename T> struct Tile { static constexpr int K = 16; };
-template <> struct Tile<double> { static constexpr int K = 8; };
 
 template <typename T> __device__ __forceinline__ cplx<T> ldc(const cplx<T>* p);
 template <> __device__ __forceinline__ cplx<float> ldc(const cplx<float>* p) {
@@ -40,58 +38,113 @@ template <> __device__ __forceinline__ void stc(cplx<double>* p, cplx<double> v)
     __stcs(reinterpret_cast<double2*>(p), make_double2(v.re, v.im));
 }
 
+// ----------------------------------------------------------------------------
+// Time segments.  The coefficient is constant (LTI), so a segment of SL steps
+// maps its entering state by x_out = abar^SL x_in + X (X = the state reached
+// from zero).  An aggregate pass computes every segment's X (reading v once),
+// the main pass folds the maps of the segments to its left in a fixed order
+// and runs the segment with the true carry.  Lanes = flattened (b, p): a warp
+// step is one contiguous run of 32 complex values.  (The previous single-pass
+// anchored look-back serialised on a chain of anchor publications; here the
+// only serial work is the per-thread fold over <= S maps.)
+constexpr int kSeg = 128;  // steps per segment (= partial rows per batch row)
+
+template <typename T> struct Unroll { static constexpr int K = 16; };
+template <> struct Unroll<double> { static constexpr int K = 8; };
+
+template <typename T>
+__device__ __forceinline__ cplx<T> cpow2k(cplx<T> a, int e) {  // a^e for e a power of two
+    for (int i = 1; i < e; i <<= 1) a = a * a;
+    return a;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) fwd_agg_kernel(const cplx<T>* __restrict__ abar,
+                                                           const cplx<T>* __restrict__ scale,
+                                                           const cplx<T>* __restrict__ bu, cplx<T>* __restrict__ aggX,
+                                                           int64_t B, int64_t L, int64_t P) {
+    using V = cplx<T>;
+    constexpr int K = Unroll<T>::K;
+    const int64_t n_lanes = B * P;
+    const int64_t lane = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (lane >= n_lanes) return;
+    const int s = blockIdx.y;
+    const int64_t b = lane / P, p = lane % P;
+    const V ab = abar[p], sc = scale[p];
+    const cplx<T>* src = bu + (b * L + (int64_t)s * kSeg) * P + p;
+    V X = Traits<V>::zero();
+    for (int k0 = 0; k0 < kSeg; k0 += K) {  // full segments only (s < S-1)
+        V v[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] = ldc(src + (int64_t)(k0 + k) * P);
+#pragma unroll
+        for (int k = 0; k < K; ++k) X = ab * X + sc * v[k];
+    }
+    aggX[(int64_t)s * n_lanes + lane] = X;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) fwd_kernel(const cplx<T>* __restrict__ abar,
                                                        const cplx<T>* __restrict__ scale,
-                                                       const cplx<T>* __restrict__ bu, cplx<T>* __restrict__ x,
-                                                       int64_t B, int64_t L, int64_t P, int n_blk, LookbackWS ws) {
+                                                       const cplx<T>* __restrict__ bu,
+                                                       const cplx<T>* __restrict__ aggX, cplx<T>* __restrict__ x,
+                                                       int64_t B, int64_t L, int64_t P) {
     using V = cplx<T>;
-    using Tr = Traits<V>;
-    constexpr int K = Tile<T>::K;
-    const int tile = next_tile(ws.ticket);
-    const int c = tile / n_blk, blk = tile % n_blk;
+    constexpr int K = Unroll<T>::K;
     const int64_t n_lanes = B * P;
-    const int64_t lane = (int64_t)blk * kThreads + threadIdx.x;
-    const bool valid = lane < n_lanes;
-    const int64_t b = valid ? lane / P : 0, p = valid ? lane % P : 0;
-    const int64_t t0 = (int64_t)c * K;
-    const int nt = (int)min((int64_t)K, L - t0);
-    const V ab = valid ? abar[p] : Tr::one();
-    const V sc = valid ? scale[p] : Tr::zero();
-    V v[K];
+    const int64_t lane = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (lane >= n_lanes) return;
+    const int s = blockIdx.y;
+    const int64_t b = lane / P, p = lane % P;
+    const V ab = abar[p], sc = scale[p];
+    V xs = Traits<V>::zero();
+    if (s > 0) {
+        const V AS = cpow2k(ab, kSeg);
+        for (int r = 0; r < s; ++r) xs = AS * xs + aggX[(int64_t)r * n_lanes + lane];
+    }
+    const int64_t t0 = (int64_t)s * kSeg;
+    const int nt = (int)min((int64_t)kSeg, L - t0);
+    const int64_t base = (b * L + t0) * P + p;
+    for (int k0 = 0; k0 < nt; k0 += K) {
+        V v[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const bool ok = valid && k < nt;
-        v[k] = ok ? sc * ldc(bu + (b * L + t0 + k) * P + p) : Tr::zero();
-    }
-    V A = Tr::one(), X = Tr::zero();
+        for (int k = 0; k < K; ++k) v[k] = k0 + k < nt ? ldc(bu + base + (int64_t)(k0 + k) * P) : Traits<V>::zero();
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        if (k < nt) {
-            X = ab * X + v[k];
-            A = ab * A;
-        }
+        for (int k = 0; k < K; ++k)
+            if (k0 + k < nt) {
+                xs = ab * xs + sc * v[k];
+                stc(x + base + (int64_t)(k0 + k) * P, xs);
+            }
     }
-    V* agg_a = static_cast<V*>(ws.agg_a);
-    V* agg_x = static_cast<V*>(ws.agg_x);
-    V* inc_x = static_cast<V*>(ws.inc_x);
-    const int64_t woff = (int64_t)c * n_lanes + lane;
-    int* sw = ws.status + (int64_t)c * n_blk + blk;
-    V xin = Tr::zero();
-    if (c > 0) {
-        lb_publish<V>(sw, LB_AGG, agg_a + woff, A, agg_x + woff, X, valid);
-        xin = lb_lookback<V>(ws, c, blk, n_blk, lane, n_lanes, valid);
-    }
-    if ((c % kAnchor) == 0)
-        lb_publish<V>(sw, LB_INC, (V*)nullptr, A, inc_x + woff, A * xin + X, valid);
-    V xs = xin;
+}
+
+// backward: carry h = the term added to gx at a segment's last step
+// (conj(abar) g of the next step); a segment maps h_in -> conj(abar)^SL h_in + H
+template <typename T>
+__global__ void __launch_bounds__(kThreads) bwd_agg_kernel(const cplx<T>* __restrict__ abar,
+                                                           const cplx<T>* __restrict__ gx, cplx<T>* __restrict__ aggH,
+                                                           int64_t B, int64_t L, int64_t P) {
+    using V = cplx<T>;
+    constexpr int K = Unroll<T>::K;
+    const int64_t n_lanes = B * P;
+    const int64_t lane = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (lane >= n_lanes) return;
+    const int s = blockIdx.y + 1;  // segments 1 .. S-1
+    const int64_t b = lane / P, p = lane % P;
+    const V abc = conj(abar[p]);
+    const int64_t t0 = (int64_t)s * kSeg;
+    const int nt = (int)min((int64_t)kSeg, L - t0);
+    const int64_t base = (b * L + t0) * P + p;
+    V h = Traits<V>::zero();
+    for (int k1 = nt; k1 > 0; k1 -= K) {
+        V g[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        if (valid && k < nt) {
-            xs = ab * xs + v[k];
-            stc(x + (b * L + t0 + k) * P + p, xs);
-        }
+        for (int k = 0; k < K; ++k) g[k] = k1 - 1 - k >= 0 ? ldc(gx + base + (int64_t)(k1 - 1 - k) * P) : Traits<V>::zero();
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (k1 - 1 - k >= 0) h = abc * (g[k] + h);
     }
+    aggH[(int64_t)s * n_lanes + lane] = h;
 }
 
 template <typename T>
@@ -99,116 +152,96 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const cplx<T>* __restrict
                                                        const cplx<T>* __restrict__ scale,
                                                        const cplx<T>* __restrict__ bu,
                                                        const cplx<T>* __restrict__ x, const cplx<T>* __restrict__ gx,
-                                                       cplx<T>* __restrict__ gbu, cplx<T>* __restrict__ gabar_part,
+                                                       const cplx<T>* __restrict__ aggH, cplx<T>* __restrict__ gbu,
+                                                       cplx<T>* __restrict__ gabar_part,
                                                        cplx<T>* __restrict__ gscale_part, int64_t B, int64_t L,
-                                                       int64_t P, int n_blk, int n_chunks, LookbackWS ws) {
+                                                       int64_t P, int S) {
     using V = cplx<T>;
-    using Tr = Traits<V>;
-    constexpr int K = Tile<T>::K;
-    const int tile = next_tile(ws.ticket);
-    const int s = tile / n_blk, blk = tile % n_blk;
-    const int c = n_chunks - 1 - s;
+    constexpr int K = Unroll<T>::K / 2;
     const int64_t n_lanes = B * P;
-    const int64_t lane = (int64_t)blk * kThreads + threadIdx.x;
-    const bool valid = lane < n_lanes;
-    const int64_t b = valid ? lane / P : 0, p = valid ? lane % P : 0;
-    const int64_t t0 = (int64_t)c * K;
-    const int nt = (int)min((int64_t)K, L - t0);
-    const V abc = valid ? conj(abar[p]) : Tr::one();
-    const V scc = valid ? conj(scale[p]) : Tr::zero();
-    V gxv[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const bool ok = valid && k < nt;
-        gxv[k] = ok ? ldc(gx + (b * L + t0 + k) * P + p) : Tr::zero();
+    const int64_t lane = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (lane >= n_lanes) return;
+    const int s = blockIdx.y;
+    const int64_t b = lane / P, p = lane % P;
+    const V ab = abar[p];
+    const V abc = conj(ab), scc = conj(scale[p]);
+    V h = Traits<V>::zero();
+    if (s < S - 1) {
+        const V AS = cpow2k(abc, kSeg);
+        for (int r = S - 1; r > s; --r) h = AS * h + aggH[(int64_t)r * n_lanes + lane];
     }
-    V A = Tr::one(), H = Tr::zero();
+    const int64_t t0 = (int64_t)s * kSeg;
+    const int nt = (int)min((int64_t)kSeg, L - t0);
+    const int64_t base = (b * L + t0) * P + p;
+    V sa = Traits<V>::zero(), ss = Traits<V>::zero();
+    for (int k1 = nt; k1 > 0; k1 -= K) {
+        V g[K], xp[K], bv[K];
 #pragma unroll
-    for (int k = K - 1; k >= 0; --k) {
-        if (k < nt) {
-            const V g = gxv[k] + H;
-            H = abc * g;
-            A = abc * A;
+        for (int k = 0; k < K; ++k) {
+            const int kk = k1 - 1 - k;
+            const bool ok = kk >= 0;
+            const int64_t off = base + (int64_t)kk * P;
+            g[k] = ok ? ldc(gx + off) : Traits<V>::zero();
+            xp[k] = (ok && t0 + kk > 0) ? ldc(x + off - P) : Traits<V>::zero();
+            bv[k] = ok ? ldc(bu + off) : Traits<V>::zero();
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int kk = k1 - 1 - k;
+            if (kk >= 0) {
+                const V gk = g[k] + h;
+                h = abc * gk;
+                stc(gbu + base + (int64_t)kk * P, scc * gk);
+                sa = sa + gk * conj(xp[k]);
+                ss = ss + conj(bv[k]) * gk;
+            }
         }
     }
-    V* agg_a = static_cast<V*>(ws.agg_a);
-    V* agg_x = static_cast<V*>(ws.agg_x);
-    V* inc_x = static_cast<V*>(ws.inc_x);
-    const int64_t woff = (int64_t)s * n_lanes + lane;
-    int* sw = ws.status + (int64_t)s * n_blk + blk;
-    V hin = Tr::zero();
-    if (s > 0) {
-        lb_publish<V>(sw, LB_AGG, agg_a + woff, A, agg_x + woff, H, valid);
-        hin = lb_lookback<V>(ws, s, blk, n_blk, lane, n_lanes, valid);
-    }
-    if ((s % kAnchor) == 0)
-        lb_publish<V>(sw, LB_INC, (V*)nullptr, A, inc_x + woff, A * hin + H, valid);
-    V h = hin, sa = Tr::zero(), ss = Tr::zero();
-#pragma unroll
-    for (int k = K - 1; k >= 0; --k) {
-        if (valid && k < nt) {
-            const int64_t off = (b * L + t0 + k) * P + p;
-            const V g = gxv[k] + h;
-            h = abc * g;
-            stc(gbu + off, scc * g);
-            const V xp = (t0 + k == 0) ? Tr::zero() : ldc(x + off - P);
-            sa = sa + g * conj(xp);
-            ss = ss + conj(ldc(bu + off)) * g;
-        }
-    }
-    if (valid) {
-        gabar_part[(int64_t)c * n_lanes + lane] = sa;
-        gscale_part[(int64_t)c * n_lanes + lane] = ss;
-    }
+    gabar_part[(int64_t)s * n_lanes + lane] = sa;
+    gscale_part[(int64_t)s * n_lanes + lane] = ss;
 }
 
 template <typename T>
 static size_t ws_bytes(int64_t B, int64_t L, int64_t P) {
-    const int64_t nc = cdiv(L, Tile<T>::K), nb = cdiv(B * P, kThreads);
-    Carver cv(nullptr);
-    cv.take<int>(1);
-    cv.take<int>((size_t)(nc * nb));
-    for (int i = 0; i < 3; ++i) cv.take<cplx<T>>((size_t)(nc * B * P));
-    return cv.off;
-}
-
-template <typename T>
-static int carve(void* w, size_t wb, int64_t B, int64_t L, int64_t P, LookbackWS* ws, cudaStream_t st) {
-    const int64_t nc = cdiv(L, Tile<T>::K), nb = cdiv(B * P, kThreads);
-    const size_t need = ws_bytes<T>(B, L, P);
-    LRX_REQUIRE(w && wb >= need, LRX_ERR_VALUE, "mimo workspace too small: %zu < %zu", wb, need);
-    Carver cv(w);
-    ws->ticket = cv.take<int>(1);
-    ws->status = cv.take<int>((size_t)(nc * nb));
-    const size_t head = cv.off;
-    ws->agg_a = cv.take<cplx<T>>((size_t)(nc * B * P));
-    ws->agg_x = cv.take<cplx<T>>((size_t)(nc * B * P));
-    ws->inc_x = cv.take<cplx<T>>((size_t)(nc * B * P));
-    LRX_REQUIRE(cudaMemsetAsync(w, 0, head, st) == cudaSuccess, LRX_ERR_CUDA, "workspace memset failed");
-    return LRX_OK;
+    const int64_t S = cdiv(L, kSeg);
+    return align_up((size_t)(S * B * P) * sizeof(cplx<T>));
 }
 
 template <typename T>
 static int fwd_t(const void* abar, const void* scale, const void* bu, void* x, int64_t B, int64_t L, int64_t P,
                  void* w, size_t wb, cudaStream_t st) {
-    LookbackWS ws;
-    if (int rc = carve<T>(w, wb, B, L, P, &ws, st)) return rc;
-    const int64_t nc = cdiv(L, Tile<T>::K), nb = cdiv(B * P, kThreads);
-    fwd_kernel<T><<<(unsigned)(nc * nb), kThreads, 0, st>>>((const cplx<T>*)abar, (const cplx<T>*)scale,
-                                                            (const cplx<T>*)bu, (cplx<T>*)x, B, L, P, (int)nb, ws);
-    return launched("lrx_mimo_fwd");
+    const int64_t S = cdiv(L, kSeg), nb = cdiv(B * P, kThreads);
+    LRX_REQUIRE(S <= 65535 && nb <= 0x7fffffff, LRX_ERR_UNSUPPORTED, "mimo: extents too large");
+    LRX_REQUIRE(S == 1 || (w && wb >= ws_bytes<T>(B, L, P)), LRX_ERR_VALUE, "mimo workspace too small");
+    cplx<T>* aggX = static_cast<cplx<T>*>(w);
+    int n = 1;
+    if (S > 1) {
+        fwd_agg_kernel<T><<<dim3((unsigned)nb, (unsigned)(S - 1)), kThreads, 0, st>>>(
+            (const cplx<T>*)abar, (const cplx<T>*)scale, (const cplx<T>*)bu, aggX, B, L, P);
+        ++n;
+    }
+    fwd_kernel<T><<<dim3((unsigned)nb, (unsigned)S), kThreads, 0, st>>>(
+        (const cplx<T>*)abar, (const cplx<T>*)scale, (const cplx<T>*)bu, aggX, (cplx<T>*)x, B, L, P);
+    return launched("lrx_mimo_fwd", n);
 }
 
 template <typename T>
 static int bwd_t(const void* abar, const void* scale, const void* bu, const void* x, const void* gx, void* gbu,
                  void* gap, void* gsp, int64_t B, int64_t L, int64_t P, void* w, size_t wb, cudaStream_t st) {
-    LookbackWS ws;
-    if (int rc = carve<T>(w, wb, B, L, P, &ws, st)) return rc;
-    const int64_t nc = cdiv(L, Tile<T>::K), nb = cdiv(B * P, kThreads);
-    bwd_kernel<T><<<(unsigned)(nc * nb), kThreads, 0, st>>>(
-        (const cplx<T>*)abar, (const cplx<T>*)scale, (const cplx<T>*)bu, (const cplx<T>*)x, (const cplx<T>*)gx,
-        (cplx<T>*)gbu, (cplx<T>*)gap, (cplx<T>*)gsp, B, L, P, (int)nb, (int)nc, ws);
-    return launched("lrx_mimo_bwd");
+    const int64_t S = cdiv(L, kSeg), nb = cdiv(B * P, kThreads);
+    LRX_REQUIRE(S <= 65535 && nb <= 0x7fffffff, LRX_ERR_UNSUPPORTED, "mimo: extents too large");
+    LRX_REQUIRE(S == 1 || (w && wb >= ws_bytes<T>(B, L, P)), LRX_ERR_VALUE, "mimo workspace too small");
+    cplx<T>* aggH = static_cast<cplx<T>*>(w);
+    int n = 1;
+    if (S > 1) {
+        bwd_agg_kernel<T><<<dim3((unsigned)nb, (unsigned)(S - 1)), kThreads, 0, st>>>((const cplx<T>*)abar,
+                                                                                     (const cplx<T>*)gx, aggH, B, L, P);
+        ++n;
+    }
+    bwd_kernel<T><<<dim3((unsigned)nb, (unsigned)S), kThreads, 0, st>>>(
+        (const cplx<T>*)abar, (const cplx<T>*)scale, (const cplx<T>*)bu, (const cplx<T>*)x, (const cplx<T>*)gx, aggH,
+        (cplx<T>*)gbu, (cplx<T>*)gap, (cplx<T>*)gsp, B, L, P, (int)S);
+    return launched("lrx_mimo_bwd", n);
 }
 
 }  // namespace mimo
@@ -220,9 +253,9 @@ extern "C" {
 
 int lrx_mimo_chunking(int dtype, int64_t L, int64_t* chunk_len, int64_t* n_chunks) {
     LRX_REQUIRE(L >= 1, LRX_ERR_SHAPE, "length must be >= 1");
-    const int K = dtype == LRX_C128 ? mimo::Tile<double>::K : mimo::Tile<float>::K;
-    *chunk_len = K;
-    *n_chunks = cdiv(L, K);
+    (void)dtype;
+    *chunk_len = mimo::kSeg;  // partial rows = one per (segment, batch row)
+    *n_chunks = cdiv(L, mimo::kSeg);
     return LRX_OK;
 }
 

@@ -347,7 +347,6 @@ __global__ void __launch_bounds__(FG<NPT>::THREADS) fwd_kernel(
             dub[idx] = dl * ld1(us + idx);
         }
         __syncthreads();
-#pragma unroll
         // reduced readouts stay in registers until the tile is done: no shared
         // store sits between the tile's shared loads, so they can all be hoisted
         float yk[TF / 4][2];
