@@ -265,6 +265,49 @@ __global__ void reduce_rows_part_kernel(const V* __restrict__ in, const V* __res
     if (r0 == 0 && j < N) part[(int64_t)blockIdx.y * N + j] = red[c];
 }
 
+// float, N % 4 == 0: float4 loads (a warp reads 512 contiguous bytes per row),
+// so four times the bytes are in flight per load instruction
+__global__ void reduce_rows_part4_kernel(const float4* __restrict__ in, const float4* __restrict__ in2,
+                                         float4* __restrict__ part, int64_t R, int64_t N4, int64_t rpg) {
+    __shared__ float4 red[256];
+    const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * 32 + c;
+    const int64_t rb = (int64_t)blockIdx.y * rpg, re = min(R, rb + rpg);
+    float4 a0 = make_float4(0, 0, 0, 0), a1 = a0;
+    auto fma4 = [](float4 acc, float4 x, float4 y) {
+        return make_float4(fmaf(x.x, y.x, acc.x), fmaf(x.y, y.y, acc.y), fmaf(x.z, y.z, acc.z), fmaf(x.w, y.w, acc.w));
+    };
+    auto add4 = [](float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); };
+    if (j < N4) {
+        int64_t r = rb + r0;
+        if (in2) {
+            for (; r + 8 < re; r += 16) {
+                a0 = fma4(a0, __ldcs(in + r * N4 + j), __ldcs(in2 + r * N4 + j));
+                a1 = fma4(a1, __ldcs(in + (r + 8) * N4 + j), __ldcs(in2 + (r + 8) * N4 + j));
+            }
+            for (; r < re; r += 8) a0 = fma4(a0, __ldcs(in + r * N4 + j), __ldcs(in2 + r * N4 + j));
+        } else {
+            for (; r + 8 < re; r += 16) {
+                a0 = add4(a0, __ldcs(in + r * N4 + j));
+                a1 = add4(a1, __ldcs(in + (r + 8) * N4 + j));
+            }
+            for (; r < re; r += 8) a0 = add4(a0, __ldcs(in + r * N4 + j));
+        }
+    }
+    red[threadIdx.x] = add4(a0, a1);
+    __syncthreads();
+    for (int h = 4; h >= 1; h >>= 1) {
+        if (r0 < h) red[threadIdx.x] = add4(red[threadIdx.x], red[threadIdx.x + 32 * h]);
+        __syncthreads();
+    }
+    if (r0 == 0 && j < N4) part[(int64_t)blockIdx.y * N4 + j] = red[c];
+}
+
+static int64_t reduce_groups4(int64_t R, int64_t N) {  // float4 plan (N % 4 == 0)
+    const int64_t cb = cdiv(N / 4, 32);
+    return std::max<int64_t>(1, std::min<int64_t>(cdiv(4 * 148, cb), R / 256));
+}
+
 static int64_t reduce_groups(int64_t R, int64_t N) {
     const int64_t cb = cdiv(N, 32);
     int64_t G = cdiv(4 * 148, cb);                 // ~4 blocks of 256 threads per SM
@@ -272,15 +315,37 @@ static int64_t reduce_groups(int64_t R, int64_t N) {
     return std::max<int64_t>(1, G);
 }
 
+
 template <typename V>
 static size_t reduce_ws(int64_t R, int64_t N) {
-    const int64_t G = reduce_groups(R, N);
+    int64_t G = reduce_groups(R, N);
+    if (sizeof(V) == 4 && !Traits<V>::complex && N % 4 == 0) G = std::max(G, reduce_groups4(R, N));
     return G > 1 ? (size_t)G * N * sizeof(V) : 0;
 }
 
 template <typename V>
 static int reduce_rows2(const V* in, const V* in2, V* out, int64_t R, int64_t N, void* ws, size_t wb,
                         cudaStream_t st) {
+    if constexpr (sizeof(V) == 4 && !Traits<V>::complex) {
+        const bool al = !((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(in2) |
+                           reinterpret_cast<uintptr_t>(out)) & 15);
+        if (N % 4 == 0 && al) {
+            const int64_t N4 = N / 4, cb = cdiv(N4, 32);
+            const int64_t G = reduce_groups4(R, N);
+            const int64_t rpg = cdiv(R, G);
+            if (G == 1) {
+                reduce_rows_part4_kernel<<<dim3((unsigned)cb, 1), 256, 0, st>>>(
+                    (const float4*)in, (const float4*)in2, (float4*)out, R, N4, rpg);
+                return launched("lrx_reduce_rows_ws");
+            }
+            LRX_REQUIRE(ws && wb >= (size_t)G * N * sizeof(V), LRX_ERR_VALUE,
+                        "reduce_rows: workspace of %zu bytes needed", (size_t)G * N * sizeof(V));
+            reduce_rows_part4_kernel<<<dim3((unsigned)cb, (unsigned)G), 256, 0, st>>>(
+                (const float4*)in, (const float4*)in2, (float4*)ws, R, N4, rpg);
+            reduce_rows_launch<V>(static_cast<V*>(ws), out, G, N, st);
+            return launched("lrx_reduce_rows_ws", 2);
+        }
+    }
     const int64_t G = reduce_groups(R, N);
     const int64_t rpg = cdiv(R, G);
     if (G == 1) {
