@@ -313,12 +313,12 @@ __host__ __device__ constexpr uint32_t idesc_tf32_mn() {
     return idesc_tf32<BN>() | (1u << 15) | (1u << 16);  // A and B MN-major
 }
 
-template <int BN>
+template <int BN, int MT>
 struct LayTN {
-    static constexpr int A = BM * BKN * 4;  // 4 boxes of BKN x 32
-    static constexpr int B = BN * BKN * 4;  // BN/32 boxes
+    static constexpr int A = MT * BM * BKN * 4;  // 4 MT boxes of BKN x 32
+    static constexpr int B = BN * BKN * 4;       // BN/32 boxes
     static constexpr int STAGE = 2 * A + 2 * B;
-    static constexpr int STAGES = BN >= 256 ? 4 : 6;
+    static constexpr int STAGES = STAGE >= 64 * 1024 ? 3 : STAGE >= 48 * 1024 ? 4 : 6;
     static constexpr size_t smem() { return 2048 + (size_t)STAGES * STAGE; }
 };
 
@@ -331,11 +331,13 @@ __device__ __forceinline__ float4 tf32_low4(float4 v) {
     return lo;
 }
 
-template <int BN>
+// MT M-tiles of 128 per CTA share every B stage (MT = 2 halves the B traffic
+// of the weight-gradient reductions, whose M = N = 256)
+template <int BN, int MT>
 __global__ void __launch_bounds__(THREADS_TN, 1) gemm_tn_kernel(
     const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, float* __restrict__ part,
     int M, int N, int K, int kb_per_split, float alpha) {
-    using LY = LayTN<BN>;
+    using LY = LayTN<BN, MT>;
     constexpr int STAGES = LY::STAGES;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* base = reinterpret_cast<unsigned char*>(
@@ -347,11 +349,11 @@ __global__ void __launch_bounds__(THREADS_TN, 1) gemm_tn_kernel(
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
     unsigned char* stages = base + 1024;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, kz = blockIdx.z;
+    const int m0 = blockIdx.x * BM * MT, n0 = blockIdx.y * BN, kz = blockIdx.z;
     const int nk_all = (K + BKN - 1) / BKN;
     const int kb0 = kz * kb_per_split, kb1 = min(nk_all, kb0 + kb_per_split);
     const int nk = max(0, kb1 - kb0);
-    constexpr uint32_t kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    constexpr uint32_t kTmemCols = MT * BN <= 32 ? 32 : MT * BN <= 64 ? 64 : MT * BN <= 128 ? 128 : MT * BN <= 256 ? 256 : 512;
 
     if (threadIdx.x == 0) {
         tma::prefetch_map(&mA);
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(THREADS_TN, 1) gemm_tn_kernel(
                 const int k0 = (kb0 + i) * BKN;
                 tma::mbar_arrive_expect_tx(&full[st], LY::A + LY::B);
 #pragma unroll
-                for (int c = 0; c < BM / 32; ++c) tma::load_2d(sp + c * BKN * 128, &mA, m0 + 32 * c, k0, &full[st]);
+                for (int c = 0; c < MT * BM / 32; ++c) tma::load_2d(sp + c * BKN * 128, &mA, m0 + 32 * c, k0, &full[st]);
 #pragma unroll
                 for (int c = 0; c < BN / 32; ++c)
                     tma::load_2d(sp + 2 * LY::A + c * BKN * 128, &mB, n0 + 32 * c, k0, &full[st]);
@@ -403,11 +405,16 @@ __global__ void __launch_bounds__(THREADS_TN, 1) gemm_tn_kernel(
 #pragma unroll
                 for (int k = 0; k < BKN / 8; ++k) {
                     const uint32_t off = k * 1024;  // 8 K-rows x 128 B
-                    const uint64_t dA = sw128_mn_desc(sa + off), dAl = sw128_mn_desc(sal + off);
                     const uint64_t dB = sw128_mn_desc(sb + off), dBl = sw128_mn_desc(sbl + off);
-                    mma_tf32(tmem, dA, dB, idesc, (i | k) != 0);
-                    mma_tf32(tmem, dA, dBl, idesc, 1);
-                    mma_tf32(tmem, dAl, dB, idesc, 1);
+#pragma unroll
+                    for (int h = 0; h < MT; ++h) {  // M half h: its 4 boxes of 32 columns
+                        const uint32_t ah = h * 4 * BKN * 128;
+                        const uint64_t dA = sw128_mn_desc(sa + ah + off), dAl = sw128_mn_desc(sal + ah + off);
+                        const uint32_t td = tmem + h * BN;
+                        mma_tf32(td, dA, dB, idesc, (i | k) != 0);
+                        mma_tf32(td, dA, dBl, idesc, 1);
+                        mma_tf32(td, dAl, dB, idesc, 1);
+                    }
                 }
                 mma_commit(&empty[st]);
             }
@@ -433,18 +440,21 @@ __global__ void __launch_bounds__(THREADS_TN, 1) gemm_tn_kernel(
         if (warp >= 6) goto done;  // warps 2..5 cover the four TMEM lane quarters
         {
         const int q = warp & 3;
-        const int row = m0 + 32 * q + lane;
+        if (nk > 0) {
+            tma::mbar_wait(tfull, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        for (int h = 0; h < MT; ++h) {
+        const int row = m0 + h * BM + 32 * q + lane;
         float* dst = part + ((int64_t)kz * M + row) * N;
         if (nk == 0) {
             if (row < M)
                 for (int c = n0; c < min(N, n0 + BN); ++c) dst[c] = 0.f;
         } else {
-            tma::mbar_wait(tfull, 0);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t r[32];
-                const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+                const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(h * BN + c0);
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
                     "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -461,6 +471,7 @@ __global__ void __launch_bounds__(THREADS_TN, 1) gemm_tn_kernel(
                         if (col < N) dst[col] = alpha * __uint_as_float(r[j]);
                     }
             }
+        }
         }
         }
     }
@@ -549,12 +560,16 @@ static bool enc_sw128_box32(CUtensorMap* m, const void* p, uint64_t rows, uint64
 }
 
 struct TNPlan {
-    int BN, ks, kb_per_split;
+    int BN, MT, ks, kb_per_split;
 };
 static TNPlan tn_plan(int64_t M, int64_t N, int64_t K) {
     TNPlan p;
     p.BN = N <= 64 ? 64 : N <= 128 ? 128 : 256;
-    const int64_t tiles = cdiv(M, BM) * cdiv(N, p.BN);
+    // MT = 2 (both M halves per CTA sharing each B stage) halves the B traffic
+    // but measured slower on the S5 shapes (192 vs 137 us for 256x256x131072:
+    // fewer stages in flight); kept selectable for other shapes
+    p.MT = getenv("LRX_GEMM_TN_MT2") && M > BM ? 2 : 1;
+    const int64_t tiles = cdiv(M, BM * p.MT) * cdiv(N, p.BN);
     const int64_t nk = cdiv(K, BKN);
     int64_t ks = std::max<int64_t>(1, std::min<int64_t>(cdiv(2 * 148, tiles), nk / 4 > 0 ? nk / 4 : 1));
     p.kb_per_split = (int)cdiv(nk, ks);
@@ -562,7 +577,7 @@ static TNPlan tn_plan(int64_t M, int64_t N, int64_t K) {
     return p;
 }
 
-template <int BN>
+template <int BN, int MT>
 static int launch_tn(const float* A, const float* B, float* part, const TNPlan& pl, int64_t M, int64_t N, int64_t K,
                      float alpha, cudaStream_t st) {
     CUtensorMap mA, mB;
@@ -570,13 +585,13 @@ static int launch_tn(const float* A, const float* B, float* part, const TNPlan& 
         set_error("gemm_tn: TMA descriptor rejected (M, N %% 4 == 0 and 16-byte aligned rows required)");
         return LRX_ERR_VALUE;
     }
-    const size_t smem = LayTN<BN>::smem();
-    auto k = gemm_tn_kernel<BN>;
+    const size_t smem = LayTN<BN, MT>::smem();
+    auto k = gemm_tn_kernel<BN, MT>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         set_error("gemm_tn: cannot reserve %zu B of shared memory", smem);
         return LRX_ERR_CUDA;
     }
-    const dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN), (unsigned)pl.ks);
+    const dim3 grid((unsigned)cdiv(M, BM * MT), (unsigned)cdiv(N, BN), (unsigned)pl.ks);
     k<<<grid, THREADS_TN, smem, st>>>(mA, mB, part, (int)M, (int)N, (int)K, pl.kb_per_split, alpha);
     return launched("lrx_gemm_f32_tn/tcgen05");
 }
@@ -618,9 +633,14 @@ int lrx_gemm_f32_tn(const void* A, const void* B, void* part, int64_t M, int64_t
     const gemm::TNPlan pl = gemm::tn_plan(M, N, K);
     cudaStream_t st = (cudaStream_t)stream;
     const float *a = (const float*)A, *b = (const float*)B;
-    if (pl.BN == 64) return gemm::launch_tn<64>(a, b, (float*)part, pl, M, N, K, alpha, st);
-    if (pl.BN == 128) return gemm::launch_tn<128>(a, b, (float*)part, pl, M, N, K, alpha, st);
-    return gemm::launch_tn<256>(a, b, (float*)part, pl, M, N, K, alpha, st);
+    if (pl.MT == 2) {
+        if (pl.BN == 64) return gemm::launch_tn<64, 2>(a, b, (float*)part, pl, M, N, K, alpha, st);
+        if (pl.BN == 128) return gemm::launch_tn<128, 2>(a, b, (float*)part, pl, M, N, K, alpha, st);
+        return gemm::launch_tn<256, 2>(a, b, (float*)part, pl, M, N, K, alpha, st);
+    }
+    if (pl.BN == 64) return gemm::launch_tn<64, 1>(a, b, (float*)part, pl, M, N, K, alpha, st);
+    if (pl.BN == 128) return gemm::launch_tn<128, 1>(a, b, (float*)part, pl, M, N, K, alpha, st);
+    return gemm::launch_tn<256, 1>(a, b, (float*)part, pl, M, N, K, alpha, st);
 }
 
 }  // extern "C"
