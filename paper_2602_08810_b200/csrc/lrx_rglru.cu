@@ -28,6 +28,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+#include <cmath>
+
 #include "lrx_common.cuh"
 #include "lrx_host.h"
 #include "lrx_tma.cuh"
@@ -106,13 +109,22 @@ __device__ __forceinline__ Ring<IO> ring(unsigned char* smem, int S) {
     return r;
 }
 
-template <typename IO, typename C, int LW, int PF>
+// Time segments.  When B*W lanes are too few to keep ~24 warps per SM (the
+// per-rank batch of an 8-GPU job), the sequence is cut into n_seg segments
+// of seg_len steps (gridDim.y).  A first pass (AGG) reduces each segment to
+// its transfer pair with a zero carry in: A_s = sum log a_k, X_s = the state
+// the segment produces from x = 0.  The main pass folds the pairs of the
+// segments before it in fixed order (x = exp(A_r) x + X_r) and streams its
+// own segment.  The kernel is latency-bound at few warps per SM, so the extra
+// read pass costs less than the parallelism it buys.
+template <typename IO, typename C, int LW, int PF, bool AGG>
 __global__ void __launch_bounds__(LW) fwd_tma_kernel(const __grid_constant__ CUtensorMap mu,
                                                      const __grid_constant__ CUtensorMap mr,
                                                      const __grid_constant__ CUtensorMap mi, const C* __restrict__ lam,
                                                      const C* __restrict__ b_r, const C* __restrict__ b_i,
-                                                     IO* __restrict__ y, C* __restrict__ ckpt, int64_t L, int64_t W,
-                                                     int n_wblk, int Bn, int S) {
+                                                     IO* __restrict__ y, C* __restrict__ ckpt, C* __restrict__ seg_a,
+                                                     C* __restrict__ seg_x, int64_t L, int64_t W, int n_wblk, int Bn,
+                                                     int S, int seg_len, int seg0) {
     constexpr int CK = Tile<IO>::T;
     constexpr int NW = LW / 32;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -122,8 +134,12 @@ __global__ void __launch_bounds__(LW) fwd_tma_kernel(const __grid_constant__ CUt
     const int w0 = (blockIdx.x % n_wblk) * LW;
     const int64_t w = w0 + tid;
     const bool valid = w < W;
+    const int seg = seg0 + blockIdx.y;
+    const int64_t t_beg = (int64_t)seg * seg_len;
+    const int64_t t_end = min(L, t_beg + seg_len);
+    const int j_beg = (int)(t_beg / PF);
+    const int n_tiles = (int)((t_end + PF - 1) / PF) - j_beg;
     const int row0 = b * (int)L;
-    const int n_tiles = (int)((L + PF - 1) / PF);
     constexpr uint32_t kStageBytes = 3u * PF * LW * sizeof(IO);
     if (tid == 0) {
         tma::prefetch_map(&mu);
@@ -139,10 +155,11 @@ __global__ void __launch_bounds__(LW) fwd_tma_kernel(const __grid_constant__ CUt
     auto issue = [&](int j) {
         const int s = j % S;
         IO* dst = R.data + (size_t)s * 3 * PF * LW;
+        const int r = row0 + (j_beg + j) * PF;
         tma::mbar_arrive_expect_tx(&R.full[s], kStageBytes);
-        tma::load_2d(dst, &mu, w0, row0 + j * PF, &R.full[s]);
-        tma::load_2d(dst + PF * LW, &mr, w0, row0 + j * PF, &R.full[s]);
-        tma::load_2d(dst + 2 * PF * LW, &mi, w0, row0 + j * PF, &R.full[s]);
+        tma::load_2d(dst, &mu, w0, r, &R.full[s]);
+        tma::load_2d(dst + PF * LW, &mr, w0, r, &R.full[s]);
+        tma::load_2d(dst + 2 * PF * LW, &mi, w0, r, &R.full[s]);
     };
     if (tid == 0)
         for (int j = 0; j < S && j < n_tiles; ++j) issue(j);
@@ -153,10 +170,13 @@ __global__ void __launch_bounds__(LW) fwd_tma_kernel(const __grid_constant__ CUt
         br = b_r[w];
         bi = b_i[w];
     }
-    C x = 0;
-    IO* py = y + (int64_t)row0 * W + w;
-    C* pc = ckpt ? ckpt + (int64_t)b * W + w : nullptr;
-    const int64_t ck_stride = (int64_t)Bn * W;
+    const int64_t BW = (int64_t)Bn * W;
+    const int64_t lane = (int64_t)b * W + w;
+    C x = 0, sla = 0;
+    if (!AGG && valid)
+        for (int r = 0; r < seg; ++r) x = Fast<C>::exp(seg_a[r * BW + lane]) * x + seg_x[r * BW + lane];
+    IO* py = y + ((int64_t)row0 + t_beg) * W + w;
+    C* pc = ckpt ? ckpt + (t_beg / CK) * BW + lane : nullptr;
     static_assert(CK % PF == 0, "checkpoint interval must be a multiple of the tile");
     for (int j = 0; j < n_tiles; ++j) {
         const int s = j % S;
@@ -176,44 +196,49 @@ __global__ void __launch_bounds__(LW) fwd_tma_kernel(const __grid_constant__ CUt
             tma::mbar_wait(&R.empty[s], ph);
             issue(j + S);
         }
-        if (pc && (j % (CK / PF)) == 0) {  // state entering this checkpoint chunk
+        if (!AGG && pc && (j % (CK / PF)) == 0) {  // state entering this checkpoint chunk
             if (valid) __stcs(pc, x);
-            pc += ck_stride;
+            pc += BW;
         }
-        const int nk = (int)min((int64_t)PF, L - (int64_t)j * PF);
-        if (nk == PF) {
+        const int nk = (int)min((int64_t)PF, t_end - (int64_t)(j_beg + j) * PF);
+        C tla = 0;
 #pragma unroll
-            for (int k = 0; k < PF; ++k) {
+        for (int k = 0; k < PF; ++k) {
+            if (nk == PF || k < nk) {
                 const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
                 x = q.a * x + (q.s * q.i) * q.u;
-                if (valid) st_io(py, x);
-                py += W;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < PF; ++k) {
-                if (k < nk) {
-                    const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
-                    x = q.a * x + (q.s * q.i) * q.u;
+                if (AGG) {
+                    tla += (C(kGate) * q.r) * la;
+                } else {
                     if (valid) st_io(py, x);
                     py += W;
                 }
             }
         }
+        if (AGG) sla += tla;
+    }
+    if (AGG && valid) {
+        seg_a[seg * BW + lane] = sla;
+        seg_x[seg * BW + lane] = x;
     }
 }
 
 // Reverse streaming pass; the y tile of a time tile is loaded one row early
-// so its row k holds x_{t-1}.
-template <typename IO, typename C, int LW, int PF>
+// so its row k holds x_{t-1}.  Segmented like the forward: the AGG pass
+// streams qr and gy only (A_s = sum log a_k, H_s = the carry the segment
+// hands to its left neighbour from h = 0); the main pass folds the segments
+// to its right (h = exp(A_r) h + H_r, r = n_seg-1 .. seg+1) and writes
+// per-(segment, lane) parameter-gradient partials.
+template <typename IO, typename C, int LW, int PF, bool AGG>
 __global__ void __launch_bounds__(LW) bwd_tma_kernel(
     const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mr,
     const __grid_constant__ CUtensorMap mi, const __grid_constant__ CUtensorMap mg,
     const __grid_constant__ CUtensorMap my, const C* __restrict__ lam, const C* __restrict__ b_r,
     const C* __restrict__ b_i, IO* __restrict__ gu, IO* __restrict__ gqr, IO* __restrict__ gqi,
-    C* __restrict__ gla_part, C* __restrict__ gbr_part, C* __restrict__ gbi_part, int64_t L, int64_t W, int n_wblk,
-    int S) {
+    C* __restrict__ gla_part, C* __restrict__ gbr_part, C* __restrict__ gbi_part, C* __restrict__ seg_a,
+    C* __restrict__ seg_h, int64_t L, int64_t W, int n_wblk, int Bn, int S, int seg_len, int seg0, int n_seg) {
     constexpr int NW = LW / 32;
+    constexpr int NA = AGG ? 2 : 5;  // staged arrays: AGG {qr, gy}; main {u, qr, qi, gy, y}
     extern __shared__ __align__(128) unsigned char smem[];
     auto R = ring<IO>(smem, S);
     const int tid = threadIdx.x;
@@ -221,15 +246,19 @@ __global__ void __launch_bounds__(LW) bwd_tma_kernel(
     const int w0 = (blockIdx.x % n_wblk) * LW;
     const int64_t w = w0 + tid;
     const bool valid = w < W;
+    const int seg = seg0 + blockIdx.y;
+    const int64_t t_beg = (int64_t)seg * seg_len;
+    const int64_t t_end = min(L, t_beg + seg_len);
+    const int j_beg = (int)(t_beg / PF);
+    const int n_tiles = (int)((t_end + PF - 1) / PF) - j_beg;
     const int row0 = b * (int)L;
-    const int n_tiles = (int)((L + PF - 1) / PF);
-    constexpr uint32_t kStageBytes = 5u * PF * LW * sizeof(IO);
+    constexpr uint32_t kStageBytes = (uint32_t)NA * PF * LW * sizeof(IO);
     if (tid == 0) {
-        tma::prefetch_map(&mu);
+        if (!AGG) tma::prefetch_map(&mu);
         tma::prefetch_map(&mr);
-        tma::prefetch_map(&mi);
+        if (!AGG) tma::prefetch_map(&mi);
         tma::prefetch_map(&mg);
-        tma::prefetch_map(&my);
+        if (!AGG) tma::prefetch_map(&my);
         for (int s = 0; s < S; ++s) {
             tma::mbar_init(&R.full[s], 1);
             tma::mbar_init(&R.empty[s], NW);
@@ -238,16 +267,21 @@ __global__ void __launch_bounds__(LW) bwd_tma_kernel(
     }
     __syncthreads();
     auto issue = [&](int j) {  // j-th tile in reverse order
-        const int tt = n_tiles - 1 - j;
+        const int tt = j_beg + n_tiles - 1 - j;
         const int s = j % S;
-        IO* dst = R.data + (size_t)s * 5 * PF * LW;
+        IO* dst = R.data + (size_t)s * NA * PF * LW;
         const int r = row0 + tt * PF;
         tma::mbar_arrive_expect_tx(&R.full[s], kStageBytes);
-        tma::load_2d(dst, &mu, w0, r, &R.full[s]);
-        tma::load_2d(dst + PF * LW, &mr, w0, r, &R.full[s]);
-        tma::load_2d(dst + 2 * PF * LW, &mi, w0, r, &R.full[s]);
-        tma::load_2d(dst + 3 * PF * LW, &mg, w0, r, &R.full[s]);
-        tma::load_2d(dst + 4 * PF * LW, &my, w0, r - 1, &R.full[s]);  // rows t-1
+        if (AGG) {
+            tma::load_2d(dst, &mr, w0, r, &R.full[s]);
+            tma::load_2d(dst + PF * LW, &mg, w0, r, &R.full[s]);
+        } else {
+            tma::load_2d(dst, &mu, w0, r, &R.full[s]);
+            tma::load_2d(dst + PF * LW, &mr, w0, r, &R.full[s]);
+            tma::load_2d(dst + 2 * PF * LW, &mi, w0, r, &R.full[s]);
+            tma::load_2d(dst + 3 * PF * LW, &mg, w0, r, &R.full[s]);
+            tma::load_2d(dst + 4 * PF * LW, &my, w0, r - 1, &R.full[s]);  // rows t-1
+        }
     };
     if (tid == 0)
         for (int j = 0; j < S && j < n_tiles; ++j) issue(j);
@@ -258,23 +292,32 @@ __global__ void __launch_bounds__(LW) bwd_tma_kernel(
         br = b_r[w];
         bi = b_i[w];
     }
-    C h = 0;
+    const int64_t BW = (int64_t)Bn * W;
+    const int64_t lane = (int64_t)b * W + w;
+    C h = 0, asum = 0;
+    if (!AGG && valid)
+        for (int r = n_seg - 1; r > seg; --r) h = Fast<C>::exp(seg_a[r * BW + lane]) * h + seg_h[r * BW + lane];
     Kahan<C> sla, sbr, sbi;
     IO *pgu = gu + (int64_t)row0 * W + w, *pgr = gqr + (int64_t)row0 * W + w, *pgi = gqi + (int64_t)row0 * W + w;
     for (int j = 0; j < n_tiles; ++j) {
         const int s = j % S;
         const uint32_t ph = (j / S) & 1;
-        const int tt = n_tiles - 1 - j;
+        const int tt = j_beg + n_tiles - 1 - j;
         tma::mbar_wait(&R.full[s], ph);
-        const IO* src = R.data + (size_t)s * 5 * PF * LW + tid;
+        const IO* src = R.data + (size_t)s * NA * PF * LW + tid;
         IO cu[PF], cr[PF], ci[PF], cg[PF], cy[PF];
 #pragma unroll
         for (int k = 0; k < PF; ++k) {
-            cu[k] = src[k * LW];
-            cr[k] = src[(PF + k) * LW];
-            ci[k] = src[(2 * PF + k) * LW];
-            cg[k] = src[(3 * PF + k) * LW];
-            cy[k] = src[(4 * PF + k) * LW];
+            if (AGG) {
+                cr[k] = src[k * LW];
+                cg[k] = src[(PF + k) * LW];
+            } else {
+                cu[k] = src[k * LW];
+                cr[k] = src[(PF + k) * LW];
+                ci[k] = src[(2 * PF + k) * LW];
+                cg[k] = src[(3 * PF + k) * LW];
+                cy[k] = src[(4 * PF + k) * LW];
+            }
         }
         __syncwarp();
         if ((tid & 31) == 0) tma::mbar_arrive(&R.empty[s]);
@@ -283,7 +326,21 @@ __global__ void __launch_bounds__(LW) bwd_tma_kernel(
             issue(j + S);
         }
         const int64_t t0 = (int64_t)tt * PF;
-        const int nk = (int)min((int64_t)PF, L - t0);
+        const int nk = (int)min((int64_t)PF, t_end - t0);
+        if (AGG) {
+            C tla = 0;
+#pragma unroll
+            for (int k = PF - 1; k >= 0; --k) {
+                if (k < nk) {
+                    const C r = Fast<C>::sigmoid(C(cvt(cr[k])) + br);
+                    const C loga = (C(kGate) * r) * la;
+                    h = Fast<C>::exp(loga) * (C(cvt(cg[k])) + h);
+                    tla += loga;
+                }
+            }
+            asum += tla;
+            continue;
+        }
         if (tt == 0) cy[0] = IO(0);  // x_{-1} = 0
         C tla = 0, tbr = 0, tbi = 0;
         const int64_t o0 = t0 * W;
@@ -309,8 +366,12 @@ __global__ void __launch_bounds__(LW) bwd_tma_kernel(
         sbr.add(tbr);
         sbi.add(tbi);
     }
-    if (valid) {
-        const int64_t p = (int64_t)b * W + w;
+    if (!valid) return;
+    if (AGG) {
+        seg_a[seg * BW + lane] = asum;
+        seg_h[seg * BW + lane] = h;
+    } else {
+        const int64_t p = seg * BW + lane;
         gla_part[p] = sla.s;
         gbr_part[p] = sbr.s;
         gbi_part[p] = sbi.s;
@@ -737,58 +798,129 @@ static int carve(void* w, size_t wb, int64_t B, int64_t L, int64_t W, LookbackWS
 // TMA plan: lanes per CTA, ring stages, shared-memory bytes.  False when TMA
 // does not apply (row alignment, residency), so the caller falls back.
 struct TmaPlan {
-    int LW, S, n_wblk, n_blk;
+    int LW, PF, S, n_wblk, n_blk, n_seg, seg_len;
     size_t smem;
 };
 
+// Launch plan of a TMA streaming pass with `narr` staged arrays.  The walk is
+// latency-bound unless each SM holds enough independent steps in flight:
+// resident warps x PF (the tile rows a thread evaluates between barrier
+// waits) >= kWork.  The plan takes the smallest tile PF in {4, 8, 16} that
+// reaches it and fits shared memory.  With few lanes (the per-rank batch of
+// an 8-GPU job: < 6 warps per SM) the sequence is first cut into n_seg time
+// segments (>= 256 steps, a multiple of the checkpoint interval) at the
+// price of the AGG pass.  Env overrides (tests, sweeps):
+// LRX_RGLRU_LW, _PF, _SEGS, _STAGES.
+constexpr int kWork = 128;
+
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 template <typename IO>
-static bool tma_plan(int64_t B, int64_t W, int narr, int PF, TmaPlan* p) {
+static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p) {
+    constexpr int CK = Tile<IO>::T;
     if ((W * (int64_t)sizeof(IO)) % 16) return false;
     const int sms = sm_count();
-    int LW = 128;
-    while (LW > 32 && B * cdiv(W, LW) < 4 * sms) LW /= 2;
+    int LW = W <= 32 ? 32 : W <= 64 ? 64 : 128;
+    if (const char* e = getenv("LRX_RGLRU_LW")) LW = atoi(e) == 32 ? 32 : atoi(e) == 64 ? 64 : 128;
+    const int n_wblk = (int)cdiv(W, LW);
+    const int64_t n_blk = B * n_wblk;
+    const int smax = env_int("LRX_RGLRU_STAGES", 6);
+    // ring depth that fits for (PF, n_seg); 0 = does not fit
+    auto stages = [&](int PF, int64_t n_seg) -> int {
+        const int64_t per_sm = cdiv(n_blk * n_seg, (int64_t)sms);
+        if (per_sm > 32) return 0;
+        const size_t stage = (size_t)narr * PF * LW * sizeof(IO);
+        // 228 KB per SM minus the 1 KB the runtime reserves per resident CTA
+        const size_t budget = ((size_t)(228 - per_sm - 4) * 1024u) / per_sm;
+        if (budget < 256 + 2 * stage) return 0;
+        return (int)std::min<size_t>((size_t)smax, (budget - 256) / stage);
+    };
+    const double warps = (double)n_blk * (LW / 32) / sms;
+    const int64_t max_seg = std::max<int64_t>(1, std::min<int64_t>(64, L / 256));
+    // segments only below ~6 resident warps per SM (measured: the AGG pass
+    // costs more than it buys above that); aim for ~12.
+    int64_t n_seg = warps < 6 ? std::min<int64_t>(max_seg, (int64_t)std::ceil(12 / warps)) : 1;
+    int PF = 0;
+    for (; n_seg >= 1 && !PF; n_seg = n_seg > 1 ? n_seg - 1 : 0) {
+        for (int pf = 4; pf <= CK; pf *= 2) {
+            if (!stages(pf, n_seg)) break;
+            PF = pf;
+            if (warps * n_seg * pf >= kWork) break;
+        }
+        if (PF) break;
+    }
+    if (!PF) return false;
+    if (const char* e = getenv("LRX_RGLRU_PF")) PF = std::min(CK, atoi(e) >= 16 ? 16 : atoi(e) >= 8 ? 8 : 4);
+    if (const char* e = getenv("LRX_RGLRU_SEGS"))
+        n_seg = std::max<int64_t>(1, std::min<int64_t>({(int64_t)atoi(e), 64, std::max<int64_t>(1, L / 64)}));
+    const int64_t len = cdiv(cdiv(L, n_seg), (int64_t)CK) * CK;
+    p->seg_len = (int)std::min<int64_t>(len, 1ll << 30);
+    p->n_seg = (int)cdiv(L, len);
+    while (!(p->S = stages(PF, p->n_seg)) && PF > 4) PF /= 2;  // overrides that do not fit
+    if (!p->S) return false;
     p->LW = LW;
-    p->n_wblk = (int)cdiv(W, LW);
-    p->n_blk = (int)(B * p->n_wblk);
-    const int per_sm = (int)cdiv(p->n_blk, sms);
-    if (per_sm > 32) return false;
-    const size_t stage = (size_t)narr * PF * LW * sizeof(IO);
-    // 228 KB per SM minus the 1 KB the runtime reserves per resident CTA
-    const size_t budget = ((size_t)(228 - per_sm - 4) * 1024u) / per_sm;
-    if (budget < 256 + 2 * stage) return false;
-    int S = (int)((budget - 256) / stage);
-    if (S > 6) S = 6;
-    p->S = S;
-    p->smem = 128 * ((2 * S * 8 + 127) / 128) + (size_t)S * stage;
+    p->PF = PF;
+    p->n_wblk = n_wblk;
+    p->n_blk = (int)n_blk;
+    p->smem = 128 * ((2 * p->S * 8 + 127) / 128) + (size_t)p->S * narr * PF * LW * sizeof(IO);
     return true;
 }
 
-template <typename IO, typename C, int LW, int PF>
-static int launch_fwd_tma(const TmaPlan& pl, const CUtensorMap* m, const void* lam, const void* br, const void* bi,
-                          void* y, void* ckpt, int64_t B, int64_t L, int64_t W, cudaStream_t st) {
-    auto k = fwd_tma_kernel<IO, C, LW, PF>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem) != cudaSuccess) {
-        set_error("rglru fwd: cannot reserve %zu B of shared memory", pl.smem);
+template <typename K>
+static int reserve_smem(K k, size_t smem, const char* what) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        set_error("%s: cannot reserve %zu B of shared memory", what, smem);
         return LRX_ERR_CUDA;
     }
-    k<<<pl.n_blk, LW, pl.smem, st>>>(m[0], m[1], m[2], (const C*)lam, (const C*)br, (const C*)bi, (IO*)y, (C*)ckpt,
-                                     L, W, pl.n_wblk, (int)B, pl.S);
+    return LRX_OK;
+}
+
+// seg: 2 * n_seg * B * W values (A then X) when pl.n_seg > 1.
+template <typename IO, typename C, int LW, int PF>
+static int launch_fwd_tma(const TmaPlan& pl, const CUtensorMap* m, const void* lam, const void* br, const void* bi,
+                          void* y, void* ckpt, C* seg, int64_t B, int64_t L, int64_t W, cudaStream_t st) {
+    const int64_t sn = (int64_t)pl.n_seg * B * W;
+    if (pl.n_seg > 1) {
+        auto a = fwd_tma_kernel<IO, C, LW, PF, true>;
+        if (int rc = reserve_smem(a, pl.smem, "rglru fwd")) return rc;
+        a<<<dim3(pl.n_blk, pl.n_seg - 1), LW, pl.smem, st>>>(m[0], m[1], m[2], (const C*)lam, (const C*)br,
+                                                              (const C*)bi, nullptr, nullptr, seg, seg + sn, L, W,
+                                                              pl.n_wblk, (int)B, pl.S, pl.seg_len, 0);
+        if (int rc = launched("lrx_rglru_fwd/tma_agg")) return rc;
+    }
+    auto k = fwd_tma_kernel<IO, C, LW, PF, false>;
+    if (int rc = reserve_smem(k, pl.smem, "rglru fwd")) return rc;
+    k<<<dim3(pl.n_blk, pl.n_seg), LW, pl.smem, st>>>(m[0], m[1], m[2], (const C*)lam, (const C*)br, (const C*)bi,
+                                                     (IO*)y, (C*)ckpt, seg, seg + sn, L, W, pl.n_wblk, (int)B, pl.S,
+                                                     pl.seg_len, 0);
     return launched("lrx_rglru_fwd/tma");
 }
 
+// parts: 3 * n_seg * B * W; seg: 2 * n_seg * B * W (A then H).  `pa` is the
+// plan of the 2-array AGG pass (same segments, deeper ring).
 template <typename IO, typename C, int LW, int PF>
-static int launch_bwd_tma(const TmaPlan& pl, const CUtensorMap* m, const void* lam, const void* br, const void* bi,
-                          void* gu, void* gqr, void* gqi, C* parts, int64_t B, int64_t L, int64_t W,
-                          cudaStream_t st) {
-    auto k = bwd_tma_kernel<IO, C, LW, PF>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem) != cudaSuccess) {
-        set_error("rglru bwd: cannot reserve %zu B of shared memory", pl.smem);
-        return LRX_ERR_CUDA;
+static int launch_bwd_tma(const TmaPlan& pl, const TmaPlan& pa, const CUtensorMap* m, const void* lam,
+                          const void* br, const void* bi, void* gu, void* gqr, void* gqi, C* parts, C* seg, int64_t B,
+                          int64_t L, int64_t W, cudaStream_t st) {
+    const int64_t n = (int64_t)pl.n_seg * B * W;
+    if (pl.n_seg > 1) {
+        auto a = bwd_tma_kernel<IO, C, LW, PF, true>;
+        if (int rc = reserve_smem(a, pa.smem, "rglru bwd")) return rc;
+        // segment 0's pair is never read
+        a<<<dim3(pl.n_blk, pl.n_seg - 1), LW, pa.smem, st>>>(
+            m[0], m[1], m[2], m[3], m[4], (const C*)lam, (const C*)br, (const C*)bi, nullptr, nullptr, nullptr,
+            nullptr, nullptr, nullptr, seg, seg + n, L, W, pl.n_wblk, (int)B, pa.S, pl.seg_len, 1, pl.n_seg);
+        if (int rc = launched("lrx_rglru_bwd/tma_agg")) return rc;
     }
-    const int64_t n = B * W;
-    k<<<pl.n_blk, LW, pl.smem, st>>>(m[0], m[1], m[2], m[3], m[4], (const C*)lam, (const C*)br, (const C*)bi,
-                                     (IO*)gu, (IO*)gqr, (IO*)gqi, parts, parts + n, parts + 2 * n, L, W, pl.n_wblk,
-                                     pl.S);
+    auto k = bwd_tma_kernel<IO, C, LW, PF, false>;
+    if (int rc = reserve_smem(k, pl.smem, "rglru bwd")) return rc;
+    k<<<dim3(pl.n_blk, pl.n_seg), LW, pl.smem, st>>>(m[0], m[1], m[2], m[3], m[4], (const C*)lam, (const C*)br,
+                                                     (const C*)bi, (IO*)gu, (IO*)gqr, (IO*)gqi, parts, parts + n,
+                                                     parts + 2 * n, seg, seg + n, L, W, pl.n_wblk, (int)B, pl.S,
+                                                     pl.seg_len, 0, pl.n_seg);
     return launched("lrx_rglru_bwd/tma");
 }
 
@@ -811,8 +943,42 @@ static int launch_bwd_rc(const CUtensorMap* m, const void* lam, const void* br, 
     return launched("lrx_rglru_bwd/rc");
 }
 
-constexpr int kPfF = 4;  // forward TMA tile rows
-constexpr int kPfB = 4;  // backward TMA tile rows
+// The backward AGG pass (2 arrays) runs the main pass's tile and segments
+// with the deeper ring its smaller stages allow.
+template <typename IO>
+static bool agg_plan(const TmaPlan& pl, int64_t B, int64_t L, int64_t W, TmaPlan* pa) {
+    *pa = pl;
+    const int sms = sm_count();
+    const int64_t per_sm = cdiv((int64_t)pl.n_blk * pl.n_seg, (int64_t)sms);
+    const size_t stage = (size_t)2 * pl.PF * pl.LW * sizeof(IO);
+    const size_t budget = ((size_t)(228 - per_sm - 4) * 1024u) / per_sm;
+    pa->S = (int)std::min<size_t>((size_t)env_int("LRX_RGLRU_STAGES", 6), (budget - 256) / stage);
+    pa->smem = 128 * ((2 * pa->S * 8 + 127) / 128) + (size_t)pa->S * stage;
+    return pa->S >= 2;
+}
+
+template <typename IO, typename C, int LW>
+static int fwd_pf(const TmaPlan& pl, const CUtensorMap* m, const void* lam, const void* br, const void* bi, void* y,
+                  void* ckpt, C* seg, int64_t B, int64_t L, int64_t W, cudaStream_t st) {
+    switch (pl.PF) {
+        case 16: if constexpr (Tile<IO>::T >= 16) return launch_fwd_tma<IO, C, LW, 16>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
+        [[fallthrough]];
+        case 8: return launch_fwd_tma<IO, C, LW, 8>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
+        default: return launch_fwd_tma<IO, C, LW, 4>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
+    }
+}
+
+template <typename IO, typename C, int LW>
+static int bwd_pf(const TmaPlan& pl, const TmaPlan& pa, const CUtensorMap* m, const void* lam, const void* br,
+                  const void* bi, void* gu, void* gqr, void* gqi, C* parts, C* seg, int64_t B, int64_t L, int64_t W,
+                  cudaStream_t st) {
+    switch (pl.PF) {
+        case 16: if constexpr (Tile<IO>::T >= 16) return launch_bwd_tma<IO, C, LW, 16>(pl, pa, m, lam, br, bi, gu, gqr, gqi, parts, seg, B, L, W, st);
+        [[fallthrough]];
+        case 8: return launch_bwd_tma<IO, C, LW, 8>(pl, pa, m, lam, br, bi, gu, gqr, gqi, parts, seg, B, L, W, st);
+        default: return launch_bwd_tma<IO, C, LW, 4>(pl, pa, m, lam, br, bi, gu, gqr, gqi, parts, seg, B, L, W, st);
+    }
+}
 
 template <typename IO, typename C>
 static int colsums(C* parts, int64_t rows, int64_t B, int64_t W, void* gla, void* gbr, void* gbi,
@@ -830,16 +996,22 @@ static int fwd_t(const void* u, const void* qr, const void* qi, const void* lam,
                  void* y, void* ckpt, int64_t B, int64_t L, int64_t W, void* w, size_t wb, cudaStream_t st) {
     const int mode = mode_env();
     TmaPlan pl;
-    if ((mode == 0 || mode == 1) && B * L < (1ll << 31) && tma_plan<IO>(B, W, 3, kPfF, &pl)) {
+    if ((mode == 0 || mode == 1) && B * L < (1ll << 31) && tma_plan<IO>(B, L, W, 3, &pl)) {
         CUtensorMap m[3];
         const void* src[3] = {u, qr, qi};
         bool ok = true;
-        for (int i = 0; i < 3; ++i) ok &= tma::encode_2d(&m[i], src[i], sizeof(IO), B * L, W, kPfF, pl.LW);
+        for (int i = 0; i < 3; ++i) ok &= tma::encode_2d(&m[i], src[i], sizeof(IO), B * L, W, pl.PF, pl.LW);
         if (ok) {
+            C* seg = nullptr;
+            if (pl.n_seg > 1) {
+                Carver cv(w);
+                seg = cv.take<C>((size_t)2 * pl.n_seg * B * W);
+                LRX_REQUIRE(w && cv.off <= wb, LRX_ERR_VALUE, "rglru workspace too small");
+            }
             switch (pl.LW) {
-                case 128: return launch_fwd_tma<IO, C, 128, kPfF>(pl, m, lam, br, bi, y, ckpt, B, L, W, st);
-                case 64: return launch_fwd_tma<IO, C, 64, kPfF>(pl, m, lam, br, bi, y, ckpt, B, L, W, st);
-                default: return launch_fwd_tma<IO, C, 32, kPfF>(pl, m, lam, br, bi, y, ckpt, B, L, W, st);
+                case 128: return fwd_pf<IO, C, 128>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
+                case 64: return fwd_pf<IO, C, 64>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
+                default: return fwd_pf<IO, C, 32>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
             }
         }
         LRX_REQUIRE(mode != 1, LRX_ERR_UNSUPPORTED, "rglru: TMA descriptors unavailable");
@@ -867,7 +1039,7 @@ static int bwd_t(const void* u, const void* qr, const void* qi, const void* lam,
                  void* gbr, void* gbi, int64_t B, int64_t L, int64_t W, void* w, size_t wb, cudaStream_t st) {
     const int mode = mode_env();
     const int64_t n = B * W;
-    TmaPlan pl;
+    TmaPlan pl, pa;
     // recompute variant (LRX_RGLRU_MODE=rc): 7 array passes, no y stream.
     // Measured slower on C4 (18.3 vs 16.4 ms: the 2 x gates per element at
     // ~14 warps/SM, limited by the 512 B of staged rows per thread), so the
@@ -893,23 +1065,25 @@ static int bwd_t(const void* u, const void* qr, const void* qi, const void* lam,
     }
     // y (= the state) is exact only at fp32/f64 I/O; bf16 recomputes instead
     if (y && sizeof(IO) != 2 && (mode == 0 || mode == 1) && B * L < (1ll << 31) &&
-        tma_plan<IO>(B, W, 5, kPfB, &pl)) {
+        tma_plan<IO>(B, L, W, 5, &pl) && agg_plan<IO>(pl, B, L, W, &pa)) {
         CUtensorMap m[5];
         const void* src[5] = {u, qr, qi, gy, y};
         bool ok = true;
-        for (int i = 0; i < 5; ++i) ok &= tma::encode_2d(&m[i], src[i], sizeof(IO), B * L, W, kPfB, pl.LW);
+        for (int i = 0; i < 5; ++i) ok &= tma::encode_2d(&m[i], src[i], sizeof(IO), B * L, W, pl.PF, pl.LW);
         if (ok) {
+            const int64_t sn = (int64_t)pl.n_seg * B * W;
             Carver cv(w);
-            C* parts = cv.take<C>((size_t)3 * n);
+            C* parts = cv.take<C>((size_t)3 * sn);
+            C* seg = cv.take<C>((size_t)2 * sn);
             LRX_REQUIRE(w && cv.off <= wb, LRX_ERR_VALUE, "rglru workspace too small");
             int rc;
             switch (pl.LW) {
-                case 128: rc = launch_bwd_tma<IO, C, 128, kPfB>(pl, m, lam, br, bi, gu, gqr, gqi, parts, B, L, W, st); break;
-                case 64: rc = launch_bwd_tma<IO, C, 64, kPfB>(pl, m, lam, br, bi, gu, gqr, gqi, parts, B, L, W, st); break;
-                default: rc = launch_bwd_tma<IO, C, 32, kPfB>(pl, m, lam, br, bi, gu, gqr, gqi, parts, B, L, W, st); break;
+                case 128: rc = bwd_pf<IO, C, 128>(pl, pa, m, lam, br, bi, gu, gqr, gqi, parts, seg, B, L, W, st); break;
+                case 64: rc = bwd_pf<IO, C, 64>(pl, pa, m, lam, br, bi, gu, gqr, gqi, parts, seg, B, L, W, st); break;
+                default: rc = bwd_pf<IO, C, 32>(pl, pa, m, lam, br, bi, gu, gqr, gqi, parts, seg, B, L, W, st); break;
             }
             if (rc) return rc;
-            return colsums<IO, C>(parts, 1, B, W, gla, gbr, gbi, st);
+            return colsums<IO, C>(parts, pl.n_seg, B, W, gla, gbr, gbi, st);
         }
         LRX_REQUIRE(mode != 1, LRX_ERR_UNSUPPORTED, "rglru: TMA descriptors unavailable");
     }
@@ -933,7 +1107,10 @@ template <typename IO, typename C>
 static size_t bwd_ws_bytes(int64_t B, int64_t L, int64_t W) {
     int nc, nw, nb;
     geometry<IO>(B, L, W, &nc, &nw, &nb);
-    return ws_lookback<IO, C>(B, L, W) + align_up((size_t)3 * nc * B * W * sizeof(C));
+    const size_t lb = ws_lookback<IO, C>(B, L, W) + align_up((size_t)3 * nc * B * W * sizeof(C));
+    TmaPlan pl;  // segmented TMA passes: 3 partial + 2 pair rows per segment
+    const size_t tm = tma_plan<IO>(B, L, W, 5, &pl) ? 5 * align_up((size_t)pl.n_seg * B * W * sizeof(C)) : 0;
+    return std::max(lb, tm);
 }
 
 }  // namespace rglru

@@ -427,6 +427,32 @@ def test_rglru_kernel_variants_match_oracle(lrx, monkeypatch, mode):
         assert rel(g.params[k], rg[k]) < TOL["f32"], (mode, k)
 
 
+@pytest.mark.parametrize("segs", ["1", "2", "5", "64"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_rglru_time_segments_match_oracle(lrx, monkeypatch, segs, dtype):
+    """Segmented TMA passes (LRX_RGLRU_SEGS; ragged last segment) give the
+    oracle's answer, and the same bits on a second run."""
+    monkeypatch.setenv("LRX_RGLRU_MODE", "tma")
+    monkeypatch.setenv("LRX_RGLRU_SEGS", segs)
+    m, B, L = 64, 2, 1000 if dtype == "f32" else 517
+    layer = lrx.make_layer("rglru", m, dtype=dtype, seed=37)
+    io = torch.bfloat16 if dtype == "bf16" else torch.float32
+    u = torch.from_numpy(port.Rng(15).normal((B, L, m))).to("cuda", io)
+    gy = torch.from_numpy(port.Rng(16).normal((B, L, m))).to("cuda", io)
+    y, tape = layer.forward(u, tape=True)
+    g = lrx.layer_backward(layer, tape, gy)
+    y2, tape2 = layer.forward(u, tape=True)
+    g2 = lrx.layer_backward(layer, tape2, gy)
+    assert torch.equal(y, y2) and torch.equal(g.u, g2.u)
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64("rglru", None, params, u.float().cpu().numpy(), gy.float().cpu().numpy())
+    tol = TOL[dtype]
+    assert rel(y, ry) < tol
+    assert rel(g.u, rgu) < tol
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < tol, (segs, k)
+
+
 # ---- step mode (decode), reference test_layers.py:277-315 -------------------
 
 STEP_KINDS = [("s4d", 4), ("s5", 8), ("lru", 4), ("s6", 4), ("rglru", None)]
