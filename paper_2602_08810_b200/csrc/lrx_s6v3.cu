@@ -825,9 +825,12 @@ Geo geometry(int64_t B, int64_t L, int64_t D) {
     if (const char* e = getenv("LRX_S6_SEGS")) S = atoll(e);
     else {
         // segments cost an extra aggregate pass (~40% of the main pass), so
-        // only split when the CTAs cannot give every SM ~2 (8 warps)
-        const int64_t want = 2LL * num_sms();
-        if (ctas < want) S = cdiv(want, ctas);
+        // only split when the CTAs cannot give every SM ~2 (8 warps); then
+        // split finely (~16 CTAs per SM over the segments): the aggregate
+        // pass runs on S-1 of them and is latency-bound with fewer
+        // (measured C3 at B=8/4/2 per GPU: S=2 3.87 ms, S=16 3.35 ms at B=8)
+        const int64_t sms = num_sms();
+        if (ctas * 10 < 2 * sms * 9) S = cdiv(16 * sms, ctas);
     }
     const int64_t tiles = cdiv(L, T);
     S = std::max<int64_t>(1, std::min<int64_t>(S, std::max<int64_t>(1, tiles / 4)));  // >= 4 tiles per segment

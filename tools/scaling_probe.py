@@ -7,13 +7,22 @@ import torch
 import bench
 
 def tm(prob, n=5):
+    """fwd+bwd replayed from CUDA graphs (as bench.py times it)."""
     for _ in range(2):
         c = prob["fwd"](); prob["bwd"](c)
+    torch.cuda.synchronize()
+    g_f, g_b = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_f):
+        gc = prob["fwd"]()
+    with torch.cuda.graph(g_b):
+        prob["bwd"](gc)
+    for _ in range(2):
+        g_f.replay(); g_b.replay()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(n):
-        c = prob["fwd"](); prob["bwd"](c)
+        g_f.replay(); g_b.replay()
     b.record(); torch.cuda.synchronize()
     return a.elapsed_time(b) / n
 
