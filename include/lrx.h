@@ -189,6 +189,29 @@ int lrx_s4d_step(int dtype, void* x, const void* abar, const void* w, const void
 int lrx_mimo_step(int dtype, void* x, const void* abar, const void* scale, const void* Bre, const void* Bim,
                   const void* Cre, const void* Cim, const void* D, const void* u, void* y, double out_scale,
                   int64_t B, int64_t P, int64_t H, void* stream);
+/* ---- MIMO LTI coefficient work (S5 / LRU), one launch each way ------------
+ * Replaces the parameter-sized torch glue of S5._abar_scale / LRU._abar_scale
+ * (layers.py:823-834, 936-943) and the coefficient + B/C gradient assembly of
+ * S5._backward / LRU._backward (layers.py:836-895, 945-980) with
+ * scheme_partials (autograd.py:186-211).
+ * kind 0 = S5 (p0 lambda_re_log, p1 lambda_im, p2 log_delta; scheme ZOH or
+ * DIRAC: bilinear keeps its host-side singular check), kind 1 = LRU (p0
+ * nu_log, p1 theta_log, p2 gamma_log).  dtype = parameter dtype (F32 / F64);
+ * abar, scale: complex [P] of that precision; extra: f64 [P][8] kept for the
+ * gradient call; wbt [2P,m], wb [m,2P], wct [m,2P], wgt [2P,m]: real layouts
+ * of B [P,m] and C [m,P] for the projection GEMMs (any may be NULL); with
+ * lo_planes (F32 only) each is followed by a second plane holding the
+ * 3xTF32 low parts v - tf32(v) (the Bt_lo operand of lrx_gemm_f32). */
+int lrx_mimo_coef(int kind, int scheme, int dtype, const void* p0, const void* p1, const void* p2, const void* b_re,
+                  const void* b_im, const void* c_re, const void* c_im, int64_t P, int64_t m, void* abar, void* scale,
+                  double* extra, void* wbt, void* wb, void* wct, void* wgt, int lo_planes, void* stream);
+/* ga, gsc: complex [P] (sum g conj(x_prev), sum conj(bu) g); R [m,2P] = gy^T x,
+ * R2 [2P,m] = gbu^T u.  g0..g2: [P] coefficient grads (keys as p0..p2),
+ * gb_re/gb_im [P,m], gc_re/gc_im [m,P] = out_scale (R_re, -R_im). */
+int lrx_mimo_coef_grads(int kind, int scheme, int dtype, const void* p0, const void* p1, const void* p2,
+                        const double* extra, const void* ga, const void* gsc, const void* R, const void* R2,
+                        double out_scale, void* g0, void* g1, void* g2, void* gb_re, void* gb_im, void* gc_re,
+                        void* gc_im, int64_t P, int64_t m, void* stream);
 /* S6: x[B,D,N] compute precision; u, y io dtype; pre [B,D] = the delta
  * projection (bias not added), Bk, Ck [B,N] compute precision. */
 int lrx_s6_step(int io_dtype, void* x, const void* u, const void* pre, const void* Bk, const void* Ck,

@@ -23,6 +23,7 @@ parameters and fp32 accumulation.
 """
 from __future__ import annotations
 
+import os
 import warnings
 from dataclasses import dataclass, field
 
@@ -41,6 +42,9 @@ __all__ = ["LAYER_KINDS", "SCHEMES_BY_KIND", "UnknownLayer", "LayerConfig", "Lay
            "layer_step"]
 
 LAYER_KINDS = ("s4d", "s5", "lru", "s6", "rglru")
+# tokens from which the MIMO projections run on the tcgen05 GEMMs (below: cuBLAS)
+_TC_MIN_TOKENS = int(os.environ.get("LRX_TC_MIN_TOKENS", "4096"))
+
 SCHEMES_BY_KIND = {"s4d": ("zoh", "bilinear", "dirac"), "s5": ("zoh", "bilinear", "dirac"),
                    "lru": (), "s6": (), "rglru": ()}
 STREAM_BLOCK = 512  # layers.py:77 (kept for API parity; the device path is not block-streamed)
@@ -434,15 +438,67 @@ class _MIMOBase(LinearRecurrence):
         """(abar, scale) in the compute dtype plus f64 context for the grads."""
         raise NotImplementedError
 
+    # -- fused coefficient work (csrc/lrx_coef.cu) ------------------------------
+    _KIND_CODE = None
+    _SCHEME_CODE = {"zoh": 0, "bilinear": 1, "dirac": 2}
+
+    def _coef_params(self):
+        raise NotImplementedError
+
+    def _fused(self, deltas):
+        """One-launch coefficient/layout work for constant steps (bilinear S5
+        keeps the torch path: its singular-set check is a host decision)."""
+        return deltas is None and (self.kind == "lru" or self.discretization in ("zoh", "dirac"))
+
+    def _coef_pack(self):
+        """abar, scale, the f64 context and the four real GEMM layouts of B / C
+        (with 3xTF32 low planes for fp32) from one lrx_mimo_coef launch."""
+        P, m, dev = self._P, self.d_model, self.device
+        lo = self.tdt == torch.float32
+        abar = torch.empty(P, dtype=self.tcdt, device=dev)
+        scale = torch.empty(P, dtype=self.tcdt, device=dev)
+        extra = torch.empty((P, 8), dtype=torch.float64, device=dev)
+        w = torch.empty((4, 2 if lo else 1, 2 * P * m), dtype=self.tdt, device=dev)
+        p0, p1, p2 = self._coef_params()
+        _lib.check(_lib.lib().lrx_mimo_coef(
+            self._KIND_CODE, self._SCHEME_CODE.get(self.discretization, 0), _lib.code_of(self.tdt), _lib.ptr(p0),
+            _lib.ptr(p1), _lib.ptr(p2), _lib.ptr(self.B_re), _lib.ptr(self.B_im), _lib.ptr(self.C_re),
+            _lib.ptr(self.C_im), P, m, _lib.ptr(abar), _lib.ptr(scale), _lib.ptr(extra), _lib.ptr(w[0]),
+            _lib.ptr(w[1]), _lib.ptr(w[2]), _lib.ptr(w[3]), int(lo), _lib.stream()))
+        shp = {"wbt": (2 * P, m), "wb": (m, 2 * P), "wct": (m, 2 * P), "wgt": (2 * P, m)}
+        pk = {"abar": abar, "scale": scale, "extra": extra}
+        for i, k in enumerate(shp):
+            pk[k] = w[i, 0].view(shp[k])
+            pk[k + "_lo"] = w[i, 1].view(shp[k]) if lo else None
+        return pk
+
+    def _coef_grads_fused(self, pk, ga, gsc, R, R2):
+        P, m, dev, dt = self._P, self.d_model, self.device, self.tdt
+        g = torch.empty((3, P), dtype=dt, device=dev)
+        gb = torch.empty((2, P, m), dtype=dt, device=dev)
+        gc = torch.empty((2, m, P), dtype=dt, device=dev)
+        p0, p1, p2 = self._coef_params()
+        _lib.check(_lib.lib().lrx_mimo_coef_grads(
+            self._KIND_CODE, self._SCHEME_CODE.get(self.discretization, 0), _lib.code_of(dt), _lib.ptr(p0),
+            _lib.ptr(p1), _lib.ptr(p2), _lib.ptr(pk["extra"]), _lib.ptr(ga.contiguous()), _lib.ptr(gsc.contiguous()),
+            _lib.ptr(R.contiguous()), _lib.ptr(R2.contiguous()), float(self.OUT_SCALE), _lib.ptr(g[0]),
+            _lib.ptr(g[1]), _lib.ptr(g[2]), _lib.ptr(gb[0]), _lib.ptr(gb[1]), _lib.ptr(gc[0]), _lib.ptr(gc[1]),
+            P, m, _lib.stream()))
+        keys = self._coef_keys
+        return {keys[0]: g[0], keys[1]: g[1], keys[2]: g[2], "B.re": gb[0], "B.im": gb[1], "C.re": gc[0],
+                "C.im": gc[1]}
+
     def _tc(self, K, T):
         """fp32 projections run on the tcgen05 3xTF32 GEMMs (ops.gemm_f32 /
         gemm_f32_tn) when the row width keeps TMA rows 16-byte aligned and
-        there are enough tokens T to fill the GPU with 128-row tiles; f64
-        layers, odd widths and small batches (C1: 8k tokens, launch-bound)
-        use the library (cuBLAS) GEMM."""
-        return self.tdt == torch.float32 and K % 4 == 0 and T >= 32768
+        there are enough tokens T (>= 4096, measured: C1 LRU 8k tokens 0.18 ->
+        0.15 ms per step on them; at 1k tokens cuBLAS wins); f64 layers, odd
+        widths and tiny batches use the library (cuBLAS) GEMM."""
+        return self.tdt == torch.float32 and K % 4 == 0 and T >= _TC_MIN_TOKENS
 
     def _forward(self, u, deltas, keep):
+        if self._fused(deltas):
+            return self._forward_fused(u, keep)
         B, L, m = u.shape
         P = self._P
         u2 = u.reshape(B * L, m)
@@ -465,6 +521,52 @@ class _MIMOBase(LinearRecurrence):
                             alpha=self.OUT_SCALE).reshape(B, L, m)
         saved = {"u": u, "x": x, "bu": bu, "deltas": deltas} if keep else {}
         return y, saved, x[:, -1]
+
+    def _forward_fused(self, u, keep):
+        B, L, m = u.shape
+        P = self._P
+        u2 = u.reshape(B * L, m).contiguous()
+        pk = self._coef_pack()
+        if self._tc(m, B * L):
+            bu2 = ops.gemm_f32(u2, pk["wbt"], Bt_lo=pk["wbt_lo"])
+        else:
+            bu2 = u2 @ pk["wb"]
+        bu = torch.view_as_complex(bu2.reshape(B, L, P, 2))
+        x = ops.mimo_scan_fwd(pk["abar"], pk["scale"], bu)
+        x2 = torch.view_as_real(x).reshape(B * L, 2 * P)
+        if self._tc(2 * P, B * L):  # y = OUT Re(C x) + D u, the D u skip fused into the epilogue
+            y = ops.gemm_f32(x2, pk["wct"], Bt_lo=pk["wct_lo"], Cin=u2, colscale=self.D.contiguous(),
+                             alpha=self.OUT_SCALE).reshape(B, L, m)
+        else:
+            y = torch.addmm((self.D * u).reshape(B * L, m), x2, pk["wct"].T, alpha=self.OUT_SCALE).reshape(B, L, m)
+        saved = {"u": u, "x": x, "bu": bu, "deltas": None, "pk": pk} if keep else {}
+        return y, saved, x[:, -1]
+
+    def _backward_fused(self, s, gy):
+        u, x, bu, pk, host = s["u"], s["x"], s["bu"], s["pk"], s["host"]
+        B, L, m = u.shape
+        P = self._P
+        gy = self._gy(gy, u.shape)
+        gy2, u2 = gy.reshape(B * L, m).contiguous(), u.reshape(B * L, m).contiguous()
+        x2 = torch.view_as_real(x).reshape(B * L, 2 * P)
+        gD = ops.reduce_rows(gy2, B * L, m, other=u2)  # sum_t gy u per channel
+        tn = self._tc(m, B * L) and self._tc(2 * P, B * L)
+        R = ops.gemm_f32_tn(gy2, x2) if tn else gy2.T @ x2     # [m, 2P]
+        if self._tc(m, B * L):
+            gx2 = ops.gemm_f32(gy2, pk["wgt"], Bt_lo=pk["wgt_lo"], alpha=self.OUT_SCALE)
+        else:
+            gx2 = self.OUT_SCALE * (gy2 @ pk["wct"])
+        gx = torch.view_as_complex(gx2.reshape(B, L, P, 2))
+        gbu, ga, gsc = ops.mimo_scan_bwd(pk["abar"], pk["scale"], bu, x, gx)
+        gbu2 = torch.view_as_real(gbu).reshape(B * L, 2 * P)
+        R2 = ops.gemm_f32_tn(gbu2, u2) if tn else gbu2.T @ u2  # [2P, m]
+        if self._tc(2 * P, B * L):  # gu = D gy + Re(g conj(B)), the skip fused into the epilogue
+            gu = ops.gemm_f32(gbu2, pk["wb"], Bt_lo=pk["wb_lo"], Cin=gy2, colscale=self.D.contiguous()).reshape(B, L, m)
+        else:
+            gu = gy * self.D + (gbu2 @ pk["wbt"]).reshape(B, L, m)
+        grads = self._coef_grads_fused(pk, ga, gsc, R, R2)
+        grads["D"] = gD
+        return self._out({k: grads[k] for k in self.parameters()}, gu, host)
 
     # -- step mode (layers.py:708-783) ----------------------------------------
     def _zero_state(self, batch):
@@ -503,6 +605,8 @@ class _MIMOBase(LinearRecurrence):
         return scale.conj() * gv, ga_k, bu.conj() * gv
 
     def _backward(self, s, gy):
+        if "pk" in s:
+            return self._backward_fused(s, gy)
         u, x, bu, deltas, host = s["u"], s["x"], s["bu"], s["deltas"], s["host"]
         B, L, m = u.shape
         P = self._P
@@ -558,9 +662,15 @@ class S5(_MIMOBase):
         self.D = self._p(np.ones(m, dt))
         self.log_delta = self._p(_log_delta_init(r_d, P, dt))
 
+    _KIND_CODE = 0
+    _coef_keys = ("lambda_re_log", "lambda_im", "log_delta")
+
     @property
     def _P(self):
         return self.d_state // 2
+
+    def _coef_params(self):
+        return self.lambda_re_log, self.lambda_im, self.log_delta
 
     def parameters(self):
         return {"lambda_re_log": self.lambda_re_log, "lambda_im": self.lambda_im, "B.re": self.B_re,
@@ -616,9 +726,15 @@ class LRU(_MIMOBase):
         self.B_re, self.B_im, self.C_re, self.C_im = map(self._p, (Br, Bi, Cr, Ci))
         self.D = self._p(np.ones(m, dt))
 
+    _KIND_CODE = 1
+    _coef_keys = ("nu_log", "theta_log", "gamma_log")
+
     @property
     def _P(self):
         return self.d_state
+
+    def _coef_params(self):
+        return self.nu_log, self.theta_log, self.gamma_log
 
     def parameters(self):
         return {"nu_log": self.nu_log, "theta_log": self.theta_log, "gamma_log": self.gamma_log,
