@@ -118,7 +118,7 @@ __device__ __forceinline__ Ring<IO> ring(unsigned char* smem, int S) {
 // own segment.  The kernel is latency-bound at few warps per SM, so the extra
 // read pass costs less than the parallelism it buys.
 template <typename IO, typename C, int LW, int PF, bool AGG>
-__global__ void __launch_bounds__(LW) fwd_tma_kernel(const __grid_constant__ CUtensorMap mu,
+__global__ void __launch_bounds__(LW, PF == 4 && LW >= 64 ? 1152 / LW : 1) fwd_tma_kernel(const __grid_constant__ CUtensorMap mu,
                                                      const __grid_constant__ CUtensorMap mr,
                                                      const __grid_constant__ CUtensorMap mi, const C* __restrict__ lam,
                                                      const C* __restrict__ b_r, const C* __restrict__ b_i,
@@ -201,21 +201,38 @@ __global__ void __launch_bounds__(LW) fwd_tma_kernel(const __grid_constant__ CUt
             pc += BW;
         }
         const int nk = (int)min((int64_t)PF, t_end - (int64_t)(j_beg + j) * PF);
-        C tla = 0;
+        // the whole-tile case runs without per-step guards; stores are
+        // predicated once per tile
+        C tla = 0, xs[PF];
+        auto step = [&](int k) {
+            const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
+            x = q.a * x + (q.s * q.i) * q.u;
+            xs[k] = x;
+            if (AGG) tla += (C(kGate) * q.r) * la;
+        };
+        if (nk == PF) {
 #pragma unroll
-        for (int k = 0; k < PF; ++k) {
-            if (nk == PF || k < nk) {
-                const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
-                x = q.a * x + (q.s * q.i) * q.u;
-                if (AGG) {
-                    tla += (C(kGate) * q.r) * la;
+            for (int k = 0; k < PF; ++k) step(k);
+        } else {
+#pragma unroll
+            for (int k = 0; k < PF; ++k)
+                if (k < nk) step(k);
+        }
+        if (AGG) {
+            sla += tla;
+        } else {
+            if (valid) {
+                if (nk == PF) {
+#pragma unroll
+                    for (int k = 0; k < PF; ++k) st_io(py + k * W, xs[k]);
                 } else {
-                    if (valid) st_io(py, x);
-                    py += W;
+#pragma unroll
+                    for (int k = 0; k < PF; ++k)
+                        if (k < nk) st_io(py + k * W, xs[k]);
                 }
             }
+            py += PF * W;
         }
-        if (AGG) sla += tla;
     }
     if (AGG && valid) {
         seg_a[seg * BW + lane] = sla;
@@ -230,7 +247,7 @@ __global__ void __launch_bounds__(LW) fwd_tma_kernel(const __grid_constant__ CUt
 // to its right (h = exp(A_r) h + H_r, r = n_seg-1 .. seg+1) and writes
 // per-(segment, lane) parameter-gradient partials.
 template <typename IO, typename C, int LW, int PF, bool AGG>
-__global__ void __launch_bounds__(LW) bwd_tma_kernel(
+__global__ void __launch_bounds__(LW, PF == 4 && LW >= 64 ? 1152 / LW : 1) bwd_tma_kernel(
     const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mr,
     const __grid_constant__ CUtensorMap mi, const __grid_constant__ CUtensorMap mg,
     const __grid_constant__ CUtensorMap my, const C* __restrict__ lam, const C* __restrict__ b_r,
@@ -344,23 +361,28 @@ __global__ void __launch_bounds__(LW) bwd_tma_kernel(
         if (tt == 0) cy[0] = IO(0);  // x_{-1} = 0
         C tla = 0, tbr = 0, tbi = 0;
         const int64_t o0 = t0 * W;
-#pragma unroll
-        for (int k = PF - 1; k >= 0; --k) {
-            if (k < nk) {
-                const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
-                const C g = C(cvt(cg[k])) + h;
-                h = q.a * g;
-                const BwdOut<C> o = bwd_step<C>(q, g, C(cvt(cy[k])), la);
-                if (valid) {
-                    const int64_t off = o0 + (int64_t)k * W;
-                    st_io(pgu + off, o.gu);
-                    st_io(pgr + off, o.gqr);
-                    st_io(pgi + off, o.gqi);
-                }
-                tla += o.la_term;
-                tbr += o.gqr;
-                tbi += o.gqi;
+        IO *qu = pgu + o0, *qr = pgr + o0, *qi = pgi + o0;
+        auto step = [&](int k) {
+            const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
+            const C g = C(cvt(cg[k])) + h;
+            h = q.a * g;
+            const BwdOut<C> o = bwd_step<C>(q, g, C(cvt(cy[k])), la);
+            if (valid) {  // predicated stores
+                st_io(qu + k * W, o.gu);
+                st_io(qr + k * W, o.gqr);
+                st_io(qi + k * W, o.gqi);
             }
+            tla += o.la_term;
+            tbr += o.gqr;
+            tbi += o.gqi;
+        };
+        if (nk == PF) {  // whole tile: no per-step guards
+#pragma unroll
+            for (int k = PF - 1; k >= 0; --k) step(k);
+        } else {
+#pragma unroll
+            for (int k = PF - 1; k >= 0; --k)
+                if (k < nk) step(k);
         }
         sla.add(tla);
         sbr.add(tbr);
