@@ -28,6 +28,7 @@
 #include <stdint.h>
 
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -70,13 +71,15 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
-template <int BN>
+template <int BN, bool TE = false>
 struct Lay {
     static constexpr int A = BM * BKT * 4;  // 8 KB
     static constexpr int B = BN * BKT * 4;
     static constexpr int STAGE = 2 * A + 2 * B;  // A, A_lo, Bt, Bt_lo
     static constexpr int STAGES = BN >= 256 ? 4 : 6;
-    static constexpr int EPI = 8 * 32 * 33 * 4;  // per epilogue warp: 32 x 32 fp32 transpose tile (padded)
+    // per epilogue warp: TE = one 32 x 32 fp32 TMA box (128B-swizzled, 4 KB);
+    // else a 32 x 32 transpose tile (padded)
+    static constexpr int EPI = TE ? 8 * 4096 : 8 * 32 * 33 * 4;
     // 1 KB alignment slack + 1 KB barrier block + the stage ring + epilogue tiles
     static constexpr size_t smem() { return 2048 + (size_t)STAGES * STAGE + EPI; }
 };
@@ -88,12 +91,21 @@ struct Lay {
 // row stores) overlaps the mainloop of tile i+1.
 constexpr int THREADS_P = 448;  // + 8 epilogue warps (2 per TMEM lane quarter)
 
-template <int BN>
+// TE: TMA epilogue.  Each epilogue warp owns one 4 KB box buffer (32 rows x
+// 32 columns, 128-byte swizzle): the skip input Cin lands there by TMA
+// (issued before the accumulator wait, so the first chunk's read overlaps
+// the mainloop), the lane of row r combines it with its accumulator row in
+// place (16-byte accesses at the swizzled chunk: conflict-free), and one
+// TMA store writes the box (out-of-bounds rows / columns clipped).  The
+// direct-store epilogue kept 32 loads of 128 B in flight per warp, which
+// bounded the skip-input GEMMs at ~2 TB/s.
+template <int BN, bool TE>
 __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
     const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
-    const __grid_constant__ CUtensorMap mBl, float* C, const float* Cin,
+    const __grid_constant__ CUtensorMap mBl, const __grid_constant__ CUtensorMap mC,
+    const __grid_constant__ CUtensorMap mCin, float* C, const float* Cin,
     const float* __restrict__ colscale, int M, int N, int K, float alpha, float beta) {
-    using LY = Lay<BN>;
+    using LY = Lay<BN, TE>;
     constexpr int STAGES = LY::STAGES;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* base = reinterpret_cast<unsigned char*>(
@@ -103,7 +115,8 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
     uint64_t* empty = split + STAGES;                        // [STAGES] MMAs done with the stage
     uint64_t* tfull = empty + STAGES;                        // [2] accumulator ready
     uint64_t* tempty = tfull + 2;                            // [2] accumulator drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* cbar = tempty + 2;                             // [8] TE: Cin box landed (per epilogue warp)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 8);
     unsigned char* stages = base + 1024;
     float* epi = reinterpret_cast<float*>(stages + STAGES * LY::STAGE);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -123,6 +136,11 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
         for (int i = 0; i < 2; ++i) {
             tma::mbar_init(&tfull[i], 1);
             tma::mbar_init(&tempty[i], 256);
+        }
+        for (int i = 0; i < 8; ++i) tma::mbar_init(&cbar[i], 1);
+        if (TE) {
+            tma::prefetch_map(&mC);
+            if (Cin) tma::prefetch_map(&mCin);
         }
         tma::fence_barrier_init();
     }
@@ -206,6 +224,88 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
                 tma::fence_proxy_async();  // generic writes -> async-proxy (MMA) reads
                 tma::mbar_arrive(&split[st]);
             }
+    } else if (TE) {
+        // ------------------------------------------------- epilogue (TMA)
+        const int q = warp & 3;
+        const int half = (warp - 6) >> 2;
+        float* buf = epi + (warp - 6) * 1024;  // 4 KB, 1 KB aligned
+        uint64_t* cb = &cbar[warp - 6];
+        uint32_t cph = 0;
+        int ti = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+            const int m0 = (tile % tm) * BM, n0 = (tile / tm) * BN;
+            const int acc = ti & 1;
+            const int rbase = m0 + 32 * q;
+            auto issue_cin = [&](int c0) {
+                if (lane == 0) {
+                    tma::mbar_arrive_expect_tx(cb, 4096);
+                    tma::load_2d(buf, &mCin, n0 + c0, rbase, cb);
+                }
+            };
+            if (lane == 0) tma::bulk_wait_read<0>();  // the last store has read the buffer
+            __syncwarp();
+            if (Cin) issue_cin(32 * half);
+            tma::mbar_wait(&tfull[acc], (ti >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int c0 = 32 * half; c0 < BN; c0 += 64) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem + acc * BN + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                    "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                      "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                      "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+                      "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+                      "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c0 + 64 >= BN) {
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    tma::mbar_arrive(&tempty[acc]);
+                }
+                if (Cin) tma::mbar_wait(cb, (cph++) & 1);
+                float* rowp = buf + lane * 32;  // this lane's row: 8 swizzled 16-byte chunks
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    float4* p4 = reinterpret_cast<float4*>(rowp + 4 * (g ^ (lane & 7)));
+                    float4 v;
+                    v.x = alpha * __uint_as_float(r[4 * g]);
+                    v.y = alpha * __uint_as_float(r[4 * g + 1]);
+                    v.z = alpha * __uint_as_float(r[4 * g + 2]);
+                    v.w = alpha * __uint_as_float(r[4 * g + 3]);
+                    if (Cin) {
+                        const float4 c = *p4;
+                        const int col = n0 + c0 + 4 * g;
+                        float s0 = beta, s1 = beta, s2 = beta, s3 = beta;
+                        if (colscale) {
+                            s0 = __ldg(colscale + min(col, N - 1));
+                            s1 = __ldg(colscale + min(col + 1, N - 1));
+                            s2 = __ldg(colscale + min(col + 2, N - 1));
+                            s3 = __ldg(colscale + min(col + 3, N - 1));
+                        }
+                        v.x += s0 * c.x;
+                        v.y += s1 * c.y;
+                        v.z += s2 * c.z;
+                        v.w += s3 * c.w;
+                    }
+                    *p4 = v;
+                }
+                tma::fence_proxy_async();  // generic smem writes -> the TMA store's reads
+                __syncwarp();
+                if (lane == 0) {
+                    tma::store_2d(&mC, buf, n0 + c0, rbase);
+                    tma::bulk_commit();
+                }
+                if (c0 + 64 < BN) {
+                    if (lane == 0) tma::bulk_wait_read<0>();
+                    __syncwarp();
+                    if (Cin) issue_cin(c0 + 64);
+                }
+            }
+        }
+        if (lane == 0) tma::bulk_wait<0>();
     } else {
         // ---------------------------------------------------------- epilogue
         const int q = warp & 3;            // TMEM lane quarter this warp may access
@@ -484,16 +584,23 @@ done:
 
 static bool enc_k(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows);
 
+static bool enc_epi(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols);
+
 template <int BN>
 static int launch(const float* A, const float* Bt, const float* Btl, float* C, const float* Cin, const float* cs,
                   int64_t M, int64_t N, int64_t K, float alpha, float beta, cudaStream_t st) {
-    CUtensorMap mA, mB, mBl;
+    CUtensorMap mA, mB, mBl, mC, mCin;
     if (!enc_k(&mA, A, M, K, BM) || !enc_k(&mB, Bt, N, K, BN) || !enc_k(&mBl, Btl, N, K, BN)) {
         set_error("gemm: TMA descriptor rejected (K %% 4 == 0 and 16-byte aligned rows required)");
         return LRX_ERR_VALUE;
     }
-    const size_t smem = Lay<BN>::smem();
-    auto k = gemm_tf32x3_kernel<BN>;
+    // TMA epilogue when C / Cin rows are 16-byte aligned (LRX_GEMM_EPI=direct forces the old one)
+    const char* ee = getenv("LRX_GEMM_EPI");
+    const bool te = !(ee && !strcmp(ee, "direct")) && enc_epi(&mC, C, M, N) && (!Cin || enc_epi(&mCin, Cin, M, N));
+    if (!te) mC = mA, mCin = mA;  // unused
+    else if (!Cin) mCin = mC;
+    const size_t smem = te ? Lay<BN, true>::smem() : Lay<BN, false>::smem();
+    auto k = te ? gemm_tf32x3_kernel<BN, true> : gemm_tf32x3_kernel<BN, false>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         set_error("gemm: cannot reserve %zu B of shared memory", smem);
         return LRX_ERR_CUDA;
@@ -507,8 +614,8 @@ static int launch(const float* A, const float* Bt, const float* Btl, float* C, c
     }
     const int64_t tiles = cdiv(M, BM) * cdiv(N, BN);
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
-    k<<<grid, THREADS_P, smem, st>>>(mA, mB, mBl, C, Cin, cs, (int)M, (int)N, (int)K, alpha, beta);
-    return launched("lrx_gemm_f32/tcgen05");
+    k<<<grid, THREADS_P, smem, st>>>(mA, mB, mBl, mC, mCin, C, Cin, cs, (int)M, (int)N, (int)K, alpha, beta);
+    return launched(te ? "lrx_gemm_f32/tcgen05+tma_epilogue" : "lrx_gemm_f32/tcgen05");
 }
 
 }  // namespace gemm
@@ -533,6 +640,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 enc_fn() {
 
 
 // [rows, cols] fp32 row-major, box [box_rows, BKT = 16 cols = 64 B], 64-byte swizzle
+// C / Cin boxes of the TMA epilogue: 32 rows x 32 fp32 (128 B), 128B swizzle.
+static bool enc_epi(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols) {
+    auto fn = enc_fn();
+    if (!fn || (reinterpret_cast<uintptr_t>(p) & 15) || ((cols * 4) & 15)) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(p), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static bool enc_k(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t box_rows) {
     auto fn = enc_fn();
     if (!fn || (reinterpret_cast<uintptr_t>(p) & 15) || ((cols * 4) & 15)) return false;

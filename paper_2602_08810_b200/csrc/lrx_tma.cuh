@@ -86,6 +86,13 @@ __device__ __forceinline__ void store_3d(const CUtensorMap* m, const void* src, 
                  "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
                  : "memory");
 }
+// 2D tile store smem -> global (bulk group); out-of-bounds parts clipped.
+__device__ __forceinline__ void store_2d(const CUtensorMap* m, const void* src, int c0, int r0) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(r0), "r"(smem_u32(src))
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
