@@ -94,6 +94,37 @@ def _log_delta_init(rng, shape, dt):
     return np.asarray(rng.uniform(np.log(1e-3), np.log(1e-1), shape), dt)
 
 
+def _tc_ok(a, *dims):
+    """The tcgen05 3xTF32 GEMMs take fp32 operands with 16-byte rows and enough
+    tokens to fill the GPU (see _MIMOBase._tc)."""
+    return (a.dtype == torch.float32 and a.is_cuda and a.shape[0] >= _TC_MIN_TOKENS
+            and all(d % 4 == 0 and d >= 16 for d in dims))
+
+
+def _proj(a2, w, lib=None):
+    """a2 [T, K] @ w^T for a weight w [N, K]: tcgen05 3xTF32 (fp32-accurate)
+    for fp32 activations at >= 4k tokens, else the library GEMM (`lib`,
+    default _mm)."""
+    if _tc_ok(a2, a2.shape[1], w.shape[0]) and w.dtype == torch.float32:
+        return ops.gemm_f32(a2.contiguous(), w.contiguous())
+    return (lib or _mm)(a2, w.T)
+
+
+def _proj_acc(acc, a2, w):
+    """acc + a2 @ w^T (acc [T, N] fp32, consumed): the add rides the GEMM epilogue."""
+    if _tc_ok(a2, a2.shape[1], w.shape[0]) and w.dtype == torch.float32 and acc.dtype == torch.float32:
+        return ops.gemm_f32(a2.contiguous(), w.contiguous(), Cin=acc.contiguous(), beta=1.0)
+    return acc + a2 @ w.T
+
+
+def _wgrad(g2, a2):
+    """g2^T @ a2 (token-summed weight gradient): the split-K tcgen05 TN GEMM
+    with its fixed-order partial sum, else the library GEMM."""
+    if _tc_ok(g2, g2.shape[1], a2.shape[1]) and a2.dtype == torch.float32 and min(g2.shape[1], a2.shape[1]) >= 32:
+        return ops.gemm_f32_tn(g2.contiguous(), a2.contiguous())
+    return g2.T @ a2
+
+
 def _mm(a, b):
     """Projection GEMM (cuBLAS).  bf16 activations multiply bf16-cast weights
     with fp32 accumulation AND fp32 output, so the scan sees unrounded
@@ -791,10 +822,10 @@ class S6(LinearRecurrence):
         B, L, m = u.shape
         n = self.d_state
         u2 = u.reshape(B * L, m)
-        p1 = _mm(u2, self.W_delta)
-        pre = (p1 @ self.W_delta_proj).reshape(B, L, m)
-        Bk = _mm(u2, self.W_B.T).reshape(B, L, n)
-        Ck = _mm(u2, self.W_C.T).reshape(B, L, n)
+        p1 = _proj(u2, self.W_delta.T)
+        pre = _proj(p1, self.W_delta_proj.T).reshape(B, L, m)
+        Bk = _proj(u2, self.W_B).reshape(B, L, n)
+        Ck = _proj(u2, self.W_C).reshape(B, L, n)
         y, ckpt = ops.s6_scan_fwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D)
         saved = {"u": u, "p1": p1, "pre": pre, "Bk": Bk, "Ck": Ck, "ckpt": ckpt} if keep else {}
         return y, saved, ckpt[:, -1]
@@ -826,10 +857,13 @@ class S6(LinearRecurrence):
         u2 = u.reshape(B * L, m).to(c)
         gpre2 = r["gpre"].reshape(B * L, m)
         gBk, gCk = r["gBk"].reshape(B * L, n), r["gCk"].reshape(B * L, n)
-        gp1 = gpre2 @ self.W_delta_proj.T
-        gu = (r["gu_local"].reshape(B * L, m).to(c) + gp1 @ self.W_delta.T + gBk @ self.W_B + gCk @ self.W_C)
-        grads = {"a_log": r["ga_log"], "W_B": gBk.T @ u2, "W_C": gCk.T @ u2, "W_delta": u2.T @ gp1,
-                 "W_delta_proj": p1.to(c).T @ gpre2, "b_delta": r["gb_delta"], "D": r["gD"]}
+        gp1 = _proj(gpre2, self.W_delta_proj)
+        gu = r["gu_local"].reshape(B * L, m).to(c)
+        gu = _proj_acc(gu, gp1, self.W_delta)
+        gu = _proj_acc(gu, gBk, self.W_B.T)
+        gu = _proj_acc(gu, gCk, self.W_C.T)
+        grads = {"a_log": r["ga_log"], "W_B": _wgrad(gBk, u2), "W_C": _wgrad(gCk, u2), "W_delta": _wgrad(u2, gp1),
+                 "W_delta_proj": _wgrad(p1.to(c), gpre2), "b_delta": r["gb_delta"], "D": r["gD"]}
         return self._out(grads, gu.reshape(B, L, m).to(self.io_dtype), host)
 
 
@@ -868,8 +902,8 @@ class RGLRU(LinearRecurrence):
     def _forward(self, u, deltas, keep):
         B, L, W = u.shape
         u2 = u.reshape(B * L, W)
-        qr = (u2 @ self._w(self.W_r).T).reshape(B, L, W)
-        qi = (u2 @ self._w(self.W_i).T).reshape(B, L, W)
+        qr = _proj(u2, self._w(self.W_r), torch.matmul).reshape(B, L, W)
+        qi = _proj(u2, self._w(self.W_i), torch.matmul).reshape(B, L, W)
         y, ckpt = ops.rglru_scan_fwd(u, qr, qi, self.lambda_param, self.b_r, self.b_i)
         saved = {"u": u, "qr": qr, "qi": qi, "ckpt": ckpt, "y": y} if keep else {}
         return y, saved, y[:, -1].to(self.tdt)
@@ -896,9 +930,10 @@ class RGLRU(LinearRecurrence):
         c = self.tdt
         u2 = u.reshape(B * L, W).to(c)
         gqr2, gqi2 = r["gqr"].reshape(B * L, W).to(c), r["gqi"].reshape(B * L, W).to(c)
-        gu = r["gu_local"].reshape(B * L, W).to(c) + gqr2 @ self.W_r + gqi2 @ self.W_i
-        grads = {"lambda_param": sigmoid(-self.lambda_param) * r["gla"], "W_r": gqr2.T @ u2, "b_r": r["gb_r"],
-                 "W_i": gqi2.T @ u2, "b_i": r["gb_i"]}
+        gu = _proj_acc(r["gu_local"].reshape(B * L, W).to(c), gqr2, self.W_r.T)
+        gu = _proj_acc(gu, gqi2, self.W_i.T)
+        grads = {"lambda_param": sigmoid(-self.lambda_param) * r["gla"], "W_r": _wgrad(gqr2, u2), "b_r": r["gb_r"],
+                 "W_i": _wgrad(gqi2, u2), "b_i": r["gb_i"]}
         return self._out(grads, gu.reshape(B, L, W).to(self.io_dtype), host)
 
 

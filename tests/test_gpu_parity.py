@@ -96,6 +96,7 @@ def test_modes_agree_bitwise_and_runs_are_deterministic(lrx):
     ("rglru", 200, None, 3, 1111), ("rglru", 7, None, 1, 1), ("rglru", 130, None, 2, 33),
     ("s5", 64, 128, 2, 1024), ("s5", 10, 6, 3, 2), ("lru", 128, 64, 2, 1024), ("lru", 5, 3, 1, 17),
     ("lru", 128, 64, 8, 1024), ("s5", 64, 128, 4, 1100),  # >= 4096 tokens: tcgen05 projections
+    ("rglru", 64, None, 2, 2100), ("s6", 256, 16, 2, 2100),
     ("s4d", 6, 10, 2, 300),
 ])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
