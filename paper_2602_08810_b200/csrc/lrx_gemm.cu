@@ -691,7 +691,12 @@ static TNPlan tn_plan(int64_t M, int64_t N, int64_t K) {
     p.MT = getenv("LRX_GEMM_TN_MT2") && M > BM ? 2 : 1;
     const int64_t tiles = cdiv(M, BM * p.MT) * cdiv(N, p.BN);
     const int64_t nk = cdiv(K, BKN);
-    int64_t ks = std::max<int64_t>(1, std::min<int64_t>(cdiv(2 * 148, tiles), nk / 4 > 0 ? nk / 4 : 1));
+    // split-K CTAs over the GPU: one wave (measured 256x256x131072: 148 CTAs
+    // 104 us, 296 136 us, 592 194 us: each extra wave re-pays the pipeline
+    // fill and writes more partial tiles)
+    const char* ew = getenv("LRX_GEMM_TN_CTAS");
+    const int64_t ctas = ew ? std::max(1, atoi(ew)) : 148;
+    int64_t ks = std::max<int64_t>(1, std::min<int64_t>(cdiv(ctas, tiles), nk / 4 > 0 ? nk / 4 : 1));
     p.kb_per_split = (int)cdiv(nk, ks);
     p.ks = (int)cdiv(nk, p.kb_per_split);
     return p;
