@@ -11,7 +11,7 @@ from .scan import (MIN_CHUNK_LEN, StepState, combine, identity_element, init_ste
                    scan_sequential, step)
 from .autograd import (FiniteDiffReport, GradBundle, RecomputeTape, Tape, TapeConsumed, check_layer_gradients,
                        finite_diff_check, layer_backward, scan_backward, scan_forward, scheme_partials)
-from .layers import (LAYER_KINDS, LRU, RGLRU, S4D, S5, S6, SCHEMES_BY_KIND, LayerConfig, LayerStepState,
+from .layers import (LAYER_KINDS, LRU, RGLRU, S4D, S5, S6, SCHEMES_BY_KIND, LayerConfig, LayerStepState, StepGraph,
                      LinearRecurrence, UnknownLayer, init_layer, layer_step, lti_forward, ltv_forward, make_layer)
 
 __version__ = "0.1.0"

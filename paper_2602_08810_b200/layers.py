@@ -79,6 +79,60 @@ class LayerStepState:
         self.coef = {}
 
 
+class StepGraph:
+    """Graph-captured decode (the reference's generation
+    loop calls Layer.step per token, model.py:512-573): the whole per-token
+    step of one layer -- input projections, the fused lrx step kernel, the
+    readout -- is captured once into a CUDA graph over static input / output
+    buffers and replayed per token, so a token costs one graph launch instead
+    of 3-6 kernel launches from the host.  The state is updated in place,
+    exactly as by Layer.step (same kernels, same results).
+
+        g = layer.step_graph(state)          # or StepGraph(layer, state)
+        y_k = g.step(u_k)                    # [batch, d_model] CUDA tensor
+        ys = g.run(u_seq)                    # [batch, T, d_model]
+
+    `y_k` is the graph's static output buffer: clone it to keep it past the
+    next step.  Per-step deltas (asynchronous dirac layers) are not captured."""
+
+    def __init__(self, layer, state, warmup: int = 2):
+        if layer.device.type != "cuda":
+            raise RuntimeError("StepGraph needs a CUDA layer")
+        self.layer, self.state = layer, state
+        self.u = torch.zeros((state.batch, layer.d_model), dtype=layer.io_dtype, device=layer.device)
+        x0 = state.x.clone()
+        cur = torch.cuda.current_stream()
+        side = torch.cuda.Stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):  # library handles / workspaces before capture
+            for _ in range(warmup):
+                layer._step(state, self.u, None)
+        cur.wait_stream(side)
+        state.x.copy_(x0)  # warm-up steps leave no trace
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.y = layer._step(state, self.u, None)
+
+    def step(self, u_k):
+        """One token: u_k [batch, d_model] (device or host array) -> y_k."""
+        u_k = u_k if isinstance(u_k, torch.Tensor) else torch.as_tensor(np.asarray(u_k))
+        if tuple(u_k.shape) != tuple(self.u.shape):
+            raise ShapeError(f"u_k shape {tuple(u_k.shape)} does not match {tuple(self.u.shape)}")
+        self.u.copy_(u_k, non_blocking=True)
+        self.graph.replay()
+        self.state.k += 1
+        return self.y
+
+    def run(self, u_seq):
+        """Feed u_seq [batch, T, d_model] token by token; returns y [batch, T, d_model]."""
+        u_seq = u_seq if isinstance(u_seq, torch.Tensor) else torch.as_tensor(np.asarray(u_seq))
+        u_seq = u_seq.to(self.layer.device)
+        out = torch.empty(u_seq.shape, dtype=self.y.dtype, device=self.layer.device)
+        for t in range(u_seq.shape[1]):
+            out[:, t].copy_(self.step(u_seq[:, t]))
+        return out
+
+
 def _device(device=None):
     if device is not None:
         return torch.device(device)
@@ -247,6 +301,10 @@ class LinearRecurrence:
         state.k += 1
         out = y.cpu().numpy() if host else y
         return (out[0] if squeeze else out), state
+
+    def step_graph(self, state) -> "StepGraph":
+        """A CUDA-graph-captured per-token step bound to `state` (StepGraph)."""
+        return StepGraph(self, state)
 
     def _zero_state(self, batch):
         raise NotImplementedError

@@ -482,6 +482,30 @@ def test_step_matches_forward(lrx, kind, n, dtype):
         assert rel(yk, ref[:, k]) < tol
 
 
+@pytest.mark.parametrize("kind,n", STEP_KINDS)
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_step_graph_matches_eager_steps(lrx, kind, n, dtype):
+    """StepGraph (CUDA-graph decode) gives the eager step's bits and the
+    forward's values; prefill via forward(return_state=True) then decode."""
+    if dtype == "bf16" and kind not in ("s6", "rglru"):
+        pytest.skip("bf16 I/O exists for S6 / RG-LRU only")
+    m, B, L = 32, 3, 24
+    layer = lrx.make_layer(kind, m, n, dtype=dtype, seed=45)
+    u = torch.from_numpy(port.Rng(46).normal((B, L, m))).to("cuda", layer.io_dtype)
+    ref = layer.forward(u).float().cpu().numpy()
+    st_e, st_g = layer.init_state(B), layer.init_state(B)
+    g = layer.step_graph(st_g)
+    for k in range(L):
+        ye, st_e = layer.step(st_e, u[:, k])
+        yg = g.step(u[:, k])
+        assert torch.equal(ye, yg), k
+        assert rel(yg.float(), ref[:, k]) < TOL[dtype]
+    assert st_g.k == L and torch.equal(st_e.x, st_g.x)
+    _, st2 = layer.forward(u[:, :L // 2], return_state=True)
+    ys = layer.step_graph(st2).run(u[:, L // 2:])
+    assert rel(ys.float(), ref[:, L // 2:]) < TOL[dtype]
+
+
 @pytest.mark.parametrize("kind", ["s6", "rglru"])
 def test_step_bf16_and_device_tensors(lrx, kind):
     m, B, L = 64, 2, 50
