@@ -220,6 +220,12 @@ int lrx_s6_step(int io_dtype, void* x, const void* u, const void* pre, const voi
 /* RG-LRU: x[B,W] compute precision; u, qr, qi, y io dtype. */
 int lrx_rglru_step(int io_dtype, void* x, const void* u, const void* qr, const void* qi, const void* lambda_param,
                    const void* b_r, const void* b_i, void* y, int64_t B, int64_t W, void* stream);
+/* RG-LRU token in one kernel: the gate GEMVs qr = u W_r^T, qi = u W_i^T
+ * (fp32 weights [W, W]) fused with the update; batch <= 16, W % 8 == 0,
+ * f32 / bf16 I/O (LRX_ERR_UNSUPPORTED otherwise: use lrx_rglru_step). */
+int lrx_rglru_step_fused(int io_dtype, void* x, const void* u, const void* W_r, const void* W_i,
+                         const void* lambda_param, const void* b_r, const void* b_i, void* y, int64_t B, int64_t W,
+                         void* stream);
 
 /* ------------------------------------------------------------------------ *
  * fp32 GEMM on the tcgen05 tensor cores with the 3xTF32 split (the dense

@@ -5,8 +5,11 @@
 // GEMVs and an elementwise update, so each kernel fuses its GEMV with the
 // state update (warp per output row, lanes over the contraction, shuffle
 // reduction) and no kernel allocates.
+#include <algorithm>
+
 #include "lrx_common.cuh"
 #include "lrx_host.h"
+#include "lrx_tma.cuh"
 
 namespace lrx {
 namespace step {
@@ -121,6 +124,105 @@ __global__ void rglru_step_kernel(C* __restrict__ x, const IO* __restrict__ u, c
     const C xv = a * x[i] + (s * ig) * uk;
     x[i] = xv;
     st_io(y + i, xv);
+}
+
+// RG-LRU token in ONE kernel (fp32 gate weights, batch <= 16): the two gate
+// GEMVs qr = u W_r^T, qi = u W_i^T (layers.py:1213-1214) and the gated update.
+// The batch's u rows land in shared memory with one bulk copy; each warp owns
+// CPW = 2 channels and streams their rows of W_r and W_i (16-byte loads, 4
+// rows x 4 iterations in flight per lane), butterfly-reduces the dot
+// products and lane b applies the update of (b, w).  Bound: reading the
+// weights once per token (2 W^2 fp32).
+constexpr int kCPW = 2;
+
+template <typename IO, int BM>
+__global__ void __launch_bounds__(256) rglru_step_fused_kernel(float* __restrict__ x, const IO* __restrict__ u,
+                                                               const float* __restrict__ Wr,
+                                                               const float* __restrict__ Wi,
+                                                               const float* __restrict__ lam,
+                                                               const float* __restrict__ b_r,
+                                                               const float* __restrict__ b_i, IO* __restrict__ y,
+                                                               int Bn, int W) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    const IO* us = reinterpret_cast<const IO*>(smem + 128);  // [Bn][W]
+    if (threadIdx.x == 0) {
+        tma::mbar_init(bar, 1);
+        tma::fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)Bn * W * sizeof(IO);
+        tma::mbar_arrive_expect_tx(bar, bytes);
+        tma::load_1d(smem + 128, u, bytes, bar);
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int w0 = (blockIdx.x * 8 + warp) * kCPW;
+    if (w0 >= W) return;  // (after the copy is issued: thread 0 is in warp 0)
+    float ar[kCPW][BM], ai[kCPW][BM];
+#pragma unroll
+    for (int c = 0; c < kCPW; ++c)
+#pragma unroll
+        for (int b = 0; b < BM; ++b) ar[c][b] = ai[c][b] = 0.f;
+    const float4* wr[kCPW];
+    const float4* wi[kCPW];
+#pragma unroll
+    for (int c = 0; c < kCPW; ++c) {
+        const int w = min(w0 + c, W - 1);
+        wr[c] = reinterpret_cast<const float4*>(Wr + (int64_t)w * W);
+        wi[c] = reinterpret_cast<const float4*>(Wi + (int64_t)w * W);
+    }
+    tma::mbar_wait(bar, 0);
+#pragma unroll 4
+    for (int k4 = lane; k4 < W / 4; k4 += 32) {
+        float4 r4[kCPW], i4[kCPW];
+#pragma unroll
+        for (int c = 0; c < kCPW; ++c) r4[c] = __ldcs(wr[c] + k4), i4[c] = __ldcs(wi[c] + k4);
+#pragma unroll
+        for (int b = 0; b < BM; ++b) {
+            if (b < Bn) {
+                float4 u4;
+                if constexpr (sizeof(IO) == 4) {
+                    u4 = reinterpret_cast<const float4*>(us + b * W)[k4];
+                } else {
+                    const uint2 h = reinterpret_cast<const uint2*>(us + b * W)[k4];
+                    u4.x = __uint_as_float(h.x << 16), u4.y = __uint_as_float(h.x & 0xFFFF0000u);
+                    u4.z = __uint_as_float(h.y << 16), u4.w = __uint_as_float(h.y & 0xFFFF0000u);
+                }
+#pragma unroll
+                for (int c = 0; c < kCPW; ++c) {
+                    ar[c][b] += r4[c].x * u4.x + r4[c].y * u4.y + r4[c].z * u4.z + r4[c].w * u4.w;
+                    ai[c][b] += i4[c].x * u4.x + i4[c].y * u4.y + i4[c].z * u4.z + i4[c].w * u4.w;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < kCPW; ++c) {
+        float qr = 0.f, qi = 0.f;
+#pragma unroll
+        for (int b = 0; b < BM; ++b) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                ar[c][b] += __shfl_xor_sync(0xffffffffu, ar[c][b], o);
+                ai[c][b] += __shfl_xor_sync(0xffffffffu, ai[c][b], o);
+            }
+            if (lane == b) qr = ar[c][b], qi = ai[c][b];
+        }
+        const int w = w0 + c;
+        if (lane < Bn && w < W) {
+            const int64_t i = (int64_t)lane * W + w;
+            const float uk = float(cvt(us[lane * W + w]));
+            const float r = Math<float>::sigmoid(qr + b_r[w]);
+            const float ig = Math<float>::sigmoid(qi + b_i[w]);
+            const float loga = (8.f * r) * (-Math<float>::softplus(-lam[w]));  // GATE_POWER 8
+            const float a = Math<float>::exp(loga);
+            const float s = Math<float>::sqrt(-Math<float>::expm1(2.f * loga));
+            const float xv = a * x[i] + (s * ig) * uk;
+            x[i] = xv;
+            st_io(y + i, xv);
+        }
+    }
 }
 
 static unsigned warps_grid(int64_t rows, int wpb) { return (unsigned)cdiv(rows, wpb); }
@@ -264,6 +366,47 @@ int lrx_rglru_step(int io_dtype, void* x, const void* u, const void* qr, const v
         default: set_error("rglru step: unsupported io dtype %d", io_dtype); return LRX_ERR_VALUE;
     }
     return launched("lrx_rglru_step");
+}
+
+int lrx_rglru_step_fused(int io_dtype, void* x, const void* u, const void* W_r, const void* W_i,
+                         const void* lambda_param, const void* b_r, const void* b_i, void* y, int64_t B, int64_t W,
+                         void* stream) {
+    LRX_REQUIRE(B >= 1 && W >= 1, LRX_ERR_SHAPE, "bad extents");
+    const size_t esz = io_dtype == LRX_BF16 ? 2 : 4;
+    const size_t smem = 128 + (size_t)B * W * esz;
+    LRX_REQUIRE(B <= 16 && W % 8 == 0 && smem <= 200 * 1024 && (io_dtype == LRX_F32 || io_dtype == LRX_BF16) &&
+                    (reinterpret_cast<uintptr_t>(u) & 15) == 0,
+                LRX_ERR_UNSUPPORTED, "rglru fused step: batch <= 16, width %% 8 == 0, f32 / bf16 I/O");
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    (void)sms;
+    const unsigned g = (unsigned)cdiv(W, 8 * step::kCPW);
+#define LRX_RG_FUSED(IO_, BM_)                                                                                  \
+    do {                                                                                                        \
+        auto k = step::rglru_step_fused_kernel<IO_, BM_>;                                                      \
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) { \
+            set_error("rglru fused step: cannot reserve %zu B of shared memory", smem);                         \
+            return LRX_ERR_CUDA;                                                                               \
+        }                                                                                                       \
+        k<<<g, 256, smem, st>>>((float*)x, (const IO_*)u, (const float*)W_r, (const float*)W_i,                 \
+                                (const float*)lambda_param, (const float*)b_r, (const float*)b_i, (IO_*)y, (int)B, \
+                                (int)W);                                                                        \
+    } while (0)
+#define LRX_RG_FUSED_B(IO_)                \
+    do {                                   \
+        if (B <= 1) LRX_RG_FUSED(IO_, 1);  \
+        else if (B <= 2) LRX_RG_FUSED(IO_, 2);  \
+        else if (B <= 4) LRX_RG_FUSED(IO_, 4);  \
+        else if (B <= 8) LRX_RG_FUSED(IO_, 8);  \
+        else LRX_RG_FUSED(IO_, 16);        \
+    } while (0)
+    if (io_dtype == LRX_F32) LRX_RG_FUSED_B(float);
+    else LRX_RG_FUSED_B(__nv_bfloat16);
+#undef LRX_RG_FUSED_B
+#undef LRX_RG_FUSED
+    return launched("lrx_rglru_step_fused");
 }
 
 }  // extern "C"

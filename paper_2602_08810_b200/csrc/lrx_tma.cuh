@@ -86,6 +86,14 @@ __device__ __forceinline__ void store_3d(const CUtensorMap* m, const void* src, 
                  "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
                  : "memory");
 }
+// 1D bulk copy global -> shared (bytes % 16 == 0, 16-byte aligned), completion on bar.
+__device__ __forceinline__ void load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // 2D tile store smem -> global (bulk group); out-of-bounds parts clipped.
 __device__ __forceinline__ void store_2d(const CUtensorMap* m, const void* src, int c0, int r0) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(

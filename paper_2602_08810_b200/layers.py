@@ -971,6 +971,15 @@ class RGLRU(LinearRecurrence):
         return torch.zeros((batch, self.d_model), dtype=self.tdt, device=self.device)
 
     def _step(self, st, uk, delta_k):
+        if self.tdt == torch.float32 and st.batch <= 16 and self.d_model % 8 == 0 and \
+                st.batch * self.d_model * 4 <= 190 * 1024:
+            # gate GEMVs + update in one kernel (fp32 weights read once per token)
+            y = torch.empty((st.batch, self.d_model), dtype=self.io_dtype, device=self.device)
+            _lib.check(_lib.lib().lrx_rglru_step_fused(
+                _lib.code_of(self.io_dtype), _lib.ptr(st.x), _lib.ptr(uk), _lib.ptr(self.W_r), _lib.ptr(self.W_i),
+                _lib.ptr(self.lambda_param), _lib.ptr(self.b_r), _lib.ptr(self.b_i), _lib.ptr(y), st.batch,
+                self.d_model, _lib.stream()))
+            return y
         qr = (uk @ self._w(self.W_r).T).contiguous()
         qi = (uk @ self._w(self.W_i).T).contiguous()
         y = torch.empty((st.batch, self.d_model), dtype=self.io_dtype, device=self.device)
