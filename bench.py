@@ -575,9 +575,17 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # LRX_BENCH_ONE_GPU=1 (test hook): every rank on cuda:0 over gloo, to
+    # exercise the multi-rank plumbing on a single-GPU box (timings meaningless)
+    one_gpu = os.environ.get("LRX_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
     torch.cuda.set_device(device)
     r = run_gpu(args, w, rank, world, device)
