@@ -697,6 +697,17 @@ static TNPlan tn_plan(int64_t M, int64_t N, int64_t K) {
     const char* ew = getenv("LRX_GEMM_TN_CTAS");
     const int64_t ctas = ew ? std::max(1, atoi(ew)) : 148;
     int64_t ks = std::max<int64_t>(1, std::min<int64_t>(cdiv(ctas, tiles), nk / 4 > 0 ? nk / 4 : 1));
+    if (!ew && tiles >= ctas) {
+        // more tiles than SMs: pick the split (1..4) with the least wave
+        // quantisation (2560 x 2560 outputs = 200 tiles: ks 2 fills 90% of 3 waves
+        // where ks 1 fills 68% of 2)
+        double best = 0;
+        for (int64_t k = 1; k <= 4 && k <= std::max<int64_t>(1, nk / 4); ++k) {
+            const int64_t n = tiles * k;
+            const double eff = (double)n / (double)(cdiv(n, ctas) * ctas);
+            if (eff > best + 0.02) best = eff, ks = k;
+        }
+    }
     p.kb_per_split = (int)cdiv(nk, ks);
     p.ks = (int)cdiv(nk, p.kb_per_split);
     return p;
