@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
 // 512 B (SBO); the next 32-wide MN chunk is the next box, 4 KB on (LBO).  One
 // UMMA k-step of 8 tf32 rows = two atoms: advance the start address by 1 KB.
 constexpr int BKN = 16;  // K-block (rows) of the TN kernel: boxes of 16 rows x 128 B
+constexpr int kMaxSpan = 4096;  // K rows one TN CTA accumulates in TMEM (see tn_plan)
 constexpr int THREADS_TN = 320;  // TMA, MMA, 8 split warps (the first 4 also run the epilogue)
 
 __device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr) {
@@ -697,6 +698,10 @@ static TNPlan tn_plan(int64_t M, int64_t N, int64_t K) {
     const char* ew = getenv("LRX_GEMM_TN_CTAS");
     const int64_t ctas = ew ? std::max(1, atoi(ew)) : 148;
     int64_t ks = std::max<int64_t>(1, std::min<int64_t>(cdiv(ctas, tiles), nk / 4 > 0 ? nk / 4 : 1));
+    // accuracy: the tensor core's fp32 accumulation is not round-to-nearest;
+    // its error grows ~6e-8 per accumulated 8-row MMA step, so one CTA spans
+    // at most kMaxSpan rows of K (3e-5) and longer sums split further
+    const int64_t ks_acc = cdiv(nk * BKN, (int64_t)kMaxSpan);
     if (!ew && tiles >= ctas) {
         // more tiles than SMs: pick the split (1..4) with the least wave
         // quantisation (2560 x 2560 outputs = 200 tiles: ks 2 fills 90% of 3 waves
@@ -708,6 +713,7 @@ static TNPlan tn_plan(int64_t M, int64_t N, int64_t K) {
             if (eff > best + 0.02) best = eff, ks = k;
         }
     }
+    ks = std::max(ks, std::min(ks_acc, nk));
     p.kb_per_split = (int)cdiv(nk, ks);
     p.ks = (int)cdiv(nk, p.kb_per_split);
     return p;
@@ -743,7 +749,9 @@ int lrx_gemm_f32(const void* A, const void* Bt, const void* Bt_lo, void* C, cons
                  int64_t M, int64_t N, int64_t K, float alpha, float beta, void* stream) {
     LRX_REQUIRE(M >= 1 && N >= 1 && K >= 1, LRX_ERR_SHAPE, "gemm: bad extents M=%lld N=%lld K=%lld", (long long)M,
                 (long long)N, (long long)K);
-    LRX_REQUIRE(M < (1ll << 31) && N <= (1 << 16) && K < (1 << 24), LRX_ERR_UNSUPPORTED, "gemm: extents too large");
+    // K <= 8192: the whole K is accumulated in TMEM (not round-to-nearest:
+    // ~6e-8 per 8-wide step, 6e-5 at the cap); longer sums go to the library
+    LRX_REQUIRE(M < (1ll << 31) && N <= (1 << 16) && K <= 8192, LRX_ERR_UNSUPPORTED, "gemm: extents too large");
     cudaStream_t st = (cudaStream_t)stream;
     const float *a = (const float*)A, *b = (const float*)Bt, *bl = (const float*)Bt_lo;
     if (N <= 64) return gemm::launch<64>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K, alpha,

@@ -150,9 +150,10 @@ def _log_delta_init(rng, shape, dt):
 
 def _tc_ok(a, *dims):
     """The tcgen05 3xTF32 GEMMs take fp32 operands with 16-byte rows and enough
-    tokens to fill the GPU (see _MIMOBase._tc)."""
+    tokens to fill the GPU (see _MIMOBase._tc); the reduction width of the
+    NT GEMM (dims[0]) is capped at 8192 (TMEM accumulation, lrx_gemm.cu)."""
     return (a.dtype == torch.float32 and a.is_cuda and a.shape[0] >= _TC_MIN_TOKENS
-            and all(d % 4 == 0 and d >= 16 for d in dims))
+            and all(d % 4 == 0 and d >= 16 for d in dims) and dims[0] <= 8192)
 
 
 def _proj(a2, w, lib=None):
@@ -174,7 +175,8 @@ def _proj_acc(acc, a2, w):
 def _wgrad(g2, a2):
     """g2^T @ a2 (token-summed weight gradient): the split-K tcgen05 TN GEMM
     with its fixed-order partial sum, else the library GEMM."""
-    if _tc_ok(g2, g2.shape[1], a2.shape[1]) and a2.dtype == torch.float32 and min(g2.shape[1], a2.shape[1]) >= 32:
+    if (_tc_ok(g2, g2.shape[1], a2.shape[1]) and a2.dtype == torch.float32 and min(g2.shape[1], a2.shape[1]) >= 32
+            and g2.shape[1] * a2.shape[1] * max(1, g2.shape[0] // 4096) <= (1 << 31)):  # split-K partials <= 8 GB
         return ops.gemm_f32_tn(g2.contiguous(), a2.contiguous())
     return g2.T @ a2
 
@@ -583,7 +585,7 @@ class _MIMOBase(LinearRecurrence):
         there are enough tokens T (>= 4096, measured: C1 LRU 8k tokens 0.18 ->
         0.15 ms per step on them; at 1k tokens cuBLAS wins); f64 layers, odd
         widths and tiny batches use the library (cuBLAS) GEMM."""
-        return self.tdt == torch.float32 and K % 4 == 0 and T >= _TC_MIN_TOKENS
+        return self.tdt == torch.float32 and K % 4 == 0 and K <= 8192 and T >= _TC_MIN_TOKENS
 
     def _forward(self, u, deltas, keep):
         if self._fused(deltas):

@@ -378,7 +378,7 @@ def test_gemm_f32_tcgen05_matches_f64(lrx, M, N, K):
 
 
 @pytest.mark.parametrize("K,M,N", [(4096, 256, 256), (131072, 256, 256), (1000, 128, 64), (77, 64, 192),
-                                   (8192, 128, 128)])
+                                   (8192, 128, 128), (1 << 20, 64, 64)])
 def test_gemm_f32_tn_tcgen05_matches_f64(lrx, K, M, N):
     from paper_2602_08810_b200 import ops
     g = torch.Generator(device="cuda").manual_seed(K + M + N)
