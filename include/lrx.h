@@ -261,7 +261,7 @@ int lrx_mimo_fwd(int dtype, const void* abar, const void* scale, const void* bu,
  *   gabar_part[c, b*P+p] = sum_{k in chunk c} g_k conj(x_{k-1})
  *   gscale_part[c, b*P+p] = sum_{k in chunk c} conj(bu_k) g_k
  * (reduce the [n_chunks*B, P] partials with lrx_reduce_rows). */
-int lrx_mimo_chunking(int dtype, int64_t L, int64_t* chunk_len, int64_t* n_chunks);
+int lrx_mimo_chunking(int dtype, int64_t B, int64_t L, int64_t P, int64_t* chunk_len, int64_t* n_chunks);
 size_t lrx_mimo_bwd_workspace_bytes(int dtype, int64_t B, int64_t L, int64_t P);
 int lrx_mimo_bwd(int dtype, const void* abar, const void* scale, const void* bu, const void* x,
                  const void* gx, void* gbu, void* gabar_part, void* gscale_part, int64_t B, int64_t L,

@@ -43,7 +43,7 @@ SIGNATURES = {
                         _vp, _i64, _i64, _i64, _i64, _vp, _i64, _i, _vp]),
     "lrx_s6_fwd_carry": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp]),
     "lrx_s6_bwd_carry": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp]),
-    "lrx_mimo_chunking": (_i, [_i, _i64, _P64, _P64]),
+    "lrx_mimo_chunking": (_i, [_i, _i64, _i64, _i64, _P64, _P64]),
     "lrx_mimo_workspace_bytes": (_sz, [_i, _i64, _i64, _i64]),
     "lrx_mimo_fwd": (_i, [_i, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp]),
     "lrx_mimo_bwd_workspace_bytes": (_sz, [_i, _i64, _i64, _i64]),

@@ -13,6 +13,8 @@
 // two per-coefficient reductions sum_k g conj(x_{k-1}) (-> d abar) and
 // sum_k conj(bu_k) g_k (-> d scale) into the reverse pass, written as
 // per-chunk partials that lrx_reduce_rows folds in a fixed order.
+#include <stdlib.h>
+
 #include "lrx_common.cuh"
 #include "lrx_host.h"
 
@@ -47,7 +49,21 @@ template <> __device__ __forceinline__ void stc(cplx<double>* p, cplx<double> v)
 // step is one contiguous run of 32 complex values.  (The previous single-pass
 // anchored look-back serialised on a chain of anchor publications; here the
 // only serial work is the per-thread fold over <= S maps.)
-constexpr int kSeg = 128;  // steps per segment (= partial rows per batch row)
+constexpr int kSeg = 128;  // default steps per segment (= partial rows per batch row)
+
+// Segment length (a power of two, 16..128): shorter when the (b, p) lanes are
+// few, so lanes x segments keep ~64k threads in flight (C1: 512 lanes ->
+// 16-step segments; C2: 4096 lanes keep 128).  LRX_MIMO_SEG overrides.
+static int seg_len(int64_t B, int64_t L, int64_t P) {
+    if (const char* e = getenv("LRX_MIMO_SEG")) {
+        int v = atoi(e), s = 16;
+        while (s < v && s < 1024) s <<= 1;
+        return s;
+    }
+    int s = kSeg;
+    while (s > 16 && B * P * cdiv(L, (int64_t)s) < 65536) s >>= 1;
+    return s;
+}
 
 template <typename T> struct Unroll { static constexpr int K = 16; };
 template <> struct Unroll<double> { static constexpr int K = 8; };
@@ -62,7 +78,7 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads) fwd_agg_kernel(const cplx<T>* __restrict__ abar,
                                                            const cplx<T>* __restrict__ scale,
                                                            const cplx<T>* __restrict__ bu, cplx<T>* __restrict__ aggX,
-                                                           int64_t B, int64_t L, int64_t P) {
+                                                           int64_t B, int64_t L, int64_t P, int seg) {
     using V = cplx<T>;
     constexpr int K = Unroll<T>::K;
     const int64_t n_lanes = B * P;
@@ -71,9 +87,9 @@ __global__ void __launch_bounds__(kThreads) fwd_agg_kernel(const cplx<T>* __rest
     const int s = blockIdx.y;
     const int64_t b = lane / P, p = lane % P;
     const V ab = abar[p], sc = scale[p];
-    const cplx<T>* src = bu + (b * L + (int64_t)s * kSeg) * P + p;
+    const cplx<T>* src = bu + (b * L + (int64_t)s * seg) * P + p;
     V X = Traits<V>::zero();
-    for (int k0 = 0; k0 < kSeg; k0 += K) {  // full segments only (s < S-1)
+    for (int k0 = 0; k0 < seg; k0 += K) {  // full segments only (s < S-1)
         V v[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) v[k] = ldc(src + (int64_t)(k0 + k) * P);
@@ -88,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const cplx<T>* __restrict
                                                        const cplx<T>* __restrict__ scale,
                                                        const cplx<T>* __restrict__ bu,
                                                        const cplx<T>* __restrict__ aggX, cplx<T>* __restrict__ x,
-                                                       int64_t B, int64_t L, int64_t P) {
+                                                       int64_t B, int64_t L, int64_t P, int seg) {
     using V = cplx<T>;
     constexpr int K = Unroll<T>::K;
     const int64_t n_lanes = B * P;
@@ -99,11 +115,11 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const cplx<T>* __restrict
     const V ab = abar[p], sc = scale[p];
     V xs = Traits<V>::zero();
     if (s > 0) {
-        const V AS = cpow2k(ab, kSeg);
+        const V AS = cpow2k(ab, seg);
         for (int r = 0; r < s; ++r) xs = AS * xs + aggX[(int64_t)r * n_lanes + lane];
     }
-    const int64_t t0 = (int64_t)s * kSeg;
-    const int nt = (int)min((int64_t)kSeg, L - t0);
+    const int64_t t0 = (int64_t)s * seg;
+    const int nt = (int)min((int64_t)seg, L - t0);
     const int64_t base = (b * L + t0) * P + p;
     for (int k0 = 0; k0 < nt; k0 += K) {
         V v[K];
@@ -123,7 +139,7 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const cplx<T>* __restrict
 template <typename T>
 __global__ void __launch_bounds__(kThreads) bwd_agg_kernel(const cplx<T>* __restrict__ abar,
                                                            const cplx<T>* __restrict__ gx, cplx<T>* __restrict__ aggH,
-                                                           int64_t B, int64_t L, int64_t P) {
+                                                           int64_t B, int64_t L, int64_t P, int seg) {
     using V = cplx<T>;
     constexpr int K = Unroll<T>::K;
     const int64_t n_lanes = B * P;
@@ -132,8 +148,8 @@ __global__ void __launch_bounds__(kThreads) bwd_agg_kernel(const cplx<T>* __rest
     const int s = blockIdx.y + 1;  // segments 1 .. S-1
     const int64_t b = lane / P, p = lane % P;
     const V abc = conj(abar[p]);
-    const int64_t t0 = (int64_t)s * kSeg;
-    const int nt = (int)min((int64_t)kSeg, L - t0);
+    const int64_t t0 = (int64_t)s * seg;
+    const int nt = (int)min((int64_t)seg, L - t0);
     const int64_t base = (b * L + t0) * P + p;
     V h = Traits<V>::zero();
     for (int k1 = nt; k1 > 0; k1 -= K) {
@@ -155,7 +171,7 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const cplx<T>* __restrict
                                                        const cplx<T>* __restrict__ aggH, cplx<T>* __restrict__ gbu,
                                                        cplx<T>* __restrict__ gabar_part,
                                                        cplx<T>* __restrict__ gscale_part, int64_t B, int64_t L,
-                                                       int64_t P, int S) {
+                                                       int64_t P, int S, int seg) {
     using V = cplx<T>;
     constexpr int K = Unroll<T>::K / 2;
     const int64_t n_lanes = B * P;
@@ -167,11 +183,11 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const cplx<T>* __restrict
     const V abc = conj(ab), scc = conj(scale[p]);
     V h = Traits<V>::zero();
     if (s < S - 1) {
-        const V AS = cpow2k(abc, kSeg);
+        const V AS = cpow2k(abc, seg);
         for (int r = S - 1; r > s; --r) h = AS * h + aggH[(int64_t)r * n_lanes + lane];
     }
-    const int64_t t0 = (int64_t)s * kSeg;
-    const int nt = (int)min((int64_t)kSeg, L - t0);
+    const int64_t t0 = (int64_t)s * seg;
+    const int nt = (int)min((int64_t)seg, L - t0);
     const int64_t base = (b * L + t0) * P + p;
     V sa = Traits<V>::zero(), ss = Traits<V>::zero();
     for (int k1 = nt; k1 > 0; k1 -= K) {
@@ -203,44 +219,46 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const cplx<T>* __restrict
 
 template <typename T>
 static size_t ws_bytes(int64_t B, int64_t L, int64_t P) {
-    const int64_t S = cdiv(L, kSeg);
+    const int64_t S = cdiv(L, (int64_t)seg_len(B, L, P));
     return align_up((size_t)(S * B * P) * sizeof(cplx<T>));
 }
 
 template <typename T>
 static int fwd_t(const void* abar, const void* scale, const void* bu, void* x, int64_t B, int64_t L, int64_t P,
                  void* w, size_t wb, cudaStream_t st) {
-    const int64_t S = cdiv(L, kSeg), nb = cdiv(B * P, kThreads);
+    const int seg = seg_len(B, L, P);
+    const int64_t S = cdiv(L, (int64_t)seg), nb = cdiv(B * P, kThreads);
     LRX_REQUIRE(S <= 65535 && nb <= 0x7fffffff, LRX_ERR_UNSUPPORTED, "mimo: extents too large");
     LRX_REQUIRE(S == 1 || (w && wb >= ws_bytes<T>(B, L, P)), LRX_ERR_VALUE, "mimo workspace too small");
     cplx<T>* aggX = static_cast<cplx<T>*>(w);
     int n = 1;
     if (S > 1) {
         fwd_agg_kernel<T><<<dim3((unsigned)nb, (unsigned)(S - 1)), kThreads, 0, st>>>(
-            (const cplx<T>*)abar, (const cplx<T>*)scale, (const cplx<T>*)bu, aggX, B, L, P);
+            (const cplx<T>*)abar, (const cplx<T>*)scale, (const cplx<T>*)bu, aggX, B, L, P, seg);
         ++n;
     }
     fwd_kernel<T><<<dim3((unsigned)nb, (unsigned)S), kThreads, 0, st>>>(
-        (const cplx<T>*)abar, (const cplx<T>*)scale, (const cplx<T>*)bu, aggX, (cplx<T>*)x, B, L, P);
+        (const cplx<T>*)abar, (const cplx<T>*)scale, (const cplx<T>*)bu, aggX, (cplx<T>*)x, B, L, P, seg);
     return launched("lrx_mimo_fwd", n);
 }
 
 template <typename T>
 static int bwd_t(const void* abar, const void* scale, const void* bu, const void* x, const void* gx, void* gbu,
                  void* gap, void* gsp, int64_t B, int64_t L, int64_t P, void* w, size_t wb, cudaStream_t st) {
-    const int64_t S = cdiv(L, kSeg), nb = cdiv(B * P, kThreads);
+    const int seg = seg_len(B, L, P);
+    const int64_t S = cdiv(L, (int64_t)seg), nb = cdiv(B * P, kThreads);
     LRX_REQUIRE(S <= 65535 && nb <= 0x7fffffff, LRX_ERR_UNSUPPORTED, "mimo: extents too large");
     LRX_REQUIRE(S == 1 || (w && wb >= ws_bytes<T>(B, L, P)), LRX_ERR_VALUE, "mimo workspace too small");
     cplx<T>* aggH = static_cast<cplx<T>*>(w);
     int n = 1;
     if (S > 1) {
         bwd_agg_kernel<T><<<dim3((unsigned)nb, (unsigned)(S - 1)), kThreads, 0, st>>>((const cplx<T>*)abar,
-                                                                                     (const cplx<T>*)gx, aggH, B, L, P);
+                                                                                     (const cplx<T>*)gx, aggH, B, L, P, seg);
         ++n;
     }
     bwd_kernel<T><<<dim3((unsigned)nb, (unsigned)S), kThreads, 0, st>>>(
         (const cplx<T>*)abar, (const cplx<T>*)scale, (const cplx<T>*)bu, (const cplx<T>*)x, (const cplx<T>*)gx, aggH,
-        (cplx<T>*)gbu, (cplx<T>*)gap, (cplx<T>*)gsp, B, L, P, (int)S);
+        (cplx<T>*)gbu, (cplx<T>*)gap, (cplx<T>*)gsp, B, L, P, (int)S, seg);
     return launched("lrx_mimo_bwd", n);
 }
 
@@ -251,11 +269,12 @@ using namespace lrx;
 
 extern "C" {
 
-int lrx_mimo_chunking(int dtype, int64_t L, int64_t* chunk_len, int64_t* n_chunks) {
-    LRX_REQUIRE(L >= 1, LRX_ERR_SHAPE, "length must be >= 1");
+int lrx_mimo_chunking(int dtype, int64_t B, int64_t L, int64_t P, int64_t* chunk_len, int64_t* n_chunks) {
+    LRX_REQUIRE(B >= 1 && L >= 1 && P >= 1, LRX_ERR_SHAPE, "bad extents");
     (void)dtype;
-    *chunk_len = mimo::kSeg;  // partial rows = one per (segment, batch row)
-    *n_chunks = cdiv(L, mimo::kSeg);
+    const int seg = mimo::seg_len(B, L, P);
+    *chunk_len = seg;  // partial rows = one per (segment, batch row)
+    *n_chunks = cdiv(L, (int64_t)seg);
     return LRX_OK;
 }
 

@@ -229,7 +229,7 @@ def mimo_scan_bwd(abar, scale, bu, x, gx):
     lib = _lib.lib()
     code = _lib.code_of(x.dtype)
     ck, nc = _lib.i64(), _lib.i64()
-    _lib.check(lib.lrx_mimo_chunking(code, L, _lib.ref(ck), _lib.ref(nc)))
+    _lib.check(lib.lrx_mimo_chunking(code, B, L, P, _lib.ref(ck), _lib.ref(nc)))
     nc = nc.value
     gbu = torch.empty_like(x)
     gap = torch.empty(nc * B * P, dtype=x.dtype, device=x.device)

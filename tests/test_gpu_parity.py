@@ -395,6 +395,23 @@ def test_gemm_f32_tn_tcgen05_matches_f64(lrx, K, M, N):
     assert torch.equal(C, C2)  # deterministic split-K
 
 
+@pytest.mark.parametrize("seg", ["16", "128", "1024"])
+def test_mimo_segment_lengths_match_oracle(lrx, monkeypatch, seg):
+    """MIMO scans with forced segment lengths (LRX_MIMO_SEG; ragged last one)."""
+    monkeypatch.setenv("LRX_MIMO_SEG", seg)
+    layer = lrx.make_layer("s5", 16, 24, dtype="f32", seed=51)
+    u = port.Rng(52).normal((3, 1000, 16)).astype(np.float32)
+    gy = port.Rng(53).normal((3, 1000, 16)).astype(np.float32)
+    y, tape = layer.forward(u, tape=True)
+    g = lrx.layer_backward(layer, tape, gy)
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64("s5", layer.discretization, params, u, gy)
+    assert rel(y, ry) < TOL["f32"]
+    assert rel(g.u, rgu) < TOL["f32"]
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < TOL["f32"], (seg, k)
+
+
 @pytest.mark.parametrize("kind", ["s5", "lru"])
 def test_mimo_layer_on_tensor_cores_matches_oracle(lrx, kind):
     """B*L = 32768 tokens: the projections run on the tcgen05 3xTF32 GEMMs."""
