@@ -189,6 +189,21 @@ int lrx_s4d_step(int dtype, void* x, const void* abar, const void* w, const void
 int lrx_mimo_step(int dtype, void* x, const void* abar, const void* scale, const void* Bre, const void* Bim,
                   const void* Cre, const void* Cim, const void* D, const void* u, void* y, double out_scale,
                   int64_t B, int64_t P, int64_t H, void* stream);
+/* ---- S4D fused scan (layers.py:352-546), constant step ------------------------
+ * u, y, gy, gu [B, L, H] real (F32 / F64); abar, w (= scale b), c [H, N] complex
+ * of that precision; d [H].  N in {8, 16, 32, 64} (LRX_ERR_UNSUPPORTED
+ * otherwise: the generic operator path).  ckpt [B, n_chunks, H, N] complex =
+ * the state entering every chunk (lrx_s4d_chunking); xlast [B, H, N] (or
+ * NULL) = the final state.  Backward partials per
+ * batch row: gabar_part, gw_part, gc_part [B, H, N] complex (sum g conj(x_prev),
+ * sum u g, sum gy conj(x)), gd_part [B, H]; the caller sums over B. */
+int lrx_s4d_chunking(int64_t L, int64_t* chunk_len, int64_t* n_chunks);
+int lrx_s4d_fwd(int dtype, const void* u, const void* abar, const void* w, const void* c, const void* d, void* y,
+                void* ckpt, void* xlast, int64_t B, int64_t L, int64_t H, int64_t N, void* stream);
+int lrx_s4d_bwd(int dtype, const void* u, const void* gy, const void* abar, const void* w, const void* c,
+                const void* d, const void* ckpt, void* gu, void* gabar_part, void* gw_part, void* gc_part,
+                void* gd_part, int64_t B, int64_t L, int64_t H, int64_t N, void* stream);
+
 /* ---- MIMO LTI coefficient work (S5 / LRU), one launch each way ------------
  * Replaces the parameter-sized torch glue of S5._abar_scale / LRU._abar_scale
  * (layers.py:823-834, 936-943) and the coefficient + B/C gradient assembly of

@@ -411,7 +411,19 @@ class S4D(LinearRecurrence):
             abar, scale = scheme_factors(self.discretization, lam, deff[..., None])
         return lam, delta, b, abar, scale
 
+    def _fused(self, deltas):
+        """Fused S4D kernel (csrc/lrx_s4d.cu) for constant steps and d_state
+        in {8, 16, 32, 64}; per-step deltas keep the generic operator path."""
+        return deltas is None and self.d_state in ops.S4D_FUSED_N and os.environ.get("LRX_S4D_GENERIC") != "1"
+
     def _forward(self, u, deltas, keep):
+        if self._fused(deltas):
+            lam, delta, b, abar, scale = self._coeffs(None)
+            w = (scale * b).to(self.tcdt).contiguous()
+            c = torch.complex(self.c_re, self.c_im).contiguous()
+            y, ckpt, xlast = ops.s4d_scan_fwd(u, abar.to(self.tcdt).contiguous(), w, c, self.d.contiguous())
+            saved = {"u": u, "ckpt": ckpt, "deltas": None, "fused": True} if keep else {}
+            return y, saved, xlast
         B, L, m = u.shape
         n = self.d_state
         lam, delta, b, abar, scale = self._coeffs(deltas)
@@ -452,7 +464,30 @@ class S4D(LinearRecurrence):
                                            st.batch, self.d_model, self.d_state, _lib.stream()))
         return y
 
+    def _backward_fused(self, s, gy):
+        u, ckpt, host = s["u"], s["ckpt"], s["host"]
+        gy = self._gy(gy, u.shape)
+        lam, delta, b, abar, scale = self._coeffs(None)
+        w = (scale * b).to(self.tcdt).contiguous()
+        c = torch.complex(self.c_re, self.c_im).contiguous()
+        r = ops.s4d_scan_bwd(u, gy, abar.to(self.tcdt).contiguous(), w, c, self.d.contiguous(), ckpt)
+        c128 = torch.complex128
+        gabar, gpsi = r["gabar"].to(c128), r["gw"].to(c128)
+        gscale = b.conj() * gpsi
+        gb = scale.conj() * gpsi
+        dal, dad, dsl, dsd = scheme_partials(self.discretization, lam, delta[:, None], abar, scale)
+        glam = dal.conj() * gabar + dsl.conj() * gscale
+        gdel = ((dad.conj() * gabar).real + (dsd.conj() * gscale).real).sum(-1)
+        gc = r["gc"]
+        grads = {"lambda_re_log": -torch.exp(self.lambda_re_log.double()) * glam.real, "lambda_im": glam.imag,
+                 "b.re": gb.real, "b.im": gb.imag, "c.re": gc.real, "c.im": gc.imag, "d": r["gd"],
+                 "log_delta": gdel * delta}
+        grads = {k: v.to(self.tdt).contiguous() for k, v in grads.items()}
+        return self._out({k: grads[k] for k in self.parameters()}, r["gu"], host)
+
     def _backward(self, s, gy):
+        if s.get("fused"):
+            return self._backward_fused(s, gy)
         u, x2, deltas, host = s["u"], s["x2"], s["deltas"], s["host"]
         B, L, m = u.shape
         n = self.d_state

@@ -20,7 +20,8 @@ import torch
 from . import _lib
 
 __all__ = ["rglru_scan_fwd", "rglru_scan_bwd", "s6_geometry", "s6_scan_fwd", "s6_scan_bwd", "s6_fwd_carry",
-           "s6_bwd_carry", "mimo_scan_fwd", "mimo_scan_bwd", "reduce_rows", "gemm_f32", "gemm_f32_tn", "tf32_lo"]
+           "s6_bwd_carry", "mimo_scan_fwd", "mimo_scan_bwd", "reduce_rows", "gemm_f32", "gemm_f32_tn", "tf32_lo",
+           "s4d_scan_fwd", "s4d_scan_bwd", "S4D_FUSED_N"]
 
 
 def reduce_rows(part, rows, cols, other=None):
@@ -239,3 +240,40 @@ def mimo_scan_bwd(abar, scale, bu, x, gx):
                                 _lib.ptr(x), _lib.ptr(gx), _lib.ptr(gbu), _lib.ptr(gap), _lib.ptr(gsp), B, L, P,
                                 _lib.ptr(ws), ws.numel(), _lib.stream()))
     return gbu, reduce_rows(gap, nc * B, P), reduce_rows(gsp, nc * B, P)
+
+
+# ---------------------------------------------------------------------------
+# S4D (fused per-channel complex LTI scan)
+
+S4D_FUSED_N = (8, 16, 32, 64)
+
+
+def s4d_scan_fwd(u, abar, w, c, d):
+    """y = Re(sum_n c x) + d u with x_n = abar_n x_n + w_n u over u [B, L, H]
+    (real, f32/f64); abar, w, c [H, N] complex.  Returns (y, ckpt)."""
+    B, L, H = u.shape
+    N = abar.shape[-1]
+    ck, nc = _lib.i64(), _lib.i64()
+    _lib.check(_lib.lib().lrx_s4d_chunking(L, _lib.ref(ck), _lib.ref(nc)))
+    y = torch.empty_like(u)
+    ckpt = torch.empty((B, nc.value, H, N), dtype=abar.dtype, device=u.device)
+    xl = torch.empty((B, H, N), dtype=abar.dtype, device=u.device)
+    _lib.check(_lib.lib().lrx_s4d_fwd(_lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(abar), _lib.ptr(w), _lib.ptr(c),
+                                      _lib.ptr(d), _lib.ptr(y), _lib.ptr(ckpt), _lib.ptr(xl), B, L, H, N,
+                                      _lib.stream()))
+    return y, ckpt, xl
+
+
+def s4d_scan_bwd(u, gy, abar, w, c, d, ckpt):
+    """Pullback of s4d_scan_fwd: dict gu [B, L, H]; gabar, gw (= sum u g), gc [H, N]
+    complex; gd [H] (batch sums in a fixed order)."""
+    B, L, H = u.shape
+    N = abar.shape[-1]
+    gu = torch.empty_like(u)
+    f = dict(dtype=abar.dtype, device=u.device)
+    gab, gw, gc = (torch.empty((B, H, N), **f) for _ in range(3))
+    gd = torch.empty((B, H), dtype=u.dtype, device=u.device)
+    _lib.check(_lib.lib().lrx_s4d_bwd(_lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(gy), _lib.ptr(abar), _lib.ptr(w),
+                                      _lib.ptr(c), _lib.ptr(d), _lib.ptr(ckpt), _lib.ptr(gu), _lib.ptr(gab),
+                                      _lib.ptr(gw), _lib.ptr(gc), _lib.ptr(gd), B, L, H, N, _lib.stream()))
+    return {"gu": gu, "gabar": gab.sum(0), "gw": gw.sum(0), "gc": gc.sum(0), "gd": gd.sum(0)}

@@ -395,6 +395,35 @@ def test_gemm_f32_tn_tcgen05_matches_f64(lrx, K, M, N):
     assert torch.equal(C, C2)  # deterministic split-K
 
 
+@pytest.mark.parametrize("n", [8, 16, 32, 64])
+@pytest.mark.parametrize("scheme", ["zoh", "bilinear", "dirac"])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_s4d_fused_kernel_matches_oracle(lrx, n, scheme, dtype):
+    """The fused S4D kernel (d_state in {8, 16, 32, 64}, ragged L) against the
+    oracle; prefill state and the kernel's launch are checked too."""
+    from paper_2602_08810_b200 import _lib
+    m, B, L = 12, 3, 301
+    layer = lrx.make_layer("s4d", m, n, scheme, dtype=dtype, seed=61)
+    u = port.Rng(62).normal((B, L, m)).astype(layer.rdt)
+    gy = port.Rng(63).normal((B, L, m)).astype(layer.rdt)
+    before = _lib.launch_count()
+    y, tape = layer.forward(u, tape=True)
+    g = lrx.layer_backward(layer, tape, gy)
+    assert _lib.launch_count() > before
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64("s4d", scheme, params, u, gy)
+    tol = TOL[dtype]
+    assert rel(y, ry) < tol
+    assert rel(g.u, rgu) < tol
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < tol, (k, rel(g.params[k], rg[k]))
+    # prefill -> decode continues from the fused kernel's final state
+    _, st = layer.forward(u[:, :200], return_state=True)
+    for k in range(200, 204):
+        yk, st = layer.step(st, u[:, k])
+        assert rel(yk, ry[:, k]) < tol
+
+
 @pytest.mark.parametrize("seg", ["16", "128", "1024"])
 def test_mimo_segment_lengths_match_oracle(lrx, monkeypatch, seg):
     """MIMO scans with forced segment lengths (LRX_MIMO_SEG; ragged last one)."""
