@@ -146,6 +146,18 @@ template <> struct Fast<float> {
         const float big = exp(x) - 1.f;
         return fabsf(x) < 0.7f ? small : big;
     }
+    // expm1(x) when e^x is already known (ex): no extra MUFU op
+    __device__ static float expm1_known(float x, float ex) {
+        const float h = 0.5f * x;
+        float p = 1.f / 720.f;
+        p = fmaf(p, h, 1.f / 120.f);
+        p = fmaf(p, h, 1.f / 24.f);
+        p = fmaf(p, h, 1.f / 6.f);
+        p = fmaf(p, h, 0.5f);
+        p = fmaf(p, h, 1.f);
+        p *= h;
+        return fabsf(x) < 0.7f ? p * (p + 2.f) : ex - 1.f;
+    }
 };
 template <> struct Fast<double> {
     __device__ static double exp(double x) { return ::exp(x); }
@@ -154,6 +166,7 @@ template <> struct Fast<double> {
     __device__ static double sqrt(double x) { return ::sqrt(x); }
     __device__ static double sigmoid(double x) { return Math<double>::sigmoid(x); }
     __device__ static double expm1(double x) { return ::expm1(x); }
+    __device__ static double expm1_known(double x, double) { return ::expm1(x); }
 };
 
 // ---------------------------------------------------------------- look-back

@@ -58,7 +58,7 @@ __device__ __forceinline__ Coef<C> gates(IO uu, IO q_r, IO q_i, C la, C br, C bi
     k.i = F::sigmoid(C(cvt(q_i)) + bi);
     const C loga = (C(kGate) * k.r) * la;
     k.a = F::exp(loga);
-    k.s = F::sqrt(-F::expm1(C(2) * loga));
+    k.s = F::sqrt(-F::expm1_known(C(2) * loga, k.a * k.a));  // e^{2 log a} = a^2
     return k;
 }
 
@@ -1063,10 +1063,12 @@ static int bwd_t(const void* u, const void* qr, const void* qi, const void* lam,
     const int64_t n = B * W;
     TmaPlan pl, pa;
     // recompute variant (LRX_RGLRU_MODE=rc): 7 array passes, no y stream.
-    // Measured slower on C4 (18.3 vs 16.4 ms: the 2 x gates per element at
-    // ~14 warps/SM, limited by the 512 B of staged rows per thread), so the
-    // y-streaming kernel stays the default.
-    if (ckpt && sizeof(IO) == 4 && mode == 4 && B * L < (1ll << 31) && (W * 4) % 16 == 0) {
+    // fp32: measured slower on C4 (18.3 vs 16.4 ms: the 2 x gates per element
+    // at ~14 warps/SM, limited by the 512 B of staged rows per thread), so the
+    // y-streaming kernel stays the default there.  bf16 I/O: y is rounded, so
+    // this is the default backward (the look-back recompute took 65 ms on C4).
+    const bool rc_ok = ckpt && B * L < (1ll << 31) && (W * (int64_t)sizeof(IO)) % 16 == 0 && sizeof(IO) <= 4;
+    if (rc_ok && (mode == 4 || (sizeof(IO) == 2 && (mode == 0 || mode == 1)))) {
         constexpr int RC = Tile<IO>::T;
         const int LW = B * cdiv(W, 64) >= 4 * sm_count() ? 64 : 32;
         CUtensorMap m[4];
