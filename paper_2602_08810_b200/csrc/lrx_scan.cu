@@ -16,6 +16,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <type_traits>
+
 #include "lrx_common.cuh"
 
 #include <algorithm>
@@ -211,10 +213,41 @@ __global__ void reduce_rows_kernel(const V* __restrict__ in, V* __restrict__ out
     if (r0 == 0 && j < N) out[j] = red[c];
 }
 
+// Few rows, many columns (the S6 dB_k / dC_k channel-block partials: 24-32
+// rows of B*L*N columns): thread per 4 columns, 8 rows' 16-byte loads in
+// flight, summed in row order (deterministic).
+__global__ void reduce_cols4_kernel(const float4* __restrict__ in, float4* __restrict__ out, int64_t R, int64_t N4) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N4) return;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int64_t r = 0;
+    for (; r + 8 <= R; r += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __ldcs(in + (r + i) * N4 + j);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc.x += v[i].x, acc.y += v[i].y, acc.z += v[i].z, acc.w += v[i].w;
+    }
+    for (; r < R; ++r) {
+        const float4 v = __ldcs(in + r * N4 + j);
+        acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+    }
+    out[j] = acc;
+}
+
 // launch: many row lanes when there are few columns (the S5/LRU parameter
 // partials: R ~ 1e4 rows of P columns), 8 when columns are plentiful
 template <typename V>
 static void reduce_rows_launch(const V* in, V* out, int64_t R, int64_t N, cudaStream_t st) {
+    if constexpr (std::is_same<V, float>::value) {
+        if (R <= 64 && N % 4 == 0 && N >= 4 * 256 * 148 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+            (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+            const int64_t n4 = N / 4;
+            reduce_cols4_kernel<<<(unsigned)cdiv(n4, 256), 256, 0, st>>>(reinterpret_cast<const float4*>(in),
+                                                                         reinterpret_cast<float4*>(out), R, n4);
+            return;
+        }
+    }
     const int64_t blocks = cdiv(N, 32);
     int RL = 8;
     while (RL < 32 && blocks * RL < 148 * 64 && RL * 8 < R) RL *= 2;

@@ -356,6 +356,20 @@ def test_s6_is_deterministic_with_segments(lrx, monkeypatch):
         assert torch.equal(outs[0][1][k], outs[1][1][k]), k
 
 
+@pytest.mark.parametrize("R,N", [(24, 2_000_000), (3, 600_004), (33, 151_552), (4096, 100), (10_000, 7),
+                                 (5, 31)])
+def test_reduce_rows_matches_f64_and_is_deterministic(lrx, R, N):
+    """Fixed-order row reductions (every launch shape: wide float4, row-lane
+    tree, two-stage) against an f64 sum; bitwise equal on a re-run."""
+    from paper_2602_08810_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(R * 7 + N)
+    part = torch.randn((R, N), generator=g, device="cuda")
+    out = ops.reduce_rows(part, R, N)
+    ref = part.double().sum(0)
+    assert float((out.double() - ref).abs().max()) <= 1e-5 * max(1.0, float(ref.abs().max()))
+    assert torch.equal(out, ops.reduce_rows(part, R, N))
+
+
 # ---- tcgen05 3xTF32 GEMM ---------------------------------------------------
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 256), (1000, 256, 256), (4096, 128, 256), (300, 64, 36),
