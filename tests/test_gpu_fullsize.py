@@ -87,6 +87,28 @@ def test_rglru_c4_full_size(lrx):
     assert float((y12 - y).abs().max()) / float(y.abs().max()) < 1e-5
 
 
+def test_rglru_c4_bf16_full_size(lrx):
+    """C4 shape with bf16 I/O (the optional dtype): the backward recomputes the
+    states from the forward's fp32 checkpoints (bwd_rc); oracle spot check on
+    4 channels with the bf16-rounded inputs."""
+    from paper_2602_08810_b200 import ops
+    B, L, W = 64, 16384, 2560
+    layer = lrx.make_layer("rglru", W, dtype="f32", seed=0)
+    p = (layer.lambda_param, layer.b_r, layer.b_i)
+    u, qr, qi, gy = (randn((B, L, W), s, torch.bfloat16) for s in (6, 7, 8, 9))
+    y, ck = ops.rglru_scan_fwd(u, qr, qi, *p)
+    r = ops.rglru_scan_bwd(u, qr, qi, *p, ck, gy)  # no y: the bf16 state is rounded
+    cols = torch.tensor([3, 1024, W - 2, W - 1], device="cuda")
+    sl = lambda t: t.index_select(2, cols).double().cpu().numpy()  # noqa: E731
+    pn = [t.index_select(0, cols).double().cpu().numpy() for t in p]
+    ry, rg = port.rglru_scan(sl(u), sl(qr), sl(qi), *pn, sl(gy))
+    assert rel(y.index_select(2, cols), ry) < 1e-2
+    for k in ("gu_local", "gqr", "gqi"):
+        assert rel(r[k].index_select(2, cols), rg[k]) < 1e-2, k
+    for k in ("gla", "gb_r", "gb_i"):
+        assert rel(r[k].index_select(0, cols), rg[k]) < 1e-2, k
+
+
 @pytest.mark.parametrize("io", ["bf16", "f32"])
 def test_s6_c3_full_size(lrx, io):
     """C3: S6 B=16 L=8192 D=1536 N=16 (bf16 I/O as configured; f32 I/O for the
