@@ -235,6 +235,13 @@ int lrx_s6_step(int io_dtype, void* x, const void* u, const void* pre, const voi
 /* RG-LRU: x[B,W] compute precision; u, qr, qi, y io dtype. */
 int lrx_rglru_step(int io_dtype, void* x, const void* u, const void* qr, const void* qi, const void* lambda_param,
                    const void* b_r, const void* b_i, void* y, int64_t B, int64_t W, void* stream);
+/* S6 token in two kernels: the input projections p1 = u W_delta [B, R],
+ * B_k = u W_B^T, C_k = u W_C^T [B, N] into proj_ws ([B][R + 2N] fp32, caller
+ * allocated), then pre = p1 W_delta_proj and the update (fp32 weights;
+ * batch <= 16, f32 / bf16 I/O; LRX_ERR_UNSUPPORTED otherwise). */
+int lrx_s6_step_fused(int io_dtype, void* x, const void* u, const void* W_delta, const void* W_delta_proj,
+                      const void* W_B, const void* W_C, const void* b_delta, const void* a_log, const void* Dskip,
+                      void* y, void* proj_ws, int64_t B, int64_t D, int64_t R, int64_t N, void* stream);
 /* RG-LRU token in one kernel: the gate GEMVs qr = u W_r^T, qi = u W_i^T
  * (fp32 weights [W, W]) fused with the update; batch <= 16, W % 8 == 0,
  * f32 / bf16 I/O (LRX_ERR_UNSUPPORTED otherwise: use lrx_rglru_step). */

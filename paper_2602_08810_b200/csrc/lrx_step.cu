@@ -107,6 +107,83 @@ __global__ void s6_step_kernel(C* __restrict__ x, const IO* __restrict__ u, cons
     st_io(y + i, acc + Dskip[d] * uk);
 }
 
+// S6 token in two kernels (fp32 weights, batch <= 16; layers.py:1020-1027 +
+// 1145-1168).  (1) the input projections p1 = u W_delta [B, r], B_k = u W_B^T,
+// C_k = u W_C^T [B, n]: CTA per output column, its 8 warps split the model
+// width, u staged in shared memory; (2) thread per (b, d): pre = p1 . W_dp[:, d]
+// then the update of the channel's N states.
+template <typename IO>
+__global__ void __launch_bounds__(256) s6_step_proj_kernel(const IO* __restrict__ u, const float* __restrict__ Wd,
+                                                           const float* __restrict__ WB,
+                                                           const float* __restrict__ WC, float* __restrict__ out,
+                                                           int Bn, int m, int r, int n) {
+    extern __shared__ float sm[];  // u [Bn][m], then [8 warps][16] partials
+    float* us = sm;
+    float* part = sm + Bn * m;
+    for (int i = threadIdx.x; i < Bn * m; i += blockDim.x) us[i] = float(cvt(u[i]));
+    __syncthreads();
+    const int c = blockIdx.x;  // output column: [0, r) p1, [r, r+n) B_k, [r+n, r+2n) C_k
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float acc[16];
+#pragma unroll
+    for (int b = 0; b < 16; ++b) acc[b] = 0.f;
+    for (int i = warp * 32 + lane; i < m; i += 256) {
+        float wv = c < r ? Wd[(int64_t)i * r + c] : c < r + n ? WB[(int64_t)(c - r) * m + i]
+                                                             : WC[(int64_t)(c - r - n) * m + i];
+        // bf16 layers multiply bf16 activations by bf16-cast weights (layers._mm)
+        if constexpr (sizeof(IO) == 2) wv = __bfloat162float(__float2bfloat16_rn(wv));
+#pragma unroll
+        for (int b = 0; b < 16; ++b)
+            if (b < Bn) acc[b] = fmaf(wv, us[b * m + i], acc[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        if (b < Bn) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], o);
+        }
+    }
+    if (lane < Bn) {
+        float v = 0.f;
+#pragma unroll
+        for (int b = 0; b < 16; ++b)
+            if (lane == b) v = acc[b];
+        part[warp * 16 + lane] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < Bn) {
+        float v = 0.f;
+        for (int w = 0; w < 8; ++w) v += part[w * 16 + threadIdx.x];  // fixed order
+        out[(int64_t)threadIdx.x * (r + 2 * n) + c] = v;
+    }
+}
+
+template <typename IO>
+__global__ void s6_step_fused_kernel(float* __restrict__ x, const IO* __restrict__ u,
+                                     const float* __restrict__ proj, const float* __restrict__ Wdp,
+                                     const float* __restrict__ bdelta, const float* __restrict__ a_log,
+                                     const float* __restrict__ Dskip, IO* __restrict__ y, int Bn, int D, int r,
+                                     int N) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (b, d)
+    if (i >= (int64_t)Bn * D) return;
+    const int b = (int)(i / D), d = (int)(i % D);
+    const float* pb = proj + (int64_t)b * (r + 2 * N);
+    float pre = 0.f;
+    for (int j = 0; j < r; ++j) pre = fmaf(pb[j], Wdp[(int64_t)j * D + d], pre);
+    const float uk = float(cvt(u[i]));
+    const float delta = Math<float>::softplus(pre + bdelta[d]);
+    const float du = delta * uk;
+    float acc = 0.f;
+    for (int k = 0; k < N; ++k) {
+        const float a = -Math<float>::exp(a_log[(int64_t)d * N + k]);
+        float xv = x[i * N + k];
+        xv = Math<float>::exp(delta * a) * xv + du * pb[r + k];
+        x[i * N + k] = xv;
+        acc += pb[r + N + k] * xv;
+    }
+    st_io(y + i, acc + Dskip[d] * uk);
+}
+
 // RG-LRU: gates, x = a x + sqrt(1 - a^2) i u, y = x   (thread per (b, w))
 template <typename IO, typename C>
 __global__ void rglru_step_kernel(C* __restrict__ x, const IO* __restrict__ u, const IO* __restrict__ qr,
@@ -366,6 +443,35 @@ int lrx_rglru_step(int io_dtype, void* x, const void* u, const void* qr, const v
         default: set_error("rglru step: unsupported io dtype %d", io_dtype); return LRX_ERR_VALUE;
     }
     return launched("lrx_rglru_step");
+}
+
+int lrx_s6_step_fused(int io_dtype, void* x, const void* u, const void* W_delta, const void* W_delta_proj,
+                      const void* W_B, const void* W_C, const void* b_delta, const void* a_log, const void* Dskip,
+                      void* y, void* proj_ws, int64_t B, int64_t D, int64_t R, int64_t N, void* stream) {
+    LRX_REQUIRE(B >= 1 && D >= 1 && R >= 1 && N >= 1, LRX_ERR_SHAPE, "bad extents");
+    const size_t smem = ((size_t)B * D + 8 * 16) * 4;
+    LRX_REQUIRE(B <= 16 && smem <= 200 * 1024 && (io_dtype == LRX_F32 || io_dtype == LRX_BF16), LRX_ERR_UNSUPPORTED,
+                "s6 fused step: batch <= 16, f32 / bf16 I/O");
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned g2 = (unsigned)cdiv(B * D, 128);
+#define LRX_S6_FUSED(IO_)                                                                                         \
+    do {                                                                                                          \
+        auto k = step::s6_step_proj_kernel<IO_>;                                                                 \
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {   \
+            set_error("s6 fused step: cannot reserve %zu B of shared memory", smem);                              \
+            return LRX_ERR_CUDA;                                                                                 \
+        }                                                                                                         \
+        k<<<(unsigned)(R + 2 * N), 256, smem, st>>>((const IO_*)u, (const float*)W_delta, (const float*)W_B,      \
+                                                    (const float*)W_C, (float*)proj_ws, (int)B, (int)D, (int)R,  \
+                                                    (int)N);                                                      \
+        step::s6_step_fused_kernel<IO_><<<g2, 128, 0, st>>>(                                                     \
+            (float*)x, (const IO_*)u, (const float*)proj_ws, (const float*)W_delta_proj, (const float*)b_delta,  \
+            (const float*)a_log, (const float*)Dskip, (IO_*)y, (int)B, (int)D, (int)R, (int)N);                  \
+    } while (0)
+    if (io_dtype == LRX_F32) LRX_S6_FUSED(float);
+    else LRX_S6_FUSED(__nv_bfloat16);
+#undef LRX_S6_FUSED
+    return launched("lrx_s6_step_fused", 2);
 }
 
 int lrx_rglru_step_fused(int io_dtype, void* x, const void* u, const void* W_r, const void* W_i,

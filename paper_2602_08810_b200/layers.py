@@ -930,6 +930,16 @@ class S6(LinearRecurrence):
         return torch.zeros((batch, self.d_model, self.d_state), dtype=self.tdt, device=self.device)
 
     def _step(self, st, uk, delta_k):
+        if self.tdt == torch.float32 and st.batch <= 16 and st.batch * self.d_model * 4 <= 190 * 1024:
+            # projections + update in two kernels (fp32 weights read once per token)
+            y = torch.empty((st.batch, self.d_model), dtype=self.io_dtype, device=self.device)
+            ws = torch.empty((st.batch, self.d_rank + 2 * self.d_state), dtype=torch.float32, device=self.device)
+            _lib.check(_lib.lib().lrx_s6_step_fused(
+                _lib.code_of(self.io_dtype), _lib.ptr(st.x), _lib.ptr(uk), _lib.ptr(self.W_delta),
+                _lib.ptr(self.W_delta_proj), _lib.ptr(self.W_B), _lib.ptr(self.W_C), _lib.ptr(self.b_delta),
+                _lib.ptr(self.a_log), _lib.ptr(self.D), _lib.ptr(y), _lib.ptr(ws), st.batch, self.d_model,
+                self.d_rank, self.d_state, _lib.stream()))
+            return y
         p1 = _mm(uk, self.W_delta)
         pre = (p1 @ self.W_delta_proj).contiguous()
         Bk = _mm(uk, self.W_B.T).contiguous()
