@@ -65,6 +65,32 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
         "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
+// multicast flavours for 2-CTA clusters (MC = 2): the B / B_lo k-blocks land
+// in both CTAs' shared memory from one TMA each, and every MMA commit frees
+// the stage in both CTAs
+__device__ __forceinline__ void load_2d_mc(void* dst, const CUtensorMap* m, int c0, int r0, uint64_t* bar,
+                                           uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(tma::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(r0), "r"(tma::smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     tma::smem_u32(bar)),
+                 "h"(mask)
+                 : "memory");
+}
+__device__ __forceinline__ int cluster_rank() {
+    int r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      tma::smem_u32(bar))
@@ -99,7 +125,7 @@ constexpr int THREADS_P = 448;  // + 8 epilogue warps (2 per TMEM lane quarter)
 // TMA store writes the box (out-of-bounds rows / columns clipped).  The
 // direct-store epilogue kept 32 loads of 128 B in flight per warp, which
 // bounded the skip-input GEMMs at ~2 TB/s.
-template <int BN, bool TE>
+template <int BN, bool TE, int MC>
 __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
     const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
     const __grid_constant__ CUtensorMap mBl, const __grid_constant__ CUtensorMap mC,
@@ -121,7 +147,12 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
     float* epi = reinterpret_cast<float*>(stages + STAGES * LY::STAGE);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (K + BKT - 1) / BKT;
-    const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN, ntiles = tm * tn;
+    const int tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
+    // tile schedule: a cluster of MC CTAs walks units of MC adjacent M-tiles
+    // (same N-tile) in lockstep; CTA rank r takes M-tile MC * (unit % tmp) + r
+    const int crank = MC == 2 ? cluster_rank() : 0;
+    const int cid = blockIdx.x / MC, ncl = gridDim.x / MC;
+    const int tmp = (tm + MC - 1) / MC, ntiles = tmp * tn;
     constexpr uint32_t kCols = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
 
     if (threadIdx.x == 0) {
@@ -131,7 +162,7 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
         for (int i = 0; i < STAGES; ++i) {
             tma::mbar_init(&full[i], 1);
             tma::mbar_init(&split[i], 128);
-            tma::mbar_init(&empty[i], 1);
+            tma::mbar_init(&empty[i], MC);  // MC = 2: both CTAs' MMAs release a stage
         }
         for (int i = 0; i < 2; ++i) {
             tma::mbar_init(&tfull[i], 1);
@@ -153,22 +184,28 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (MC == 2) cluster_sync();  // the peer's barriers exist before any multicast reaches them
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {  // ------------------------------------------ producer
             int it = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const int m0 = (tile % tm) * BM, n0 = (tile / tm) * BN;
+            for (int tile = cid; tile < ntiles; tile += ncl) {
+                const int m0 = ((tile % tmp) * MC + crank) * BM, n0 = (tile / tmp) * BN;
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int st = it % STAGES;
                     if (it >= STAGES) tma::mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
                     unsigned char* sp = stages + st * LY::STAGE;
                     tma::mbar_arrive_expect_tx(&full[st], LY::A + 2 * LY::B);
                     tma::load_2d(sp, &mA, kb * BKT, m0, &full[st]);
-                    tma::load_2d(sp + 2 * LY::A, &mB, kb * BKT, n0, &full[st]);
-                    tma::load_2d(sp + 2 * LY::A + LY::B, &mBl, kb * BKT, n0, &full[st]);
+                    if (MC == 2) {  // rank 0 brings B, rank 1 B_lo, each to both CTAs
+                        if (crank == 0) load_2d_mc(sp + 2 * LY::A, &mB, kb * BKT, n0, &full[st], 0x3);
+                        else load_2d_mc(sp + 2 * LY::A + LY::B, &mBl, kb * BKT, n0, &full[st], 0x3);
+                    } else {
+                        tma::load_2d(sp + 2 * LY::A, &mB, kb * BKT, n0, &full[st]);
+                        tma::load_2d(sp + 2 * LY::A + LY::B, &mBl, kb * BKT, n0, &full[st]);
+                    }
                 }
             }
         }
@@ -176,7 +213,7 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
         if (lane == 0) {  // ------------------------------------------ MMA issuer
             constexpr uint32_t idesc = idesc_tf32<BN>();
             int it = 0, ti = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+            for (int tile = cid; tile < ntiles; tile += ncl, ++ti) {
                 const int acc = ti & 1;
                 if (ti >= 2) tma::mbar_wait(&tempty[acc], ((ti >> 1) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -196,7 +233,8 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
                         mma_tf32(td, dA, dBl, idesc, 1);
                         mma_tf32(td, dAl, dB, idesc, 1);
                     }
-                    mma_commit(&empty[st]);  // stage reusable once these MMAs have read it
+                    if (MC == 2) mma_commit_mc(&empty[st], 0x3);  // frees the stage in both CTAs
+                    else mma_commit(&empty[st]);  // stage reusable once these MMAs have read it
                 }
                 mma_commit(&tfull[acc]);
             }
@@ -205,7 +243,7 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
         // ---------------------------------------------------------- split
         const int t = threadIdx.x - 64;  // 0..127
         int it = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        for (int tile = cid; tile < ntiles; tile += ncl)
             for (int kb = 0; kb < nk; ++kb, ++it) {
                 const int st = it % STAGES;
                 tma::mbar_wait(&full[st], (it / STAGES) & 1);
@@ -232,8 +270,8 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
         uint64_t* cb = &cbar[warp - 6];
         uint32_t cph = 0;
         int ti = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
-            const int m0 = (tile % tm) * BM, n0 = (tile / tm) * BN;
+        for (int tile = cid; tile < ntiles; tile += ncl, ++ti) {
+            const int m0 = ((tile % tmp) * MC + crank) * BM, n0 = (tile / tmp) * BN;
             const int acc = ti & 1;
             const int rbase = m0 + 32 * q;
             auto issue_cin = [&](int c0) {
@@ -312,8 +350,8 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
         const int half = (warp - 6) >> 2;  // which of the interleaved 32-column chunks
         float* tp = epi + (warp - 6) * 32 * 33;
         int ti = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
-            const int m0 = (tile % tm) * BM, n0 = (tile / tm) * BN;
+        for (int tile = cid; tile < ntiles; tile += ncl, ++ti) {
+            const int m0 = ((tile % tmp) * MC + crank) * BM, n0 = (tile / tmp) * BN;
             const int acc = ti & 1;
             const int rbase = m0 + 32 * q;
             // skip-input rows for column chunk c0 (lane = column: coalesced);
@@ -375,6 +413,7 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (MC == 2) cluster_sync();  // no CTA leaves while its peer may still multicast into it
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
 }
@@ -601,7 +640,11 @@ static int launch(const float* A, const float* Bt, const float* Btl, float* C, c
     if (!te) mC = mA, mCin = mA;  // unused
     else if (!Cin) mCin = mC;
     const size_t smem = te ? Lay<BN, true>::smem() : Lay<BN, false>::smem();
-    auto k = te ? gemm_tf32x3_kernel<BN, true> : gemm_tf32x3_kernel<BN, false>;
+    // 2-CTA clusters sharing the B / B_lo stream (LRX_GEMM_MC=1 disables)
+    const char* em = getenv("LRX_GEMM_MC");
+    const bool mc = !(em && !strcmp(em, "1")) && cdiv(M, BM) >= 2;
+    auto k = te ? (mc ? gemm_tf32x3_kernel<BN, true, 2> : gemm_tf32x3_kernel<BN, true, 1>)
+                : (mc ? gemm_tf32x3_kernel<BN, false, 2> : gemm_tf32x3_kernel<BN, false, 1>);
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         set_error("gemm: cannot reserve %zu B of shared memory", smem);
         return LRX_ERR_CUDA;
@@ -612,6 +655,34 @@ static int launch(const float* A, const float* Bt, const float* Btl, float* C, c
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
+    }
+    if (mc) {
+        const int64_t units = cdiv(cdiv(M, BM), 2) * cdiv(N, BN);
+        cudaLaunchConfig_t cfg = {};
+        cfg.blockDim = dim3(THREADS_P);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        // persistent: only as many pairs as can be co-resident (an odd SM
+        // count per GPC leaves SMs no pair can use)
+        static int max_cl = 0;
+        if (!max_cl) {
+            cfg.gridDim = dim3(sms);
+            if (cudaOccupancyMaxActiveClusters(&max_cl, (void*)k, &cfg) != cudaSuccess || max_cl < 1) max_cl = sms / 2;
+        }
+        cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(units, max_cl)));
+        if (cudaLaunchKernelEx(&cfg, k, mA, mB, mBl, mC, mCin, C, Cin, cs, (int)M, (int)N, (int)K, alpha, beta) !=
+            cudaSuccess) {
+            set_error("gemm: cluster launch failed");
+            return LRX_ERR_CUDA;
+        }
+        return launched(te ? "lrx_gemm_f32/tcgen05x2+tma_epilogue" : "lrx_gemm_f32/tcgen05x2");
     }
     const int64_t tiles = cdiv(M, BM) * cdiv(N, BN);
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
