@@ -192,6 +192,10 @@ def build_problem(w, B, device, L=None, group=None):
         prob["bytes"] = {"fwd": 4 * B * L * H * bpe, "bwd": 7 * B * L * H * bpe}
         prob["probe"] = dict(name="lrx_rglru_bwd (+3 column sums)", bound="hbm", amount=prob["bytes"]["bwd"],
                              fn=bwd)
+        if bpe == 4:  # the kernel streams 8 arrays (y too): its measured mix ceiling
+            prob["probe"]["stream"] = dict(dram_bytes=8 * B * L * H * bpe, ceiling_gbs=6124.0,
+                                           source="tools/ubench/streams.cu: 5 reads + 3 writes, float4, "
+                                                  "C4-sized arrays, same pool of B200s")
     elif kind == "s6":
         with torch.no_grad():
             from paper_2602_08810_b200.layers import _mm
@@ -608,6 +612,11 @@ def main():
                 "traffic": _traffic(args.workload, "probe"), "kernel": pr["name"], "peak_source": peak_kind,
                 "per_launch_ms": pms, "algorithmic_bytes_per_launch": pr["amount"],
                 "step_share": pms / r["ms"]}
+        if "stream" in pr:  # achieved DRAM rate against the measured ceiling of the kernel's stream mix
+            sc = pr["stream"]
+            dr = sc["dram_bytes"] / (pms * 1e-3) / 1e9
+            roof["stream_ceiling"] = {"dram_GBps": dr, "ceiling_GBps": sc["ceiling_gbs"],
+                                      "frac": dr / sc["ceiling_gbs"], "source": sc["source"]}
         if "mufu_ops" in pr:  # the binding unit of the S6 scan: MUFU ex2 (16/clk/SM, ubench-measured 4.62 T/s)
             mu = pr["mufu_ops"] / (pms * 1e-3) / 1e12
             roof["compute"] = {"bound": "mufu", "achieved": mu, "peak": 4.62, "unit": "Tops/s", "frac": mu / 4.62,
