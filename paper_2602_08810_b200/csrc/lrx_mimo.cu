@@ -114,9 +114,17 @@ __global__ void __launch_bounds__(kThreads) fwd_kernel(const cplx<T>* __restrict
     const int64_t b = lane / P, p = lane % P;
     const V ab = abar[p], sc = scale[p];
     V xs = Traits<V>::zero();
-    if (s > 0) {
+    if (s > 0) {  // fold the maps to the left; 8 loads in flight per round
         const V AS = cpow2k(ab, seg);
-        for (int r = 0; r < s; ++r) xs = AS * xs + aggX[(int64_t)r * n_lanes + lane];
+        int r = 0;
+        for (; r + 8 <= s; r += 8) {
+            V m[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m[i] = aggX[(int64_t)(r + i) * n_lanes + lane];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xs = AS * xs + m[i];
+        }
+        for (; r < s; ++r) xs = AS * xs + aggX[(int64_t)r * n_lanes + lane];
     }
     const int64_t t0 = (int64_t)s * seg;
     const int nt = (int)min((int64_t)seg, L - t0);
@@ -182,9 +190,17 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const cplx<T>* __restrict
     const V ab = abar[p];
     const V abc = conj(ab), scc = conj(scale[p]);
     V h = Traits<V>::zero();
-    if (s < S - 1) {
+    if (s < S - 1) {  // fold the maps to the right; 8 loads in flight per round
         const V AS = cpow2k(abc, seg);
-        for (int r = S - 1; r > s; --r) h = AS * h + aggH[(int64_t)r * n_lanes + lane];
+        int r = S - 1;
+        for (; r - 8 >= s; r -= 8) {
+            V m[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m[i] = aggH[(int64_t)(r - i) * n_lanes + lane];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) h = AS * h + m[i];
+        }
+        for (; r > s; --r) h = AS * h + aggH[(int64_t)r * n_lanes + lane];
     }
     const int64_t t0 = (int64_t)s * seg;
     const int nt = (int)min((int64_t)seg, L - t0);
