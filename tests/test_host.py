@@ -59,3 +59,28 @@ def test_host_numerics():
     np.testing.assert_allclose(lrx.softplus(x), [0.0, np.log(2), 40.0, 60.0], atol=1e-15)
     np.testing.assert_allclose(lrx.sigmoid(np.array([-800.0, 0.0, 800.0])), [0.0, 0.5, 1.0])
     assert lrx.real_dtype("f32") == np.float32
+
+
+def test_init_invariants():
+    """The reference's initialisation invariants (test_layers.py:128-176),
+    checked on the drop-in layers' parameters (CPU, no compute)."""
+    m, n = 8, 6
+    s4d = lrx.make_layer("s4d", m, n, device="cpu")
+    lam_re = -np.exp(s4d.parameters()["lambda_re_log"].numpy())
+    np.testing.assert_allclose(lam_re, -0.5)  # S4D-Lin: lambda = -1/2 + i pi n
+    np.testing.assert_allclose(s4d.parameters()["lambda_im"].numpy(), np.pi * np.arange(n)[None, :].repeat(m, 0))
+    lru = lrx.make_layer("lru", m, n, device="cpu", r_min=0.9, r_max=0.999, max_phase=np.pi / 10)
+    p = {k: v.numpy() for k, v in lru.parameters().items()}
+    mag = np.exp(-np.exp(p["nu_log"]))
+    assert np.all((mag >= 0.9 - 1e-12) & (mag <= 0.999 + 1e-12))  # the LRU ring
+    phase = np.exp(p["theta_log"])
+    assert np.all((phase > 0) & (phase <= np.pi / 10 + 1e-12))
+    np.testing.assert_allclose(np.exp(p["gamma_log"]), np.sqrt(1 - mag ** 2), rtol=1e-12)
+    s6 = lrx.make_layer("s6", m, n, device="cpu")
+    q = {k: v.numpy() for k, v in s6.parameters().items()}
+    np.testing.assert_allclose(-np.exp(q["a_log"]), -np.arange(1, n + 1)[None, :].repeat(m, 0))  # a = -(n+1)
+    dt = lrx.softplus(q["b_delta"])
+    assert np.all((dt >= 1e-3 - 1e-12) & (dt <= 1e-1 + 1e-12))
+    rg = lrx.make_layer("rglru", m, device="cpu")
+    a = lrx.sigmoid(rg.parameters()["lambda_param"].numpy())
+    assert np.all((a >= 0.9 - 1e-12) & (a <= 0.999 + 1e-12))
