@@ -233,7 +233,7 @@ class LinearRecurrence:
 
     # -- parameters --------------------------------------------------------
     def _p(self, arr):
-        return torch.as_tensor(np.ascontiguousarray(arr)).to(self.device, self.tdt)
+        return torch.from_numpy(np.array(arr, copy=True, order="C")).to(self.device, self.tdt)
 
     def parameters(self):
         raise NotImplementedError

@@ -90,6 +90,31 @@ def test_modes_agree_bitwise_and_runs_are_deterministic(lrx):
                 np.testing.assert_array_equal(gp[k], outs[0][2][k], err_msg=f"{kind}:{k}")
 
 
+@pytest.mark.parametrize("kind", ["s4d", "s5", "lru", "s6", "rglru"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_validation_grid(lrx, kind, dtype):
+    """The reference's validation grid (bench.py:185-190, run_validation):
+    L in {1, 2, 257, 1024} x B in {1, 4} x H in {1, 8} x N in {2, 16}, every
+    output and gradient against the f64 oracle."""
+    tol = TOL[dtype]
+    for L in (1, 2, 257, 1024):
+        for B in (1, 4):
+            for H in (1, 8):
+                for N in (2, 16):
+                    layer = lrx.make_layer(kind, H, None if kind == "rglru" else N, dtype=dtype, seed=L + B + H + N)
+                    u = port.Rng(L * 7 + B).normal((B, L, H)).astype(layer.rdt)
+                    gy = port.Rng(L * 7 + B + 1).normal((B, L, H)).astype(layer.rdt)
+                    y, tape = layer.forward(u, tape=True)
+                    g = lrx.layer_backward(layer, tape, gy)
+                    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+                    ry, rg, rgu = _oracle_f64(kind, layer.discretization, params, u, gy)
+                    case = (L, B, H, N)
+                    assert rel(y, ry) < tol, case
+                    assert rel(g.u, rgu) < tol, case
+                    for k in rg:
+                        assert rel(g.params[k], rg[k]) < tol, (case, k, rel(g.params[k], rg[k]))
+
+
 @pytest.mark.parametrize("kind,m,n,B,L", [
     ("s6", 40, 16, 2, 1500), ("s6", 33, 4, 3, 70), ("s6", 16, 8, 1, 129), ("s6", 8, 32, 2, 100),
     ("s6", 12, 64, 1, 80), ("s6", 20, 13, 2, 65),
