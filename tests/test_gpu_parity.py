@@ -90,6 +90,20 @@ def test_modes_agree_bitwise_and_runs_are_deterministic(lrx):
                 np.testing.assert_array_equal(gp[k], outs[0][2][k], err_msg=f"{kind}:{k}")
 
 
+def test_lti_ltv_entry_points(lrx):
+    """lti_forward / ltv_forward route to forward and refuse the other family
+    (reference test_layers.py:318-329)."""
+    u = port.Rng(71).normal((2, 9, 3))
+    layer = lrx.make_layer("s5", 3, 4)
+    np.testing.assert_array_equal(lrx.lti_forward(layer, u), layer.forward(u))
+    with pytest.raises(ValueError):
+        lrx.lti_forward(lrx.make_layer("s6", 3, 2), u)
+    ltv = lrx.make_layer("rglru", 3)
+    np.testing.assert_array_equal(lrx.ltv_forward(ltv, u), ltv.forward(u))
+    with pytest.raises(ValueError):
+        lrx.ltv_forward(layer, u)
+
+
 @pytest.mark.parametrize("kind", ["s4d", "s5", "lru", "s6", "rglru"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_validation_grid(lrx, kind, dtype):
