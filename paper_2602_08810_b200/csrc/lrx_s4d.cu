@@ -25,9 +25,6 @@ namespace s4d {
 
 constexpr int TT = 16;  // steps per tile (checkpoint interval)
 
-template <typename T>
-__device__ __forceinline__ T ld(const T* p) { return *p; }
-
 // transposed butterfly over lane bits HI..LO (see lrx_s6v3.cu tr_reduce)
 template <typename T, int V, int HI, int LO>
 __device__ __forceinline__ void tr_reduce(T* v) {

@@ -484,10 +484,6 @@ int lrx_rglru_step_fused(int io_dtype, void* x, const void* u, const void* W_r, 
                     (reinterpret_cast<uintptr_t>(u) & 15) == 0,
                 LRX_ERR_UNSUPPORTED, "rglru fused step: batch <= 16, width %% 8 == 0, f32 / bf16 I/O");
     cudaStream_t st = (cudaStream_t)stream;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    (void)sms;
     const unsigned g = (unsigned)cdiv(W, 8 * step::kCPW);
 #define LRX_RG_FUSED(IO_, BM_)                                                                                  \
     do {                                                                                                        \
