@@ -117,11 +117,22 @@ __global__ void __launch_bounds__(256) s6_step_proj_kernel(const IO* __restrict_
                                                            const float* __restrict__ WB,
                                                            const float* __restrict__ WC, float* __restrict__ out,
                                                            int Bn, int m, int r, int n) {
-    extern __shared__ float sm[];  // u [Bn][m], then [8 warps][16] partials
-    float* us = sm;
-    float* part = sm + Bn * m;
-    for (int i = threadIdx.x; i < Bn * m; i += blockDim.x) us[i] = float(cvt(u[i]));
+    // u [Bn][m] lands by one bulk copy (IO dtype); [8 warps][16] partials after it
+    extern __shared__ __align__(128) unsigned char smp[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smp);
+    const IO* us = reinterpret_cast<const IO*>(smp + 128);
+    float* part = reinterpret_cast<float*>(smp + 128 + (((size_t)Bn * m * sizeof(IO) + 15) & ~(size_t)15));
+    if (threadIdx.x == 0) {
+        tma::mbar_init(bar, 1);
+        tma::fence_barrier_init();
+    }
     __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)Bn * m * sizeof(IO);
+        tma::mbar_arrive_expect_tx(bar, bytes);
+        tma::load_1d(smp + 128, u, bytes, bar);
+    }
+    tma::mbar_wait(bar, 0);
     const int c = blockIdx.x;  // output column: [0, r) p1, [r, r+n) B_k, [r+n, r+2n) C_k
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float acc[16];
@@ -134,7 +145,7 @@ __global__ void __launch_bounds__(256) s6_step_proj_kernel(const IO* __restrict_
         if constexpr (sizeof(IO) == 2) wv = __bfloat162float(__float2bfloat16_rn(wv));
 #pragma unroll
         for (int b = 0; b < 16; ++b)
-            if (b < Bn) acc[b] = fmaf(wv, us[b * m + i], acc[b]);
+            if (b < Bn) acc[b] = fmaf(wv, float(cvt(us[b * m + i])), acc[b]);
     }
 #pragma unroll
     for (int b = 0; b < 16; ++b) {
@@ -449,9 +460,12 @@ int lrx_s6_step_fused(int io_dtype, void* x, const void* u, const void* W_delta,
                       const void* W_B, const void* W_C, const void* b_delta, const void* a_log, const void* Dskip,
                       void* y, void* proj_ws, int64_t B, int64_t D, int64_t R, int64_t N, void* stream) {
     LRX_REQUIRE(B >= 1 && D >= 1 && R >= 1 && N >= 1, LRX_ERR_SHAPE, "bad extents");
-    const size_t smem = ((size_t)B * D + 8 * 16) * 4;
-    LRX_REQUIRE(B <= 16 && smem <= 200 * 1024 && (io_dtype == LRX_F32 || io_dtype == LRX_BF16), LRX_ERR_UNSUPPORTED,
-                "s6 fused step: batch <= 16, f32 / bf16 I/O");
+    const size_t esz = io_dtype == LRX_BF16 ? 2 : 4;
+    const size_t ubytes = (size_t)B * D * esz;
+    const size_t smem = 128 + ((ubytes + 15) & ~(size_t)15) + 8 * 16 * 4;
+    LRX_REQUIRE(B <= 16 && smem <= 200 * 1024 && (io_dtype == LRX_F32 || io_dtype == LRX_BF16) && ubytes % 16 == 0 &&
+                    (reinterpret_cast<uintptr_t>(u) & 15) == 0,
+                LRX_ERR_UNSUPPORTED, "s6 fused step: batch <= 16, 16-byte u rows, f32 / bf16 I/O");
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned g2 = (unsigned)cdiv(B * D, 128);
 #define LRX_S6_FUSED(IO_)                                                                                         \

@@ -930,7 +930,8 @@ class S6(LinearRecurrence):
         return torch.zeros((batch, self.d_model, self.d_state), dtype=self.tdt, device=self.device)
 
     def _step(self, st, uk, delta_k):
-        if self.tdt == torch.float32 and st.batch <= 16 and st.batch * self.d_model * 4 <= 190 * 1024:
+        if self.tdt == torch.float32 and st.batch <= 16 and st.batch * self.d_model * 4 <= 190 * 1024 and \
+                (st.batch * self.d_model * uk.element_size()) % 16 == 0:
             # projections + update in two kernels (fp32 weights read once per token)
             y = torch.empty((st.batch, self.d_model), dtype=self.io_dtype, device=self.device)
             ws = torch.empty((st.batch, self.d_rank + 2 * self.d_state), dtype=torch.float32, device=self.device)
