@@ -4,7 +4,8 @@ for S4D / S5 / LRU / S6 / RG-LRU, behind the reference's layer and operator
 API.  Kernels live in liblrx.so (include/lrx.h); this package is the host-side
 mirror of the reference interface.  There is no CPU fallback.
 """
-from .numerics import REAL_DTYPES, Rng, ShapeError, complex_dtype, real_dtype, sigmoid, softplus
+from .numerics import (REAL_DTYPES, ComplexPair, Rng, ShapeError, alloc, allocation_count, as_tensor, complex_dtype,
+                       complex_exp, real_dtype, sigmoid, softplus)
 from .discretize import (NonMonotoneTimestamps, SingularBilinear, deltas_from_timestamps, discretize,
                          discretize_bilinear, discretize_dirac, discretize_zoh, scheme_factors)
 from .scan import (MIN_CHUNK_LEN, StepState, combine, identity_element, init_step_state, plan_chunks, scan_parallel,

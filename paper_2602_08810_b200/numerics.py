@@ -11,7 +11,8 @@ import numpy as np
 import torch
 
 __all__ = ["REAL_DTYPES", "SOFTPLUS_THRESHOLD", "ShapeError", "real_dtype", "complex_dtype",
-           "torch_real", "torch_complex", "softplus", "sigmoid", "Rng"]
+           "torch_real", "torch_complex", "softplus", "sigmoid", "Rng", "as_tensor", "complex_exp",
+           "ComplexPair", "alloc", "allocation_count"]
 
 REAL_DTYPES = {"f32": np.dtype(np.float32), "f64": np.dtype(np.float64)}
 # numerics.py:36-39
@@ -105,3 +106,86 @@ class Rng:
 
     def split(self, n: int):
         return [Rng(_seq=s) for s in self._seq.spawn(n)]
+
+
+# ---------------------------------------------------------------------------
+# host array helpers of the reference's public numerics API (numerics.py:67-175)
+
+_CPLX_OF = {np.dtype(np.float32): np.dtype(np.complex64), np.dtype(np.float64): np.dtype(np.complex128)}
+_SUPPORTED = set(_CPLX_OF) | set(_CPLX_OF.values())
+
+
+def as_tensor(values, dtype=None) -> np.ndarray:
+    """C-contiguous array in a supported dtype (f32/f64/c64/c128); integer or
+    bool input becomes float64, other complex input complex128 (numerics.py:67-83)."""
+    arr = np.asarray(values)
+    if dtype is not None:
+        dt = REAL_DTYPES[dtype] if isinstance(dtype, str) and dtype in REAL_DTYPES else np.dtype(dtype)
+    elif arr.dtype in _SUPPORTED:
+        dt = arr.dtype
+    else:
+        dt = np.dtype(np.complex128 if np.issubdtype(arr.dtype, np.complexfloating) else np.float64)
+    if dt not in _SUPPORTED:
+        raise ValueError(f"unsupported tensor dtype {dt}")
+    return np.ascontiguousarray(arr, dtype=dt)
+
+
+def complex_exp(re, im=None):
+    """e^z.  One complex argument -> complex result; two real planes (re, im)
+    -> the planes (e^re cos im, e^re sin im) (numerics.py:108-128)."""
+    if im is None:
+        z = np.asarray(re)
+        r = np.exp(z.real)
+        out = (r * np.cos(z.imag) + 1j * (r * np.sin(z.imag))).astype(_CPLX_OF.get(np.asarray(r).dtype,
+                                                                                     np.dtype(np.complex128)))
+        return out[()] if out.ndim == 0 else out
+    re, im = np.asarray(re), np.asarray(im)
+    if re.shape != im.shape:
+        raise ShapeError(f"plane shapes differ: {re.shape} vs {im.shape}")
+    r = np.exp(re)
+    return r * np.cos(im), r * np.sin(im)
+
+
+class ComplexPair:
+    """A complex array held as two real planes of one shape (numerics.py:131-154)."""
+
+    __slots__ = ("re", "im")
+
+    def __init__(self, re, im):
+        if np.shape(re) != np.shape(im):
+            raise ShapeError(f"plane shapes differ: {np.shape(re)} vs {np.shape(im)}")
+        object.__setattr__(self, "re", re)
+        object.__setattr__(self, "im", im)
+
+    def __setattr__(self, name, value):  # frozen, like the reference's dataclass
+        raise AttributeError("ComplexPair is immutable")
+
+    @property
+    def shape(self):
+        return np.shape(self.re)
+
+    def to_complex(self) -> np.ndarray:
+        re = np.asarray(self.re)
+        return (re + 1j * np.asarray(self.im)).astype(_CPLX_OF[np.dtype(re.dtype)])
+
+    @classmethod
+    def from_complex(cls, z) -> "ComplexPair":
+        z = np.asarray(z)
+        return cls(np.ascontiguousarray(z.real), np.ascontiguousarray(z.imag))
+
+
+_ALLOCATIONS = [0]
+
+
+def alloc(shape, dtype) -> np.ndarray:
+    """Uninitialised host buffer, counted (numerics.py:165-169).  The device
+    paths allocate through torch; step mode (Layer.step / StepGraph) allocates
+    no host buffers per token."""
+    _ALLOCATIONS[0] += 1
+    return np.empty(shape, dtype)
+
+
+def allocation_count() -> int:
+    """alloc() calls since import (compare deltas; numerics.py:172-174)."""
+    return _ALLOCATIONS[0]
+

@@ -84,3 +84,27 @@ def test_init_invariants():
     rg = lrx.make_layer("rglru", m, device="cpu")
     a = lrx.sigmoid(rg.parameters()["lambda_param"].numpy())
     assert np.all((a >= 0.9 - 1e-12) & (a <= 0.999 + 1e-12))
+
+
+def test_numerics_helpers():
+    """as_tensor / complex_exp / ComplexPair / allocation_count (reference
+    numerics.py:67-175)."""
+    assert lrx.as_tensor([1, 2]).dtype == np.float64
+    assert lrx.as_tensor(np.ones(2, np.complex64)).dtype == np.complex64
+    assert lrx.as_tensor([1.0], dtype="f32").dtype == np.float32
+    with pytest.raises(ValueError):
+        lrx.as_tensor([1], dtype=np.int32)
+    z = np.array([0.3 + 1.2j, -2.0 + 0.1j])
+    np.testing.assert_allclose(lrx.complex_exp(z), np.exp(z), rtol=1e-15)
+    re, im = lrx.complex_exp(z.real, z.imag)
+    np.testing.assert_allclose(re + 1j * im, np.exp(z), rtol=1e-15)
+    with pytest.raises(lrx.ShapeError):
+        lrx.complex_exp(np.zeros(2), np.zeros(3))
+    p = lrx.ComplexPair.from_complex(z.astype(np.complex64))
+    assert p.shape == (2,) and p.to_complex().dtype == np.complex64
+    np.testing.assert_allclose(p.to_complex(), z.astype(np.complex64))
+    with pytest.raises(lrx.ShapeError):
+        lrx.ComplexPair(np.zeros(2), np.zeros(3))
+    n0 = lrx.allocation_count()
+    lrx.alloc((3,), np.float32)
+    assert lrx.allocation_count() == n0 + 1
