@@ -71,6 +71,22 @@ def _slice_product(pre, b_delta, a_log):
     return torch.exp(-torch.exp(a_log)[None] * sd[..., None])
 
 
+
+def _all_gather(t, group):
+    """[world, *t.shape]: every rank's t.  NCCL gathers device tensors in place
+    (all_gather_into_tensor over NVLink); a gloo group (CPU tests, the
+    single-GPU multi-rank bench hook) gathers host copies."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = t.contiguous()
+    if dist.get_backend(group) == "gloo":
+        parts = [torch.empty_like(t, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, t.cpu(), group=group)
+        return torch.stack(parts).to(t.device)
+    out = torch.empty((world * t.shape[0], *t.shape[1:]), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return out.view(world, *t.shape)
+
 class SeqParallelS6:
     """Sequence-parallel selective scan over a process group (or simulated).
 
@@ -86,12 +102,7 @@ class SeqParallelS6:
 
     # -- collective helpers -------------------------------------------------
     def _gather(self, t):
-        import torch.distributed as dist
-        world = dist.get_world_size(self.group)
-        t = t.contiguous()
-        out = torch.empty((world * t.shape[0], *t.shape[1:]), dtype=t.dtype, device=t.device)
-        dist.all_gather_into_tensor(out, t, group=self.group)
-        return out.view(world, *t.shape)
+        return _all_gather(t, self.group)
 
     # -- forward / backward on this rank's slice ----------------------------
     def forward(self, u, pre, b_delta, a_log, Bk, Ck, Dskip):
@@ -183,12 +194,7 @@ class LongS6:
         return dist.get_rank(self.group), dist.get_world_size(self.group)
 
     def _gather(self, t):
-        import torch.distributed as dist
-        world = dist.get_world_size(self.group)
-        t = t.contiguous()
-        out = torch.empty((world * t.shape[0], *t.shape[1:]), dtype=t.dtype, device=t.device)
-        dist.all_gather_into_tensor(out, t, group=self.group)
-        return out.view(world, *t.shape)
+        return _all_gather(t, self.group)
 
     @staticmethod
     def _prod(a_log, sd):
