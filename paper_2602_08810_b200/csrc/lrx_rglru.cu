@@ -870,7 +870,9 @@ static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p) {
         for (int pf = 4; pf <= CK; pf *= 2) {
             if (!stages(pf, n_seg)) break;
             PF = pf;
-            if (warps * n_seg * pf >= kWork) break;
+            // bf16 streams half the bytes per element: the walk is issue-bound, so
+            // it takes twice the in-flight work (C4 bf16 fwd: PF 4 6.9 ms, PF 8 5.7 ms)
+            if (warps * n_seg * pf >= (sizeof(IO) == 2 ? 2 * kWork : kWork)) break;
         }
         if (PF) break;
     }
