@@ -1072,7 +1072,10 @@ static int bwd_t(const void* u, const void* qr, const void* qi, const void* lam,
     const bool rc_ok = ckpt && B * L < (1ll << 31) && (W * (int64_t)sizeof(IO)) % 16 == 0 && sizeof(IO) <= 4;
     if (rc_ok && (mode == 4 || (sizeof(IO) == 2 && (mode == 0 || mode == 1)))) {
         constexpr int RC = Tile<IO>::T;
-        const int LW = B * cdiv(W, 64) >= 4 * sm_count() ? 64 : 32;
+        // 128-channel CTAs when they still give 4 per SM (C4 bf16: 14.5 vs 15.3 ms at 64)
+        int LW = B * cdiv(W, 128) >= 4 * sm_count() ? 128 : B * cdiv(W, 64) >= 4 * sm_count() ? 64 : 32;
+        if (const char* e = getenv("LRX_RGLRU_RC_LW")) LW = atoi(e) >= 128 ? 128 : atoi(e) >= 64 ? 64 : 32;
+        const int S = env_int("LRX_RGLRU_RC_STAGES", 2);
         CUtensorMap m[4];
         const void* src[4] = {u, qr, qi, gy};
         bool ok = true;
@@ -1081,9 +1084,9 @@ static int bwd_t(const void* u, const void* qr, const void* qi, const void* lam,
             Carver cv(w);
             C* parts = cv.take<C>((size_t)3 * n);
             LRX_REQUIRE(w && cv.off <= wb, LRX_ERR_VALUE, "rglru workspace too small");
-            const int S = 2;
-            const int rc = LW == 64 ? launch_bwd_rc<IO, C, 64>(m, lam, br, bi, ckpt, gu, gqr, gqi, parts, B, L, W, S, st)
-                                    : launch_bwd_rc<IO, C, 32>(m, lam, br, bi, ckpt, gu, gqr, gqi, parts, B, L, W, S, st);
+            const int rc = LW == 128 ? launch_bwd_rc<IO, C, 128>(m, lam, br, bi, ckpt, gu, gqr, gqi, parts, B, L, W, S, st)
+                           : LW == 64 ? launch_bwd_rc<IO, C, 64>(m, lam, br, bi, ckpt, gu, gqr, gqi, parts, B, L, W, S, st)
+                                      : launch_bwd_rc<IO, C, 32>(m, lam, br, bi, ckpt, gu, gqr, gqi, parts, B, L, W, S, st);
             if (rc) return rc;
             return colsums<IO, C>(parts, 1, B, W, gla, gbr, gbi, st);
         }
