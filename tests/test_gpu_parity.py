@@ -412,9 +412,12 @@ def test_reduce_rows_matches_f64_and_is_deterministic(lrx, R, N):
 # ---- tcgen05 3xTF32 GEMM ---------------------------------------------------
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 256), (1000, 256, 256), (4096, 128, 256), (300, 64, 36),
-                                   (131072, 256, 256), (257, 200, 64)])
+                                   (131072, 256, 256), (257, 200, 64), (640, 96, 2560)])
 def test_gemm_f32_tcgen05_matches_f64(lrx, M, N, K):
     from paper_2602_08810_b200 import ops
+    # the tensor core's fp32 accumulation is not round-to-nearest: ~6e-8 per
+    # 8-wide K step (K = 2560: 1.5e-5 measured), still far inside 1e-4
+    tol = 1e-5 if K <= 1024 else 3e-5
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
     A = torch.randn((M, K), generator=g, device="cuda")
     Bt = torch.randn((N, K), generator=g, device="cuda")
@@ -422,12 +425,12 @@ def test_gemm_f32_tcgen05_matches_f64(lrx, M, N, K):
     cs = torch.randn(N, generator=g, device="cuda")
     ref = A.double() @ Bt.double().T
     C = ops.gemm_f32(A, Bt)
-    assert rel(C, ref.cpu().numpy()) < 1e-5
+    assert rel(C, ref.cpu().numpy()) < tol
     C2 = ops.gemm_f32(A, Bt, Cin=Cin, colscale=cs, alpha=2.0)
     ref2 = 2.0 * ref + cs.double() * Cin.double()
-    assert rel(C2, ref2.cpu().numpy()) < 1e-5
+    assert rel(C2, ref2.cpu().numpy()) < tol
     C3 = ops.gemm_f32(A, Bt, Cin=Cin, beta=-0.5)
-    assert rel(C3, (ref - 0.5 * Cin.double()).cpu().numpy()) < 1e-5
+    assert rel(C3, (ref - 0.5 * Cin.double()).cpu().numpy()) < tol
 
 
 @pytest.mark.parametrize("K,M,N", [(4096, 256, 256), (131072, 256, 256), (1000, 128, 64), (77, 64, 192),
