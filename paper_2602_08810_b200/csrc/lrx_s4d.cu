@@ -26,22 +26,26 @@ namespace s4d {
 constexpr int TT = 16;  // steps per tile (checkpoint interval)
 
 // transposed butterfly over lane bits HI..LO (see lrx_s6v3.cu tr_reduce)
-template <typename T, int V, int HI, int LO>
-__device__ __forceinline__ void tr_reduce(T* v) {
-    const int lane = threadIdx.x & 31;
-    int cnt = V;
-#pragma unroll
-    for (int m = HI; m >= LO; m >>= 1) {
-        const int half = cnt / 2;
-        const bool up = lane & m;
+// (one level per template instance: the halves are compile-time, so the
+// per-lane selection stays a value select and the arrays stay in registers)
+template <typename T, int CNT, int M, int LO>
+__device__ __forceinline__ void tr_level(T* v) {
+    if constexpr (M >= LO && CNT >= 2) {
+        constexpr int half = CNT / 2;
+        const bool up = (threadIdx.x & 31) & M;
 #pragma unroll
         for (int i = 0; i < half; ++i) {
-            const T send = up ? v[i] : v[i + half];
-            const T keep = up ? v[i + half] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+            const T a = v[i], b = v[i + half];
+            const T send = up ? a : b;
+            const T keep = up ? b : a;
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, M);
         }
-        cnt = half;
+        tr_level<T, half, M / 2, LO>(v);
     }
+}
+template <typename T, int V, int HI, int LO>
+__device__ __forceinline__ void tr_reduce(T* v) {
+    tr_level<T, V, HI, LO>(v);
 }
 
 // G = lanes per channel (min(N, 32)), NPL = states per lane (N / G)
