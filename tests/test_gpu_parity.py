@@ -186,9 +186,11 @@ def test_scan_operator_matches_reference(lrx, key):
         lrx.scan_backward(tape, z[key + ":gx"])
 
 
+@pytest.mark.parametrize("stream", ["0", "1"])  # chunked look-back / one-pass streaming walk
 @pytest.mark.parametrize("dt", [np.float32, np.float64, np.complex64, np.complex128])
 @pytest.mark.parametrize("L,N", [(1, 1), (2, 3), (255, 129), (4097, 300), (33, 5000)])
-def test_scan_operator_sizes_vs_oracle(lrx, dt, L, N):
+def test_scan_operator_sizes_vs_oracle(lrx, monkeypatch, dt, L, N, stream):
+    monkeypatch.setenv("LRX_SCAN_STREAM", stream)
     rng = port.Rng(L * 7 + N)
     cplx = np.dtype(dt).kind == "c"
 
