@@ -125,18 +125,28 @@ __global__ void __launch_bounds__(kLanes) scan_fwd_kernel(const V* __restrict__ 
 template <typename V> struct STile { static constexpr int T = 8; };
 template <> struct STile<cplx<double>> { static constexpr int T = 4; };
 
-template <typename V, bool PER_STEP>
+template <typename V, bool PER_STEP, bool AGG>
 __global__ void __launch_bounds__(kLanes) scan_fwd_stream_kernel(const V* __restrict__ a, const V* __restrict__ b,
                                                                  const V* __restrict__ x0, V* __restrict__ out,
-                                                                 int64_t L, int64_t N) {
+                                                                 V* __restrict__ mapA, V* __restrict__ mapX,
+                                                                 int64_t L, int64_t N, int64_t seg_len) {
+    // segment s = blockIdx.y walks [s seg_len, (s+1) seg_len); AGG: its map
+    // (prod a, state from 0) -> mapA / mapX; main: folds the maps of the
+    // segments to its left in a fixed order, then writes the states
     using Tr = Traits<V>;
     constexpr int T = STile<V>::T;
     const int64_t lane = (int64_t)blockIdx.x * kLanes + threadIdx.x;
     if (lane >= N) return;
+    const int s = blockIdx.y;
+    const int64_t tb = (int64_t)s * seg_len, te = min(L, tb + seg_len);
     const V ac = PER_STEP ? Tr::one() : ld(a + lane);
-    V x = x0 ? ld(x0 + lane) : Tr::zero();
-    for (int64_t t0 = 0; t0 < L; t0 += T) {
-        const int nt = (int)min((int64_t)T, L - t0);
+    V x = Tr::zero(), A = Tr::one();
+    if (!AGG) {
+        x = x0 ? ld(x0 + lane) : Tr::zero();
+        for (int r = 0; r < s; ++r) x = mapA[(int64_t)r * N + lane] * x + mapX[(int64_t)r * N + lane];
+    }
+    for (int64_t t0 = tb; t0 < te; t0 += T) {
+        const int nt = (int)min((int64_t)T, te - t0);
         V av[T], bv[T];
 #pragma unroll
         for (int k = 0; k < T; ++k) {
@@ -148,28 +158,76 @@ __global__ void __launch_bounds__(kLanes) scan_fwd_stream_kernel(const V* __rest
         for (int k = 0; k < T; ++k) {
             if (k < nt) {
                 x = av[k] * x + bv[k];
-                st(out + (t0 + k) * N + lane, x);
+                if (AGG) A = av[k] * A;
+                else st(out + (t0 + k) * N + lane, x);
             }
         }
     }
+    if (AGG) {
+        mapA[(int64_t)s * N + lane] = A;
+        mapX[(int64_t)s * N + lane] = x;
+    }
 }
 
+// backward aggregate of segment s: its cotangent map (prod conj a, the carry
+// leaving to the left from a zero carry entering on the right)
 template <typename V, bool PER_STEP>
-__global__ void __launch_bounds__(kLanes) scan_bwd_stream_kernel(const V* __restrict__ a, const V* __restrict__ x,
-                                                                 const V* __restrict__ x0, const V* __restrict__ gx,
-                                                                 V* __restrict__ gb, V* __restrict__ ga,
-                                                                 V* __restrict__ gx0, int64_t L, int64_t N) {
+__global__ void __launch_bounds__(kLanes) scan_bwd_agg_kernel(const V* __restrict__ a, const V* __restrict__ gx,
+                                                              V* __restrict__ mapA, V* __restrict__ mapH, int64_t L,
+                                                              int64_t N, int64_t seg_len) {
     using Tr = Traits<V>;
     constexpr int T = STile<V>::T;
     const int64_t lane = (int64_t)blockIdx.x * kLanes + threadIdx.x;
     if (lane >= N) return;
+    const int s = blockIdx.y + 1;  // segment 0's map is never folded
+    const int64_t tb = (int64_t)s * seg_len, te = min(L, tb + seg_len);
+    const V acst = PER_STEP ? Tr::one() : Tr::cj(ld(a + lane));
+    V h = Tr::zero(), A = Tr::one();
+    for (int64_t t1 = te; t1 > tb; t1 -= T) {
+        const int64_t t0 = max(tb, t1 - T);
+        const int nt = (int)(t1 - t0);
+        V acv[T], gxv[T];
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+            const int64_t off = (t0 + k) * N + lane;
+            gxv[k] = k < nt ? ld(gx + off) : Tr::zero();
+            acv[k] = PER_STEP ? (k < nt ? Tr::cj(ld(a + off)) : Tr::one()) : acst;
+        }
+#pragma unroll
+        for (int k = T - 1; k >= 0; --k) {
+            if (k < nt) {
+                h = acv[k] * (gxv[k] + h);
+                A = acv[k] * A;
+            }
+        }
+    }
+    mapA[(int64_t)s * N + lane] = A;
+    mapH[(int64_t)s * N + lane] = h;
+}
+
+// backward main: segment s walks right to left after folding the maps of the
+// segments to its right (fixed order); for a constant a its sum of
+// g conj(x_prev) lands in ga[s N + lane] (summed over segments by the caller)
+template <typename V, bool PER_STEP>
+__global__ void __launch_bounds__(kLanes) scan_bwd_stream_kernel(const V* __restrict__ a, const V* __restrict__ x,
+                                                                 const V* __restrict__ x0, const V* __restrict__ gx,
+                                                                 V* __restrict__ gb, V* __restrict__ ga,
+                                                                 V* __restrict__ gx0, const V* __restrict__ mapA,
+                                                                 const V* __restrict__ mapH, int64_t L, int64_t N,
+                                                                 int64_t seg_len) {
+    using Tr = Traits<V>;
+    constexpr int T = STile<V>::T;
+    const int64_t lane = (int64_t)blockIdx.x * kLanes + threadIdx.x;
+    if (lane >= N) return;
+    const int s = blockIdx.y, S = gridDim.y;
+    const int64_t tb = (int64_t)s * seg_len, te = min(L, tb + seg_len);
     const V acst = PER_STEP ? Tr::one() : Tr::cj(ld(a + lane));
     const V x0v = x0 ? ld(x0 + lane) : Tr::zero();
     V h = Tr::zero(), gsum = Tr::zero();
-    const int64_t nch = (L + T - 1) / T;
-    for (int64_t c = nch - 1; c >= 0; --c) {
-        const int64_t t0 = c * T;
-        const int nt = (int)min((int64_t)T, L - t0);
+    for (int r = S - 1; r > s; --r) h = mapA[(int64_t)r * N + lane] * h + mapH[(int64_t)r * N + lane];
+    for (int64_t t1 = te; t1 > tb; t1 -= T) {
+        const int64_t t0 = max(tb, t1 - T);
+        const int nt = (int)(t1 - t0);
         V acv[T], gxv[T], xpv[T];
 #pragma unroll
         for (int k = 0; k < T; ++k) {
@@ -194,19 +252,32 @@ __global__ void __launch_bounds__(kLanes) scan_bwd_stream_kernel(const V* __rest
             }
         }
     }
-    if (!PER_STEP && ga) st(ga + lane, gsum);
-    if (gx0) st(gx0 + lane, h);
+    if (!PER_STEP && ga) st(ga + (int64_t)s * N + lane, gsum);
+    if (gx0 && s == 0) st(gx0 + lane, h);
 }
 
-// Streaming walk when a time step's lanes carry enough bytes to keep HBM busy
-// (measured on B200: f32 / c64 at >= 512 KB per step 2-5x faster than the
-// look-back forward; the look-back backward loses already at 64 KB per step;
-// at a few KB per step, e.g. N = 1024, the chunked look-back wins by 10x).
-// LRX_SCAN_STREAM=0/1 forces either.
-static bool stream_ok(int64_t N, size_t esize, bool bwd) {
-    if (const char* e = getenv("LRX_SCAN_STREAM")) return atoi(e) != 0;
-    const int64_t bytes = N * (int64_t)esize;
-    return bytes >= (bwd ? (64 << 10) : (512 << 10));
+// Time segments of the streaming walk (S = 1: the whole sequence, one pass);
+// segments of >= 64 steps.
+// LRX_SCAN_SEGS overrides.
+static int64_t stream_segs(int64_t L, int64_t N, int64_t* seg_len) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t warps = cdiv(N, (int64_t)kLanes) * (kLanes / 32);
+    // lanes alone at >= 16 warps per SM stream best in one pass (c64 x 131072:
+    // 2.1 ms unsegmented vs 2.8 ms in 2 segments); fewer: ~32 warps per SM
+    int64_t S = warps >= (int64_t)sms * 16 ? 1 : cdiv((int64_t)sms * 32, warps);
+    if (const char* e = getenv("LRX_SCAN_SEGS")) S = std::max<int64_t>(1, atoll(e));
+    S = std::min<int64_t>(S, std::max<int64_t>(1, L / 64));
+    *seg_len = cdiv(cdiv(L, S), (int64_t)8) * 8;
+    return cdiv(L, *seg_len);
+}
+
+// The streaming walk (time-segmented when the lanes are few) is the default;
+// LRX_SCAN_STREAM=0 selects the single-pass chunked look-back kernels.
+static bool stream_ok() {
+    const char* e = getenv("LRX_SCAN_STREAM");
+    return !(e && atoi(e) == 0);
 }
 
 // ---------------------------------------------------------------- backward
@@ -533,14 +604,30 @@ static int carve(void* w, size_t wb, int64_t L, int64_t N, bool bwd, LookbackWS*
 template <typename V>
 static int fwd_t(int per_step, const void* a, const void* b, const void* x0, void* out, int64_t L, int64_t N,
                  void* w, size_t wb, cudaStream_t st) {
-    if (stream_ok(N, sizeof(V), false)) {
+    if (stream_ok()) {
+        int64_t seg;
+        const int64_t S = stream_segs(L, N, &seg);
+        LRX_REQUIRE(S == 1 || (w && wb >= (size_t)2 * S * N * sizeof(V)), LRX_ERR_VALUE, "scan workspace too small");
+        V* mA = static_cast<V*>(w);
+        V* mX = mA + S * N;
         const unsigned g = (unsigned)cdiv(N, kLanes);
+        int n = 1;
+        if (S > 1) {
+            if (per_step)
+                scan_fwd_stream_kernel<V, true, true><<<dim3(g, (unsigned)(S - 1)), kLanes, 0, st>>>(
+                    (const V*)a, (const V*)b, nullptr, nullptr, mA, mX, L, N, seg);
+            else
+                scan_fwd_stream_kernel<V, false, true><<<dim3(g, (unsigned)(S - 1)), kLanes, 0, st>>>(
+                    (const V*)a, (const V*)b, nullptr, nullptr, mA, mX, L, N, seg);
+            ++n;
+        }
         if (per_step)
-            scan_fwd_stream_kernel<V, true><<<g, kLanes, 0, st>>>((const V*)a, (const V*)b, (const V*)x0, (V*)out, L, N);
+            scan_fwd_stream_kernel<V, true, false><<<dim3(g, (unsigned)S), kLanes, 0, st>>>(
+                (const V*)a, (const V*)b, (const V*)x0, (V*)out, mA, mX, L, N, seg);
         else
-            scan_fwd_stream_kernel<V, false><<<g, kLanes, 0, st>>>((const V*)a, (const V*)b, (const V*)x0, (V*)out, L,
-                                                                   N);
-        return launched("lrx_scan_fwd/stream");
+            scan_fwd_stream_kernel<V, false, false><<<dim3(g, (unsigned)S), kLanes, 0, st>>>(
+                (const V*)a, (const V*)b, (const V*)x0, (V*)out, mA, mX, L, N, seg);
+        return launched("lrx_scan_fwd/stream", n);
     }
     int nc, nb;
     chunking<V>(L, N, &nc, &nb);
@@ -560,15 +647,36 @@ static int fwd_t(int per_step, const void* a, const void* b, const void* x0, voi
 template <typename V>
 static int bwd_t(int per_step, const void* a, const void* x, const void* x0, const void* gx, void* gb, void* ga,
                  void* gx0, int64_t L, int64_t N, void* w, size_t wb, cudaStream_t st) {
-    if (stream_ok(N, sizeof(V), true)) {
+    if (stream_ok()) {
+        int64_t seg;
+        const int64_t S = stream_segs(L, N, &seg);
+        const bool part = !per_step && ga && S > 1;  // constant a: per-segment partial sums
+        const size_t need = (size_t)(S > 1 ? 2 * S * N : 0) * sizeof(V) + (part ? (size_t)S * N * sizeof(V) : 0);
+        LRX_REQUIRE(need == 0 || (w && wb >= need), LRX_ERR_VALUE, "scan workspace too small");
+        V* mA = static_cast<V*>(w);
+        V* mH = mA + S * N;
+        V* gap = part ? mH + S * N : (V*)ga;
         const unsigned g = (unsigned)cdiv(N, kLanes);
+        int n = 1;
+        if (S > 1) {  // maps of segments 1 .. S-1
+            if (per_step)
+                scan_bwd_agg_kernel<V, true><<<dim3(g, (unsigned)(S - 1)), kLanes, 0, st>>>((const V*)a, (const V*)gx,
+                                                                                          mA, mH, L, N, seg);
+            else
+                scan_bwd_agg_kernel<V, false><<<dim3(g, (unsigned)(S - 1)), kLanes, 0, st>>>((const V*)a, (const V*)gx,
+                                                                                           mA, mH, L, N, seg);
+            ++n;
+        }
         if (per_step)
-            scan_bwd_stream_kernel<V, true><<<g, kLanes, 0, st>>>((const V*)a, (const V*)x, (const V*)x0,
-                                                                  (const V*)gx, (V*)gb, (V*)ga, (V*)gx0, L, N);
+            scan_bwd_stream_kernel<V, true><<<dim3(g, (unsigned)S), kLanes, 0, st>>>(
+                (const V*)a, (const V*)x, (const V*)x0, (const V*)gx, (V*)gb, (V*)ga, (V*)gx0, mA, mH, L, N, seg);
         else
-            scan_bwd_stream_kernel<V, false><<<g, kLanes, 0, st>>>((const V*)a, (const V*)x, (const V*)x0,
-                                                                   (const V*)gx, (V*)gb, (V*)ga, (V*)gx0, L, N);
-        return launched("lrx_scan_bwd/stream");
+            scan_bwd_stream_kernel<V, false><<<dim3(g, (unsigned)S), kLanes, 0, st>>>(
+                (const V*)a, (const V*)x, (const V*)x0, (const V*)gx, (V*)gb, (V*)gap, (V*)gx0, mA, mH, L, N, seg);
+        if (int rc = launched("lrx_scan_bwd/stream", n)) return rc;
+        if (!part) return LRX_OK;
+        reduce_rows_launch<V>(gap, (V*)ga, S, N, st);
+        return launched("lrx_scan_bwd/reduce");
     }
     int nc, nb;
     chunking<V>(L, N, &nc, &nb);
