@@ -14,6 +14,7 @@ current CUDA device; outputs are allocated here, workspaces are transient.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
@@ -96,7 +97,58 @@ def _s6_ws(geo, device, ws):
     return _lib.workspace(geo["ws_bytes"], device)
 
 
+class GroupedCkpt:
+    """Checkpoints of a d_state > 16 scan run as 16-state groups (one v3
+    checkpoint tensor per group); [:, -1] is the final state [B, D, N]."""
+
+    def __init__(self, parts):
+        self.parts = parts
+
+    def __getitem__(self, idx):
+        if idx != (slice(None), -1):
+            raise IndexError("GroupedCkpt supports [:, -1] (the final state) only")
+        return torch.cat([c[:, -1] for c in self.parts], dim=-1)
+
+
+def _grouped(u, D, N, x0=None, ws=None, flags=0):
+    """d_state a multiple of 16 above 16: the v3 kernels run per 16-state group
+    (the recurrence is diagonal; the readout and the gradients of u / pre are
+    sums over the groups, accumulated in fp32)."""
+    if N <= 16 or N % 16 or ws is not None or flags or u.dtype not in (torch.float32, torch.bfloat16):
+        return False
+    geo = s6_geometry(torch.float32, u.shape[0], u.shape[1], D, 16)
+    return geo["n_dblk"] > 0 and D % 4 == 0 and os.environ.get("LRX_S6_NOGROUP") != "1"
+
+
+def _group_args(a_log, Bk, Ck, Dskip, g):
+    sl = slice(16 * g, 16 * g + 16)
+    return (a_log[:, sl].contiguous(), Bk[..., sl].contiguous(), Ck[..., sl].contiguous(),
+            Dskip if g == 0 else torch.zeros_like(Dskip))
+
+
 def s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=None, ws=None, flags=0, ckpt=True):
+    """Selective scan; u [B, L, D] (f32/f64/bf16), pre [B, L, D] and Bk/Ck
+    [B, L, N] in compute precision.  x0 [B, D, N] optionally seeds the state.
+    Returns (y, ckpt); ckpt[:, -1] is the final state [B, D, N] (None with
+    ckpt=False: inference, no checkpoint writes).  `ws`/`flags`: workspace
+    holding per-segment maps from s6_fwd_carry (flags=S6_REUSE_AGG).
+    d_state = 32, 48, 64, ...: 16-state groups on the v3 kernels."""
+    B, L, D = u.shape
+    N = Bk.shape[-1]
+    if _grouped(u, D, N, x0, ws, flags):
+        u32 = u.float()
+        y, parts = None, []
+        for g in range(N // 16):
+            ag, Bg, Cg, Dg = _group_args(a_log, Bk, Ck, Dskip, g)
+            x0g = x0[..., 16 * g:16 * g + 16].contiguous() if x0 is not None else None
+            yg, ckg = s6_scan_fwd(u32, pre, b_delta, ag, Bg, Cg, Dg, x0=x0g, ckpt=ckpt)
+            y = yg if y is None else y.add_(yg)
+            parts.append(ckg)
+        return y.to(u.dtype), (GroupedCkpt(parts) if ckpt else None)
+    return _s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0, ws, flags, ckpt)
+
+
+def _s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=None, ws=None, flags=0, ckpt=True):
     """Selective scan; u [B, L, D] (f32/f64/bf16), pre [B, L, D] and Bk/Ck
     [B, L, N] in compute precision.  x0 [B, D, N] optionally seeds the state.
     Returns (y, ckpt); ckpt[:, -1] is the final state [B, D, N] (None with
@@ -116,6 +168,32 @@ def s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=None, ws=None, flags=0
 
 
 def s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in=None, want_h_out=False, ws=None, flags=0):
+    if isinstance(ckpt, GroupedCkpt):
+        if h_in is not None or want_h_out:
+            raise ValueError("carries across ranks need d_state == 16")
+        B, L, D = u.shape
+        u32, gy32 = u.float(), gy.float()
+        out = None
+        for g, ckg in enumerate(ckpt.parts):
+            ag, Bg, Cg, Dg = _group_args(a_log, Bk, Ck, Dskip, g)
+            r = _s6_scan_bwd(u32, pre, b_delta, ag, Bg, Cg, Dg, ckg, gy32)
+            if out is None:
+                out = {"gu_local": r["gu_local"], "gpre": r["gpre"], "gBk": [r["gBk"]], "gCk": [r["gCk"]],
+                       "ga_log": [r["ga_log"]], "gD": r["gD"], "gb_delta": r["gb_delta"]}
+            else:  # fixed group order
+                out["gu_local"].add_(r["gu_local"])
+                out["gpre"].add_(r["gpre"])
+                out["gb_delta"].add_(r["gb_delta"])
+                for k in ("gBk", "gCk", "ga_log"):
+                    out[k].append(r[k])
+        out["gu_local"] = out["gu_local"].to(u.dtype)
+        for k in ("gBk", "gCk", "ga_log"):
+            out[k] = torch.cat(out[k], dim=-1)
+        return out
+    return _s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in, want_h_out, ws, flags)
+
+
+def _s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in=None, want_h_out=False, ws=None, flags=0):
     """Pullback of s6_scan_fwd.  Returns dict: gu_local (D gy + delta sum_n g B),
     gpre (d/d pre) [B, L, D]; gBk, gCk [B, L, N]; ga_log [D, N]; gD, gb_delta [D];
     with want_h_out also h_out [B, D, N] = d loss / d x0.  h_in [B, D, N] is

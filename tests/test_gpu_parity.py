@@ -154,6 +154,30 @@ def test_layer_matches_oracle_multichunk(lrx, kind, m, n, B, L, dtype):
         assert rel(g.params[k], rg[k]) < tol, (k, rel(g.params[k], rg[k]))
 
 
+@pytest.mark.parametrize("n", [32, 64])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_s6_wide_state_groups_match_oracle(lrx, n, dtype):
+    """d_state 32 / 64 run as 16-state groups on the v3 kernels (fp32 sums over
+    the groups); prefill state for step mode comes from the grouped checkpoints."""
+    m, B, L = 24, 2, 700
+    layer = lrx.make_layer("s6", m, n, dtype=dtype, seed=81)
+    io = torch.bfloat16 if dtype == "bf16" else torch.float32
+    u = torch.from_numpy(port.Rng(82).normal((B, L, m))).to("cuda", io)
+    gy = torch.from_numpy(port.Rng(83).normal((B, L, m))).to("cuda", io)
+    y, tape = layer.forward(u, tape=True)
+    g = lrx.layer_backward(layer, tape, gy)
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64("s6", None, params, u.float().cpu().numpy(), gy.float().cpu().numpy())
+    tol = TOL[dtype]
+    assert rel(y, ry) < tol
+    assert rel(g.u, rgu) < tol
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < tol, (k, rel(g.params[k], rg[k]))
+    _, st = layer.forward(u[:, :300], return_state=True)
+    yk, st = layer.step(st, u[:, 300])
+    assert rel(yk.float(), ry[:, 300]) < tol
+
+
 @pytest.mark.parametrize("kind", ["s6", "rglru"])
 def test_bf16_io_matches_f64_oracle(lrx, kind):
     m, n, B, L = (64, 16, 2, 1200) if kind == "s6" else (256, None, 2, 1500)
