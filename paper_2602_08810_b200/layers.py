@@ -411,13 +411,22 @@ class S4D(LinearRecurrence):
             abar, scale = scheme_factors(self.discretization, lam, deff[..., None])
         return lam, delta, b, abar, scale
 
-    def _fused(self, deltas):
+    def _fused(self, deltas, shape):
         """Fused S4D kernel (csrc/lrx_s4d.cu) for constant steps and d_state
-        in {8, 16, 32, 64}; per-step deltas keep the generic operator path."""
-        return deltas is None and self.d_state in ops.S4D_FUSED_N and os.environ.get("LRX_S4D_GENERIC") != "1"
+        in {8, 16, 32, 64}; per-step deltas keep the generic operator path, and
+        so do long sequences over few channels, where the fused kernel's one
+        walk per lane is latency-bound and the time-segmented generic scan wins
+        (measured: B1 L65536 H64 N64 24.6 vs 8.7 ms; B8 L4096 H256 N64 3.2 vs
+        25.8 ms the other way)."""
+        env = os.environ.get("LRX_S4D_GENERIC")
+        if deltas is not None or self.d_state not in ops.S4D_FUSED_N or env == "1":
+            return False
+        B, L, m = shape
+        threads = B * m * min(self.d_state, 32)
+        return env == "0" or not (threads < 148 * 32 * 3 // 2 and L >= 8192)
 
     def _forward(self, u, deltas, keep):
-        if self._fused(deltas):
+        if self._fused(deltas, u.shape):
             lam, delta, b, abar, scale = self._coeffs(None)
             w = (scale * b).to(self.tcdt).contiguous()
             c = torch.complex(self.c_re, self.c_im).contiguous()
