@@ -485,51 +485,108 @@ def run_e2e(args, w, prob, device):
 # ---------------------------------------------------------------------------
 # CPU reference arm (oracle restatement of the reference algorithm)
 
-def cpu_sample(w, budget_s=12.0, seed=0):
-    """Bounded sample of the workload on the host's cores: (Gelem/s, desc, cores)."""
+# Sample shapes of the CPU arms: identical B / H / N,
+# C1 and C2 at full length, C3 / C4 at L/64, C5 at L/1024 (its L/64 sample
+# alone would take ~30 s per step).  Time scales linearly in L for a scan.
+CPU_TIMED_L = {"lru": 1024, "s5": 4096, "s6": 8192 // 64, "rglru": 16384 // 64, "s6_long": 2 ** 20 // 1024}
+
+
+def cpu_problem(w, workload, cores, seed=0):
+    """One fwd+bwd of the reference algorithm (the oracle restatement: numpy +
+    the C restatement of the numba loops, time-chunk parallel over `cores`
+    workers as the reference's mode="parallel") on the sample shape.
+    Returns (run, elems, desc)."""
     from oracle import port
 
-    kind, H, N = w["kind"], w["H"], w["N"]
-    cores = os.cpu_count() or 1
+    kind, B, H, N = w["kind"], w["B"], w["H"], w["N"]
+    L = CPU_TIMED_L[workload]
     dt = np.float32
     p = port.init_params(kind, H, None if kind == "rglru" else (N if kind != "s5" else 2 * N), dtype="f32",
                          seed=seed)
-    # sample: one batch row, L chosen so one fwd+bwd is a few seconds
-    B, L = {"rglru": (2, 1024), "s6": (2, 256), "s5": (8, 512), "lru": (8, 1024)}[kind]
-    if kind == "s6" and H > 1536:
-        B = 1
     rng = port.Rng(seed + 1)
     u = rng.normal((B, L, H)).astype(dt)
     gy = rng.normal((B, L, H)).astype(dt)
     if kind == "rglru":
         qr, qi = u @ p["W_r"].T, u @ p["W_i"].T
 
-        def one():
+        def run():
             port.rglru_scan(u, qr, qi, p["lambda_param"], p["b_r"], p["b_i"], gy, "parallel", cores)
     elif kind == "s6":
         pre = (u @ p["W_delta"]) @ p["W_delta_proj"]
         Bk, Ck = u @ p["W_B"].T, u @ p["W_C"].T
 
-        def one():
+        def run():
             port.s6_scan(u, pre, p["b_delta"], p["a_log"], Bk, Ck, p["D"], gy, "parallel", cores)
     else:
         lay = port.Layer(kind, p)
 
-        def one():
-            y, s = lay.forward(u, "parallel", cores)
-            lay.backward(s, gy)
-    one()  # warm (pools, page-in)
-    n, t0 = 0, time.perf_counter()
-    while True:
-        one()
-        n += 1
-        if time.perf_counter() - t0 > budget_s or n >= 20:
-            break
+        def run():
+            y, sv = lay.forward(u, "parallel", cores)
+            lay.backward(sv, gy)
+    desc = (f"{kind} B={B} L={L} (of {w['L']}) H={H} N={N} f32, fwd+bwd at the same operator boundary, "
+            f"reference algorithm (oracle port), mode='parallel' workers={cores}")
+    return run, B * L * H * N, desc
+
+
+def _blas_threads(n):
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=n)
+    except Exception:  # pragma: no cover - threadpoolctl is in the image
+        import contextlib
+        return contextlib.nullcontext()
+
+
+def cpu_sample(w, workload, budget_s=12.0, cores=None, seed=0):
+    """Rate of the reference algorithm on the host's cores: (Gelem/s, desc, cores, ms per sample)."""
+    cores = cores or os.cpu_count() or 1
+    with _blas_threads(cores):
+        run, elems, desc = cpu_problem(w, workload, cores, seed)
+        run()  # warm (pools, page-in)
+        n, t0 = 0, time.perf_counter()
+        while True:
+            run()
+            n += 1
+            if time.perf_counter() - t0 > budget_s or n >= 20:
+                break
     dt_s = (time.perf_counter() - t0) / n
-    elems = B * L * H * N
-    desc = (f"{kind} B={B} L={L} H={H} N={N} f32, fwd+bwd at the same operator boundary, "
-            f"parallel mode workers={cores}, mean of {n} runs")
-    return elems / dt_s / 1e9, desc, cores
+    return elems / dt_s / 1e9, f"{desc}, mean of {n} runs", cores, dt_s * 1e3
+
+
+def reference_arm(args, w, config):
+    """--impl reference: the reference's CPU algorithm on all host cores, one
+    sample step per timed step (measured, not extrapolated), then one 1-core
+    step for the single-thread row."""
+    cores = os.cpu_count() or 1
+    with _blas_threads(cores):
+        run, elems, desc = cpu_problem(w, args.workload, cores)
+        for _ in range(args.warmup):
+            run()
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            run()
+            times.append(time.perf_counter() - t0)
+    ms = float(np.mean(times)) * 1e3
+    v = elems / (ms * 1e-3) / 1e9
+    with _blas_threads(1):
+        run1, _, desc1 = cpu_problem(w, args.workload, 1)
+        t0 = time.perf_counter()
+        run1()
+        ms1 = (time.perf_counter() - t0) * 1e3
+    L_t = CPU_TIMED_L[args.workload]
+    cfg = dict(config, timed_L=L_t,
+               timing=(f"measured at L={L_t} with the config's B/H/N (value = rate of the timed sample; "
+                       f"a full-L step takes ms_per_step x {w['L'] // L_t}, linear in L)"
+                       if L_t != w["L"] else "measured at the full config"))
+    return {"metric": METRIC, "value": v, "unit": "Gelem/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference", "config": cfg,
+            "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "port",
+                             "sample": f"{desc}, mean of {args.steps} steps",
+                             "one_core": {"value": elems / (ms1 * 1e-3) / 1e9, "unit": "Gelem/s", "cores": 1,
+                                          "ms": ms1, "sample": f"{desc1}, OpenBLAS 1 thread, one step"}},
+            "e2e": {"value": v, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def main():
@@ -559,22 +616,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
-        for _ in range(args.warmup):
-            cpu_sample(w, budget_s=min(budget, 3.0))
-        vals = []
-        for _ in range(args.steps):
-            v, desc, cores = cpu_sample(w, budget_s=budget)
-            vals.append(v)
-        v = float(np.mean(vals))
-        print(json.dumps({"metric": METRIC, "value": v, "unit": "Gelem/s", "n_gpus": args.gpus, "steps": args.steps,
-                          "warmup": args.warmup, "ms_per_step": elems / (v * 1e9) * 1e3, "higher_is_better": True,
-                          "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                          "impl": "reference", "config": config,
-                          "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "port",
-                                           "sample": desc},
-                          "e2e": {"value": v, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
-              flush=True)
+        print(json.dumps(reference_arm(args, w, config)), flush=True)
         return
 
     import torch
@@ -623,7 +665,7 @@ def main():
                                "peak_source": "tools/ubench/mufu.cu on this pool's B200 (ex2.approx.f32)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v, desc, cores = cpu_sample(w)
+        v, desc, cores, _ = cpu_sample(w, args.workload)
         cpu = {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "port", "sample": desc}
     e = r["e2e"]
     e2e = {"value": e["elems"] * world / (e["ms"] * 1e-3) / 1e9, "unit": "Gelem/s",
@@ -635,7 +677,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": {"f32": "f32", "bf16": "bf16 io / f32 accum"}[w["dtype"]],
             "data": "synthetic (reference init, N(0,1) activations, projections from the layer's weights)",
-            "config": dict(config, cuda_graphs=r["graphed"]), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "config": config, "cuda_graphs": r["graphed"], "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": r["launches"],
             "clocks": r["clocks"],
             "kernels": {"fwd_ms": r["ms_fwd"], "bwd_ms": r["ms_bwd"],

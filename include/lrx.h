@@ -95,7 +95,8 @@ int lrx_scan_bwd(int dtype, int a_per_step, const void* a, const void* x, const 
  * qr = u W_r^T and qi = u W_i^T are the layer's gate GEMM outputs (bias not
  * added).  io_dtype in {F32, F64, BF16}; params (lambda, b_r, b_i) are F32 for
  * F32/BF16 I/O and F64 for F64 I/O.  ckpt receives the state entering every
- * time chunk ([n_chunks, B*W], compute precision) for the recomputing backward.
+ * time chunk and, in its last row, the final state ([n_chunks + 1, B*W],
+ * compute precision): the backward's reconstruction anchors.
  * ------------------------------------------------------------------------ */
 int lrx_rglru_chunking(int io_dtype, int64_t L, int64_t* chunk_len, int64_t* n_chunks);
 size_t lrx_rglru_workspace_bytes(int io_dtype, int64_t B, int64_t L, int64_t W);
@@ -106,9 +107,11 @@ int lrx_rglru_fwd(int io_dtype, const void* u, const void* qr, const void* qi, c
  * gqi W_i are the caller's), gqr, gqi ([B, L, W], io dtype), and the
  * parameter-gradient sums over batch and time gla = sum 8 r dlog(a),
  * gb_r = sum gqr, gb_i = sum gqi ([W], compute precision; fixed-order,
- * compensated).  y is the forward output (= the state); when given (f32/f64
- * I/O) the backward streams it instead of recomputing, otherwise it
- * recomputes from ckpt.  Workspace: lrx_rglru_workspace_bytes(). */
+ * compensated).  The default walk reconstructs x_{t-1} = (x_t - b_t) / a_t
+ * from the gates it evaluates for the pullback, re-anchored on ckpt at every
+ * chunk boundary (<= 7 reconstructed steps).  y (the forward output = the
+ * state) is read only by the y-streaming variant (LRX_RGLRU_MODE=tma, f32/f64
+ * I/O) and may be NULL.  Workspace: lrx_rglru_workspace_bytes(). */
 int lrx_rglru_bwd(int io_dtype, const void* u, const void* qr, const void* qi, const void* lambda_param,
                   const void* b_r, const void* b_i, const void* ckpt, const void* y, const void* gy,
                   void* gu_local, void* gqr, void* gqi, void* gla, void* gb_r, void* gb_i, int64_t B,

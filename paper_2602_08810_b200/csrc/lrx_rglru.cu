@@ -41,8 +41,13 @@ namespace rglru {
 constexpr int kThreads = 128;
 constexpr float kGate = 8.0f;  // GATE_POWER, layers.py:1177
 
-template <typename IO> struct Tile { static constexpr int T = 16; };
-template <> struct Tile<double> { static constexpr int T = 8; };
+// Checkpoint interval: the forward saves the state entering every T-step
+// chunk (plus the final state); the backward re-anchors its reverse state
+// reconstruction there, so no reconstruction runs deeper than T - 1 steps.
+template <typename IO> struct Tile { static constexpr int T = 8; };
+// Largest TMA time tile (rows per barrier wait).
+template <typename IO> struct MaxPF { static constexpr int T = 16; };
+template <> struct MaxPF<double> { static constexpr int T = 8; };
 
 template <typename C>
 struct Coef {
@@ -176,8 +181,7 @@ __global__ void __launch_bounds__(LW, PF == 4 && LW >= 64 ? 1152 / LW : 1) fwd_t
     if (!AGG && valid)
         for (int r = 0; r < seg; ++r) x = Fast<C>::exp(seg_a[r * BW + lane]) * x + seg_x[r * BW + lane];
     IO* py = y + ((int64_t)row0 + t_beg) * W + w;
-    C* pc = ckpt ? ckpt + (t_beg / CK) * BW + lane : nullptr;
-    static_assert(CK % PF == 0, "checkpoint interval must be a multiple of the tile");
+    static_assert(CK % PF == 0 || PF % CK == 0, "tile and checkpoint interval must nest");
     for (int j = 0; j < n_tiles; ++j) {
         const int s = j % S;
         const uint32_t ph = (j / S) & 1;
@@ -196,11 +200,9 @@ __global__ void __launch_bounds__(LW, PF == 4 && LW >= 64 ? 1152 / LW : 1) fwd_t
             tma::mbar_wait(&R.empty[s], ph);
             issue(j + S);
         }
-        if (!AGG && pc && (j % (CK / PF)) == 0) {  // state entering this checkpoint chunk
-            if (valid) __stcs(pc, x);
-            pc += BW;
-        }
-        const int nk = (int)min((int64_t)PF, t_end - (int64_t)(j_beg + j) * PF);
+        const int64_t t0 = (int64_t)(j_beg + j) * PF;
+        const int nk = (int)min((int64_t)PF, t_end - t0);
+        const C xin = x;
         // the whole-tile case runs without per-step guards; stores are
         // predicated once per tile
         C tla = 0, xs[PF];
@@ -221,6 +223,11 @@ __global__ void __launch_bounds__(LW, PF == 4 && LW >= 64 ? 1152 / LW : 1) fwd_t
         if (AGG) {
             sla += tla;
         } else {
+            if (ckpt && valid) {  // the state entering each checkpoint chunk of the tile
+#pragma unroll
+                for (int k = 0; k < PF; k += (PF < CK ? PF : CK))
+                    if (k < nk && ((t0 + k) % CK) == 0) __stcs(ckpt + ((t0 + k) / CK) * BW + lane, k ? xs[k - 1] : xin);
+            }
             if (valid) {
                 if (nk == PF) {
 #pragma unroll
@@ -238,6 +245,7 @@ __global__ void __launch_bounds__(LW, PF == 4 && LW >= 64 ? 1152 / LW : 1) fwd_t
         seg_a[seg * BW + lane] = sla;
         seg_x[seg * BW + lane] = x;
     }
+    if (!AGG && ckpt && valid && t_end == L) __stcs(ckpt + ((L + CK - 1) / CK) * BW + lane, x);  // final state
 }
 
 // Reverse streaming pass; the y tile of a time tile is loaded one row early
@@ -398,6 +406,154 @@ __global__ void __launch_bounds__(LW, PF == 4 && LW >= 64 ? 1152 / LW : 1) bwd_t
         gbr_part[p] = sbr.s;
         gbi_part[p] = sbi.s;
     }
+}
+
+// Backward without the y stream and with one gate evaluation per element:
+// the reverse walk reconstructs the state it needs, x_{t-1} = (x_t - b_t) / a_t,
+// from the gates it evaluates anyway for the pullback.  The division expands
+// rounding errors by 1/a per step, so the walk re-anchors on the forward's
+// checkpoints: x_t at the end of every T-step chunk and x_{t-1} at its start
+// are the saved states (exact), leaving at most T - 1 = 7 reconstructed steps
+// (measured on C4-distributed gates: 2.5e-6 max-normalised state error at
+// T = 8 against 1.2e-4 at T = 16).  Streams u, qr, qi, gy in and gu, gqr, gqi
+// out -- the 7 algorithmic arrays -- plus 1/T of a state array of anchors.
+// Segmented like bwd_tma_kernel (its AGG pass supplies the segment maps).
+template <typename IO, typename C, int LW, int PF>
+__global__ void __launch_bounds__(LW, PF == 4 && LW >= 64 ? 1152 / LW : 1) bwd_rev_kernel(
+    const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mr,
+    const __grid_constant__ CUtensorMap mi, const __grid_constant__ CUtensorMap mg, const C* __restrict__ lam,
+    const C* __restrict__ b_r, const C* __restrict__ b_i, const C* __restrict__ ckpt, IO* __restrict__ gu,
+    IO* __restrict__ gqr, IO* __restrict__ gqi, C* __restrict__ gla_part, C* __restrict__ gbr_part,
+    C* __restrict__ gbi_part, const C* __restrict__ seg_a, const C* __restrict__ seg_h, int64_t L, int64_t W,
+    int n_wblk, int Bn, int S, int seg_len, int n_seg) {
+    constexpr int NW = LW / 32;
+    constexpr int NA = 4;  // u, qr, qi, gy
+    constexpr int CK = Tile<IO>::T;
+    static_assert(CK % PF == 0 || PF % CK == 0, "tile and checkpoint interval must nest");
+    extern __shared__ __align__(128) unsigned char smem[];
+    auto R = ring<IO>(smem, S);
+    const int tid = threadIdx.x;
+    const int b = blockIdx.x / n_wblk;
+    const int w0 = (blockIdx.x % n_wblk) * LW;
+    const int64_t w = w0 + tid;
+    const bool valid = w < W;
+    const int seg = blockIdx.y;
+    const int64_t t_beg = (int64_t)seg * seg_len;
+    const int64_t t_end = min(L, t_beg + seg_len);
+    const int j_beg = (int)(t_beg / PF);
+    const int n_tiles = (int)((t_end + PF - 1) / PF) - j_beg;
+    const int row0 = b * (int)L;
+    constexpr uint32_t kStageBytes = (uint32_t)NA * PF * LW * sizeof(IO);
+    if (tid == 0) {
+        tma::prefetch_map(&mu);
+        tma::prefetch_map(&mr);
+        tma::prefetch_map(&mi);
+        tma::prefetch_map(&mg);
+        for (int s = 0; s < S; ++s) {
+            tma::mbar_init(&R.full[s], 1);
+            tma::mbar_init(&R.empty[s], NW);
+        }
+        tma::fence_barrier_init();
+    }
+    __syncthreads();
+    auto issue = [&](int j) {  // j-th tile in reverse order
+        const int tt = j_beg + n_tiles - 1 - j;
+        const int s = j % S;
+        IO* dst = R.data + (size_t)s * NA * PF * LW;
+        const int r = row0 + tt * PF;
+        tma::mbar_arrive_expect_tx(&R.full[s], kStageBytes);
+        tma::load_2d(dst, &mu, w0, r, &R.full[s]);
+        tma::load_2d(dst + PF * LW, &mr, w0, r, &R.full[s]);
+        tma::load_2d(dst + 2 * PF * LW, &mi, w0, r, &R.full[s]);
+        tma::load_2d(dst + 3 * PF * LW, &mg, w0, r, &R.full[s]);
+    };
+    if (tid == 0)
+        for (int j = 0; j < S && j < n_tiles; ++j) issue(j);
+
+    C la = 0, br = 0, bi = 0;
+    if (valid) {
+        la = -Math<C>::softplus(-lam[w]);
+        br = b_r[w];
+        bi = b_i[w];
+    }
+    const int64_t BW = (int64_t)Bn * W;
+    const int64_t lane = (int64_t)b * W + (valid ? w : 0);
+    C h = 0;
+    if (valid)
+        for (int r = n_seg - 1; r > seg; --r) h = Fast<C>::exp(seg_a[r * BW + lane]) * h + seg_h[r * BW + lane];
+    // x = the state after the step being walked; anc = the saved state entering
+    // the next chunk start below it (prefetched one chunk ahead)
+    const C* pck = ckpt + lane;
+    C x = __ldcg(pck + ((t_end + CK - 1) / CK) * BW);
+    int64_t c_next = (t_end - 1) / CK;
+    C anc = __ldcg(pck + c_next * BW);
+    Kahan<C> sla, sbr, sbi;
+    IO *pgu = gu + (int64_t)row0 * W + w, *pgr = gqr + (int64_t)row0 * W + w, *pgi = gqi + (int64_t)row0 * W + w;
+    for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % S;
+        const uint32_t ph = (j / S) & 1;
+        const int tt = j_beg + n_tiles - 1 - j;
+        tma::mbar_wait(&R.full[s], ph);
+        const IO* src = R.data + (size_t)s * NA * PF * LW + tid;
+        IO cu[PF], cr[PF], ci[PF], cg[PF];
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            cu[k] = src[k * LW];
+            cr[k] = src[(PF + k) * LW];
+            ci[k] = src[(2 * PF + k) * LW];
+            cg[k] = src[(3 * PF + k) * LW];
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) tma::mbar_arrive(&R.empty[s]);
+        if (tid == 0 && j + S < n_tiles) {
+            tma::mbar_wait(&R.empty[s], ph);
+            issue(j + S);
+        }
+        const int64_t t0 = (int64_t)tt * PF;
+        const int nk = (int)min((int64_t)PF, t_end - t0);
+        C tla = 0, tbr = 0, tbi = 0;
+        const int64_t o0 = t0 * W;
+        IO *qu = pgu + o0, *qr = pgr + o0, *qi = pgi + o0;
+        auto step = [&](int k) {
+            const Coef<C> q = gates<C>(cu[k], cr[k], ci[k], la, br, bi);
+            const C g = C(cvt(cg[k])) + h;
+            h = q.a * g;
+            C xprev;
+            if (((t0 + k) % CK) == 0) {  // chunk start: the saved state
+                xprev = anc;
+                c_next -= 1;
+                anc = (c_next >= 0 && valid) ? __ldcg(pck + c_next * BW) : C(0);
+            } else {
+                xprev = (x - (q.s * q.i) * q.u) * Fast<C>::rcp(q.a);
+            }
+            const BwdOut<C> o = bwd_step<C>(q, g, xprev, la);
+            x = xprev;
+            if (valid) {
+                st_io(qu + k * W, o.gu);
+                st_io(qr + k * W, o.gqr);
+                st_io(qi + k * W, o.gqi);
+            }
+            tla += o.la_term;
+            tbr += o.gqr;
+            tbi += o.gqi;
+        };
+        if (nk == PF) {
+#pragma unroll
+            for (int k = PF - 1; k >= 0; --k) step(k);
+        } else {
+#pragma unroll
+            for (int k = PF - 1; k >= 0; --k)
+                if (k < nk) step(k);
+        }
+        sla.add(tla);
+        sbr.add(tbr);
+        sbi.add(tbi);
+    }
+    if (!valid) return;
+    const int64_t p = seg * BW + lane;
+    gla_part[p] = sla.s;
+    gbr_part[p] = sbr.s;
+    gbi_part[p] = sbi.s;
 }
 
 // Backward without the y stream: time tiles of one checkpoint chunk (RC = 16
@@ -579,6 +735,7 @@ __global__ void __launch_bounds__(kThreads) fwd_stream_kernel(
             }
         }
     }
+    if (pc) __stcs(ckpt + ((L + CK - 1) / CK) * ck_stride + (int64_t)b * W + w, x);  // final state
 }
 
 // ================================================================== lookback
@@ -653,6 +810,8 @@ __global__ void __launch_bounds__(kThreads, 4) fwd_kernel(const IO* __restrict__
         if (valid && k < nt) st_io(py, x);
         py += W;
     }
+    // final state (the padded steps past L keep x: a = 1, b = 0)
+    if (valid && ckpt && t0 + nt == L) ckpt[((int64_t)(c + 1) * Bn + b) * W + w] = x;
 }
 
 // Backward.  Reverse recurrence g_k = gy_k + a_{k+1} g_{k+1}; the carry passed
@@ -771,7 +930,8 @@ __global__ void colsum_kernel(const C* __restrict__ in, C* __restrict__ out, int
 // ====================================================================== host
 static int mode_env() {  // read per call so tests can switch kernels in-process
     const char* e = getenv("LRX_RGLRU_MODE");
-    return !e ? 0 : !strcmp(e, "tma") ? 1 : !strcmp(e, "stream") ? 2 : !strcmp(e, "lookback") ? 3 : !strcmp(e, "rc") ? 4 : 0;
+    return !e ? 0 : !strcmp(e, "tma") ? 1 : !strcmp(e, "stream") ? 2 : !strcmp(e, "lookback") ? 3 : !strcmp(e, "rc") ? 4
+                  : !strcmp(e, "rev") ? 5 : 0;
 }
 
 static int sm_count() {
@@ -867,7 +1027,7 @@ static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p) {
     int64_t n_seg = warps < 6 ? std::min<int64_t>(max_seg, (int64_t)std::ceil(12 / warps)) : 1;
     int PF = 0;
     for (; n_seg >= 1 && !PF; n_seg = n_seg > 1 ? n_seg - 1 : 0) {
-        for (int pf = 4; pf <= CK; pf *= 2) {
+        for (int pf = 4; pf <= MaxPF<IO>::T; pf *= 2) {
             if (!stages(pf, n_seg)) break;
             PF = pf;
             // bf16 streams half the bytes per element: the walk is issue-bound, so
@@ -877,10 +1037,12 @@ static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p) {
         if (PF) break;
     }
     if (!PF) return false;
-    if (const char* e = getenv("LRX_RGLRU_PF")) PF = std::min(CK, atoi(e) >= 16 ? 16 : atoi(e) >= 8 ? 8 : 4);
+    if (const char* e = getenv("LRX_RGLRU_PF")) PF = std::min(MaxPF<IO>::T, atoi(e) >= 16 ? 16 : atoi(e) >= 8 ? 8 : 4);
     if (const char* e = getenv("LRX_RGLRU_SEGS"))
         n_seg = std::max<int64_t>(1, std::min<int64_t>({(int64_t)atoi(e), 64, std::max<int64_t>(1, L / 64)}));
-    const int64_t len = cdiv(cdiv(L, n_seg), (int64_t)CK) * CK;
+    // segments start on a tile and on a checkpoint boundary
+    constexpr int64_t kAlign = CK > MaxPF<IO>::T ? CK : MaxPF<IO>::T;
+    const int64_t len = cdiv(cdiv(L, n_seg), kAlign) * kAlign;
     p->seg_len = (int)std::min<int64_t>(len, 1ll << 30);
     p->n_seg = (int)cdiv(L, len);
     while (!(p->S = stages(PF, p->n_seg)) && PF > 4) PF /= 2;  // overrides that do not fit
@@ -948,6 +1110,42 @@ static int launch_bwd_tma(const TmaPlan& pl, const TmaPlan& pa, const CUtensorMa
     return launched("lrx_rglru_bwd/tma");
 }
 
+// Reverse-reconstruction backward (4 staged arrays + anchors); the AGG pass
+// is bwd_tma_kernel's (it stages qr and gy only).
+template <typename IO, typename C, int LW, int PF>
+static int launch_bwd_rev(const TmaPlan& pl, const TmaPlan& pa, const CUtensorMap* m, const void* lam,
+                          const void* br, const void* bi, const void* ckpt, void* gu, void* gqr, void* gqi, C* parts,
+                          C* seg, int64_t B, int64_t L, int64_t W, cudaStream_t st) {
+    const int64_t n = (int64_t)pl.n_seg * B * W;
+    if (pl.n_seg > 1) {
+        auto a = bwd_tma_kernel<IO, C, LW, PF, true>;
+        if (int rc = reserve_smem(a, pa.smem, "rglru bwd")) return rc;
+        a<<<dim3(pl.n_blk, pl.n_seg - 1), LW, pa.smem, st>>>(
+            m[0], m[1], m[2], m[3], m[0], (const C*)lam, (const C*)br, (const C*)bi, nullptr, nullptr, nullptr,
+            nullptr, nullptr, nullptr, seg, seg + n, L, W, pl.n_wblk, (int)B, pa.S, pl.seg_len, 1, pl.n_seg);
+        if (int rc = launched("lrx_rglru_bwd/tma_agg")) return rc;
+    }
+    auto k = bwd_rev_kernel<IO, C, LW, PF>;
+    if (int rc = reserve_smem(k, pl.smem, "rglru bwd")) return rc;
+    k<<<dim3(pl.n_blk, pl.n_seg), LW, pl.smem, st>>>(m[0], m[1], m[2], m[3], (const C*)lam, (const C*)br,
+                                                     (const C*)bi, (const C*)ckpt, (IO*)gu, (IO*)gqr, (IO*)gqi, parts,
+                                                     parts + n, parts + 2 * n, seg, seg + n, L, W, pl.n_wblk, (int)B,
+                                                     pl.S, pl.seg_len, pl.n_seg);
+    return launched("lrx_rglru_bwd/rev");
+}
+
+template <typename IO, typename C, int LW>
+static int rev_pf(const TmaPlan& pl, const TmaPlan& pa, const CUtensorMap* m, const void* lam, const void* br,
+                  const void* bi, const void* ckpt, void* gu, void* gqr, void* gqi, C* parts, C* seg, int64_t B,
+                  int64_t L, int64_t W, cudaStream_t st) {
+    switch (pl.PF) {
+        case 16: if constexpr (MaxPF<IO>::T >= 16) return launch_bwd_rev<IO, C, LW, 16>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st);
+        [[fallthrough]];
+        case 8: return launch_bwd_rev<IO, C, LW, 8>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st);
+        default: return launch_bwd_rev<IO, C, LW, 4>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st);
+    }
+}
+
 template <typename IO, typename C, int LW>
 static int launch_bwd_rc(const CUtensorMap* m, const void* lam, const void* br, const void* bi, const void* ckpt,
                          void* gu, void* gqr, void* gqi, C* parts, int64_t B, int64_t L, int64_t W, int S,
@@ -985,7 +1183,7 @@ template <typename IO, typename C, int LW>
 static int fwd_pf(const TmaPlan& pl, const CUtensorMap* m, const void* lam, const void* br, const void* bi, void* y,
                   void* ckpt, C* seg, int64_t B, int64_t L, int64_t W, cudaStream_t st) {
     switch (pl.PF) {
-        case 16: if constexpr (Tile<IO>::T >= 16) return launch_fwd_tma<IO, C, LW, 16>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
+        case 16: if constexpr (MaxPF<IO>::T >= 16) return launch_fwd_tma<IO, C, LW, 16>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
         [[fallthrough]];
         case 8: return launch_fwd_tma<IO, C, LW, 8>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
         default: return launch_fwd_tma<IO, C, LW, 4>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
@@ -997,7 +1195,7 @@ static int bwd_pf(const TmaPlan& pl, const TmaPlan& pa, const CUtensorMap* m, co
                   const void* bi, void* gu, void* gqr, void* gqi, C* parts, C* seg, int64_t B, int64_t L, int64_t W,
                   cudaStream_t st) {
     switch (pl.PF) {
-        case 16: if constexpr (Tile<IO>::T >= 16) return launch_bwd_tma<IO, C, LW, 16>(pl, pa, m, lam, br, bi, gu, gqr, gqi, parts, seg, B, L, W, st);
+        case 16: if constexpr (MaxPF<IO>::T >= 16) return launch_bwd_tma<IO, C, LW, 16>(pl, pa, m, lam, br, bi, gu, gqr, gqi, parts, seg, B, L, W, st);
         [[fallthrough]];
         case 8: return launch_bwd_tma<IO, C, LW, 8>(pl, pa, m, lam, br, bi, gu, gqr, gqi, parts, seg, B, L, W, st);
         default: return launch_bwd_tma<IO, C, LW, 4>(pl, pa, m, lam, br, bi, gu, gqr, gqi, parts, seg, B, L, W, st);
@@ -1020,7 +1218,7 @@ static int fwd_t(const void* u, const void* qr, const void* qi, const void* lam,
                  void* y, void* ckpt, int64_t B, int64_t L, int64_t W, void* w, size_t wb, cudaStream_t st) {
     const int mode = mode_env();
     TmaPlan pl;
-    if ((mode == 0 || mode == 1) && B * L < (1ll << 31) && tma_plan<IO>(B, L, W, 3, &pl)) {
+    if ((mode == 0 || mode == 1 || mode == 5) && B * L < (1ll << 31) && tma_plan<IO>(B, L, W, 3, &pl)) {
         CUtensorMap m[3];
         const void* src[3] = {u, qr, qi};
         bool ok = true;
@@ -1064,6 +1262,31 @@ static int bwd_t(const void* u, const void* qr, const void* qi, const void* lam,
     const int mode = mode_env();
     const int64_t n = B * W;
     TmaPlan pl, pa;
+    // default: the reverse-reconstruction walk (7 streams + 1/8 of anchors,
+    // gates once per element); needs the forward's checkpoints
+    if (ckpt && (mode == 0 || mode == 5) && B * L < (1ll << 31) && tma_plan<IO>(B, L, W, 4, &pl) &&
+        agg_plan<IO>(pl, B, L, W, &pa)) {
+        CUtensorMap m[4];
+        const void* src[4] = {u, qr, qi, gy};
+        bool ok = true;
+        for (int i = 0; i < 4; ++i) ok &= tma::encode_2d(&m[i], src[i], sizeof(IO), B * L, W, pl.PF, pl.LW);
+        if (ok) {
+            const int64_t sn = (int64_t)pl.n_seg * B * W;
+            Carver cv(w);
+            C* parts = cv.take<C>((size_t)3 * sn);
+            C* seg = cv.take<C>((size_t)2 * sn);
+            LRX_REQUIRE(w && cv.off <= wb, LRX_ERR_VALUE, "rglru workspace too small");
+            int rc;
+            switch (pl.LW) {
+                case 128: rc = rev_pf<IO, C, 128>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st); break;
+                case 64: rc = rev_pf<IO, C, 64>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st); break;
+                default: rc = rev_pf<IO, C, 32>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st); break;
+            }
+            if (rc) return rc;
+            return colsums<IO, C>(parts, pl.n_seg, B, W, gla, gbr, gbi, st);
+        }
+        LRX_REQUIRE(mode != 5, LRX_ERR_UNSUPPORTED, "rglru: TMA descriptors unavailable");
+    }
     // recompute variant (LRX_RGLRU_MODE=rc): 7 array passes, no y stream.
     // fp32: measured slower on C4 (18.3 vs 16.4 ms: the 2 x gates per element
     // at ~14 warps/SM, limited by the 512 B of staged rows per thread), so the
@@ -1139,7 +1362,8 @@ static size_t bwd_ws_bytes(int64_t B, int64_t L, int64_t W) {
     const size_t lb = ws_lookback<IO, C>(B, L, W) + align_up((size_t)3 * nc * B * W * sizeof(C));
     TmaPlan pl;  // segmented TMA passes: 3 partial + 2 pair rows per segment
     const size_t tm = tma_plan<IO>(B, L, W, 5, &pl) ? 5 * align_up((size_t)pl.n_seg * B * W * sizeof(C)) : 0;
-    return std::max(lb, tm);
+    const size_t tr = tma_plan<IO>(B, L, W, 4, &pl) ? 5 * align_up((size_t)pl.n_seg * B * W * sizeof(C)) : 0;
+    return std::max(lb, std::max(tm, tr));
 }
 
 }  // namespace rglru

@@ -139,6 +139,19 @@ def _device(device=None):
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_SMS = {}
+
+
+def _sm_count(device):
+    """Multiprocessor count of `device` (cached; MIG slices and other parts
+    differ from the B200's 148)."""
+    idx = torch.device(device).index
+    idx = torch.cuda.current_device() if idx is None else idx
+    if idx not in _SMS:
+        _SMS[idx] = torch.cuda.get_device_properties(idx).multi_processor_count
+    return _SMS[idx]
+
+
 def _pair(rng, shape, std, dt):
     g = rng.split(2)
     return np.asarray(g[0].normal(shape) * std, dt), np.asarray(g[1].normal(shape) * std, dt)
@@ -423,7 +436,14 @@ class S4D(LinearRecurrence):
             return False
         B, L, m = shape
         threads = B * m * min(self.d_state, 32)
-        return env == "0" or not (threads < 148 * 32 * 3 // 2 and L >= 8192)
+        if env == "0" or not (threads < _sm_count(self.device) * 32 * 3 // 2 and L >= 8192):
+            return True
+        # the generic path materialises ~6 complex [B, L, m, n] planes (w, its
+        # time-major copy, x, and the backward's cotangents): keep the fused
+        # kernel whenever they would not fit comfortably in free memory
+        plane = B * L * m * self.d_state * torch.tensor([], dtype=self.tcdt).element_size()
+        free, _ = torch.cuda.mem_get_info(self.device)
+        return 6 * plane > free // 2
 
     def _forward(self, u, deltas, keep):
         if self._fused(deltas, u.shape):
@@ -930,8 +950,11 @@ class S6(LinearRecurrence):
         pre = _proj(p1, self.W_delta_proj.T).reshape(B, L, m)
         Bk = _proj(u2, self.W_B).reshape(B, L, n)
         Ck = _proj(u2, self.W_C).reshape(B, L, n)
-        y, ckpt = ops.s6_scan_fwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D)
-        saved = {"u": u, "p1": p1, "pre": pre, "Bk": Bk, "Ck": Ck, "ckpt": ckpt} if keep else {}
+        # inference (no tape, no returned state) skips the checkpoint stores
+        y, ckpt = ops.s6_scan_fwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, ckpt=keep)
+        if not keep:
+            return y, {}, None
+        saved = {"u": u, "p1": p1, "pre": pre, "Bk": Bk, "Ck": Ck, "ckpt": ckpt}
         return y, saved, ckpt[:, -1]
 
     # -- step mode (layers.py:1120-1168) --------------------------------------

@@ -44,14 +44,15 @@ def reduce_rows(part, rows, cols, other=None):
 
 def rglru_scan_fwd(u, qr, qi, lambda_param, b_r, b_i):
     """y = x of the gated recurrence; u/qr/qi [B, L, W] (f32/f64/bf16).
-    Returns (y, ckpt) where ckpt holds the state entering every time chunk."""
+    Returns (y, ckpt): ckpt [n_chunks + 1, B*W] holds the state entering every
+    time chunk and, in its last row, the final state."""
     B, L, W = u.shape
     lib = _lib.lib()
     code = _lib.code_of(u.dtype)
     ck, nc = _lib.i64(), _lib.i64()
     _lib.check(lib.lrx_rglru_chunking(code, L, _lib.ref(ck), _lib.ref(nc)))
     y = torch.empty_like(u)
-    ckpt = torch.empty((nc.value, B * W), dtype=lambda_param.dtype, device=u.device)
+    ckpt = torch.empty((nc.value + 1, B * W), dtype=lambda_param.dtype, device=u.device)
     ws = _lib.workspace(lib.lrx_rglru_workspace_bytes(code, B, L, W), u.device)
     _lib.check(lib.lrx_rglru_fwd(code, _lib.ptr(u), _lib.ptr(qr), _lib.ptr(qi), _lib.ptr(lambda_param),
                                  _lib.ptr(b_r), _lib.ptr(b_i), _lib.ptr(y), _lib.ptr(ckpt), B, L, W, _lib.ptr(ws),
@@ -60,8 +61,9 @@ def rglru_scan_fwd(u, qr, qi, lambda_param, b_r, b_i):
 
 
 def rglru_scan_bwd(u, qr, qi, lambda_param, b_r, b_i, ckpt, gy, y=None):
-    """Pullback of rglru_scan_fwd.  Pass the forward output y (= the state) to
-    let the kernel stream it instead of recomputing from ckpt.  Returns dict
+    """Pullback of rglru_scan_fwd.  The default kernel reconstructs the states
+    from ckpt while it walks backwards; y (the forward output = the state) is
+    used only by the y-streaming variant (LRX_RGLRU_MODE=tma).  Returns dict
     with gu_local (the s*i*g term; the gate-GEMM terms are the caller's), gqr,
     gqi ([B, L, W]) and the batch/time sums gla (sum 8 r gloga), gb_r, gb_i."""
     B, L, W = u.shape

@@ -62,8 +62,11 @@ def test_rglru_c4_full_size(lrx):
     u, qr, qi, gy = (randn((B, L, W), s) for s in (1, 2, 3, 4))
     y, ck = ops.rglru_scan_fwd(u, qr, qi, *p)
     r = ops.rglru_scan_bwd(u, qr, qi, *p, ck, gy, y=y)
-    # oracle: 4 channels, every batch row, the whole sequence
-    cols = torch.tensor([0, 777, 1500, W - 1], device="cuda")
+    # oracle: 5 channels (incl. the most contracting one, where the backward's
+    # state reconstruction expands rounding the most), every batch row, the
+    # whole sequence
+    worst = int(torch.argmin(layer.lambda_param))
+    cols = torch.tensor([0, 777, 1500, W - 1, worst], device="cuda")
     sl = lambda t: t.index_select(2, cols).double().cpu().numpy()  # noqa: E731
     pn = [t.index_select(0, cols).double().cpu().numpy() for t in p]
     ry, rg = port.rglru_scan(sl(u), sl(qr), sl(qi), *pn, sl(gy))
@@ -88,9 +91,10 @@ def test_rglru_c4_full_size(lrx):
 
 
 def test_rglru_c4_bf16_full_size(lrx):
-    """C4 shape with bf16 I/O (the optional dtype): the backward recomputes the
-    states from the forward's fp32 checkpoints (bwd_rc); oracle spot check on
-    4 channels with the bf16-rounded inputs."""
+    """C4 shape with bf16 I/O (the optional dtype): the backward reconstructs
+    the fp32 states anchored on the forward's checkpoints (y is rounded, so it
+    is never read); oracle spot check on 4 channels with the bf16-rounded
+    inputs."""
     from paper_2602_08810_b200 import ops
     B, L, W = 64, 16384, 2560
     layer = lrx.make_layer("rglru", W, dtype="f32", seed=0)

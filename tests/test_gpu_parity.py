@@ -543,7 +543,7 @@ def test_mimo_layer_on_tensor_cores_matches_oracle(lrx, kind):
         assert rel(g.params[k], rg[k]) < TOL["f32"], (k, rel(g.params[k], rg[k]))
 
 
-@pytest.mark.parametrize("mode", ["tma", "stream", "lookback", "rc"])
+@pytest.mark.parametrize("mode", ["tma", "stream", "lookback", "rc", "rev"])
 def test_rglru_kernel_variants_match_oracle(lrx, monkeypatch, mode):
     """Every RG-LRU kernel family (LRX_RGLRU_MODE) gives the oracle's answer."""
     monkeypatch.setenv("LRX_RGLRU_MODE", mode)
@@ -563,10 +563,12 @@ def test_rglru_kernel_variants_match_oracle(lrx, monkeypatch, mode):
 
 @pytest.mark.parametrize("segs", ["1", "2", "5", "64"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_rglru_time_segments_match_oracle(lrx, monkeypatch, segs, dtype):
+@pytest.mark.parametrize("mode", ["tma", "rev"])
+def test_rglru_time_segments_match_oracle(lrx, monkeypatch, segs, dtype, mode):
     """Segmented TMA passes (LRX_RGLRU_SEGS; ragged last segment) give the
-    oracle's answer, and the same bits on a second run."""
-    monkeypatch.setenv("LRX_RGLRU_MODE", "tma")
+    oracle's answer, and the same bits on a second run (y-streaming and
+    reverse-reconstruction backward)."""
+    monkeypatch.setenv("LRX_RGLRU_MODE", mode)
     monkeypatch.setenv("LRX_RGLRU_SEGS", segs)
     m, B, L = 64, 2, 1000 if dtype == "f32" else 517
     layer = lrx.make_layer("rglru", m, dtype=dtype, seed=37)
