@@ -890,3 +890,39 @@ def s6_scan(u, pre, b_delta, a_log, Bk, Ck, D, gy, mode="parallel", workers=1):
                "gCk": np.einsum("blh,lbhn->bln", gy, xt, optimize=True),
                "ga_log": a * np.einsum("blhn,blh->hn", t, delta, optimize=True),
                "gD": np.einsum("blh,blh->h", gy, u, optimize=True), "gb_delta": gpre.sum(axis=(0, 1))}
+
+
+def s6_layer_blocked(params, u, gy, block=128):
+    """The S6 layer's taped forward + analytic backward (layers.py:1020-1027,
+    1051-1118) with the scan part run over blocks of `block` channels: the
+    recurrence is per channel, only gB_k / gC_k (layers.py:1080, 1098) sum
+    over channels, so they are accumulated over the blocks.  Same arithmetic
+    as Layer("s6").forward/backward with a bounded [L, B, block, N] footprint
+    (full-length C3 rows).  Returns (y, grads, gu, {gBk, gCk})."""
+    p = {k: np.asarray(v, np.float64) for k, v in params.items()}
+    u, gy = np.asarray(u, np.float64), np.asarray(gy, np.float64)
+    m = u.shape[-1]
+    p1 = u @ p["W_delta"]
+    pre0 = p1 @ p["W_delta_proj"]  # s6_scan adds b_delta
+    bk, ck = u @ p["W_B"].T, u @ p["W_C"].T
+    y = np.empty_like(u)
+    gu, gpre = np.empty_like(u), np.empty_like(u)
+    gbk, gck = np.zeros_like(bk), np.zeros_like(ck)
+    ga_log, gD, gb = np.empty_like(p["a_log"]), np.empty(m), np.empty(m)
+    for h0 in range(0, m, block):
+        hs = slice(h0, min(m, h0 + block))
+        yb, r = s6_scan(u[..., hs], pre0[..., hs], p["b_delta"][hs], p["a_log"][hs], bk, ck, p["D"][hs],
+                        gy[..., hs], "sequential", 1)
+        y[..., hs], gu[..., hs], gpre[..., hs] = yb, r["gu_local"], r["gpre"]
+        gbk += r["gBk"]
+        gck += r["gCk"]
+        ga_log[hs], gD[hs], gb[hs] = r["ga_log"], r["gD"], r["gb_delta"]
+    gp1 = gpre @ p["W_delta_proj"].T
+    gu = gu + gp1 @ p["W_delta"].T + gbk @ p["W_B"] + gck @ p["W_C"]
+    grads = {"a_log": ga_log,
+             "W_B": np.einsum("bln,blh->nh", gbk, u, optimize=True),
+             "W_C": np.einsum("bln,blh->nh", gck, u, optimize=True),
+             "W_delta": np.einsum("blh,blr->hr", u, gp1, optimize=True),
+             "W_delta_proj": np.einsum("blr,blh->rh", p1, gpre, optimize=True),
+             "b_delta": gb, "D": gD}
+    return y, grads, gu, {"gBk": gbk, "gCk": gck}

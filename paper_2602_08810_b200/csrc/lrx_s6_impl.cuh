@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(Cfg<C, NS>::THREADS) fwd_kernel(
         for (int k = 0; k < kTT; ++k) {
             if (k < nt) {
                 const int64_t t = t0 + k;
-                if (valid && (t % CF::CK) == 0) {
+                if (valid && ckpt != nullptr && (t % CF::CK) == 0) {
                     C* cp = ckpt + (((int64_t)b * (n_ck + 1) + t / CF::CK) * D + d) * N;
 #pragma unroll
                     for (int n = 0; n < NS; ++n)
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(Cfg<C, NS>::THREADS) fwd_kernel(
             }
         }
     }
-    if (valid) {  // final state (prefill / return_state) in the last slot
+    if (valid && ckpt != nullptr) {  // final state (prefill / return_state) in the last slot
         C* cp = ckpt + (((int64_t)b * (n_ck + 1) + n_ck) * D + d) * N;
 #pragma unroll
         for (int n = 0; n < NS; ++n)
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(V2<NST>::FWD_T) fwd_v2_kernel(
             const float delta = __shfl_sync(0xffffffffu, dl_own[k / TPC], gbase | (k % TPC));
             if (k < nt) {
                 const int64_t t = t0 + k;
-                if (valid && (t % G::CK) == 0) {
+                if (valid && ckpt != nullptr && (t % G::CK) == 0) {
                     float* cp = ckpt + (((int64_t)b * (n_ck + 1) + t / G::CK) * D + d) * N + n0;
 #pragma unroll
                     for (int j = 0; j < NPT; ++j)
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(V2<NST>::FWD_T) fwd_v2_kernel(
             }
         }
     }
-    if (valid) {
+    if (valid && ckpt != nullptr) {
         float* cp = ckpt + (((int64_t)b * (n_ck + 1) + n_ck) * D + d) * N + n0;
 #pragma unroll
         for (int j = 0; j < NPT; ++j)

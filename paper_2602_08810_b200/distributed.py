@@ -3,37 +3,37 @@
 One process per GPU (torchrun, NCCL).  Two modes:
 
 * **Batch sharding** (RG-LRU, S6, S5, LRU): lanes are independent, so each rank
-  takes a contiguous batch slice and runs the single-GPU operator — no data-path
+  takes a contiguous batch slice and runs the single-GPU operator -- no data-path
   collective.  Parameter gradients are summed by the caller's usual DP
   all-reduce.  `shard_range` is the split.
 
-* **Sequence parallelism** (S6, config C5: B=1, L=2^20): the time axis is split
-  into G contiguous slices, one per rank.  The recurrence is affine in its
-  carry, so a slice is summarised by (A_r, X_r) with A_r[b,d,n] =
-  exp(a[d,n] * sum_t delta_t) (the product of the slice's abar) and X_r = the
-  slice's final state from a zero start.  Forward: every rank scans from zero,
-  the (A_r, X_r) pairs are all-gathered (2 x B*D*N fp32 per rank, 262 KB for
-  C5), each rank composes its exclusive prefix x_in = sum_k<r (prod A) X_k --
-  the multi-rank analog of the reference's serial chunk stitch
-  (scan.py:184-189, layers.py:167-169) -- and continues its slice from x_in.
-  Backward mirrors it right-to-left with the cotangent carry h: the slice maps
-  h_in -> h_out = A_r h_in + H_r, so the H_r are all-gathered and composed
-  from the right.  Rank r's scan is re-run with the true carry (2x MUFU work on
-  the ranks that receive a carry); the fix-up-only variant is next
-  (DESIGN.md §8).
+* **Sequence parallelism** (S6, config C5: B=1, L=2^20; `LongS6`, and the S6
+  layer with `seq_group=`): the time axis is split into G contiguous slices,
+  one per rank.  The recurrence is affine in its carry, so a slice is
+  summarised by (A_r, X_r) with A_r[b,d,n] = exp(a[d,n] * sum_t delta_t) (the
+  product of the slice's abar) and X_r = the slice's final state from a zero
+  start.  Forward: the (A_r, X_r) pairs are all-gathered (2 x B*D*N fp32 per
+  rank, 262 KB for C5), each rank composes its exclusive prefix
+  x_in = sum_k<r (prod A) X_k -- the multi-rank analog of the reference's serial
+  chunk stitch (scan.py:184-189, layers.py:167-169) -- and scans its slice from
+  x_in.  Backward mirrors it right-to-left with the cotangent carry h (the slice
+  maps h_in -> h_out = A_r h_in + H_r).  The parameter gradients are sums over
+  the whole sequence, so the per-rank partials are reduced inside the backward
+  (`reduce_fixed_order`: all-gather, then summed in rank order -- bitwise
+  reproducible, and equal to `LongS6.simulate`'s order), giving every rank the
+  complete gradients the layer contract returns (autograd.py:222-233).
 
 The carry algebra is in pure functions (`compose_prefix`, `compose_suffix`) so
-it is tested on CPU with gloo, and `SeqParallelS6.simulate` runs the whole
-protocol on one GPU (slices processed in turn) for the parity tests.
+it is tested on CPU with gloo, and `LongS6.simulate` runs the whole protocol on
+one GPU (slices processed in turn) for the parity tests.
 """
 from __future__ import annotations
 
 import torch
 
 from . import ops
-from .numerics import softplus
 
-__all__ = ["shard_range", "compose_prefix", "compose_suffix", "SeqParallelS6", "LongS6"]
+__all__ = ["shard_range", "compose_prefix", "compose_suffix", "reduce_fixed_order", "LongS6"]
 
 
 def shard_range(n: int, world: int, rank: int):
@@ -65,13 +65,6 @@ def compose_suffix(A, H, rank):
     return h
 
 
-def _slice_product(pre, b_delta, a_log):
-    """A_r = exp(a * sum_t softplus(pre_t + b)) for a [B, L, D] slice -> [B, D, N]."""
-    sd = softplus(pre.to(a_log.dtype) + b_delta).sum(dim=1)            # [B, D]
-    return torch.exp(-torch.exp(a_log)[None] * sd[..., None])
-
-
-
 def _all_gather(t, group):
     """[world, *t.shape]: every rank's t.  NCCL gathers device tensors in place
     (all_gather_into_tensor over NVLink); a gloo group (CPU tests, the
@@ -87,78 +80,25 @@ def _all_gather(t, group):
     dist.all_gather_into_tensor(out, t, group=group)
     return out.view(world, *t.shape)
 
-class SeqParallelS6:
-    """Sequence-parallel selective scan over a process group (or simulated).
-
-    `scan_fwd(u, pre, b_delta, a_log, Bk, Ck, D, x0=None) -> (y, ckpt)` and
-    `scan_bwd(..., ckpt, gy, h_in=None, want_h_out=False) -> dict` default to
-    the device operators in ops.py; they are injectable so the exchange
-    protocol can be exercised by CPU tests."""
-
-    def __init__(self, group=None, scan_fwd=None, scan_bwd=None):
-        self.group = group
-        self.scan_fwd = scan_fwd or ops.s6_scan_fwd
-        self.scan_bwd = scan_bwd or ops.s6_scan_bwd
-
-    # -- collective helpers -------------------------------------------------
-    def _gather(self, t):
-        return _all_gather(t, self.group)
-
-    # -- forward / backward on this rank's slice ----------------------------
-    def forward(self, u, pre, b_delta, a_log, Bk, Ck, Dskip):
-        import torch.distributed as dist
-        rank = dist.get_rank(self.group)
-        y, ckpt = self.scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip)
-        A = _slice_product(pre, b_delta, a_log)
-        AX = self._gather(torch.stack((A, ckpt[:, -1])))                   # [G, 2, B, D, N]
-        x_in = compose_prefix(AX[:, 0], AX[:, 1], rank)
-        if rank > 0:
-            y, ckpt = self.scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=x_in.contiguous())
-        return y, {"ckpt": ckpt, "A": AX[:, 0]}
-
-    def backward(self, ctx, u, pre, b_delta, a_log, Bk, Ck, Dskip, gy):
-        import torch.distributed as dist
-        rank = dist.get_rank(self.group)
-        world = dist.get_world_size(self.group)
-        r = self.scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ctx["ckpt"], gy, want_h_out=True)
-        H = self._gather(r["h_out"])
-        h_in = compose_suffix(ctx["A"], H, rank)
-        if rank < world - 1:
-            r = self.scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ctx["ckpt"], gy, h_in=h_in.contiguous(),
-                              want_h_out=True)
-        return r  # per-rank parameter-gradient contributions: sum them across ranks
-
-    # -- single-process simulation (tests, one GPU) ---------------------------
-    @staticmethod
-    def simulate(G, u, pre, b_delta, a_log, Bk, Ck, Dskip, gy):
-        """Run the protocol with the sequence split into G slices on one device.
-        Returns (y, grads) assembled over slices, parameter grads summed."""
-        L = u.shape[1]
-        cuts = [shard_range(L, G, r) for r in range(G)]
-        sl = [(lambda t, s=s, e=e: t[:, s:e].contiguous()) for s, e in cuts]
-        loc = [ops.s6_scan_fwd(sl[r](u), sl[r](pre), b_delta, a_log, sl[r](Bk), sl[r](Ck), Dskip) for r in range(G)]
-        A = torch.stack([_slice_product(sl[r](pre), b_delta, a_log) for r in range(G)])
-        X = torch.stack([c[:, -1] for _, c in loc])
-        ys, ckpts = [], []
-        for r in range(G):
-            if r == 0:
-                y, c = loc[0]
-            else:
-                y, c = ops.s6_scan_fwd(sl[r](u), sl[r](pre), b_delta, a_log, sl[r](Bk), sl[r](Ck), Dskip,
-                                       x0=compose_prefix(A, X, r).contiguous())
-            ys.append(y)
-            ckpts.append(c)
-        H = torch.stack([ops.s6_scan_bwd(sl[r](u), sl[r](pre), b_delta, a_log, sl[r](Bk), sl[r](Ck), Dskip, ckpts[r],
-                                         sl[r](gy), want_h_out=True)["h_out"] for r in range(G)])
-        outs = []
-        for r in range(G):
-            h_in = compose_suffix(A, H, r) if r < G - 1 else None
-            outs.append(ops.s6_scan_bwd(sl[r](u), sl[r](pre), b_delta, a_log, sl[r](Bk), sl[r](Ck), Dskip, ckpts[r],
-                                        sl[r](gy), h_in=None if h_in is None else h_in.contiguous()))
-        grads = {k: torch.cat([o[k] for o in outs], dim=1) for k in ("gu_local", "gpre", "gBk", "gCk")}
-        for k in ("ga_log", "gD", "gb_delta"):
-            grads[k] = sum(o[k] for o in outs)
-        return torch.cat(ys, dim=1), grads
+def reduce_fixed_order(tensors, group=None):
+    """Sum each tensor over the ranks of `group`, in rank order (one all-gather
+    of the flattened tensors, then r0 + r1 + ... on every rank): the same bits
+    on every rank and on every run, unlike a reduction whose order depends on
+    the collective's algorithm.  Returns new tensors of the same shapes."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return [t.clone() for t in tensors]
+    dt = tensors[0].dtype
+    flat = torch.cat([t.reshape(-1).to(dt) for t in tensors])
+    parts = _all_gather(flat[None], group)[:, 0]                          # [G, total]
+    tot = parts[0].clone()
+    for r in range(1, parts.shape[0]):
+        tot += parts[r]
+    out, o = [], 0
+    for t in tensors:
+        out.append(tot[o:o + t.numel()].view(t.shape).to(t.dtype))
+        o += t.numel()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -201,9 +141,30 @@ class LongS6:
         """prod abar over a slice = exp(a * sum delta), [B, D, N]."""
         return torch.exp(-torch.exp(a_log)[None] * sd[..., None])
 
+    @staticmethod
+    def _groups(u, N):
+        """d_state 32 / 48 / 64 ...: the protocol runs per 16-state group (the
+        recurrence is diagonal, as ops.s6_scan_*'s grouping)."""
+        return N > 16 and N % 16 == 0 and u.dtype in (torch.float32, torch.bfloat16)
+
     def forward(self, u, pre, b_delta, a_log, Bk, Ck, Dskip):
-        o = self.ops
+        """This rank's slice of the scan: (y, ctx) for backward."""
         rank, world = self._rank_world()
+        N = Bk.shape[-1]
+        if world > 1 and self._groups(u, N):
+            u32, y, ctxs = u.float(), None, []
+            for g in range(N // 16):
+                sl = slice(16 * g, 16 * g + 16)
+                yg, cg = self._forward16(u32, pre, b_delta, a_log[:, sl].contiguous(), Bk[..., sl].contiguous(),
+                                         Ck[..., sl].contiguous(), Dskip if g == 0 else torch.zeros_like(Dskip),
+                                         rank, world)
+                y = yg if y is None else y.add_(yg)
+                ctxs.append(cg)
+            return y.to(u.dtype), {"groups": ctxs}
+        return self._forward16(u, pre, b_delta, a_log, Bk, Ck, Dskip, rank, world)
+
+    def _forward16(self, u, pre, b_delta, a_log, Bk, Ck, Dskip, rank, world):
+        o = self.ops
         if world == 1:
             y, ckpt = o.s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip)
             return y, {"ckpt": ckpt}
@@ -213,15 +174,43 @@ class LongS6:
         y, ckpt = o.s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=x_in, ws=ws, flags=o.S6_REUSE_AGG)
         return y, {"ckpt": ckpt, "A": AX[:, 0]}
 
-    def backward(self, ctx, u, pre, b_delta, a_log, Bk, Ck, Dskip, gy):
-        o = self.ops
+    def backward(self, ctx, u, pre, b_delta, a_log, Bk, Ck, Dskip, gy, reduce=True):
+        """Pullback of this rank's slice: gu_local, gpre, gBk, gCk of the slice and
+        the parameter gradients ga_log, gD, gb_delta -- summed over all ranks in
+        a fixed order when `reduce` (the default; the S6 layer reduces all its
+        parameter gradients in one collective and passes reduce=False)."""
         rank, world = self._rank_world()
+        if "groups" in ctx:
+            u32, gy32, out = u.float(), gy.float(), None
+            for g, cg in enumerate(ctx["groups"]):
+                sl = slice(16 * g, 16 * g + 16)
+                r = self._backward16(cg, u32, pre, b_delta, a_log[:, sl].contiguous(), Bk[..., sl].contiguous(),
+                                     Ck[..., sl].contiguous(), Dskip if g == 0 else torch.zeros_like(Dskip),
+                                     gy32, rank, world)
+                if out is None:
+                    out = {k: (v if k in ("gu_local", "gpre", "gD", "gb_delta") else [v]) for k, v in r.items()}
+                else:  # fixed group order; gD = sum gy u does not depend on the group
+                    for k in ("gu_local", "gpre", "gb_delta"):
+                        out[k].add_(r[k])
+                    for k in ("gBk", "gCk", "ga_log"):
+                        out[k].append(r[k])
+            out["gu_local"] = out["gu_local"].to(u.dtype)
+            for k in ("gBk", "gCk", "ga_log"):
+                out[k] = torch.cat(out[k], dim=-1)
+        else:
+            out = self._backward16(ctx, u, pre, b_delta, a_log, Bk, Ck, Dskip, gy, rank, world)
+        if reduce and world > 1:
+            out["ga_log"], out["gD"], out["gb_delta"] = reduce_fixed_order(
+                [out["ga_log"], out["gD"], out["gb_delta"]], self.group)
+        return out
+
+    def _backward16(self, ctx, u, pre, b_delta, a_log, Bk, Ck, Dskip, gy, rank, world):
+        o = self.ops
         if world == 1:
             return o.s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ctx["ckpt"], gy)
         h_agg, _, ws = o.s6_bwd_carry(gy, pre, b_delta, a_log, Ck)
         H = self._gather(h_agg)
         h_in = compose_suffix(ctx["A"], H, rank).contiguous()
-        # per-rank parameter-gradient contributions: the caller sums them across ranks
         return o.s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ctx["ckpt"], gy, h_in=h_in, ws=ws,
                              flags=o.S6_REUSE_AGG)
 

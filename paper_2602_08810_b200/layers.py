@@ -922,8 +922,19 @@ class S6(LinearRecurrence):
     bf16_ok = True
 
     def __init__(self, d_model, d_state=None, discretization=None, *, asynchronous=False, dtype="f64", rng=None,
-                 seed=0, d_rank=None, device=None):
+                 seed=0, d_rank=None, device=None, seq_group=None):
+        """`seq_group`: a torch.distributed process group (or "world") for
+        sequence parallelism -- every rank passes its contiguous slice
+        [B, L_r, d_model] of the sequence (in rank order) to forward; the state
+        and cotangent carries cross ranks through distributed.LongS6, and
+        layer_backward returns the complete parameter gradients (summed over
+        the ranks in a fixed order) on every rank, the slice's grad u."""
         super().__init__(d_model, 64 if d_state is None else d_state, discretization, asynchronous, dtype, device)
+        self.seq_group = seq_group
+        self._long = None
+        if seq_group is not None:
+            from .distributed import LongS6
+            self._long = LongS6(None if seq_group == "world" else seq_group)
         rng = rng if rng is not None else Rng(seed)
         r_b, r_c, r_dn, r_up, r_dt = rng.split(5)
         m, n, dt = self.d_model, self.d_state, self.rdt
@@ -950,6 +961,11 @@ class S6(LinearRecurrence):
         pre = _proj(p1, self.W_delta_proj.T).reshape(B, L, m)
         Bk = _proj(u2, self.W_B).reshape(B, L, n)
         Ck = _proj(u2, self.W_C).reshape(B, L, n)
+        if self._long is not None:  # sequence parallel: this rank's slice
+            y, lctx = self._long.forward(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D)
+            saved = {"u": u, "p1": p1, "pre": pre, "Bk": Bk, "Ck": Ck, "ckpt": None, "lctx": lctx}
+            cks = [c["ckpt"] for c in lctx.get("groups", [lctx])]
+            return y, saved, torch.cat([c[:, -1] for c in cks], dim=-1)
         # inference (no tape, no returned state) skips the checkpoint stores
         y, ckpt = ops.s6_scan_fwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, ckpt=keep)
         if not keep:
@@ -989,7 +1005,11 @@ class S6(LinearRecurrence):
         B, L, m = u.shape
         n = self.d_state
         gy = self._gy(gy, u.shape)
-        r = ops.s6_scan_bwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, ckpt, gy)
+        lctx = s.get("lctx")
+        if lctx is not None:
+            r = self._long.backward(lctx, u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, gy, reduce=False)
+        else:
+            r = ops.s6_scan_bwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, ckpt, gy)
         # projection GEMMs (layers.py:1100-1112), compute precision
         c = self.tdt
         u2 = u.reshape(B * L, m).to(c)
@@ -1002,6 +1022,9 @@ class S6(LinearRecurrence):
         gu = _proj_acc(gu, gCk, self.W_C.T)
         grads = {"a_log": r["ga_log"], "W_B": _wgrad(gBk, u2), "W_C": _wgrad(gCk, u2), "W_delta": _wgrad(u2, gp1),
                  "W_delta_proj": _wgrad(p1.to(c), gpre2), "b_delta": r["gb_delta"], "D": r["gD"]}
+        if lctx is not None:  # every gradient is a sum over the whole sequence: one fixed-order reduction
+            from .distributed import reduce_fixed_order
+            grads = dict(zip(grads, reduce_fixed_order(list(grads.values()), self._long.group)))
         return self._out(grads, gu.reshape(B, L, m).to(self.io_dtype), host)
 
 

@@ -171,25 +171,24 @@ def _s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=None, ws=None, flags=
 
 def s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in=None, want_h_out=False, ws=None, flags=0):
     if isinstance(ckpt, GroupedCkpt):
-        if h_in is not None or want_h_out:
-            raise ValueError("carries across ranks need d_state == 16")
-        B, L, D = u.shape
+        if ws is not None or flags:
+            raise ValueError("reused segment maps (ws / flags) need d_state == 16; LongS6 groups itself")
         u32, gy32 = u.float(), gy.float()
-        out = None
+        out, cat = None, ("gBk", "gCk", "ga_log") + (("h_out",) if want_h_out else ())
         for g, ckg in enumerate(ckpt.parts):
             ag, Bg, Cg, Dg = _group_args(a_log, Bk, Ck, Dskip, g)
-            r = _s6_scan_bwd(u32, pre, b_delta, ag, Bg, Cg, Dg, ckg, gy32)
+            hg = h_in[..., 16 * g:16 * g + 16].contiguous() if h_in is not None else None
+            r = _s6_scan_bwd(u32, pre, b_delta, ag, Bg, Cg, Dg, ckg, gy32, h_in=hg, want_h_out=want_h_out)
             if out is None:
-                out = {"gu_local": r["gu_local"], "gpre": r["gpre"], "gBk": [r["gBk"]], "gCk": [r["gCk"]],
-                       "ga_log": [r["ga_log"]], "gD": r["gD"], "gb_delta": r["gb_delta"]}
-            else:  # fixed group order
+                out = {k: ([v] if k in cat else v) for k, v in r.items()}
+            else:  # fixed group order; the carries split by group (diagonal recurrence)
                 out["gu_local"].add_(r["gu_local"])
                 out["gpre"].add_(r["gpre"])
                 out["gb_delta"].add_(r["gb_delta"])
-                for k in ("gBk", "gCk", "ga_log"):
+                for k in cat:
                     out[k].append(r[k])
         out["gu_local"] = out["gu_local"].to(u.dtype)
-        for k in ("gBk", "gCk", "ga_log"):
+        for k in cat:
             out[k] = torch.cat(out[k], dim=-1)
         return out
     return _s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in, want_h_out, ws, flags)

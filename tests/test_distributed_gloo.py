@@ -12,7 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import port
-from paper_2602_08810_b200.distributed import SeqParallelS6, compose_prefix, compose_suffix, shard_range
+from paper_2602_08810_b200.distributed import compose_prefix, compose_suffix, reduce_fixed_order, shard_range
 
 
 def test_shard_range_partitions():
@@ -66,6 +66,7 @@ def _bwd(u, pre, b_delta, a_log, Bk, Ck, D, ckpt, gy, h_in=None, want_h_out=Fals
     h = torch.zeros_like(ckpt[:, 0]) if h_in is None else h_in.clone()
     gu = torch.zeros_like(u)
     gpre = torch.zeros_like(u)
+    gBk, gCk = torch.zeros_like(Bk), torch.zeros_like(Ck)
     ga = torch.zeros_like(a)
     for t in range(L - 1, -1, -1):
         ab = torch.exp(delta[:, t, :, None] * a)
@@ -75,9 +76,12 @@ def _bwd(u, pre, b_delta, a_log, Bk, Ck, D, ckpt, gy, h_in=None, want_h_out=Fals
         gdelta = (term * a).sum(-1) + s1 * u[:, t]
         gpre[:, t] = torch.sigmoid(pre_b[:, t]) * gdelta
         gu[:, t] = gy[:, t] * D + delta[:, t] * s1
+        gBk[:, t] = (g * (delta[:, t] * u[:, t])[..., None]).sum(1)
+        gCk[:, t] = (gy[:, t, :, None] * ckpt[:, t + 1]).sum(1)
         ga += (term * delta[:, t, :, None]).sum(0)
         h = ab * g
-    out = {"gu_local": gu, "gpre": gpre, "ga_log": a * ga}
+    out = {"gu_local": gu, "gpre": gpre, "gBk": gBk, "gCk": gCk, "ga_log": a * ga,
+           "gD": (gy * u).sum((0, 1)), "gb_delta": gpre.sum((0, 1))}
     if want_h_out:
         out["h_out"] = h
     return out
@@ -111,95 +115,87 @@ class _CpuOps:
         return h, delta.sum(1), None
 
 
-def _problem(L=24, m=3, n=4):
+def _problem(L=24, m=3, n=4, dt=np.float64):
     p = port.init_params("s6", m, n, seed=3)
     rng = port.Rng(7)
     u = rng.normal((1, L, m))
     pre = (u @ p["W_delta"]) @ p["W_delta_proj"]
-    T = lambda x: torch.tensor(np.asarray(x))
+    T = lambda x: torch.tensor(np.asarray(x, dt))  # noqa: E731
     return dict(u=T(u), pre=T(pre), b_delta=T(p["b_delta"]), a_log=T(p["a_log"]), Bk=T(u @ p["W_B"].T),
                 Ck=T(u @ p["W_C"].T), D=T(p["D"]), gy=T(rng.normal((1, L, m)))), p, u, pre
 
 
-def _worker(rank, world, port_no, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        pb, p, u, pre = _problem()
-        s, e = shard_range(pb["u"].shape[1], world, rank)
-        sl = {k: (v[:, s:e].contiguous() if k in ("u", "pre", "Bk", "Ck", "gy") else v) for k, v in pb.items()}
-        sp = SeqParallelS6(scan_fwd=_fwd, scan_bwd=_bwd)
-        args = (sl["u"], sl["pre"], sl["b_delta"], sl["a_log"], sl["Bk"], sl["Ck"], sl["D"])
-        y, ctx = sp.forward(*args)
-        r = sp.backward(ctx, *args, sl["gy"])
-        ga = r["ga_log"].clone()
-        dist.all_reduce(ga)  # parameter grads sum over ranks
-        q.put((rank, y.numpy(), r["gu_local"].numpy(), r["gpre"].numpy(), ga.numpy()))
-    finally:
-        dist.destroy_process_group()
-
-
-def test_sequence_parallel_exchange_gloo():
+def _spawn(target, world, *args):
     with socket.socket() as sck:
         sck.bind(("127.0.0.1", 0))
         port_no = sck.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port_no, q)) for r in range(2)]
+    procs = [ctx.Process(target=target, args=(r, world, port_no, q) + args) for r in range(world)]
     for pr in procs:
         pr.start()
-    res = sorted(q.get(timeout=120) for _ in range(2))
+    res = sorted((q.get(timeout=120) for _ in range(world)), key=lambda r: r[0])
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    pb, p, u, pre = _problem()
-    y_ref, o = port.s6_scan(u, pre, p["b_delta"], p["a_log"], u @ p["W_B"].T, u @ p["W_C"].T, p["D"],
-                            pb["gy"].numpy())
-    y = np.concatenate([r[1] for r in res], axis=1)
-    gu = np.concatenate([r[2] for r in res], axis=1)
-    gpre = np.concatenate([r[3] for r in res], axis=1)
-    assert port.rel_err(y, y_ref) < 1e-12
-    assert port.rel_err(gu, o["gu_local"]) < 1e-12
-    assert port.rel_err(gpre, o["gpre"]) < 1e-12
-    assert port.rel_err(res[0][4], o["ga_log"]) < 1e-12
+    return res
 
 
-def _worker_long(rank, world, port_no, q):
+def _worker_reduce(rank, world, port_no, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = torch.full((2, 3), 0.1 * (rank + 1), dtype=torch.float32)
+        b = torch.arange(4, dtype=torch.float32) * (rank + 1)
+        ra, rb = reduce_fixed_order([a, b])
+        q.put((rank, ra.numpy(), rb.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_reduce_fixed_order_gloo():
+    """Rank-order sum, identical bits on every rank (the S6 sequence-parallel
+    parameter-gradient reduction)."""
+    res = _spawn(_worker_reduce, 3)
+    want_a = (np.float32(0.1) + np.float32(0.2)) + np.float32(0.1 * 3)
+    for _, ra, rb in res:
+        assert ra.shape == (2, 3) and rb.shape == (4,)
+        np.testing.assert_array_equal(ra, np.full((2, 3), np.float32(want_a)))
+        np.testing.assert_array_equal(rb, np.arange(4, dtype=np.float32) * 6)
+    assert all(np.array_equal(res[0][1], r[1]) for r in res)
+
+
+def _worker_long(rank, world, port_no, q, L, n, dt):
     from paper_2602_08810_b200.distributed import LongS6
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        pb, p, u, pre = _problem(L=36)
-        s, e = shard_range(36, world, rank)
+        pb, p, u, pre = _problem(L=L, n=n, dt=dt)
+        s, e = shard_range(L, world, rank)
         sl = {k: (v[:, s:e].contiguous() if k in ("u", "pre", "Bk", "Ck", "gy") else v) for k, v in pb.items()}
         ls = LongS6(impl=_CpuOps)
         args = (sl["u"], sl["pre"], sl["b_delta"], sl["a_log"], sl["Bk"], sl["Ck"], sl["D"])
         y, ctx = ls.forward(*args)
-        r = ls.backward(ctx, *args, sl["gy"])
-        ga = r["ga_log"].clone()
-        dist.all_reduce(ga)
-        q.put((rank, y.numpy(), r["gu_local"].numpy(), r["gpre"].numpy(), ga.numpy()))
+        r = ls.backward(ctx, *args, sl["gy"])  # parameter gradients reduced inside
+        q.put((rank, y.numpy(), {k: v.numpy() for k, v in r.items()}))
     finally:
         dist.destroy_process_group()
 
 
-def test_hierarchical_long_sequence_gloo():
-    with socket.socket() as sck:
-        sck.bind(("127.0.0.1", 0))
-        port_no = sck.getsockname()[1]
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=_worker_long, args=(r, 2, port_no, q)) for r in range(2)]
-    for pr in procs:
-        pr.start()
-    res = sorted(q.get(timeout=120) for _ in range(2))
-    for pr in procs:
-        pr.join(timeout=60)
-        assert pr.exitcode == 0
-    pb, p, u, pre = _problem(L=36)
+@pytest.mark.parametrize("n,dt,tol", [(4, np.float64, 1e-12), (32, np.float32, 2e-5)])
+def test_hierarchical_long_sequence_gloo(n, dt, tol):
+    """LongS6 over 2 gloo ranks (CPU stand-in kernels): slices stitched by the
+    all-gathered carries equal the oracle's single pass; the parameter
+    gradients come back complete (and bitwise equal) on every rank; d_state 32
+    runs the protocol per 16-state group."""
+    L = 36
+    res = _spawn(_worker_long, 2, L, n, dt)
+    pb, p, u, pre = _problem(L=L, n=n)
     y_ref, o = port.s6_scan(u, pre, p["b_delta"], p["a_log"], u @ p["W_B"].T, u @ p["W_C"].T, p["D"],
                             pb["gy"].numpy())
-    assert port.rel_err(np.concatenate([r[1] for r in res], 1), y_ref) < 1e-12
-    assert port.rel_err(np.concatenate([r[2] for r in res], 1), o["gu_local"]) < 1e-12
-    assert port.rel_err(np.concatenate([r[3] for r in res], 1), o["gpre"]) < 1e-12
-    assert port.rel_err(res[0][4], o["ga_log"]) < 1e-12
+    assert port.rel_err(np.concatenate([r[1] for r in res], 1), y_ref) < tol
+    for k in ("gu_local", "gpre", "gBk", "gCk"):
+        assert port.rel_err(np.concatenate([r[2][k] for r in res], 1), o[k]) < tol, k
+    for k in ("ga_log", "gD", "gb_delta"):
+        assert port.rel_err(res[0][2][k], o[k]) < tol, k
+        assert np.array_equal(res[0][2][k], res[1][2][k]), k

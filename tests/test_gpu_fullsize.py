@@ -139,6 +139,20 @@ def test_s6_c3_full_size(lrx, io):
         assert rel(r[k].index_select(2, cols), rg[k]) < tol, k
     for k in ("ga_log", "gD", "gb_delta"):
         assert rel(r[k].index_select(0, cols), rg[k]) < tol, k
+    # the channel sums gB_k / gC_k (layers.py:1080, 1098) of batch row 0 over
+    # all 1536 channels and the whole sequence, oracle in channel blocks
+    gbk, gck = np.zeros((1, L, N)), np.zeros((1, L, N))
+    row = lambda t, hs: t[:1, :, hs].double().cpu().numpy()  # noqa: E731
+    Bk0, Ck0 = Bk[:1].double().cpu().numpy(), Ck[:1].double().cpu().numpy()
+    for h0 in range(0, D, 256):
+        hs = slice(h0, h0 + 256)
+        _, rb = port.s6_scan(row(u, hs), row(pre, hs), layer.b_delta[hs].double().cpu().numpy(),
+                             layer.a_log[hs].double().cpu().numpy(), Bk0, Ck0,
+                             layer.D[hs].double().cpu().numpy(), row(gy, hs), "sequential", 1)
+        gbk += rb["gBk"]
+        gck += rb["gCk"]
+    assert rel(r["gBk"][:1], gbk) < tol
+    assert rel(r["gCk"][:1], gck) < tol
     y_again, _ = ops.s6_scan_fwd(u, pre, *p, Bk, Ck, layer.D)
     assert torch.equal(y, y_again)
     if io == "f32":
@@ -150,10 +164,11 @@ def test_s6_c3_full_size(lrx, io):
 
 
 def test_s5_c2_full_size(lrx):
-    """C2: S5 layer B=32 L=4096 H=256 P=128 ZOH through the drop-in layer API:
-    the LTI layer is linear in u, so forward linearity and the adjoint
-    identity with layer_backward hold at full size; batch rows 0-1 against
-    the oracle's layer restatement."""
+    """C2: S5 layer B=32 L=4096 H=256 P=128 ZOH through the drop-in layer API,
+    against the f64 oracle on the WHOLE batch: y, gu and every parameter
+    gradient (the B*L = 131072-term reductions of layers.py:836-895 run on the
+    split-K tensor-core GEMMs); plus forward linearity and the adjoint
+    identity with layer_backward."""
     B, L, H = 32, 4096, 256
     layer = lrx.make_layer("s5", H, 256, dtype="f32", seed=0)
     u, u2, gy = randn((B, L, H), 21), randn((B, L, H), 22), randn((B, L, H), 23)
@@ -161,10 +176,14 @@ def test_s5_c2_full_size(lrx):
     g = lrx.layer_backward(layer, tape, gy)
     params = {k: v.double().cpu().numpy() for k, v in layer.parameters().items()}
     lay = port.Layer("s5", params, layer.discretization)
-    ry, saved = lay.forward(u[:2].double().cpu().numpy())
-    _, rgu = lay.backward(saved, gy[:2].double().cpu().numpy())
-    assert rel(y[:2], ry) < 1e-4
-    assert rel(g.u[:2], rgu) < 1e-4
+    ry, saved = lay.forward(u.double().cpu().numpy())
+    rg, rgu = lay.backward(saved, gy.double().cpu().numpy())
+    del saved
+    assert rel(y, ry) < 1e-4
+    assert rel(g.u, rgu) < 1e-4
+    assert set(rg) == set(g.params)
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < 1e-4, (k, rel(g.params[k], rg[k]))
     y2 = layer.forward(u2)
     assert adjoint_gap(gy, y2, g.u, u2) < 1e-5
     y12 = layer.forward(u + 2.0 * u2)
@@ -214,3 +233,25 @@ def test_s6_c5_long_full_size(lrx):
         assert rel(r[k].index_select(0, cols), rg[k]) < 1e-2, k
     y_again, _ = ops.s6_scan_fwd(u, pre, *p, Bk, Ck, layer.D)
     assert torch.equal(y, y_again)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_s6_c3_layer_full_row(lrx, dtype):
+    """C3 through the drop-in layer API on one full-length batch row with all
+    1536 channels: y, gu and EVERY parameter gradient (W_B / W_C are the
+    channel-summed gB_k / gC_k contracted with u, layers.py:1068-1118) against
+    the f64 oracle (run in channel blocks)."""
+    L, D, N = 8192, 1536, 16
+    layer = lrx.make_layer("s6", D, N, dtype=dtype, seed=0)
+    u = randn((1, L, D), 51, layer.io_dtype)
+    gy = randn((1, L, D), 52, layer.io_dtype)
+    y, tape = layer.forward(u, tape=True)
+    g = lrx.layer_backward(layer, tape, gy)
+    params = {k: v.double().cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu, _ = port.s6_layer_blocked(params, u.double().cpu().numpy(), gy.double().cpu().numpy(), 256)
+    tol = 1e-2 if dtype == "bf16" else 1e-4
+    assert rel(y, ry) < tol
+    assert rel(g.u, rgu) < tol
+    assert set(rg) == set(g.params)
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < tol, (k, rel(g.params[k], rg[k]))

@@ -318,7 +318,7 @@ def _s6_inputs(lrx, m, n, L, seed=5, dtype="f32"):
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_long_sequence_parallel_matches_single_pass(lrx, dtype):
     from paper_2602_08810_b200 import ops
-    from paper_2602_08810_b200.distributed import LongS6, SeqParallelS6
+    from paper_2602_08810_b200.distributed import LongS6
     layer, args, gy = _s6_inputs(lrx, 64, 16, 4096, dtype=dtype)
     y_ref, ck = ops.s6_scan_fwd(*args)
     r_ref = ops.s6_scan_bwd(*args, ck, gy)
@@ -328,9 +328,34 @@ def test_long_sequence_parallel_matches_single_pass(lrx, dtype):
         assert rel(y, y_ref.float().cpu().numpy()) < tol
         for k in ("gu_local", "gpre", "gBk", "gCk", "ga_log", "gD", "gb_delta"):
             assert rel(r[k], r_ref[k].float().cpu().numpy()) < tol, (G, k)
-    y2, g2 = SeqParallelS6.simulate(3, *args, gy)
-    assert rel(y2, y_ref.float().cpu().numpy()) < tol
-    assert rel(g2["ga_log"], r_ref["ga_log"].cpu().numpy()) < tol
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_grouped_carries_match_single_pass(lrx, dtype):
+    """d_state 64 (the layer default: 16-state groups) with the state carry
+    x0 and the cotangent carry h_in / h_out across a sequence cut: the two
+    halves stitched by their carries equal one pass (the grouped
+    path used to refuse carries)."""
+    from paper_2602_08810_b200 import ops
+    layer, args, gy = _s6_inputs(lrx, 64, 64, 3000, dtype=dtype)
+    u, pre, bd, al, Bk, Ck, D = args
+    y_ref, ck = ops.s6_scan_fwd(*args)
+    r_ref = ops.s6_scan_bwd(*args, ck, gy, want_h_out=True)
+    c = 1234
+    h0 = lambda t: t[:, :c].contiguous()  # noqa: E731
+    h1 = lambda t: t[:, c:].contiguous()  # noqa: E731
+    y0, ck0 = ops.s6_scan_fwd(h0(u), h0(pre), bd, al, h0(Bk), h0(Ck), D)
+    y1, ck1 = ops.s6_scan_fwd(h1(u), h1(pre), bd, al, h1(Bk), h1(Ck), D, x0=ck0[:, -1].contiguous())
+    r1 = ops.s6_scan_bwd(h1(u), h1(pre), bd, al, h1(Bk), h1(Ck), D, ck1, h1(gy), want_h_out=True)
+    r0 = ops.s6_scan_bwd(h0(u), h0(pre), bd, al, h0(Bk), h0(Ck), D, ck0, h0(gy), h_in=r1["h_out"],
+                         want_h_out=True)
+    tol = 1e-5 if dtype == "f32" else 1e-2
+    assert rel(torch.cat((y0, y1), 1), y_ref.float().cpu().numpy()) < tol
+    for k in ("gu_local", "gpre", "gBk", "gCk"):
+        assert rel(torch.cat((r0[k], r1[k]), 1), r_ref[k].float().cpu().numpy()) < tol, k
+    for k in ("ga_log", "gb_delta"):
+        assert rel(r0[k] + r1[k], r_ref[k].cpu().numpy()) < tol, k
+    assert rel(r0["h_out"], r_ref["h_out"].cpu().numpy()) < tol
 
 
 # ---- S6 v3 (TMA tiles, channel pairs, in-kernel time segments) -------------
@@ -711,3 +736,26 @@ def test_scan_step_operator(lrx):  # reference test_scan.py:133-146
         xk, st = lrx.step(st, a_k, b_k)
         x = a_k * x + b_k
         np.testing.assert_allclose(xk.cpu().numpy(), x, rtol=1e-6)
+
+
+@pytest.mark.parametrize("kind,n", STEP_KINDS)
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_step_matches_oracle_loop(lrx, kind, n, dtype):
+    """Step mode pinned directly to the oracle's independent per-step loop
+    (port.naive_forward, the restatement of test_layers.py:21-87) rather than
+    to this package's forward; async steps for the kinds that take them."""
+    m, B, L = 6, 2, 30
+    asyn = kind in ("s4d", "s5")
+    layer = lrx.make_layer(kind, m, n, dtype=dtype, seed=47, asynchronous=asyn,
+                           **({"discretization": "dirac"} if asyn else {}))
+    u = port.Rng(48).normal((B, L, m)).astype(layer.rdt)
+    deltas = port.Rng(49).uniform(0.2, 2.0, L) if asyn else None
+    params = {k: np.asarray(v.cpu().numpy() if isinstance(v, torch.Tensor) else v, np.float64)
+              for k, v in layer.parameters().items()}
+    ref = port.naive_forward(kind, params, u.astype(np.float64), scheme=layer.discretization,
+                             deltas=None if deltas is None else np.broadcast_to(deltas, (B, L)))
+    st = layer.init_state(B)
+    tol = 1e-10 if dtype == "f64" else 1e-4
+    for k in range(L):
+        yk, st = layer.step(st, u[:, k], **({"delta_k": float(deltas[k])} if asyn else {}))
+        assert rel(yk, ref[:, k]) < tol, (k, rel(yk, ref[:, k]))

@@ -117,3 +117,20 @@ def test_kat_length_one_f32():  # test_scan.py:155-160
     out = port.scan_sequential(np.array([0.5], np.float32), np.array([[2.0]], np.float32))
     assert out.dtype == np.float32
     np.testing.assert_array_equal(out, [[2.0]])
+
+
+def test_s6_layer_blocked_equals_layer():
+    """The channel-blocked S6 oracle (used for full-length C3 rows) equals the
+    unblocked layer restatement (layers.py:1051-1118)."""
+    params = port.init_params("s6", 12, 4, dtype="f64", seed=3)
+    u = port.Rng(4).normal((2, 37, 12))
+    gy = port.Rng(5).normal((2, 37, 12))
+    lay = port.Layer("s6", params)
+    ry, saved = lay.forward(u)
+    rg, rgu = lay.backward(saved, gy)
+    y, g, gu, extra = port.s6_layer_blocked(params, u, gy, block=5)
+    assert port.rel_err(y, ry) < 1e-13
+    assert port.rel_err(gu, rgu) < 1e-13
+    assert set(g) == set(rg)
+    for k in rg:
+        assert port.rel_err(g[k], rg[k]) < 1e-12, k
