@@ -73,6 +73,16 @@ __device__ __forceinline__ float rcp(float x) {
     return y;
 }
 
+// Packed fp32 pairs (FFMA2 / FMUL2 on sm_100: one instruction for two lanes,
+// same IEEE rounding as two FFMAs).  The scan's elementwise work is packed
+// over PAIRS OF STATES of one channel, so B_k / C_k / a pair up naturally and
+// only the per-(t, d) scalars (delta, delta*u, gy) are broadcast.
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 ex2x2(float2 v) { return make_float2(ex2(v.x), ex2(v.y)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float hsum(float2 v) { return v.x + v.y; }
+
 // delta = softplus(x) (x > 30 -> x; small e^x through the log1p series so
 // delta keeps its relative precision, numerics.py:86-94) and sigmoid(x).
 __device__ __forceinline__ float softplus_sig(float x, float* sig) {
@@ -301,7 +311,9 @@ __global__ void __launch_bounds__(FG<NPT>::THREADS) fwd_kernel(
     if (tid == 0)
         for (int j = 0; j < NS && j < ntiles; ++j) issue(j);
 
-    float a2[2][NPT], x[2][NPT], Dd[2];
+    constexpr int NP = NPT / 2;  // state pairs per channel
+    float2 a2[2][NP], x[2][NP];
+    float Dd[2];
     bool okc[2];
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
@@ -309,17 +321,22 @@ __global__ void __launch_bounds__(FG<NPT>::THREADS) fwd_kernel(
         okc[c] = dg < D;
         Dd[c] = okc[c] ? Dskip[dg] : 0.f;
 #pragma unroll
-        for (int j = 0; j < NPT; ++j) {
-            a2[c][j] = okc[c] ? -expf(a_log[dg * NST + n0 + j]) * kLog2e : 0.f;
-            x[c][j] = (x0 && okc[c]) ? x0[((int64_t)b * D + dg) * NST + n0 + j] : 0.f;
+        for (int j = 0; j < NP; ++j) {
+            const int n = n0 + 2 * j;
+            a2[c][j] = okc[c] ? make_float2(-expf(a_log[dg * NST + n]) * kLog2e, -expf(a_log[dg * NST + n + 1]) * kLog2e)
+                              : make_float2(0.f, 0.f);
+            x[c][j] = (x0 && okc[c]) ? *reinterpret_cast<const float2*>(x0 + ((int64_t)b * D + dg) * NST + n)
+                                     : make_float2(0.f, 0.f);
         }
         // fold the maps of the segments to the left (fixed order)
         for (int r = 0; r < s; ++r) {
             if (!okc[c]) break;
             const int64_t o = ((int64_t)r * Bn + b) * D + dg;
-            const float sdr = aggSD[o];
+            const float2 sdr = bc2(aggSD[o]);
 #pragma unroll
-            for (int j = 0; j < NPT; ++j) x[c][j] = fmaf(ex2(a2[c][j] * sdr), x[c][j], aggX[o * NST + n0 + j]);
+            for (int j = 0; j < NP; ++j)
+                x[c][j] = fma2(ex2x2(mul2(a2[c][j], sdr)), x[c][j],
+                               *reinterpret_cast<const float2*>(aggX + o * NST + n0 + 2 * j));
         }
     }
     const int pd = tid & (CH - 1), pr = tid / CH;
@@ -363,34 +380,33 @@ __global__ void __launch_bounds__(FG<NPT>::THREADS) fwd_kernel(
                         if (okc[c]) {
                             if constexpr (NPT == 4)
                                 __stcs(reinterpret_cast<float4*>(cp + c * NST),
-                                       make_float4(x[c][0], x[c][1], x[c][2], x[c][3]));
+                                       make_float4(x[c][0].x, x[c][0].y, x[c][1].x, x[c][1].y));
                             else
-                                __stcs(reinterpret_cast<float2*>(cp + c * NST), make_float2(x[c][0], x[c][1]));
+                                __stcs(reinterpret_cast<float2*>(cp + c * NST), x[c][0]);
                         }
                 }
                 const float2 dl = ld_pair(ps + k * CH + 2 * pp), du = ld_pair(dub + k * CH + 2 * pp);
-                float bv[NPT], cv[NPT];
+                float2 bv[NP], cv[NP];
                 if constexpr (NPT == 4) {
                     const float4 bb = *reinterpret_cast<const float4*>(Bs + k * NST + n0);
                     const float4 cc = *reinterpret_cast<const float4*>(Cs + k * NST + n0);
-                    bv[0] = bb.x; bv[1] = bb.y; bv[2] = bb.z; bv[3] = bb.w;
-                    cv[0] = cc.x; cv[1] = cc.y; cv[2] = cc.z; cv[3] = cc.w;
+                    bv[0] = make_float2(bb.x, bb.y); bv[1] = make_float2(bb.z, bb.w);
+                    cv[0] = make_float2(cc.x, cc.y); cv[1] = make_float2(cc.z, cc.w);
                 } else {
-                    const float2 bb = *reinterpret_cast<const float2*>(Bs + k * NST + n0);
-                    const float2 cc = *reinterpret_cast<const float2*>(Cs + k * NST + n0);
-                    bv[0] = bb.x; bv[1] = bb.y;
-                    cv[0] = cc.x; cv[1] = cc.y;
+                    bv[0] = *reinterpret_cast<const float2*>(Bs + k * NST + n0);
+                    cv[0] = *reinterpret_cast<const float2*>(Cs + k * NST + n0);
                 }
                 const float dlc[2] = {dl.x, dl.y}, duc[2] = {du.x, du.y};
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    float acc = 0.f;
+                    const float2 dl2 = bc2(dlc[c]), du2 = bc2(duc[c]);
+                    float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int jj = 0; jj < NPT; ++jj) {
-                        x[c][jj] = fmaf(ex2(dlc[c] * a2[c][jj]), x[c][jj], duc[c] * bv[jj]);
-                        acc = fmaf(x[c][jj], cv[jj], acc);
+                    for (int jj = 0; jj < NP; ++jj) {
+                        x[c][jj] = fma2(ex2x2(mul2(dl2, a2[c][jj])), x[c][jj], mul2(du2, bv[jj]));
+                        acc = fma2(x[c][jj], cv[jj], acc);
                     }
-                    yp[kk * 2 + c] = acc;
+                    yp[kk * 2 + c] = hsum(acc);
                 }
             }
             if constexpr (NPT == 4) {
@@ -428,7 +444,7 @@ __global__ void __launch_bounds__(FG<NPT>::THREADS) fwd_kernel(
         for (int c = 0; c < 2; ++c)
             if (okc[c])
 #pragma unroll
-                for (int jj = 0; jj < NPT; ++jj) cp[c * NST + jj] = x[c][jj];
+                for (int jj = 0; jj < NP; ++jj) *reinterpret_cast<float2*>(cp + c * NST + 2 * jj) = x[c][jj];
     }
     if (tid == 0) tma::bulk_wait<0>();
 }
@@ -564,7 +580,9 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(
     if (tid == 0)
         for (int j = 0; j < NSB && j < sg.ntiles; ++j) issue(j);
 
-    float a2[2][4], h[2][4], gacc[2][4], Dd[2];
+    // per thread: channels 2pp, 2pp+1 x states 4q..4q+3 as 2 packed state pairs
+    float2 a2[2][2], h[2][2], gacc[2][2];
+    float Dd[2];
     bool okc[2];
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
@@ -572,20 +590,22 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(
         okc[c] = dg < D;
         Dd[c] = okc[c] ? Dskip[dg] : 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            a2[c][j] = okc[c] ? -expf(a_log[dg * NST + 4 * q + j]) * kLog2e : 0.f;
-            h[c][j] = (h_in && okc[c]) ? h_in[((int64_t)b * D + dg) * NST + 4 * q + j] : 0.f;
-            gacc[c][j] = 0.f;
+        for (int j = 0; j < 2; ++j) {
+            const int n = 4 * q + 2 * j;
+            a2[c][j] = okc[c] ? make_float2(-expf(a_log[dg * NST + n]) * kLog2e, -expf(a_log[dg * NST + n + 1]) * kLog2e)
+                              : make_float2(0.f, 0.f);
+            h[c][j] = (h_in && okc[c]) ? *reinterpret_cast<const float2*>(h_in + ((int64_t)b * D + dg) * NST + n)
+                                       : make_float2(0.f, 0.f);
+            gacc[c][j] = make_float2(0.f, 0.f);
         }
         // fold the cotangent maps of the segments to the right (fixed order)
         for (int r = S - 1; r > s; --r) {
             if (!okc[c]) break;
             const int64_t o = ((int64_t)r * Bn + b) * D + dg;
-            const float sdr = aggSD[o];
+            const float2 sdr = bc2(aggSD[o]);
             const float4 H = *reinterpret_cast<const float4*>(aggH + o * NST + 4 * q);
-            const float Hv[4] = {H.x, H.y, H.z, H.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) h[c][j] = fmaf(ex2(a2[c][j] * sdr), h[c][j], Hv[j]);
+            h[c][0] = fma2(ex2x2(mul2(a2[c][0], sdr)), h[c][0], make_float2(H.x, H.y));
+            h[c][1] = fma2(ex2x2(mul2(a2[c][1], sdr)), h[c][1], make_float2(H.z, H.w));
         }
     }
     const int pd = tid & (CH - 1), pr = tid >> 6;
@@ -593,14 +613,15 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(
     float gD_acc = 0.f, gb_acc = 0.f;
     const int cq = q & 1;                         // channel of this lane's per-step output
     const float Dq = cq ? Dd[1] : Dd[0];
-    float xn[2][4];                               // checkpoint of the next chunk (prefetched)
+    float2 xn[2][2];                              // checkpoint of the next chunk (prefetched)
     auto load_ck = [&](int64_t t) {
         const int64_t slot = min((int64_t)n_ck, t / CK);
         const float* cp = ckpt + (((int64_t)b * (n_ck + 1) + slot) * D + d0 + 2 * pp) * NST + 4 * q;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const float4 v = okc[c] ? __ldcs(reinterpret_cast<const float4*>(cp + c * NST)) : make_float4(0, 0, 0, 0);
-            xn[c][0] = v.x; xn[c][1] = v.y; xn[c][2] = v.z; xn[c][3] = v.w;
+            xn[c][0] = make_float2(v.x, v.y);
+            xn[c][1] = make_float2(v.z, v.w);
         }
     };
     load_ck((int64_t)(sg.tile0 + sg.ntiles - 1) * T + CK);
@@ -636,11 +657,11 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(
 #pragma unroll 1
         for (int ch = 1; ch >= 0; --ch) {
             // recompute the chunk's states: hist[k] = x_{k-1} for step k of the chunk
-            float hist[CK][2][4], xe[2][4];
+            float2 hist[CK][2][2], xe[2][2];
 #pragma unroll
             for (int c = 0; c < 2; ++c)
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) xe[c][jj] = xn[c][jj];
+                for (int jj = 0; jj < 2; ++jj) xe[c][jj] = xn[c][jj];
             // prefetch the checkpoint of the next chunk to the left
             if (ch == 1) load_ck(t0);
             else if (j + 1 < sg.ntiles) load_ck(t0 - T + CK);
@@ -649,15 +670,17 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(
                 const int k = ch * CK + kk;
                 const float2 dl = ld_pair(ps + k * CH + 2 * pp), du = ld_pair(dub + k * CH + 2 * pp);
                 const float4 bb = *reinterpret_cast<const float4*>(Bs + k * NST + 4 * q);
-                const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
+                const float2 bv[2] = {make_float2(bb.x, bb.y), make_float2(bb.z, bb.w)};
                 const float dlc[2] = {dl.x, dl.y}, duc[2] = {du.x, du.y};
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
+                for (int c = 0; c < 2; ++c) {
+                    const float2 dl2 = bc2(dlc[c]), du2 = bc2(duc[c]);
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
+                    for (int jj = 0; jj < 2; ++jj) {
                         hist[kk][c][jj] = xe[c][jj];
-                        xe[c][jj] = fmaf(ex2(dlc[c] * a2[c][jj]), xe[c][jj], duc[c] * bv[jj]);
+                        xe[c][jj] = fma2(ex2x2(mul2(dl2, a2[c][jj])), xe[c][jj], mul2(du2, bv[jj]));
                     }
+                }
             }
             // reverse recurrence over the chunk
 #pragma unroll
@@ -667,33 +690,36 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(
                 const float2 gy = ld_pair(gs + k * CH + 2 * pp), uu = ld_pair(us + k * CH + 2 * pp);
                 const float4 bb = *reinterpret_cast<const float4*>(Bs + k * NST + 4 * q);
                 const float4 cc = *reinterpret_cast<const float4*>(Cs + k * NST + 4 * q);
-                const float bv[4] = {bb.x, bb.y, bb.z, bb.w}, cv[4] = {cc.x, cc.y, cc.z, cc.w};
+                const float2 bv[2] = {make_float2(bb.x, bb.y), make_float2(bb.z, bb.w)};
+                const float2 cv[2] = {make_float2(cc.x, cc.y), make_float2(cc.z, cc.w)};
                 const float dlc[2] = {dl.x, dl.y}, duc[2] = {du.x, du.y}, gyc[2] = {gy.x, gy.y};
                 const float uc[2] = {uu.x, uu.y};
                 float nv[4];      // r1[c0], r1[c1], r2[c0], r2[c1]
-                float dv[8];      // dB[4q..4q+3], dC[4q..4q+3] summed over the pair
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) dv[jj] = 0.f;
+                float2 dB[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // summed over the pair
+                float2 dC[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    float sa = 0.f, sb = 0.f;
+                    const float2 dl2 = bc2(dlc[c]), du2 = bc2(duc[c]), gy2 = bc2(gyc[c]);
+                    float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        const float ab = ex2(dlc[c] * a2[c][jj]);
-                        const float xp = hist[kk][c][jj];
-                        const float xk = kk == CK - 1 ? xe[c][jj] : hist[kk + 1 < CK ? kk + 1 : 0][c][jj];
-                        const float gg = fmaf(gyc[c], cv[jj], h[c][jj]);
-                        const float tt = ab * (gg * xp);         // abar * g * x_{k-1}
-                        sa = fmaf(tt, a2[c][jj], sa);
-                        gacc[c][jj] = fmaf(tt, dlc[c], gacc[c][jj]);
-                        sb = fmaf(gg, bv[jj], sb);
-                        dv[jj] = fmaf(gg, duc[c], dv[jj]);
-                        dv[4 + jj] = fmaf(gyc[c], xk, dv[4 + jj]);
-                        h[c][jj] = ab * gg;
+                    for (int jj = 0; jj < 2; ++jj) {
+                        const float2 ab = ex2x2(mul2(dl2, a2[c][jj]));
+                        const float2 xp = hist[kk][c][jj];
+                        const float2 xk = kk == CK - 1 ? xe[c][jj] : hist[kk + 1 < CK ? kk + 1 : 0][c][jj];
+                        const float2 gg = fma2(gy2, cv[jj], h[c][jj]);
+                        const float2 tt = mul2(ab, mul2(gg, xp));    // abar * g * x_{k-1}
+                        sa = fma2(tt, a2[c][jj], sa);
+                        gacc[c][jj] = fma2(tt, dl2, gacc[c][jj]);
+                        sb = fma2(gg, bv[jj], sb);
+                        dB[jj] = fma2(gg, du2, dB[jj]);
+                        dC[jj] = fma2(gy2, xk, dC[jj]);
+                        h[c][jj] = mul2(ab, gg);
                     }
-                    nv[c] = fmaf(uc[c], sb, sa * kLn2);   // d delta (a = a2 ln 2)
-                    nv[2 + c] = sb;
+                    const float sbs = hsum(sb);
+                    nv[c] = fmaf(uc[c], sbs, hsum(sa) * kLn2);   // d delta (a = a2 ln 2)
+                    nv[2 + c] = sbs;
                 }
+                float dv[8] = {dB[0].x, dB[0].y, dB[1].x, dB[1].y, dC[0].x, dC[0].y, dC[1].x, dC[1].y};
                 tr_reduce<4, 2, 1>(nv);    // lane q: nv[0] = value q
                 tr_reduce<8, 16, 4>(dv);   // lane g: dv[0] = value g of its q block
                 red[(k * 4 + w) * 32 + q * 8 + g] = dv[0];
@@ -738,11 +764,12 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(
         if (okc[c]) {
             float ga[4];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) ga[jj] = -expf(a_log[dg * NST + 4 * q + jj]) * gacc[c][jj];
+            for (int jj = 0; jj < 4; ++jj)
+                ga[jj] = -expf(a_log[dg * NST + 4 * q + jj]) * (jj & 1 ? gacc[c][jj >> 1].y : gacc[c][jj >> 1].x);
             *reinterpret_cast<float4*>(ga_part + (prow * D + dg) * NST + 4 * q) = make_float4(ga[0], ga[1], ga[2], ga[3]);
             if (h_out && s == 0)
                 *reinterpret_cast<float4*>(h_out + ((int64_t)b * D + dg) * NST + 4 * q) =
-                    make_float4(h[c][0], h[c][1], h[c][2], h[c][3]);
+                    make_float4(h[c][0].x, h[c][0].y, h[c][1].x, h[c][1].y);
         }
     }
     if (q < 2 && okc[cq]) gb_part[prow * D + d0 + 2 * pp + cq] = gb_acc;
