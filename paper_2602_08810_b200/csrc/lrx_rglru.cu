@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "lrx_common.cuh"
 #include "lrx_host.h"
@@ -554,6 +555,352 @@ __global__ void __launch_bounds__(LW, PF == 4 && LW >= 64 ? 1152 / LW : 1) bwd_r
     gla_part[p] = sla.s;
     gbr_part[p] = sbr.s;
     gbi_part[p] = sbi.s;
+}
+
+// ---------------------------------------------------------------- lane pairs
+// fp32 compute with two channels per thread: every elementwise operation of
+// the gates and the pullback runs on packed fp32x2 (FFMA2 / FMUL2 / FADD2, one
+// instruction for both lanes, IEEE rounding per lane) and the per-step
+// overhead (shared loads, global stores, addressing, barrier waits) is paid
+// once per pair.  The scalar walk issued ~130 instructions per element and
+// was issue-bound below the HBM ceiling (ncu, C4 bwd: issue 66%, 5.1 TB/s).
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 ex2_2(float2 x) { return make_float2(Fast<float>::ex2(x.x), Fast<float>::ex2(x.y)); }
+__device__ __forceinline__ float2 rcp2(float2 x) { return make_float2(Fast<float>::rcp(x.x), Fast<float>::rcp(x.y)); }
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float2 ld2(const float* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ float2 ld2(const __nv_bfloat16* p) {
+    const uint32_t v = *reinterpret_cast<const uint32_t*>(p);
+    return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
+}
+__device__ __forceinline__ void st2(float* p, float2 v) { __stcs(reinterpret_cast<float2*>(p), v); }
+__device__ __forceinline__ void st2(__nv_bfloat16* p, float2 v) {
+    *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(v.x, v.y);
+}
+
+struct Coef2 {
+    float2 r, i, a, s, rs, u;  // rs = 1 / s
+};
+// gates() on a lane pair; s and 1/s from one rsqrt of -expm1(2 log a) = 1 - a^2
+__device__ __forceinline__ Coef2 gates2(float2 u, float2 qr, float2 qi, float2 la, float2 br, float2 bi) {
+    constexpr float kL2e = 1.4426950408889634f;
+    Coef2 k;
+    k.u = u;
+    k.r = rcp2(add2(f2(1.f), ex2_2(mul2(add2(qr, br), f2(-kL2e)))));
+    k.i = rcp2(add2(f2(1.f), ex2_2(mul2(add2(qi, bi), f2(-kL2e)))));
+    const float2 loga = mul2(mul2(f2(kGate), k.r), la);
+    k.a = ex2_2(mul2(loga, f2(kL2e)));
+    // expm1(2 loga): degree-6 Taylor at h = loga (half the argument), doubled
+    const float2 h = loga;
+    float2 p = fma2(f2(1.f / 720.f), h, f2(1.f / 120.f));
+    p = fma2(p, h, f2(1.f / 24.f));
+    p = fma2(p, h, f2(1.f / 6.f));
+    p = fma2(p, h, f2(0.5f));
+    p = fma2(p, h, f2(1.f));
+    p = mul2(p, h);
+    const float2 small = mul2(p, add2(p, f2(2.f)));
+    const float2 big = fma2(k.a, k.a, f2(-1.f));
+    const float2 m = make_float2(-(fabsf(2.f * loga.x) < 0.7f ? small.x : big.x),
+                                 -(fabsf(2.f * loga.y) < 0.7f ? small.y : big.y));  // 1 - a^2 > 0
+    k.rs = make_float2(rsqrt_approx(m.x), rsqrt_approx(m.y));
+    k.s = mul2(m, k.rs);
+    return k;
+}
+
+template <typename IO, int LW, int PF>
+__global__ void __launch_bounds__(LW / 2, PF == 4 ? 1152 / LW : 512 / LW) bwd_rev2_kernel(
+    const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mr,
+    const __grid_constant__ CUtensorMap mi, const __grid_constant__ CUtensorMap mg, const float* __restrict__ lam,
+    const float* __restrict__ b_r, const float* __restrict__ b_i, const float* __restrict__ ckpt, IO* __restrict__ gu,
+    IO* __restrict__ gqr, IO* __restrict__ gqi, float* __restrict__ gla_part, float* __restrict__ gbr_part,
+    float* __restrict__ gbi_part, const float* __restrict__ seg_a, const float* __restrict__ seg_h, int64_t L,
+    int64_t W, int n_wblk, int Bn, int S, int seg_len, int n_seg) {
+    constexpr int NT = LW / 2;
+    constexpr int NW = NT / 32;
+    static_assert(NW >= 1, "lane pairs need LW >= 64");
+    constexpr int NA = 4;  // u, qr, qi, gy
+    constexpr int CK = Tile<IO>::T;
+    static_assert(CK % PF == 0 || PF % CK == 0, "tile and checkpoint interval must nest");
+    extern __shared__ __align__(128) unsigned char smem[];
+    auto R = ring<IO>(smem, S);
+    const int tid = threadIdx.x;
+    const int b = blockIdx.x / n_wblk;
+    const int w0 = (blockIdx.x % n_wblk) * LW;
+    const int64_t w = w0 + 2 * tid;  // lanes w, w + 1 (W is even: 16-byte rows)
+    const bool valid = w < W;
+    const int seg = blockIdx.y;
+    const int64_t t_beg = (int64_t)seg * seg_len;
+    const int64_t t_end = min(L, t_beg + seg_len);
+    const int j_beg = (int)(t_beg / PF);
+    const int n_tiles = (int)((t_end + PF - 1) / PF) - j_beg;
+    const int row0 = b * (int)L;
+    constexpr uint32_t kStageBytes = (uint32_t)NA * PF * LW * sizeof(IO);
+    if (tid == 0) {
+        tma::prefetch_map(&mu);
+        tma::prefetch_map(&mr);
+        tma::prefetch_map(&mi);
+        tma::prefetch_map(&mg);
+        for (int s = 0; s < S; ++s) {
+            tma::mbar_init(&R.full[s], 1);
+            tma::mbar_init(&R.empty[s], NW);
+        }
+        tma::fence_barrier_init();
+    }
+    __syncthreads();
+    auto issue = [&](int j, int s) {  // j-th tile in reverse order, into stage s
+        const int tt = j_beg + n_tiles - 1 - j;
+        IO* dst = R.data + (size_t)s * NA * PF * LW;
+        const int r = row0 + tt * PF;
+        tma::mbar_arrive_expect_tx(&R.full[s], kStageBytes);
+        tma::load_2d(dst, &mu, w0, r, &R.full[s]);
+        tma::load_2d(dst + PF * LW, &mr, w0, r, &R.full[s]);
+        tma::load_2d(dst + 2 * PF * LW, &mi, w0, r, &R.full[s]);
+        tma::load_2d(dst + 3 * PF * LW, &mg, w0, r, &R.full[s]);
+    };
+    if (tid == 0)
+        for (int j = 0; j < S && j < n_tiles; ++j) issue(j, j);
+
+    float2 la = f2(0.f), br = f2(0.f), bi = f2(0.f);
+    if (valid) {
+        la = make_float2(-Math<float>::softplus(-lam[w]), -Math<float>::softplus(-lam[w + 1]));
+        br = ld2(b_r + w);
+        bi = ld2(b_i + w);
+    }
+    const float2 la8 = mul2(f2(kGate), la);
+    const int64_t BW = (int64_t)Bn * W;
+    const int64_t lane = (int64_t)b * W + (valid ? w : 0);
+    float2 h = f2(0.f);
+    if (valid)
+        for (int r = n_seg - 1; r > seg; --r)
+            h = fma2(ex2_2(mul2(ld2(seg_a + r * BW + lane), f2(1.4426950408889634f))), h, ld2(seg_h + r * BW + lane));
+    // x = the state after the step being walked; anc = the saved state entering
+    // the next chunk start below it (prefetched one chunk ahead)
+    const float* pck = ckpt + lane;
+    float2 x = valid ? __ldcg(reinterpret_cast<const float2*>(pck + ((t_end + CK - 1) / CK) * BW)) : f2(0.f);
+    int64_t c_next = (t_end - 1) / CK;
+    float2 anc = valid ? __ldcg(reinterpret_cast<const float2*>(pck + c_next * BW)) : f2(0.f);
+    Kahan<float> sla[2], sbr[2], sbi[2];
+    const int64_t tile_stride = (int64_t)PF * W;
+    const int64_t o_last = ((int64_t)row0 + (int64_t)(j_beg + n_tiles - 1) * PF) * W + w;
+    IO *qu = gu + o_last, *qr = gqr + o_last, *qi = gqi + o_last;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int j = 0; j < n_tiles; ++j) {
+        const int tt = j_beg + n_tiles - 1 - j;
+        tma::mbar_wait(&R.full[s], ph);
+        const IO* src = R.data + (size_t)s * NA * PF * LW + 2 * tid;
+        float2 cu[PF], cr[PF], ci[PF], cg[PF];
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            cu[k] = ld2(src + k * LW);
+            cr[k] = ld2(src + (PF + k) * LW);
+            ci[k] = ld2(src + (2 * PF + k) * LW);
+            cg[k] = ld2(src + (3 * PF + k) * LW);
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) tma::mbar_arrive(&R.empty[s]);
+        if (tid == 0 && j + S < n_tiles) {
+            tma::mbar_wait(&R.empty[s], ph);
+            issue(j + S, s);
+        }
+        if (++s == S) {
+            s = 0;
+            ph ^= 1;
+        }
+        const int64_t t0 = (int64_t)tt * PF;
+        const int nk = (int)min((int64_t)PF, t_end - t0);
+        float2 tla = f2(0.f), tbr = f2(0.f), tbi = f2(0.f);
+        auto step = [&](int k) {
+            const Coef2 q = gates2(cu[k], cr[k], ci[k], la, br, bi);
+            const float2 g = add2(cg[k], h);
+            h = mul2(q.a, g);
+            const float2 si = mul2(q.s, q.i);
+            float2 xprev;
+            if (((t0 + k) % CK) == 0) {  // chunk start: the saved state
+                xprev = anc;
+                c_next -= 1;
+                anc = (c_next >= 0 && valid) ? __ldcg(reinterpret_cast<const float2*>(pck + c_next * BW)) : f2(0.f);
+            } else {
+                xprev = mul2(fma2(f2(-1.f), mul2(si, q.u), x), rcp2(q.a));
+            }
+            // pullback (bwd_step): gloga = a g x_{k-1} - (a^2 / s) i u g
+            const float2 gs = mul2(mul2(q.i, q.u), g);
+            const float2 gloga = fma2(mul2(q.a, q.a), mul2(f2(-1.f), mul2(q.rs, gs)), mul2(q.a, mul2(g, xprev)));
+            const float2 gqr_v = mul2(mul2(q.r, sub2(f2(1.f), q.r)), mul2(la8, gloga));
+            const float2 gqi_v = mul2(mul2(q.i, sub2(f2(1.f), q.i)), mul2(mul2(q.s, q.u), g));
+            const float2 gu_v = mul2(si, g);
+            x = xprev;
+            if (valid) {
+                st2(qu + k * W, gu_v);
+                st2(qr + k * W, gqr_v);
+                st2(qi + k * W, gqi_v);
+            }
+            tla = fma2(mul2(f2(kGate), q.r), gloga, tla);
+            tbr = add2(tbr, gqr_v);
+            tbi = add2(tbi, gqi_v);
+        };
+        if (nk == PF) {
+#pragma unroll
+            for (int k = PF - 1; k >= 0; --k) step(k);
+        } else {
+#pragma unroll
+            for (int k = PF - 1; k >= 0; --k)
+                if (k < nk) step(k);
+        }
+        qu -= tile_stride;
+        qr -= tile_stride;
+        qi -= tile_stride;
+        sla[0].add(tla.x);
+        sla[1].add(tla.y);
+        sbr[0].add(tbr.x);
+        sbr[1].add(tbr.y);
+        sbi[0].add(tbi.x);
+        sbi[1].add(tbi.y);
+    }
+    if (!valid) return;
+    const int64_t p = seg * BW + lane;
+    *reinterpret_cast<float2*>(gla_part + p) = make_float2(sla[0].s, sla[1].s);
+    *reinterpret_cast<float2*>(gbr_part + p) = make_float2(sbr[0].s, sbr[1].s);
+    *reinterpret_cast<float2*>(gbi_part + p) = make_float2(sbi[0].s, sbi[1].s);
+}
+
+// Lane-pair forward (fp32 compute, LW >= 64): fwd_tma_kernel on packed fp32x2.
+template <typename IO, int LW, int PF, bool AGG>
+__global__ void __launch_bounds__(LW / 2, PF == 4 ? 1152 / LW : 512 / LW) fwd2_kernel(
+    const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mr,
+    const __grid_constant__ CUtensorMap mi, const float* __restrict__ lam, const float* __restrict__ b_r,
+    const float* __restrict__ b_i, IO* __restrict__ y, float* __restrict__ ckpt, float* __restrict__ seg_a,
+    float* __restrict__ seg_x, int64_t L, int64_t W, int n_wblk, int Bn, int S, int seg_len, int seg0) {
+    constexpr int CK = Tile<IO>::T;
+    constexpr int NT = LW / 2;
+    constexpr int NW = NT / 32;
+    static_assert(NW >= 1, "lane pairs need LW >= 64");
+    static_assert(CK % PF == 0 || PF % CK == 0, "tile and checkpoint interval must nest");
+    extern __shared__ __align__(128) unsigned char smem[];
+    auto R = ring<IO>(smem, S);
+    const int tid = threadIdx.x;
+    const int b = blockIdx.x / n_wblk;
+    const int w0 = (blockIdx.x % n_wblk) * LW;
+    const int64_t w = w0 + 2 * tid;
+    const bool valid = w < W;
+    const int seg = seg0 + blockIdx.y;
+    const int64_t t_beg = (int64_t)seg * seg_len;
+    const int64_t t_end = min(L, t_beg + seg_len);
+    const int j_beg = (int)(t_beg / PF);
+    const int n_tiles = (int)((t_end + PF - 1) / PF) - j_beg;
+    const int row0 = b * (int)L;
+    constexpr uint32_t kStageBytes = 3u * PF * LW * sizeof(IO);
+    if (tid == 0) {
+        tma::prefetch_map(&mu);
+        tma::prefetch_map(&mr);
+        tma::prefetch_map(&mi);
+        for (int s = 0; s < S; ++s) {
+            tma::mbar_init(&R.full[s], 1);
+            tma::mbar_init(&R.empty[s], NW);
+        }
+        tma::fence_barrier_init();
+    }
+    __syncthreads();
+    auto issue = [&](int j, int s) {
+        IO* dst = R.data + (size_t)s * 3 * PF * LW;
+        const int r = row0 + (j_beg + j) * PF;
+        tma::mbar_arrive_expect_tx(&R.full[s], kStageBytes);
+        tma::load_2d(dst, &mu, w0, r, &R.full[s]);
+        tma::load_2d(dst + PF * LW, &mr, w0, r, &R.full[s]);
+        tma::load_2d(dst + 2 * PF * LW, &mi, w0, r, &R.full[s]);
+    };
+    if (tid == 0)
+        for (int j = 0; j < S && j < n_tiles; ++j) issue(j, j);
+
+    float2 la = f2(0.f), br = f2(0.f), bi = f2(0.f);
+    if (valid) {
+        la = make_float2(-Math<float>::softplus(-lam[w]), -Math<float>::softplus(-lam[w + 1]));
+        br = ld2(b_r + w);
+        bi = ld2(b_i + w);
+    }
+    const int64_t BW = (int64_t)Bn * W;
+    const int64_t lane = (int64_t)b * W + (valid ? w : 0);
+    float2 x = f2(0.f), sla = f2(0.f);
+    if (!AGG && valid)
+        for (int r = 0; r < seg; ++r)
+            x = fma2(ex2_2(mul2(ld2(seg_a + r * BW + lane), f2(1.4426950408889634f))), x, ld2(seg_x + r * BW + lane));
+    IO* py = y + ((int64_t)row0 + t_beg) * W + w;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int j = 0; j < n_tiles; ++j) {
+        tma::mbar_wait(&R.full[s], ph);
+        const IO* src = R.data + (size_t)s * 3 * PF * LW + 2 * tid;
+        float2 cu[PF], cr[PF], ci[PF];
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            cu[k] = ld2(src + k * LW);
+            cr[k] = ld2(src + (PF + k) * LW);
+            ci[k] = ld2(src + (2 * PF + k) * LW);
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) tma::mbar_arrive(&R.empty[s]);
+        if (tid == 0 && j + S < n_tiles) {
+            tma::mbar_wait(&R.empty[s], ph);
+            issue(j + S, s);
+        }
+        if (++s == S) {
+            s = 0;
+            ph ^= 1;
+        }
+        const int64_t t0 = (int64_t)(j_beg + j) * PF;
+        const int nk = (int)min((int64_t)PF, t_end - t0);
+        const float2 xin = x;
+        float2 tla = f2(0.f), xs[PF];
+        auto step = [&](int k) {
+            const Coef2 q = gates2(cu[k], cr[k], ci[k], la, br, bi);
+            x = fma2(q.a, x, mul2(mul2(q.s, q.i), q.u));
+            xs[k] = x;
+            if (AGG) tla = fma2(mul2(f2(kGate), q.r), la, tla);
+        };
+        if (nk == PF) {
+#pragma unroll
+            for (int k = 0; k < PF; ++k) step(k);
+        } else {
+#pragma unroll
+            for (int k = 0; k < PF; ++k)
+                if (k < nk) step(k);
+        }
+        if (AGG) {
+            sla = add2(sla, tla);
+        } else {
+            if (ckpt && valid) {  // the state entering each checkpoint chunk of the tile
+#pragma unroll
+                for (int k = 0; k < PF; k += (PF < CK ? PF : CK))
+                    if (k < nk && ((t0 + k) % CK) == 0)
+                        __stcs(reinterpret_cast<float2*>(ckpt + ((t0 + k) / CK) * BW + lane), k ? xs[k - 1] : xin);
+            }
+            if (valid) {
+                if (nk == PF) {
+#pragma unroll
+                    for (int k = 0; k < PF; ++k) st2(py + k * W, xs[k]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < PF; ++k)
+                        if (k < nk) st2(py + k * W, xs[k]);
+                }
+            }
+            py += PF * W;
+        }
+    }
+    if (AGG && valid) {
+        *reinterpret_cast<float2*>(seg_a + seg * BW + lane) = sla;
+        *reinterpret_cast<float2*>(seg_x + seg * BW + lane) = x;
+    }
+    if (!AGG && ckpt && valid && t_end == L)  // final state
+        __stcs(reinterpret_cast<float2*>(ckpt + ((L + CK - 1) / CK) * BW + lane), x);
 }
 
 // Backward without the y stream: time tiles of one checkpoint chunk (RC = 16
@@ -1134,10 +1481,40 @@ static int launch_bwd_rev(const TmaPlan& pl, const TmaPlan& pa, const CUtensorMa
     return launched("lrx_rglru_bwd/rev");
 }
 
+// Lane-pair variant of launch_bwd_rev (fp32 compute, LW >= 64).
+template <typename IO, int LW, int PF>
+static int launch_bwd_rev2(const TmaPlan& pl, const TmaPlan& pa, const CUtensorMap* m, const void* lam,
+                           const void* br, const void* bi, const void* ckpt, void* gu, void* gqr, void* gqi,
+                           float* parts, float* seg, int64_t B, int64_t L, int64_t W, cudaStream_t st) {
+    const int64_t n = (int64_t)pl.n_seg * B * W;
+    if (pl.n_seg > 1) {
+        auto a = bwd_tma_kernel<IO, float, LW, PF, true>;
+        if (int rc = reserve_smem(a, pa.smem, "rglru bwd")) return rc;
+        a<<<dim3(pl.n_blk, pl.n_seg - 1), LW, pa.smem, st>>>(
+            m[0], m[1], m[2], m[3], m[0], (const float*)lam, (const float*)br, (const float*)bi, nullptr, nullptr,
+            nullptr, nullptr, nullptr, nullptr, seg, seg + n, L, W, pl.n_wblk, (int)B, pa.S, pl.seg_len, 1, pl.n_seg);
+        if (int rc = launched("lrx_rglru_bwd/tma_agg")) return rc;
+    }
+    auto k = bwd_rev2_kernel<IO, LW, PF>;
+    if (int rc = reserve_smem(k, pl.smem, "rglru bwd")) return rc;
+    k<<<dim3(pl.n_blk, pl.n_seg), LW / 2, pl.smem, st>>>(m[0], m[1], m[2], m[3], (const float*)lam, (const float*)br,
+                                                         (const float*)bi, (const float*)ckpt, (IO*)gu, (IO*)gqr,
+                                                         (IO*)gqi, parts, parts + n, parts + 2 * n, seg, seg + n, L, W,
+                                                         pl.n_wblk, (int)B, pl.S, pl.seg_len, pl.n_seg);
+    return launched("lrx_rglru_bwd/rev2");
+}
+
 template <typename IO, typename C, int LW>
 static int rev_pf(const TmaPlan& pl, const TmaPlan& pa, const CUtensorMap* m, const void* lam, const void* br,
                   const void* bi, const void* ckpt, void* gu, void* gqr, void* gqi, C* parts, C* seg, int64_t B,
                   int64_t L, int64_t W, cudaStream_t st) {
+    if constexpr (LW >= 64 && std::is_same<C, float>::value) {
+        if (!getenv("LRX_RGLRU_SCALAR")) switch (pl.PF) {
+            case 16: return launch_bwd_rev2<IO, LW, 16>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st);
+            case 8: return launch_bwd_rev2<IO, LW, 8>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st);
+            default: return launch_bwd_rev2<IO, LW, 4>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st);
+        }
+    }
     switch (pl.PF) {
         case 16: if constexpr (MaxPF<IO>::T >= 16) return launch_bwd_rev<IO, C, LW, 16>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st);
         [[fallthrough]];
@@ -1179,9 +1556,37 @@ static bool agg_plan(const TmaPlan& pl, int64_t B, int64_t L, int64_t W, TmaPlan
     return pa->S >= 2;
 }
 
+template <typename IO, int LW, int PF>
+static int launch_fwd2(const TmaPlan& pl, const CUtensorMap* m, const void* lam, const void* br, const void* bi,
+                       void* y, void* ckpt, float* seg, int64_t B, int64_t L, int64_t W, cudaStream_t st) {
+    const int64_t sn = (int64_t)pl.n_seg * B * W;
+    if (pl.n_seg > 1) {
+        auto a = fwd2_kernel<IO, LW, PF, true>;
+        if (int rc = reserve_smem(a, pl.smem, "rglru fwd")) return rc;
+        a<<<dim3(pl.n_blk, pl.n_seg - 1), LW / 2, pl.smem, st>>>(m[0], m[1], m[2], (const float*)lam,
+                                                                  (const float*)br, (const float*)bi, nullptr, nullptr,
+                                                                  seg, seg + sn, L, W, pl.n_wblk, (int)B, pl.S,
+                                                                  pl.seg_len, 0);
+        if (int rc = launched("lrx_rglru_fwd/tma2_agg")) return rc;
+    }
+    auto k = fwd2_kernel<IO, LW, PF, false>;
+    if (int rc = reserve_smem(k, pl.smem, "rglru fwd")) return rc;
+    k<<<dim3(pl.n_blk, pl.n_seg), LW / 2, pl.smem, st>>>(m[0], m[1], m[2], (const float*)lam, (const float*)br,
+                                                         (const float*)bi, (IO*)y, (float*)ckpt, seg, seg + sn, L, W,
+                                                         pl.n_wblk, (int)B, pl.S, pl.seg_len, 0);
+    return launched("lrx_rglru_fwd/tma2");
+}
+
 template <typename IO, typename C, int LW>
 static int fwd_pf(const TmaPlan& pl, const CUtensorMap* m, const void* lam, const void* br, const void* bi, void* y,
                   void* ckpt, C* seg, int64_t B, int64_t L, int64_t W, cudaStream_t st) {
+    if constexpr (LW >= 64 && std::is_same<C, float>::value) {
+        if (!getenv("LRX_RGLRU_SCALAR")) switch (pl.PF) {
+            case 16: return launch_fwd2<IO, LW, 16>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
+            case 8: return launch_fwd2<IO, LW, 8>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
+            default: return launch_fwd2<IO, LW, 4>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
+        }
+    }
     switch (pl.PF) {
         case 16: if constexpr (MaxPF<IO>::T >= 16) return launch_fwd_tma<IO, C, LW, 16>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
         [[fallthrough]];
