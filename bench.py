@@ -59,6 +59,10 @@ WORKLOADS = {
     "s6": dict(kind="s6", B=16, L=8192, H=1536, N=16, dtype="bf16", cfg=2),
     "rglru": dict(kind="rglru", B=64, L=16384, H=2560, N=1, dtype="f32", cfg=3),
     "s6_long": dict(kind="s6", B=1, L=2 ** 20, H=2048, N=16, dtype="bf16", cfg=4, seqpar=True),
+    # drop-in layer level (make_layer forward(tape) + layer_backward): the input
+    # projections on the tcgen05 GEMMs (bf16 kind::f16 / fp32 3xTF32) + the scan
+    "s6_layer": dict(kind="s6", B=16, L=8192, H=1536, N=16, dtype="bf16", cfg=2, layer=True),
+    "rglru_layer": dict(kind="rglru", B=64, L=16384, H=2560, N=1, dtype="f32", cfg=3, layer=True),
 }
 DEFAULT_WORKLOAD = "rglru"
 METRIC = "scan Gelem/s (B·L·H·N) fwd+bwd, HBM GB/s vs peak, at 1/2/4/8 B200"
@@ -173,6 +177,8 @@ def build_problem(w, B, device, L=None, group=None):
     u = torch.randn((B, L, H), generator=g, device=device, dtype=torch.float32).to(io)
     gy = torch.randn((B, L, H), generator=g, device=device, dtype=torch.float32).to(io)
     prob = {"layer": layer, "u": u, "gy": gy, "B": B}
+    if w.get("layer"):
+        return _layer_problem(w, prob, layer, B, L, device)
     if kind == "rglru":
         with torch.no_grad():
             u2 = u.reshape(B * L, H)
@@ -192,9 +198,9 @@ def build_problem(w, B, device, L=None, group=None):
         prob["bytes"] = {"fwd": 4 * B * L * H * bpe, "bwd": 7 * B * L * H * bpe}
         prob["probe"] = dict(name="lrx_rglru_bwd (+3 column sums)", bound="hbm", amount=prob["bytes"]["bwd"],
                              fn=bwd)
-        if bpe == 4:  # the kernel streams 8 arrays (y too): its measured mix ceiling
-            prob["probe"]["stream"] = dict(dram_bytes=8 * B * L * H * bpe, ceiling_gbs=6124.0,
-                                           source="tools/ubench/streams.cu: 5 reads + 3 writes, float4, "
+        if bpe == 4:  # the kernel streams 7 arrays + the 1/8-size anchor states: its measured mix ceiling
+            prob["probe"]["stream"] = dict(dram_bytes=(7 + 1 / 8) * B * L * H * bpe, ceiling_gbs=6097.0,
+                                           source="tools/ubench/streams.cu: 4 reads + 3 writes (bwd7), float4, "
                                                   "C4-sized arrays, same pool of B200s")
     elif kind == "s6":
         with torch.no_grad():
@@ -280,6 +286,49 @@ def build_problem(w, B, device, L=None, group=None):
         else:
             prob["probe"] = dict(name=f"lrx_{kind}_bwd (projections + scan)", bound="hbm", amount=3 * per,
                                  fn=lambda ctx: bwd(ctx))
+    prob["fwd"], prob["bwd"] = fwd, bwd
+    return prob
+
+
+def _layer_problem(w, prob, layer, B, L, device):
+    """Layer-level step: forward(tape) + layer_backward of the drop-in layer,
+    projections included (layers.py:1020-1118 / 1208-1291).  Roofline probe:
+    the dominant kernel -- the S6 backward scan, or the RG-LRU gate projection
+    GEMM (tcgen05 3xTF32, issued TF32 FLOP)."""
+    import torch
+
+    from paper_2602_08810_b200 import ops
+    kind, H, N = w["kind"], w["H"], w["N"]
+    T_ = B * L
+
+    def fwd():
+        return layer._forward(prob["u"], None, True)
+
+    def bwd(ctx):
+        saved = dict(ctx[1])
+        saved["host"] = False
+        return layer._backward(saved, prob["gy"])
+
+    bpe = prob["u"].element_size()
+    if kind == "rglru":
+        # scan streams + the four gate GEMMs' operand / output passes
+        prob["bytes"] = {"fwd": 4 * T_ * H * bpe + 2 * 2 * T_ * H * 4, "bwd": 7 * T_ * H * bpe + 6 * T_ * H * 4}
+        u2 = prob["u"].reshape(T_, H)
+        wr = layer.W_r.contiguous()
+        wl = ops.tf32_lo(wr)
+        out = torch.empty((T_, H), device=device)
+        prob["probe"] = dict(name="lrx_gemm_f32 (tcgen05 3xTF32 gate projection u W_r^T)", bound="tensor",
+                             amount=3 * 2 * T_ * H * H, fn=lambda ctx: ops.gemm_f32(u2, wr, wl, out=out))
+    else:
+        saved = fwd()[1]
+        pa = (layer.b_delta, layer.a_log)
+        pre, Bk, Ck = saved["pre"], saved["Bk"], saved["Ck"]
+        prob["bytes"] = {"fwd": T_ * H * (2 * bpe + 4) + 2 * T_ * N * 4, "bwd": T_ * H * (3 * bpe + 2 * 4) + 4 * T_ * N * 4}
+        geo = ops.s6_geometry(prob["u"].dtype, B, L, H, N)
+        prob["probe"] = dict(name="lrx_s6_bwd (inside the layer step)", bound="hbm", amount=prob["bytes"]["bwd"],
+                             fn=lambda ctx: ops.s6_scan_bwd(prob["u"], pre, *pa, Bk, Ck, layer.D, ctx[1]["ckpt"],
+                                                            prob["gy"]),
+                             mufu_ops=B * L * H * ((2 * N + 3) + (N + 2) * (geo["n_seg"] - 1) / geo["n_seg"]))
     prob["fwd"], prob["bwd"] = fwd, bwd
     return prob
 
@@ -424,7 +473,8 @@ def run_e2e(args, w, prob, device):
         for n in ("u", "pre", "Bk", "Ck", "gy"):
             prob = dict(prob)
             prob[n] = prob[n][:, :L].contiguous()
-    names = {"rglru": ("u", "qr", "qi", "gy"), "s6": ("u", "pre", "Bk", "Ck", "gy")}.get(kind, ("u", "gy"))
+    names = ({"rglru": ("u", "qr", "qi", "gy"), "s6": ("u", "pre", "Bk", "Ck", "gy")}.get(kind, ("u", "gy"))
+             if not w.get("layer") else ("u", "gy"))
     host = {n: prob[n][:Bs].cpu().pin_memory() for n in names}
     layer = prob["layer"]
     h2d = sum(t.numel() * t.element_size() for t in host.values())
@@ -436,6 +486,10 @@ def run_e2e(args, w, prob, device):
     streams = [torch.cuda.Stream(device) for _ in range(n_sub)]
 
     def compute(d):
+        if w.get("layer"):
+            y, tape = layer.forward(d["u"], tape=True)
+            g = layer_backward(layer, tape, d["gy"])
+            return [y, g.u] + list(g.params.values())
         if kind == "rglru":
             y, ck = ops.rglru_scan_fwd(d["u"], d["qr"], d["qi"], layer.lambda_param, layer.b_r, layer.b_i)
             r = ops.rglru_scan_bwd(d["u"], d["qr"], d["qi"], layer.lambda_param, layer.b_r, layer.b_i, ck, d["gy"],
@@ -488,7 +542,8 @@ def run_e2e(args, w, prob, device):
 # Sample shapes of the CPU arms: identical B / H / N,
 # C1 and C2 at full length, C3 / C4 at L/64, C5 at L/1024 (its L/64 sample
 # alone would take ~30 s per step).  Time scales linearly in L for a scan.
-CPU_TIMED_L = {"lru": 1024, "s5": 4096, "s6": 8192 // 64, "rglru": 16384 // 64, "s6_long": 2 ** 20 // 1024}
+CPU_TIMED_L = {"lru": 1024, "s5": 4096, "s6": 8192 // 64, "rglru": 16384 // 64, "s6_long": 2 ** 20 // 1024,
+               "s6_layer": 8192 // 64, "rglru_layer": 16384 // 64}
 
 
 def cpu_problem(w, workload, cores, seed=0):
@@ -506,7 +561,13 @@ def cpu_problem(w, workload, cores, seed=0):
     rng = port.Rng(seed + 1)
     u = rng.normal((B, L, H)).astype(dt)
     gy = rng.normal((B, L, H)).astype(dt)
-    if kind == "rglru":
+    if w.get("layer"):
+        lay = port.Layer(kind, p)
+
+        def run():
+            y, sv = lay.forward(u, "parallel", cores)
+            lay.backward(sv, gy)
+    elif kind == "rglru":
         qr, qi = u @ p["W_r"].T, u @ p["W_i"].T
 
         def run():
@@ -523,7 +584,8 @@ def cpu_problem(w, workload, cores, seed=0):
         def run():
             y, sv = lay.forward(u, "parallel", cores)
             lay.backward(sv, gy)
-    desc = (f"{kind} B={B} L={L} (of {w['L']}) H={H} N={N} f32, fwd+bwd at the same operator boundary, "
+    where = "the layer boundary (projections included)" if w.get("layer") else "the same operator boundary"
+    desc = (f"{kind} B={B} L={L} (of {w['L']}) H={H} N={N} f32, fwd+bwd at {where}, "
             f"reference algorithm (oracle port), mode='parallel' workers={cores}")
     return run, B * L * H * N, desc
 

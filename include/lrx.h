@@ -271,6 +271,23 @@ int lrx_gemm_f32_tn(const void* A, const void* B, void* part, int64_t M, int64_t
                     void* stream);
 
 /* ------------------------------------------------------------------------ *
+ * bf16 GEMM on the tcgen05 tensor cores (kind::f16, fp32 accumulation) with a
+ * fused epilogue, for the input projections of the bf16-I/O layers (S6
+ * _projections layers.py:1020-1027: B_k, C_k, the low-rank delta input;
+ * RG-LRU _gates layers.py:1212-1218):
+ *   C[M,N] = act(alpha A[M,K] Bt[N,K]^T + bias[n]) + beta Cin[M,N]
+ * A, Bt bf16 row-major K-contiguous; C, Cin fp32 (Cin / bias may be NULL);
+ * act: 0 identity, 1 softplus (numerics.py:36-39), 2 sigmoid (:97-105).
+ * K % 8 == 0, N % 4 == 0, 16-byte aligned rows.  Replaces the numpy matmuls
+ * of those reference lines (cuBLAS in round 1).
+ * ------------------------------------------------------------------------ */
+#define LRX_ACT_NONE 0
+#define LRX_ACT_SOFTPLUS 1
+#define LRX_ACT_SIGMOID 2
+int lrx_gemm_bf16(const void* A, const void* Bt, void* C, const void* Cin, const void* bias, int64_t M, int64_t N,
+                  int64_t K, float alpha, float beta, int act, void* stream);
+
+/* ------------------------------------------------------------------------ *
  * MIMO complex diagonal scan for S5 / LRU (layers.py:616-980): the recurrence
  * between the dense projections bu = B u and y = Re(C x) (cuBLAS GEMMs):
  *   x_k[b,p] = abar[p] x_{k-1} + scale[p] bu_k[b,p]        (lanes b*P + p)

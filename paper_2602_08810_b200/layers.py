@@ -195,10 +195,15 @@ def _wgrad(g2, a2):
 
 
 def _mm(a, b):
-    """Projection GEMM (cuBLAS).  bf16 activations multiply bf16-cast weights
-    with fp32 accumulation AND fp32 output, so the scan sees unrounded
-    projections (layers.py:1020-1027 computes them at full precision)."""
+    """Projection GEMM a @ b.  bf16 activations multiply bf16-cast weights on
+    the tcgen05 tensor cores (ops.gemm_bf16: fp32 accumulation AND fp32
+    output, so the scan sees unrounded projections; layers.py:1020-1027
+    computes them at full precision); shapes the kernel does not take go to
+    the library GEMM."""
     if a.dtype == torch.bfloat16:
+        K, N = b.shape
+        if a.is_cuda and K % 8 == 0 and N % 4 == 0 and K <= 16384:
+            return ops.gemm_bf16(a.contiguous(), b.T.to(torch.bfloat16).contiguous())
         return torch.mm(a, b.to(torch.bfloat16), out_dtype=torch.float32)
     return a @ b
 
@@ -953,14 +958,21 @@ class S6(LinearRecurrence):
         return {"a_log": self.a_log, "W_B": self.W_B, "W_C": self.W_C, "W_delta": self.W_delta,
                 "W_delta_proj": self.W_delta_proj, "b_delta": self.b_delta, "D": self.D}
 
+    def _wcat(self):
+        """[W_delta^T; W_B; W_C] ([r + 2n, m]): the three input projections of
+        layers.py:1020-1027 as ONE GEMM that reads u once."""
+        return torch.cat((self.W_delta.T, self.W_B, self.W_C), 0).contiguous()
+
     def _forward(self, u, deltas, keep):
         B, L, m = u.shape
-        n = self.d_state
+        n, r = self.d_state, self.d_rank
         u2 = u.reshape(B * L, m)
-        p1 = _proj(u2, self.W_delta.T)
+        P = _proj(u2, self._wcat())                                    # [T, r + 2n] fp32
+        # own (aligned) storage for each part: the kernels' TMA maps need 16-byte bases
+        p1 = P[:, :r].clone()
         pre = _proj(p1, self.W_delta_proj.T).reshape(B, L, m)
-        Bk = _proj(u2, self.W_B).reshape(B, L, n)
-        Ck = _proj(u2, self.W_C).reshape(B, L, n)
+        Bk = P[:, r:r + n].clone().reshape(B, L, n)
+        Ck = P[:, r + n:].clone().reshape(B, L, n)
         if self._long is not None:  # sequence parallel: this rank's slice
             y, lctx = self._long.forward(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D)
             saved = {"u": u, "p1": p1, "pre": pre, "Bk": Bk, "Ck": Ck, "ckpt": None, "lctx": lctx}
@@ -1010,18 +1022,20 @@ class S6(LinearRecurrence):
             r = self._long.backward(lctx, u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, gy, reduce=False)
         else:
             r = ops.s6_scan_bwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, ckpt, gy)
-        # projection GEMMs (layers.py:1100-1112), compute precision
+        # projection GEMMs (layers.py:1100-1112), compute precision; the three
+        # input projections share one GEMM each way: G = [gp1 | gB_k | gC_k]
         c = self.tdt
+        rk = self.d_rank
         u2 = u.reshape(B * L, m).to(c)
         gpre2 = r["gpre"].reshape(B * L, m)
-        gBk, gCk = r["gBk"].reshape(B * L, n), r["gCk"].reshape(B * L, n)
         gp1 = _proj(gpre2, self.W_delta_proj)
+        G = torch.cat((gp1, r["gBk"].reshape(B * L, n).to(c), r["gCk"].reshape(B * L, n).to(c)), 1)
         gu = r["gu_local"].reshape(B * L, m).to(c)
-        gu = _proj_acc(gu, gp1, self.W_delta)
-        gu = _proj_acc(gu, gBk, self.W_B.T)
-        gu = _proj_acc(gu, gCk, self.W_C.T)
-        grads = {"a_log": r["ga_log"], "W_B": _wgrad(gBk, u2), "W_C": _wgrad(gCk, u2), "W_delta": _wgrad(u2, gp1),
-                 "W_delta_proj": _wgrad(p1.to(c), gpre2), "b_delta": r["gb_delta"], "D": r["gD"]}
+        gu = _proj_acc(gu, G, self._wcat().T)                          # gu += G [W_delta^T; W_B; W_C]
+        gW = _wgrad(G, u2)                                             # [r + 2n, m]
+        grads = {"a_log": r["ga_log"], "W_B": gW[rk:rk + n].contiguous(), "W_C": gW[rk + n:].contiguous(),
+                 "W_delta": gW[:rk].T.contiguous(), "W_delta_proj": _wgrad(p1.to(c), gpre2),
+                 "b_delta": r["gb_delta"], "D": r["gD"]}
         if lctx is not None:  # every gradient is a sum over the whole sequence: one fixed-order reduction
             from .distributed import reduce_fixed_order
             grads = dict(zip(grads, reduce_fixed_order(list(grads.values()), self._long.group)))

@@ -22,6 +22,7 @@ from . import _lib
 
 __all__ = ["rglru_scan_fwd", "rglru_scan_bwd", "s6_geometry", "s6_scan_fwd", "s6_scan_bwd", "s6_fwd_carry",
            "s6_bwd_carry", "mimo_scan_fwd", "mimo_scan_bwd", "reduce_rows", "gemm_f32", "gemm_f32_tn", "tf32_lo",
+           "gemm_bf16", "ACT_NONE", "ACT_SOFTPLUS", "ACT_SIGMOID",
            "s4d_scan_fwd", "s4d_scan_bwd", "S4D_FUSED_N"]
 
 
@@ -286,6 +287,23 @@ def gemm_f32_tn(A, B, alpha=1.0):
     part = torch.empty((ks.value, M * N), dtype=torch.float32, device=A.device)
     _lib.check(_lib.lib().lrx_gemm_f32_tn(_lib.ptr(A), _lib.ptr(B), _lib.ptr(part), M, N, K, alpha, _lib.stream()))
     return reduce_rows(part, ks.value, M * N).reshape(M, N)
+
+
+# ---------------------------------------------------------------------------
+# bf16 GEMM on tcgen05 (kind::f16, fp32 accumulation) with a fused epilogue
+
+ACT_NONE, ACT_SOFTPLUS, ACT_SIGMOID = 0, 1, 2
+
+
+def gemm_bf16(A, Bt, bias=None, act=ACT_NONE, Cin=None, alpha=1.0, beta=0.0, out=None):
+    """C = act(alpha A Bt^T + bias) + beta Cin, fp32 out, on the tensor cores.
+    A [M, K], Bt [N, K] bf16 contiguous (K % 8 == 0, N % 4 == 0)."""
+    M, K = A.shape
+    N = Bt.shape[0]
+    C = out if out is not None else torch.empty((M, N), dtype=torch.float32, device=A.device)
+    _lib.check(_lib.lib().lrx_gemm_bf16(_lib.ptr(A), _lib.ptr(Bt), _lib.ptr(C), _lib.ptr(Cin), _lib.ptr(bias), M, N,
+                                        K, alpha, beta, act, _lib.stream()))
+    return C
 
 
 # ---------------------------------------------------------------------------

@@ -502,6 +502,31 @@ def test_gemm_f32_tn_tcgen05_matches_f64(lrx, K, M, N):
     assert torch.equal(C, C2)  # deterministic split-K
 
 
+@pytest.mark.parametrize("M,N,K", [(131072, 128, 1536), (4096, 16, 1536), (1000, 96, 72), (300, 256, 64),
+                                   (5, 32, 8), (2049, 300, 264)])
+def test_gemm_bf16_tcgen05_matches_fp64(lrx, M, N, K):
+    """bf16 tcgen05 GEMM (kind::f16, fp32 accumulation) with its fused epilogue
+    (bias + identity / softplus / sigmoid, + beta Cin) against an fp64 GEMM of
+    the same bf16-rounded operands.  The products are exact in fp32, so only
+    the accumulation rounds: bar 1e-5."""
+    from paper_2602_08810_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = (0.5 * torch.randn((M, K), generator=g, device="cuda")).to(torch.bfloat16)
+    Bt = (torch.randn((N, K), generator=g, device="cuda") / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(N, generator=g, device="cuda")
+    Cin = torch.randn((M, N), generator=g, device="cuda")
+    ref = A.double() @ Bt.double().T
+    assert rel(ops.gemm_bf16(A, Bt), ref.cpu().numpy()) < 1e-5
+    pre = 1.5 * ref + bias.double()
+    sp = torch.where(pre > 30, pre, torch.log1p(torch.exp(pre.clamp(max=30))))
+    got = ops.gemm_bf16(A, Bt, bias=bias, act=ops.ACT_SOFTPLUS, alpha=1.5)
+    assert rel(got, sp.cpu().numpy()) < 1e-5
+    got = ops.gemm_bf16(A, Bt, bias=bias, act=ops.ACT_SIGMOID, Cin=Cin, beta=-0.5)
+    want = torch.sigmoid(ref + bias.double()) - 0.5 * Cin.double()
+    assert rel(got, want.cpu().numpy()) < 1e-5
+    assert torch.equal(ops.gemm_bf16(A, Bt), ops.gemm_bf16(A, Bt))
+
+
 @pytest.mark.parametrize("n", [8, 16, 32, 64])
 @pytest.mark.parametrize("scheme", ["zoh", "bilinear", "dirac"])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
