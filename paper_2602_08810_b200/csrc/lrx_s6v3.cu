@@ -221,15 +221,28 @@ __global__ void __launch_bounds__(THREADS) fwd_agg_kernel(
         float* ps = reinterpret_cast<float*>(sp + LY::U);
         const float* Bs = reinterpret_cast<const float*>(sp + LY::U + LY::P);
         tma::mbar_wait(&full[st], (j / NSF) & 1);
+        // prologue in three phases (all loads, then the math, then all stores):
+        // the stores may alias the loads, so an interleaved loop serialises on
+        // shared-memory latency
+        float pv[T / 2], uv[T / 2];
 #pragma unroll
         for (int i = 0; i < T / 2; ++i) {
-            const int r = pr + 2 * i, idx = r * CH + pd;
+            const int idx = (pr + 2 * i) * CH + pd;
+            pv[i] = ps[idx];
+            uv[i] = ld1(us + idx);
+        }
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) {
             float sig;
-            float dl = softplus_sig(ps[idx] + pbd, &sig);
-            dl = r < nt ? dl : 0.f;
-            sd += dl;
-            ps[idx] = dl;
-            dub[idx] = dl * ld1(us + idx);
+            const float dl = softplus_sig(pv[i] + pbd, &sig);
+            pv[i] = pr + 2 * i < nt ? dl : 0.f;
+            sd += pv[i];
+        }
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) {
+            const int idx = (pr + 2 * i) * CH + pd;
+            ps[idx] = pv[i];
+            dub[idx] = pv[i] * uv[i];
         }
         __syncthreads();
 #pragma unroll
@@ -354,14 +367,26 @@ __global__ void __launch_bounds__(FG<NPT>::THREADS) fwd_kernel(
         IO* yo = ybuf + (j & 1) * TF * CH;
         if (tid == 0 && j >= 2) tma::bulk_wait_read<1>();  // the store that used yo is done reading
         tma::mbar_wait(&full[st], (j / NS) & 1);
+        // prologue: all loads, then softplus, then all stores (see fwd_agg_kernel)
+        constexpr int NPR = TF * CH / TH;
+        float pv[NPR], uv[NPR];
 #pragma unroll
-        for (int i = 0; i < TF * CH / TH; ++i) {
-            const int r = pr + (TH / CH) * i, idx = r * CH + pd;
+        for (int i = 0; i < NPR; ++i) {
+            const int idx = (pr + (TH / CH) * i) * CH + pd;
+            pv[i] = ps[idx];
+            uv[i] = ld1(us + idx);
+        }
+#pragma unroll
+        for (int i = 0; i < NPR; ++i) {
             float sig;
-            float dl = softplus_sig(ps[idx] + pbd, &sig);
-            dl = r < nt ? dl : 0.f;  // past L: abar = 1, no input -> the state is carried unchanged
-            ps[idx] = dl;
-            dub[idx] = dl * ld1(us + idx);
+            const float dl = softplus_sig(pv[i] + pbd, &sig);
+            pv[i] = pr + (TH / CH) * i < nt ? dl : 0.f;  // past L: abar = 1, no input -> the state is carried
+        }
+#pragma unroll
+        for (int i = 0; i < NPR; ++i) {
+            const int idx = (pr + (TH / CH) * i) * CH + pd;
+            ps[idx] = pv[i];
+            dub[idx] = pv[i] * uv[i];
         }
         __syncthreads();
         // reduced readouts stay in registers until the tile is done: no shared
@@ -502,15 +527,18 @@ __global__ void __launch_bounds__(THREADS) bwd_agg_kernel(
         float* ps = reinterpret_cast<float*>(sp + LY::U);
         const float* Cs = reinterpret_cast<const float*>(sp + LY::U + LY::P);
         tma::mbar_wait(&full[st], (j / NSF) & 1);
+        float pv[T / 2];
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) pv[i] = ps[(pr + 2 * i) * CH + pd];
 #pragma unroll
         for (int i = 0; i < T / 2; ++i) {
-            const int r = pr + 2 * i, idx = r * CH + pd;
             float sig;
-            float dl = softplus_sig(ps[idx] + pbd, &sig);
-            dl = r < nt ? dl : 0.f;
-            sd += dl;
-            ps[idx] = dl;
+            const float dl = softplus_sig(pv[i] + pbd, &sig);
+            pv[i] = pr + 2 * i < nt ? dl : 0.f;
+            sd += pv[i];
         }
+#pragma unroll
+        for (int i = 0; i < T / 2; ++i) ps[(pr + 2 * i) * CH + pd] = pv[i];
         __syncthreads();
 #pragma unroll
         for (int k = T - 1; k >= 0; --k) {
@@ -542,7 +570,7 @@ __global__ void __launch_bounds__(THREADS) bwd_agg_kernel(
 // ============================================================================
 // Backward main pass.
 template <typename IO>
-__global__ void __launch_bounds__(THREADS) bwd_kernel(
+__global__ void __launch_bounds__(THREADS, 3) bwd_kernel(
     const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mp,
     const __grid_constant__ CUtensorMap mg, const __grid_constant__ CUtensorMap mB,
     const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mgu,
@@ -640,18 +668,30 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(
         float* gp_o = reinterpret_cast<float*>(ob + (j & 1) * (LY::U + LY::P) + LY::U);
         if (tid == 0 && j >= 2) tma::bulk_wait_read<1>();
         tma::mbar_wait(&full[st], (j / NSB) & 1);
+        {  // prologue: all loads, then the math, then all stores (see fwd_agg_kernel)
+            float pv[T / 2], uv[T / 2], sv[T / 2];
 #pragma unroll
-        for (int i = 0; i < T / 2; ++i) {
-            const int r = pr + 2 * i, idx = r * CH + pd;
-            float sig;
-            float dl = softplus_sig(ps[idx] + pbd, &sig);
-            const bool in = r < nt;
-            dl = in ? dl : 0.f;
-            const float uu = ld1(us + idx);
-            gD_acc = fmaf(ld1(gs + idx), uu, gD_acc);  // zero-filled past L
-            ps[idx] = dl;
-            dub[idx] = dl * uu;
-            sgb[idx] = in ? sig : 0.f;
+            for (int i = 0; i < T / 2; ++i) {
+                const int idx = (pr + 2 * i) * CH + pd;
+                pv[i] = ps[idx];
+                uv[i] = ld1(us + idx);
+                gD_acc = fmaf(ld1(gs + idx), uv[i], gD_acc);  // zero-filled past L
+            }
+#pragma unroll
+            for (int i = 0; i < T / 2; ++i) {
+                float sig;
+                const float dl = softplus_sig(pv[i] + pbd, &sig);
+                const bool in = pr + 2 * i < nt;
+                pv[i] = in ? dl : 0.f;
+                sv[i] = in ? sig : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < T / 2; ++i) {
+                const int idx = (pr + 2 * i) * CH + pd;
+                ps[idx] = pv[i];
+                dub[idx] = pv[i] * uv[i];
+                sgb[idx] = sv[i];
+            }
         }
         __syncthreads();
 #pragma unroll 1
