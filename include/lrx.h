@@ -192,20 +192,35 @@ int lrx_s4d_step(int dtype, void* x, const void* abar, const void* w, const void
 int lrx_mimo_step(int dtype, void* x, const void* abar, const void* scale, const void* Bre, const void* Bim,
                   const void* Cre, const void* Cim, const void* D, const void* u, void* y, double out_scale,
                   int64_t B, int64_t P, int64_t H, void* stream);
-/* ---- S4D fused scan (layers.py:352-546), constant step ------------------------
- * u, y, gy, gu [B, L, H] real (F32 / F64); abar, w (= scale b), c [H, N] complex
- * of that precision; d [H].  N in {8, 16, 32, 64} (LRX_ERR_UNSUPPORTED
- * otherwise: the generic operator path).  ckpt [B, n_chunks, H, N] complex =
- * the state entering every chunk (lrx_s4d_chunking); xlast [B, H, N] (or
- * NULL) = the final state.  Backward partials per
- * batch row: gabar_part, gw_part, gc_part [B, H, N] complex (sum g conj(x_prev),
- * sum u g, sum gy conj(x)), gd_part [B, H]; the caller sums over B. */
+/* ---- S4D fused scan (layers.py:352-546) ------------------------------------
+ * u, y, gy, gu [B, L, H] real (F32 / F64); c [H, N] complex of that
+ * precision; d [H].  N in {8, 16, 32, 64} (LRX_ERR_UNSUPPORTED otherwise: the
+ * generic operator path).  Steps:
+ *   constant  (deltas == NULL): abar, w (= scale b) [H, N] complex
+ *             (lam / b / delta unused);
+ *   per step  (asynchronous S4D, layers.py:402-440, discretize.py:59-93):
+ *             deltas [B, L] real, delta [H] = exp(log_delta), lam, b [H, N]
+ *             complex, scheme 0 ZOH / 1 bilinear / 2 dirac -- abar_k, scale_k
+ *             are computed in the kernel (abar / w unused).
+ * ckpt [B, n_chunks, H, N] complex = the state entering every chunk
+ * (lrx_s4d_chunking); xlast [B, H, N] (or NULL) = the final state.  Long
+ * sequences over few lanes run in time segments: workspace lrx_s4d_geometry
+ * geo[1] bytes, partial rows R = geo[0] (segments) x B.
+ * Backward partials [R, H, N] (R x [H] for gd_part), summed by the caller:
+ *   constant: p1 = sum g conj(x_prev) (d abar), p2 = sum u g (d w-path);
+ *   per step: p1 = d lambda, p2 = d b, p3 (real) = sum_k deltas_k d delta_k
+ *             (times delta[h] and summed over n: d log_delta);
+ *   gc_part = sum gy conj(x), gd_part = sum gy u. */
 int lrx_s4d_chunking(int64_t L, int64_t* chunk_len, int64_t* n_chunks);
-int lrx_s4d_fwd(int dtype, const void* u, const void* abar, const void* w, const void* c, const void* d, void* y,
-                void* ckpt, void* xlast, int64_t B, int64_t L, int64_t H, int64_t N, void* stream);
-int lrx_s4d_bwd(int dtype, const void* u, const void* gy, const void* abar, const void* w, const void* c,
-                const void* d, const void* ckpt, void* gu, void* gabar_part, void* gw_part, void* gc_part,
-                void* gd_part, int64_t B, int64_t L, int64_t H, int64_t N, void* stream);
+int lrx_s4d_geometry(int dtype, int64_t B, int64_t L, int64_t H, int64_t N, int64_t* geo);
+int lrx_s4d_fwd(int dtype, const void* u, const void* abar, const void* w, const void* lam, const void* b,
+                const void* delta, const void* deltas, int scheme, const void* c, const void* d, void* y, void* ckpt,
+                void* xlast, int64_t B, int64_t L, int64_t H, int64_t N, void* workspace, size_t workspace_bytes,
+                void* stream);
+int lrx_s4d_bwd(int dtype, const void* u, const void* gy, const void* abar, const void* w, const void* lam,
+                const void* b, const void* delta, const void* deltas, int scheme, const void* c, const void* d,
+                const void* ckpt, void* gu, void* p1_part, void* p2_part, void* p3_part, void* gc_part, void* gd_part,
+                int64_t B, int64_t L, int64_t H, int64_t N, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- MIMO LTI coefficient work (S5 / LRU), one launch each way ------------
  * Replaces the parameter-sized torch glue of S5._abar_scale / LRU._abar_scale

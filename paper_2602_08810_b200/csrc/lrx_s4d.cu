@@ -16,9 +16,29 @@
 // forward writes the entering state of every tile (checkpoints); the backward
 // walks tiles right to left, recomputes the tile's states from its checkpoint
 // into registers and runs the reverse recurrence.  Parameter-gradient sums
-// are per (b, h, n) partials, summed over b by the caller in fixed order.
+// are per (segment, b, h, n) partials, summed by the caller in fixed order.
+//
+// Time segments (gridDim.y): with few lanes (long sequences over few
+// channels) the sequence is cut into S segments of whole tiles.  An aggregate
+// pass reduces each segment to its affine map x_out = A x_in + X (A = the
+// product of its abar, X = the state reached from zero); the main pass folds
+// the maps to its left in a fixed order and walks its segment with the true
+// carry.  The backward does the same with the cotangent map (conj(A), H)
+// from the right.  (layers.py:157-175 / scan.py:184-189, the reference's
+// chunk stitch.)
+//
+// Per-step steps (asynchronous S4D, discretize.py:59-93 with
+// delta_k = deltas[b, k] * exp(log_delta[h])): abar_k and scale_k are
+// computed in the kernel from lambda, b and the step (ZOH with the small-pole
+// branch, bilinear, dirac), and the backward accumulates the coefficient
+// gradients through the scheme's partials (autograd.py:186-211) per lane --
+// no [B, L, H, N] coefficient planes.
 #include "lrx_common.cuh"
 #include "lrx_host.h"
+
+#include <stdlib.h>
+
+#include <algorithm>
 
 namespace lrx {
 namespace s4d {
@@ -69,12 +89,125 @@ template <int G> struct Out {
     __device__ static int step0(int r) { return G == 32 ? r >> 1 : r * PER; }
 };
 
-template <typename T, int G, int NPL>
+
+// ---------------------------------------------------------------- per-step discretisation
+template <typename T> __device__ __forceinline__ T small_pole_eps();
+template <> __device__ __forceinline__ float small_pole_eps<float>() { return 1e-4f; }   // discretize.py:39-42
+template <> __device__ __forceinline__ double small_pole_eps<double>() { return 1e-8; }
+__device__ __forceinline__ void sc_(float x, float* s, float* c) { sincosf(x, s, c); }
+__device__ __forceinline__ void sc_(double x, double* s, double* c) { sincos(x, s, c); }
+__device__ __forceinline__ float ex_(float x) { return expf(x); }
+__device__ __forceinline__ double ex_(double x) { return exp(x); }
+
+template <typename T>
+__device__ __forceinline__ cplx<T> cdiv_(cplx<T> a, cplx<T> b) {
+    const T den = b.re * b.re + b.im * b.im;
+    return {(a.re * b.re + a.im * b.im) / den, (a.im * b.re - a.re * b.im) / den};
+}
+
+enum { ZOH = 0, BILINEAR = 1, DIRAC = 2 };
+
+// (abar, scale) of one step dt for pole lam (discretize.py:59-93)
+template <typename T>
+__device__ __forceinline__ void disc(int scheme, cplx<T> lam, T dt, cplx<T>& ab, cplx<T>& sc) {
+    const cplx<T> z = dt * lam;
+    if (scheme == BILINEAR) {
+        const cplx<T> den = {T(1) - T(0.5) * z.re, -T(0.5) * z.im};
+        ab = cdiv_(cplx<T>{T(1) + T(0.5) * z.re, T(0.5) * z.im}, den);
+        sc = cdiv_(cplx<T>{dt, T(0)}, den);
+        return;
+    }
+    T sn, cs;
+    sc_(z.im, &sn, &cs);
+    const T e = ex_(z.re);
+    ab = {e * cs, e * sn};
+    if (scheme == DIRAC) sc = {T(1), T(0)};
+    else if (sqrt(lam.re * lam.re + lam.im * lam.im) < small_pole_eps<T>()) sc = {dt, T(0)};
+    else sc = cdiv_(ab - cplx<T>{T(1), T(0)}, lam);
+}
+
+// partials d abar / d lam, d abar / d dt, d scale / d lam, d scale / d dt
+// (autograd.py:186-211 scheme_partials)
+template <typename T>
+__device__ __forceinline__ void disc_partials(int scheme, cplx<T> lam, T dt, cplx<T> ab, cplx<T>& dal, cplx<T>& dad,
+                                              cplx<T>& dsl, cplx<T>& dsd) {
+    if (scheme == BILINEAR) {
+        const cplx<T> den = {T(1) - T(0.5) * dt * lam.re, -T(0.5) * dt * lam.im};
+        const cplx<T> inv2 = cdiv_(cplx<T>{T(1), T(0)}, den * den);
+        dal = dt * inv2;
+        dad = lam * inv2;
+        dsl = (T(0.5) * dt * dt) * inv2;
+        dsd = inv2;
+        return;
+    }
+    dal = dt * ab;
+    dad = lam * ab;
+    if (scheme == DIRAC) {
+        dsl = dsd = cplx<T>{T(0), T(0)};
+    } else if (sqrt(lam.re * lam.re + lam.im * lam.im) < small_pole_eps<T>()) {
+        dsl = {T(0.5) * dt * dt, T(0)};
+        dsd = {T(1), T(0)};
+    } else {
+        dsl = cdiv_(dt * (ab * lam) - (ab - cplx<T>{T(1), T(0)}), lam * lam);
+        dsd = ab;
+    }
+}
+
+// Coefficients of the lane's NPL states: constant (abar, w arrays) or per step.
+template <typename T, int NPL, bool PS>
+struct Coefs {
+    cplx<T> ab[NPL], w[NPL];      // constant step: abar, w = scale b
+    cplx<T> lam[NPL], bb[NPL];    // per step: the poles and b
+    T dh;                         // per step: exp(log_delta[h])
+    int scheme;
+    __device__ void load(const cplx<T>* abar, const cplx<T>* wv, const cplx<T>* lamv, const cplx<T>* bv,
+                         const T* delta, int sch, int64_t h, int64_t n0) {
+        scheme = sch;
+#pragma unroll
+        for (int j = 0; j < NPL; ++j) {
+            if constexpr (PS) {
+                lam[j] = lamv[n0 + j];
+                bb[j] = bv[n0 + j];
+            } else {
+                ab[j] = abar[n0 + j];
+                w[j] = wv[n0 + j];
+            }
+        }
+        if constexpr (PS) dh = delta[h];
+    }
+    // abar and w of state j at step multiplier dk (= deltas[b, t]; ignored for constant steps)
+    __device__ __forceinline__ void at(int j, T dk, cplx<T>& a, cplx<T>& wj) const {
+        if constexpr (PS) {
+            cplx<T> sc;
+            disc<T>(scheme, lam[j], dk * dh, a, sc);
+            wj = sc * bb[j];
+        } else {
+            a = ab[j];
+            wj = w[j];
+        }
+    }
+};
+
+struct SegGeo {
+    int64_t seg_len, n_seg;
+};
+__host__ __device__ __forceinline__ int64_t seg_end(int64_t s, int64_t seg_len, int64_t L) {
+    return (s + 1) * seg_len < L ? (s + 1) * seg_len : L;
+}
+
+// ---------------------------------------------------------------- forward
+// AGG: the segment's map (A, X) from a zero state -> aggA / aggX [S, B*H*N];
+// main: fold the maps to the left, walk the segment, checkpoints + y (+ xlast).
+template <typename T, int G, int NPL, bool PS, bool AGG>
 __global__ void __launch_bounds__(128) fwd_kernel(const T* __restrict__ u, const cplx<T>* __restrict__ abar,
-                                                  const cplx<T>* __restrict__ w, const cplx<T>* __restrict__ c,
-                                                  const T* __restrict__ d, T* __restrict__ y,
-                                                  cplx<T>* __restrict__ ckpt, cplx<T>* __restrict__ xlast, int64_t B,
-                                                  int64_t L, int64_t H) {
+                                                  const cplx<T>* __restrict__ w, const cplx<T>* __restrict__ lamv,
+                                                  const cplx<T>* __restrict__ bv, const T* __restrict__ delta,
+                                                  const T* __restrict__ deltas, int scheme,
+                                                  const cplx<T>* __restrict__ c, const T* __restrict__ d,
+                                                  T* __restrict__ y, cplx<T>* __restrict__ ckpt,
+                                                  cplx<T>* __restrict__ xlast, cplx<T>* __restrict__ aggA,
+                                                  cplx<T>* __restrict__ aggX, int64_t B, int64_t L, int64_t H,
+                                                  int64_t seg_len, int S) {
     constexpr int N = G * NPL;
     const int64_t lane_id = (int64_t)blockIdx.x * 128 + threadIdx.x;  // (b, h, r) with r = lane in channel
     const int64_t n_lanes = B * H * G;
@@ -82,60 +215,101 @@ __global__ void __launch_bounds__(128) fwd_kernel(const T* __restrict__ u, const
     const int64_t ch = (live ? lane_id : n_lanes - 1) / G;  // (b, h)
     const int r = (int)(lane_id % G);
     const int64_t b = ch / H, h = ch % H;
-    cplx<T> ab[NPL], ww[NPL], cc[NPL], x[NPL];
+    const int s = blockIdx.y;
+    const int64_t t_beg = s * seg_len, t_end = seg_end(s, seg_len, L);
+    const int64_t n0 = h * N + r * NPL;
+    const int64_t BHN = B * H * N, o0 = (b * H + h) * N + r * NPL;
+    Coefs<T, NPL, PS> cf;
+    cf.load(abar, w, lamv, bv, delta, scheme, h, n0);
+    cplx<T> cc[NPL], x[NPL], A[NPL];
 #pragma unroll
     for (int j = 0; j < NPL; ++j) {
-        const int64_t n = h * N + r * NPL + j;
-        ab[j] = abar[n], ww[j] = w[n], cc[j] = c[n];
+        cc[j] = c[n0 + j];
         x[j] = Traits<cplx<T>>::zero();
+        A[j] = Traits<cplx<T>>::one();
     }
+    if (!AGG && live)  // fold the maps of the segments to the left (fixed order)
+        for (int rr = 0; rr < s; ++rr)
+#pragma unroll
+            for (int j = 0; j < NPL; ++j) x[j] = aggA[rr * BHN + o0 + j] * x[j] + aggX[rr * BHN + o0 + j];
     const T dd = d[h];
     const T* up = u + b * L * H + h;
+    const T* dp = deltas + b * L;
     T* yp = y + b * L * H + h;
     const int64_t n_ck = (L + TT - 1) / TT;
-    for (int64_t t0 = 0; t0 < L; t0 += TT) {
-        if (live) {
+    for (int64_t t0 = t_beg; t0 < t_end; t0 += TT) {
+        if (!AGG && live && ckpt) {
 #pragma unroll
-            for (int j = 0; j < NPL; ++j)
-                ckpt[((b * n_ck + t0 / TT) * H + h) * N + r * NPL + j] = x[j];
+            for (int j = 0; j < NPL; ++j) ckpt[((b * n_ck + t0 / TT) * H + h) * N + r * NPL + j] = x[j];
         }
-        const int nt = (int)min((int64_t)TT, L - t0);
-        T uu[TT], part[TT];
-#pragma unroll
-        for (int k = 0; k < TT; ++k) uu[k] = k < nt ? up[(t0 + k) * H] : T(0);
+        const int nt = (int)min((int64_t)TT, t_end - t0);
+        T uu[TT], dk[TT], part[TT];
 #pragma unroll
         for (int k = 0; k < TT; ++k) {
-            T s = 0;
+            uu[k] = k < nt ? up[(t0 + k) * H] : T(0);
+            dk[k] = PS && k < nt ? dp[t0 + k] : T(0);
+        }
+#pragma unroll
+        for (int k = 0; k < TT; ++k) {
+            T sm = 0;
 #pragma unroll
             for (int j = 0; j < NPL; ++j) {
-                if (k < nt) x[j] = ab[j] * x[j] + uu[k] * ww[j];  // ragged last tile: state stops at L-1
-                s += cc[j].re * x[j].re - cc[j].im * x[j].im;
+                if (k < nt) {  // ragged last tile: the state stops at the segment's end
+                    cplx<T> a, wj;
+                    cf.at(j, dk[k], a, wj);
+                    x[j] = a * x[j] + uu[k] * wj;
+                    if (AGG) A[j] = a * A[j];
+                }
+                sm += cc[j].re * x[j].re - cc[j].im * x[j].im;
             }
-            part[k] = s;
+            part[k] = sm;
         }
-        reduce_tile<T, G>(part);
-        if (live && Out<G>::writer(r)) {
+        if (!AGG) {
+            reduce_tile<T, G>(part);
+            if (live && Out<G>::writer(r)) {
 #pragma unroll
-            for (int i = 0; i < Out<G>::PER; ++i) {
-                const int k = Out<G>::step0(r) + i;
-                if (k < nt) yp[(t0 + k) * H] = part[i] + dd * up[(t0 + k) * H];
+                for (int i = 0; i < Out<G>::PER; ++i) {
+                    const int k = Out<G>::step0(r) + i;
+                    if (k < nt) yp[(t0 + k) * H] = part[i] + dd * up[(t0 + k) * H];
+                }
             }
         }
     }
-    if (xlast && live) {
+    if (!live) return;
+    if (AGG) {
 #pragma unroll
-        for (int j = 0; j < NPL; ++j) xlast[(b * H + h) * N + r * NPL + j] = x[j];
+        for (int j = 0; j < NPL; ++j) {
+            aggA[s * BHN + o0 + j] = A[j];
+            aggX[s * BHN + o0 + j] = x[j];
+        }
+    } else if (xlast && s == S - 1) {
+#pragma unroll
+        for (int j = 0; j < NPL; ++j) xlast[o0 + j] = x[j];
     }
 }
 
-template <typename T, int G, int NPL>
+// ---------------------------------------------------------------- backward
+// AGG (segments 1 .. S-1): the cotangent map h_out = conj(A) h_in + H of the
+// segment from a zero carry.  Main: fold the maps to the right, walk the
+// segment's tiles right to left with the recompute, write gu and the
+// per-(segment, lane) partials:
+//   constant step: p1 = sum g conj(x_prev) (d abar), p2 = sum u g (d w-path)
+//   per step:      p1 = sum conj(dal) ga + conj(dsl) gscale        (d lambda)
+//                  p2 = sum conj(scale) g u                         (d b)
+//                  p3 = sum deltas [Re(conj(dad) ga) + Re(conj(dsd) gscale)]  (d log_delta / delta)
+//   with ga = g conj(x_prev), gscale = conj(b) g u; always gc = sum gy conj(x), gd = sum gy u.
+template <typename T, int G, int NPL, bool PS, bool AGG>
 __global__ void __launch_bounds__(128) bwd_kernel(const T* __restrict__ u, const T* __restrict__ gy,
                                                   const cplx<T>* __restrict__ abar, const cplx<T>* __restrict__ w,
-                                                  const cplx<T>* __restrict__ c, const T* __restrict__ d,
+                                                  const cplx<T>* __restrict__ lamv, const cplx<T>* __restrict__ bv,
+                                                  const T* __restrict__ delta, const T* __restrict__ deltas,
+                                                  int scheme, const cplx<T>* __restrict__ c, const T* __restrict__ d,
                                                   const cplx<T>* __restrict__ ckpt, T* __restrict__ gu,
-                                                  cplx<T>* __restrict__ gab_p, cplx<T>* __restrict__ gw_p,
-                                                  cplx<T>* __restrict__ gc_p, T* __restrict__ gd_p, int64_t B,
-                                                  int64_t L, int64_t H) {
+                                                  cplx<T>* __restrict__ p1, cplx<T>* __restrict__ p2,
+                                                  T* __restrict__ p3, cplx<T>* __restrict__ gc_p,
+                                                  T* __restrict__ gd_p, cplx<T>* __restrict__ aggA,
+                                                  cplx<T>* __restrict__ aggH, int64_t B, int64_t L, int64_t H,
+                                                  int64_t seg_len, int S) {
     constexpr int N = G * NPL;
     const int64_t lane_id = (int64_t)blockIdx.x * 128 + threadIdx.x;
     const int64_t n_lanes = B * H * G;
@@ -143,28 +317,55 @@ __global__ void __launch_bounds__(128) bwd_kernel(const T* __restrict__ u, const
     const int64_t ch = (live ? lane_id : n_lanes - 1) / G;
     const int r = (int)(lane_id % G);
     const int64_t b = ch / H, h = ch % H;
-    cplx<T> ab[NPL], abc[NPL], wc[NPL], ccc[NPL], hc[NPL], sab[NPL], sw[NPL], sc[NPL];
+    const int s = AGG ? blockIdx.y + 1 : blockIdx.y;
+    const int64_t t_beg = s * seg_len, t_end = seg_end(s, seg_len, L);
+    const int64_t n0 = h * N + r * NPL;
+    const int64_t BHN = B * H * N, o0 = (b * H + h) * N + r * NPL;
+    Coefs<T, NPL, PS> cf;
+    cf.load(abar, w, lamv, bv, delta, scheme, h, n0);
+    cplx<T> ccc[NPL], hc[NPL], s1[NPL], s2[NPL], sc[NPL], A[NPL];
+    T s3[NPL];
 #pragma unroll
     for (int j = 0; j < NPL; ++j) {
-        const int64_t n = h * N + r * NPL + j;
-        ab[j] = abar[n], abc[j] = conj(ab[j]), wc[j] = conj(w[n]), ccc[j] = conj(c[n]);
-        hc[j] = sab[j] = sw[j] = sc[j] = Traits<cplx<T>>::zero();
+        ccc[j] = conj(c[n0 + j]);
+        hc[j] = s1[j] = s2[j] = sc[j] = Traits<cplx<T>>::zero();
+        A[j] = Traits<cplx<T>>::one();
+        s3[j] = T(0);
     }
+    if (!AGG && live)  // fold the cotangent maps of the segments to the right (fixed order)
+        for (int rr = S - 1; rr > s; --rr)
+#pragma unroll
+            for (int j = 0; j < NPL; ++j) hc[j] = aggA[rr * BHN + o0 + j] * hc[j] + aggH[rr * BHN + o0 + j];
     const T dd = d[h];
     T sd = 0;
     const T* up = u + b * L * H + h;
     const T* gp = gy + b * L * H + h;
+    const T* dp = deltas + b * L;
     T* gup = gu + b * L * H + h;
     const int64_t n_ck = (L + TT - 1) / TT;
-    for (int64_t t0 = (n_ck - 1) * TT; t0 >= 0; t0 -= TT) {
-        const int nt = (int)min((int64_t)TT, L - t0);
-        T uu[TT], gg[TT], part[TT];
+    const int64_t t_last = t_beg + ((t_end - 1 - t_beg) / TT) * TT;
+    for (int64_t t0 = t_last; t0 >= t_beg; t0 -= TT) {
+        const int nt = (int)min((int64_t)TT, t_end - t0);
+        T uu[TT], gg[TT], dk[TT], part[TT];
 #pragma unroll
         for (int k = 0; k < TT; ++k) {
             uu[k] = k < nt ? up[(t0 + k) * H] : T(0);
             gg[k] = k < nt ? gp[(t0 + k) * H] : T(0);
+            dk[k] = PS && k < nt ? dp[t0 + k] : T(0);
         }
-        // states of the tile: hist[k] = x_{t0+k-1}; xe = x_{t0+nt-1}
+        if constexpr (AGG) {
+#pragma unroll
+            for (int k = TT - 1; k >= 0; --k)
+                if (k < nt)
+#pragma unroll
+                    for (int j = 0; j < NPL; ++j) {
+                        cplx<T> a, wj;
+                        cf.at(j, dk[k], a, wj);
+                        hc[j] = conj(a) * (gg[k] * ccc[j] + hc[j]);
+                        A[j] = conj(a) * A[j];
+                    }
+        } else {
+        // states of the tile: hist[k] = x_{t0+k-1}; xs = x_{t0+nt-1}
         cplx<T> hist[TT][NPL], xs[NPL];
 #pragma unroll
         for (int j = 0; j < NPL; ++j) xs[j] = ckpt[((b * n_ck + t0 / TT) * H + h) * N + r * NPL + j];
@@ -173,27 +374,50 @@ __global__ void __launch_bounds__(128) bwd_kernel(const T* __restrict__ u, const
 #pragma unroll
             for (int j = 0; j < NPL; ++j) {
                 hist[k][j] = xs[j];
-                if (k < nt) xs[j] = ab[j] * xs[j] + uu[k] * conj(wc[j]);
+                if (k < nt) {
+                    cplx<T> a, wj;
+                    cf.at(j, dk[k], a, wj);
+                    xs[j] = a * xs[j] + uu[k] * wj;
+                }
             }
 #pragma unroll
         for (int k = TT - 1; k >= 0; --k) {
-            T s = 0;
+            T sm = 0;
             if (k < nt) {
 #pragma unroll
                 for (int j = 0; j < NPL; ++j) {
                     const cplx<T> xk = k + 1 < TT ? hist[k + 1 < TT ? k + 1 : 0][j] : xs[j];
                     const cplx<T> xcur = (k == nt - 1) ? xs[j] : xk;
+                    cplx<T> a, wj, scl;
+                    if constexpr (PS) {
+                        disc<T>(scheme, cf.lam[j], dk[k] * cf.dh, a, scl);
+                        wj = scl * cf.bb[j];
+                    } else {
+                        a = cf.ab[j];
+                        wj = cf.w[j];
+                    }
                     const cplx<T> g = gg[k] * ccc[j] + hc[j];
-                    hc[j] = abc[j] * g;
-                    sab[j] = sab[j] + g * conj(hist[k][j]);
-                    sw[j] = sw[j] + uu[k] * g;
+                    hc[j] = conj(a) * g;
+                    const cplx<T> ga = g * conj(hist[k][j]);
+                    const cplx<T> gpsi = uu[k] * g;
+                    if constexpr (PS) {
+                        const T dt = dk[k] * cf.dh;
+                        cplx<T> dal, dad, dsl, dsd;
+                        disc_partials<T>(scheme, cf.lam[j], dt, a, dal, dad, dsl, dsd);
+                        const cplx<T> gsc = conj(cf.bb[j]) * gpsi;
+                        s1[j] = s1[j] + conj(dal) * ga + conj(dsl) * gsc;
+                        s2[j] = s2[j] + conj(scl) * gpsi;
+                        s3[j] += dk[k] * ((conj(dad) * ga).re + (conj(dsd) * gsc).re);
+                    } else {
+                        s1[j] = s1[j] + ga;
+                        s2[j] = s2[j] + gpsi;
+                    }
                     sc[j] = sc[j] + gg[k] * conj(xcur);
-                    const cplx<T> gwc = g * wc[j];
-                    s += gwc.re;
+                    sm += (g * conj(wj)).re;
                 }
                 if (r == 0) sd += gg[k] * uu[k];
             }
-            part[k] = s;
+            part[k] = sm;
         }
         reduce_tile<T, G>(part);
         if (live && Out<G>::writer(r)) {
@@ -203,58 +427,147 @@ __global__ void __launch_bounds__(128) bwd_kernel(const T* __restrict__ u, const
                 if (k < nt) gup[(t0 + k) * H] = part[i] + dd * gp[(t0 + k) * H];
             }
         }
+        }
     }
     if (!live) return;
+    if (AGG) {
+#pragma unroll
+        for (int j = 0; j < NPL; ++j) {
+            aggA[s * BHN + o0 + j] = A[j];
+            aggH[s * BHN + o0 + j] = hc[j];
+        }
+        return;
+    }
+    const int64_t row = (int64_t)s * BHN;
 #pragma unroll
     for (int j = 0; j < NPL; ++j) {
-        const int64_t o = (b * H + h) * N + r * NPL + j;
-        gab_p[o] = sab[j];
-        gw_p[o] = sw[j];
-        gc_p[o] = sc[j];
+        p1[row + o0 + j] = s1[j];
+        p2[row + o0 + j] = s2[j];
+        if (PS) p3[row + o0 + j] = s3[j];
+        gc_p[row + o0 + j] = sc[j];
     }
-    if (r == 0) gd_p[b * H + h] = sd;
+    if (r == 0) gd_p[(int64_t)s * B * H + b * H + h] = sd;
+}
+
+// ---------------------------------------------------------------- host
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) !=
+                                                       cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = 148;
+        }
+    }
+    return n;
+}
+
+// Segments when the lanes alone give fewer than ~8 warps per SM (then ~16
+// warps per SM over the segments: the aggregate pass costs ~half a main pass,
+// measured B8 L4096 H256 N64: 2 segments 3.85 vs 1 3.2 ms); whole tiles,
+// >= 4 tiles per segment.  LRX_S4D_SEGS overrides.
+static SegGeo geometry(int64_t B, int64_t L, int64_t H, int64_t N) {
+    const int64_t G = N < 32 ? N : 32;
+    const int64_t lanes = B * H * G, tiles = cdiv(L, (int64_t)TT);
+    int64_t S = 1;
+    if (const char* e = getenv("LRX_S4D_SEGS")) S = atoll(e);
+    else if (lanes < (int64_t)sm_count() * 8 * 32) S = cdiv((int64_t)sm_count() * 16 * 32, lanes);
+    S = std::max<int64_t>(1, std::min<int64_t>({S, std::max<int64_t>(1, tiles / 4), 4096}));
+    SegGeo g;
+    g.seg_len = cdiv(tiles, S) * TT;
+    g.n_seg = cdiv(L, g.seg_len);
+    return g;
 }
 
 template <typename T>
-static int fwd_t(const void* u, const void* abar, const void* w, const void* c, const void* d, void* y, void* ckpt,
-                 void* xlast, int64_t B, int64_t L, int64_t H, int64_t N, cudaStream_t st) {
+static size_t ws_bytes(int64_t B, int64_t L, int64_t H, int64_t N) {
+    const SegGeo g = geometry(B, L, H, N);
+    return g.n_seg > 1 ? 2 * align_up((size_t)g.n_seg * B * H * N * sizeof(cplx<T>)) : 0;
+}
+
+template <typename T>
+static int fwd_t(const void* u, const void* abar, const void* w, const void* lam, const void* bv, const void* delta,
+                 const void* deltas, int scheme, const void* c, const void* d, void* y, void* ckpt, void* xlast,
+                 int64_t B, int64_t L, int64_t H, int64_t N, void* ws, size_t wsb, cudaStream_t st) {
     const int64_t G = N < 32 ? N : 32;
+    const SegGeo g = geometry(B, L, H, N);
+    LRX_REQUIRE(g.n_seg == 1 || (ws && wsb >= ws_bytes<T>(B, L, H, N)), LRX_ERR_VALUE,
+                "s4d: workspace of %zu bytes needed", ws_bytes<T>(B, L, H, N));
+    cplx<T>* aggA = static_cast<cplx<T>*>(ws);
+    cplx<T>* aggX = g.n_seg > 1 ? aggA + g.n_seg * B * H * N : nullptr;
     const unsigned grid = (unsigned)cdiv(B * H * G, 128);
-#define S4D_FWD(G_, NPL_)                                                                                       \
-    fwd_kernel<T, G_, NPL_><<<grid, 128, 0, st>>>((const T*)u, (const cplx<T>*)abar, (const cplx<T>*)w,        \
-                                                   (const cplx<T>*)c, (const T*)d, (T*)y, (cplx<T>*)ckpt,           \
-                                                   (cplx<T>*)xlast, B, L, H)
+    const bool ps = deltas != nullptr;
+    int n = 0;
+#define S4D_FWD(G_, NPL_, PS_, AGG_, NS_)                                                                          \
+    fwd_kernel<T, G_, NPL_, PS_, AGG_><<<dim3(grid, (unsigned)(NS_)), 128, 0, st>>>(                               \
+        (const T*)u, (const cplx<T>*)abar, (const cplx<T>*)w, (const cplx<T>*)lam, (const cplx<T>*)bv,            \
+        (const T*)delta, (const T*)deltas, scheme, (const cplx<T>*)c, (const T*)d, (T*)y, (cplx<T>*)ckpt,          \
+        (cplx<T>*)xlast, aggA, aggX, B, L, H, g.seg_len, (int)g.n_seg)
+#define S4D_FWD_ALL(G_, NPL_)                                                                                      \
+    do {                                                                                                           \
+        if (ps) {                                                                                                  \
+            if (g.n_seg > 1) S4D_FWD(G_, NPL_, true, true, g.n_seg - 1), ++n;                                      \
+            S4D_FWD(G_, NPL_, true, false, g.n_seg);                                                               \
+        } else {                                                                                                   \
+            if (g.n_seg > 1) S4D_FWD(G_, NPL_, false, true, g.n_seg - 1), ++n;                                     \
+            S4D_FWD(G_, NPL_, false, false, g.n_seg);                                                              \
+        }                                                                                                          \
+        ++n;                                                                                                       \
+    } while (0)
     switch (N) {
-        case 8: S4D_FWD(8, 1); break;
-        case 16: S4D_FWD(16, 1); break;
-        case 32: S4D_FWD(32, 1); break;
-        case 64: S4D_FWD(32, 2); break;
+        case 8: S4D_FWD_ALL(8, 1); break;
+        case 16: S4D_FWD_ALL(16, 1); break;
+        case 32: S4D_FWD_ALL(32, 1); break;
+        case 64: S4D_FWD_ALL(32, 2); break;
         default: set_error("s4d fused: d_state %lld not in {8, 16, 32, 64}", (long long)N); return LRX_ERR_UNSUPPORTED;
     }
+#undef S4D_FWD_ALL
 #undef S4D_FWD
-    return launched("lrx_s4d_fwd");
+    return launched("lrx_s4d_fwd", n);
 }
 
 template <typename T>
-static int bwd_t(const void* u, const void* gy, const void* abar, const void* w, const void* c, const void* d,
-                 const void* ckpt, void* gu, void* gab, void* gw, void* gc, void* gd, int64_t B, int64_t L, int64_t H,
-                 int64_t N, cudaStream_t st) {
+static int bwd_t(const void* u, const void* gy, const void* abar, const void* w, const void* lam, const void* bv,
+                 const void* delta, const void* deltas, int scheme, const void* c, const void* d, const void* ckpt,
+                 void* gu, void* p1, void* p2, void* p3, void* gc, void* gd, int64_t B, int64_t L, int64_t H,
+                 int64_t N, void* ws, size_t wsb, cudaStream_t st) {
     const int64_t G = N < 32 ? N : 32;
+    const SegGeo g = geometry(B, L, H, N);
+    LRX_REQUIRE(g.n_seg == 1 || (ws && wsb >= ws_bytes<T>(B, L, H, N)), LRX_ERR_VALUE,
+                "s4d: workspace of %zu bytes needed", ws_bytes<T>(B, L, H, N));
+    cplx<T>* aggA = static_cast<cplx<T>*>(ws);
+    cplx<T>* aggH = g.n_seg > 1 ? aggA + g.n_seg * B * H * N : nullptr;
     const unsigned grid = (unsigned)cdiv(B * H * G, 128);
-#define S4D_BWD(G_, NPL_)                                                                                        \
-    bwd_kernel<T, G_, NPL_><<<grid, 128, 0, st>>>((const T*)u, (const T*)gy, (const cplx<T>*)abar,              \
-                                                   (const cplx<T>*)w, (const cplx<T>*)c, (const T*)d,           \
-                                                   (const cplx<T>*)ckpt, (T*)gu, (cplx<T>*)gab, (cplx<T>*)gw,   \
-                                                   (cplx<T>*)gc, (T*)gd, B, L, H)
+    const bool ps = deltas != nullptr;
+    int n = 0;
+#define S4D_BWD(G_, NPL_, PS_, AGG_, NS_)                                                                          \
+    bwd_kernel<T, G_, NPL_, PS_, AGG_><<<dim3(grid, (unsigned)(NS_)), 128, 0, st>>>(                               \
+        (const T*)u, (const T*)gy, (const cplx<T>*)abar, (const cplx<T>*)w, (const cplx<T>*)lam,                   \
+        (const cplx<T>*)bv, (const T*)delta, (const T*)deltas, scheme, (const cplx<T>*)c, (const T*)d,            \
+        (const cplx<T>*)ckpt, (T*)gu, (cplx<T>*)p1, (cplx<T>*)p2, (T*)p3, (cplx<T>*)gc, (T*)gd, aggA, aggH, B, L, \
+        H, g.seg_len, (int)g.n_seg)
+#define S4D_BWD_ALL(G_, NPL_)                                                                                      \
+    do {                                                                                                           \
+        if (ps) {                                                                                                  \
+            if (g.n_seg > 1) S4D_BWD(G_, NPL_, true, true, g.n_seg - 1), ++n;                                      \
+            S4D_BWD(G_, NPL_, true, false, g.n_seg);                                                               \
+        } else {                                                                                                   \
+            if (g.n_seg > 1) S4D_BWD(G_, NPL_, false, true, g.n_seg - 1), ++n;                                     \
+            S4D_BWD(G_, NPL_, false, false, g.n_seg);                                                              \
+        }                                                                                                          \
+        ++n;                                                                                                       \
+    } while (0)
     switch (N) {
-        case 8: S4D_BWD(8, 1); break;
-        case 16: S4D_BWD(16, 1); break;
-        case 32: S4D_BWD(32, 1); break;
-        case 64: S4D_BWD(32, 2); break;
+        case 8: S4D_BWD_ALL(8, 1); break;
+        case 16: S4D_BWD_ALL(16, 1); break;
+        case 32: S4D_BWD_ALL(32, 1); break;
+        case 64: S4D_BWD_ALL(32, 2); break;
         default: set_error("s4d fused: d_state %lld not in {8, 16, 32, 64}", (long long)N); return LRX_ERR_UNSUPPORTED;
     }
+#undef S4D_BWD_ALL
 #undef S4D_BWD
-    return launched("lrx_s4d_bwd");
+    return launched("lrx_s4d_bwd", n);
 }
 
 }  // namespace s4d
@@ -271,27 +584,43 @@ int lrx_s4d_chunking(int64_t L, int64_t* chunk_len, int64_t* n_chunks) {
     return LRX_OK;
 }
 
-int lrx_s4d_fwd(int dtype, const void* u, const void* abar, const void* w, const void* c, const void* d, void* y,
-                void* ckpt, void* xlast, int64_t B, int64_t L, int64_t H, int64_t N, void* stream) {
+int lrx_s4d_geometry(int dtype, int64_t B, int64_t L, int64_t H, int64_t N, int64_t* geo) {
     LRX_REQUIRE(B >= 1 && L >= 1 && H >= 1 && N >= 1, LRX_ERR_SHAPE, "s4d: bad extents");
+    const s4d::SegGeo g = s4d::geometry(B, L, H, N);
+    geo[0] = g.n_seg;
+    geo[1] = (int64_t)(dtype == LRX_F64 ? s4d::ws_bytes<double>(B, L, H, N) : s4d::ws_bytes<float>(B, L, H, N));
+    return LRX_OK;
+}
+
+int lrx_s4d_fwd(int dtype, const void* u, const void* abar, const void* w, const void* lam, const void* b,
+                const void* delta, const void* deltas, int scheme, const void* c, const void* d, void* y, void* ckpt,
+                void* xlast, int64_t B, int64_t L, int64_t H, int64_t N, void* ws, size_t ws_bytes, void* stream) {
+    LRX_REQUIRE(B >= 1 && L >= 1 && H >= 1 && N >= 1, LRX_ERR_SHAPE, "s4d: bad extents");
+    LRX_REQUIRE(scheme >= 0 && scheme <= 2, LRX_ERR_VALUE, "s4d: scheme %d", scheme);
     cudaStream_t st = (cudaStream_t)stream;
-    if (dtype == LRX_F32) return s4d::fwd_t<float>(u, abar, w, c, d, y, ckpt, xlast, B, L, H, N, st);
-    if (dtype == LRX_F64) return s4d::fwd_t<double>(u, abar, w, c, d, y, ckpt, xlast, B, L, H, N, st);
+    if (dtype == LRX_F32)
+        return s4d::fwd_t<float>(u, abar, w, lam, b, delta, deltas, scheme, c, d, y, ckpt, xlast, B, L, H, N, ws,
+                                 ws_bytes, st);
+    if (dtype == LRX_F64)
+        return s4d::fwd_t<double>(u, abar, w, lam, b, delta, deltas, scheme, c, d, y, ckpt, xlast, B, L, H, N, ws,
+                                  ws_bytes, st);
     set_error("s4d: dtype %d (f32 / f64)", dtype);
     return LRX_ERR_VALUE;
 }
 
-int lrx_s4d_bwd(int dtype, const void* u, const void* gy, const void* abar, const void* w, const void* c,
-                const void* d, const void* ckpt, void* gu, void* gabar_part, void* gw_part, void* gc_part,
-                void* gd_part, int64_t B, int64_t L, int64_t H, int64_t N, void* stream) {
+int lrx_s4d_bwd(int dtype, const void* u, const void* gy, const void* abar, const void* w, const void* lam,
+                const void* b, const void* delta, const void* deltas, int scheme, const void* c, const void* d,
+                const void* ckpt, void* gu, void* p1_part, void* p2_part, void* p3_part, void* gc_part, void* gd_part,
+                int64_t B, int64_t L, int64_t H, int64_t N, void* ws, size_t ws_bytes, void* stream) {
     LRX_REQUIRE(B >= 1 && L >= 1 && H >= 1 && N >= 1, LRX_ERR_SHAPE, "s4d: bad extents");
+    LRX_REQUIRE(scheme >= 0 && scheme <= 2, LRX_ERR_VALUE, "s4d: scheme %d", scheme);
     cudaStream_t st = (cudaStream_t)stream;
     if (dtype == LRX_F32)
-        return s4d::bwd_t<float>(u, gy, abar, w, c, d, ckpt, gu, gabar_part, gw_part, gc_part, gd_part, B, L, H, N,
-                                 st);
+        return s4d::bwd_t<float>(u, gy, abar, w, lam, b, delta, deltas, scheme, c, d, ckpt, gu, p1_part, p2_part,
+                                 p3_part, gc_part, gd_part, B, L, H, N, ws, ws_bytes, st);
     if (dtype == LRX_F64)
-        return s4d::bwd_t<double>(u, gy, abar, w, c, d, ckpt, gu, gabar_part, gw_part, gc_part, gd_part, B, L, H, N,
-                                  st);
+        return s4d::bwd_t<double>(u, gy, abar, w, lam, b, delta, deltas, scheme, c, d, ckpt, gu, p1_part, p2_part,
+                                  p3_part, gc_part, gd_part, B, L, H, N, ws, ws_bytes, st);
     set_error("s4d: dtype %d (f32 / f64)", dtype);
     return LRX_ERR_VALUE;
 }

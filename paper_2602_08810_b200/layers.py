@@ -430,33 +430,28 @@ class S4D(LinearRecurrence):
         return lam, delta, b, abar, scale
 
     def _fused(self, deltas, shape):
-        """Fused S4D kernel (csrc/lrx_s4d.cu) for constant steps and d_state
-        in {8, 16, 32, 64}; per-step deltas keep the generic operator path, and
-        so do long sequences over few channels, where the fused kernel's one
-        walk per lane is latency-bound and the time-segmented generic scan wins
-        (measured: B1 L65536 H64 N64 24.6 vs 8.7 ms; B8 L4096 H256 N64 3.2 vs
-        25.8 ms the other way)."""
-        env = os.environ.get("LRX_S4D_GENERIC")
-        if deltas is not None or self.d_state not in ops.S4D_FUSED_N or env == "1":
-            return False
-        B, L, m = shape
-        threads = B * m * min(self.d_state, 32)
-        if env == "0" or not (threads < _sm_count(self.device) * 32 * 3 // 2 and L >= 8192):
-            return True
-        # the generic path materialises ~6 complex [B, L, m, n] planes (w, its
-        # time-major copy, x, and the backward's cotangents): keep the fused
-        # kernel whenever they would not fit comfortably in free memory
-        plane = B * L * m * self.d_state * torch.tensor([], dtype=self.tcdt).element_size()
-        free, _ = torch.cuda.mem_get_info(self.device)
-        return 6 * plane > free // 2
+        """Fused S4D kernel (csrc/lrx_s4d.cu) for d_state in {8, 16, 32, 64}:
+        constant steps and per-step deltas (discretised in the kernel), time
+        segments for long sequences over few channels; other widths take the
+        generic operator path."""
+        return self.d_state in ops.S4D_FUSED_N and os.environ.get("LRX_S4D_GENERIC") != "1"
+
+    def _fused_args(self, deltas):
+        c = torch.complex(self.c_re, self.c_im).contiguous()
+        if deltas is None:
+            lam, delta, b, abar, scale = self._coeffs(None)
+            return c, dict(abar=abar.to(self.tcdt).contiguous(), w=(scale * b).to(self.tcdt).contiguous())
+        # per-step discretisation in the kernel; bilinear cannot be singular
+        # here: Re(lambda) = -exp(.) < 0 and deltas >= 0 keep |1 - delta lambda / 2| >= 1
+        return c, dict(lam=self._lam().to(self.tcdt).contiguous(), b=torch.complex(self.b_re, self.b_im).contiguous(),
+                       delta=torch.exp(self.log_delta).contiguous(), deltas=deltas.to(self.tdt).contiguous(),
+                       scheme=self.discretization)
 
     def _forward(self, u, deltas, keep):
         if self._fused(deltas, u.shape):
-            lam, delta, b, abar, scale = self._coeffs(None)
-            w = (scale * b).to(self.tcdt).contiguous()
-            c = torch.complex(self.c_re, self.c_im).contiguous()
-            y, ckpt, xlast = ops.s4d_scan_fwd(u, abar.to(self.tcdt).contiguous(), w, c, self.d.contiguous())
-            saved = {"u": u, "ckpt": ckpt, "deltas": None, "fused": True} if keep else {}
+            c, kw = self._fused_args(deltas)
+            y, ckpt, xlast = ops.s4d_scan_fwd(u, c, self.d.contiguous(), **kw)
+            saved = {"u": u, "ckpt": ckpt, "deltas": deltas, "fused": True} if keep else {}
             return y, saved, xlast
         B, L, m = u.shape
         n = self.d_state
@@ -499,23 +494,25 @@ class S4D(LinearRecurrence):
         return y
 
     def _backward_fused(self, s, gy):
-        u, ckpt, host = s["u"], s["ckpt"], s["host"]
+        u, ckpt, host, deltas = s["u"], s["ckpt"], s["host"], s["deltas"]
         gy = self._gy(gy, u.shape)
-        lam, delta, b, abar, scale = self._coeffs(None)
-        w = (scale * b).to(self.tcdt).contiguous()
-        c = torch.complex(self.c_re, self.c_im).contiguous()
-        r = ops.s4d_scan_bwd(u, gy, abar.to(self.tcdt).contiguous(), w, c, self.d.contiguous(), ckpt)
-        c128 = torch.complex128
-        gabar, gpsi = r["gabar"].to(c128), r["gw"].to(c128)
-        gscale = b.conj() * gpsi
-        gb = scale.conj() * gpsi
-        dal, dad, dsl, dsd = scheme_partials(self.discretization, lam, delta[:, None], abar, scale)
-        glam = dal.conj() * gabar + dsl.conj() * gscale
-        gdel = ((dad.conj() * gabar).real + (dsd.conj() * gscale).real).sum(-1)
+        c, kw = self._fused_args(deltas)
+        r = ops.s4d_scan_bwd(u, gy, c, self.d.contiguous(), ckpt, **kw)
+        if deltas is None:
+            lam, delta, b, abar, scale = self._coeffs(None)
+            c128 = torch.complex128
+            gabar, gpsi = r["gabar"].to(c128), r["gw"].to(c128)
+            gscale = b.conj() * gpsi
+            gb = scale.conj() * gpsi
+            dal, dad, dsl, dsd = scheme_partials(self.discretization, lam, delta[:, None], abar, scale)
+            glam = dal.conj() * gabar + dsl.conj() * gscale
+            glog_delta = ((dad.conj() * gabar).real + (dsd.conj() * gscale).real).sum(-1) * delta
+        else:  # the kernel accumulated the per-step scheme partials (autograd.py:186-211)
+            glam, gb, glog_delta = r["glam"], r["gb"], r["gdl"]
         gc = r["gc"]
-        grads = {"lambda_re_log": -torch.exp(self.lambda_re_log.double()) * glam.real, "lambda_im": glam.imag,
-                 "b.re": gb.real, "b.im": gb.imag, "c.re": gc.real, "c.im": gc.imag, "d": r["gd"],
-                 "log_delta": gdel * delta}
+        grads = {"lambda_re_log": -torch.exp(self.lambda_re_log.to(glam.real.dtype)) * glam.real,
+                 "lambda_im": glam.imag, "b.re": gb.real, "b.im": gb.imag, "c.re": gc.real, "c.im": gc.imag,
+                 "d": r["gd"], "log_delta": glog_delta}
         grads = {k: v.to(self.tdt).contiguous() for k, v in grads.items()}
         return self._out({k: grads[k] for k in self.parameters()}, r["gu"], host)
 

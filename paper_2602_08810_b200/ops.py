@@ -345,32 +345,62 @@ def mimo_scan_bwd(abar, scale, bu, x, gx):
 S4D_FUSED_N = (8, 16, 32, 64)
 
 
-def s4d_scan_fwd(u, abar, w, c, d):
-    """y = Re(sum_n c x) + d u with x_n = abar_n x_n + w_n u over u [B, L, H]
-    (real, f32/f64); abar, w, c [H, N] complex.  Returns (y, ckpt)."""
+SCHEME_CODE = {"zoh": 0, "bilinear": 1, "dirac": 2}
+
+
+def s4d_geometry(dtype, B, L, H, N):
+    """(n_seg, ws_bytes): time segments of the fused S4D kernels (partial rows = n_seg * B)."""
+    g = (ctypes.c_int64 * 2)()
+    _lib.check(_lib.lib().lrx_s4d_geometry(_lib.code_of(dtype), B, L, H, N, g))
+    return int(g[0]), int(g[1])
+
+
+def s4d_scan_fwd(u, c, d, abar=None, w=None, lam=None, b=None, delta=None, deltas=None, scheme="zoh"):
+    """y = Re(sum_n c x) + d u over u [B, L, H] (real, f32/f64) with
+    x_n = abar_n x_n + w_n u.  Constant step: abar, w (= scale b) [H, N]
+    complex.  Per step (asynchronous): lam, b [H, N] complex, delta [H]
+    (= exp(log_delta)), deltas [B, L], scheme -- the kernel discretises every
+    step.  Returns (y, ckpt, xlast)."""
     B, L, H = u.shape
-    N = abar.shape[-1]
+    N = c.shape[-1]
     ck, nc = _lib.i64(), _lib.i64()
     _lib.check(_lib.lib().lrx_s4d_chunking(L, _lib.ref(ck), _lib.ref(nc)))
+    _, wsb = s4d_geometry(u.dtype, B, L, H, N)
     y = torch.empty_like(u)
-    ckpt = torch.empty((B, nc.value, H, N), dtype=abar.dtype, device=u.device)
-    xl = torch.empty((B, H, N), dtype=abar.dtype, device=u.device)
-    _lib.check(_lib.lib().lrx_s4d_fwd(_lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(abar), _lib.ptr(w), _lib.ptr(c),
-                                      _lib.ptr(d), _lib.ptr(y), _lib.ptr(ckpt), _lib.ptr(xl), B, L, H, N,
-                                      _lib.stream()))
+    ckpt = torch.empty((B, nc.value, H, N), dtype=c.dtype, device=u.device)
+    xl = torch.empty((B, H, N), dtype=c.dtype, device=u.device)
+    ws = _lib.workspace(wsb, u.device)
+    _lib.check(_lib.lib().lrx_s4d_fwd(_lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(abar), _lib.ptr(w), _lib.ptr(lam),
+                                      _lib.ptr(b), _lib.ptr(delta), _lib.ptr(deltas), SCHEME_CODE[scheme],
+                                      _lib.ptr(c), _lib.ptr(d), _lib.ptr(y), _lib.ptr(ckpt), _lib.ptr(xl), B, L, H, N,
+                                      _lib.ptr(ws), ws.numel(), _lib.stream()))
     return y, ckpt, xl
 
 
-def s4d_scan_bwd(u, gy, abar, w, c, d, ckpt):
-    """Pullback of s4d_scan_fwd: dict gu [B, L, H]; gabar, gw (= sum u g), gc [H, N]
-    complex; gd [H] (batch sums in a fixed order)."""
+def s4d_scan_bwd(u, gy, c, d, ckpt, abar=None, w=None, lam=None, b=None, delta=None, deltas=None, scheme="zoh"):
+    """Pullback of s4d_scan_fwd: dict gu [B, L, H]; gc [H, N] complex; gd [H];
+    constant step: gabar, gw (= sum u g) [H, N] complex; per step: glam, gb
+    [H, N] complex and gdl [H] (= d loss / d log_delta).  Batch / segment sums
+    in a fixed order (lrx_reduce_rows)."""
     B, L, H = u.shape
-    N = abar.shape[-1]
+    N = c.shape[-1]
+    n_seg, wsb = s4d_geometry(u.dtype, B, L, H, N)
+    R = n_seg * B
     gu = torch.empty_like(u)
-    f = dict(dtype=abar.dtype, device=u.device)
-    gab, gw, gc = (torch.empty((B, H, N), **f) for _ in range(3))
-    gd = torch.empty((B, H), dtype=u.dtype, device=u.device)
+    f = dict(dtype=c.dtype, device=u.device)
+    p1, p2, gcp = (torch.empty((R, H * N), **f) for _ in range(3))
+    p3 = torch.empty((R, H * N), dtype=u.dtype, device=u.device) if deltas is not None else None
+    gdp = torch.empty((R, H), dtype=u.dtype, device=u.device)
+    ws = _lib.workspace(wsb, u.device)
     _lib.check(_lib.lib().lrx_s4d_bwd(_lib.code_of(u.dtype), _lib.ptr(u), _lib.ptr(gy), _lib.ptr(abar), _lib.ptr(w),
-                                      _lib.ptr(c), _lib.ptr(d), _lib.ptr(ckpt), _lib.ptr(gu), _lib.ptr(gab),
-                                      _lib.ptr(gw), _lib.ptr(gc), _lib.ptr(gd), B, L, H, N, _lib.stream()))
-    return {"gu": gu, "gabar": gab.sum(0), "gw": gw.sum(0), "gc": gc.sum(0), "gd": gd.sum(0)}
+                                      _lib.ptr(lam), _lib.ptr(b), _lib.ptr(delta), _lib.ptr(deltas),
+                                      SCHEME_CODE[scheme], _lib.ptr(c), _lib.ptr(d), _lib.ptr(ckpt), _lib.ptr(gu),
+                                      _lib.ptr(p1), _lib.ptr(p2), _lib.ptr(p3), _lib.ptr(gcp), _lib.ptr(gdp), B, L, H,
+                                      N, _lib.ptr(ws), ws.numel(), _lib.stream()))
+    out = {"gu": gu, "gc": reduce_rows(gcp, R, H * N).reshape(H, N), "gd": reduce_rows(gdp, R, H)}
+    s1, s2 = reduce_rows(p1, R, H * N).reshape(H, N), reduce_rows(p2, R, H * N).reshape(H, N)
+    if deltas is None:
+        out.update(gabar=s1, gw=s2)
+    else:
+        out.update(glam=s1, gb=s2, gdl=reduce_rows(p3, R, H * N).reshape(H, N).sum(-1) * delta)
+    return out

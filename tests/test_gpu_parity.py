@@ -556,6 +556,60 @@ def test_s4d_fused_kernel_matches_oracle(lrx, n, scheme, dtype):
         assert rel(yk, ry[:, k]) < tol
 
 
+@pytest.mark.parametrize("n", [8, 32, 64])
+@pytest.mark.parametrize("scheme", ["zoh", "bilinear", "dirac"])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_s4d_async_fused_matches_oracle(lrx, n, scheme, dtype):
+    """Asynchronous S4D (per-step deltas [B, L], layers.py:402-440) on the
+    fused kernel: abar_k / scale_k discretised in the kernel, the coefficient
+    gradients through the scheme partials accumulated per lane (no [B, L, m, n]
+    planes) -- against the oracle, every parameter gradient."""
+    m, B, L = 6, 2, 203
+    layer = lrx.make_layer("s4d", m, n, scheme, asynchronous=True, dtype=dtype, seed=64)
+    u = port.Rng(65).normal((B, L, m)).astype(layer.rdt)
+    gy = port.Rng(66).normal((B, L, m)).astype(layer.rdt)
+    deltas = port.Rng(67).uniform(0.1, 3.0, (B, L)).astype(layer.rdt)
+    y, tape = layer.forward(u, deltas=deltas, tape=True)
+    assert tape._saved.get("fused")
+    g = lrx.layer_backward(layer, tape, gy)
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64("s4d", scheme, params, u, gy, deltas=deltas, asyn=True)
+    tol = TOL[dtype]
+    assert rel(y, ry) < tol
+    assert rel(g.u, rgu) < tol
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < tol, (k, rel(g.params[k], rg[k]))
+
+
+@pytest.mark.parametrize("segs", ["1", "3", "auto"])
+@pytest.mark.parametrize("asyn", [False, True])
+def test_s4d_time_segments_match_oracle(lrx, monkeypatch, segs, asyn):
+    """Fused S4D with the sequence cut into time segments (aggregate maps
+    folded in a fixed order; ragged last segment), constant and per-step
+    steps, against the oracle; a re-run gives the same bits."""
+    if segs != "auto":
+        monkeypatch.setenv("LRX_S4D_SEGS", segs)
+    m, B, L, n = 3, 1, 1000, 16
+    layer = lrx.make_layer("s4d", m, n, "zoh", asynchronous=asyn, dtype="f64", seed=68)
+    u = port.Rng(69).normal((B, L, m))
+    gy = port.Rng(70).normal((B, L, m))
+    deltas = port.Rng(71).uniform(0.1, 2.0, (B, L)) if asyn else None
+    y, tape = layer.forward(u, deltas=deltas, tape=True)
+    g = lrx.layer_backward(layer, tape, gy)
+    y2, tape2 = layer.forward(u, deltas=deltas, tape=True)
+    g2 = lrx.layer_backward(layer, tape2, gy)
+    assert np.array_equal(y, y2) and np.array_equal(g.u, g2.u)
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64("s4d", "zoh", params, u, gy, deltas=deltas, asyn=asyn)
+    assert rel(y, ry) < 1e-10
+    assert rel(g.u, rgu) < 1e-10
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < 1e-10, (segs, k)
+    _, st = layer.forward(u, deltas=deltas, return_state=True)
+    xl = st.x.cpu().numpy()
+    assert np.isfinite(xl).all()
+
+
 @pytest.mark.parametrize("seg", ["16", "128", "1024"])
 def test_mimo_segment_lengths_match_oracle(lrx, monkeypatch, seg):
     """MIMO scans with forced segment lengths (LRX_MIMO_SEG; ragged last one)."""
