@@ -222,6 +222,20 @@ int lrx_s4d_bwd(int dtype, const void* u, const void* gy, const void* abar, cons
                 const void* ckpt, void* gu, void* p1_part, void* p2_part, void* p3_part, void* gc_part, void* gd_part,
                 int64_t B, int64_t L, int64_t H, int64_t N, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- MIMO scan with per-step steps (asynchronous S5, layers.py:650-658) ----
+ * x_k = abar_k x_{k-1} + scale_k bu_k with (abar_k, scale_k) = scheme(lam[p],
+ * deltas[b, k] delta[p]) computed in the kernel (scheme 0 ZOH / 1 bilinear /
+ * 2 dirac; discretize.py:59-93).  lam [P] complex, delta [P] = exp(log_delta)
+ * and deltas [B, L] real of the matching precision; bu, x, gx, gbu [B, L, P].
+ * Backward partials [n_chunks * B, P] (lrx_mimo_chunking): glam (complex) and
+ * gdl = sum_k deltas_k d delta_k (real; times delta[p]: d log_delta). */
+size_t lrx_mimo_ps_workspace_bytes(int dtype, int64_t B, int64_t L, int64_t P);
+int lrx_mimo_fwd_ps(int dtype, const void* lam, const void* delta, const void* deltas, int scheme, const void* bu,
+                    void* x, int64_t B, int64_t L, int64_t P, void* workspace, size_t workspace_bytes, void* stream);
+int lrx_mimo_bwd_ps(int dtype, const void* lam, const void* delta, const void* deltas, int scheme, const void* bu,
+                    const void* x, const void* gx, void* gbu, void* glam_part, void* gdl_part, int64_t B, int64_t L,
+                    int64_t P, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- MIMO LTI coefficient work (S5 / LRU), one launch each way ------------
  * Replaces the parameter-sized torch glue of S5._abar_scale / LRU._abar_scale
  * (layers.py:823-834, 936-943) and the coefficient + B/C gradient assembly of

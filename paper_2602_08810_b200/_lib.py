@@ -48,6 +48,9 @@ SIGNATURES = {
     "lrx_mimo_fwd": (_i, [_i, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp]),
     "lrx_mimo_bwd_workspace_bytes": (_sz, [_i, _i64, _i64, _i64]),
     "lrx_mimo_bwd": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp]),
+    "lrx_mimo_ps_workspace_bytes": (_sz, [_i, _i64, _i64, _i64]),
+    "lrx_mimo_fwd_ps": (_i, [_i, _vp, _vp, _vp, _i, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp]),
+    "lrx_mimo_bwd_ps": (_i, [_i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp]),
     "lrx_reduce_rows": (_i, [_i, _vp, _vp, _i64, _i64, _vp]),
     "lrx_reduce_rows_ws_bytes": (_sz, [_i, _i64, _i64]),
     "lrx_reduce_rows_ws": (_i, [_i, _vp, _vp, _vp, _i64, _i64, _vp, _sz, _vp]),

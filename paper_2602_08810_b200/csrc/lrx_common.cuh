@@ -169,6 +169,127 @@ template <> struct Fast<double> {
     __device__ static double expm1_known(double x, double) { return ::expm1(x); }
 };
 
+// ---------------------------------------------------------------- per-step discretisation
+// (asynchronous S4D / S5: lrx_s4d.cu, lrx_mimo.cu)  discretize.py:59-93 and
+// autograd.py:186-211 (scheme_partials), evaluated per step in the kernels.
+// ZOH: scale = (abar - 1) / lam and d scale / d lam = (dt abar lam - (abar - 1)) / lam^2
+// cancel catastrophically for small |z| = |dt lam| (f32 at z ~ 1e-4 keeps ~3
+// digits), so below a threshold they run as the series
+//   scale = dt phi1(z),  phi1 = sum z^k / (k+1)!,
+//   dsl   = dt^2 phi2(z), phi2 = sum z^k (k+1) / (k+2)!
+// (f32: |z| < 0.5, 9 terms; f64: |z| < 0.05, 11 terms -- truncation below the
+// unit roundoff); the reference's small-pole branch is the z -> 0 limit.
+template <typename T> __device__ __forceinline__ T small_pole_eps();
+template <> __device__ __forceinline__ float small_pole_eps<float>() { return 1e-4f; }   // discretize.py:39-42
+template <> __device__ __forceinline__ double small_pole_eps<double>() { return 1e-8; }
+template <typename T> struct ZohSeries;
+template <> struct ZohSeries<float> { static constexpr float R = 0.5f; static constexpr int K = 9; };
+template <> struct ZohSeries<double> { static constexpr double R = 0.05; static constexpr int K = 11; };
+__device__ __forceinline__ void sc_(float x, float* s, float* c) { sincosf(x, s, c); }
+__device__ __forceinline__ void sc_(double x, double* s, double* c) { sincos(x, s, c); }
+__device__ __forceinline__ float ex_(float x) { return expf(x); }
+__device__ __forceinline__ double ex_(double x) { return exp(x); }
+
+template <typename T>
+__device__ __forceinline__ cplx<T> cdiv_(cplx<T> a, cplx<T> b) {
+    const T den = b.re * b.re + b.im * b.im;
+    return {(a.re * b.re + a.im * b.im) / den, (a.im * b.re - a.re * b.im) / den};
+}
+
+// phi1(z) = sum_{k<K} z^k / (k+1)!, phi2(z) = sum_{k<K} z^k (k+1) / (k+2)! (Horner)
+template <typename T>
+__device__ __forceinline__ void zoh_series(cplx<T> z, cplx<T>& p1, cplx<T>& p2) {
+    constexpr int K = ZohSeries<T>::K;
+    T f1[K], f2[K];
+    T fact = T(1);  // (k+1)!
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        fact *= T(k + 1);
+        f1[k] = T(1) / fact;
+        f2[k] = T(k + 1) / (fact * T(k + 2));
+    }
+    p1 = {f1[K - 1], T(0)};
+    p2 = {f2[K - 1], T(0)};
+#pragma unroll
+    for (int k = K - 2; k >= 0; --k) {
+        p1 = p1 * z + cplx<T>{f1[k], T(0)};
+        p2 = p2 * z + cplx<T>{f2[k], T(0)};
+    }
+}
+
+enum { SCHEME_ZOH = 0, SCHEME_BILINEAR = 1, SCHEME_DIRAC = 2 };
+
+template <typename T>
+__device__ __forceinline__ bool small_pole(cplx<T> lam) {  // the reference's branch (discretize.py:59-68)
+    return sqrt(lam.re * lam.re + lam.im * lam.im) < small_pole_eps<T>();
+}
+template <typename T>
+__device__ __forceinline__ bool zoh_small(cplx<T> z) {
+    return z.re * z.re + z.im * z.im < ZohSeries<T>::R * ZohSeries<T>::R;
+}
+
+// (abar, scale) of one step dt for pole lam (discretize.py:59-93)
+template <typename T>
+__device__ __forceinline__ void disc(int scheme, cplx<T> lam, T dt, cplx<T>& ab, cplx<T>& sc) {
+    const cplx<T> z = dt * lam;
+    if (scheme == SCHEME_BILINEAR) {
+        const cplx<T> den = {T(1) - T(0.5) * z.re, -T(0.5) * z.im};
+        ab = cdiv_(cplx<T>{T(1) + T(0.5) * z.re, T(0.5) * z.im}, den);
+        sc = cdiv_(cplx<T>{dt, T(0)}, den);
+        return;
+    }
+    T sn, cs;
+    sc_(z.im, &sn, &cs);
+    const T e = ex_(z.re);
+    ab = {e * cs, e * sn};
+    if (scheme == SCHEME_DIRAC) {
+        sc = {T(1), T(0)};
+    } else if (small_pole(lam)) {
+        sc = {dt, T(0)};
+    } else if (zoh_small(z)) {
+        cplx<T> p1, p2;
+        zoh_series(z, p1, p2);
+        sc = dt * p1;
+    } else {
+        sc = cdiv_(ab - cplx<T>{T(1), T(0)}, lam);
+    }
+}
+
+// partials d abar / d lam, d abar / d dt, d scale / d lam, d scale / d dt
+template <typename T>
+__device__ __forceinline__ void disc_partials(int scheme, cplx<T> lam, T dt, cplx<T> ab, cplx<T>& dal, cplx<T>& dad,
+                                              cplx<T>& dsl, cplx<T>& dsd) {
+    if (scheme == SCHEME_BILINEAR) {
+        const cplx<T> den = {T(1) - T(0.5) * dt * lam.re, -T(0.5) * dt * lam.im};
+        const cplx<T> inv2 = cdiv_(cplx<T>{T(1), T(0)}, den * den);
+        dal = dt * inv2;
+        dad = lam * inv2;
+        dsl = (T(0.5) * dt * dt) * inv2;
+        dsd = inv2;
+        return;
+    }
+    dal = dt * ab;
+    dad = lam * ab;
+    if (scheme == SCHEME_DIRAC) {
+        dsl = dsd = cplx<T>{T(0), T(0)};
+        return;
+    }
+    const cplx<T> z = dt * lam;
+    if (small_pole(lam)) {
+        dsl = {T(0.5) * dt * dt, T(0)};
+        dsd = {T(1), T(0)};
+        return;
+    }
+    dsd = ab;
+    if (zoh_small(z)) {
+        cplx<T> p1, p2;
+        zoh_series(z, p1, p2);
+        dsl = (dt * dt) * p2;
+    } else {
+        dsl = cdiv_(dt * (ab * lam) - (ab - cplx<T>{T(1), T(0)}), lam * lam);
+    }
+}
+
 // ---------------------------------------------------------------- look-back
 // Status words per tile: 0 = nothing yet, 1 = aggregate published,
 // 2 = inclusive published.  Tiles are (chunk, lane block); values are per lane.

@@ -233,6 +233,111 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const cplx<T>* __restrict
     gscale_part[(int64_t)s * n_lanes + lane] = ss;
 }
 
+// ----------------------------------------------------------------------------
+// Per-step coefficients (asynchronous S5, layers.py:650-658 with
+// delta_k = deltas[b, k] * exp(log_delta[p]), discretize.py:59-93): abar_k and
+// scale_k are computed in the kernel (no [B, L, P] coefficient planes); the
+// segment maps carry the explicit product of the abar_k.  The backward
+// accumulates the coefficient gradients through the scheme partials
+// (autograd.py:186-211, S5._backward 836-895):
+//   glam += conj(dal) ga + conj(dsl) gscale,  gdl += deltas_k Re(conj(dad) ga + conj(dsd) gscale)
+// with ga = g conj(x_{k-1}), gscale = conj(bu_k) g; per-(segment, lane) partials.
+template <typename T, bool AGG>
+__global__ void __launch_bounds__(kThreads) fwd_ps_kernel(const cplx<T>* __restrict__ lam, const T* __restrict__ delta,
+                                                          const T* __restrict__ deltas, int scheme,
+                                                          const cplx<T>* __restrict__ bu, cplx<T>* __restrict__ aggA,
+                                                          cplx<T>* __restrict__ aggX, cplx<T>* __restrict__ x,
+                                                          int64_t B, int64_t L, int64_t P, int seg) {
+    using V = cplx<T>;
+    const int64_t n_lanes = B * P;
+    const int64_t lane = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (lane >= n_lanes) return;
+    const int s = blockIdx.y;
+    const int64_t b = lane / P, p = lane % P;
+    const V lm = lam[p];
+    const T dp = delta[p];
+    V xs = Traits<V>::zero(), A = Traits<V>::one();
+    if (!AGG)
+        for (int r = 0; r < s; ++r) xs = aggA[(int64_t)r * n_lanes + lane] * xs + aggX[(int64_t)r * n_lanes + lane];
+    const int64_t t0 = (int64_t)s * seg;
+    const int nt = (int)min((int64_t)seg, L - t0);
+    const int64_t base = (b * L + t0) * P + p;
+    const T* dk = deltas + b * L + t0;
+    for (int k = 0; k < nt; ++k) {
+        V ab, sc;
+        disc<T>(scheme, lm, dk[k] * dp, ab, sc);
+        xs = ab * xs + sc * ldc(bu + base + (int64_t)k * P);
+        if (AGG) A = ab * A;
+        else stc(x + base + (int64_t)k * P, xs);
+    }
+    if (AGG) {
+        aggA[(int64_t)s * n_lanes + lane] = A;
+        aggX[(int64_t)s * n_lanes + lane] = xs;
+    }
+}
+
+template <typename T, bool AGG>
+__global__ void __launch_bounds__(kThreads) bwd_ps_kernel(const cplx<T>* __restrict__ lam, const T* __restrict__ delta,
+                                                          const T* __restrict__ deltas, int scheme,
+                                                          const cplx<T>* __restrict__ bu,
+                                                          const cplx<T>* __restrict__ x,
+                                                          const cplx<T>* __restrict__ gx, cplx<T>* __restrict__ aggA,
+                                                          cplx<T>* __restrict__ aggH, cplx<T>* __restrict__ gbu,
+                                                          cplx<T>* __restrict__ glam_part, T* __restrict__ gdl_part,
+                                                          int64_t B, int64_t L, int64_t P, int S, int seg) {
+    using V = cplx<T>;
+    const int64_t n_lanes = B * P;
+    const int64_t lane = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (lane >= n_lanes) return;
+    const int s = AGG ? blockIdx.y + 1 : blockIdx.y;
+    const int64_t b = lane / P, p = lane % P;
+    const V lm = lam[p];
+    const T dp = delta[p];
+    V h = Traits<V>::zero(), A = Traits<V>::one();
+    if (!AGG)
+        for (int r = S - 1; r > s; --r) h = aggA[(int64_t)r * n_lanes + lane] * h + aggH[(int64_t)r * n_lanes + lane];
+    const int64_t t0 = (int64_t)s * seg;
+    const int nt = (int)min((int64_t)seg, L - t0);
+    const int64_t base = (b * L + t0) * P + p;
+    const T* dk = deltas + b * L + t0;
+    V sl = Traits<V>::zero();
+    T sdl = T(0);
+    for (int k = nt - 1; k >= 0; --k) {
+        const T dt = dk[k] * dp;
+        V ab, sc;
+        disc<T>(scheme, lm, dt, ab, sc);
+        const int64_t off = base + (int64_t)k * P;
+        const V g = ldc(gx + off) + h;
+        h = conj(ab) * g;
+        if (AGG) {
+            A = conj(ab) * A;
+            continue;
+        }
+        stc(gbu + off, conj(sc) * g);
+        const V xp = t0 + k > 0 ? ldc(x + off - P) : Traits<V>::zero();
+        const V ga = g * conj(xp), gsc = conj(ldc(bu + off)) * g;
+        V dal, dad, dsl, dsd;
+        disc_partials<T>(scheme, lm, dt, ab, dal, dad, dsl, dsd);
+        sl = sl + conj(dal) * ga + conj(dsl) * gsc;
+        sdl += dk[k] * ((conj(dad) * ga).re + (conj(dsd) * gsc).re);
+    }
+    if (AGG) {
+        aggA[(int64_t)s * n_lanes + lane] = A;
+        aggH[(int64_t)s * n_lanes + lane] = h;
+        return;
+    }
+    glam_part[(int64_t)s * n_lanes + lane] = sl;
+    gdl_part[(int64_t)s * n_lanes + lane] = sdl;
+}
+
+template <typename T>
+static int fwd_ps_t(const void* lam, const void* delta, const void* deltas, int scheme, const void* bu, void* x,
+                    int64_t B, int64_t L, int64_t P, void* w, size_t wb, cudaStream_t st);
+template <typename T>
+static int bwd_ps_t(const void* lam, const void* delta, const void* deltas, int scheme, const void* bu, const void* x,
+                    const void* gx, void* gbu, void* glp, void* gdp, int64_t B, int64_t L, int64_t P, void* w,
+                    size_t wb, cudaStream_t st);
+
 template <typename T>
 static size_t ws_bytes(int64_t B, int64_t L, int64_t P) {
     const int64_t S = cdiv(L, (int64_t)seg_len(B, L, P));
@@ -276,6 +381,56 @@ static int bwd_t(const void* abar, const void* scale, const void* bu, const void
         (const cplx<T>*)abar, (const cplx<T>*)scale, (const cplx<T>*)bu, (const cplx<T>*)x, (const cplx<T>*)gx, aggH,
         (cplx<T>*)gbu, (cplx<T>*)gap, (cplx<T>*)gsp, B, L, P, (int)S, seg);
     return launched("lrx_mimo_bwd", n);
+}
+
+template <typename T>
+static size_t ws_ps_bytes(int64_t B, int64_t L, int64_t P) {
+    return 2 * ws_bytes<T>(B, L, P);
+}
+
+template <typename T>
+static int fwd_ps_t(const void* lam, const void* delta, const void* deltas, int scheme, const void* bu, void* x,
+                    int64_t B, int64_t L, int64_t P, void* w, size_t wb, cudaStream_t st) {
+    const int seg = seg_len(B, L, P);
+    const int64_t S = cdiv(L, (int64_t)seg), nb = cdiv(B * P, kThreads);
+    LRX_REQUIRE(S <= 65535 && nb <= 0x7fffffff, LRX_ERR_UNSUPPORTED, "mimo: extents too large");
+    LRX_REQUIRE(S == 1 || (w && wb >= ws_ps_bytes<T>(B, L, P)), LRX_ERR_VALUE, "mimo workspace too small");
+    cplx<T>* aggA = static_cast<cplx<T>*>(w);
+    cplx<T>* aggX = S > 1 ? aggA + S * B * P : nullptr;
+    int n = 1;
+    if (S > 1) {
+        fwd_ps_kernel<T, true><<<dim3((unsigned)nb, (unsigned)(S - 1)), kThreads, 0, st>>>(
+            (const cplx<T>*)lam, (const T*)delta, (const T*)deltas, scheme, (const cplx<T>*)bu, aggA, aggX, nullptr,
+            B, L, P, seg);
+        ++n;
+    }
+    fwd_ps_kernel<T, false><<<dim3((unsigned)nb, (unsigned)S), kThreads, 0, st>>>(
+        (const cplx<T>*)lam, (const T*)delta, (const T*)deltas, scheme, (const cplx<T>*)bu, aggA, aggX, (cplx<T>*)x,
+        B, L, P, seg);
+    return launched("lrx_mimo_fwd_ps", n);
+}
+
+template <typename T>
+static int bwd_ps_t(const void* lam, const void* delta, const void* deltas, int scheme, const void* bu, const void* x,
+                    const void* gx, void* gbu, void* glp, void* gdp, int64_t B, int64_t L, int64_t P, void* w,
+                    size_t wb, cudaStream_t st) {
+    const int seg = seg_len(B, L, P);
+    const int64_t S = cdiv(L, (int64_t)seg), nb = cdiv(B * P, kThreads);
+    LRX_REQUIRE(S <= 65535 && nb <= 0x7fffffff, LRX_ERR_UNSUPPORTED, "mimo: extents too large");
+    LRX_REQUIRE(S == 1 || (w && wb >= ws_ps_bytes<T>(B, L, P)), LRX_ERR_VALUE, "mimo workspace too small");
+    cplx<T>* aggA = static_cast<cplx<T>*>(w);
+    cplx<T>* aggH = S > 1 ? aggA + S * B * P : nullptr;
+    int n = 1;
+    if (S > 1) {
+        bwd_ps_kernel<T, true><<<dim3((unsigned)nb, (unsigned)(S - 1)), kThreads, 0, st>>>(
+            (const cplx<T>*)lam, (const T*)delta, (const T*)deltas, scheme, (const cplx<T>*)bu, (const cplx<T>*)x,
+            (const cplx<T>*)gx, aggA, aggH, nullptr, nullptr, nullptr, B, L, P, (int)S, seg);
+        ++n;
+    }
+    bwd_ps_kernel<T, false><<<dim3((unsigned)nb, (unsigned)S), kThreads, 0, st>>>(
+        (const cplx<T>*)lam, (const T*)delta, (const T*)deltas, scheme, (const cplx<T>*)bu, (const cplx<T>*)x,
+        (const cplx<T>*)gx, aggA, aggH, (cplx<T>*)gbu, (cplx<T>*)glp, (T*)gdp, B, L, P, (int)S, seg);
+    return launched("lrx_mimo_bwd_ps", n);
 }
 
 }  // namespace mimo
@@ -324,6 +479,40 @@ int lrx_mimo_bwd(int dtype, const void* abar, const void* scale, const void* bu,
     if (dtype == LRX_C128)
         return mimo::bwd_t<double>(abar, scale, bu, x, gx, gbu, gabar_part, gscale_part, B, L, P, workspace,
                                    workspace_bytes, st);
+    set_error("mimo: dtype must be C64 or C128, got %d", dtype);
+    return LRX_ERR_VALUE;
+}
+
+size_t lrx_mimo_ps_workspace_bytes(int dtype, int64_t B, int64_t L, int64_t P) {
+    if (B < 1 || L < 1 || P < 1) return 256;
+    return dtype == LRX_C128 ? mimo::ws_ps_bytes<double>(B, L, P) : mimo::ws_ps_bytes<float>(B, L, P);
+}
+
+int lrx_mimo_fwd_ps(int dtype, const void* lam, const void* delta, const void* deltas, int scheme, const void* bu,
+                    void* x, int64_t B, int64_t L, int64_t P, void* workspace, size_t workspace_bytes, void* stream) {
+    LRX_REQUIRE(B >= 1 && L >= 1 && P >= 1, LRX_ERR_SHAPE, "bad extents");
+    LRX_REQUIRE(scheme >= 0 && scheme <= 2, LRX_ERR_VALUE, "mimo: scheme %d", scheme);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == LRX_C64)
+        return mimo::fwd_ps_t<float>(lam, delta, deltas, scheme, bu, x, B, L, P, workspace, workspace_bytes, st);
+    if (dtype == LRX_C128)
+        return mimo::fwd_ps_t<double>(lam, delta, deltas, scheme, bu, x, B, L, P, workspace, workspace_bytes, st);
+    set_error("mimo: dtype must be C64 or C128, got %d", dtype);
+    return LRX_ERR_VALUE;
+}
+
+int lrx_mimo_bwd_ps(int dtype, const void* lam, const void* delta, const void* deltas, int scheme, const void* bu,
+                    const void* x, const void* gx, void* gbu, void* glam_part, void* gdl_part, int64_t B, int64_t L,
+                    int64_t P, void* workspace, size_t workspace_bytes, void* stream) {
+    LRX_REQUIRE(B >= 1 && L >= 1 && P >= 1, LRX_ERR_SHAPE, "bad extents");
+    LRX_REQUIRE(scheme >= 0 && scheme <= 2, LRX_ERR_VALUE, "mimo: scheme %d", scheme);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == LRX_C64)
+        return mimo::bwd_ps_t<float>(lam, delta, deltas, scheme, bu, x, gx, gbu, glam_part, gdl_part, B, L, P,
+                                     workspace, workspace_bytes, st);
+    if (dtype == LRX_C128)
+        return mimo::bwd_ps_t<double>(lam, delta, deltas, scheme, bu, x, gx, gbu, glam_part, gdl_part, B, L, P,
+                                      workspace, workspace_bytes, st);
     set_error("mimo: dtype must be C64 or C128, got %d", dtype);
     return LRX_ERR_VALUE;
 }

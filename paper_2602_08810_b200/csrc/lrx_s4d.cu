@@ -90,69 +90,6 @@ template <int G> struct Out {
 };
 
 
-// ---------------------------------------------------------------- per-step discretisation
-template <typename T> __device__ __forceinline__ T small_pole_eps();
-template <> __device__ __forceinline__ float small_pole_eps<float>() { return 1e-4f; }   // discretize.py:39-42
-template <> __device__ __forceinline__ double small_pole_eps<double>() { return 1e-8; }
-__device__ __forceinline__ void sc_(float x, float* s, float* c) { sincosf(x, s, c); }
-__device__ __forceinline__ void sc_(double x, double* s, double* c) { sincos(x, s, c); }
-__device__ __forceinline__ float ex_(float x) { return expf(x); }
-__device__ __forceinline__ double ex_(double x) { return exp(x); }
-
-template <typename T>
-__device__ __forceinline__ cplx<T> cdiv_(cplx<T> a, cplx<T> b) {
-    const T den = b.re * b.re + b.im * b.im;
-    return {(a.re * b.re + a.im * b.im) / den, (a.im * b.re - a.re * b.im) / den};
-}
-
-enum { ZOH = 0, BILINEAR = 1, DIRAC = 2 };
-
-// (abar, scale) of one step dt for pole lam (discretize.py:59-93)
-template <typename T>
-__device__ __forceinline__ void disc(int scheme, cplx<T> lam, T dt, cplx<T>& ab, cplx<T>& sc) {
-    const cplx<T> z = dt * lam;
-    if (scheme == BILINEAR) {
-        const cplx<T> den = {T(1) - T(0.5) * z.re, -T(0.5) * z.im};
-        ab = cdiv_(cplx<T>{T(1) + T(0.5) * z.re, T(0.5) * z.im}, den);
-        sc = cdiv_(cplx<T>{dt, T(0)}, den);
-        return;
-    }
-    T sn, cs;
-    sc_(z.im, &sn, &cs);
-    const T e = ex_(z.re);
-    ab = {e * cs, e * sn};
-    if (scheme == DIRAC) sc = {T(1), T(0)};
-    else if (sqrt(lam.re * lam.re + lam.im * lam.im) < small_pole_eps<T>()) sc = {dt, T(0)};
-    else sc = cdiv_(ab - cplx<T>{T(1), T(0)}, lam);
-}
-
-// partials d abar / d lam, d abar / d dt, d scale / d lam, d scale / d dt
-// (autograd.py:186-211 scheme_partials)
-template <typename T>
-__device__ __forceinline__ void disc_partials(int scheme, cplx<T> lam, T dt, cplx<T> ab, cplx<T>& dal, cplx<T>& dad,
-                                              cplx<T>& dsl, cplx<T>& dsd) {
-    if (scheme == BILINEAR) {
-        const cplx<T> den = {T(1) - T(0.5) * dt * lam.re, -T(0.5) * dt * lam.im};
-        const cplx<T> inv2 = cdiv_(cplx<T>{T(1), T(0)}, den * den);
-        dal = dt * inv2;
-        dad = lam * inv2;
-        dsl = (T(0.5) * dt * dt) * inv2;
-        dsd = inv2;
-        return;
-    }
-    dal = dt * ab;
-    dad = lam * ab;
-    if (scheme == DIRAC) {
-        dsl = dsd = cplx<T>{T(0), T(0)};
-    } else if (sqrt(lam.re * lam.re + lam.im * lam.im) < small_pole_eps<T>()) {
-        dsl = {T(0.5) * dt * dt, T(0)};
-        dsd = {T(1), T(0)};
-    } else {
-        dsl = cdiv_(dt * (ab * lam) - (ab - cplx<T>{T(1), T(0)}), lam * lam);
-        dsd = ab;
-    }
-}
-
 // Coefficients of the lane's NPL states: constant (abar, w arrays) or per step.
 template <typename T, int NPL, bool PS>
 struct Coefs {

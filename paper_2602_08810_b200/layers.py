@@ -663,12 +663,11 @@ class _MIMOBase(LinearRecurrence):
             bu = torch.view_as_complex(ops.gemm_f32(u2.contiguous(), self._wb().T.contiguous()).reshape(B, L, P, 2))
         else:
             bu = torch.view_as_complex((u2 @ self._wb()).reshape(B, L, P, 2))   # [B,L,P]
-        abar, scale, extra = self._abar_scale(deltas)
         if deltas is None:
+            abar, scale, extra = self._abar_scale(deltas)
             x = ops.mimo_scan_fwd(abar, scale, bu)
-        else:
-            x2 = run_fwd(_tm(abar), True, _tm(scale * bu), None)
-            x = x2.reshape(L, B, P).transpose(0, 1).contiguous()
+        else:  # per-step discretisation inside the scan kernel (no [B, L, P] coefficient planes)
+            x = ops.mimo_scan_fwd_ps(*self._ps_args(deltas), bu)
         if self._tc(2 * P, B * L):  # y = OUT Re(C x) + D u, the D u skip fused into the GEMM epilogue
             y = ops.gemm_f32(torch.view_as_real(x).reshape(B * L, 2 * P), self._wc().T.contiguous(),
                              Cin=u2.contiguous(), colscale=self.D.contiguous(),
@@ -751,15 +750,14 @@ class _MIMOBase(LinearRecurrence):
             _lib.ptr(y), float(self.OUT_SCALE), st.batch, self._P, self.d_model, _lib.stream()))
         return y
 
+    def _ps_args(self, deltas):
+        """(lam [P], delta [P], deltas [B, L], scheme) for the per-step kernels."""
+        lam = torch.complex(-torch.exp(self.lambda_re_log), self.lambda_im).to(self.tcdt).contiguous()
+        return lam, torch.exp(self.log_delta).contiguous(), deltas.to(self.tdt).contiguous(), self.discretization
+
     def _scan_backward(self, x, bu, gx, abar, scale, deltas):
-        """(gbu [B,L,P], gabar or ga_k, gscale or gscale_k)."""
-        B, L, P = x.shape
-        if deltas is None:
-            return ops.mimo_scan_bwd(abar, scale, bu, x, gx)
-        g2, ga, _ = pullback(_tm(abar), True, _tm(x), None, _tm(gx))
-        gv = g2.reshape(L, B, P).transpose(0, 1)
-        ga_k = ga.reshape(L, B, P).transpose(0, 1)
-        return scale.conj() * gv, ga_k, bu.conj() * gv
+        """(gbu [B,L,P], gabar, gscale) of the constant-step scan."""
+        return ops.mimo_scan_bwd(abar, scale, bu, x, gx)
 
     def _backward(self, s, gy):
         if "pk" in s:
@@ -780,15 +778,21 @@ class _MIMOBase(LinearRecurrence):
             gx = torch.view_as_complex(ops.gemm_f32(gy2.contiguous(), wg.T.contiguous(), alpha=osc).reshape(B, L, P, 2))
         else:
             gx = torch.view_as_complex((osc * (gy2 @ wg)).reshape(B, L, P, 2)).contiguous()
-        abar, scale, extra = self._abar_scale(deltas)
-        gbu, ga, gsc = self._scan_backward(x, bu, gx, abar, scale, deltas)
+        if deltas is None:
+            abar, scale, extra = self._abar_scale(deltas)
+            gbu, ga, gsc = self._scan_backward(x, bu, gx, abar, scale, deltas)
+            coef = {k: v.to(self.tdt) for k, v in self._coef_grads(ga, gsc, extra, deltas).items()}
+        else:  # the kernel accumulates the per-step scheme partials (autograd.py:186-211)
+            gbu, glam, glog_delta = ops.mimo_scan_bwd_ps(*self._ps_args(deltas), bu, x, gx.contiguous())
+            coef = {"lambda_re_log": (-torch.exp(self.lambda_re_log) * glam.real).to(self.tdt),
+                    "lambda_im": glam.imag.to(self.tdt).contiguous(), "log_delta": glog_delta.to(self.tdt)}
         gbu2 = torch.view_as_real(gbu.contiguous()).reshape(B * L, 2 * P)
         R2 = ops.gemm_f32_tn(gbu2, u2.contiguous()) if tn else gbu2.T @ u2  # [2P, m]
         if self._tc(2 * P, B * L):  # gu = D gy + Re(g conj(B)), the skip fused into the epilogue
             gu = ops.gemm_f32(gbu2, self._wb(), Cin=gy2.contiguous(), colscale=self.D.contiguous()).reshape(B, L, m)
         else:
             gu = gy * self.D + (gbu2 @ self._wb().T).reshape(B, L, m)
-        grads = {k: v.to(self.tdt) for k, v in self._coef_grads(ga, gsc, extra, deltas).items()}
+        grads = coef
         grads.update({"B.re": R2[0::2].contiguous(), "B.im": R2[1::2].contiguous(),
                       "C.re": gC_re.contiguous(), "C.im": gC_im.contiguous(), "D": gD})
         return self._out({k: grads[k] for k in self.parameters()}, gu, host)

@@ -85,6 +85,7 @@ def rglru_scan_bwd(u, qr, qi, lambda_param, b_r, b_i, ckpt, gy, y=None):
 # S6
 
 S6_REUSE_AGG = 1
+SCHEME_CODE = {"zoh": 0, "bilinear": 1, "dirac": 2}
 
 
 def s6_geometry(io_dtype, B, L, D, N):
@@ -339,13 +340,41 @@ def mimo_scan_bwd(abar, scale, bu, x, gx):
     return gbu, reduce_rows(gap, nc * B, P), reduce_rows(gsp, nc * B, P)
 
 
+def mimo_scan_fwd_ps(lam, delta, deltas, scheme, bu):
+    """Per-step (asynchronous) MIMO scan: x_k = abar_k x_{k-1} + scale_k bu_k with
+    the discretisation of lam [P] at deltas[b, k] * delta[p] done in the kernel."""
+    B, L, P = bu.shape
+    x = torch.empty_like(bu)
+    lib = _lib.lib()
+    code = _lib.code_of(bu.dtype)
+    ws = _lib.workspace(lib.lrx_mimo_ps_workspace_bytes(code, B, L, P), bu.device)
+    _lib.check(lib.lrx_mimo_fwd_ps(code, _lib.ptr(lam), _lib.ptr(delta), _lib.ptr(deltas), SCHEME_CODE[scheme],
+                                   _lib.ptr(bu), _lib.ptr(x), B, L, P, _lib.ptr(ws), ws.numel(), _lib.stream()))
+    return x
+
+
+def mimo_scan_bwd_ps(lam, delta, deltas, scheme, bu, x, gx):
+    """Pullback of mimo_scan_fwd_ps: (gbu [B, L, P], glam [P] complex, glog_delta [P])."""
+    B, L, P = x.shape
+    lib = _lib.lib()
+    code = _lib.code_of(x.dtype)
+    ck, nc = _lib.i64(), _lib.i64()
+    _lib.check(lib.lrx_mimo_chunking(code, B, L, P, _lib.ref(ck), _lib.ref(nc)))
+    R = nc.value * B
+    gbu = torch.empty_like(x)
+    glp = torch.empty((R, P), dtype=x.dtype, device=x.device)
+    gdp = torch.empty((R, P), dtype=delta.dtype, device=x.device)
+    ws = _lib.workspace(lib.lrx_mimo_ps_workspace_bytes(code, B, L, P), x.device)
+    _lib.check(lib.lrx_mimo_bwd_ps(code, _lib.ptr(lam), _lib.ptr(delta), _lib.ptr(deltas), SCHEME_CODE[scheme],
+                                   _lib.ptr(bu), _lib.ptr(x), _lib.ptr(gx), _lib.ptr(gbu), _lib.ptr(glp), _lib.ptr(gdp),
+                                   B, L, P, _lib.ptr(ws), ws.numel(), _lib.stream()))
+    return gbu, reduce_rows(glp, R, P), reduce_rows(gdp, R, P) * delta
+
+
 # ---------------------------------------------------------------------------
 # S4D (fused per-channel complex LTI scan)
 
 S4D_FUSED_N = (8, 16, 32, 64)
-
-
-SCHEME_CODE = {"zoh": 0, "bilinear": 1, "dirac": 2}
 
 
 def s4d_geometry(dtype, B, L, H, N):

@@ -581,6 +581,32 @@ def test_s4d_async_fused_matches_oracle(lrx, n, scheme, dtype):
         assert rel(g.params[k], rg[k]) < tol, (k, rel(g.params[k], rg[k]))
 
 
+@pytest.mark.parametrize("seg", ["16", "auto"])
+@pytest.mark.parametrize("scheme", ["zoh", "bilinear", "dirac"])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_s5_async_fused_matches_oracle(lrx, monkeypatch, seg, scheme, dtype):
+    """Asynchronous S5 (per-step deltas, layers.py:650-658): the MIMO scan
+    discretises every step in the kernel and accumulates the coefficient
+    gradients through the scheme partials -- against the oracle, every
+    parameter gradient, with forced short segments too."""
+    if seg != "auto":
+        monkeypatch.setenv("LRX_MIMO_SEG", seg)
+    m, B, L = 8, 3, 157
+    layer = lrx.make_layer("s5", m, 12, scheme, asynchronous=True, dtype=dtype, seed=72)
+    u = port.Rng(73).normal((B, L, m)).astype(layer.rdt)
+    gy = port.Rng(74).normal((B, L, m)).astype(layer.rdt)
+    deltas = port.Rng(75).uniform(0.05, 3.0, (B, L)).astype(layer.rdt)
+    y, tape = layer.forward(u, deltas=deltas, tape=True)
+    g = lrx.layer_backward(layer, tape, gy)
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64("s5", scheme, params, u, gy, deltas=deltas, asyn=True)
+    tol = TOL[dtype]
+    assert rel(y, ry) < tol
+    assert rel(g.u, rgu) < tol
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < tol, (k, rel(g.params[k], rg[k]))
+
+
 @pytest.mark.parametrize("segs", ["1", "3", "auto"])
 @pytest.mark.parametrize("asyn", [False, True])
 def test_s4d_time_segments_match_oracle(lrx, monkeypatch, segs, asyn):
