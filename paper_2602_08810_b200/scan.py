@@ -2,11 +2,14 @@
 
 x_k = a_k * x_{k-1} + b_k over time-major arrays b [L, *lanes] with a either
 [*lanes] (constant) or [L, *lanes] (per-step).  Both entry points run the same
-single-pass sm_100a kernel (lrx_scan_fwd): lanes across threads, time chunks
-across CTAs chained by a decoupled look-back.  `workers` is accepted for API
-compatibility and ignored — the chunking is the GPU's, so unlike the
-reference (scan.py:160-162) `scan_parallel` is bitwise identical to
-`scan_sequential` for every `workers` value.
+sm_100a operator (lrx_scan_fwd): by default a streaming walk -- one thread per
+lane over its time segment, 8-step register tiles, and (when the lanes alone
+cannot fill the GPU) time segments reduced by an aggregate pass and folded in
+a fixed order; the single-pass anchored decoupled look-back remains behind
+LRX_SCAN_STREAM=0.  `workers` is accepted for API compatibility and ignored --
+the chunking is the GPU's, so unlike the reference (scan.py:160-162)
+`scan_parallel` is bitwise identical to `scan_sequential` for every `workers`
+value.
 
 Inputs may be numpy arrays (copied to the current CUDA device; numpy is
 returned) or CUDA tensors (results stay on the device).
