@@ -689,6 +689,10 @@ def main():
     if one_gpu:
         local = 0
     if world > 1:
+        # NCCL's init log states the communicator's rank count and transport
+        # (NVLink / NVLS) on stderr, so the scaling run can be checked
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         if one_gpu:
             dist.init_process_group("gloo")
