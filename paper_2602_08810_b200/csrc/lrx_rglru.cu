@@ -616,7 +616,7 @@ __device__ __forceinline__ Coef2 gates2(float2 u, float2 qr, float2 qi, float2 l
 }
 
 template <typename IO, int LW, int PF>
-__global__ void __launch_bounds__(LW / 2, PF == 4 ? 1152 / LW : 512 / LW) bwd_rev2_kernel(
+__global__ void __launch_bounds__(LW / 2, PF <= 4 ? 1152 / LW : 512 / LW) bwd_rev2_kernel(
     const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mr,
     const __grid_constant__ CUtensorMap mi, const __grid_constant__ CUtensorMap mg, const float* __restrict__ lam,
     const float* __restrict__ b_r, const float* __restrict__ b_i, const float* __restrict__ ckpt, IO* __restrict__ gu,
@@ -774,7 +774,7 @@ __global__ void __launch_bounds__(LW / 2, PF == 4 ? 1152 / LW : 512 / LW) bwd_re
 
 // Lane-pair forward (fp32 compute, LW >= 64): fwd_tma_kernel on packed fp32x2.
 template <typename IO, int LW, int PF, bool AGG>
-__global__ void __launch_bounds__(LW / 2, PF == 4 ? 1152 / LW : 512 / LW) fwd2_kernel(
+__global__ void __launch_bounds__(LW / 2, PF <= 4 ? 1152 / LW : 512 / LW) fwd2_kernel(
     const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mr,
     const __grid_constant__ CUtensorMap mi, const float* __restrict__ lam, const float* __restrict__ b_r,
     const float* __restrict__ b_i, IO* __restrict__ y, float* __restrict__ ckpt, float* __restrict__ seg_a,
@@ -1356,7 +1356,14 @@ static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p) {
     if (const char* e = getenv("LRX_RGLRU_LW")) LW = atoi(e) == 32 ? 32 : atoi(e) == 64 ? 64 : 128;
     const int n_wblk = (int)cdiv(W, LW);
     const int64_t n_blk = B * n_wblk;
-    const int smax = env_int("LRX_RGLRU_STAGES", 6);
+    // per-direction overrides (narr 3 = forward, 4 = backward) before the shared ones
+    const char* dir = narr == 3 ? "LRX_RGLRU_FWD_STAGES" : "LRX_RGLRU_BWD_STAGES";
+    const double warps = (double)n_blk * (LW / 32) / sms;  // one lane per thread (the lane-pair kernels run half)
+    // fp32 lane-pair walks with a full GPU of lanes (C4: ~35): short tiles in a
+    // 2-stage ring stream best (measured C4 fwd 7.9 -> 7.0 ms, bwd 14.1 -> 13.3);
+    // half as many lanes (~17) still prefer the short tile with the deep ring
+    const bool pair32 = sizeof(IO) == 4 && LW >= 64 && !getenv("LRX_RGLRU_SCALAR");
+    const int smax = env_int(dir, env_int("LRX_RGLRU_STAGES", pair32 && warps >= 24 ? 2 : 6));
     // ring depth that fits for (PF, n_seg); 0 = does not fit
     auto stages = [&](int PF, int64_t n_seg) -> int {
         const int64_t per_sm = cdiv(n_blk * n_seg, (int64_t)sms);
@@ -1367,7 +1374,6 @@ static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p) {
         if (budget < 256 + 2 * stage) return 0;
         return (int)std::min<size_t>((size_t)smax, (budget - 256) / stage);
     };
-    const double warps = (double)n_blk * (LW / 32) / sms;
     const int64_t max_seg = std::max<int64_t>(1, std::min<int64_t>(64, L / 256));
     // segments only below ~6 resident warps per SM (measured: the AGG pass
     // costs more than it buys above that); aim for ~12.
@@ -1384,7 +1390,10 @@ static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p) {
         if (PF) break;
     }
     if (!PF) return false;
-    if (const char* e = getenv("LRX_RGLRU_PF")) PF = std::min(MaxPF<IO>::T, atoi(e) >= 16 ? 16 : atoi(e) >= 8 ? 8 : 4);
+    if (pair32 && warps >= 12 && n_seg == 1) PF = 2;
+    const char* epf = getenv(narr == 3 ? "LRX_RGLRU_FWD_PF" : "LRX_RGLRU_BWD_PF");
+    if (!epf) epf = getenv("LRX_RGLRU_PF");
+    if (epf) PF = std::min(MaxPF<IO>::T, atoi(epf) >= 16 ? 16 : atoi(epf) >= 8 ? 8 : atoi(epf) >= 4 ? 4 : 2);
     if (const char* e = getenv("LRX_RGLRU_SEGS"))
         n_seg = std::max<int64_t>(1, std::min<int64_t>({(int64_t)atoi(e), 64, std::max<int64_t>(1, L / 64)}));
     // segments start on a tile and on a checkpoint boundary
@@ -1392,7 +1401,7 @@ static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p) {
     const int64_t len = cdiv(cdiv(L, n_seg), kAlign) * kAlign;
     p->seg_len = (int)std::min<int64_t>(len, 1ll << 30);
     p->n_seg = (int)cdiv(L, len);
-    while (!(p->S = stages(PF, p->n_seg)) && PF > 4) PF /= 2;  // overrides that do not fit
+    while (!(p->S = stages(PF, p->n_seg)) && PF > 2) PF /= 2;  // overrides that do not fit
     if (!p->S) return false;
     p->LW = LW;
     p->PF = PF;
@@ -1512,6 +1521,7 @@ static int rev_pf(const TmaPlan& pl, const TmaPlan& pa, const CUtensorMap* m, co
         if (!getenv("LRX_RGLRU_SCALAR")) switch (pl.PF) {
             case 16: return launch_bwd_rev2<IO, LW, 16>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st);
             case 8: return launch_bwd_rev2<IO, LW, 8>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st);
+            case 2: return launch_bwd_rev2<IO, LW, 2>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st);
             default: return launch_bwd_rev2<IO, LW, 4>(pl, pa, m, lam, br, bi, ckpt, gu, gqr, gqi, parts, seg, B, L, W, st);
         }
     }
@@ -1584,6 +1594,7 @@ static int fwd_pf(const TmaPlan& pl, const CUtensorMap* m, const void* lam, cons
         if (!getenv("LRX_RGLRU_SCALAR")) switch (pl.PF) {
             case 16: return launch_fwd2<IO, LW, 16>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
             case 8: return launch_fwd2<IO, LW, 8>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
+            case 2: return launch_fwd2<IO, LW, 2>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
             default: return launch_fwd2<IO, LW, 4>(pl, m, lam, br, bi, y, ckpt, seg, B, L, W, st);
         }
     }
