@@ -305,16 +305,17 @@ int lrx_gemm_f32_tn(const void* A, const void* B, void* part, int64_t M, int64_t
  * _projections layers.py:1020-1027: B_k, C_k, the low-rank delta input;
  * RG-LRU _gates layers.py:1212-1218):
  *   C[M,N] = act(alpha A[M,K] Bt[N,K]^T + bias[n]) + beta Cin[M,N]
- * A, Bt bf16 row-major K-contiguous; C, Cin fp32 (Cin / bias may be NULL);
+ * A, Bt bf16 row-major K-contiguous; C fp32 (or bf16 with out_bf16, then no
+ * Cin), Cin fp32 (Cin / bias may be NULL);
  * act: 0 identity, 1 softplus (numerics.py:36-39), 2 sigmoid (:97-105).
- * K % 8 == 0, N % 4 == 0, 16-byte aligned rows.  Replaces the numpy matmuls
+ * K % 8 == 0, N % 4 == 0 (N % 8 == 0 for bf16 out), 16-byte aligned rows.  Replaces the numpy matmuls
  * of those reference lines (cuBLAS in round 1).
  * ------------------------------------------------------------------------ */
 #define LRX_ACT_NONE 0
 #define LRX_ACT_SOFTPLUS 1
 #define LRX_ACT_SIGMOID 2
 int lrx_gemm_bf16(const void* A, const void* Bt, void* C, const void* Cin, const void* bias, int64_t M, int64_t N,
-                  int64_t K, float alpha, float beta, int act, void* stream);
+                  int64_t K, float alpha, float beta, int act, int out_bf16, void* stream);
 
 /* ------------------------------------------------------------------------ *
  * MIMO complex diagonal scan for S5 / LRU (layers.py:616-980): the recurrence

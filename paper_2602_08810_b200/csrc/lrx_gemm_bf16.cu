@@ -89,7 +89,7 @@ struct Lay {
     static constexpr size_t smem() { return 2048 + (size_t)STAGES * STAGE + EPI; }
 };
 
-template <int BN>
+template <int BN, bool OB>  // OB: bf16 output (no Cin)
 __global__ void __launch_bounds__(THREADS, 1) gemm_bf16_kernel(
     const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
     const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mCin, const float* Cin,
@@ -226,6 +226,27 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_bf16_kernel(
                     tma::mbar_arrive(&tempty[acc]);
                 }
                 if (Cin) tma::mbar_wait(cb, (cph++) & 1);
+                if constexpr (OB) {  // bf16 row of CW values: 64-byte rows, 64B swizzle (CW = 32)
+                    unsigned char* rb = reinterpret_cast<unsigned char*>(buf) + lane * CW * 2;
+#pragma unroll
+                    for (int g = 0; g < CW / 8; ++g) {
+                        const int col = n0 + c0 + 8 * g;
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            float x0 = alpha * __uint_as_float(r[8 * g + 2 * e]);
+                            float x1 = alpha * __uint_as_float(r[8 * g + 2 * e + 1]);
+                            if (bias) {
+                                x0 += __ldg(bias + min(col + 2 * e, N - 1));
+                                x1 += __ldg(bias + min(col + 2 * e + 1, N - 1));
+                            }
+                            const __nv_bfloat162 h2 = __floats2bfloat162_rn(act(x0, act_kind), act(x1, act_kind));
+                            pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
+                        }
+                        const int chunk = CW == 32 ? (g ^ ((lane >> 1) & 3)) : g;
+                        *reinterpret_cast<uint4*>(rb + 16 * chunk) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    }
+                } else {
                 float* rowp = buf + lane * CW;  // this lane's row: CW / 4 16-byte chunks (swizzled at CW = 32)
 #pragma unroll
                 for (int g = 0; g < CW / 4; ++g) {
@@ -246,6 +267,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_bf16_kernel(
                         v[3] += beta * c.w;
                     }
                     *p4 = make_float4(v[0], v[1], v[2], v[3]);
+                }
                 }
                 tma::fence_proxy_async();  // generic smem writes -> the TMA store's reads
                 __syncwarp();
@@ -302,6 +324,19 @@ static bool enc_out(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// bf16 C boxes: 32 rows x cw bf16 (64-byte rows, 64B swizzle at cw = 32)
+static bool enc_out16(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols, uint32_t cw) {
+    auto fn = enc_fn();
+    if (!fn || (reinterpret_cast<uintptr_t>(p) & 15) || ((cols * 2) & 15)) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {cw, 32};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, cw == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int sm_count() {
     static int sms = 0;
     if (!sms) {
@@ -314,18 +349,19 @@ static int sm_count() {
 }
 
 template <int BN>
-static int launch(const void* A, const void* Bt, float* C, const float* Cin, const float* bias, int64_t M, int64_t N,
-                  int64_t K, float alpha, float beta, int act_kind, cudaStream_t st) {
+static int launch(const void* A, const void* Bt, void* C, const float* Cin, const float* bias, int64_t M, int64_t N,
+                  int64_t K, float alpha, float beta, int act_kind, bool out_bf16, cudaStream_t st) {
     CUtensorMap mA, mB, mC, mCin;
     constexpr uint32_t cw = BN < 32 ? BN : 32;
-    if (!enc_bf16(&mA, A, M, K, BM) || !enc_bf16(&mB, Bt, N, K, BN) || !enc_out(&mC, C, M, N, cw) ||
+    const bool oc = out_bf16 ? enc_out16(&mC, C, M, N, cw) : enc_out(&mC, C, M, N, cw);
+    if (!enc_bf16(&mA, A, M, K, BM) || !enc_bf16(&mB, Bt, N, K, BN) || !oc ||
         (Cin && !enc_out(&mCin, Cin, M, N, cw))) {
         set_error("gemm_bf16: TMA descriptor rejected (K %% 8 == 0, N %% 4 == 0 and 16-byte aligned rows required)");
         return LRX_ERR_VALUE;
     }
     if (!Cin) mCin = mC;
     const size_t smem = Lay<BN>::smem();
-    auto k = gemm_bf16_kernel<BN>;
+    auto k = out_bf16 ? gemm_bf16_kernel<BN, true> : gemm_bf16_kernel<BN, false>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         set_error("gemm_bf16: cannot reserve %zu B of shared memory", smem);
         return LRX_ERR_CUDA;
@@ -333,7 +369,7 @@ static int launch(const void* A, const void* Bt, float* C, const float* Cin, con
     const int64_t tiles = cdiv(M, BM) * cdiv(N, BN);
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, sm_count());
     k<<<grid, THREADS, smem, st>>>(mA, mB, mC, mCin, Cin, bias, (int)M, (int)N, (int)K, alpha, beta, act_kind);
-    return launched("lrx_gemm_bf16/tcgen05");
+    return launched(out_bf16 ? "lrx_gemm_bf16/tcgen05 (bf16 out)" : "lrx_gemm_bf16/tcgen05");
 }
 
 }  // namespace gemm16
@@ -344,22 +380,24 @@ using namespace lrx;
 extern "C" {
 
 int lrx_gemm_bf16(const void* A, const void* Bt, void* C, const void* Cin, const void* bias, int64_t M, int64_t N,
-                  int64_t K, float alpha, float beta, int act, void* stream) {
+                  int64_t K, float alpha, float beta, int act, int out_bf16, void* stream) {
     LRX_REQUIRE(M >= 1 && N >= 1 && K >= 1, LRX_ERR_SHAPE, "gemm_bf16: bad extents M=%lld N=%lld K=%lld",
                 (long long)M, (long long)N, (long long)K);
     LRX_REQUIRE(act >= 0 && act <= 2, LRX_ERR_VALUE, "gemm_bf16: unknown activation %d", act);
+    LRX_REQUIRE(!(out_bf16 && Cin), LRX_ERR_VALUE, "gemm_bf16: Cin needs the fp32 output");
     // the whole K is accumulated in TMEM (not round-to-nearest; the bf16
     // operands' own rounding dominates), N is tiled by 32-column boxes
     LRX_REQUIRE(M < (1ll << 31) && N <= (1 << 16) && N % 4 == 0 && K <= 16384, LRX_ERR_UNSUPPORTED,
                 "gemm_bf16: extents unsupported (N %% 4 == 0, K <= 16384)");
     cudaStream_t st = (cudaStream_t)stream;
-    float* c = (float*)C;
+    void* c = C;
+    const bool ob = out_bf16 != 0;
     const float *cin = (const float*)Cin, *b = (const float*)bias;
-    if (N <= 16) return gemm16::launch<16>(A, Bt, c, cin, b, M, N, K, alpha, beta, act, st);
-    if (N <= 32) return gemm16::launch<32>(A, Bt, c, cin, b, M, N, K, alpha, beta, act, st);
-    if (N <= 64) return gemm16::launch<64>(A, Bt, c, cin, b, M, N, K, alpha, beta, act, st);
-    if (N <= 128) return gemm16::launch<128>(A, Bt, c, cin, b, M, N, K, alpha, beta, act, st);
-    return gemm16::launch<256>(A, Bt, c, cin, b, M, N, K, alpha, beta, act, st);
+    if (N <= 16) return gemm16::launch<16>(A, Bt, c, cin, b, M, N, K, alpha, beta, act, ob, st);
+    if (N <= 32) return gemm16::launch<32>(A, Bt, c, cin, b, M, N, K, alpha, beta, act, ob, st);
+    if (N <= 64) return gemm16::launch<64>(A, Bt, c, cin, b, M, N, K, alpha, beta, act, ob, st);
+    if (N <= 128) return gemm16::launch<128>(A, Bt, c, cin, b, M, N, K, alpha, beta, act, ob, st);
+    return gemm16::launch<256>(A, Bt, c, cin, b, M, N, K, alpha, beta, act, ob, st);
 }
 
 }  // extern "C"

@@ -194,6 +194,17 @@ def _wgrad(g2, a2):
     return g2.T @ a2
 
 
+def _mm_io(a, b):
+    """a @ b in the activation dtype (RG-LRU bf16 gate pre-activations stay
+    bf16: the scan streams them at 2 bytes): the bf16 tcgen05 GEMM with a
+    bf16 epilogue."""
+    if a.dtype == torch.bfloat16 and a.is_cuda:
+        K, N = b.shape
+        if K % 8 == 0 and N % 8 == 0 and K <= 16384:
+            return ops.gemm_bf16(a.contiguous(), b.T.to(torch.bfloat16).contiguous(), out_dtype=torch.bfloat16)
+    return torch.matmul(a, b)
+
+
 def _mm(a, b):
     """Projection GEMM a @ b.  bf16 activations multiply bf16-cast weights on
     the tcgen05 tensor cores (ops.gemm_bf16: fp32 accumulation AND fp32
@@ -1078,8 +1089,8 @@ class RGLRU(LinearRecurrence):
     def _forward(self, u, deltas, keep):
         B, L, W = u.shape
         u2 = u.reshape(B * L, W)
-        qr = _proj(u2, self._w(self.W_r), torch.matmul).reshape(B, L, W)
-        qi = _proj(u2, self._w(self.W_i), torch.matmul).reshape(B, L, W)
+        qr = _proj(u2, self._w(self.W_r), _mm_io).reshape(B, L, W)
+        qi = _proj(u2, self._w(self.W_i), _mm_io).reshape(B, L, W)
         y, ckpt = ops.rglru_scan_fwd(u, qr, qi, self.lambda_param, self.b_r, self.b_i)
         saved = {"u": u, "qr": qr, "qi": qi, "ckpt": ckpt, "y": y} if keep else {}
         return y, saved, y[:, -1].to(self.tdt)

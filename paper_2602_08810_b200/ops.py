@@ -296,14 +296,15 @@ def gemm_f32_tn(A, B, alpha=1.0):
 ACT_NONE, ACT_SOFTPLUS, ACT_SIGMOID = 0, 1, 2
 
 
-def gemm_bf16(A, Bt, bias=None, act=ACT_NONE, Cin=None, alpha=1.0, beta=0.0, out=None):
-    """C = act(alpha A Bt^T + bias) + beta Cin, fp32 out, on the tensor cores.
-    A [M, K], Bt [N, K] bf16 contiguous (K % 8 == 0, N % 4 == 0)."""
+def gemm_bf16(A, Bt, bias=None, act=ACT_NONE, Cin=None, alpha=1.0, beta=0.0, out=None, out_dtype=torch.float32):
+    """C = act(alpha A Bt^T + bias) + beta Cin on the tensor cores, fp32 (or
+    bf16, without Cin) out.  A [M, K], Bt [N, K] bf16 contiguous (K % 8 == 0,
+    N % 4 == 0)."""
     M, K = A.shape
     N = Bt.shape[0]
-    C = out if out is not None else torch.empty((M, N), dtype=torch.float32, device=A.device)
+    C = out if out is not None else torch.empty((M, N), dtype=out_dtype, device=A.device)
     _lib.check(_lib.lib().lrx_gemm_bf16(_lib.ptr(A), _lib.ptr(Bt), _lib.ptr(C), _lib.ptr(Cin), _lib.ptr(bias), M, N,
-                                        K, alpha, beta, act, _lib.stream()))
+                                        K, alpha, beta, act, int(C.dtype == torch.bfloat16), _lib.stream()))
     return C
 
 

@@ -525,6 +525,14 @@ def test_gemm_bf16_tcgen05_matches_fp64(lrx, M, N, K):
     want = torch.sigmoid(ref + bias.double()) - 0.5 * Cin.double()
     assert rel(got, want.cpu().numpy()) < 1e-5
     assert torch.equal(ops.gemm_bf16(A, Bt), ops.gemm_bf16(A, Bt))
+    # bf16 output (RG-LRU gate pre-activations; 16-byte rows: N % 8 == 0): the fp32 result rounded once
+    if N % 8:
+        with pytest.raises(ValueError):
+            ops.gemm_bf16(A, Bt, out_dtype=torch.bfloat16)
+        return
+    got16 = ops.gemm_bf16(A, Bt, bias=bias, act=ops.ACT_SIGMOID, out_dtype=torch.bfloat16)
+    assert got16.dtype == torch.bfloat16
+    assert torch.equal(got16, ops.gemm_bf16(A, Bt, bias=bias, act=ops.ACT_SIGMOID).to(torch.bfloat16))
 
 
 @pytest.mark.parametrize("n", [8, 16, 32, 64])
