@@ -136,6 +136,10 @@ int lrx_rglru_bwd(int io_dtype, const void* u, const void* qr, const void* qi, c
  * the ga/gD/gb partials = n_seg*B), out[5] workspace bytes. */
 int lrx_s6_geometry(int io_dtype, int64_t B, int64_t L, int64_t D, int64_t N, int64_t* out6);
 /* flags for lrx_s6_fwd / lrx_s6_bwd */
+#define LRX_S6_DELTA_IN 2  /* `pre` already holds delta = softplus(pre + b_delta)
+                              (the projection GEMM's epilogue): no softplus in the
+                              scan, sigmoid(pre) = 1 - exp(-delta) in the backward;
+                              b_delta is ignored; gpre stays d loss / d pre */
 #define LRX_S6_REUSE_AGG 1 /* ws already holds the per-segment maps from a
                               preceding lrx_s6_{fwd,bwd}_carry on the same inputs */
 /* x0 [B, D, N] (compute precision, NULL = zeros) seeds the state: the
@@ -284,13 +288,15 @@ int lrx_rglru_step_fused(int io_dtype, void* x, const void* u, const void* W_r, 
 /* ------------------------------------------------------------------------ *
  * fp32 GEMM on the tcgen05 tensor cores with the 3xTF32 split (the dense
  * projections of S5 / LRU, layers.py:650-704):
- *   C[M,N] = alpha A[M,K] Bt[N,K]^T + (colscale ? colscale[n] : beta) Cin[M,N]
+ *   C[M,N] = act(alpha A[M,K] Bt[N,K]^T + bias[n]) + (colscale ? colscale[n] : beta) Cin[M,N]
  * fp32 row-major, K contiguous in both A and Bt; Bt_lo = Bt - tf32(Bt) is the
- * caller's pre-split low part of the (small) right operand.  Cin may be NULL
- * or alias C.  Rows must be 16-byte aligned (K % 4 == 0).
+ * caller's pre-split low part of the (small) right operand.  Cin / bias may
+ * be NULL, Cin may alias C; act 0 identity / 1 softplus / 2 sigmoid (the S6
+ * delta projection's softplus(. + b_delta), layers.py:1020-1027, fused).
+ * Rows must be 16-byte aligned (K % 4 == 0).
  * ------------------------------------------------------------------------ */
 int lrx_gemm_f32(const void* A, const void* Bt, const void* Bt_lo, void* C, const void* Cin, const void* colscale,
-                 int64_t M, int64_t N, int64_t K, float alpha, float beta, void* stream);
+                 const void* bias, int act, int64_t M, int64_t N, int64_t K, float alpha, float beta, void* stream);
 /* Reduction ("TN") GEMM for the weight gradients: with A [K, M] and B [K, N]
  * row-major (K = tokens, long), part[s, M, N] = alpha sum_{k in split s}
  * A[k, m] B[k, n] for s < n_splits; sum the split axis with lrx_reduce_rows.

@@ -63,7 +63,8 @@ SIGNATURES = {
     "lrx_s6_step_fused": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64,
                                _vp]),
     "lrx_rglru_step_fused": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp]),
-    "lrx_gemm_f32": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_float, ctypes.c_float, _vp]),
+    "lrx_gemm_f32": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i64, _i64, _i64, ctypes.c_float, ctypes.c_float,
+                          _vp]),
     "lrx_gemm_f32_tn_splits": (_i, [_i64, _i64, _i64, _P64]),
     "lrx_gemm_f32_tn": (_i, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_float, _vp]),
     "lrx_gemm_bf16": (_i, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_float, ctypes.c_float, _i, _i, _vp]),

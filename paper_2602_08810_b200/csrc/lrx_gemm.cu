@@ -97,6 +97,28 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+// epilogue activation (the projection's nonlinearity fused into the GEMM):
+// 1 softplus (threshold 30, numerics.py:36-39), 2 sigmoid
+__device__ __forceinline__ float epi_act(float x, int a) {
+    // MUFU forms (ex2 / lg2 / rcp, ~2 ulp): softplus keeps its relative
+    // precision for e^x << 1 through the log1p series (as the S6 scan's
+    // softplus); threshold 30 (numerics.py:36-39)
+    if (a == 1) {
+        float e, lg;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fminf(x, 30.f) * 1.4426950408889634f));
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(1.f + e));
+        const float ser = e * (1.f - e * (0.5f - e * (1.f / 3.f)));
+        return x > 30.f ? x : (e < 1e-2f ? ser : lg * 0.6931471805599453f);
+    }
+    if (a == 2) {
+        float e, r;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-x * 1.4426950408889634f));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + e));
+        return r;
+    }
+    return x;
+}
+
 template <int BN, bool TE = false>
 struct Lay {
     static constexpr int A = BM * BKT * 4;  // 8 KB
@@ -130,7 +152,8 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
     const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
     const __grid_constant__ CUtensorMap mBl, const __grid_constant__ CUtensorMap mC,
     const __grid_constant__ CUtensorMap mCin, float* C, const float* Cin,
-    const float* __restrict__ colscale, int M, int N, int K, float alpha, float beta) {
+    const float* __restrict__ colscale, const float* __restrict__ bias, int act_kind, int M, int N, int K, float alpha,
+    float beta) {
     using LY = Lay<BN, TE>;
     constexpr int STAGES = LY::STAGES;
     extern __shared__ unsigned char smem_raw[];
@@ -313,6 +336,17 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
                     v.y = alpha * __uint_as_float(r[4 * g + 1]);
                     v.z = alpha * __uint_as_float(r[4 * g + 2]);
                     v.w = alpha * __uint_as_float(r[4 * g + 3]);
+                    if (bias || act_kind) {
+                        const int col = n0 + c0 + 4 * g;
+                        const float b0 = bias ? __ldg(bias + min(col, N - 1)) : 0.f;
+                        const float b1 = bias ? __ldg(bias + min(col + 1, N - 1)) : 0.f;
+                        const float b2 = bias ? __ldg(bias + min(col + 2, N - 1)) : 0.f;
+                        const float b3 = bias ? __ldg(bias + min(col + 3, N - 1)) : 0.f;
+                        v.x = epi_act(v.x + b0, act_kind);
+                        v.y = epi_act(v.y + b1, act_kind);
+                        v.z = epi_act(v.z + b2, act_kind);
+                        v.w = epi_act(v.w + b3, act_kind);
+                    }
                     if (Cin) {
                         const float4 c = *p4;
                         const int col = n0 + c0 + 4 * g;
@@ -403,6 +437,7 @@ __global__ void __launch_bounds__(THREADS_P, 1) gemm_tf32x3_kernel(
                     const int row = rbase + i;
                     if (row < M && colok) {
                         float v = alpha * tp[i * 33 + lane];
+                        if (bias || act_kind) v = epi_act(v + (bias ? bias[col] : 0.f), act_kind);
                         if (Cin) v += cin[i];
                         __stcs(C + (int64_t)row * N + col, v);
                     }
@@ -628,7 +663,8 @@ static bool enc_epi(CUtensorMap* m, const void* p, uint64_t rows, uint64_t cols)
 
 template <int BN>
 static int launch(const float* A, const float* Bt, const float* Btl, float* C, const float* Cin, const float* cs,
-                  int64_t M, int64_t N, int64_t K, float alpha, float beta, cudaStream_t st) {
+                  const float* bias, int act, int64_t M, int64_t N, int64_t K, float alpha, float beta,
+                  cudaStream_t st) {
     CUtensorMap mA, mB, mBl, mC, mCin;
     if (!enc_k(&mA, A, M, K, BM) || !enc_k(&mB, Bt, N, K, BN) || !enc_k(&mBl, Btl, N, K, BN)) {
         set_error("gemm: TMA descriptor rejected (K %% 4 == 0 and 16-byte aligned rows required)");
@@ -677,7 +713,8 @@ static int launch(const float* A, const float* Bt, const float* Btl, float* C, c
             if (cudaOccupancyMaxActiveClusters(&max_cl, (void*)k, &cfg) != cudaSuccess || max_cl < 1) max_cl = sms / 2;
         }
         cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(units, max_cl)));
-        if (cudaLaunchKernelEx(&cfg, k, mA, mB, mBl, mC, mCin, C, Cin, cs, (int)M, (int)N, (int)K, alpha, beta) !=
+        if (cudaLaunchKernelEx(&cfg, k, mA, mB, mBl, mC, mCin, C, Cin, cs, bias, act, (int)M, (int)N, (int)K, alpha,
+                               beta) !=
             cudaSuccess) {
             set_error("gemm: cluster launch failed");
             return LRX_ERR_CUDA;
@@ -686,7 +723,8 @@ static int launch(const float* A, const float* Bt, const float* Btl, float* C, c
     }
     const int64_t tiles = cdiv(M, BM) * cdiv(N, BN);
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
-    k<<<grid, THREADS_P, smem, st>>>(mA, mB, mBl, mC, mCin, C, Cin, cs, (int)M, (int)N, (int)K, alpha, beta);
+    k<<<grid, THREADS_P, smem, st>>>(mA, mB, mBl, mC, mCin, C, Cin, cs, bias, act, (int)M, (int)N, (int)K, alpha,
+                                     beta);
     return launched(te ? "lrx_gemm_f32/tcgen05+tma_epilogue" : "lrx_gemm_f32/tcgen05");
 }
 
@@ -817,21 +855,22 @@ using namespace lrx;
 extern "C" {
 
 int lrx_gemm_f32(const void* A, const void* Bt, const void* Bt_lo, void* C, const void* Cin, const void* colscale,
-                 int64_t M, int64_t N, int64_t K, float alpha, float beta, void* stream) {
+                 const void* bias, int act, int64_t M, int64_t N, int64_t K, float alpha, float beta, void* stream) {
     LRX_REQUIRE(M >= 1 && N >= 1 && K >= 1, LRX_ERR_SHAPE, "gemm: bad extents M=%lld N=%lld K=%lld", (long long)M,
                 (long long)N, (long long)K);
     // K <= 8192: the whole K is accumulated in TMEM (not round-to-nearest:
     // ~6e-8 per 8-wide step, 6e-5 at the cap); longer sums go to the library
     LRX_REQUIRE(M < (1ll << 31) && N <= (1 << 16) && K <= 8192, LRX_ERR_UNSUPPORTED, "gemm: extents too large");
+    LRX_REQUIRE(act >= 0 && act <= 2, LRX_ERR_VALUE, "gemm: unknown activation %d", act);
     cudaStream_t st = (cudaStream_t)stream;
-    const float *a = (const float*)A, *b = (const float*)Bt, *bl = (const float*)Bt_lo;
-    if (N <= 64) return gemm::launch<64>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K, alpha,
+    const float *a = (const float*)A, *b = (const float*)Bt, *bl = (const float*)Bt_lo, *bs = (const float*)bias;
+    if (N <= 64) return gemm::launch<64>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, bs, act, M, N, K, alpha,
                                          beta, st);
     const char* e = getenv("LRX_GEMM_BN");
     const int bn_cap = e ? atoi(e) : 256;
-    if (N <= 128 || bn_cap <= 128) return gemm::launch<128>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K,
+    if (N <= 128 || bn_cap <= 128) return gemm::launch<128>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, bs, act, M, N, K,
                                            alpha, beta, st);
-    return gemm::launch<256>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, M, N, K, alpha, beta, st);
+    return gemm::launch<256>(a, b, bl, (float*)C, (const float*)Cin, (const float*)colscale, bs, act, M, N, K, alpha, beta, st);
 }
 
 int lrx_gemm_f32_tn_splits(int64_t M, int64_t N, int64_t K, int64_t* n_splits) {

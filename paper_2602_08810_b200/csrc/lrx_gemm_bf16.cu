@@ -74,8 +74,22 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 }
 
 __device__ __forceinline__ float act(float x, int a) {
-    if (a == ACT_SOFTPLUS) return x > 30.f ? x : log1pf(__expf(x));  // numerics.py:36-39 (f32 threshold)
-    if (a == ACT_SIGMOID) return 1.f / (1.f + __expf(-x));
+    // MUFU forms (ex2 / lg2 / rcp, ~2 ulp): softplus keeps its relative
+    // precision for e^x << 1 through the log1p series (as the S6 scan's
+    // softplus); threshold 30 (numerics.py:36-39)
+    if (a == 1) {
+        float e, lg;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fminf(x, 30.f) * 1.4426950408889634f));
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(1.f + e));
+        const float ser = e * (1.f - e * (0.5f - e * (1.f / 3.f)));
+        return x > 30.f ? x : (e < 1e-2f ? ser : lg * 0.6931471805599453f);
+    }
+    if (a == 2) {
+        float e, r;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-x * 1.4426950408889634f));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + e));
+        return r;
+    }
     return x;
 }
 

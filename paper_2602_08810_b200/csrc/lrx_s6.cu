@@ -70,6 +70,8 @@ int lrx_s6_fwd(int io_dtype, const void* u, const void* pre, const void* b_delta
         return s6v3::fwd<float>(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0, y, ckpt, B, L, D, ws, ws_bytes, flags,
                                 st);
     }
+    LRX_REQUIRE(!(flags & LRX_S6_DELTA_IN), LRX_ERR_UNSUPPORTED,
+                "s6: LRX_S6_DELTA_IN needs the v3 kernels (d_state 16, f32 / bf16 I/O)");
     switch (io_dtype) {
         case LRX_F32: return s6::fwd_f32(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0, y, ckpt, B, L, D, N, st);
         case LRX_BF16: return s6::fwd_bf16(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0, y, ckpt, B, L, D, N, st);
@@ -93,6 +95,8 @@ int lrx_s6_bwd(int io_dtype, const void* u, const void* pre, const void* b_delta
         return s6v3::bwd<float>(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in, gu_local, gpre, gBk_part,
                                 gCk_part, ga_part, gD_part, gb_part, h_out, B, L, D, ws, ws_bytes, flags, st);
     }
+    LRX_REQUIRE(!(flags & LRX_S6_DELTA_IN), LRX_ERR_UNSUPPORTED,
+                "s6: LRX_S6_DELTA_IN needs the v3 kernels (d_state 16, f32 / bf16 I/O)");
     switch (io_dtype) {
         case LRX_F32:
             return s6::bwd_f32(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in, gu_local, gpre, gBk_part,

@@ -93,6 +93,22 @@ __device__ __forceinline__ float softplus_sig(float x, float* sig) {
     return x > 30.f ? x : (e < 1e-2f ? ser : lg);
 }
 
+// delta-input mode (LRX_S6_DELTA_IN): the projection GEMM already applied
+// softplus; sigmoid(pre) = 1 - exp(-delta), relative-accurate for small delta
+// (= e^pre when pre << 0) through the series of -expm1(-delta)
+__device__ __forceinline__ float sig_of_delta(float dl) {
+    const float ser = dl * (1.f - dl * (0.5f - dl * (1.f / 6.f - dl * (1.f / 24.f))));
+    return dl < 1e-2f ? ser : 1.f - ex2(-dl * kLog2e);
+}
+// one prologue value: (delta, sigmoid) from pre (+ b) or from delta itself
+__device__ __forceinline__ float pro_delta(float v, float pbd, int din, float* sig) {
+    if (din) {
+        *sig = sig_of_delta(v);
+        return v;
+    }
+    return softplus_sig(v + pbd, sig);
+}
+
 __device__ __forceinline__ float2 ld_pair(const __nv_bfloat16* p) {
     const uint32_t v = *reinterpret_cast<const uint32_t*>(p);
     return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
@@ -174,7 +190,7 @@ __global__ void __launch_bounds__(THREADS) fwd_agg_kernel(
     const __grid_constant__ CUtensorMap mu, const __grid_constant__ CUtensorMap mp,
     const __grid_constant__ CUtensorMap mB, const float* __restrict__ bdelta, const float* __restrict__ a_log,
     float* __restrict__ aggX, float* __restrict__ aggSD, int64_t Bn, int64_t L, int64_t D, int64_t seg_len,
-    int s_lo) {
+    int s_lo, int din) {
     using LY = Lay<IO>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -234,7 +250,7 @@ __global__ void __launch_bounds__(THREADS) fwd_agg_kernel(
 #pragma unroll
         for (int i = 0; i < T / 2; ++i) {
             float sig;
-            const float dl = softplus_sig(pv[i] + pbd, &sig);
+            const float dl = pro_delta(pv[i], pbd, din, &sig);
             pv[i] = pr + 2 * i < nt ? dl : 0.f;
             sd += pv[i];
         }
@@ -292,7 +308,7 @@ __global__ void __launch_bounds__(FG<NPT>::THREADS) fwd_kernel(
     const __grid_constant__ CUtensorMap my, const float* __restrict__ bdelta, const float* __restrict__ a_log,
     const float* __restrict__ Dskip, const float* __restrict__ x0, const float* __restrict__ aggX,
     const float* __restrict__ aggSD, float* __restrict__ ckpt, int64_t Bn, int64_t L, int64_t D, int64_t seg_len,
-    int n_ck) {
+    int n_ck, int din) {
     using G = FG<NPT>;
     constexpr int LU = TF * CH * (int)sizeof(IO), LP = TF * CH * 4, LBC = TF * NST * 4;
     constexpr int LFWD = LU + LP + 2 * LBC;
@@ -379,7 +395,7 @@ __global__ void __launch_bounds__(FG<NPT>::THREADS) fwd_kernel(
 #pragma unroll
         for (int i = 0; i < NPR; ++i) {
             float sig;
-            const float dl = softplus_sig(pv[i] + pbd, &sig);
+            const float dl = pro_delta(pv[i], pbd, din, &sig);
             pv[i] = pr + (TH / CH) * i < nt ? dl : 0.f;  // past L: abar = 1, no input -> the state is carried
         }
 #pragma unroll
@@ -482,7 +498,7 @@ __global__ void __launch_bounds__(THREADS) bwd_agg_kernel(
     const __grid_constant__ CUtensorMap mg, const __grid_constant__ CUtensorMap mp,
     const __grid_constant__ CUtensorMap mC, const float* __restrict__ bdelta, const float* __restrict__ a_log,
     float* __restrict__ aggH, float* __restrict__ aggSD, int64_t Bn, int64_t L, int64_t D, int64_t seg_len,
-    int s_lo) {
+    int s_lo, int din) {
     using LY = Lay<IO>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -533,7 +549,7 @@ __global__ void __launch_bounds__(THREADS) bwd_agg_kernel(
 #pragma unroll
         for (int i = 0; i < T / 2; ++i) {
             float sig;
-            const float dl = softplus_sig(pv[i] + pbd, &sig);
+            const float dl = pro_delta(pv[i], pbd, din, &sig);
             pv[i] = pr + 2 * i < nt ? dl : 0.f;
             sd += pv[i];
         }
@@ -579,7 +595,7 @@ __global__ void __launch_bounds__(THREADS, 3) bwd_kernel(
     const float* __restrict__ aggH, const float* __restrict__ aggSD, float* __restrict__ gB_part,
     float* __restrict__ gC_part, float* __restrict__ ga_part, float* __restrict__ gD_part,
     float* __restrict__ gb_part, float* __restrict__ h_out, int64_t Bn, int64_t L, int64_t D, int64_t seg_len,
-    int n_ck) {
+    int n_ck, int din) {
     using LY = Lay<IO>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -680,7 +696,7 @@ __global__ void __launch_bounds__(THREADS, 3) bwd_kernel(
 #pragma unroll
             for (int i = 0; i < T / 2; ++i) {
                 float sig;
-                const float dl = softplus_sig(pv[i] + pbd, &sig);
+                const float dl = pro_delta(pv[i], pbd, din, &sig);
                 const bool in = pr + 2 * i < nt;
                 pv[i] = in ? dl : 0.f;
                 sv[i] = in ? sig : 0.f;
@@ -951,7 +967,8 @@ static WS carve(void* ws, const Geo& g, int64_t B, int64_t D) {
 
 template <typename IO>
 static int fwd_agg_launch(const void* u, const void* pre, const void* bd, const void* al, const void* Bk, WS w,
-                          const Geo& g, int64_t B, int64_t L, int64_t D, int s_lo, int s_hi, cudaStream_t st) {
+                          const Geo& g, int64_t B, int64_t L, int64_t D, int s_lo, int s_hi, int din,
+                          cudaStream_t st) {
     if (s_hi <= s_lo) return LRX_OK;
     CUtensorMap mu, mp, mB;
     S6V3_MAP(enc_act<IO>(&mu, u, B, L, D));
@@ -960,13 +977,14 @@ static int fwd_agg_launch(const void* u, const void* pre, const void* bd, const 
     const size_t smem = Lay<IO>::smem_fagg();
     if (int e = set_smem(fwd_agg_kernel<IO>, smem, "s6 fwd agg")) return e;
     fwd_agg_kernel<IO><<<dim3((unsigned)g.n_dblk, (unsigned)B, (unsigned)(s_hi - s_lo)), THREADS, smem, st>>>(
-        mu, mp, mB, (const float*)bd, (const float*)al, w.X, w.SD, B, L, D, g.seg_len, s_lo);
+        mu, mp, mB, (const float*)bd, (const float*)al, w.X, w.SD, B, L, D, g.seg_len, s_lo, din);
     return launched("lrx_s6_fwd_agg/v3");
 }
 
 template <typename IO>
 static int bwd_agg_launch(const void* gy, const void* pre, const void* bd, const void* al, const void* Ck, WS w,
-                          const Geo& g, int64_t B, int64_t L, int64_t D, int s_lo, int s_hi, cudaStream_t st) {
+                          const Geo& g, int64_t B, int64_t L, int64_t D, int s_lo, int s_hi, int din,
+                          cudaStream_t st) {
     if (s_hi <= s_lo) return LRX_OK;
     CUtensorMap mg, mp, mC;
     S6V3_MAP(enc_act<IO>(&mg, gy, B, L, D));
@@ -975,7 +993,7 @@ static int bwd_agg_launch(const void* gy, const void* pre, const void* bd, const
     const size_t smem = Lay<IO>::smem_bagg();
     if (int e = set_smem(bwd_agg_kernel<IO>, smem, "s6 bwd agg")) return e;
     bwd_agg_kernel<IO><<<dim3((unsigned)g.n_dblk, (unsigned)B, (unsigned)(s_hi - s_lo)), THREADS, smem, st>>>(
-        mg, mp, mC, (const float*)bd, (const float*)al, w.X, w.SD, B, L, D, g.seg_len, s_lo);
+        mg, mp, mC, (const float*)bd, (const float*)al, w.X, w.SD, B, L, D, g.seg_len, s_lo, din);
     return launched("lrx_s6_bwd_agg/v3");
 }
 
@@ -987,8 +1005,9 @@ int fwd(const void* u, const void* pre, const void* bd, const void* al, const vo
     LRX_REQUIRE(ws != nullptr && ws_bytes >= g.ws_bytes, LRX_ERR_VALUE, "s6: workspace of %lld bytes needed",
                 (long long)g.ws_bytes);
     const WS w = carve(ws, g, B, D);
+    const int din = (flags & LRX_S6_DELTA_IN) ? 1 : 0;
     if (g.n_seg > 1 && !(flags & LRX_S6_REUSE_AGG))
-        if (int e = fwd_agg_launch<IO>(u, pre, bd, al, Bk, w, g, B, L, D, 0, (int)g.n_seg - 1, st)) return e;
+        if (int e = fwd_agg_launch<IO>(u, pre, bd, al, Bk, w, g, B, L, D, 0, (int)g.n_seg - 1, din, st)) return e;
     CUtensorMap mu, mp, mB, mC, my;
     const int TF = fwd_tile();
     const int box = CH;
@@ -1006,7 +1025,7 @@ int fwd(const void* u, const void* pre, const void* bd, const void* al, const vo
         if (int e = set_smem(fwd_kernel<IO, NPT_, TF_>, smem, "s6 fwd")) return e;                                 \
         fwd_kernel<IO, NPT_, TF_><<<grid, FG<NPT_>::THREADS, smem, st>>>(                                          \
             mu, mp, mB, mC, my, (const float*)bd, (const float*)al, (const float*)Dk, (const float*)x0, w.X, w.SD,  \
-            (float*)ckpt, B, L, D, g.seg_len, (int)g.n_ck);                                                        \
+            (float*)ckpt, B, L, D, g.seg_len, (int)g.n_ck, din);                                                   \
     } while (0)
     if (npt == 2 && TF == 32) S6V3_FWD(2, 32);
     else if (npt == 2) S6V3_FWD(2, 16);
@@ -1025,8 +1044,9 @@ int bwd(const void* u, const void* pre, const void* bd, const void* al, const vo
     LRX_REQUIRE(ws != nullptr && ws_bytes >= g.ws_bytes, LRX_ERR_VALUE, "s6: workspace of %lld bytes needed",
                 (long long)g.ws_bytes);
     const WS w = carve(ws, g, B, D);
+    const int din = (flags & LRX_S6_DELTA_IN) ? 1 : 0;
     if (g.n_seg > 1 && !(flags & LRX_S6_REUSE_AGG))
-        if (int e = bwd_agg_launch<IO>(gy, pre, bd, al, Ck, w, g, B, L, D, 1, (int)g.n_seg, st)) return e;
+        if (int e = bwd_agg_launch<IO>(gy, pre, bd, al, Ck, w, g, B, L, D, 1, (int)g.n_seg, din, st)) return e;
     CUtensorMap mu, mp, mg, mB, mC, mgu, mgp;
     S6V3_MAP(enc_act<IO>(&mu, u, B, L, D));
     S6V3_MAP(enc_act<float>(&mp, pre, B, L, D));
@@ -1040,7 +1060,7 @@ int bwd(const void* u, const void* pre, const void* bd, const void* al, const vo
     bwd_kernel<IO><<<dim3((unsigned)g.n_dblk, (unsigned)B, (unsigned)g.n_seg), THREADS, smem, st>>>(
         mu, mp, mg, mB, mC, mgu, mgp, (const float*)bd, (const float*)al, (const float*)Dk, (const float*)ckpt,
         (const float*)h_in, w.X, w.SD, (float*)gBp, (float*)gCp, (float*)gap, (float*)gDp, (float*)gbp,
-        (float*)h_out, B, L, D, g.seg_len, (int)g.n_ck);
+        (float*)h_out, B, L, D, g.seg_len, (int)g.n_ck, din);
     return launched("lrx_s6_bwd/v3");
 }
 
@@ -1053,7 +1073,7 @@ int fwd_carry(const void* u, const void* pre, const void* bd, const void* al, co
     LRX_REQUIRE(ws != nullptr && ws_bytes >= g.ws_bytes, LRX_ERR_VALUE, "s6: workspace of %lld bytes needed",
                 (long long)g.ws_bytes);
     const WS w = carve(ws, g, B, D);
-    if (int e = fwd_agg_launch<IO>(u, pre, bd, al, Bk, w, g, B, L, D, 0, (int)g.n_seg, st)) return e;
+    if (int e = fwd_agg_launch<IO>(u, pre, bd, al, Bk, w, g, B, L, D, 0, (int)g.n_seg, 0, st)) return e;
     const int64_t n = B * D * NST;
     fold_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const float*)al, w.X, w.SD, (float*)x_agg, (float*)sd_agg,
                                                         B, D, (int)g.n_seg, +1);
@@ -1067,7 +1087,7 @@ int bwd_carry(const void* gy, const void* pre, const void* bd, const void* al, c
     LRX_REQUIRE(ws != nullptr && ws_bytes >= g.ws_bytes, LRX_ERR_VALUE, "s6: workspace of %lld bytes needed",
                 (long long)g.ws_bytes);
     const WS w = carve(ws, g, B, D);
-    if (int e = bwd_agg_launch<IO>(gy, pre, bd, al, Ck, w, g, B, L, D, 0, (int)g.n_seg, st)) return e;
+    if (int e = bwd_agg_launch<IO>(gy, pre, bd, al, Ck, w, g, B, L, D, 0, (int)g.n_seg, 0, st)) return e;
     const int64_t n = B * D * NST;
     fold_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const float*)al, w.X, w.SD, (float*)h_agg, (float*)sd_agg,
                                                         B, D, (int)g.n_seg, -1);

@@ -970,6 +970,14 @@ class S6(LinearRecurrence):
         return {"a_log": self.a_log, "W_B": self.W_B, "W_C": self.W_C, "W_delta": self.W_delta,
                 "W_delta_proj": self.W_delta_proj, "b_delta": self.b_delta, "D": self.D}
 
+    def _delta_in(self, p1):
+        """The delta projection's softplus rides the tcgen05 GEMM epilogue when
+        that GEMM runs on the tensor cores and the scan is a v3 kernel."""
+        m = self.d_model
+        v3 = self.d_state % 16 == 0 and (m % 8 == 0 if self.io_dtype == torch.bfloat16 else m % 4 == 0)
+        return (v3 and self.tdt == torch.float32 and _tc_ok(p1, p1.shape[1], m)
+                and os.environ.get("LRX_S6_DELTA_IN") != "0")
+
     def _wcat(self):
         """[W_delta^T; W_B; W_C] ([r + 2n, m]): the three input projections of
         layers.py:1020-1027 as ONE GEMM that reads u once."""
@@ -982,19 +990,27 @@ class S6(LinearRecurrence):
         P = _proj(u2, self._wcat())                                    # [T, r + 2n] fp32
         # own (aligned) storage for each part: the kernels' TMA maps need 16-byte bases
         p1 = P[:, :r].clone()
-        pre = _proj(p1, self.W_delta_proj.T).reshape(B, L, m)
         Bk = P[:, r:r + n].clone().reshape(B, L, n)
         Ck = P[:, r + n:].clone().reshape(B, L, n)
+        flags = 0
+        if self._long is None and self._delta_in(p1):
+            # delta = softplus(p1 W_delta_proj + b_delta) in the GEMM epilogue
+            # (layers.py:1020-1027): the scan reads delta (LRX_S6_DELTA_IN)
+            pre = ops.gemm_f32(p1, self.W_delta_proj.T.contiguous(), bias=self.b_delta,
+                               act=ops.ACT_SOFTPLUS).reshape(B, L, m)
+            flags = ops.S6_DELTA_IN
+        else:
+            pre = _proj(p1, self.W_delta_proj.T).reshape(B, L, m)
         if self._long is not None:  # sequence parallel: this rank's slice
             y, lctx = self._long.forward(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D)
             saved = {"u": u, "p1": p1, "pre": pre, "Bk": Bk, "Ck": Ck, "ckpt": None, "lctx": lctx}
             cks = [c["ckpt"] for c in lctx.get("groups", [lctx])]
             return y, saved, torch.cat([c[:, -1] for c in cks], dim=-1)
         # inference (no tape, no returned state) skips the checkpoint stores
-        y, ckpt = ops.s6_scan_fwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, ckpt=keep)
+        y, ckpt = ops.s6_scan_fwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, ckpt=keep, flags=flags)
         if not keep:
             return y, {}, None
-        saved = {"u": u, "p1": p1, "pre": pre, "Bk": Bk, "Ck": Ck, "ckpt": ckpt}
+        saved = {"u": u, "p1": p1, "pre": pre, "Bk": Bk, "Ck": Ck, "ckpt": ckpt, "flags": flags}
         return y, saved, ckpt[:, -1]
 
     # -- step mode (layers.py:1120-1168) --------------------------------------
@@ -1033,7 +1049,7 @@ class S6(LinearRecurrence):
         if lctx is not None:
             r = self._long.backward(lctx, u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, gy, reduce=False)
         else:
-            r = ops.s6_scan_bwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, ckpt, gy)
+            r = ops.s6_scan_bwd(u, pre, self.b_delta, self.a_log, Bk, Ck, self.D, ckpt, gy, flags=s.get("flags", 0))
         # projection GEMMs (layers.py:1100-1112), compute precision; the three
         # input projections share one GEMM each way: G = [gp1 | gB_k | gC_k]
         c = self.tdt

@@ -85,6 +85,7 @@ def rglru_scan_bwd(u, qr, qi, lambda_param, b_r, b_i, ckpt, gy, y=None):
 # S6
 
 S6_REUSE_AGG = 1
+S6_DELTA_IN = 2
 SCHEME_CODE = {"zoh": 0, "bilinear": 1, "dirac": 2}
 
 
@@ -118,7 +119,7 @@ def _grouped(u, D, N, x0=None, ws=None, flags=0):
     """d_state a multiple of 16 above 16: the v3 kernels run per 16-state group
     (the recurrence is diagonal; the readout and the gradients of u / pre are
     sums over the groups, accumulated in fp32)."""
-    if N <= 16 or N % 16 or ws is not None or flags or u.dtype not in (torch.float32, torch.bfloat16):
+    if N <= 16 or N % 16 or ws is not None or flags & S6_REUSE_AGG or u.dtype not in (torch.float32, torch.bfloat16):
         return False
     geo = s6_geometry(torch.float32, u.shape[0], u.shape[1], D, 16)
     return geo["n_dblk"] > 0 and D % 4 == 0 and os.environ.get("LRX_S6_NOGROUP") != "1"
@@ -145,7 +146,7 @@ def s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=None, ws=None, flags=0
         for g in range(N // 16):
             ag, Bg, Cg, Dg = _group_args(a_log, Bk, Ck, Dskip, g)
             x0g = x0[..., 16 * g:16 * g + 16].contiguous() if x0 is not None else None
-            yg, ckg = s6_scan_fwd(u32, pre, b_delta, ag, Bg, Cg, Dg, x0=x0g, ckpt=ckpt)
+            yg, ckg = s6_scan_fwd(u32, pre, b_delta, ag, Bg, Cg, Dg, x0=x0g, ckpt=ckpt, flags=flags)
             y = yg if y is None else y.add_(yg)
             parts.append(ckg)
         return y.to(u.dtype), (GroupedCkpt(parts) if ckpt else None)
@@ -173,14 +174,15 @@ def _s6_scan_fwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, x0=None, ws=None, flags=
 
 def s6_scan_bwd(u, pre, b_delta, a_log, Bk, Ck, Dskip, ckpt, gy, h_in=None, want_h_out=False, ws=None, flags=0):
     if isinstance(ckpt, GroupedCkpt):
-        if ws is not None or flags:
+        if ws is not None or flags & S6_REUSE_AGG:
             raise ValueError("reused segment maps (ws / flags) need d_state == 16; LongS6 groups itself")
         u32, gy32 = u.float(), gy.float()
         out, cat = None, ("gBk", "gCk", "ga_log") + (("h_out",) if want_h_out else ())
         for g, ckg in enumerate(ckpt.parts):
             ag, Bg, Cg, Dg = _group_args(a_log, Bk, Ck, Dskip, g)
             hg = h_in[..., 16 * g:16 * g + 16].contiguous() if h_in is not None else None
-            r = _s6_scan_bwd(u32, pre, b_delta, ag, Bg, Cg, Dg, ckg, gy32, h_in=hg, want_h_out=want_h_out)
+            r = _s6_scan_bwd(u32, pre, b_delta, ag, Bg, Cg, Dg, ckg, gy32, h_in=hg, want_h_out=want_h_out,
+                             flags=flags)
             if out is None:
                 out = {k: ([v] if k in cat else v) for k, v in r.items()}
             else:  # fixed group order; the carries split by group (diagonal recurrence)
@@ -265,16 +267,17 @@ def tf32_lo(t):
     return t - (t.view(torch.int32) & -8192).view(torch.float32)
 
 
-def gemm_f32(A, Bt, Bt_lo=None, Cin=None, colscale=None, alpha=1.0, beta=0.0, out=None):
-    """C = alpha A Bt^T + (colscale or beta) * Cin on the tensor cores (3xTF32,
-    fp32-accurate).  A [M, K], Bt [N, K] fp32 contiguous (K % 4 == 0)."""
+def gemm_f32(A, Bt, Bt_lo=None, Cin=None, colscale=None, alpha=1.0, beta=0.0, out=None, bias=None, act=0):
+    """C = act(alpha A Bt^T + bias) + (colscale or beta) * Cin on the tensor
+    cores (3xTF32, fp32-accurate).  A [M, K], Bt [N, K] fp32 contiguous
+    (K % 4 == 0); act: ACT_NONE / ACT_SOFTPLUS / ACT_SIGMOID."""
     M, K = A.shape
     N = Bt.shape[0]
     if Bt_lo is None:
         Bt_lo = tf32_lo(Bt)
     C = out if out is not None else torch.empty((M, N), dtype=torch.float32, device=A.device)
     _lib.check(_lib.lib().lrx_gemm_f32(_lib.ptr(A), _lib.ptr(Bt), _lib.ptr(Bt_lo), _lib.ptr(C), _lib.ptr(Cin),
-                                       _lib.ptr(colscale), M, N, K, alpha, beta, _lib.stream()))
+                                       _lib.ptr(colscale), _lib.ptr(bias), act, M, N, K, alpha, beta, _lib.stream()))
     return C
 
 

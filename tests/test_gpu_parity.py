@@ -502,6 +502,33 @@ def test_gemm_f32_tn_tcgen05_matches_f64(lrx, K, M, N):
     assert torch.equal(C, C2)  # deterministic split-K
 
 
+@pytest.mark.parametrize("n", [16, 64])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_s6_layer_delta_epilogue_matches_oracle(lrx, monkeypatch, n, dtype):
+    """S6 layer with >= 4096 tokens: delta = softplus(p1 W_delta_proj + b_delta)
+    in the tcgen05 GEMM epilogue and the scan in delta-input mode
+    (LRX_S6_DELTA_IN; sigmoid(pre) = 1 - exp(-delta) in the backward) against
+    the oracle -- and against the pre-activation path (LRX_S6_DELTA_IN=0)."""
+    m, B, L = 256, 2, 2500  # d_rank 16: the delta GEMM's K qualifies for the tensor cores
+    layer = lrx.make_layer("s6", m, n, dtype=dtype, seed=81)
+    u = torch.from_numpy(port.Rng(82).normal((B, L, m))).to("cuda", layer.io_dtype)
+    gy = torch.from_numpy(port.Rng(83).normal((B, L, m))).to("cuda", layer.io_dtype)
+    y, tape = layer.forward(u, tape=True)
+    assert tape._saved["flags"] == 2
+    g = lrx.layer_backward(layer, tape, gy)
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64("s6", None, params, u.float().cpu().numpy(), gy.float().cpu().numpy())
+    tol = TOL[dtype]
+    assert rel(y, ry) < tol
+    assert rel(g.u, rgu) < tol
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < tol, (k, rel(g.params[k], rg[k]))
+    monkeypatch.setenv("LRX_S6_DELTA_IN", "0")
+    y0, tape0 = layer.forward(u, tape=True)
+    assert tape0._saved["flags"] == 0
+    assert rel(y, y0.float().cpu().numpy()) < (1e-5 if dtype == "f32" else 1e-2)
+
+
 @pytest.mark.parametrize("M,N,K", [(131072, 128, 1536), (4096, 16, 1536), (1000, 96, 72), (300, 256, 64),
                                    (5, 32, 8), (2049, 300, 264)])
 def test_gemm_bf16_tcgen05_matches_fp64(lrx, M, N, K):

@@ -31,3 +31,17 @@ print(f"{wl} B={B} geo={ops.s6_geometry(prob['u'].dtype, B, w['L'], w['H'], w['N
 print(f"fwd (ckpt)    {timeit(lambda: ops.s6_scan_fwd(*args)):.3f} ms")
 print(f"fwd (no ckpt) {timeit(lambda: ops.s6_scan_fwd(*args, ckpt=False)):.3f} ms")
 print(f"bwd           {timeit(lambda: ops.s6_scan_bwd(*args, ck, prob['gy'])):.3f} ms")
+
+# delta-input mode (the layer's GEMM-epilogue softplus): scan only, and the GEMM itself
+if wl == "s6":
+    import torch.nn.functional as F
+    delta = F.softplus(prob["pre"] + layer.b_delta).contiguous()
+    ad = (prob["u"], delta, layer.b_delta, layer.a_log, prob["Bk"], prob["Ck"], layer.D)
+    yd, ckd = ops.s6_scan_fwd(*ad, flags=ops.S6_DELTA_IN)
+    print(f"fwd delta-in  {timeit(lambda: ops.s6_scan_fwd(*ad, flags=ops.S6_DELTA_IN)):.3f} ms")
+    print(f"bwd delta-in  {timeit(lambda: ops.s6_scan_bwd(*ad, ckd, prob['gy'], flags=ops.S6_DELTA_IN)):.3f} ms")
+    T_ = prob["u"].shape[0] * prob["u"].shape[1]
+    p1 = torch.randn((T_, layer.d_rank), device="cuda")
+    wdp = layer.W_delta_proj.T.contiguous()
+    print(f"gemm p1 W_dp        {timeit(lambda: ops.gemm_f32(p1, wdp)):.3f} ms")
+    print(f"gemm p1 W_dp + sp   {timeit(lambda: ops.gemm_f32(p1, wdp, bias=layer.b_delta, act=ops.ACT_SOFTPLUS)):.3f} ms")
