@@ -15,11 +15,13 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 from ncu_summary import full, launches  # noqa: E402
 
 tag = sys.argv[1]
-out = os.path.join(ROOT, "profiles")
+out = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles")
+os.makedirs(out, exist_ok=True)
 go = os.path.join(ROOT, "gpurun_out")
 # dominant kernel per workload (the bench.py probe), matched on the launch list
-DOM = {"rglru": r"bwd_tma_kernel", "s6": r"s6v3::bwd_kernel", "s6_long": r"s6v3::bwd(_agg)?_kernel",
-       "s5": r"gemm_tf32x3_kernel", "lru": r"mimo::bwd_kernel"}
+DOM = {"rglru": r"bwd_rev2_kernel", "s6": r"s6v3::bwd_kernel", "s6_long": r"s6v3::bwd(_agg)?_kernel",
+       "s5": r"gemm_tf32x3_kernel", "lru": r"mimo::bwd_kernel", "s6_layer": r"s6v3::bwd_kernel",
+       "rglru_layer": r"gemm_tf32x3_kernel"}
 traffic = {}
 for wl, pat in DOM.items():
     path = os.path.join(go, f"launches_{wl}_{tag}.csv")
@@ -37,13 +39,13 @@ for wl, pat in DOM.items():
     json.dump({"step_ns": tot, "launches": half}, open(os.path.join(out, f"{tag}_launches_{wl}.json"), "w"), indent=1)
     dom = [r for r in half if re.search(pat, r["kernel"])]
     if dom:
-        if wl == "s5":  # the skip-fused output projection: the GEMM launch with the most DRAM traffic
+        if wl in ("s5", "rglru_layer"):  # one GEMM launch: the one with the most DRAM traffic
             dom = [max(dom, key=lambda r: r["dram__bytes_read.sum"] + r["dram__bytes_write.sum"])]
         b = sum(r["dram__bytes_read.sum"] + r["dram__bytes_write.sum"] for r in dom)
         traffic[wl] = {"probe": b,
                        "kernels": [r["kernel"][:80] for r in dom], "source": f"profiles/{tag}_launches_{wl}.json"}
     print(wl, f"step {tot / 1e3:.1f} us", f"dominant {[r['kernel'][:40] for r in dom]}")
-for wl in ("s6", "s5", "rglru", "s6_long"):
+for wl in ("s6", "s5", "rglru", "s6_long", "s6_layer"):
     rep = os.path.join(go, f"prof_{wl}_{tag}.ncu-rep")
     if os.path.exists(rep):
         json.dump(full(rep), open(os.path.join(out, f"{tag}_ncu_full_{wl}.json"), "w"), indent=1)
