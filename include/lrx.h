@@ -240,6 +240,10 @@ int lrx_mimo_bwd_ps(int dtype, const void* lam, const void* delta, const void* d
                     const void* x, const void* gx, void* gbu, void* glam_part, void* gdl_part, int64_t B, int64_t L,
                     int64_t P, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- bf16 <-> fp32 conversion of activation planes (n elements, 16-byte
+ * aligned): the bf16 layers' fp32 GEMM operands and results. */
+int lrx_cast(int dtype_in, int dtype_out, const void* in, void* out, int64_t n, void* stream);
+
 /* ---- MIMO LTI coefficient work (S5 / LRU), one launch each way ------------
  * Replaces the parameter-sized torch glue of S5._abar_scale / LRU._abar_scale
  * (layers.py:823-834, 936-943) and the coefficient + B/C gradient assembly of

@@ -1054,11 +1054,11 @@ class S6(LinearRecurrence):
         # input projections share one GEMM each way: G = [gp1 | gB_k | gC_k]
         c = self.tdt
         rk = self.d_rank
-        u2 = u.reshape(B * L, m).to(c)
+        u2 = ops.cast(u.reshape(B * L, m), c)
         gpre2 = r["gpre"].reshape(B * L, m)
         gp1 = _proj(gpre2, self.W_delta_proj)
         G = torch.cat((gp1, r["gBk"].reshape(B * L, n).to(c), r["gCk"].reshape(B * L, n).to(c)), 1)
-        gu = r["gu_local"].reshape(B * L, m).to(c)
+        gu = ops.cast(r["gu_local"].reshape(B * L, m), c)
         gu = _proj_acc(gu, G, self._wcat().T)                          # gu += G [W_delta^T; W_B; W_C]
         gW = _wgrad(G, u2)                                             # [r + 2n, m]
         grads = {"a_log": r["ga_log"], "W_B": gW[rk:rk + n].contiguous(), "W_C": gW[rk + n:].contiguous(),
@@ -1067,7 +1067,7 @@ class S6(LinearRecurrence):
         if lctx is not None:  # every gradient is a sum over the whole sequence: one fixed-order reduction
             from .distributed import reduce_fixed_order
             grads = dict(zip(grads, reduce_fixed_order(list(grads.values()), self._long.group)))
-        return self._out(grads, gu.reshape(B, L, m).to(self.io_dtype), host)
+        return self._out(grads, ops.cast(gu, self.io_dtype).reshape(B, L, m), host)
 
 
 # ---------------------------------------------------------------------------
@@ -1140,13 +1140,13 @@ class RGLRU(LinearRecurrence):
         gy = self._gy(gy, u.shape)
         r = ops.rglru_scan_bwd(u, qr, qi, self.lambda_param, self.b_r, self.b_i, ckpt, gy, y=s["y"])
         c = self.tdt
-        u2 = u.reshape(B * L, W).to(c)
-        gqr2, gqi2 = r["gqr"].reshape(B * L, W).to(c), r["gqi"].reshape(B * L, W).to(c)
-        gu = _proj_acc(r["gu_local"].reshape(B * L, W).to(c), gqr2, self.W_r.T)
+        u2 = ops.cast(u.reshape(B * L, W), c)
+        gqr2, gqi2 = ops.cast(r["gqr"].reshape(B * L, W), c), ops.cast(r["gqi"].reshape(B * L, W), c)
+        gu = _proj_acc(ops.cast(r["gu_local"].reshape(B * L, W), c), gqr2, self.W_r.T)
         gu = _proj_acc(gu, gqi2, self.W_i.T)
         grads = {"lambda_param": sigmoid(-self.lambda_param) * r["gla"], "W_r": _wgrad(gqr2, u2), "b_r": r["gb_r"],
                  "W_i": _wgrad(gqi2, u2), "b_i": r["gb_i"]}
-        return self._out(grads, gu.reshape(B, L, W).to(self.io_dtype), host)
+        return self._out(grads, ops.cast(gu, self.io_dtype).reshape(B, L, W), host)
 
 
 # ---------------------------------------------------------------------------

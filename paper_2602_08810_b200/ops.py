@@ -293,6 +293,19 @@ def gemm_f32_tn(A, B, alpha=1.0):
     return reduce_rows(part, ks.value, M * N).reshape(M, N)
 
 
+def cast(t, dtype):
+    """bf16 <-> fp32 copy of an activation plane on the lrx streaming kernel
+    (any other pair: torch)."""
+    pair = (t.dtype, dtype)
+    if pair not in ((torch.bfloat16, torch.float32), (torch.float32, torch.bfloat16)) or not t.is_cuda:
+        return t.to(dtype)
+    t = t.contiguous()
+    out = torch.empty(t.shape, dtype=dtype, device=t.device)
+    _lib.check(_lib.lib().lrx_cast(_lib.code_of(t.dtype), _lib.code_of(dtype), _lib.ptr(t), _lib.ptr(out), t.numel(),
+                                   _lib.stream()))
+    return out
+
+
 # ---------------------------------------------------------------------------
 # bf16 GEMM on tcgen05 (kind::f16, fp32 accumulation) with a fused epilogue
 

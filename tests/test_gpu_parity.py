@@ -529,6 +529,17 @@ def test_s6_layer_delta_epilogue_matches_oracle(lrx, monkeypatch, n, dtype):
     assert rel(y, y0.float().cpu().numpy()) < (1e-5 if dtype == "f32" else 1e-2)
 
 
+@pytest.mark.parametrize("n", [0, 5, 8, 1003, 1 << 20])
+def test_cast_matches_torch_bitwise(lrx, n):
+    """lrx_cast (bf16 <-> fp32 planes, ragged tail) gives torch's conversion bits."""
+    from paper_2602_08810_b200 import ops
+    x = torch.randn(n, device="cuda") * 3
+    b = ops.cast(x, torch.bfloat16)
+    assert b.dtype == torch.bfloat16 and torch.equal(b, x.to(torch.bfloat16))
+    f = ops.cast(b, torch.float32)
+    assert f.dtype == torch.float32 and torch.equal(f, b.float())
+
+
 @pytest.mark.parametrize("M,N,K", [(131072, 128, 1536), (4096, 16, 1536), (1000, 96, 72), (300, 256, 64),
                                    (5, 32, 8), (2049, 300, 264)])
 def test_gemm_bf16_tcgen05_matches_fp64(lrx, M, N, K):
