@@ -950,6 +950,9 @@ class S6(LinearRecurrence):
         self.seq_group = seq_group
         self._long = None
         if seq_group is not None:
+            if self.dtype == "f64" or self.d_state % 16 or d_model % (8 if self.dtype == "bf16" else 4):
+                raise ValueError("seq_group needs the v3 kernels: f32 / bf16 I/O, d_state a multiple of 16 and "
+                                 "d_model a multiple of 4 (f32) / 8 (bf16)")
             from .distributed import LongS6
             self._long = LongS6(None if seq_group == "world" else seq_group)
         rng = rng if rng is not None else Rng(seed)
