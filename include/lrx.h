@@ -244,6 +244,20 @@ int lrx_mimo_bwd_ps(int dtype, const void* lam, const void* delta, const void* d
  * aligned): the bf16 layers' fp32 GEMM operands and results. */
 int lrx_cast(int dtype_in, int dtype_out, const void* in, void* out, int64_t n, void* stream);
 
+/* ---- S4D coefficient work (constant steps), one launch each way ----------
+ * S4D._lam / scheme_factors and the coefficient part of S4D._backward through
+ * scheme_partials (layers.py:382-386, 520-546; discretize.py:59-93;
+ * autograd.py:186-211), in f64 on the device: parameters [H, N] (log_delta
+ * [H]) of the layer dtype (F32 / F64) -> abar, w = scale b [H, N] complex of
+ * that precision; backward from the fused kernel's gabar / gw sums to the
+ * parameter gradients (N <= 64). */
+int lrx_s4d_coef(int dtype, int scheme, const void* lambda_re_log, const void* lambda_im, const void* b_re,
+                 const void* b_im, const void* log_delta, int64_t H, int64_t N, void* abar, void* w, void* stream);
+int lrx_s4d_coef_grads(int dtype, int scheme, const void* lambda_re_log, const void* lambda_im, const void* b_re,
+                       const void* b_im, const void* log_delta, const void* gabar, const void* gpsi, int64_t H,
+                       int64_t N, void* g_lambda_re_log, void* g_lambda_im, void* g_b_re, void* g_b_im,
+                       void* g_log_delta, void* stream);
+
 /* ---- MIMO LTI coefficient work (S5 / LRU), one launch each way ------------
  * Replaces the parameter-sized torch glue of S5._abar_scale / LRU._abar_scale
  * (layers.py:823-834, 936-943) and the coefficient + B/C gradient assembly of

@@ -67,6 +67,8 @@ SIGNATURES = {
                           _vp]),
     "lrx_gemm_f32_tn_splits": (_i, [_i64, _i64, _i64, _P64]),
     "lrx_gemm_f32_tn": (_i, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_float, _vp]),
+    "lrx_s4d_coef": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "lrx_s4d_coef_grads": (_i, [_i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "lrx_cast": (_i, [_i, _i, _vp, _vp, _i64, _vp]),
     "lrx_gemm_bf16": (_i, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, ctypes.c_float, ctypes.c_float, _i, _i, _vp]),
     "lrx_s4d_chunking": (_i, [_i64, _P64, _P64]),

@@ -172,6 +172,69 @@ static unsigned grid_for(int64_t n) {
 
 using namespace lrx;
 
+namespace lrx {
+namespace coef {
+
+// ---- S4D (layers.py:352-546): per (h, n) coefficients and their gradients --
+// Forward: lam = -exp(lambda_re_log) + i lambda_im, delta = exp(log_delta[h]),
+// (abar, scale) = scheme(lam, delta) in f64 (lrx_common.cuh disc), w = scale b.
+template <typename T>
+__global__ void s4d_coef_kernel(int scheme, const T* lre, const T* lim, const T* bre, const T* bim, const T* ldl,
+                                int64_t H, int64_t N, cplx<T>* abar, cplx<T>* w) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= H * N) return;
+    const z64 lam = {-exp((double)lre[i]), (double)lim[i]};
+    const double delta = exp((double)ldl[i / N]);
+    z64 ab, sc;
+    disc<double>(scheme, lam, delta, ab, sc);
+    const z64 wv = sc * z64{(double)bre[i], (double)bim[i]};
+    abar[i] = {(T)ab.re, (T)ab.im};
+    w[i] = {(T)wv.re, (T)wv.im};
+}
+
+// Backward, block per channel h (threads over n): from gabar = sum g conj(x_prev)
+// and gpsi = sum u g (the fused kernel's partial sums):
+//   gscale = conj(b) gpsi, gb = conj(scale) gpsi,
+//   glam = conj(dal) gabar + conj(dsl) gscale,
+//   glog_delta[h] = delta sum_n Re(conj(dad) gabar) + Re(conj(dsd) gscale)
+// (S4D._backward, layers.py:520-546; the n-sum is a fixed-order tree).
+template <typename T>
+__global__ void s4d_coef_grads_kernel(int scheme, const T* lre, const T* lim, const T* bre, const T* bim,
+                                      const T* ldl, const cplx<T>* gabar, const cplx<T>* gpsi, int64_t H, int64_t N,
+                                      T* g_lre, T* g_lim, T* g_bre, T* g_bim, T* g_ldl) {
+    __shared__ double red[64];
+    const int64_t h = blockIdx.x;
+    const int n = threadIdx.x;
+    double gd = 0.0;
+    if (n < N) {
+        const int64_t i = h * N + n;
+        const z64 lam = {-exp((double)lre[i]), (double)lim[i]};
+        const double delta = exp((double)ldl[h]);
+        z64 ab, sc, dal, dad, dsl, dsd;
+        disc<double>(scheme, lam, delta, ab, sc);
+        disc_partials<double>(scheme, lam, delta, ab, dal, dad, dsl, dsd);
+        const z64 ga = {(double)gabar[i].re, (double)gabar[i].im}, gp = {(double)gpsi[i].re, (double)gpsi[i].im};
+        const z64 b = {(double)bre[i], (double)bim[i]};
+        const z64 gsc = conj(b) * gp, gb = conj(sc) * gp;
+        const z64 glam = conj(dal) * ga + conj(dsl) * gsc;
+        g_lre[i] = (T)(lam.re * glam.re);  // d lam.re / d lambda_re_log = -exp(.) = lam.re
+        g_lim[i] = (T)glam.im;
+        g_bre[i] = (T)gb.re;
+        g_bim[i] = (T)gb.im;
+        gd = ((conj(dad) * ga).re + (conj(dsd) * gsc).re) * delta;
+    }
+    red[n] = gd;
+    __syncthreads();
+    for (int s2 = 32; s2 >= 1; s2 >>= 1) {
+        if (n < s2) red[n] += red[n + s2];
+        __syncthreads();
+    }
+    if (n == 0) g_ldl[h] = (T)red[0];
+}
+
+}  // namespace coef
+}  // namespace lrx
+
 extern "C" {
 
 int lrx_mimo_coef(int kind, int scheme, int dtype, const void* p0, const void* p1, const void* p2, const void* b_re,
@@ -215,6 +278,53 @@ int lrx_mimo_coef_grads(int kind, int scheme, int dtype, const void* p0, const v
         return LRX_ERR_VALUE;
     }
     return launched("lrx_mimo_coef_grads");
+}
+
+int lrx_s4d_coef(int dtype, int scheme, const void* lambda_re_log, const void* lambda_im, const void* b_re,
+                 const void* b_im, const void* log_delta, int64_t H, int64_t N, void* abar, void* w, void* stream) {
+    LRX_REQUIRE(H >= 1 && N >= 1, LRX_ERR_SHAPE, "s4d coef: bad extents");
+    LRX_REQUIRE(scheme >= 0 && scheme <= 2, LRX_ERR_VALUE, "s4d coef: scheme %d", scheme);
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned grid = (unsigned)cdiv(H * N, 128);
+    if (dtype == LRX_F32)
+        coef::s4d_coef_kernel<float><<<grid, 128, 0, st>>>(scheme, (const float*)lambda_re_log, (const float*)lambda_im,
+                                                            (const float*)b_re, (const float*)b_im,
+                                                            (const float*)log_delta, H, N, (cplx<float>*)abar,
+                                                            (cplx<float>*)w);
+    else if (dtype == LRX_F64)
+        coef::s4d_coef_kernel<double><<<grid, 128, 0, st>>>(scheme, (const double*)lambda_re_log,
+                                                             (const double*)lambda_im, (const double*)b_re,
+                                                             (const double*)b_im, (const double*)log_delta, H, N,
+                                                             (cplx<double>*)abar, (cplx<double>*)w);
+    else {
+        set_error("s4d coef: dtype %d (f32 / f64)", dtype);
+        return LRX_ERR_VALUE;
+    }
+    return launched("lrx_s4d_coef");
+}
+
+int lrx_s4d_coef_grads(int dtype, int scheme, const void* lambda_re_log, const void* lambda_im, const void* b_re,
+                       const void* b_im, const void* log_delta, const void* gabar, const void* gpsi, int64_t H,
+                       int64_t N, void* g_lambda_re_log, void* g_lambda_im, void* g_b_re, void* g_b_im,
+                       void* g_log_delta, void* stream) {
+    LRX_REQUIRE(H >= 1 && N >= 1 && N <= 64, LRX_ERR_SHAPE, "s4d coef grads: bad extents (N <= 64)");
+    LRX_REQUIRE(scheme >= 0 && scheme <= 2, LRX_ERR_VALUE, "s4d coef: scheme %d", scheme);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == LRX_F32)
+        coef::s4d_coef_grads_kernel<float><<<(unsigned)H, 64, 0, st>>>(
+            scheme, (const float*)lambda_re_log, (const float*)lambda_im, (const float*)b_re, (const float*)b_im,
+            (const float*)log_delta, (const cplx<float>*)gabar, (const cplx<float>*)gpsi, H, N,
+            (float*)g_lambda_re_log, (float*)g_lambda_im, (float*)g_b_re, (float*)g_b_im, (float*)g_log_delta);
+    else if (dtype == LRX_F64)
+        coef::s4d_coef_grads_kernel<double><<<(unsigned)H, 64, 0, st>>>(
+            scheme, (const double*)lambda_re_log, (const double*)lambda_im, (const double*)b_re, (const double*)b_im,
+            (const double*)log_delta, (const cplx<double>*)gabar, (const cplx<double>*)gpsi, H, N,
+            (double*)g_lambda_re_log, (double*)g_lambda_im, (double*)g_b_re, (double*)g_b_im, (double*)g_log_delta);
+    else {
+        set_error("s4d coef: dtype %d (f32 / f64)", dtype);
+        return LRX_ERR_VALUE;
+    }
+    return launched("lrx_s4d_coef_grads");
 }
 
 }  // extern "C"

@@ -449,9 +449,15 @@ class S4D(LinearRecurrence):
 
     def _fused_args(self, deltas):
         c = torch.complex(self.c_re, self.c_im).contiguous()
-        if deltas is None:
-            lam, delta, b, abar, scale = self._coeffs(None)
-            return c, dict(abar=abar.to(self.tcdt).contiguous(), w=(scale * b).to(self.tcdt).contiguous())
+        if deltas is None:  # coefficients in f64 on the device, one launch (lrx_s4d_coef)
+            m, n = self.d_model, self.d_state
+            abar = torch.empty((m, n), dtype=self.tcdt, device=self.device)
+            w = torch.empty_like(abar)
+            _lib.check(_lib.lib().lrx_s4d_coef(
+                _lib.code_of(self.tdt), ops.SCHEME_CODE[self.discretization], _lib.ptr(self.lambda_re_log),
+                _lib.ptr(self.lambda_im), _lib.ptr(self.b_re), _lib.ptr(self.b_im), _lib.ptr(self.log_delta), m, n,
+                _lib.ptr(abar), _lib.ptr(w), _lib.stream()))
+            return c, dict(abar=abar, w=w)
         # per-step discretisation in the kernel; bilinear cannot be singular
         # here: Re(lambda) = -exp(.) < 0 and deltas >= 0 keep |1 - delta lambda / 2| >= 1
         return c, dict(lam=self._lam().to(self.tcdt).contiguous(), b=torch.complex(self.b_re, self.b_im).contiguous(),
@@ -509,21 +515,22 @@ class S4D(LinearRecurrence):
         gy = self._gy(gy, u.shape)
         c, kw = self._fused_args(deltas)
         r = ops.s4d_scan_bwd(u, gy, c, self.d.contiguous(), ckpt, **kw)
-        if deltas is None:
-            lam, delta, b, abar, scale = self._coeffs(None)
-            c128 = torch.complex128
-            gabar, gpsi = r["gabar"].to(c128), r["gw"].to(c128)
-            gscale = b.conj() * gpsi
-            gb = scale.conj() * gpsi
-            dal, dad, dsl, dsd = scheme_partials(self.discretization, lam, delta[:, None], abar, scale)
-            glam = dal.conj() * gabar + dsl.conj() * gscale
-            glog_delta = ((dad.conj() * gabar).real + (dsd.conj() * gscale).real).sum(-1) * delta
-        else:  # the kernel accumulated the per-step scheme partials (autograd.py:186-211)
-            glam, gb, glog_delta = r["glam"], r["gb"], r["gdl"]
         gc = r["gc"]
-        grads = {"lambda_re_log": -torch.exp(self.lambda_re_log.to(glam.real.dtype)) * glam.real,
-                 "lambda_im": glam.imag, "b.re": gb.real, "b.im": gb.imag, "c.re": gc.real, "c.im": gc.imag,
-                 "d": r["gd"], "log_delta": glog_delta}
+        if deltas is None:  # scheme partials in f64 on the device, one launch (lrx_s4d_coef_grads)
+            m, n = self.d_model, self.d_state
+            g = torch.empty((4, m, n), dtype=self.tdt, device=self.device)
+            gld = torch.empty(m, dtype=self.tdt, device=self.device)
+            _lib.check(_lib.lib().lrx_s4d_coef_grads(
+                _lib.code_of(self.tdt), ops.SCHEME_CODE[self.discretization], _lib.ptr(self.lambda_re_log),
+                _lib.ptr(self.lambda_im), _lib.ptr(self.b_re), _lib.ptr(self.b_im), _lib.ptr(self.log_delta),
+                _lib.ptr(r["gabar"].contiguous()), _lib.ptr(r["gw"].contiguous()), m, n, _lib.ptr(g[0]),
+                _lib.ptr(g[1]), _lib.ptr(g[2]), _lib.ptr(g[3]), _lib.ptr(gld), _lib.stream()))
+            grads = {"lambda_re_log": g[0], "lambda_im": g[1], "b.re": g[2], "b.im": g[3], "log_delta": gld}
+        else:  # the kernel accumulated the per-step scheme partials (autograd.py:186-211)
+            glam, gb = r["glam"], r["gb"]
+            grads = {"lambda_re_log": -torch.exp(self.lambda_re_log.to(glam.real.dtype)) * glam.real,
+                     "lambda_im": glam.imag, "b.re": gb.real, "b.im": gb.imag, "log_delta": r["gdl"]}
+        grads.update({"c.re": gc.real, "c.im": gc.imag, "d": r["gd"]})
         grads = {k: v.to(self.tdt).contiguous() for k, v in grads.items()}
         return self._out({k: grads[k] for k in self.parameters()}, r["gu"], host)
 
