@@ -477,21 +477,42 @@ def run_e2e(args, w, prob, device):
 
     kind, H, N = w["kind"], w["H"], w["N"]
     L = prob["u"].shape[1]
-    Bs = min(prob["B"], args.e2e_batch)
-    if w.get("seqpar"):  # e2e on a 1/16 time slice of this rank's sequence (host memory)
-        L = L // 16
+    names = ({"rglru": ("u", "qr", "qi", "gy"), "s6": ("u", "pre", "Bk", "Ck", "gy")}.get(kind, ("u", "gy"))
+             if not w.get("layer") else ("u", "gy"))
+    # the whole per-rank batch by default: inputs + outputs pinned (~2x the
+    # input bytes), within ~45% of the host memory shared by the local ranks
+    row = sum(prob[n][:1].numel() * prob[n].element_size() for n in names)
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:  # pragma: no cover - psutil is in the image
+        avail = 64 << 30
+    local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    budget = 0.45 * avail / local
+    Bs = prob["B"] if args.e2e_batch <= 0 else min(prob["B"], args.e2e_batch)
+    while Bs > 1 and 2 * row * Bs > budget:
+        Bs //= 2
+    if w.get("seqpar") and 2 * row * Bs > budget:  # a time slice of this rank's sequence (host memory)
+        frac = 1
+        while frac < 64 and 2 * row * Bs / frac > budget:
+            frac *= 2
+        L = L // frac
         for n in ("u", "pre", "Bk", "Ck", "gy"):
             prob = dict(prob)
             prob[n] = prob[n][:, :L].contiguous()
-    names = ({"rglru": ("u", "qr", "qi", "gy"), "s6": ("u", "pre", "Bk", "Ck", "gy")}.get(kind, ("u", "gy"))
-             if not w.get("layer") else ("u", "gy"))
     host = {n: prob[n][:Bs].cpu().pin_memory() for n in names}
     layer = prob["layer"]
     h2d = sum(t.numel() * t.element_size() for t in host.values())
     # sub-batches pipeline the PCIe copies: H2D of sub-batch i+1 and D2H of i
     # run on the two copy engines while i computes; the step approaches
     # max(H2D, D2H) + one sub-batch's share
-    n_sub = next((k for k in (8, 4, 2) if Bs % k == 0), 1) if kind in ("rglru", "s6") else 1
+    # one-row sub-batches on their own streams: the finest overlap of the two copy engines with the
+    # kernels (measured C4 full batch: 1-row 85 GB/s of PCIe traffic, 2-row 67, 8-row 48; tools/e2e_sweep.sh)
+    n_sub = 1
+    if kind in ("rglru", "s6") and not w.get("seqpar"):
+        n_sub = next((k for k in (8, 4, 2) if Bs % k == 0), 1)
+        while Bs // n_sub > int(os.environ.get("LRX_E2E_ROWS", "1")) and n_sub < Bs:
+            n_sub *= 2
     sb = Bs // n_sub
     streams = [torch.cuda.Stream(device) for _ in range(n_sub)]
 
@@ -543,7 +564,7 @@ def run_e2e(args, w, prob, device):
         d2h = step()
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3 / reps
-    return {"ms": ms, "batch": Bs, "h2d": h2d, "d2h": d2h, "elems": Bs * L * H * N, "sub_batches": n_sub}
+    return {"ms": ms, "batch": Bs, "L": L, "h2d": h2d, "d2h": d2h, "elems": Bs * L * H * N, "sub_batches": n_sub}
 
 
 # ---------------------------------------------------------------------------
@@ -668,7 +689,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="lrx", choices=["lrx", "reference"])
-    ap.add_argument("--e2e-batch", type=int, default=8)
+    ap.add_argument("--e2e-batch", type=int, default=0, help="e2e batch rows per rank (0 = the whole per-rank batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
                     help="launch every kernel from the host instead of replaying the captured step")
@@ -747,9 +768,9 @@ def main():
     e = r["e2e"]
     e2e = {"value": e["elems"] * world / (e["ms"] * 1e-3) / 1e9, "unit": "Gelem/s",
            "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"],
-           "sample": f"batch slice B={e['batch']} per rank through paper_2602_08810_b200.ops / layer API, "
-                     f"pinned host buffers, {e['sub_batches']} overlapped sub-batches; host wall clock incl. "
-                     f"H2D + kernels + D2H", "ms_per_step": e["ms"]}
+           "sample": f"B={e['batch']} of {r['B_rank']} per rank (L={e['L']}) through paper_2602_08810_b200.ops / "
+                     f"layer API, pinned host buffers, {e['sub_batches']} overlapped sub-batches; host wall clock "
+                     f"incl. H2D + kernels + D2H", "ms_per_step": e["ms"]}
     line = {"metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": {"f32": "f32", "bf16": "bf16 io / f32 accum"}[w["dtype"]],
