@@ -868,15 +868,11 @@ class S5(_MIMOBase):
     def _coef_grads(self, ga, gsc, extra, deltas):
         lam, delta, d_arg = extra["lam"], extra["delta"], extra["d_arg"]
         ga, gsc = ga.to(torch.complex128), gsc.to(torch.complex128)
+        # constant steps (per-step deltas accumulate these partials in lrx_mimo_bwd_ps)
         dal, dad, dsl, dsd = scheme_partials(self.discretization, lam, d_arg, extra["abar"], extra["scale"])
-        if deltas is None:
-            glam = dal.conj() * ga + dsl.conj() * gsc
-            gdel = (dad.conj() * ga).real + (dsd.conj() * gsc).real
-            glog_delta = gdel * delta
-        else:
-            glam = (dal.conj() * ga + dsl.conj() * gsc).sum((0, 1))
-            gdeff = (dad.conj() * ga).real + (dsd.conj() * gsc).real
-            glog_delta = torch.einsum("blp,bl->p", gdeff, deltas.double()) * delta
+        glam = dal.conj() * ga + dsl.conj() * gsc
+        gdel = (dad.conj() * ga).real + (dsd.conj() * gsc).real
+        glog_delta = gdel * delta
         return {"lambda_re_log": -torch.exp(self.lambda_re_log.double()) * glam.real,
                 "lambda_im": glam.imag.contiguous(), "log_delta": glog_delta}
 
