@@ -506,7 +506,7 @@ def run_e2e(args, w, prob, device):
     # sub-batches pipeline the PCIe copies: H2D of sub-batch i+1 and D2H of i
     # run on the two copy engines while i computes; the step approaches
     # max(H2D, D2H) + one sub-batch's share
-    # one-row sub-batches on their own streams: the finest overlap of the two copy engines with the
+    # one-row sub-batches: the finest overlap of the two copy engines with the
     # kernels (measured C4 full batch: 1-row 85 GB/s of PCIe traffic, 2-row 67, 8-row 48; tools/e2e_sweep.sh)
     n_sub = 1
     if kind in ("rglru", "s6") and not w.get("seqpar"):
@@ -514,7 +514,11 @@ def run_e2e(args, w, prob, device):
         while Bs // n_sub > int(os.environ.get("LRX_E2E_ROWS", "1")) and n_sub < Bs:
             n_sub *= 2
     sb = Bs // n_sub
-    streams = [torch.cuda.Stream(device) for _ in range(n_sub)]
+    # sub-batches round-robin over a few streams: consecutive sub-batches still overlap, and each
+    # stream's caching-allocator pool is reused by its next sub-batch instead of growing per stream
+    # (tools/e2e_streams.sh: 4 streams vs one per sub-batch: rglru_layer 1.6 -> 5.4 Gelem/s, s6_layer 163 -> 174)
+    n_streams = min(n_sub, int(os.environ.get("LRX_E2E_STREAMS", "4")))
+    streams = [torch.cuda.Stream(device) for _ in range(n_streams)]
 
     def compute(d):
         if w.get("layer"):
@@ -545,8 +549,8 @@ def run_e2e(args, w, prob, device):
 
     def step():
         d2h = 0
-        for i, st in enumerate(streams):
-            with torch.cuda.stream(st):
+        for i in range(n_sub):
+            with torch.cuda.stream(streams[i % n_streams]):
                 d = {n: t[i * sb:(i + 1) * sb].to(device, non_blocking=True) for n, t in host.items()}
                 outs = compute(d)
                 if outs_host[i] is None:
@@ -564,7 +568,7 @@ def run_e2e(args, w, prob, device):
         d2h = step()
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3 / reps
-    return {"ms": ms, "batch": Bs, "L": L, "h2d": h2d, "d2h": d2h, "elems": Bs * L * H * N, "sub_batches": n_sub}
+    return {"ms": ms, "batch": Bs, "L": L, "h2d": h2d, "d2h": d2h, "elems": Bs * L * H * N, "sub_batches": n_sub, "streams": n_streams}
 
 
 # ---------------------------------------------------------------------------
@@ -769,7 +773,7 @@ def main():
     e2e = {"value": e["elems"] * world / (e["ms"] * 1e-3) / 1e9, "unit": "Gelem/s",
            "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"],
            "sample": f"B={e['batch']} of {r['B_rank']} per rank (L={e['L']}) through paper_2602_08810_b200.ops / "
-                     f"layer API, pinned host buffers, {e['sub_batches']} overlapped sub-batches; host wall clock "
+                     f"layer API, pinned host buffers, {e['sub_batches']} sub-batches overlapped on {e['streams']} streams; host wall clock "
                      f"incl. H2D + kernels + D2H", "ms_per_step": e["ms"]}
     line = {"metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "strong",
