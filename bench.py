@@ -271,7 +271,7 @@ def build_problem(w, B, device, L=None, group=None):
         st = B * L * N * c
         prob["bytes"] = {"fwd": 2 * per, "bwd": 3 * per}  # fused minimum: u,y / u,gy,gu
         prob["bytes_scan"] = {"fwd": 2 * st, "bwd": 4 * st}
-        T_, P2 = B * L, 2 * (N if kind == "lru" else N // 2)
+        T_, P2 = B * L, 2 * layer._P  # real width of the interleaved complex state (s5: d_state = 2N, P = N)
         if layer._tc(H, T_) and layer._tc(P2, T_):
             # dominant kernel: the skip-fused output projection y = OUT Re(C x) + D u on tcgen05 (3xTF32);
             # achieved = issued TF32 tensor FLOP/s (3 MMAs per fp32 product)

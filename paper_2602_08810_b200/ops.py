@@ -273,6 +273,11 @@ def gemm_f32(A, Bt, Bt_lo=None, Cin=None, colscale=None, alpha=1.0, beta=0.0, ou
     (K % 4 == 0); act: ACT_NONE / ACT_SOFTPLUS / ACT_SIGMOID."""
     M, K = A.shape
     N = Bt.shape[0]
+    if Bt.shape[1] != K or (Bt_lo is not None and Bt_lo.shape != Bt.shape):
+        raise ValueError(f"gemm_f32: A {tuple(A.shape)} and Bt {tuple(Bt.shape)} disagree on K")
+    for name, t in (("Cin", Cin), ("out", out)):
+        if t is not None and tuple(t.shape) != (M, N):
+            raise ValueError(f"gemm_f32: {name} {tuple(t.shape)} is not [M, N] = [{M}, {N}]")
     if Bt_lo is None:
         Bt_lo = tf32_lo(Bt)
     C = out if out is not None else torch.empty((M, N), dtype=torch.float32, device=A.device)
@@ -286,6 +291,8 @@ def gemm_f32_tn(A, B, alpha=1.0):
     tcgen05 3xTF32 partials, summed in a fixed order."""
     K, M = A.shape
     N = B.shape[1]
+    if B.shape[0] != K:
+        raise ValueError(f"gemm_f32_tn: A {tuple(A.shape)} and B {tuple(B.shape)} disagree on K")
     ks = _lib.i64()
     _lib.check(_lib.lib().lrx_gemm_f32_tn_splits(M, N, K, _lib.ref(ks)))
     part = torch.empty((ks.value, M * N), dtype=torch.float32, device=A.device)
@@ -318,6 +325,11 @@ def gemm_bf16(A, Bt, bias=None, act=ACT_NONE, Cin=None, alpha=1.0, beta=0.0, out
     N % 4 == 0)."""
     M, K = A.shape
     N = Bt.shape[0]
+    if Bt.shape[1] != K:
+        raise ValueError(f"gemm_bf16: A {tuple(A.shape)} and Bt {tuple(Bt.shape)} disagree on K")
+    for name, t in (("Cin", Cin), ("out", out)):
+        if t is not None and tuple(t.shape) != (M, N):
+            raise ValueError(f"gemm_bf16: {name} {tuple(t.shape)} is not [M, N] = [{M}, {N}]")
     C = out if out is not None else torch.empty((M, N), dtype=out_dtype, device=A.device)
     _lib.check(_lib.lib().lrx_gemm_bf16(_lib.ptr(A), _lib.ptr(Bt), _lib.ptr(C), _lib.ptr(Cin), _lib.ptr(bias), M, N,
                                         K, alpha, beta, act, int(C.dtype == torch.bfloat16), _lib.stream()))
