@@ -61,3 +61,19 @@ def test_shape_errors_are_reported_before_launch():
     rc = lib.lrx_scan_fwd(_lib.F32, 0, None, None, None, None, 0, 4, None, 0, None)
     assert rc == _lib.ERR_SHAPE
     assert b"length" in lib.lrx_last_error()
+
+
+def test_gemm_wrappers_reject_mismatched_operands():
+    import pytest
+    import torch
+
+    from paper_2602_08810_b200 import ops
+    a, bt = torch.zeros(8, 16), torch.zeros(4, 12)
+    with pytest.raises(ValueError, match="disagree on K"):
+        ops.gemm_f32(a, bt)
+    with pytest.raises(ValueError, match="disagree on K"):
+        ops.gemm_bf16(a.bfloat16(), bt.bfloat16())
+    with pytest.raises(ValueError, match="disagree on K"):
+        ops.gemm_f32_tn(a, torch.zeros(7, 4))
+    with pytest.raises(ValueError, match="not \\[M, N\\]"):
+        ops.gemm_f32(a, torch.zeros(4, 16), Cin=torch.zeros(8, 5))
