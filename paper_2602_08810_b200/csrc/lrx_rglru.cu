@@ -1348,7 +1348,7 @@ static int env_int(const char* name, int dflt) {
 }
 
 template <typename IO>
-static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p) {
+static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p, int pf_cap = 16) {
     constexpr int CK = Tile<IO>::T;
     if ((W * (int64_t)sizeof(IO)) % 16) return false;
     const int sms = sm_count();
@@ -1363,7 +1363,8 @@ static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p) {
     // 2-stage ring stream best (measured C4 fwd 7.9 -> 7.0 ms, bwd 14.1 -> 13.3);
     // half as many lanes (~17) still prefer the short tile with the deep ring
     const bool pair32 = sizeof(IO) == 4 && LW >= 64 && !getenv("LRX_RGLRU_SCALAR");
-    const int smax = env_int(dir, env_int("LRX_RGLRU_STAGES", pair32 && warps >= 24 ? 2 : 6));
+    // a shallower ring also wins at half that (B = 32 of an 2-GPU job: fwd 4.21 -> 3.58 ms with 3 stages)
+    const int smax = env_int(dir, env_int("LRX_RGLRU_STAGES", pair32 ? (warps >= 24 ? 2 : 3) : 6));
     // ring depth that fits for (PF, n_seg); 0 = does not fit
     auto stages = [&](int PF, int64_t n_seg) -> int {
         const int64_t per_sm = cdiv(n_blk * n_seg, (int64_t)sms);
@@ -1385,15 +1386,18 @@ static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p) {
             PF = pf;
             // bf16 streams half the bytes per element: the walk is issue-bound, so
             // it takes twice the in-flight work (C4 bf16 fwd: PF 4 6.9 ms, PF 8 5.7 ms)
-            if (warps * n_seg * pf >= (sizeof(IO) == 2 ? 2 * kWork : kWork)) break;
+            // the lane-pair forward reaches it with half the tile (B = 32 / 16 / 8 of an
+            // N-GPU job: PF 4 / 8 / 8, measured tools/rg_plan_grid.py)
+            if (warps * n_seg * pf >= (sizeof(IO) == 2 ? 2 * kWork : kWork) / (pair32 && narr == 3 ? 2 : 1)) break;
         }
         if (PF) break;
     }
     if (!PF) return false;
-    if (pair32 && warps >= 12 && n_seg == 1) PF = 2;
+    if (pair32 && warps >= 24 && n_seg == 1) PF = 2;
     const char* epf = getenv(narr == 3 ? "LRX_RGLRU_FWD_PF" : "LRX_RGLRU_BWD_PF");
     if (!epf) epf = getenv("LRX_RGLRU_PF");
     if (epf) PF = std::min(MaxPF<IO>::T, atoi(epf) >= 16 ? 16 : atoi(epf) >= 8 ? 8 : atoi(epf) >= 4 ? 4 : 2);
+    PF = std::min(PF, std::max(2, pf_cap));  // the caller's residency cap (pair_resident)
     if (const char* e = getenv("LRX_RGLRU_SEGS"))
         n_seg = std::max<int64_t>(1, std::min<int64_t>({(int64_t)atoi(e), 64, std::max<int64_t>(1, L / 64)}));
     // segments start on a tile and on a checkpoint boundary
@@ -1629,12 +1633,57 @@ static int colsums(C* parts, int64_t rows, int64_t B, int64_t W, void* gla, void
     return launched("lrx_rglru_bwd/colsum", 3);
 }
 
+// Every CTA of a TMA pass walks its whole segment, so the grid must be
+// resident in one wave.  The lane-pair kernels at PF >= 8 are register-bound
+// to 512 / LW CTAs per SM (B = 32 of a 2-GPU job needs 5 at LW = 128: PF 8
+// ran as 1.1 waves, bwd 6.8 -> 8.8 ms), so the plan halves PF until the
+// occupancy query says the grid fits.
+template <typename IO, int LW>
+static bool pair_resident_lw(const TmaPlan& pl, int narr) {
+    const void* k = nullptr;
+    if (narr == 3) {
+        switch (pl.PF) {
+            case 16: k = (const void*)fwd2_kernel<IO, LW, 16, false>; break;
+            case 8: k = (const void*)fwd2_kernel<IO, LW, 8, false>; break;
+            case 2: k = (const void*)fwd2_kernel<IO, LW, 2, false>; break;
+            default: k = (const void*)fwd2_kernel<IO, LW, 4, false>; break;
+        }
+    } else {
+        switch (pl.PF) {
+            case 16: k = (const void*)bwd_rev2_kernel<IO, LW, 16>; break;
+            case 8: k = (const void*)bwd_rev2_kernel<IO, LW, 8>; break;
+            case 2: k = (const void*)bwd_rev2_kernel<IO, LW, 2>; break;
+            default: k = (const void*)bwd_rev2_kernel<IO, LW, 4>; break;
+        }
+    }
+    int occ = 0;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, LW / 2, pl.smem) != cudaSuccess)
+        return true;  // no answer: keep the plan (the launch reports real errors)
+    return (int64_t)occ * sm_count() >= (int64_t)pl.n_blk * pl.n_seg;
+}
+
+template <typename IO, typename C>
+static bool pair_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* pl) {
+    if (!tma_plan<IO>(B, L, W, narr, pl)) return false;
+    if constexpr (std::is_same<C, float>::value && !std::is_same<IO, double>::value) {
+        if (pl->LW < 64 || getenv("LRX_RGLRU_SCALAR")) return true;
+        while (pl->PF > 2 &&
+               !(pl->LW == 128 ? pair_resident_lw<IO, 128>(*pl, narr) : pair_resident_lw<IO, 64>(*pl, narr))) {
+            TmaPlan q;
+            if (!tma_plan<IO>(B, L, W, narr, &q, pl->PF / 2) || q.PF >= pl->PF) break;
+            *pl = q;
+        }
+    }
+    return true;
+}
+
 template <typename IO, typename C>
 static int fwd_t(const void* u, const void* qr, const void* qi, const void* lam, const void* br, const void* bi,
                  void* y, void* ckpt, int64_t B, int64_t L, int64_t W, void* w, size_t wb, cudaStream_t st) {
     const int mode = mode_env();
     TmaPlan pl;
-    if ((mode == 0 || mode == 1 || mode == 5) && B * L < (1ll << 31) && tma_plan<IO>(B, L, W, 3, &pl)) {
+    if ((mode == 0 || mode == 1 || mode == 5) && B * L < (1ll << 31) && pair_plan<IO, C>(B, L, W, 3, &pl)) {
         CUtensorMap m[3];
         const void* src[3] = {u, qr, qi};
         bool ok = true;
@@ -1680,7 +1729,7 @@ static int bwd_t(const void* u, const void* qr, const void* qi, const void* lam,
     TmaPlan pl, pa;
     // default: the reverse-reconstruction walk (7 streams + 1/8 of anchors,
     // gates once per element); needs the forward's checkpoints
-    if (ckpt && (mode == 0 || mode == 5) && B * L < (1ll << 31) && tma_plan<IO>(B, L, W, 4, &pl) &&
+    if (ckpt && (mode == 0 || mode == 5) && B * L < (1ll << 31) && pair_plan<IO, C>(B, L, W, 4, &pl) &&
         agg_plan<IO>(pl, B, L, W, &pa)) {
         CUtensorMap m[4];
         const void* src[4] = {u, qr, qi, gy};
