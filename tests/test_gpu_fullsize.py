@@ -90,6 +90,31 @@ def test_rglru_c4_full_size(lrx):
     assert float((y12 - y).abs().max()) / float(y.abs().max()) < 1e-5
 
 
+@pytest.mark.parametrize("B", [32, 16, 8, 4])
+def test_rglru_per_rank_shares_match_oracle(lrx, B):
+    """The per-rank batch shares of an N-GPU C4 job (B = 64/N, W = 2560):
+    each lane count takes its own plan (B = 32: tile height 4 capped by the
+    occupancy check, 3-stage ring; B = 16: 8 / 16; B <= 8: time segments).
+    Oracle on 4 channels x every row at L = 2048 (plans depend on the lane
+    count, not on L, except the segment count, capped at L / 256 = 8)."""
+    from paper_2602_08810_b200 import ops
+    L, W = 2048, 2560
+    layer = lrx.make_layer("rglru", W, dtype="f32", seed=3)
+    p = (layer.lambda_param, layer.b_r, layer.b_i)
+    u, qr, qi, gy = (randn((B, L, W), s) for s in (11, 12, 13, 14))
+    y, ck = ops.rglru_scan_fwd(u, qr, qi, *p)
+    r = ops.rglru_scan_bwd(u, qr, qi, *p, ck, gy, y=y)
+    cols = torch.tensor([0, 1281, W - 2, int(torch.argmin(layer.lambda_param))], device="cuda")
+    sl = lambda t: t.index_select(2, cols).double().cpu().numpy()  # noqa: E731
+    pn = [t.index_select(0, cols).double().cpu().numpy() for t in p]
+    ry, rg = port.rglru_scan(sl(u), sl(qr), sl(qi), *pn, sl(gy))
+    assert rel(y.index_select(2, cols), ry) < 1e-4
+    for k in ("gu_local", "gqr", "gqi"):
+        assert rel(r[k].index_select(2, cols), rg[k]) < 1e-4, k
+    for k in ("gla", "gb_r", "gb_i"):
+        assert rel(r[k].index_select(0, cols), rg[k]) < 1e-4, k
+
+
 def test_rglru_c4_bf16_full_size(lrx):
     """C4 shape with bf16 I/O (the optional dtype): the backward reconstructs
     the fp32 states anchored on the forward's checkpoints (y is rounded, so it
