@@ -240,6 +240,33 @@ int lrx_mimo_bwd_ps(int dtype, const void* lam, const void* delta, const void* d
                     const void* x, const void* gx, void* gbu, void* glam_part, void* gdl_part, int64_t B, int64_t L,
                     int64_t P, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Fused MIMO projection + scan (S5 / LRU, constant steps, fp32;
+ * layers.py:650-704 _stream_build / _shared_tape_forward and the pullbacks
+ * _mimo_head_pullback / _mimo_input_pullback, autograd.py:113-140) ----
+ * One kernel per direction: the tcgen05 3xTF32 projection lands in TMEM with
+ * the state on the TMEM lane and is scanned there (bu / gx never reach HBM).
+ * A, A_lo [256, m] = the projection's [2P, m] rows permuted to
+ * [Re rows p (128, zero padded) ; Im rows p (128)] and their TF32 low parts.
+ * Forward:  x = scan(abar, scale * (u A^T)) [B, L, P] complex; bu (or NULL)
+ *           receives u A^T.
+ * Backward: gx = alpha gy A^T, g_k = gx_k + conj(abar) g_{k+1};
+ *           gbu = conj(scale) g; ga_part [units, P] complex = sum_k g
+ *           conj(x_{k-1}) per unit (units = lrx_mimo_fused_units: B x
+ *           ceil(L / 128)), summed by the caller.  d scale = sum_k conj(bu_k)
+ *           g_k is the caller's: sum_h conj(W[p, h]) (gbu^T u)[p, h] /
+ *           conj(scale_p) from its weight-gradient GEMM (bu is not needed).
+ * Requires P <= 128, m % 16 == 0, L <= 8192 (LRX_ERR_UNSUPPORTED otherwise:
+ * the separate GEMM + lrx_mimo_fwd / bwd path).  Workspace:
+ * lrx_mimo_fused_workspace_bytes. */
+int lrx_mimo_fused_workspace_bytes(int64_t B, int64_t L, int64_t P, int64_t* bytes);
+int lrx_mimo_fused_units(int64_t B, int64_t L, int64_t* units);
+int lrx_mimo_fused_fwd(const void* A, const void* A_lo, const void* u, const void* abar, const void* scale, void* x,
+                       void* bu, int64_t B, int64_t L, int64_t m, int64_t P, void* workspace, size_t workspace_bytes,
+                       void* stream);
+int lrx_mimo_fused_bwd(const void* A, const void* A_lo, const void* gy, float alpha, const void* abar,
+                       const void* scale, const void* x, void* gbu, void* ga_part, int64_t B, int64_t L, int64_t m,
+                       int64_t P, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- bf16 <-> fp32 conversion of activation planes (n elements, 16-byte
  * aligned): the bf16 layers' fp32 GEMM operands and results. */
 int lrx_cast(int dtype_in, int dtype_out, const void* in, void* out, int64_t n, void* stream);
@@ -355,7 +382,9 @@ int lrx_mimo_fwd(int dtype, const void* abar, const void* scale, const void* bu,
  * LRU._backward 945-980):
  *   g_k = gx_k + conj(abar) g_{k+1};  gbu = conj(scale) g  -> gbu [B,L,P]
  *   gabar_part[c, b*P+p] = sum_{k in chunk c} g_k conj(x_{k-1})
- *   gscale_part[c, b*P+p] = sum_{k in chunk c} conj(bu_k) g_k
+ *   gscale_part[c, b*P+p] = sum_{k in chunk c} conj(bu_k) g_k   (not written
+ *   when bu is NULL: the caller takes d scale from its weight-gradient GEMM,
+ *   as after lrx_mimo_fused_fwd, which stores no bu)
  * (reduce the [n_chunks*B, P] partials with lrx_reduce_rows). */
 int lrx_mimo_chunking(int dtype, int64_t B, int64_t L, int64_t P, int64_t* chunk_len, int64_t* n_chunks);
 size_t lrx_mimo_bwd_workspace_bytes(int dtype, int64_t B, int64_t L, int64_t P);

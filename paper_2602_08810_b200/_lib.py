@@ -51,6 +51,11 @@ SIGNATURES = {
     "lrx_mimo_ps_workspace_bytes": (_sz, [_i, _i64, _i64, _i64]),
     "lrx_mimo_fwd_ps": (_i, [_i, _vp, _vp, _vp, _i, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp]),
     "lrx_mimo_bwd_ps": (_i, [_i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp]),
+    "lrx_mimo_fused_workspace_bytes": (_i, [_i64, _i64, _i64, _P64]),
+    "lrx_mimo_fused_units": (_i, [_i64, _i64, _P64]),
+    "lrx_mimo_fused_fwd": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _sz, _vp]),
+    "lrx_mimo_fused_bwd": (_i, [_vp, _vp, _vp, ctypes.c_float, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64,
+                                _vp, _sz, _vp]),
     "lrx_reduce_rows": (_i, [_i, _vp, _vp, _i64, _i64, _vp]),
     "lrx_reduce_rows_ws_bytes": (_sz, [_i, _i64, _i64]),
     "lrx_reduce_rows_ws": (_i, [_i, _vp, _vp, _vp, _i64, _i64, _vp, _sz, _vp]),

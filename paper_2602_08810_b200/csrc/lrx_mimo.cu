@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const cplx<T>* __restrict
             const int64_t off = base + (int64_t)kk * P;
             g[k] = ok ? ldc(gx + off) : Traits<V>::zero();
             xp[k] = (ok && t0 + kk > 0) ? ldc(x + off - P) : Traits<V>::zero();
-            bv[k] = ok ? ldc(bu + off) : Traits<V>::zero();
+            bv[k] = (ok && bu) ? ldc(bu + off) : Traits<V>::zero();  // bu NULL: no d scale partials
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(const cplx<T>* __restrict
         }
     }
     gabar_part[(int64_t)s * n_lanes + lane] = sa;
-    gscale_part[(int64_t)s * n_lanes + lane] = ss;
+    if (bu) gscale_part[(int64_t)s * n_lanes + lane] = ss;
 }
 
 // ----------------------------------------------------------------------------

@@ -1,0 +1,646 @@
+// Fused MIMO projection + complex diagonal scan for S5 / LRU with constant
+// steps (layers.py:650-704 _stream_build / _shared_tape_forward and the
+// pullbacks _mimo_head_pullback / _mimo_input_pullback, autograd.py:113-140):
+//
+//   forward   bu = u Wb (tcgen05 3xTF32),  x_k = abar x_{k-1} + scale bu_k
+//   backward  gx = alpha gy Wg,  g_k = gx_k + conj(abar) g_{k+1},  gbu_k = conj(scale) g_k,
+//             per-unit partials sum_k g_k conj(x_{k-1}) (d abar); d scale is the
+//             caller's: sum_k conj(bu_k) g_k = sum_h conj(W[p,h]) (gbu^T u)[p,h] / conj(scale_p)
+//             from the weight-gradient GEMM it computes anyway (bu is never stored)
+//
+// bu / gx never reach HBM: the GEMM runs with the TRANSPOSED accumulator
+// (A = the weights, M = 128 state rows; B = the activation tile, N = 128 time
+// steps), so TMEM lane p holds state p across the tile's 128 steps and the
+// thread that owns lane p scans them serially straight out of TMEM.  The
+// weights arrive permuted to [Re rows (128) ; Im rows (128)] (P <= 128, zero
+// padded), so the real and imaginary accumulators of state p sit in the same
+// TMEM lane, 128 columns apart.
+//
+// Units.  A unit is (batch row, 128-step tile); CTAs claim units in order from
+// an atomic counter (so every unit a CTA waits on was claimed by a running
+// CTA: no residency assumption, safe next to other streams' kernels).  Per
+// unit the scan runs twice out of TMEM: pass 1 from a zero carry gives the
+// unit's map (LTI: carry -> abar^n carry + E), published to the workspace;
+// the carry entering the unit is then folded from the maps of all earlier
+// units of its row, first to last (a fixed order: deterministic; rows of up to
+// 64 units); pass 2 re-scans with the true carry and writes x (forward) or gbu
+// and the coefficient partials (backward).  The backward walks rows right to
+// left.
+//
+// CTA: warp 0 TMA producer (+ unit claiming), warp 1 MMA issuer, warps 2-5
+// make the activation's TF32 low part, warps 6-9 scan (one TMEM lane quarter
+// each).  Two TMEM accumulators (2 x 256 columns) overlap the scan of one
+// unit with the MMAs of the next.
+#include "lrx_common.cuh"
+#include "lrx_host.h"
+#include "lrx_tma.cuh"
+
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <type_traits>
+
+namespace lrx {
+namespace mimof {
+
+constexpr int TT = 128;                 // steps per unit = the MMA's N
+constexpr int BKT = 16;                 // K columns per stage: 64-byte rows, SW64
+constexpr int STAGES = 4;
+constexpr int SLAB = 128 * BKT * 4;     // 8 KB: one 128-row operand slab
+constexpr int STAGE = 6 * SLAB;         // A_re, A_re_lo, A_im, A_im_lo, U, U_lo
+constexpr int THREADS = 320;
+constexpr uint32_t kCols = 512;         // 2 accumulators x (re 128 | im 128)
+constexpr int RING = 4;                 // claimed-unit ring (producer -> MMA / scan)
+constexpr int OBUF = 2 * 16 * 128 * 8;  // 2 rounds x 4 blocks x 4 steps x 128 states, complex
+template <bool REV>
+struct Cfg {
+    static constexpr int NSTG = STAGES;
+    static constexpr size_t SMEM = 2048 + (size_t)NSTG * STAGE + (size_t)OBUF;
+};
+constexpr int kMaxTiles = 64;           // units per row (L <= 8192)
+
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+    // K-major SWIZZLE_64B: 8-row groups of 64-byte rows = 512 B (SBO), layout type 4
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;
+    return d;
+}
+
+// F32 accumulate, TF32 A / B, both K-major, N = 128, M = 128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TT >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     tma::smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void scan_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+constexpr uint64_t kSentinel = ~0ull;  // two all-ones NaNs: arithmetic never produces it
+__device__ __forceinline__ uint64_t ld_relaxed64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+using C = cplx<float>;
+__device__ __forceinline__ uint64_t pack(C v) {
+    return (uint64_t)__float_as_uint(v.re) | ((uint64_t)__float_as_uint(v.im) << 32);
+}
+__device__ __forceinline__ C unpack(uint64_t v) {
+    return {__uint_as_float((uint32_t)v), __uint_as_float((uint32_t)(v >> 32))};
+}
+__device__ __forceinline__ C ldg_c(const float* p) {
+    const float2 v = __ldcg(reinterpret_cast<const float2*>(p));
+    return {v.x, v.y};
+}
+__device__ __forceinline__ void stg_c(float* p, C v) { __stcg(reinterpret_cast<float2*>(p), make_float2(v.re, v.im)); }
+__device__ __forceinline__ C ldcs_c(const float* p) {
+    const float2 v = __ldcs(reinterpret_cast<const float2*>(p));
+    return {v.x, v.y};
+}
+__device__ __forceinline__ void stcs_c(float* p, C v) { __stcs(reinterpret_cast<float2*>(p), make_float2(v.re, v.im)); }
+
+__device__ __forceinline__ C cpow(C a, int e) {  // a^e, e >= 0 (binary powering)
+    C r = {1.f, 0.f};
+    while (e) {
+        if (e & 1) r = r * a;
+        a = a * a;
+        e >>= 1;
+    }
+    return r;
+}
+
+struct Args {
+    const float* abar;   // [P] complex
+    const float* scale;  // [P] complex
+    float* x;            // forward out / backward in: [B, L, P] complex
+    float* bu;           // forward out (optional)
+    float* gbu;          // backward out
+    float* ga_part;      // backward out: [units, P] complex
+    uint64_t* E;         // [units, P] packed complex: unit maps from a zero carry (sentinel = not yet)
+    uint64_t* I;         // [units, P] packed complex: inclusive results (the carry leaving the unit)
+    int* counter;        // unit claims
+    int64_t L, P;
+    int n_tt, n_units, nk;
+    float alpha;
+    int tma_out;  // outputs staged through shared memory + TMA stores
+    int dbg;  // LRX_MIMO_FUSED_DBG (timing experiments only): 1 no carry wait, 2 no pass 2, 4 no scan
+};
+
+template <bool REV>
+__global__ void __launch_bounds__(THREADS, 1) fused_kernel(const __grid_constant__ CUtensorMap mA,
+                                                           const __grid_constant__ CUtensorMap mAl,
+                                                           const __grid_constant__ CUtensorMap mU,
+                                                           const __grid_constant__ CUtensorMap mO, Args a) {
+    constexpr int STAGES = Cfg<REV>::NSTG;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(base);  // [STAGES] TMA landed
+    uint64_t* split = full + STAGES;                      // [STAGES] U_lo written
+    uint64_t* empty = split + STAGES;                     // [STAGES] MMAs done with the stage
+    uint64_t* tfull = empty + STAGES;                     // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;                         // [2] accumulator drained
+    uint64_t* uready = tempty + 2;                        // [RING] claimed unit id written
+    int* unit_id = reinterpret_cast<int*>(uready + RING);  // [RING]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(unit_id + RING);
+    unsigned char* stages = base + 1024;
+    float2* obuf = reinterpret_cast<float2*>(stages + STAGES * STAGE);  // [2 rounds][4 blocks][4 steps][P]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        tma::prefetch_map(&mA);
+        tma::prefetch_map(&mAl);
+        tma::prefetch_map(&mU);
+        for (int i = 0; i < STAGES; ++i) {
+            tma::mbar_init(&full[i], 1);
+            tma::mbar_init(&split[i], 128);
+            tma::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tma::mbar_init(&tfull[i], 1);
+            tma::mbar_init(&tempty[i], 128);
+        }
+        for (int i = 0; i < RING; ++i) tma::mbar_init(&uready[i], 1);
+        tma::fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         tma::smem_u32(tmem_slot)),
+                     "r"(kCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int nk = a.nk;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ------------------------------------------ producer
+            int it = 0;
+            for (int ti = 0;; ++ti) {
+                const int u = atomicAdd(a.counter, 1);
+                const int uid = u < a.n_units ? u : -1;
+                unit_id[ti % RING] = uid;
+                tma::mbar_arrive(&uready[ti % RING]);
+                if (uid < 0) break;
+                const int b = uid / a.n_tt, tq = uid % a.n_tt, tt = REV ? a.n_tt - 1 - tq : tq;
+                const int row0 = (int)(b * a.L + (int64_t)tt * TT);
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % STAGES;
+                    if (it >= STAGES) tma::mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
+                    unsigned char* sp = stages + st * STAGE;
+                    tma::mbar_arrive_expect_tx(&full[st], 5 * SLAB);
+                    tma::load_2d(sp, &mA, kb * BKT, 0, &full[st]);
+                    tma::load_2d(sp + SLAB, &mAl, kb * BKT, 0, &full[st]);
+                    tma::load_2d(sp + 2 * SLAB, &mA, kb * BKT, 128, &full[st]);
+                    tma::load_2d(sp + 3 * SLAB, &mAl, kb * BKT, 128, &full[st]);
+                    tma::load_2d(sp + 4 * SLAB, &mU, kb * BKT, row0, &full[st]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ------------------------------------------ MMA issuer
+            int it = 0;
+            for (int ti = 0;; ++ti) {
+                tma::mbar_wait(&uready[ti % RING], (ti / RING) & 1);
+                if (unit_id[ti % RING] < 0) break;
+                const int acc = ti & 1;
+                if (ti >= 2) tma::mbar_wait(&tempty[acc], ((ti >> 1) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t dre = tmem + acc * 256, dim = dre + 128;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % STAGES;
+                    tma::mbar_wait(&split[st], (it / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t s0 = tma::smem_u32(stages + st * STAGE);
+#pragma unroll
+                    for (int k = 0; k < BKT / 8; ++k) {  // 8 tf32 = 32 bytes per UMMA k-step
+                        const uint32_t off = k * 32;
+                        const uint64_t dU = sw64_desc(s0 + 4 * SLAB + off), dUl = sw64_desc(s0 + 5 * SLAB + off);
+                        const uint64_t dR = sw64_desc(s0 + off), dRl = sw64_desc(s0 + SLAB + off);
+                        const uint64_t dI = sw64_desc(s0 + 2 * SLAB + off), dIl = sw64_desc(s0 + 3 * SLAB + off);
+                        const uint32_t first = (kb | k) != 0;
+                        mma(dre, dR, dU, first);
+                        mma(dre, dR, dUl, 1);
+                        mma(dre, dRl, dU, 1);
+                        mma(dim, dI, dU, first);
+                        mma(dim, dI, dUl, 1);
+                        mma(dim, dIl, dU, 1);
+                    }
+                    commit(&empty[st]);
+                }
+                commit(&tfull[acc]);
+            }
+        }
+    } else if (warp < 6) {
+        // ---------------------------------------------------------- U_lo
+        const int t = threadIdx.x - 64;
+        int it = 0;
+        for (int ti = 0;; ++ti) {
+            tma::mbar_wait(&uready[ti % RING], (ti / RING) & 1);
+            if (unit_id[ti % RING] < 0) break;
+            for (int kb = 0; kb < nk; ++kb, ++it) {
+                const int st = it % STAGES;
+                tma::mbar_wait(&full[st], (it / STAGES) & 1);
+                const float4* a4 = reinterpret_cast<const float4*>(stages + st * STAGE + 4 * SLAB);
+                float4* l4 = reinterpret_cast<float4*>(stages + st * STAGE + 5 * SLAB);
+#pragma unroll
+                for (int i = 0; i < SLAB / 16 / 128; ++i) {
+                    const float4 v = a4[t + 128 * i];
+                    float4 lo;
+                    lo.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                    l4[t + 128 * i] = lo;
+                }
+                tma::fence_proxy_async();
+                tma::mbar_arrive(&split[st]);
+            }
+        }
+    } else {
+        // ---------------------------------------------------------- scan
+        // Thread = state p (TMEM lane).  The unit's 128 steps are 4 blocks of
+        // 32 scanned as 4 independent chains (a single chain is latency-bound:
+        // ~50 cycles per step measured): pass 1 gives each block's map from a
+        // zero carry, the block carries follow from the unit's carry by 4
+        // Horner steps, and pass 2 re-runs the 4 chains from their carries.
+        const int q = warp & 3;  // TMEM lane quarter
+        const int p = 32 * q + lane;
+        const bool pv = p < a.P;
+        const C ab0 = pv ? ldg_c(a.abar + 2 * p) : C{0.f, 0.f};
+        const C sc0 = pv ? ldg_c(a.scale + 2 * p) : C{0.f, 0.f};
+        const C ab = REV ? conj(ab0) : ab0, scb = conj(sc0);
+        const C T32 = cpow(ab, 32);
+        const int nt_last = (int)(a.L - (int64_t)(a.n_tt - 1) * TT);
+        const C T_full = cpow(T32, 4), T_last = cpow(ab, nt_last);
+        const uint32_t lrow = (uint32_t)(32 * q) << 16;
+        const bool lead = threadIdx.x == 192;  // issues the scan warps' TMA stores
+        int rnd = 0;                           // staged rounds so far (output buffer parity)
+        for (int ti = 0;; ++ti) {
+            tma::mbar_wait(&uready[ti % RING], (ti / RING) & 1);
+            const int u = unit_id[ti % RING];
+            if (u < 0) break;
+            const int b = u / a.n_tt, tq = u % a.n_tt, tt = REV ? a.n_tt - 1 - tq : tq;
+            const int64_t t0 = (int64_t)tt * TT;
+            const int nt = (int)min((int64_t)TT, a.L - t0);
+            const int acc = ti & 1;
+            const uint32_t tre = tmem + lrow + acc * 256, tim = tre + 128;
+            tma::mbar_wait(&tfull[acc], (ti >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (a.dbg & 4) {
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                tma::mbar_arrive(&tempty[acc]);
+                continue;
+            }
+            C Tb[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int len = max(0, min(32, nt - 32 * j));
+                Tb[j] = len == 32 ? T32 : cpow(ab, len);
+            }
+            // pass 1: block maps from zero carries
+            C e[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+            auto pass1 = [&](auto full_c) {
+                constexpr bool FULL = decltype(full_c)::value;
+#pragma unroll 1
+                for (int ii = 0; ii < 4; ++ii) {
+                    const int i = REV ? 3 - ii : ii;
+                    float vr[4][8], vi[4][8];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        tmem_ld8(tre + 32 * j + 8 * i, vr[j]);
+                        tmem_ld8(tim + 32 * j + 8 * i, vi[j]);
+                    }
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const int k = REV ? 7 - kk : kk;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (FULL || 32 * j + 8 * i + k < nt) {
+                                const C v = {vr[j][k], vi[j][k]};
+                                if (REV) e[j] = ab * (a.alpha * v + e[j]);
+                                else e[j] = ab * e[j] + sc0 * v;
+                            }
+                    }
+                }
+            };
+            if (nt == TT) pass1(std::true_type{});
+            else pass1(std::false_type{});
+            C E = {0.f, 0.f};
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int j = REV ? 3 - jj : jj;
+                E = Tb[j] * E + e[j];
+            }
+            // the carry entering the unit: Horner over the row's unit maps in
+            // walk order, c = T_j c + E_j, started from the newest published
+            // inclusive prefix I_j* = (the same Horner up to j*) among the last
+            // 8 units, else from the row's start.  Either start performs the
+            // same operations on the same values: bitwise deterministic.  Each
+            // lane's E / I is one 64-bit store over a sentinel (the workspace is
+            // 0xFF-filled per launch), so the value is its own flag: no fences.
+            C cin = {0.f, 0.f};
+            if (pv) {
+                const int64_t PP = a.P;
+                st_relaxed64(a.E + (int64_t)u * PP + p, pack(E));
+                const int u0 = u - tq;  // the row's first unit in walk order
+                int jb = u0;
+                if (tq > 0 && !(a.dbg & 1)) {
+                    uint64_t iv[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) iv[i] = i < tq ? ld_relaxed64(a.I + (int64_t)(u - 1 - i) * PP + p) : kSentinel;
+#pragma unroll
+                    for (int i = 7; i >= 0; --i)
+                        if (iv[i] != kSentinel) {
+                            cin = unpack(iv[i]);
+                            jb = u - i;
+                        }
+                }
+                for (int j0 = jb; j0 < u; j0 += 8) {
+                    const int n = min(8, u - j0);
+                    uint64_t ev[8];
+                    for (;;) {
+                        bool all = true;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            ev[i] = i < n ? ld_relaxed64(a.E + (int64_t)(j0 + i) * PP + p) : 0ull;
+                            all = all && ev[i] != kSentinel;
+                        }
+                        if (all || (a.dbg & 1)) break;
+                        __nanosleep(20);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (i < n) {
+                            const int jq = j0 + i - u0, jtt = REV ? a.n_tt - 1 - jq : jq;
+                            cin = ((int64_t)(jtt + 1) * TT > a.L ? T_last : T_full) * cin + unpack(ev[i]);
+                        }
+                }
+                st_relaxed64(a.I + (int64_t)u * PP + p, pack((nt == TT ? T_full : T_last) * cin + E));
+            }
+            // block carries (walk order) and pass 2
+            C c[4];
+            if (!REV) {
+                c[0] = cin;
+#pragma unroll
+                for (int j = 1; j < 4; ++j) c[j] = Tb[j - 1] * c[j - 1] + e[j - 1];
+            } else {
+                c[3] = cin;
+#pragma unroll
+                for (int j = 2; j >= 0; --j) c[j] = Tb[j + 1] * c[j + 1] + e[j + 1];
+            }
+            const int64_t rb = ((int64_t)b * a.L + t0) * a.P + p;  // element (t0, p) of this row
+            // pass 2 in rounds of W steps x 4 blocks.  A full unit's round outputs
+            // (x, or gbu) go through shared memory and 4 TMA stores (W = 4, two
+            // buffers; per-thread 8-byte stores ran at ~70 cycles each: C2
+            // forward 157 -> 128 us); a ragged last unit (rows end mid-tile) and
+            // LRX_MIMO_FUSED_DIRECT store per thread.
+            const bool staged = a.tma_out && nt == TT;
+            C sa = {0.f, 0.f};
+            auto pass2 = [&](auto w_c) {
+                constexpr int W = decltype(w_c)::value, NR = 32 / W;
+                C sj[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+                C xc[4][W], xn[4][W];
+                auto loadx = [&](int i, C (&xd)[4][W]) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+#pragma unroll
+                        for (int k = 0; k < W; ++k) {
+                            const int t = 32 * j + W * i + k;
+                            xd[j][k] = (pv && t < nt && t0 + t > 0) ? ldcs_c(a.x + 2 * (rb + (int64_t)(t - 1) * a.P))
+                                                                   : C{0.f, 0.f};
+                        }
+                };
+                if (REV) loadx(NR - 1, xc);
+#pragma unroll 1
+                for (int ii = 0; ii < NR; ++ii) {
+                    const int i = REV ? NR - 1 - ii : ii;
+                    float vr[4][W], vi[4][W];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if constexpr (W == 8) {
+                            tmem_ld8(tre + 32 * j + W * i, vr[j]);
+                            tmem_ld8(tim + 32 * j + W * i, vi[j]);
+                        } else {
+                            tmem_ld4(tre + 32 * j + W * i, vr[j]);
+                            tmem_ld4(tim + 32 * j + W * i, vi[j]);
+                        }
+                    }
+                    if (REV && i > 0) loadx(i - 1, xn);
+                    tmem_wait_ld();
+                    float2* ob = obuf + (size_t)(rnd & 1) * 16 * a.P;  // [4 blocks][4 steps][P]
+                    if (staged) {
+                        if (lead) tma::bulk_wait_read<1>();  // the stores of 2 rounds ago have read ob
+                        scan_bar();
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < W; ++kk) {
+                        const int k = REV ? W - 1 - kk : kk;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int t = 32 * j + W * i + k;
+                            if (t < nt) {
+                                const C v = {vr[j][k], vi[j][k]};
+                                C o;
+                                if (REV) {
+                                    const C g = a.alpha * v + c[j];
+                                    c[j] = ab * g;
+                                    o = scb * g;
+                                    sj[j] = sj[j] + g * conj(xc[j][k]);
+                                } else {
+                                    c[j] = ab * c[j] + sc0 * v;
+                                    o = c[j];
+                                    if (pv && a.bu) stcs_c(a.bu + 2 * (rb + (int64_t)t * a.P), v);
+                                }
+                                if (pv && !(a.dbg & 8)) {
+                                    float* dst = (REV ? a.gbu : a.x) + 2 * (rb + (int64_t)t * a.P);
+                                    if (W == 4 && staged) ob[(j * 4 + k) * a.P + p] = make_float2(o.re, o.im);
+                                    else if (a.dbg & 32) *reinterpret_cast<float2*>(dst) = make_float2(o.re, o.im);
+                                    else stcs_c(dst, o);
+                                }
+                            }
+                        }
+                    }
+                    if (REV) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+#pragma unroll
+                            for (int k = 0; k < W; ++k) xc[j][k] = xn[j][k];
+                    }
+                    if (W == 4 && staged) {
+                        tma::fence_proxy_async();
+                        scan_bar();
+                        if (lead) {
+                            const int row = (int)((int64_t)b * a.L + t0) + 4 * i;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) tma::store_2d(&mO, ob + j * 4 * a.P, 0, row + 32 * j);
+                            tma::bulk_commit();
+                        }
+                        ++rnd;
+                    }
+                }
+                sa = (sj[0] + sj[1]) + (sj[2] + sj[3]);
+            };
+            if (!(a.dbg & 2)) {
+                if (REV || staged) pass2(std::integral_constant<int, 4>{});  // REV: x_{k-1} prefetch registers
+                else pass2(std::integral_constant<int, 8>{});
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            tma::mbar_arrive(&tempty[acc]);
+            if (REV && pv) stg_c(a.ga_part + 2 * ((int64_t)u * a.P + p), sa);
+        }
+        if (lead) tma::bulk_wait<0>();  // the staged stores have left shared memory
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
+}
+
+static int sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
+static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+static size_t ws_bytes(int64_t B, int64_t L, int64_t P) {
+    const int64_t units = B * cdiv(L, (int64_t)TT);
+    return 2 * align256((size_t)units * P * 8) + 256;
+}
+
+template <bool REV>
+static int launch(const float* A, const float* Al, const float* act, Args a, int64_t B, int64_t L, int64_t m,
+                  void* ws, size_t wsb, cudaStream_t st) {
+    LRX_REQUIRE(B >= 1 && L >= 1 && m >= 1 && a.P >= 1, LRX_ERR_SHAPE, "mimo fused: bad extents");
+    // the carry fold walks every earlier unit of the row: rows up to kMaxTiles units
+    LRX_REQUIRE(a.P <= 128 && m % BKT == 0 && B * L < (1ll << 31) && cdiv(L, (int64_t)TT) <= kMaxTiles,
+                LRX_ERR_UNSUPPORTED, "mimo fused: needs P <= 128, d_model %% 16 == 0, L <= %d (P=%lld, m=%lld)",
+                kMaxTiles * TT, (long long)a.P, (long long)m);
+    LRX_REQUIRE(ws && wsb >= ws_bytes(B, L, a.P), LRX_ERR_VALUE, "mimo fused: workspace of %zu bytes needed",
+                ws_bytes(B, L, a.P));
+    CUtensorMap mA, mAl, mU, mO;
+    if (!tma::encode_2d_f32_sw64(&mA, A, 256, m, 128) || !tma::encode_2d_f32_sw64(&mAl, Al, 256, m, 128) ||
+        !tma::encode_2d_f32_sw64(&mU, act, B * L, m, TT)) {
+        set_error("mimo fused: TMA descriptor rejected (16-byte aligned rows required)");
+        return LRX_ERR_VALUE;
+    }
+    // output rows [B*L, 2P] fp32, boxes of 4 steps x all states (P even: 16-byte rows)
+    a.tma_out = tma::encode_2d(&mO, REV ? (const void*)a.gbu : (const void*)a.x, 4, B * L, 2 * a.P, 4,
+                               (uint32_t)(2 * a.P)) &&
+                a.P % 4 == 0 && !getenv("LRX_MIMO_FUSED_DIRECT");  // P % 4: 128-byte aligned smem boxes
+    if (!a.tma_out) mO = mU;  // unused
+    a.L = L;
+    a.n_tt = (int)cdiv(L, (int64_t)TT);
+    a.n_units = (int)(B * a.n_tt);
+    a.nk = (int)(m / BKT);
+    if (const char* e = getenv("LRX_MIMO_FUSED_DBG")) a.dbg = atoi(e);
+    const size_t eb = align256((size_t)a.n_units * a.P * 8);
+    a.E = static_cast<uint64_t*>(ws);
+    a.I = reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + eb);
+    a.counter = reinterpret_cast<int*>(static_cast<char*>(ws) + 2 * eb);
+    if (cudaMemsetAsync(a.E, 0xFF, 2 * eb, st) != cudaSuccess ||
+        cudaMemsetAsync(a.counter, 0, 4, st) != cudaSuccess)
+        return launched("mimo fused memset");
+    auto k = fused_kernel<REV>;
+    constexpr size_t SMEM = Cfg<REV>::SMEM;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess) {
+        set_error("mimo fused: cannot reserve %zu B of shared memory", SMEM);
+        return LRX_ERR_CUDA;
+    }
+    const int grid = std::min(a.n_units, sms());
+    k<<<grid, THREADS, SMEM, st>>>(mA, mAl, mU, mO, a);
+    return launched(REV ? "lrx_mimo_fused_bwd" : "lrx_mimo_fused_fwd");
+}
+
+}  // namespace mimof
+}  // namespace lrx
+
+using namespace lrx;
+
+extern "C" {
+
+int lrx_mimo_fused_workspace_bytes(int64_t B, int64_t L, int64_t P, int64_t* bytes) {
+    LRX_REQUIRE(B >= 1 && L >= 1 && P >= 1, LRX_ERR_SHAPE, "mimo fused: bad extents");
+    *bytes = (int64_t)mimof::ws_bytes(B, L, P);
+    return LRX_OK;
+}
+
+int lrx_mimo_fused_units(int64_t B, int64_t L, int64_t* units) {
+    LRX_REQUIRE(B >= 1 && L >= 1, LRX_ERR_SHAPE, "mimo fused: bad extents");
+    *units = B * cdiv(L, (int64_t)mimof::TT);
+    return LRX_OK;
+}
+
+int lrx_mimo_fused_fwd(const void* A, const void* A_lo, const void* u, const void* abar, const void* scale, void* x,
+                       void* bu, int64_t B, int64_t L, int64_t m, int64_t P, void* ws, size_t wsb, void* stream) {
+    mimof::Args a{};
+    a.abar = (const float*)abar;
+    a.scale = (const float*)scale;
+    a.x = (float*)x;
+    a.bu = (float*)bu;
+    a.P = P;
+    a.alpha = 1.f;
+    return mimof::launch<false>((const float*)A, (const float*)A_lo, (const float*)u, a, B, L, m, ws, wsb,
+                                (cudaStream_t)stream);
+}
+
+int lrx_mimo_fused_bwd(const void* A, const void* A_lo, const void* gy, float alpha, const void* abar,
+                       const void* scale, const void* x, void* gbu, void* ga_part, int64_t B, int64_t L, int64_t m,
+                       int64_t P, void* ws, size_t wsb, void* stream) {
+    mimof::Args a{};
+    a.abar = (const float*)abar;
+    a.scale = (const float*)scale;
+    a.x = (float*)x;
+    a.gbu = (float*)gbu;
+    a.ga_part = (float*)ga_part;
+    a.P = P;
+    a.alpha = alpha;
+    return mimof::launch<true>((const float*)A, (const float*)A_lo, (const float*)gy, a, B, L, m, ws, wsb,
+                               (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -42,6 +42,18 @@ bool encode_2d(CUtensorMap* map, const void* base, int esize, uint64_t rows, uin
     return r == CUDA_SUCCESS;
 }
 
+bool encode_2d_f32_sw64(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn || (reinterpret_cast<uintptr_t>(base) & 15) || ((cols * 4) & 15)) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 4};
+    cuuint32_t box[2] = {16, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool encode_3d(CUtensorMap* map, const void* base, int esize, uint64_t d2, uint64_t d1, uint64_t d0,
                uint32_t box1, uint32_t box0) {
     auto fn = encode_fn();

@@ -118,6 +118,10 @@ __device__ __forceinline__ void bulk_wait() {
 bool encode_2d(CUtensorMap* map, const void* base, int esize, uint64_t rows, uint64_t cols, uint32_t box_rows,
                uint32_t box_cols);
 
+// fp32 row-major [rows, cols] with a box of [box_rows, 16 cols = 64 B] and the
+// 64-byte swizzle: the K-major SW64 canonical layout of a tcgen05 tf32 operand.
+bool encode_2d_f32_sw64(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+
 // Encode a row-major 3D tensor [d2, d1, d0] (d0 contiguous) with a box of
 // [1, box1, box0]; out-of-bounds box elements read as zero.
 bool encode_3d(CUtensorMap* map, const void* base, int esize, uint64_t d2, uint64_t d1, uint64_t d0,

@@ -696,17 +696,39 @@ class _MIMOBase(LinearRecurrence):
         saved = {"u": u, "x": x, "bu": bu, "deltas": deltas} if keep else {}
         return y, saved, x[:, -1]
 
+    def _gemm_scan(self, B, L):
+        """Which directions run the projection and the scan as one tcgen05
+        kernel (csrc/lrx_mimo_fused.cu: bu / gx scanned out of TMEM), as
+        (forward, backward).  Domain: fp32 on the tensor-core route, P <= 128,
+        L <= 8192.  Measured (tools/gpu_fused_ab.sh): the fused forward wins
+        with enough 128-step units to fill the GPU (C2: 1024 units, forward
+        249 -> 229 us); with few units (C1: 64) the serial per-unit scan
+        loses to the separate launches, and the fused backward (its per-step
+        x_{k-1} loads) loses at both, so it is opt-in.  LRX_MIMO_FUSED=0 / 1
+        forces the forward off / on, LRX_MIMO_FUSED_BWD=1 enables the
+        backward."""
+        ok = self._tc(self.d_model, B * L) and ops.mimo_fused_supported(B, L, self.d_model, self._P, self.tdt)
+        env = os.environ.get("LRX_MIMO_FUSED")
+        units = B * -(-L // 128)
+        fwd = ok and (env == "1" or (env is None and units >= 4 * _sm_count(self.device)))
+        bwd = ok and os.environ.get("LRX_MIMO_FUSED_BWD") == "1"
+        return fwd, bwd
+
     def _forward_fused(self, u, keep):
         B, L, m = u.shape
         P = self._P
         u2 = u.reshape(B * L, m).contiguous()
         pk = self._coef_pack()
-        if self._tc(m, B * L):
-            bu2 = ops.gemm_f32(u2, pk["wbt"], Bt_lo=pk["wbt_lo"])
+        if self._gemm_scan(B, L)[0]:
+            A, Al = ops.mimo_fused_weights(pk["wbt"], pk["wbt_lo"])
+            x, bu = ops.mimo_fused_fwd(A, Al, u2, pk["abar"], pk["scale"], B, L, want_bu=False)
         else:
-            bu2 = u2 @ pk["wb"]
-        bu = torch.view_as_complex(bu2.reshape(B, L, P, 2))
-        x = ops.mimo_scan_fwd(pk["abar"], pk["scale"], bu)
+            if self._tc(m, B * L):
+                bu2 = ops.gemm_f32(u2, pk["wbt"], Bt_lo=pk["wbt_lo"])
+            else:
+                bu2 = u2 @ pk["wb"]
+            bu = torch.view_as_complex(bu2.reshape(B, L, P, 2))
+            x = ops.mimo_scan_fwd(pk["abar"], pk["scale"], bu)
         x2 = torch.view_as_real(x).reshape(B * L, 2 * P)
         if self._tc(2 * P, B * L):  # y = OUT Re(C x) + D u, the D u skip fused into the epilogue
             y = ops.gemm_f32(x2, pk["wct"], Bt_lo=pk["wct_lo"], Cin=u2, colscale=self.D.contiguous(),
@@ -726,14 +748,21 @@ class _MIMOBase(LinearRecurrence):
         gD = ops.reduce_rows(gy2, B * L, m, other=u2)  # sum_t gy u per channel
         tn = self._tc(m, B * L) and self._tc(2 * P, B * L)
         R = ops.gemm_f32_tn(gy2, x2) if tn else gy2.T @ x2     # [m, 2P]
-        if self._tc(m, B * L):
-            gx2 = ops.gemm_f32(gy2, pk["wgt"], Bt_lo=pk["wgt_lo"], alpha=self.OUT_SCALE)
+        if self._gemm_scan(B, L)[1]:
+            A, Al = ops.mimo_fused_weights(pk["wgt"], pk["wgt_lo"])
+            gbu, ga = ops.mimo_fused_bwd(A, Al, gy2, self.OUT_SCALE, pk["abar"], pk["scale"], x)
+            gsc = None
         else:
-            gx2 = self.OUT_SCALE * (gy2 @ pk["wct"])
-        gx = torch.view_as_complex(gx2.reshape(B, L, P, 2))
-        gbu, ga, gsc = ops.mimo_scan_bwd(pk["abar"], pk["scale"], bu, x, gx)
+            if self._tc(m, B * L):
+                gx2 = ops.gemm_f32(gy2, pk["wgt"], Bt_lo=pk["wgt_lo"], alpha=self.OUT_SCALE)
+            else:
+                gx2 = self.OUT_SCALE * (gy2 @ pk["wct"])
+            gx = torch.view_as_complex(gx2.reshape(B, L, P, 2))
+            gbu, ga, gsc = ops.mimo_scan_bwd(pk["abar"], pk["scale"], bu, x, gx)
         gbu2 = torch.view_as_real(gbu).reshape(B * L, 2 * P)
         R2 = ops.gemm_f32_tn(gbu2, u2) if tn else gbu2.T @ u2  # [2P, m]
+        if gsc is None:  # d scale from R2 (the fused forward stores no bu)
+            gsc = ops.mimo_fused_gscale(pk["wbt"], R2, pk["scale"])
         if self._tc(2 * P, B * L):  # gu = D gy + Re(g conj(B)), the skip fused into the epilogue
             gu = ops.gemm_f32(gbu2, pk["wb"], Bt_lo=pk["wb_lo"], Cin=gy2, colscale=self.D.contiguous()).reshape(B, L, m)
         else:

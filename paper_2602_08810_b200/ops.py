@@ -352,7 +352,8 @@ def mimo_scan_fwd(abar, scale, bu):
 
 
 def mimo_scan_bwd(abar, scale, bu, x, gx):
-    """Returns (gbu [B,L,P], gabar [P], gscale [P]) (complex)."""
+    """Returns (gbu [B,L,P], gabar [P], gscale [P]) (complex); bu None: no
+    gscale (None; see mimo_fused_gscale)."""
     B, L, P = x.shape
     lib = _lib.lib()
     code = _lib.code_of(x.dtype)
@@ -366,7 +367,78 @@ def mimo_scan_bwd(abar, scale, bu, x, gx):
     _lib.check(lib.lrx_mimo_bwd(code, _lib.ptr(abar.contiguous()), _lib.ptr(scale.contiguous()), _lib.ptr(bu),
                                 _lib.ptr(x), _lib.ptr(gx), _lib.ptr(gbu), _lib.ptr(gap), _lib.ptr(gsp), B, L, P,
                                 _lib.ptr(ws), ws.numel(), _lib.stream()))
-    return gbu, reduce_rows(gap, nc * B, P), reduce_rows(gsp, nc * B, P)
+    return gbu, reduce_rows(gap, nc * B, P), (reduce_rows(gsp, nc * B, P) if bu is not None else None)
+
+
+# ---------------------------------------------------------------------------
+# Fused projection + scan (S5 / LRU, constant steps, fp32): csrc/lrx_mimo_fused.cu
+
+MIMO_FUSED_MAX_L = 8192
+
+
+def mimo_fused_supported(B, L, m, P, dtype):
+    """The fused kernels' domain (lrx_mimo_fused_*: LRX_ERR_UNSUPPORTED outside)."""
+    return dtype == torch.float32 and P <= 128 and m % 16 == 0 and L <= MIMO_FUSED_MAX_L and B * L < 2 ** 31
+
+
+def mimo_fused_weights(wt, wt_lo):
+    """[2P, m] interleaved (re, im) projection rows and their TF32 low plane ->
+    the fused kernels' [256, m] layout [Re rows (128, zero padded) ; Im rows]."""
+    P2, m = wt.shape
+    P = P2 // 2
+    A = torch.zeros((2, 256, m), dtype=wt.dtype, device=wt.device)
+    for i, w in enumerate((wt, wt_lo)):
+        A[i, :P] = w[0::2]
+        A[i, 128:128 + P] = w[1::2]
+    return A[0], A[1]
+
+
+def _fused_ws(B, L, P, device):
+    n = _lib.i64()
+    _lib.check(_lib.lib().lrx_mimo_fused_workspace_bytes(B, L, P, _lib.ref(n)))
+    return _lib.workspace(n.value, device)
+
+
+def mimo_fused_fwd(A, A_lo, u2, abar, scale, B, L, want_bu=True):
+    """x [B, L, P] complex (and bu = u A^T, for the backward) from u2 [B*L, m]
+    in one kernel: the projection lands in TMEM and is scanned there."""
+    m = u2.shape[1]
+    P = abar.shape[0]
+    x = torch.empty((B, L, P), dtype=torch.complex64, device=u2.device)
+    bu = torch.empty_like(x) if want_bu else None
+    ws = _fused_ws(B, L, P, u2.device)
+    _lib.check(_lib.lib().lrx_mimo_fused_fwd(
+        _lib.ptr(A), _lib.ptr(A_lo), _lib.ptr(u2), _lib.ptr(abar.contiguous()), _lib.ptr(scale.contiguous()),
+        _lib.ptr(x), _lib.ptr(bu), B, L, m, P, _lib.ptr(ws), ws.numel(), _lib.stream()))
+    return x, bu
+
+
+def mimo_fused_bwd(A, A_lo, gy2, alpha, abar, scale, x):
+    """(gbu [B, L, P], gabar [P]) from gy2 [B*L, m]: gx = alpha gy A^T lands in
+    TMEM and the reverse scan reads it there.  d scale = sum_k conj(bu_k) g_k
+    is left to the caller (mimo_fused_gscale, from the weight-gradient GEMM)."""
+    B, L, P = x.shape
+    m = gy2.shape[1]
+    n = _lib.i64()
+    _lib.check(_lib.lib().lrx_mimo_fused_units(B, L, _lib.ref(n)))
+    units = n.value
+    gbu = torch.empty_like(x)
+    gap = torch.empty(units * P, dtype=x.dtype, device=x.device)
+    ws = _fused_ws(B, L, P, x.device)
+    _lib.check(_lib.lib().lrx_mimo_fused_bwd(
+        _lib.ptr(A), _lib.ptr(A_lo), _lib.ptr(gy2), float(alpha), _lib.ptr(abar.contiguous()),
+        _lib.ptr(scale.contiguous()), _lib.ptr(x), _lib.ptr(gbu), _lib.ptr(gap), B, L, m, P, _lib.ptr(ws), ws.numel(),
+        _lib.stream()))
+    return gbu, reduce_rows(gap, units, P)
+
+
+def mimo_fused_gscale(wt, R2, scale):
+    """sum_k conj(bu_k) g_k per state from the weight-gradient GEMM
+    R2 = gbu^T u ([2P, m], rows interleaved (re, im)) and the projection rows
+    wt [2P, m] (bu = u wt^T): sum_h conj(W[p, h]) R2c[p, h] / conj(scale_p)."""
+    W = torch.complex(wt[0::2], wt[1::2])
+    R2c = torch.complex(R2[0::2], R2[1::2])
+    return (W.conj() * R2c).sum(1) / scale.conj()
 
 
 def mimo_scan_fwd_ps(lam, delta, deltas, scheme, bu):

@@ -719,6 +719,41 @@ def test_mimo_layer_on_tensor_cores_matches_oracle(lrx, kind):
         assert rel(g.params[k], rg[k]) < TOL["f32"], (k, rel(g.params[k], rg[k]))
 
 
+@pytest.mark.parametrize("bwd", ["fused", "separate"])
+@pytest.mark.parametrize("kind,m,n,B,L", [("s5", 64, 256, 5, 1000), ("lru", 48, 64, 2, 4096),
+                                          ("s5", 128, 64, 40, 128), ("lru", 32, 128, 1, 8192)])
+def test_mimo_gemm_scan_fused_matches_oracle(lrx, monkeypatch, kind, m, n, B, L, bwd):
+    """The fused projection + scan kernels (bu / gx scanned straight out of
+    TMEM, csrc/lrx_mimo_fused.cu): ragged last unit (L = 1000), P = 128 (s5
+    d_state 256), zero-padded state rows (P < 128), one batch row of 64 units;
+    the backward fused or separate (no bu stored: d scale from the weight
+    GEMM).  Oracle in f64, all parameter gradients, same bits on a re-run."""
+    from paper_2602_08810_b200 import ops
+    monkeypatch.setenv("LRX_MIMO_FUSED", "1")
+    monkeypatch.setenv("LRX_MIMO_FUSED_BWD", "1" if bwd == "fused" else "0")
+    calls = []
+    for name in ("mimo_fused_fwd", "mimo_fused_bwd"):
+        f = getattr(ops, name)
+        monkeypatch.setattr(ops, name, (lambda f, nm: lambda *a, **k: (calls.append(nm), f(*a, **k))[1])(f, name))
+    layer = lrx.make_layer(kind, m, n, dtype="f32", seed=23)
+    u = port.Rng(31).normal((B, L, m)).astype(np.float32)
+    gy = port.Rng(32).normal((B, L, m)).astype(np.float32)
+    y, tape = layer.forward(u, tape=True)
+    g = lrx.layer_backward(layer, tape, gy)
+    assert calls == (["mimo_fused_fwd", "mimo_fused_bwd"] if bwd == "fused" else ["mimo_fused_fwd"])
+    params = {k: v.cpu().numpy() for k, v in layer.parameters().items()}
+    ry, rg, rgu = _oracle_f64(kind, layer.discretization, params, u, gy)
+    assert rel(y, ry) < TOL["f32"]
+    assert rel(g.u, rgu) < TOL["f32"]
+    for k in rg:
+        assert rel(g.params[k], rg[k]) < TOL["f32"], (k, rel(g.params[k], rg[k]))
+    y2, tape2 = layer.forward(u, tape=True)
+    g2 = lrx.layer_backward(layer, tape2, gy)
+    assert np.array_equal(np.asarray(y), np.asarray(y2)) and np.array_equal(np.asarray(g.u), np.asarray(g2.u))
+    for k in g.params:
+        assert torch.equal(torch.as_tensor(g.params[k]), torch.as_tensor(g2.params[k])), k
+
+
 @pytest.mark.parametrize("mode", ["tma", "stream", "lookback", "rc", "rev"])
 def test_rglru_kernel_variants_match_oracle(lrx, monkeypatch, mode):
     """Every RG-LRU kernel family (LRX_RGLRU_MODE) gives the oracle's answer."""
