@@ -322,6 +322,14 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(const __grid_constant
             const int nt = (int)min((int64_t)TT, a.L - t0);
             const int acc = ti & 1;
             const uint32_t tre = tmem + lrow + acc * 256, tim = tre + 128;
+            if (REV && lead) {
+                // warm L2 with the unit's x_{k-1} rows (one contiguous range)
+                // while pass 1 runs: pass 2 then reads them at L2 latency
+                const int64_t r0 = max((int64_t)0, (int64_t)b * a.L + t0 - 1);
+                const uint32_t bytes = (uint32_t)(nt * a.P * 8);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.x + 2 * r0 * a.P), "r"(bytes)
+                             : "memory");
+            }
             tma::mbar_wait(&tfull[acc], (ti >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (a.dbg & 4) {
