@@ -1378,7 +1378,11 @@ static bool tma_plan(int64_t B, int64_t L, int64_t W, int narr, TmaPlan* p, int 
     const int64_t max_seg = std::max<int64_t>(1, std::min<int64_t>(64, L / 256));
     // segments only below ~6 resident warps per SM (measured: the AGG pass
     // costs more than it buys above that); aim for ~12.
-    int64_t n_seg = warps < 6 ? std::min<int64_t>(max_seg, (int64_t)std::ceil(12 / warps)) : 1;
+    // (the lane-pair forward streams 3 arrays with one ex2-free chain per pair:
+    // it keeps one segment down to ~3 warps/SM -- B = 8 of an 8-GPU C4 job:
+    // 1.64 ms with 3 segments, 1.47 with one; tools/rg_plan_grid.py)
+    const double seg_below = pair32 && narr == 3 ? 3 : 6;
+    int64_t n_seg = warps < seg_below ? std::min<int64_t>(max_seg, (int64_t)std::ceil(12 / warps)) : 1;
     int PF = 0;
     for (; n_seg >= 1 && !PF; n_seg = n_seg > 1 ? n_seg - 1 : 0) {
         for (int pf = 4; pf <= MaxPF<IO>::T; pf *= 2) {
