@@ -37,6 +37,7 @@
 
 #include <stdint.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <type_traits>
@@ -157,6 +158,7 @@ struct Args {
     int n_tt, n_units, nk;
     float alpha;
     int tma_out;  // outputs staged through shared memory + TMA stores
+    int row_major;  // claim order (LRX_MIMO_FUSED_ORDER=row; default time-major)
     int dbg;  // LRX_MIMO_FUSED_DBG (timing experiments only): 1 no carry wait, 2 no pass 2, 4 no scan
 };
 
@@ -214,8 +216,12 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(const __grid_constant
         if (lane == 0) {  // ------------------------------------------ producer
             int it = 0;
             for (int ti = 0;; ++ti) {
-                const int u = atomicAdd(a.counter, 1);
-                const int uid = u < a.n_units ? u : -1;
+                // claims run time-major (all rows' tile 0, then tile 1, ...): a
+                // unit's row predecessors were claimed a full batch of claims
+                // earlier; the canonical id (row-major) indexes the maps
+                const int c = atomicAdd(a.counter, 1);
+                const int nb = a.n_units / a.n_tt;
+                const int uid = c >= a.n_units ? -1 : a.row_major ? c : (c % nb) * a.n_tt + c / nb;
                 unit_id[ti % RING] = uid;
                 tma::mbar_arrive(&uready[ti % RING]);
                 if (uid < 0) break;
@@ -586,6 +592,7 @@ static int launch(const float* A, const float* Al, const float* act, Args a, int
     a.n_units = (int)(B * a.n_tt);
     a.nk = (int)(m / BKT);
     if (const char* e = getenv("LRX_MIMO_FUSED_DBG")) a.dbg = atoi(e);
+    if (const char* e = getenv("LRX_MIMO_FUSED_ORDER")) a.row_major = !strcmp(e, "row");
     const size_t eb = align256((size_t)a.n_units * a.P * 8);
     a.E = static_cast<uint64_t*>(ws);
     a.I = reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + eb);

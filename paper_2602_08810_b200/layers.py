@@ -702,7 +702,7 @@ class _MIMOBase(LinearRecurrence):
         (forward, backward).  Domain: fp32 on the tensor-core route, P <= 128,
         L <= 8192.  Measured (tools/gpu_fused_ab.sh): the fused forward wins
         with enough 128-step units to fill the GPU (C2: 1024 units, forward
-        249 -> 229 us); with few units (C1: 64) the serial per-unit scan
+        249 -> 221 us); with few units (C1: 64) the serial per-unit scan
         loses to the separate launches, and the fused backward (its per-step
         x_{k-1} loads) loses at both, so it is opt-in.  LRX_MIMO_FUSED=0 / 1
         forces the forward off / on, LRX_MIMO_FUSED_BWD=1 enables the
