@@ -295,19 +295,25 @@ int lrx_s4d_coef_grads(int dtype, int scheme, const void* lambda_re_log, const v
  * nu_log, p1 theta_log, p2 gamma_log).  dtype = parameter dtype (F32 / F64);
  * abar, scale: complex [P] of that precision; extra: f64 [P][8] kept for the
  * gradient call; wbt [2P,m], wb [m,2P], wct [m,2P], wgt [2P,m]: real layouts
- * of B [P,m] and C [m,P] for the projection GEMMs (any may be NULL); with
- * lo_planes (F32 only) each is followed by a second plane holding the
- * 3xTF32 low parts v - tf32(v) (the Bt_lo operand of lrx_gemm_f32). */
+ * of B [P,m] and C [m,P] for the projection GEMMs, and wbf [256,m] = B in
+ * the lrx_mimo_fused_fwd layout (Re rows p, Im rows 128 + p, zero rows past
+ * P; P <= 128) and wgf [256,m] = wgt in that layout (lrx_mimo_fused_bwd)
+ * (any may be NULL); with lo_planes (F32 only) each is followed
+ * by a second plane holding the 3xTF32 low parts v - tf32(v) (the Bt_lo
+ * operand of lrx_gemm_f32). */
 int lrx_mimo_coef(int kind, int scheme, int dtype, const void* p0, const void* p1, const void* p2, const void* b_re,
                   const void* b_im, const void* c_re, const void* c_im, int64_t P, int64_t m, void* abar, void* scale,
-                  double* extra, void* wbt, void* wb, void* wct, void* wgt, int lo_planes, void* stream);
+                  double* extra, void* wbt, void* wb, void* wct, void* wgt, void* wbf, void* wgf, int lo_planes,
+                  void* stream);
 /* ga, gsc: complex [P] (sum g conj(x_prev), sum conj(bu) g); R [m,2P] = gy^T x,
- * R2 [2P,m] = gbu^T u.  g0..g2: [P] coefficient grads (keys as p0..p2),
+ * R2 [2P,m] = gbu^T u.  gsc may be NULL (no bu stored, after
+ * lrx_mimo_fused_fwd): then gsc = sum_h conj(B[p,h]) R2c[p,h] / conj(scale_p)
+ * from b_re / b_im [P,m].  g0..g2: [P] coefficient grads (keys as p0..p2),
  * gb_re/gb_im [P,m], gc_re/gc_im [m,P] = out_scale (R_re, -R_im). */
 int lrx_mimo_coef_grads(int kind, int scheme, int dtype, const void* p0, const void* p1, const void* p2,
                         const double* extra, const void* ga, const void* gsc, const void* R, const void* R2,
-                        double out_scale, void* g0, void* g1, void* g2, void* gb_re, void* gb_im, void* gc_re,
-                        void* gc_im, int64_t P, int64_t m, void* stream);
+                        const void* b_re, const void* b_im, double out_scale, void* g0, void* g1, void* g2,
+                        void* gb_re, void* gb_im, void* gc_re, void* gc_im, int64_t P, int64_t m, void* stream);
 /* S6: x[B,D,N] compute precision; u, y io dtype; pre [B,D] = the delta
  * projection (bias not added), Bk, Ck [B,N] compute precision. */
 int lrx_s6_step(int io_dtype, void* x, const void* u, const void* pre, const void* Bk, const void* Ck,

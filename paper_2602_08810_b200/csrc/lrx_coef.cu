@@ -18,6 +18,8 @@
 #include "lrx_common.cuh"
 #include "lrx_host.h"
 
+#include <algorithm>
+
 namespace lrx {
 namespace coef {
 
@@ -62,7 +64,7 @@ template <typename T>
 __global__ void coef_fwd_kernel(int kind, int scheme, const void* p0, const void* p1, const void* p2,
                                 const void* b_re, const void* b_im, const void* c_re, const void* c_im, int64_t P,
                                 int64_t m, void* abar, void* scale, double* extra, void* wbt, void* wb, void* wct,
-                                void* wgt, int lo) {
+                                void* wgt, void* wbf, void* wgf, int lo) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     for (int64_t p = tid; p < P; p += nth) {
@@ -109,23 +111,57 @@ __global__ void coef_fwd_kernel(int kind, int scheme, const void* p0, const void
         put<T>(wgt, (2 * pc) * m + hc, cr, lo, 2 * P * m);
         put<T>(wgt, (2 * pc + 1) * m + hc, -ci, lo, 2 * P * m);
     }
+    //   wbf [256, m]: the fused projection + scan layout (lrx_mimo_fused_fwd):
+    //   Re rows p, Im rows 128 + p, zero rows past P (all 256 rows written)
+    //   wgf [256, m]: wgt in that layout (the fused backward's gx projection)
+    if (wbf || wgf)
+        for (int64_t i = tid; i < 128 * m; i += nth) {
+            const int64_t p = i / m, h = i % m;
+            const bool in = p < P;
+            put<T>(wbf, p * m + h, in ? ld<T>(b_re, p * m + h) : 0.0, lo, 256 * m);
+            put<T>(wbf, (128 + p) * m + h, in ? ld<T>(b_im, p * m + h) : 0.0, lo, 256 * m);
+            put<T>(wgf, p * m + h, in ? ld<T>(c_re, h * P + p) : 0.0, lo, 256 * m);
+            put<T>(wgf, (128 + p) * m + h, in ? -ld<T>(c_im, h * P + p) : 0.0, lo, 256 * m);
+        }
 }
 
 // ga = sum g conj(x_{k-1}) (per state, summed over batch and time), gsc = sum
 // conj(bu) g; R [m, 2P] = gy^T x2; R2 [2P, m] = gbu2^T u2.
+//
+// gsc == NULL (the fused forward stores no bu): gsc = sum_k conj(bu_k) g_k =
+// sum_h conj(B[p, h]) (gbu^T u)[p, h] / conj(scale_p) from R2, one warp per
+// state (lane-strided over h, fixed xor tree: deterministic).
 template <typename T>
 __global__ void coef_bwd_kernel(int kind, int scheme, const void* p0, const void* p1, const void* p2,
                                 const double* extra, const void* ga, const void* gsc, const void* R, const void* R2,
-                                double osc, void* g0, void* g1, void* g2, void* gb_re, void* gb_im, void* gc_re,
-                                void* gc_im, int64_t P, int64_t m) {
+                                const void* b_re, const void* b_im, double osc, void* g0, void* g1, void* g2,
+                                void* gb_re, void* gb_im, void* gc_re, void* gc_im, int64_t P, int64_t m) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t p = tid; p < P; p += nth) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t p = tid >> 5; p < P; p += nth >> 5) {  // warp per state
         const double* e = extra + 8 * p;
         const z64 lam{e[0], e[1]}, ab{e[2], e[3]};
         const double delta = e[6];
         const z64 a{ld<T>(ga, 2 * p), ld<T>(ga, 2 * p + 1)};
-        const z64 s{ld<T>(gsc, 2 * p), ld<T>(gsc, 2 * p + 1)};
+        z64 s;
+        if (gsc) {
+            s = {ld<T>(gsc, 2 * p), ld<T>(gsc, 2 * p + 1)};
+        } else {
+            z64 acc{0.0, 0.0};
+            for (int64_t h = lane; h < m; h += 32) {
+                const z64 w{ld<T>(b_re, p * m + h), ld<T>(b_im, p * m + h)};
+                const z64 r{ld<T>(R2, (2 * p) * m + h), ld<T>(R2, (2 * p + 1) * m + h)};
+                acc = acc + conj(w) * r;
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                acc.re += __shfl_xor_sync(0xffffffffu, acc.re, o);
+                acc.im += __shfl_xor_sync(0xffffffffu, acc.im, o);
+            }
+            s = zdiv(acc, conj(z64{e[4], e[5]}));
+        }
+        if (lane) continue;
         if (kind == 0) {
             // scheme_partials (autograd.py:186-211): d abar / d lam, d abar / d delta,
             // d scale / d lam, d scale / d delta
@@ -239,7 +275,8 @@ extern "C" {
 
 int lrx_mimo_coef(int kind, int scheme, int dtype, const void* p0, const void* p1, const void* p2, const void* b_re,
                   const void* b_im, const void* c_re, const void* c_im, int64_t P, int64_t m, void* abar, void* scale,
-                  double* extra, void* wbt, void* wb, void* wct, void* wgt, int lo_planes, void* stream) {
+                  double* extra, void* wbt, void* wb, void* wct, void* wgt, void* wbf, void* wgf, int lo_planes,
+                  void* stream) {
     LRX_REQUIRE(P >= 1 && m >= 1, LRX_ERR_SHAPE, "mimo coef: bad extents P=%lld m=%lld", (long long)P, (long long)m);
     LRX_REQUIRE(kind == 0 || kind == 1, LRX_ERR_VALUE, "mimo coef: kind %d (0 = s5, 1 = lru)", kind);
     LRX_REQUIRE(kind == 1 || scheme == LRX_ZOH || scheme == LRX_DIRAC, LRX_ERR_VALUE,
@@ -248,10 +285,10 @@ int lrx_mimo_coef(int kind, int scheme, int dtype, const void* p0, const void* p
     const unsigned g = coef::grid_for(P * m);
     if (dtype == LRX_F32)
         coef::coef_fwd_kernel<float><<<g, 256, 0, st>>>(kind, scheme, p0, p1, p2, b_re, b_im, c_re, c_im, P, m, abar,
-                                                        scale, extra, wbt, wb, wct, wgt, lo_planes);
+                                                        scale, extra, wbt, wb, wct, wgt, wbf, wgf, lo_planes);
     else if (dtype == LRX_F64)
         coef::coef_fwd_kernel<double><<<g, 256, 0, st>>>(kind, scheme, p0, p1, p2, b_re, b_im, c_re, c_im, P, m, abar,
-                                                         scale, extra, wbt, wb, wct, wgt, lo_planes);
+                                                         scale, extra, wbt, wb, wct, wgt, wbf, wgf, lo_planes);
     else {
         set_error("mimo coef: parameter dtype %d (f32 or f64)", dtype);
         return LRX_ERR_VALUE;
@@ -261,18 +298,19 @@ int lrx_mimo_coef(int kind, int scheme, int dtype, const void* p0, const void* p
 
 int lrx_mimo_coef_grads(int kind, int scheme, int dtype, const void* p0, const void* p1, const void* p2,
                         const double* extra, const void* ga, const void* gsc, const void* R, const void* R2,
-                        double out_scale, void* g0, void* g1, void* g2, void* gb_re, void* gb_im, void* gc_re,
-                        void* gc_im, int64_t P, int64_t m, void* stream) {
+                        const void* b_re, const void* b_im, double out_scale, void* g0, void* g1, void* g2,
+                        void* gb_re, void* gb_im, void* gc_re, void* gc_im, int64_t P, int64_t m, void* stream) {
     LRX_REQUIRE(P >= 1 && m >= 1, LRX_ERR_SHAPE, "mimo coef grads: bad extents");
     LRX_REQUIRE(kind == 0 || kind == 1, LRX_ERR_VALUE, "mimo coef grads: kind %d", kind);
     cudaStream_t st = (cudaStream_t)stream;
-    const unsigned g = coef::grid_for(P * m);
+    LRX_REQUIRE(gsc || (b_re && b_im), LRX_ERR_VALUE, "mimo coef grads: gsc or (b_re, b_im) required");
+    const unsigned g = std::max(coef::grid_for(P * m), (unsigned)cdiv(P, 8));  // >= one warp per state
     if (dtype == LRX_F32)
-        coef::coef_bwd_kernel<float><<<g, 256, 0, st>>>(kind, scheme, p0, p1, p2, extra, ga, gsc, R, R2, out_scale,
-                                                        g0, g1, g2, gb_re, gb_im, gc_re, gc_im, P, m);
+        coef::coef_bwd_kernel<float><<<g, 256, 0, st>>>(kind, scheme, p0, p1, p2, extra, ga, gsc, R, R2, b_re, b_im,
+                                                        out_scale, g0, g1, g2, gb_re, gb_im, gc_re, gc_im, P, m);
     else if (dtype == LRX_F64)
-        coef::coef_bwd_kernel<double><<<g, 256, 0, st>>>(kind, scheme, p0, p1, p2, extra, ga, gsc, R, R2, out_scale,
-                                                         g0, g1, g2, gb_re, gb_im, gc_re, gc_im, P, m);
+        coef::coef_bwd_kernel<double><<<g, 256, 0, st>>>(kind, scheme, p0, p1, p2, extra, ga, gsc, R, R2, b_re, b_im,
+                                                         out_scale, g0, g1, g2, gb_re, gb_im, gc_re, gc_im, P, m);
     else {
         set_error("mimo coef grads: parameter dtype %d (f32 or f64)", dtype);
         return LRX_ERR_VALUE;

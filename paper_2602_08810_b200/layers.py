@@ -625,26 +625,32 @@ class _MIMOBase(LinearRecurrence):
         keeps the torch path: its singular-set check is a host decision)."""
         return deltas is None and (self.kind == "lru" or self.discretization in ("zoh", "dirac"))
 
-    def _coef_pack(self):
-        """abar, scale, the f64 context and the four real GEMM layouts of B / C
-        (with 3xTF32 low planes for fp32) from one lrx_mimo_coef launch."""
+    def _coef_pack(self, fused=(False, False)):
+        """abar, scale, the f64 context and the real GEMM layouts of B / C
+        (with 3xTF32 low planes for fp32) from one lrx_mimo_coef launch;
+        fused = (forward, backward): B / the gx projection also in the fused
+        projection + scan layout (wbf / wgf [256, m])."""
         P, m, dev = self._P, self.d_model, self.device
         lo = self.tdt == torch.float32
         abar = torch.empty(P, dtype=self.tcdt, device=dev)
         scale = torch.empty(P, dtype=self.tcdt, device=dev)
         extra = torch.empty((P, 8), dtype=torch.float64, device=dev)
         w = torch.empty((4, 2 if lo else 1, 2 * P * m), dtype=self.tdt, device=dev)
+        wbf, wgf = (torch.empty((2 if lo else 1, 256 * m), dtype=self.tdt, device=dev) if f else None for f in fused)
         p0, p1, p2 = self._coef_params()
         _lib.check(_lib.lib().lrx_mimo_coef(
             self._KIND_CODE, self._SCHEME_CODE.get(self.discretization, 0), _lib.code_of(self.tdt), _lib.ptr(p0),
             _lib.ptr(p1), _lib.ptr(p2), _lib.ptr(self.B_re), _lib.ptr(self.B_im), _lib.ptr(self.C_re),
             _lib.ptr(self.C_im), P, m, _lib.ptr(abar), _lib.ptr(scale), _lib.ptr(extra), _lib.ptr(w[0]),
-            _lib.ptr(w[1]), _lib.ptr(w[2]), _lib.ptr(w[3]), int(lo), _lib.stream()))
+            _lib.ptr(w[1]), _lib.ptr(w[2]), _lib.ptr(w[3]), _lib.ptr(wbf), _lib.ptr(wgf), int(lo), _lib.stream()))
         shp = {"wbt": (2 * P, m), "wb": (m, 2 * P), "wct": (m, 2 * P), "wgt": (2 * P, m)}
         pk = {"abar": abar, "scale": scale, "extra": extra}
         for i, k in enumerate(shp):
             pk[k] = w[i, 0].view(shp[k])
             pk[k + "_lo"] = w[i, 1].view(shp[k]) if lo else None
+        for k, t in (("wbf", wbf), ("wgf", wgf)):
+            if t is not None:
+                pk[k], pk[k + "_lo"] = t[0].view(256, m), (t[1].view(256, m) if lo else None)
         return pk
 
     def _coef_grads_fused(self, pk, ga, gsc, R, R2):
@@ -655,8 +661,9 @@ class _MIMOBase(LinearRecurrence):
         p0, p1, p2 = self._coef_params()
         _lib.check(_lib.lib().lrx_mimo_coef_grads(
             self._KIND_CODE, self._SCHEME_CODE.get(self.discretization, 0), _lib.code_of(dt), _lib.ptr(p0),
-            _lib.ptr(p1), _lib.ptr(p2), _lib.ptr(pk["extra"]), _lib.ptr(ga.contiguous()), _lib.ptr(gsc.contiguous()),
-            _lib.ptr(R.contiguous()), _lib.ptr(R2.contiguous()), float(self.OUT_SCALE), _lib.ptr(g[0]),
+            _lib.ptr(p1), _lib.ptr(p2), _lib.ptr(pk["extra"]), _lib.ptr(ga.contiguous()),
+            _lib.ptr(gsc.contiguous() if gsc is not None else None), _lib.ptr(R.contiguous()),
+            _lib.ptr(R2.contiguous()), _lib.ptr(self.B_re), _lib.ptr(self.B_im), float(self.OUT_SCALE), _lib.ptr(g[0]),
             _lib.ptr(g[1]), _lib.ptr(g[2]), _lib.ptr(gb[0]), _lib.ptr(gb[1]), _lib.ptr(gc[0]), _lib.ptr(gc[1]),
             P, m, _lib.stream()))
         keys = self._coef_keys
@@ -700,28 +707,28 @@ class _MIMOBase(LinearRecurrence):
         """Which directions run the projection and the scan as one tcgen05
         kernel (csrc/lrx_mimo_fused.cu: bu / gx scanned out of TMEM), as
         (forward, backward).  Domain: fp32 on the tensor-core route, P <= 128,
-        L <= 8192.  Measured (tools/gpu_fused_ab.sh): the fused forward wins
-        with enough 128-step units to fill the GPU (C2: 1024 units, forward
-        249 -> 221 us); with few units (C1: 64) the serial per-unit scan
-        loses to the separate launches, and the fused backward (its per-step
-        x_{k-1} loads) loses at both, so it is opt-in.  LRX_MIMO_FUSED=0 / 1
-        forces the forward off / on, LRX_MIMO_FUSED_BWD=1 enables the
-        backward."""
+        L <= 8192.  Measured (tools/gpu_fused_ab2.sh): both win with enough
+        128-step units to fill the GPU (C2, 1024 units: step 801 -> 739 us);
+        with few units (C1: 64) the serial per-unit scan loses to the
+        separate launches (133 -> 175 us).  LRX_MIMO_FUSED / LRX_MIMO_FUSED_BWD
+        = 0 / 1 force a direction off / on."""
         ok = self._tc(self.d_model, B * L) and ops.mimo_fused_supported(B, L, self.d_model, self._P, self.tdt)
-        env = os.environ.get("LRX_MIMO_FUSED")
         units = B * -(-L // 128)
-        fwd = ok and (env == "1" or (env is None and units >= 4 * _sm_count(self.device)))
-        bwd = ok and os.environ.get("LRX_MIMO_FUSED_BWD") == "1"
-        return fwd, bwd
+        auto = units >= 4 * _sm_count(self.device)
+
+        def on(var):
+            env = os.environ.get(var)
+            return ok and (env == "1" or (env is None and auto))
+        return on("LRX_MIMO_FUSED"), on("LRX_MIMO_FUSED_BWD")
 
     def _forward_fused(self, u, keep):
         B, L, m = u.shape
         P = self._P
         u2 = u.reshape(B * L, m).contiguous()
-        pk = self._coef_pack()
-        if self._gemm_scan(B, L)[0]:
-            A, Al = ops.mimo_fused_weights(pk["wbt"], pk["wbt_lo"])
-            x, bu = ops.mimo_fused_fwd(A, Al, u2, pk["abar"], pk["scale"], B, L, want_bu=False)
+        fused = self._gemm_scan(B, L)
+        pk = self._coef_pack(fused=fused)
+        if fused[0]:
+            x, bu = ops.mimo_fused_fwd(pk["wbf"], pk["wbf_lo"], u2, pk["abar"], pk["scale"], B, L, want_bu=False)
         else:
             if self._tc(m, B * L):
                 bu2 = ops.gemm_f32(u2, pk["wbt"], Bt_lo=pk["wbt_lo"])
@@ -748,9 +755,8 @@ class _MIMOBase(LinearRecurrence):
         gD = ops.reduce_rows(gy2, B * L, m, other=u2)  # sum_t gy u per channel
         tn = self._tc(m, B * L) and self._tc(2 * P, B * L)
         R = ops.gemm_f32_tn(gy2, x2) if tn else gy2.T @ x2     # [m, 2P]
-        if self._gemm_scan(B, L)[1]:
-            A, Al = ops.mimo_fused_weights(pk["wgt"], pk["wgt_lo"])
-            gbu, ga = ops.mimo_fused_bwd(A, Al, gy2, self.OUT_SCALE, pk["abar"], pk["scale"], x)
+        if "wgf" in pk:
+            gbu, ga = ops.mimo_fused_bwd(pk["wgf"], pk["wgf_lo"], gy2, self.OUT_SCALE, pk["abar"], pk["scale"], x)
             gsc = None
         else:
             if self._tc(m, B * L):
@@ -761,8 +767,6 @@ class _MIMOBase(LinearRecurrence):
             gbu, ga, gsc = ops.mimo_scan_bwd(pk["abar"], pk["scale"], bu, x, gx)
         gbu2 = torch.view_as_real(gbu).reshape(B * L, 2 * P)
         R2 = ops.gemm_f32_tn(gbu2, u2) if tn else gbu2.T @ u2  # [2P, m]
-        if gsc is None:  # d scale from R2 (the fused forward stores no bu)
-            gsc = ops.mimo_fused_gscale(pk["wbt"], R2, pk["scale"])
         if self._tc(2 * P, B * L):  # gu = D gy + Re(g conj(B)), the skip fused into the epilogue
             gu = ops.gemm_f32(gbu2, pk["wb"], Bt_lo=pk["wb_lo"], Cin=gy2, colscale=self.D.contiguous()).reshape(B, L, m)
         else:

@@ -353,7 +353,7 @@ def mimo_scan_fwd(abar, scale, bu):
 
 def mimo_scan_bwd(abar, scale, bu, x, gx):
     """Returns (gbu [B,L,P], gabar [P], gscale [P]) (complex); bu None: no
-    gscale (None; see mimo_fused_gscale)."""
+    gscale (None; lrx_mimo_coef_grads derives it from the weight-gradient GEMM)."""
     B, L, P = x.shape
     lib = _lib.lib()
     code = _lib.code_of(x.dtype)
@@ -416,7 +416,7 @@ def mimo_fused_fwd(A, A_lo, u2, abar, scale, B, L, want_bu=True):
 def mimo_fused_bwd(A, A_lo, gy2, alpha, abar, scale, x):
     """(gbu [B, L, P], gabar [P]) from gy2 [B*L, m]: gx = alpha gy A^T lands in
     TMEM and the reverse scan reads it there.  d scale = sum_k conj(bu_k) g_k
-    is left to the caller (mimo_fused_gscale, from the weight-gradient GEMM)."""
+    is left to the caller (lrx_mimo_coef_grads derives it from the weight-gradient GEMM)."""
     B, L, P = x.shape
     m = gy2.shape[1]
     n = _lib.i64()
@@ -430,15 +430,6 @@ def mimo_fused_bwd(A, A_lo, gy2, alpha, abar, scale, x):
         _lib.ptr(scale.contiguous()), _lib.ptr(x), _lib.ptr(gbu), _lib.ptr(gap), B, L, m, P, _lib.ptr(ws), ws.numel(),
         _lib.stream()))
     return gbu, reduce_rows(gap, units, P)
-
-
-def mimo_fused_gscale(wt, R2, scale):
-    """sum_k conj(bu_k) g_k per state from the weight-gradient GEMM
-    R2 = gbu^T u ([2P, m], rows interleaved (re, im)) and the projection rows
-    wt [2P, m] (bu = u wt^T): sum_h conj(W[p, h]) R2c[p, h] / conj(scale_p)."""
-    W = torch.complex(wt[0::2], wt[1::2])
-    R2c = torch.complex(R2[0::2], R2[1::2])
-    return (W.conj() * R2c).sum(1) / scale.conj()
 
 
 def mimo_scan_fwd_ps(lam, delta, deltas, scheme, bu):
