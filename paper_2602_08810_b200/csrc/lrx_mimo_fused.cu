@@ -16,16 +16,18 @@
 // padded), so the real and imaginary accumulators of state p sit in the same
 // TMEM lane, 128 columns apart.
 //
-// Units.  A unit is (batch row, 128-step tile); CTAs claim units in order from
-// an atomic counter (so every unit a CTA waits on was claimed by a running
-// CTA: no residency assumption, safe next to other streams' kernels).  Per
-// unit the scan runs twice out of TMEM: pass 1 from a zero carry gives the
-// unit's map (LTI: carry -> abar^n carry + E), published to the workspace;
-// the carry entering the unit is then folded from the maps of all earlier
-// units of its row, first to last (a fixed order: deterministic; rows of up to
-// 64 units); pass 2 re-scans with the true carry and writes x (forward) or gbu
-// and the coefficient partials (backward).  The backward walks rows right to
-// left.
+// Units.  A unit is (batch row, 128-step tile); CTAs claim units from an
+// atomic counter, time-major (all rows' first tiles, then the second, ...), so
+// every unit a CTA waits on was claimed earlier by a running CTA: no
+// residency assumption, safe next to other streams' kernels.  Per unit the
+// scan runs twice out of TMEM, each time as 4 interleaved 32-step chains:
+// pass 1 from a zero carry gives the unit's map (LTI: carry -> abar^n carry +
+// E), published to the workspace; the carry entering the unit is the Horner
+// fold of its row's earlier maps, started from the newest published
+// inclusive prefix (the same operations either way: deterministic; rows of
+// up to 64 units); pass 2 re-scans with the true carry and writes x (forward)
+// or gbu and the d abar partials (backward) through shared memory by TMA.
+// The backward walks rows right to left.
 //
 // CTA: warp 0 TMA producer (+ unit claiming), warp 1 MMA issuer, warps 2-5
 // make the activation's TF32 low part, warps 6-9 scan (one TMEM lane quarter
@@ -54,11 +56,7 @@ constexpr int THREADS = 320;
 constexpr uint32_t kCols = 512;         // 2 accumulators x (re 128 | im 128)
 constexpr int RING = 4;                 // claimed-unit ring (producer -> MMA / scan)
 constexpr int OBUF = 2 * 16 * 128 * 8;  // 2 rounds x 4 blocks x 4 steps x 128 states, complex
-template <bool REV>
-struct Cfg {
-    static constexpr int NSTG = STAGES;
-    static constexpr size_t SMEM = 2048 + (size_t)NSTG * STAGE + (size_t)OBUF;
-};
+constexpr size_t SMEM = 2048 + (size_t)STAGES * STAGE + (size_t)OBUF;
 constexpr int kMaxTiles = 64;           // units per row (L <= 8192)
 
 __device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
@@ -167,7 +165,6 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(const __grid_constant
                                                            const __grid_constant__ CUtensorMap mAl,
                                                            const __grid_constant__ CUtensorMap mU,
                                                            const __grid_constant__ CUtensorMap mO, Args a) {
-    constexpr int STAGES = Cfg<REV>::NSTG;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* base = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -601,7 +598,6 @@ static int launch(const float* A, const float* Al, const float* act, Args a, int
         cudaMemsetAsync(a.counter, 0, 4, st) != cudaSuccess)
         return launched("mimo fused memset");
     auto k = fused_kernel<REV>;
-    constexpr size_t SMEM = Cfg<REV>::SMEM;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess) {
         set_error("mimo fused: cannot reserve %zu B of shared memory", SMEM);
         return LRX_ERR_CUDA;
