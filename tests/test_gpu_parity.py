@@ -754,6 +754,35 @@ def test_mimo_gemm_scan_fused_matches_oracle(lrx, monkeypatch, kind, m, n, B, L,
         assert torch.equal(torch.as_tensor(g.params[k]), torch.as_tensor(g2.params[k])), k
 
 
+def test_mimo_fused_concurrent_streams_match_sequential(lrx, monkeypatch):
+    """Two fused projection + scan forwards+backwards on two streams at once:
+    units are claimed dynamically, so kernels sharing the GPU cannot wait on
+    each other's unlaunched CTAs; results equal the sequential ones bitwise."""
+    monkeypatch.setenv("LRX_MIMO_FUSED", "1")
+    monkeypatch.setenv("LRX_MIMO_FUSED_BWD", "1")
+    layer = lrx.make_layer("s5", 64, 128, dtype="f32", seed=5)
+    us = [torch.from_numpy(port.Rng(60 + i).normal((6, 2048, 64)).astype(np.float32)).cuda() for i in range(2)]
+    gys = [torch.from_numpy(port.Rng(70 + i).normal((6, 2048, 64)).astype(np.float32)).cuda() for i in range(2)]
+
+    def run(i):
+        y, tape = layer.forward(us[i], tape=True)
+        g = lrx.layer_backward(layer, tape, gys[i])
+        return y, g.u
+
+    ref = [run(0), run(1)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    out = [None, None]
+    for _ in range(3):
+        for i, st in enumerate(streams):
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                out[i] = run(i)
+        torch.cuda.synchronize()
+        for i in range(2):
+            assert torch.equal(out[i][0], ref[i][0]) and torch.equal(out[i][1], ref[i][1])
+
+
 @pytest.mark.parametrize("mode", ["tma", "stream", "lookback", "rc", "rev"])
 def test_rglru_kernel_variants_match_oracle(lrx, monkeypatch, mode):
     """Every RG-LRU kernel family (LRX_RGLRU_MODE) gives the oracle's answer."""
