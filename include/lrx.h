@@ -305,15 +305,18 @@ int lrx_mimo_coef(int kind, int scheme, int dtype, const void* p0, const void* p
                   const void* b_im, const void* c_re, const void* c_im, int64_t P, int64_t m, void* abar, void* scale,
                   double* extra, void* wbt, void* wb, void* wct, void* wgt, void* wbf, void* wgf, int lo_planes,
                   void* stream);
-/* ga, gsc: complex [P] (sum g conj(x_prev), sum conj(bu) g); R [m,2P] = gy^T x,
- * R2 [2P,m] = gbu^T u.  gsc may be NULL (no bu stored, after
+/* ga, gsc: complex [ga_rows, P] / [gsc_rows, P] partial rows of sum g
+ * conj(x_prev) and sum conj(bu) g (the scans' per-chunk partials; summed
+ * here in f64, fixed order); R [m,2P] = gy^T x, R2 [2P,m] = gbu^T u.  gsc
+ * may be NULL (no bu stored, after
  * lrx_mimo_fused_fwd): then gsc = sum_h conj(B[p,h]) R2c[p,h] / conj(scale_p)
  * from b_re / b_im [P,m].  g0..g2: [P] coefficient grads (keys as p0..p2),
  * gb_re/gb_im [P,m], gc_re/gc_im [m,P] = out_scale (R_re, -R_im). */
 int lrx_mimo_coef_grads(int kind, int scheme, int dtype, const void* p0, const void* p1, const void* p2,
-                        const double* extra, const void* ga, const void* gsc, const void* R, const void* R2,
-                        const void* b_re, const void* b_im, double out_scale, void* g0, void* g1, void* g2,
-                        void* gb_re, void* gb_im, void* gc_re, void* gc_im, int64_t P, int64_t m, void* stream);
+                        const double* extra, const void* ga, int64_t ga_rows, const void* gsc, int64_t gsc_rows,
+                        const void* R, const void* R2, const void* b_re, const void* b_im, double out_scale,
+                        void* g0, void* g1, void* g2, void* gb_re, void* gb_im, void* gc_re, void* gc_im, int64_t P,
+                        int64_t m, void* stream);
 /* S6: x[B,D,N] compute precision; u, y io dtype; pre [B,D] = the delta
  * projection (bias not added), Bk, Ck [B,N] compute precision. */
 int lrx_s6_step(int io_dtype, void* x, const void* u, const void* pre, const void* Bk, const void* Ck,

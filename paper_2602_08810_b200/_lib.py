@@ -84,8 +84,8 @@ SIGNATURES = {
                          _vp, _i64, _i64, _i64, _i64, _vp, _sz, _vp]),
     "lrx_mimo_coef": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                            _vp, _vp, _vp, _i, _vp]),
-    "lrx_mimo_coef_grads": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_double, _vp,
-                                 _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp]),
+    "lrx_mimo_coef_grads": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp,
+                                 ctypes.c_double, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp]),
 }
 
 _lib = None

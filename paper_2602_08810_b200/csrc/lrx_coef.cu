@@ -133,9 +133,10 @@ __global__ void coef_fwd_kernel(int kind, int scheme, const void* p0, const void
 // state (lane-strided over h, fixed xor tree: deterministic).
 template <typename T>
 __global__ void coef_bwd_kernel(int kind, int scheme, const void* p0, const void* p1, const void* p2,
-                                const double* extra, const void* ga, const void* gsc, const void* R, const void* R2,
-                                const void* b_re, const void* b_im, double osc, void* g0, void* g1, void* g2,
-                                void* gb_re, void* gb_im, void* gc_re, void* gc_im, int64_t P, int64_t m) {
+                                const double* extra, const void* ga, int64_t ga_rows, const void* gsc,
+                                int64_t gsc_rows, const void* R, const void* R2, const void* b_re, const void* b_im,
+                                double osc, void* g0, void* g1, void* g2, void* gb_re, void* gb_im, void* gc_re,
+                                void* gc_im, int64_t P, int64_t m) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
@@ -143,10 +144,22 @@ __global__ void coef_bwd_kernel(int kind, int scheme, const void* p0, const void
         const double* e = extra + 8 * p;
         const z64 lam{e[0], e[1]}, ab{e[2], e[3]};
         const double delta = e[6];
-        const z64 a{ld<T>(ga, 2 * p), ld<T>(ga, 2 * p + 1)};
+        // the scan's per-chunk partial rows [rows, P], summed here in f64 (lane-
+        // strided rows, then the fixed xor tree)
+        auto rowsum = [&](const void* v, int64_t rows) {
+            z64 acc{0.0, 0.0};
+            for (int64_t r = lane; r < rows; r += 32) acc = acc + z64{ld<T>(v, 2 * (r * P + p)), ld<T>(v, 2 * (r * P + p) + 1)};
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                acc.re += __shfl_xor_sync(0xffffffffu, acc.re, o);
+                acc.im += __shfl_xor_sync(0xffffffffu, acc.im, o);
+            }
+            return acc;
+        };
+        const z64 a = rowsum(ga, ga_rows);
         z64 s;
         if (gsc) {
-            s = {ld<T>(gsc, 2 * p), ld<T>(gsc, 2 * p + 1)};
+            s = rowsum(gsc, gsc_rows);
         } else {
             z64 acc{0.0, 0.0};
             for (int64_t h = lane; h < m; h += 32) {
@@ -297,19 +310,21 @@ int lrx_mimo_coef(int kind, int scheme, int dtype, const void* p0, const void* p
 }
 
 int lrx_mimo_coef_grads(int kind, int scheme, int dtype, const void* p0, const void* p1, const void* p2,
-                        const double* extra, const void* ga, const void* gsc, const void* R, const void* R2,
-                        const void* b_re, const void* b_im, double out_scale, void* g0, void* g1, void* g2,
-                        void* gb_re, void* gb_im, void* gc_re, void* gc_im, int64_t P, int64_t m, void* stream) {
+                        const double* extra, const void* ga, int64_t ga_rows, const void* gsc, int64_t gsc_rows,
+                        const void* R, const void* R2, const void* b_re, const void* b_im, double out_scale,
+                        void* g0, void* g1, void* g2, void* gb_re, void* gb_im, void* gc_re, void* gc_im, int64_t P,
+                        int64_t m, void* stream) {
     LRX_REQUIRE(P >= 1 && m >= 1, LRX_ERR_SHAPE, "mimo coef grads: bad extents");
     LRX_REQUIRE(kind == 0 || kind == 1, LRX_ERR_VALUE, "mimo coef grads: kind %d", kind);
     cudaStream_t st = (cudaStream_t)stream;
     LRX_REQUIRE(gsc || (b_re && b_im), LRX_ERR_VALUE, "mimo coef grads: gsc or (b_re, b_im) required");
+    LRX_REQUIRE(ga_rows >= 1 && (!gsc || gsc_rows >= 1), LRX_ERR_SHAPE, "mimo coef grads: partial rows");
     const unsigned g = std::max(coef::grid_for(P * m), (unsigned)cdiv(P, 8));  // >= one warp per state
     if (dtype == LRX_F32)
-        coef::coef_bwd_kernel<float><<<g, 256, 0, st>>>(kind, scheme, p0, p1, p2, extra, ga, gsc, R, R2, b_re, b_im,
+        coef::coef_bwd_kernel<float><<<g, 256, 0, st>>>(kind, scheme, p0, p1, p2, extra, ga, ga_rows, gsc, gsc_rows, R, R2, b_re, b_im,
                                                         out_scale, g0, g1, g2, gb_re, gb_im, gc_re, gc_im, P, m);
     else if (dtype == LRX_F64)
-        coef::coef_bwd_kernel<double><<<g, 256, 0, st>>>(kind, scheme, p0, p1, p2, extra, ga, gsc, R, R2, b_re, b_im,
+        coef::coef_bwd_kernel<double><<<g, 256, 0, st>>>(kind, scheme, p0, p1, p2, extra, ga, ga_rows, gsc, gsc_rows, R, R2, b_re, b_im,
                                                          out_scale, g0, g1, g2, gb_re, gb_im, gc_re, gc_im, P, m);
     else {
         set_error("mimo coef grads: parameter dtype %d (f32 or f64)", dtype);

@@ -661,8 +661,9 @@ class _MIMOBase(LinearRecurrence):
         p0, p1, p2 = self._coef_params()
         _lib.check(_lib.lib().lrx_mimo_coef_grads(
             self._KIND_CODE, self._SCHEME_CODE.get(self.discretization, 0), _lib.code_of(dt), _lib.ptr(p0),
-            _lib.ptr(p1), _lib.ptr(p2), _lib.ptr(pk["extra"]), _lib.ptr(ga.contiguous()),
-            _lib.ptr(gsc.contiguous() if gsc is not None else None), _lib.ptr(R.contiguous()),
+            _lib.ptr(p1), _lib.ptr(p2), _lib.ptr(pk["extra"]), _lib.ptr(ga.contiguous()), ga.numel() // P,
+            _lib.ptr(gsc.contiguous() if gsc is not None else None), gsc.numel() // P if gsc is not None else 1,
+            _lib.ptr(R.contiguous()),
             _lib.ptr(R2.contiguous()), _lib.ptr(self.B_re), _lib.ptr(self.B_im), float(self.OUT_SCALE), _lib.ptr(g[0]),
             _lib.ptr(g[1]), _lib.ptr(g[2]), _lib.ptr(gb[0]), _lib.ptr(gb[1]), _lib.ptr(gc[0]), _lib.ptr(gc[1]),
             P, m, _lib.stream()))
@@ -756,7 +757,8 @@ class _MIMOBase(LinearRecurrence):
         tn = self._tc(m, B * L) and self._tc(2 * P, B * L)
         R = ops.gemm_f32_tn(gy2, x2) if tn else gy2.T @ x2     # [m, 2P]
         if "wgf" in pk:
-            gbu, ga = ops.mimo_fused_bwd(pk["wgf"], pk["wgf_lo"], gy2, self.OUT_SCALE, pk["abar"], pk["scale"], x)
+            gbu, ga = ops.mimo_fused_bwd(pk["wgf"], pk["wgf_lo"], gy2, self.OUT_SCALE, pk["abar"], pk["scale"], x,
+                                         reduce=False)
             gsc = None
         else:
             if self._tc(m, B * L):
@@ -764,7 +766,7 @@ class _MIMOBase(LinearRecurrence):
             else:
                 gx2 = self.OUT_SCALE * (gy2 @ pk["wct"])
             gx = torch.view_as_complex(gx2.reshape(B, L, P, 2))
-            gbu, ga, gsc = ops.mimo_scan_bwd(pk["abar"], pk["scale"], bu, x, gx)
+            gbu, ga, gsc = ops.mimo_scan_bwd(pk["abar"], pk["scale"], bu, x, gx, reduce=False)
         gbu2 = torch.view_as_real(gbu).reshape(B * L, 2 * P)
         R2 = ops.gemm_f32_tn(gbu2, u2) if tn else gbu2.T @ u2  # [2P, m]
         if self._tc(2 * P, B * L):  # gu = D gy + Re(g conj(B)), the skip fused into the epilogue

@@ -351,7 +351,7 @@ def mimo_scan_fwd(abar, scale, bu):
     return x
 
 
-def mimo_scan_bwd(abar, scale, bu, x, gx):
+def mimo_scan_bwd(abar, scale, bu, x, gx, reduce=True):
     """Returns (gbu [B,L,P], gabar [P], gscale [P]) (complex); bu None: no
     gscale (None; lrx_mimo_coef_grads derives it from the weight-gradient GEMM)."""
     B, L, P = x.shape
@@ -367,6 +367,8 @@ def mimo_scan_bwd(abar, scale, bu, x, gx):
     _lib.check(lib.lrx_mimo_bwd(code, _lib.ptr(abar.contiguous()), _lib.ptr(scale.contiguous()), _lib.ptr(bu),
                                 _lib.ptr(x), _lib.ptr(gx), _lib.ptr(gbu), _lib.ptr(gap), _lib.ptr(gsp), B, L, P,
                                 _lib.ptr(ws), ws.numel(), _lib.stream()))
+    if not reduce:  # per-chunk partial rows [nc * B, P] (lrx_mimo_coef_grads sums them)
+        return gbu, gap.view(nc * B, P), (gsp.view(nc * B, P) if bu is not None else None)
     return gbu, reduce_rows(gap, nc * B, P), (reduce_rows(gsp, nc * B, P) if bu is not None else None)
 
 
@@ -413,7 +415,7 @@ def mimo_fused_fwd(A, A_lo, u2, abar, scale, B, L, want_bu=True):
     return x, bu
 
 
-def mimo_fused_bwd(A, A_lo, gy2, alpha, abar, scale, x):
+def mimo_fused_bwd(A, A_lo, gy2, alpha, abar, scale, x, reduce=True):
     """(gbu [B, L, P], gabar [P]) from gy2 [B*L, m]: gx = alpha gy A^T lands in
     TMEM and the reverse scan reads it there.  d scale = sum_k conj(bu_k) g_k
     is left to the caller (lrx_mimo_coef_grads derives it from the weight-gradient GEMM)."""
@@ -429,7 +431,7 @@ def mimo_fused_bwd(A, A_lo, gy2, alpha, abar, scale, x):
         _lib.ptr(A), _lib.ptr(A_lo), _lib.ptr(gy2), float(alpha), _lib.ptr(abar.contiguous()),
         _lib.ptr(scale.contiguous()), _lib.ptr(x), _lib.ptr(gbu), _lib.ptr(gap), B, L, m, P, _lib.ptr(ws), ws.numel(),
         _lib.stream()))
-    return gbu, reduce_rows(gap, units, P)
+    return gbu, (reduce_rows(gap, units, P) if reduce else gap.view(units, P))
 
 
 def mimo_scan_fwd_ps(lam, delta, deltas, scheme, bu):
