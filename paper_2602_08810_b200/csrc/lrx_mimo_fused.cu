@@ -157,7 +157,6 @@ struct Args {
     float alpha;
     int tma_out;  // outputs staged through shared memory + TMA stores
     int row_major;  // claim order (LRX_MIMO_FUSED_ORDER=row; default time-major)
-    int dbg;  // LRX_MIMO_FUSED_DBG (timing experiments only): 1 no carry wait, 2 no pass 2, 4 no scan
 };
 
 template <bool REV>
@@ -335,11 +334,6 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(const __grid_constant
             }
             tma::mbar_wait(&tfull[acc], (ti >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (a.dbg & 4) {
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                tma::mbar_arrive(&tempty[acc]);
-                continue;
-            }
             C Tb[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -394,7 +388,7 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(const __grid_constant
                 st_relaxed64(a.E + (int64_t)u * PP + p, pack(E));
                 const int u0 = u - tq;  // the row's first unit in walk order
                 int jb = u0;
-                if (tq > 0 && !(a.dbg & 1)) {
+                if (tq > 0) {
                     uint64_t iv[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) iv[i] = i < tq ? ld_relaxed64(a.I + (int64_t)(u - 1 - i) * PP + p) : kSentinel;
@@ -415,7 +409,7 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(const __grid_constant
                             ev[i] = i < n ? ld_relaxed64(a.E + (int64_t)(j0 + i) * PP + p) : 0ull;
                             all = all && ev[i] != kSentinel;
                         }
-                        if (all || (a.dbg & 1)) break;
+                        if (all) break;
                         __nanosleep(20);
                     }
 #pragma unroll
@@ -501,10 +495,9 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(const __grid_constant
                                     o = c[j];
                                     if (pv && a.bu) stcs_c(a.bu + 2 * (rb + (int64_t)t * a.P), v);
                                 }
-                                if (pv && !(a.dbg & 8)) {
+                                if (pv) {
                                     float* dst = (REV ? a.gbu : a.x) + 2 * (rb + (int64_t)t * a.P);
                                     if (W == 4 && staged) ob[(j * 4 + k) * a.P + p] = make_float2(o.re, o.im);
-                                    else if (a.dbg & 32) *reinterpret_cast<float2*>(dst) = make_float2(o.re, o.im);
                                     else stcs_c(dst, o);
                                 }
                             }
@@ -530,10 +523,8 @@ __global__ void __launch_bounds__(THREADS, 1) fused_kernel(const __grid_constant
                 }
                 sa = (sj[0] + sj[1]) + (sj[2] + sj[3]);
             };
-            if (!(a.dbg & 2)) {
-                if (REV || staged) pass2(std::integral_constant<int, 4>{});  // REV: x_{k-1} prefetch registers
-                else pass2(std::integral_constant<int, 8>{});
-            }
+            if (REV || staged) pass2(std::integral_constant<int, 4>{});  // REV: x_{k-1} prefetch registers
+            else pass2(std::integral_constant<int, 8>{});
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             tma::mbar_arrive(&tempty[acc]);
             if (REV && pv) stg_c(a.ga_part + 2 * ((int64_t)u * a.P + p), sa);
@@ -588,7 +579,6 @@ static int launch(const float* A, const float* Al, const float* act, Args a, int
     a.n_tt = (int)cdiv(L, (int64_t)TT);
     a.n_units = (int)(B * a.n_tt);
     a.nk = (int)(m / BKT);
-    if (const char* e = getenv("LRX_MIMO_FUSED_DBG")) a.dbg = atoi(e);
     if (const char* e = getenv("LRX_MIMO_FUSED_ORDER")) a.row_major = !strcmp(e, "row");
     const size_t eb = align256((size_t)a.n_units * a.P * 8);
     a.E = static_cast<uint64_t*>(ws);

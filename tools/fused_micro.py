@@ -1,5 +1,5 @@
 """Time the fused MIMO projection + scan kernels alone at C2 / C1 shapes
-(LRX_MIMO_FUSED_DBG bits skip parts: 1 carry wait, 2 pass 2, 4 the scan)."""
+(LRX_MIMO_FUSED_ORDER=row: row-major unit claims)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -22,12 +22,7 @@ for (B, L, m, P) in [(32, 4096, 256, 128), (8, 1024, 128, 64)]:
     abar = torch.polar(torch.full((P,), 0.9, device=dev), torch.rand(P, device=dev)).to(torch.complex64)
     scale = torch.ones(P, dtype=torch.complex64, device=dev)
     x, _ = ops.mimo_fused_fwd(A, Al, u2, abar, scale, B, L, want_bu=False)
-    out = {}
-    for dbg in ["0", "1", "2", "4"]:
-        os.environ["LRX_MIMO_FUSED_DBG"] = dbg
-        f = tm(lambda: ops.mimo_fused_fwd(A, Al, u2, abar, scale, B, L, want_bu=False))
-        b = tm(lambda: ops.mimo_fused_bwd(A, Al, u2, 2.0, abar, scale, x))
-        out[dbg] = (round(f, 1), round(b, 1))
-    os.environ["LRX_MIMO_FUSED_DBG"] = "0"
+    f = tm(lambda: ops.mimo_fused_fwd(A, Al, u2, abar, scale, B, L, want_bu=False))
+    b = tm(lambda: ops.mimo_fused_bwd(A, Al, u2, 2.0, abar, scale, x))
     g = tm(lambda: ops.gemm_f32(u2, wt, ops.tf32_lo(wt)))
-    print(f"B{B} L{L} m{m} P{P}: fused fwd/bwd us by dbg {out}; plain GEMM u W^T {g:.1f} us", flush=True)
+    print(f"B{B} L{L} m{m} P{P}: fused fwd {f:.1f} us, bwd {b:.1f} us; plain GEMM u W^T {g:.1f} us", flush=True)
